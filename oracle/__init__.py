@@ -1,0 +1,148 @@
+"""CPU oracle for the VTI step -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and the
+``--impl reference`` arm) may import this package. The product path
+(paper_1410_1387_b200 + include/vti.h) never imports it, and this package
+never imports the product. The arithmetic lives in ``vti_oracle.c`` (plain C
+loops, see its header for the paper passages and readings it follows); this
+module is argument marshalling plus the build step.
+
+Pins (tests/test_oracle_*.py) tie it to things other than itself: exact
+rational weights, polynomial exactness of the operators, early-step closed
+forms, the isotropic p == q collapse and an independent acoustic solver,
+mirror symmetry, a dense-operator brute force on an 8^3 grid, Ricker and
+Cerjan closed forms.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "vti_oracle.c")
+LIB = os.path.join(HERE, "libvti_oracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
+          "-Wall", "-Wextra"]
+
+
+class Params(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+        ("r_xy", C.c_int32), ("r_z", C.c_int32),
+        ("h", C.c_double), ("dt", C.c_double),
+        ("damp_width", C.c_int32), ("damp_alpha", C.c_double),
+        ("src_i", C.c_int32), ("src_j", C.c_int32), ("src_k", C.c_int32),
+        ("src_f", C.c_double), ("src_t0", C.c_double), ("src_amp", C.c_double),
+        ("src_mask", C.c_int32),
+    ]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle shared library (gcc; no GPU needed)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = LIB + ".tmp"
+        subprocess.check_call(["gcc", *CFLAGS, SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB)
+        fp = lambda t: np.ctypeslib.ndpointer(dtype=t, flags="C_CONTIGUOUS")
+        for sfx, t in (("f32", np.float32), ("f64", np.float64)):
+            f = getattr(L, "vto_run_" + sfx)
+            f.restype = C.c_int
+            f.argtypes = [C.POINTER(Params), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t),
+                          fp(t), fp(t), C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
+            g = getattr(L, "vto_point_" + sfx)
+            g.restype = C.c_int
+            ct = C.c_float if t is np.float32 else C.c_double
+            g.argtypes = [C.POINTER(Params), fp(t), fp(t), C.c_int32, C.c_int32, C.c_int32,
+                          C.c_int64, fp(t), fp(t), ct, ct, ct, ct, ct, fp(t)]
+        L.vto_ricker.restype = C.c_double
+        L.vto_ricker.argtypes = [C.c_double, C.c_double, C.c_double]
+        L.vto_source_f32.restype = C.c_float
+        L.vto_source_f32.argtypes = [C.POINTER(Params), C.c_int64]
+        L.vto_damping.restype = C.c_double
+        L.vto_damping.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double]
+        L.vto_damping_profile_f32.restype = None
+        L.vto_damping_profile_f32.argtypes = [C.c_int32, C.c_int32, C.c_double, fp(np.float32)]
+        L.vto_max_threads.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def params(cfg: dict, dt: float, src=None, mask=None, damp_width=None) -> Params:
+    s = cfg["src"] if src is None else src
+    return Params(
+        nx=cfg["nx"], ny=cfg["ny"], nz=cfg["nz"], r_xy=cfg["r_xy"], r_z=cfg["r_z"],
+        h=cfg["h"], dt=float(np.float32(dt)),
+        damp_width=cfg["damp_width"] if damp_width is None else damp_width,
+        damp_alpha=cfg["damp_alpha"],
+        src_i=-1 if s is None else s[0], src_j=-1 if s is None else s[1],
+        src_k=-1 if s is None else s[2],
+        src_f=cfg["f"], src_t0=cfg["t0"], src_amp=cfg["amp"],
+        src_mask=cfg["mask"] if mask is None else mask,
+    )
+
+
+def run(P: Params, wxy, wz, vx2, vn2, vz2, state=None, n0: int = 0, nsteps: int = 1,
+        dtype=np.float32, nthreads: int = 0):
+    """Advance nsteps from level n0. Returns (p, q, pm, qm, seconds).
+
+    ``state`` = (p, q, pm, qm) at levels (n0, n0-1) in [z][y][x]; None = zero.
+    """
+    shape = (P.nz, P.ny, P.nx)
+    conv = lambda a: np.ascontiguousarray(np.asarray(a, dtype=dtype))
+    if state is None:
+        p, q, pm, qm = (np.zeros(shape, dtype=dtype) for _ in range(4))
+    else:
+        p, q, pm, qm = (conv(a).copy() for a in state)
+    for a in (p, q, pm, qm):
+        assert a.shape == shape
+    vx2, vn2, vz2 = (conv(a).reshape(shape) for a in (vx2, vn2, vz2))
+    wxy = conv(wxy).reshape(-1)
+    wz = conv(wz).reshape(-1)
+    assert wxy.size == P.r_xy + 1 and wz.size == P.nz * (2 * P.r_z + 1)
+    secs = C.c_double(0.0)
+    f = lib().vto_run_f32 if dtype == np.float32 else lib().vto_run_f64
+    rc = f(C.byref(P), wxy, wz, vx2, vn2, vz2, p, q, pm, qm, n0, nsteps, nthreads, C.byref(secs))
+    if rc != 0:
+        raise ValueError(f"oracle rejected parameters (code {rc})")
+    return p, q, pm, qm, secs.value
+
+
+def point(P: Params, wxy, wzrow, i, j, k, n, pc, qc, pm, qm, vx2, vn2, vz2, dtype=np.float32):
+    """One output point of step n from gathered neighbourhoods (see vti_oracle.c)."""
+    conv = lambda a: np.ascontiguousarray(np.asarray(a, dtype=dtype)).reshape(-1)
+    out = np.zeros(2, dtype=dtype)
+    f = lib().vto_point_f32 if dtype == np.float32 else lib().vto_point_f64
+    rc = f(C.byref(P), conv(wxy), conv(wzrow), i, j, k, n, conv(pc), conv(qc),
+           float(pm), float(qm), float(vx2), float(vn2), float(vz2), out)
+    if rc != 0:
+        raise ValueError(f"oracle rejected parameters (code {rc})")
+    return out[0], out[1]
+
+
+def ricker(t, f, t0):
+    return lib().vto_ricker(t, f, t0)
+
+
+def damping_profile(n, W, alpha):
+    out = np.zeros(n, dtype=np.float32)
+    lib().vto_damping_profile_f32(n, W, alpha, out)
+    return out
+
+
+def max_threads() -> int:
+    return lib().vto_max_threads()

@@ -1,0 +1,258 @@
+/*
+ * oracle/vti_oracle.c -- CPU ORACLE FOR THE VTI STEP.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * arm may load this library. The product path (paper_1410_1387_b200/, the
+ * C-ABI in include/vti.h) never calls it and shares no code with it.
+ *
+ * A plain, slow, obviously correct implementation of one time step of the
+ * reduced elastic VTI propagator of arXiv 1410.1387 (PAPER.md = the paper's
+ * text; "P:n" = its line n):
+ *
+ *   Eq. 1  p_tt = vx2 (p_xx + p_yy) + vz2 q_zz + s(t) delta(x - x_i)
+ *   Eq. 2  q_tt = vn2 (p_xx + p_yy) + vz2 q_zz
+ *   Ricker s = (1 - 2 pi^2 f^2 t^2) exp(-pi^2 f^2 t^2), f = 15 Hz
+ *   Eq. 3  u^{n+1} - 2 u^n + u^{n-1} = dt^2 F(u^n),  t^n = n dt
+ *   Eq. 4  h^2 (d_xx + d_yy) p ~ w0 p + sum_l w_l (p_{i+l} + p_{i-l} + p_{j+l} + p_{j-l})
+ *   Eq. 5  d_zz q ~ sum_{l=-Rz}^{Rz} w^z_{k,l} q_{k+l}   (dz absorbed)
+ *   P:87-90          Cerjan damping in the embedding band; zero exterior for
+ *                    R_xy points in x, y and R_z in z.
+ *
+ * Readings where the paper is silent (DESIGN.md "Readings" lists all of them):
+ *   c1  z-sum runs l = -Rz..Rz (2Rz+1 weights); row m = l + Rz.
+ *   c3  cxy_l = w^xy_l / h^2 computed in double and rounded once to T.
+ *   c6  source at the nearest grid point, no cell-volume normalisation,
+ *       added into F_p (mask bit 1) and/or F_q (mask bit 2, test mode).
+ *   c7  source delay t0: s(t^n) = ricker(n dt - t0).
+ *   c8  u^0 = u^{-1} = 0 unless the caller supplies a state; step n uses s(n dt).
+ *   c9  damping g = exp(-(alpha (W - d))^2) for d = min(idx, N-1-idx) < W,
+ *       product over the three axes, applied as u^{n+1} = g (2u^n - g u^{n-1}
+ *       + dt^2 F)  (the "damp next, cur, prev" rule of SPEC.md l.214, exactly
+ *       equal on the observable level).
+ *   c12 accumulation order (fp32 "canonical" mode): L = c0*p, then for
+ *       l = 1..R  L = fma(c_l, (p_{i+l}+p_{i-l}) + (p_{j+l}+p_{j-l}), L);
+ *       D = w0*q_{k-Rz}, then D = fma(w_m, q_{k-Rz+m}, D) for m = 1..2Rz;
+ *       F = fma(v, L, vz2*D); u^{n+1} = g*fma(dt2, F, fma(-g, u^{n-1}, 2u^n)).
+ *   Ricker: x = pi*f*tau, a = x*x, s = (1 - 2a)*exp(-a), in double, then
+ *       s_n = (float)(amp*s).
+ *
+ * Build (by __graft_entry__.build()):  gcc -O2 -ffp-contract=off -fno-fast-math
+ *   -fopenmp -shared -fPIC.  No FTZ/DAZ: subnormals are IEEE.
+ *   Every point is independent, so results do not depend on the thread count.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef struct {
+    int32_t nx, ny, nz;          /* interior extents, damping band included (c10) */
+    int32_t r_xy, r_z;           /* stencil radii */
+    double h;                    /* dx = dy [m] */
+    double dt;                   /* [s] */
+    int32_t damp_width;          /* W (0 = no damping) */
+    double damp_alpha;           /* alpha */
+    int32_t src_i, src_j, src_k; /* source grid point (0-based, interior); src_i < 0: none */
+    double src_f, src_t0, src_amp;
+    int32_t src_mask;            /* 1 = into F_p (Eq. 1), 2 = into F_q, 3 = both */
+} vto_params;
+
+/* Ricker wavelet, at time t with delay t0 (reading c7). */
+double vto_ricker(double t, double f, double t0)
+{
+    double x = M_PI * f * (t - t0);
+    double a = x * x;
+    return (1.0 - 2.0 * a) * exp(-a);
+}
+
+/* Source sample s(t^n), t^n = n dt, rounded once to float32. */
+float vto_source_f32(const vto_params *P, int64_t n)
+{
+    return (float)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));
+}
+
+/* Cerjan taper value at index idx of an axis with n points (reading c9). */
+double vto_damping(int32_t idx, int32_t n, int32_t W, double alpha)
+{
+    int32_t d = idx < n - 1 - idx ? idx : n - 1 - idx;
+    if (d >= W) return 1.0;
+    double a = alpha * (double)(W - d);
+    return exp(-(a * a));
+}
+
+void vto_damping_profile_f32(int32_t n, int32_t W, double alpha, float *out)
+{
+    for (int32_t i = 0; i < n; ++i) out[i] = (float)vto_damping(i, n, W, alpha);
+}
+
+int vto_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+static int check_params(const vto_params *P)
+{
+    if (P->nx < 1 || P->ny < 1 || P->nz < 1) return 2;
+    if (P->r_xy < 1 || P->r_z < 1 || !(P->h > 0.0) || !(P->dt > 0.0)) return 1;
+    if (P->damp_width < 0) return 1;
+    if (P->damp_width > 0 && (2 * P->damp_width >= P->nx || 2 * P->damp_width >= P->ny ||
+                              2 * P->damp_width >= P->nz)) return 2;
+    return 0;
+}
+
+/*
+ * One definition of the per-point update, instantiated for T = float (the
+ * canonical fp32 mode) and T = double. pc[] = the Eq. 4 cross of p^n:
+ * pc[0] = p(i,j,k), pc[l] = p(i+l), pc[R+l] = p(i-l), pc[2R+l] = p(j+l),
+ * pc[3R+l] = p(j-l); qc[m] = q^n(i,j,k-Rz+m), m = 0..2Rz (Eq. 5).
+ */
+#define DEFINE_ORACLE(T, SFX, FMA)                                                              \
+static void point_##SFX(int R, int Rz, const T *cxy, const T *wzrow, T dt2, T g,               \
+                        const T *pc, const T *qc, T pm, T qm, T vx2, T vn2, T vz2,             \
+                        int src_bits, T s, T *pn, T *qn)                                        \
+{                                                                                              \
+    /* Eq. 4 divided by h^2 (reading c3): L = (p_xx + p_yy) */                                  \
+    T L = cxy[0] * pc[0];                                                                      \
+    for (int l = 1; l <= R; ++l)                                                               \
+        L = FMA(cxy[l], (pc[l] + pc[R + l]) + (pc[2 * R + l] + pc[3 * R + l]), L);             \
+    /* Eq. 5: D = q_zz, ascending l = -Rz..Rz */                                               \
+    T D = wzrow[0] * qc[0];                                                                    \
+    for (int m = 1; m <= 2 * Rz; ++m)                                                          \
+        D = FMA(wzrow[m], qc[m], D);                                                           \
+    /* Eqs. 1-2: F_p = vx2 L + vz2 D (+ s), F_q = vn2 L + vz2 D */                             \
+    T vD = vz2 * D;                                                                            \
+    T Fp = FMA(vx2, L, vD);                                                                    \
+    if (src_bits & 1) Fp = Fp + s;                                                             \
+    T Fq = FMA(vn2, L, vD);                                                                    \
+    if (src_bits & 2) Fq = Fq + s;                                                             \
+    /* Eq. 3 with Cerjan damping (reading c9) */                                               \
+    *pn = g * FMA(dt2, Fp, FMA(-g, pm, (T)2 * pc[0]));                                         \
+    *qn = g * FMA(dt2, Fq, FMA(-g, qm, (T)2 * qc[Rz]));                                        \
+}                                                                                              \
+                                                                                               \
+/* Single-point evaluation of step n from caller-gathered neighbourhoods. */                   \
+int vto_point_##SFX(const vto_params *P, const T *wxy, const T *wzrow, int32_t i, int32_t j,  \
+                    int32_t k, int64_t n, const T *pc, const T *qc, T pm, T qm, T vx2, T vn2,  \
+                    T vz2, T *out2)                                                            \
+{                                                                                              \
+    int rc = check_params(P);                                                                  \
+    if (rc) return rc;                                                                         \
+    int R = P->r_xy, Rz = P->r_z;                                                              \
+    T cxy[64];                                                                                 \
+    if (R >= 64) return 1;                                                                     \
+    for (int l = 0; l <= R; ++l) cxy[l] = (T)((double)wxy[l] / (P->h * P->h));                 \
+    T dt2 = (T)(P->dt * P->dt);                                                                \
+    int W = P->damp_width;                                                                     \
+    T gx = (T)vto_damping(i, P->nx, W, P->damp_alpha);                                         \
+    T gy = (T)vto_damping(j, P->ny, W, P->damp_alpha);                                         \
+    T gz = (T)vto_damping(k, P->nz, W, P->damp_alpha);                                         \
+    T g = (gx * gy) * gz;                                                                      \
+    int bits = (P->src_i == i && P->src_j == j && P->src_k == k) ? P->src_mask : 0;            \
+    T s = (T)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));                \
+    point_##SFX(R, Rz, cxy, wzrow, dt2, g, pc, qc, pm, qm, vx2, vn2, vz2, bits, s,             \
+                &out2[0], &out2[1]);                                                           \
+    return 0;                                                                                  \
+}                                                                                              \
+                                                                                               \
+/*                                                                                             \
+ * Run nsteps steps starting at time level n0. Arrays are interior-only, user                  \
+ * layout [z][y][x] (x fastest). On entry p,q = u^{n0}, pm,qm = u^{n0-1}; on                   \
+ * exit p,q = u^{n0+nsteps}, pm,qm = u^{n0+nsteps-1}. *seconds (if non-NULL)                   \
+ * receives the wall time of the step loop only.                                               \
+ */                                                                                            \
+int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2,               \
+                  const T *vn2, const T *vz2, T *p, T *q, T *pm, T *qm, int64_t n0,            \
+                  int32_t nsteps, int32_t nthreads, double *seconds)                           \
+{                                                                                              \
+    int rc = check_params(P);                                                                  \
+    if (rc) return rc;                                                                         \
+    const int R = P->r_xy, Rz = P->r_z, nx = P->nx, ny = P->ny, nz = P->nz;                    \
+    const int64_t X = nx + 2 * R, Y = ny + 2 * R, Z = nz + 2 * Rz;                             \
+    const int64_t npad = X * Y * Z;                                                            \
+    T *buf[4];                                                                                 \
+    for (int b = 0; b < 4; ++b) {                                                              \
+        buf[b] = (T *)calloc((size_t)npad, sizeof(T));  /* zero exterior */          \
+        if (!buf[b]) { for (int c = 0; c < b; ++c) free(buf[c]); return 3; }                   \
+    }                                                                                          \
+    T *Pc = buf[0], *Qc = buf[1], *Pm = buf[2], *Qm = buf[3];                                  \
+    _Pragma("omp parallel for collapse(2)")                                                    \
+    for (int k = 0; k < nz; ++k)                                                               \
+        for (int j = 0; j < ny; ++j)                                                           \
+            for (int i = 0; i < nx; ++i) {                                                     \
+                int64_t u = ((int64_t)k * ny + j) * nx + i;                                    \
+                int64_t a = ((int64_t)(k + Rz) * Y + (j + R)) * X + (i + R);                   \
+                Pc[a] = p[u]; Qc[a] = q[u]; Pm[a] = pm[u]; Qm[a] = qm[u];                      \
+            }                                                                                  \
+    T cxy[64];                                                                                 \
+    if (R >= 64) { for (int b = 0; b < 4; ++b) free(buf[b]); return 1; }                      \
+    for (int l = 0; l <= R; ++l) cxy[l] = (T)((double)wxy[l] / (P->h * P->h));                 \
+    const T dt2 = (T)(P->dt * P->dt);                                                          \
+    T *gx = (T *)malloc(sizeof(T) * nx), *gy = (T *)malloc(sizeof(T) * ny),                    \
+      *gz = (T *)malloc(sizeof(T) * nz);                                                       \
+    for (int i = 0; i < nx; ++i) gx[i] = (T)vto_damping(i, nx, P->damp_width, P->damp_alpha);  \
+    for (int j = 0; j < ny; ++j) gy[j] = (T)vto_damping(j, ny, P->damp_width, P->damp_alpha);  \
+    for (int k = 0; k < nz; ++k) gz[k] = (T)vto_damping(k, nz, P->damp_width, P->damp_alpha);  \
+    const int nt = nthreads > 0 ? nthreads : vto_max_threads();                                \
+    double t_start = now_s();                                                                  \
+    for (int64_t n = n0; n < n0 + nsteps; ++n) {                                               \
+        const T s = (T)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));      \
+        _Pragma("omp parallel for collapse(2) schedule(static) num_threads(nt)")                \
+        for (int k = 0; k < nz; ++k)                                                           \
+            for (int j = 0; j < ny; ++j)                                                       \
+                for (int i = 0; i < nx; ++i) {                                                 \
+                    T pc[4 * 64 + 1], qc[2 * 64 + 1];                                          \
+                    const int64_t a = ((int64_t)(k + Rz) * Y + (j + R)) * X + (i + R);         \
+                    const int64_t u = ((int64_t)k * ny + j) * nx + i;                          \
+                    pc[0] = Pc[a];                                                             \
+                    for (int l = 1; l <= R; ++l) {                                             \
+                        pc[l] = Pc[a + l];                                                     \
+                        pc[R + l] = Pc[a - l];                                                 \
+                        pc[2 * R + l] = Pc[a + l * X];                                         \
+                        pc[3 * R + l] = Pc[a - l * X];                                         \
+                    }                                                                          \
+                    for (int m = 0; m <= 2 * Rz; ++m) qc[m] = Qc[a + (int64_t)(m - Rz) * X * Y]; \
+                    const T g = (gx[i] * gy[j]) * gz[k];                                       \
+                    const int bits = (P->src_i == i && P->src_j == j && P->src_k == k)         \
+                                         ? P->src_mask : 0;                                    \
+                    T pn, qn;                                                                  \
+                    point_##SFX(R, Rz, cxy, wz + (int64_t)k * (2 * Rz + 1), dt2, g, pc, qc,    \
+                                Pm[a], Qm[a], vx2[u], vn2[u], vz2[u], bits, s, &pn, &qn);      \
+                    Pm[a] = pn;  /* u^{n+1} overwrites u^{n-1} in place */                     \
+                    Qm[a] = qn;                                                                \
+                }                                                                              \
+        T *t;                                                                                  \
+        t = Pc; Pc = Pm; Pm = t;                                                               \
+        t = Qc; Qc = Qm; Qm = t;                                                               \
+    }                                                                                          \
+    double t_end = now_s();                                                                    \
+    if (seconds) *seconds = t_end - t_start;                                                   \
+    _Pragma("omp parallel for collapse(2)")                                                    \
+    for (int k = 0; k < nz; ++k)                                                               \
+        for (int j = 0; j < ny; ++j)                                                           \
+            for (int i = 0; i < nx; ++i) {                                                     \
+                int64_t u = ((int64_t)k * ny + j) * nx + i;                                    \
+                int64_t a = ((int64_t)(k + Rz) * Y + (j + R)) * X + (i + R);                   \
+                p[u] = Pc[a]; q[u] = Qc[a]; pm[u] = Pm[a]; qm[u] = Qm[a];                      \
+            }                                                                                  \
+    free(gx); free(gy); free(gz);                                                              \
+    for (int b = 0; b < 4; ++b) free(buf[b]);                                                  \
+    return 0;                                                                                  \
+}
+
+DEFINE_ORACLE(float, f32, fmaf)
+DEFINE_ORACLE(double, f64, fma)
