@@ -1,0 +1,191 @@
+/*
+ * vti.h -- C ABI of the B200-native VTI propagator step (arXiv 1410.1387).
+ *
+ * One time step advances the coupled p/q wavefields of the reduced elastic
+ * VTI system (Eqs. 1-2) with the centred leapfrog of Eq. 3
+ * (l.47-53):  u^{n+1} = g (2 u^n - g u^{n-1} + dt^2 F(u^n)),  u = (p, q),
+ *   F_p = vx2 L(p) + vz2 D(q) + s(t^n) delta(x - x_src),
+ *   F_q = vn2 L(p) + vz2 D(q),
+ * with L the symmetric R_xy-radius x-y Laplacian of Eq. 4 (l.74-78), D the
+ * variable-spacing z second derivative of Eq. 5 (l.82-87, 2R_z+1 weights per
+ * plane k), s the Ricker wavelet of l.44-45, g the separable Cerjan taper of
+ * l.87-89 and a zero exterior (l.89-90).
+ *
+ * Conventions (all entry points):
+ *  - Every call returns a vti_status; on error the handle (if any) keeps a
+ *    message readable with vti_last_error(). No call aborts the process.
+ *  - Ownership: the library owns all device memory behind a vti_t. Caller
+ *    buffers are borrowed for the duration of the call only (copied in/out).
+ *    Pointers may be host memory or device memory (UVA): the library detects
+ *    which with cudaPointerGetAttributes.
+ *  - User layout of every 3-D array: [z][y][x], x fastest,
+ *    interior points only (no halo, no padding). With nranks > 1 an array
+ *    covers this rank's y-slab only: [nz][ny_local][nx] (see vti_slab).
+ *  - Precision: fp32 storage and arithmetic in a fixed "canonical" operation
+ *    order (reading c12), so results are bitwise reproducible.
+ *  - Threading: a handle is single-writer; calls on one handle must not race.
+ *  - Asynchrony: vti_step enqueues work on the handle's stream and returns;
+ *    vti_get_fields / vti_sync synchronise.
+ */
+#ifndef VTI_H
+#define VTI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VTI_ABI_VERSION 1
+
+typedef struct vti_s *vti_t;
+
+typedef enum {
+    VTI_OK = 0,
+    VTI_E_PARAM = 1,        /* bad scalar argument: radius, h, dt, mask, NULL pointer */
+    VTI_E_GEOMETRY = 2,     /* bad extents: too few planes, 2W >= extent, slab thinner than R_xy (l.59, l.136) */
+    VTI_E_MODEL = 3,        /* vz2 <= 0 or non-finite model value */
+    VTI_E_ANISO = 4,        /* reserved: strict eps >= delta check (warn-only by default) */
+    VTI_E_INSTABILITY = 5,  /* non-finite wavefield detected (check_every > 0) */
+    VTI_E_INDEX = 6,        /* source or plane range outside the domain */
+    VTI_E_CUDA = 7,         /* CUDA runtime / driver failure (message has the CUDA error) */
+    VTI_E_COMM = 8,         /* NCCL failure or NCCL unavailable for nranks > 1 */
+    VTI_E_STATE = 9,        /* call not valid in the handle's current state */
+    VTI_E_UNSUPPORTED = 10  /* (r_xy, r_z) pair not compiled into this library */
+} vti_status;
+
+typedef struct {
+    int32_t nx, ny, nz;     /* GLOBAL interior extents incl. the damping band (c10); ny global */
+    double h;               /* dx = dy [m] (Eq. 4 is for h^2-scaled weights) */
+    int32_t r_xy, r_z;      /* radii; compiled pairs: (4,4) (8,4) (6,6) (12,8) */
+    double dt;              /* time step [s]; used as float32 dt^2 = (float)(dt*dt) */
+    int32_t damp_width;     /* Cerjan width W in points per face (0 = off) */
+    double damp_alpha;      /* Cerjan alpha (default 0.015) */
+    int32_t device;         /* CUDA device ordinal */
+    void *stream;           /* cudaStream_t to run on, or NULL (library creates one) */
+    int32_t rank, nranks;   /* y-slab index / count; (0, 1) on a single GPU */
+    const void *nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (nranks > 1);
+                               NULL with nranks > 1 = "local group" mode (vti_group_step) */
+    int32_t check_every;    /* > 0: test for non-finite values every this many steps */
+} vti_config;
+
+typedef struct {
+    int32_t y0, ny_local;   /* this rank's rows [y0, y0 + ny_local) of the global grid */
+    int32_t nx_pad;         /* padded x stride (floats) of the internal layout */
+    int32_t tile_x, tile_y; /* CTA tile of the step kernel */
+    int32_t zchunk;         /* planes per work item */
+    int32_t grid;           /* CTAs launched per step (persistent) */
+    int32_t work_items;     /* tiles x z-chunks per step */
+    int32_t launches_per_step; /* kernels per vti_step step: 1 (one slab) or 2 (edge + interior) */
+    int64_t device_bytes;   /* device memory owned by the handle */
+    int64_t time_index;     /* n: fields hold u^n and u^{n-1} */
+} vti_info;
+
+/* Library ABI version (VTI_ABI_VERSION). */
+int32_t vti_abi_version(void);
+
+/* Static text for a status code. */
+const char *vti_status_string(vti_status s);
+
+/* y-slab of rank cfg->rank: rows [*y0, *y0 + *ny_local), the first ny % nranks
+ * ranks getting one extra row. Host-only; never touches the GPU. */
+vti_status vti_slab(const vti_config *cfg, int32_t *y0, int32_t *ny_local);
+
+/* Fill out[128] with a fresh ncclUniqueId (rank 0 calls it, then broadcasts).
+ * VTI_E_COMM if NCCL cannot be loaded. */
+vti_status vti_nccl_unique_id(void *out128);
+
+/*
+ * Create a propagator. w_xy: R_xy+1 float32 weights of Eq. 4 for the
+ * h^2-scaled Laplacian (w_xy[0] = centre). w_z: nz*(2R_z+1) float32 weights of
+ * Eq. 5, row k = plane k (global), column m = l + R_z for l = -R_z..R_z, dz
+ * absorbed (1/m^2). Fields start at zero (u^0 = u^{-1} = 0, reading c8), the
+ * model at zero (must be set before stepping), no source.
+ * Errors: PARAM, GEOMETRY, UNSUPPORTED, CUDA, COMM. On error *out = NULL.
+ */
+vti_status vti_create(vti_t *out, const vti_config *cfg, const float *w_xy, const float *w_z);
+
+/* Upload this rank's model slab (vx2 = nu_x^2, vn2 = nu_n^2, vz2 = nu_z^2 [m^2/s^2],
+ * PAPER.md l.39-43), each [nz][ny_local][nx]. Errors: PARAM (NULL), MODEL
+ * (vz2 <= 0 or non-finite anywhere), CUDA. vn2 > vx2 (eps < delta) is
+ * accepted; vti_model_warnings() reports how many points had it (reading c5). */
+vti_status vti_set_model(vti_t h, const float *vx2, const float *vn2, const float *vz2);
+
+/* Same for planes [k0, k0+nk) only: arrays are [nk][ny_local][nx]. */
+vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx2,
+                                const float *vn2, const float *vz2);
+
+/* Points with vn2 > vx2 (eps < delta) seen by vti_set_model* so far. */
+int64_t vti_model_warnings(vti_t h);
+
+/*
+ * Point source s(t) delta(x - x_src) of Eq. 1: Ricker wavelet
+ * s(t^n) = amp * (1 - 2a) exp(-a), a = (pi f (n dt - t0))^2, evaluated in
+ * double on the host and rounded once to float32 per step; added into F_p
+ * (field_mask bit 1, Eq. 1) and/or F_q (bit 2, test mode) at GLOBAL grid
+ * point (i, j, k) (reading c6). One source per handle: a second call
+ * replaces the first. Errors: INDEX (outside the grid), PARAM (mask not 1..3).
+ * A rank whose slab does not hold row j stores the source but never injects it.
+ */
+vti_status vti_add_source(vti_t h, int32_t i, int32_t j, int32_t k, double f, double t0,
+                          double amp, int32_t field_mask);
+
+/* Replace the state: p,q = u^n and pm,qm = u^{n-1} (each [nz][ny_local][nx]),
+ * and set the time index to n. NULL pm/qm = zero. Errors: PARAM, CUDA. */
+vti_status vti_set_fields(vti_t h, const float *p, const float *q, const float *pm,
+                          const float *qm, int64_t time_index);
+
+/* Planes [k0, k0+nk) of the state (time index unchanged; pm/qm may be NULL = zero). */
+vti_status vti_set_fields_planes(vti_t h, int32_t k0, int32_t nk, const float *p, const float *q,
+                                 const float *pm, const float *qm);
+
+/* Advance nsteps time steps (async on the handle's stream). With nranks > 1
+ * and an nccl_id, every rank must call it with the same nsteps (NCCL halo
+ * exchange of p's R_xy boundary rows each step). Errors: STATE (model unset,
+ * or local-group handle), INSTABILITY (check_every), CUDA, COMM. */
+vti_status vti_step(vti_t h, int32_t nsteps);
+
+/* vti_step bracketed by CUDA events on the handle's stream; *ms = device time
+ * of the nsteps steps (synchronises). */
+vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms);
+
+/* Local group: n handles created with the same cfg except rank = 0..n-1,
+ * nranks = n and nccl_id = NULL (any devices, one process). Steps them in
+ * lockstep with device-to-device halo copies instead of NCCL. */
+vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps);
+
+/* Copy out u^n (level 0) or the stored u^{n-1} (level 1) of this slab into
+ * p, q ([nz][ny_local][nx]; either may be NULL). Synchronises.
+ * Note: with damping, the stored u^{n-1} is the undamped previous level
+ * (reading c9). Errors: PARAM, CUDA. */
+vti_status vti_get_fields(vti_t h, float *p, float *q, int32_t level);
+
+/* Planes [k0, k0+nk) of vti_get_fields. */
+vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level);
+
+/* Block until all work on the handle's stream(s) is done. */
+vti_status vti_sync(vti_t h);
+
+/* Current time index n (number of steps taken since time index 0). */
+int64_t vti_time_index(vti_t h);
+
+/* The cudaStream_t the step kernels run on. */
+void *vti_stream(vti_t h);
+
+/* Layout / launch facts of the handle. */
+vti_status vti_query(vti_t h, vti_info *info);
+
+/* Tuning knobs (0 = library default): planes per work item, CTAs per SM. */
+vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm);
+
+/* Last error message of the handle (or of the last failed vti_create when h is NULL). */
+const char *vti_last_error(vti_t h);
+
+/* Free the handle and its device memory (NULL is a no-op). */
+vti_status vti_destroy(vti_t h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VTI_H */

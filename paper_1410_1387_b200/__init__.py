@@ -1,0 +1,267 @@
+"""B200-native VTI propagator step (arXiv 1410.1387) -- Python binding.
+
+Argument marshalling only: every step of the path runs in libvti.so
+(include/vti.h), built for sm_100a by ``paper_1410_1387_b200._build``. There
+is no CPU fallback: if the library is missing, importing this package raises.
+
+Raw C-ABI functions are re-exported under their C names (``vti_create``,
+``vti_step`` ...); the ``VTI`` class wraps one handle. Arrays may be numpy
+arrays (host) or torch tensors (host or CUDA), float32, C-contiguous, in the
+user layout [z][y][x] of this rank's y-slab.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from ._build import LIB, build  # noqa: F401
+
+__all__ = ["VTI", "VTIError", "Config", "Info", "lib", "slab", "nccl_unique_id", "group_step"]
+
+STATUS = {
+    0: "VTI_OK", 1: "VTI_E_PARAM", 2: "VTI_E_GEOMETRY", 3: "VTI_E_MODEL", 4: "VTI_E_ANISO",
+    5: "VTI_E_INSTABILITY", 6: "VTI_E_INDEX", 7: "VTI_E_CUDA", 8: "VTI_E_COMM", 9: "VTI_E_STATE",
+    10: "VTI_E_UNSUPPORTED",
+}
+COMPILED_RADII = ((4, 4), (8, 4), (6, 6), (12, 8))
+
+
+class VTIError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+        ("h", C.c_double), ("r_xy", C.c_int32), ("r_z", C.c_int32), ("dt", C.c_double),
+        ("damp_width", C.c_int32), ("damp_alpha", C.c_double), ("device", C.c_int32),
+        ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
+        ("nccl_id", C.c_void_p), ("check_every", C.c_int32),
+    ]
+
+
+class Info(C.Structure):
+    _fields_ = [
+        ("y0", C.c_int32), ("ny_local", C.c_int32), ("nx_pad", C.c_int32),
+        ("tile_x", C.c_int32), ("tile_y", C.c_int32), ("zchunk", C.c_int32), ("grid", C.c_int32),
+        ("work_items", C.c_int32), ("launches_per_step", C.c_int32),
+        ("device_bytes", C.c_int64), ("time_index", C.c_int64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB):
+        raise ImportError(f"{LIB} is missing: run paper_1410_1387_b200._build.build() "
+                          "(or __graft_entry__.build()); there is no fallback path")
+    L = C.CDLL(LIB)
+    H = C.c_void_p
+    P = C.c_void_p
+    st = C.c_int
+    sig = {
+        "vti_abi_version": (C.c_int32, []),
+        "vti_status_string": (C.c_char_p, [st]),
+        "vti_slab": (st, [C.POINTER(Config), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "vti_nccl_unique_id": (st, [P]),
+        "vti_create": (st, [C.POINTER(H), C.POINTER(Config), P, P]),
+        "vti_set_model": (st, [H, P, P, P]),
+        "vti_set_model_planes": (st, [H, C.c_int32, C.c_int32, P, P, P]),
+        "vti_model_warnings": (C.c_int64, [H]),
+        "vti_add_source": (st, [H, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                C.c_int32]),
+        "vti_set_fields": (st, [H, P, P, P, P, C.c_int64]),
+        "vti_set_fields_planes": (st, [H, C.c_int32, C.c_int32, P, P, P, P]),
+        "vti_step": (st, [H, C.c_int32]),
+        "vti_step_timed": (st, [H, C.c_int32, C.POINTER(C.c_float)]),
+        "vti_group_step": (st, [C.POINTER(H), C.c_int32, C.c_int32]),
+        "vti_get_fields": (st, [H, P, P, C.c_int32]),
+        "vti_get_fields_planes": (st, [H, C.c_int32, C.c_int32, P, P, C.c_int32]),
+        "vti_sync": (st, [H]),
+        "vti_time_index": (C.c_int64, [H]),
+        "vti_stream": (C.c_void_p, [H]),
+        "vti_query": (st, [H, C.POINTER(Info)]),
+        "vti_set_tuning": (st, [H, C.c_int32, C.c_int32]),
+        "vti_last_error": (C.c_char_p, [H]),
+        "vti_destroy": (st, [H]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L, list(sig)
+
+
+lib, EXPORTS = _load()
+for _n in EXPORTS:
+    globals()[_n] = getattr(lib, _n)
+
+
+def _ptr(a, nelem: int | None = None, writable: bool = False):
+    """Raw pointer of a float32 C-contiguous numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float32 or not a.is_contiguous():
+                raise TypeError("torch tensors must be float32 and contiguous")
+            if nelem is not None and a.numel() != nelem:
+                raise ValueError(f"expected {nelem} elements, got {a.numel()}")
+            return a.data_ptr(), a
+    except ImportError:
+        pass
+    if writable:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous):
+            raise TypeError("output arrays must be float32 C-contiguous numpy arrays or torch tensors")
+        arr = a
+    else:
+        arr = np.ascontiguousarray(a, dtype=np.float32)
+    if nelem is not None and arr.size != nelem:
+        raise ValueError(f"expected {nelem} elements, got {arr.size}")
+    return arr.ctypes.data, arr
+
+
+def _check(h, status: int):
+    if status != 0:
+        msg = lib.vti_last_error(h)
+        raise VTIError(status, msg.decode() if msg else "")
+
+
+def slab(ny: int, rank: int, nranks: int):
+    """(y0, ny_local) of a rank, from the library's own partition rule."""
+    c = Config(ny=ny, rank=rank, nranks=nranks)
+    y0, n = C.c_int32(), C.c_int32()
+    _check(None, lib.vti_slab(C.byref(c), C.byref(y0), C.byref(n)))
+    return y0.value, n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(None, lib.vti_nccl_unique_id(buf))
+    return buf.raw
+
+
+class VTI:
+    """One propagator handle (one GPU, one y-slab). See include/vti.h."""
+
+    def __init__(self, nx, ny, nz, h, r_xy, r_z, dt, w_xy, w_z, damp_width=20, damp_alpha=0.015,
+                 device=0, stream=None, rank=0, nranks=1, nccl_id: bytes | None = None,
+                 check_every=0):
+        self._id_buf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        self.cfg = Config(nx=nx, ny=ny, nz=nz, h=h, r_xy=r_xy, r_z=r_z, dt=dt, damp_width=damp_width,
+                          damp_alpha=damp_alpha, device=device, stream=stream, rank=rank, nranks=nranks,
+                          nccl_id=C.cast(self._id_buf, C.c_void_p) if self._id_buf is not None else None,
+                          check_every=check_every)
+        wxy_p, self._wxy = _ptr(w_xy, r_xy + 1)
+        wz_p, self._wz = _ptr(w_z, nz * (2 * r_z + 1))
+        self.h = C.c_void_p()
+        _check(None, lib.vti_create(C.byref(self.h), C.byref(self.cfg), wxy_p, wz_p))
+        self.y0, self.ny_local = slab(ny, rank, nranks)
+        self.nx, self.ny, self.nz = nx, ny, nz
+
+    # -- lifecycle
+    def close(self):
+        if self.h:
+            lib.vti_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- inputs
+    def _n(self, nk=None):
+        return (self.nz if nk is None else nk) * self.ny_local * self.nx
+
+    def set_model(self, vx2, vn2, vz2):
+        a = [_ptr(x, self._n()) for x in (vx2, vn2, vz2)]
+        _check(self.h, lib.vti_set_model(self.h, a[0][0], a[1][0], a[2][0]))
+
+    def set_model_planes(self, k0, vx2, vn2, vz2):
+        nk = (vx2.shape[0] if hasattr(vx2, "shape") else len(vx2))
+        a = [_ptr(x, self._n(nk)) for x in (vx2, vn2, vz2)]
+        _check(self.h, lib.vti_set_model_planes(self.h, k0, nk, a[0][0], a[1][0], a[2][0]))
+
+    def model_warnings(self) -> int:
+        return lib.vti_model_warnings(self.h)
+
+    def add_source(self, i, j, k, f=15.0, t0=0.0, amp=1.0, mask=1):
+        _check(self.h, lib.vti_add_source(self.h, i, j, k, f, t0, amp, mask))
+
+    def set_fields(self, p, q, pm=None, qm=None, time_index=0):
+        a = [_ptr(x, self._n()) for x in (p, q, pm, qm)]
+        _check(self.h, lib.vti_set_fields(self.h, a[0][0], a[1][0], a[2][0], a[3][0], time_index))
+
+    def set_fields_planes(self, k0, p, q, pm=None, qm=None):
+        nk = p.shape[0]
+        a = [_ptr(x, self._n(nk)) for x in (p, q, pm, qm)]
+        _check(self.h, lib.vti_set_fields_planes(self.h, k0, nk, a[0][0], a[1][0], a[2][0], a[3][0]))
+
+    # -- stepping
+    def step(self, nsteps=1):
+        _check(self.h, lib.vti_step(self.h, nsteps))
+
+    def step_timed(self, nsteps=1) -> float:
+        ms = C.c_float()
+        _check(self.h, lib.vti_step_timed(self.h, nsteps, C.byref(ms)))
+        return ms.value
+
+    def sync(self):
+        _check(self.h, lib.vti_sync(self.h))
+
+    # -- outputs
+    def get_fields(self, level=0, p=None, q=None, planes=None):
+        """(p, q) of u^n (level 0) or u^{n-1} (level 1). Allocates numpy arrays unless given."""
+        k0, nk = (0, self.nz) if planes is None else planes
+        shape = (nk, self.ny_local, self.nx)
+        if p is None:
+            p = np.empty(shape, dtype=np.float32)
+        if q is None:
+            q = np.empty(shape, dtype=np.float32)
+        pp, _ = _ptr(p, self._n(nk), writable=True)
+        qp, _ = _ptr(q, self._n(nk), writable=True)
+        _check(self.h, lib.vti_get_fields_planes(self.h, k0, nk, pp, qp, level))
+        return p, q
+
+    @property
+    def time_index(self) -> int:
+        return lib.vti_time_index(self.h)
+
+    @property
+    def stream(self) -> int:
+        return lib.vti_stream(self.h) or 0
+
+    def info(self) -> dict:
+        i = Info()
+        _check(self.h, lib.vti_query(self.h, C.byref(i)))
+        return i.as_dict()
+
+    def set_tuning(self, zchunk=0, ctas_per_sm=0):
+        _check(self.h, lib.vti_set_tuning(self.h, zchunk, ctas_per_sm))
+
+
+def group_step(handles, nsteps=1):
+    """Local-group stepping of handles created with nranks=len(handles), nccl_id=None."""
+    arr = (C.c_void_p * len(handles))(*[h.h for h in handles])
+    st = lib.vti_group_step(arr, len(handles), nsteps)
+    if st != 0:
+        for h in handles:
+            msg = lib.vti_last_error(h.h)
+            if msg:
+                raise VTIError(st, msg.decode())
+        raise VTIError(st, "")

@@ -1,0 +1,365 @@
+// vti_kernel.cuh -- the fused VTI time-step kernel for sm_100a (B200).
+//
+// One launch = one time step of the reduced elastic VTI propagator
+// (Eqs. 1-3) over a set of x-y tiles:
+//   L  = cxy0 p + sum_l cxy_l [(p_{i+l}+p_{i-l}) + (p_{j+l}+p_{j-l})]   Eq. 4 / h^2
+//   D  = sum_{m=0}^{2Rz} w^z[k][m] q_{k-Rz+m}                            Eq. 5
+//   Fp = vx2 L + vz2 D (+ s at the source),  Fq = vn2 L + vz2 D          Eqs. 1-2
+//   u^{n+1} = g (2 u^n - g u^{n-1} + dt^2 F),  g = (gx gy) gz            Eq. 3 + Cerjan
+// in exactly the operation order of the oracle (reading c12), so
+// parity is bitwise. Build with -fmad=false (no FMA contraction beyond the
+// explicit __fmaf_rn below) and without --use_fast_math (IEEE subnormals).
+//
+// Design: 2.5-D blocking after the paper's GPU kernel
+// (x-y tile in shared memory + z register rolling), made
+// B200-native:
+//  * a persistent grid of CTAs pulls work items (64x16 x-y tile, z-chunk);
+//  * warp 8 is a TMA producer: per z plane it issues cp.async.bulk.tensor
+//    loads of the halo'd p^n plane tile, the q^n plane Rz ahead, p^{n-1},
+//    q^{n-1}, vx2, vn2, vz2 and a 1-D bulk copy of the plane's w^z row + gz,
+//    all completing on one mbarrier of an S-stage ring; out-of-bounds box
+//    elements are zero-filled by TMA, which IS the paper's zero exterior
+//    (l.89-90) in x, y and z;
+//  * warps 0-7 consume: each thread owns 4 consecutive x points (float4) of
+//    one row, keeps a (2Rz+1)-deep float4 register queue of q along z, reads
+//    the p cross from shared memory and writes p^{n+1}, q^{n+1} with 16-byte
+//    stores in place over p^{n-1}, q^{n-1}.
+#pragma once
+
+#include <cuda.h>
+#include <stdint.h>
+
+namespace vti {
+
+constexpr int TX = 64;               // tile width in x (points) = 16 threads x float4
+constexpr int TY = 16;               // tile height in y (rows)
+constexpr int NCONS_WARPS = 8;       // consumer warps: 16 x 16 threads
+constexpr int NTHREADS = (NCONS_WARPS + 1) * 32;
+constexpr int MAX_R = 12;
+
+__host__ __device__ constexpr int align128(int b) { return (b + 127) / 128 * 128; }
+
+template <int R, int RZ>
+struct Cfg {
+    // x apron rounded up to 4 floats: the TMA box must start on a 16-byte
+    // boundary in x (x0 - RA), and every shared-memory read is then a float4.
+    static constexpr int RA = (R + 3) / 4 * 4;
+    static constexpr int PW = TX + 2 * RA;                // p tile row length (floats)
+    static constexpr int PH = TY + 2 * R;                 // p tile rows
+    static constexpr int NQ = 2 * RZ + 1;                 // q queue depth
+    static constexpr int ZROW = ((NQ + 1 + 3) / 4) * 4;   // w^z row + gz, padded to 16 B
+    static constexpr int P_BYTES = PW * PH * 4;
+    static constexpr int S_BYTES = TX * TY * 4;
+    static constexpr int OFF_P = 0;
+    static constexpr int OFF_Q = align128(P_BYTES);
+    static constexpr int OFF_PM = OFF_Q + S_BYTES;
+    static constexpr int OFF_QM = OFF_PM + S_BYTES;
+    static constexpr int OFF_VX = OFF_QM + S_BYTES;
+    static constexpr int OFF_VN = OFF_VX + S_BYTES;
+    static constexpr int OFF_VZ = OFF_VN + S_BYTES;
+    static constexpr int OFF_ZR = OFF_VZ + S_BYTES;
+    static constexpr int STAGE = align128(OFF_ZR + ZROW * 4);
+    static constexpr uint32_t FULL_TX = P_BYTES + 6 * S_BYTES + ZROW * 4;
+    static constexpr uint32_t PRIME_TX = S_BYTES;
+    static_assert(PW % 4 == 0, "p tile rows must be 16-byte multiples");
+    static_assert(PW <= 256 && PH <= 256, "TMA box limit");
+};
+
+struct StepParams {
+    CUtensorMap tm_p;    // p^n  : dims {nx, nz, nyl + 2R} (y-halo rows), box {TX + 2RA, 1, TY + 2R}
+    CUtensorMap tm_q;    // q^n  : dims {nx, nz, nyl}, box {TX, 1, TY}
+    CUtensorMap tm_pm;   // p^{n-1}: interior rows of the other p buffer
+    CUtensorMap tm_qm;   // q^{n-1}
+    CUtensorMap tm_vx;   // vx2
+    CUtensorMap tm_vn;   // vn2
+    CUtensorMap tm_vz;   // vz2
+    float *p_out;        // p^{n+1}: interior row 0 of the other p buffer
+    float *q_out;        // q^{n+1}
+    const float *zrow;   // [nz][ZROW]: w^z[k][0..2Rz], gz[k], 0 ...
+    const float *gx;     // [ntx * TX] (1 beyond nx)
+    const float *gy;     // [nyl] local rows
+    float cxy[MAX_R + 1];
+    float dt2;
+    float s;             // s(t^n) this step
+    int src_i, src_j, src_k, src_mask;   // local indices; src_mask = 0: no source here
+    int nx, nyl, nz, nxp;
+    int ntx;                             // tiles along x
+    int ty_begin, ty_step, nty;          // tile rows ty_begin + t * ty_step, t < nty
+    int zchunk, nzc;                     // planes per chunk, chunks
+    int items;                           // ntx * nty * nzc
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
+{
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+
+__device__ __forceinline__ float4 lds4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ float2 lds2(const float *p) { return *reinterpret_cast<const float2 *>(p); }
+
+__device__ __forceinline__ float f4(const float4 &v, int c)
+{
+    return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+
+__device__ __forceinline__ void decode_item(const StepParams &P, int item, int &x0, int &y0, int &kb, int &ke)
+{
+    const int tx = item % P.ntx;
+    const int rest = item / P.ntx;
+    const int t = rest % P.nty;
+    const int zc = rest / P.nty;
+    x0 = tx * TX;
+    y0 = (P.ty_begin + t * P.ty_step) * TY;   // local row of the tile's first row
+    kb = zc * P.zchunk;
+    ke = min(P.nz, kb + P.zchunk);
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int R, int RZ, int STAGES, int MINB>
+__global__ void __launch_bounds__(NTHREADS, MINB) vti_step_kernel(const __grid_constant__ StepParams P)
+{
+    using C = Cfg<R, RZ>;
+    constexpr int NQ = C::NQ;
+    constexpr int RA = C::RA;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE);
+    uint64_t *empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCONS_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NCONS_WARPS) {
+        // ======================= TMA producer (one elected lane) =======================
+        if (lane == 0) {
+            prefetch_tmap(&P.tm_p);
+            prefetch_tmap(&P.tm_q);
+            prefetch_tmap(&P.tm_pm);
+            prefetch_tmap(&P.tm_qm);
+            prefetch_tmap(&P.tm_vx);
+            prefetch_tmap(&P.tm_vn);
+            prefetch_tmap(&P.tm_vz);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+                int x0, y0, kb, ke;
+                decode_item(P, item, x0, y0, kb, ke);
+                const int nload = (ke - kb) + 2 * RZ;
+                for (int t = 0; t < nload; ++t) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t *st = smem + stage * C::STAGE;
+                    uint64_t *bar = &full[stage];
+                    if (t < 2 * RZ) {
+                        // priming: q^n planes kb-Rz .. kb+Rz-1 (OOB planes -> 0)
+                        mbar_arrive_expect_tx(bar, C::PRIME_TX);
+                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, kb - RZ + t, y0, bar);
+                    } else {
+                        const int k = kb + t - 2 * RZ;
+                        mbar_arrive_expect_tx(bar, C::FULL_TX);
+                        // p^n plane with R-point apron; y coordinate is the halo'd row
+                        // index, whose row y0 is local row y0 - R.
+                        tma_load_3d(st + C::OFF_P, &P.tm_p, x0 - RA, k, y0, bar);
+                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, k + RZ, y0, bar);
+                        tma_load_3d(st + C::OFF_PM, &P.tm_pm, x0, k, y0, bar);
+                        tma_load_3d(st + C::OFF_QM, &P.tm_qm, x0, k, y0, bar);
+                        tma_load_3d(st + C::OFF_VX, &P.tm_vx, x0, k, y0, bar);
+                        tma_load_3d(st + C::OFF_VN, &P.tm_vn, x0, k, y0, bar);
+                        tma_load_3d(st + C::OFF_VZ, &P.tm_vz, x0, k, y0, bar);
+                        bulk_load(st + C::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * 4, bar);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ======================= consumers: 16 x 16 threads, 4 x-points each =======================
+    const int tx = threadIdx.x & 15;
+    const int ty = threadIdx.x >> 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    const size_t row_stride = (size_t)P.nz * P.nxp;   // floats between y rows
+
+    for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+        int x0, y0, kb, ke;
+        decode_item(P, item, x0, y0, kb, ke);
+        const int xg = x0 + 4 * tx;      // first of this thread's 4 columns
+        const int yl = y0 + ty;          // local row
+        const bool store_ok = (yl < P.nyl) && (xg < P.nx);
+        float gxy[4];
+        {
+            const float gyv = (yl < P.nyl) ? P.gy[yl] : 0.f;
+            const float4 g4 = *reinterpret_cast<const float4 *>(P.gx + xg);
+            gxy[0] = g4.x * gyv;
+            gxy[1] = g4.y * gyv;
+            gxy[2] = g4.z * gyv;
+            gxy[3] = g4.w * gyv;
+        }
+        const bool src_col = P.src_mask != 0 && P.src_j == yl && P.src_i >= xg && P.src_i < xg + 4;
+        const int src_c = P.src_i - xg;
+        float *pout = P.p_out + (size_t)yl * row_stride + xg;
+        float *qout = P.q_out + (size_t)yl * row_stride + xg;
+        const int sidx = ty * TX + 4 * tx;   // this thread's float offset in a stream tile
+
+        float4 q[NQ];
+        // prime the queue with q(kb - Rz .. kb + Rz - 1)
+#pragma unroll
+        for (int t = 0; t < 2 * RZ; ++t) {
+            mbar_wait(&full[stage], phase);
+            const float *st = reinterpret_cast<const float *>(smem + stage * C::STAGE);
+            q[t] = lds4(st + C::OFF_Q / 4 + sidx);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+
+        for (int kbase = kb; kbase < ke; kbase += NQ) {
+#pragma unroll
+            for (int u = 0; u < NQ; ++u) {
+                const int k = kbase + u;
+                if (k < ke) {
+                    mbar_wait(&full[stage], phase);
+                    const float *st = reinterpret_cast<const float *>(smem + stage * C::STAGE);
+                    q[(u + 2 * RZ) % NQ] = lds4(st + C::OFF_Q / 4 + sidx);   // q^n(k + Rz)
+                    const float *ps = st + C::OFF_P / 4;
+                    const float *prow = ps + (ty + R) * C::PW + 4 * tx;      // window start x0+4tx-RA
+                    float w[4 + 2 * RA];
+#pragma unroll
+                    for (int v = 0; v < (4 + 2 * RA) / 4; ++v) {
+                        const float4 t4 = lds4(prow + 4 * v);
+                        w[4 * v + 0] = t4.x;
+                        w[4 * v + 1] = t4.y;
+                        w[4 * v + 2] = t4.z;
+                        w[4 * v + 3] = t4.w;
+                    }
+                    const float *zr = st + C::OFF_ZR / 4;
+                    float zw[NQ + 1];
+#pragma unroll
+                    for (int m = 0; m < NQ + 1; ++m) zw[m] = zr[m];
+                    // Eq. 4 / h^2, canonical order: L = c0 p; L = fma(c_l, xpair + ypair, L)
+                    float L[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) L[c] = P.cxy[0] * w[RA + c];
+#pragma unroll
+                    for (int l = 1; l <= R; ++l) {
+                        const float4 yp = lds4(prow + l * C::PW + RA);
+                        const float4 ym = lds4(prow - l * C::PW + RA);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float xpair = w[RA + c + l] + w[RA + c - l];
+                            const float ypair = f4(yp, c) + f4(ym, c);
+                            L[c] = __fmaf_rn(P.cxy[l], xpair + ypair, L[c]);
+                        }
+                    }
+                    const float4 pm4 = lds4(st + C::OFF_PM / 4 + sidx);
+                    const float4 qm4 = lds4(st + C::OFF_QM / 4 + sidx);
+                    const float4 vx4 = lds4(st + C::OFF_VX / 4 + sidx);
+                    const float4 vn4 = lds4(st + C::OFF_VN / 4 + sidx);
+                    const float4 vz4 = lds4(st + C::OFF_VZ / 4 + sidx);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    const bool src_here = src_col && (k == P.src_k);
+                    float pn[4], qn[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
+                        float D = zw[0] * f4(q[u % NQ], c);
+#pragma unroll
+                        for (int m = 1; m < NQ; ++m) D = __fmaf_rn(zw[m], f4(q[(u + m) % NQ], c), D);
+                        const float vD = f4(vz4, c) * D;
+                        float Fp = __fmaf_rn(f4(vx4, c), L[c], vD);
+                        float Fq = __fmaf_rn(f4(vn4, c), L[c], vD);
+                        if (src_here && c == src_c) {
+                            if (P.src_mask & 1) Fp = Fp + P.s;
+                            if (P.src_mask & 2) Fq = Fq + P.s;
+                        }
+                        const float g = gxy[c] * zw[NQ];   // (gx gy) gz
+                        pn[c] = g * __fmaf_rn(P.dt2, Fp, __fmaf_rn(-g, f4(pm4, c), 2.0f * w[RA + c]));
+                        qn[c] = g * __fmaf_rn(P.dt2, Fq, __fmaf_rn(-g, f4(qm4, c), 2.0f * f4(q[(u + RZ) % NQ], c)));
+                    }
+                    if (store_ok) {
+                        const size_t off = (size_t)k * P.nxp;
+                        *reinterpret_cast<float4 *>(pout + off) = make_float4(pn[0], pn[1], pn[2], pn[3]);
+                        *reinterpret_cast<float4 *>(qout + off) = make_float4(qn[0], qn[1], qn[2], qn[3]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+}  // namespace vti

@@ -1,0 +1,1022 @@
+// vti_runtime.cu -- host runtime behind include/vti.h (B200 / sm_100a).
+//
+// Owns device buffers in the internal layout [y][z][x] (x padded to a
+// multiple of 32 floats, p with R_xy halo rows on both y sides so the
+// multi-GPU halo rows are contiguous), builds the TMA tensor maps, the
+// per-plane w^z + gz table and the 1-D Cerjan profiles, evaluates the Ricker
+// sample per step on the host, and launches the step kernel(s). With
+// nranks > 1 it exchanges p's R_xy boundary rows after each step, over NCCL
+// (one process per GPU) or with device-to-device copies (local group).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "vti.h"
+#include "vti_kernel.cuh"
+
+using namespace vti;
+
+// ============================================================ NCCL (dlopen'ed)
+typedef struct ncclComm *ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+typedef enum { ncclSuccess = 0 } ncclResult_t;
+typedef enum { ncclFloat32 = 7 } ncclDataType_t;
+
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi &nccl()
+{
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *env = getenv("VTI_NCCL_LIB");
+        const char *names[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
+        void *h = nullptr;
+        for (const char *n : names) {
+            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) {
+            api.err = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+            return;
+        }
+#define LOADSYM(field, name)                                                   \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));        \
+    if (!api.field) {                                                          \
+        api.err = std::string("missing NCCL symbol ") + name;                  \
+        return;                                                                \
+    }
+        LOADSYM(GetUniqueId, "ncclGetUniqueId");
+        LOADSYM(CommInitRank, "ncclCommInitRank");
+        LOADSYM(CommDestroy, "ncclCommDestroy");
+        LOADSYM(Send, "ncclSend");
+        LOADSYM(Recv, "ncclRecv");
+        LOADSYM(GroupStart, "ncclGroupStart");
+        LOADSYM(GroupEnd, "ncclGroupEnd");
+        LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+        api.ok = true;
+    });
+    return api;
+}
+
+// ============================================================ driver entry point
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode()
+{
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+// ============================================================ kernel table
+struct KernelEntry {
+    int r, rz, stages, minb, stage_bytes;
+    void (*fn)(StepParams);
+    int zrow;
+};
+
+template <int R, int RZ, int S, int B>
+static KernelEntry entry()
+{
+    return KernelEntry{R, RZ, S, B, Cfg<R, RZ>::STAGE, vti_step_kernel<R, RZ, S, B>, Cfg<R, RZ>::ZROW};
+}
+
+static const KernelEntry *find_kernel(int r, int rz)
+{
+    static const KernelEntry table[] = {
+        entry<4, 4, 3, 2>(),
+        entry<8, 4, 3, 2>(),
+        entry<6, 6, 3, 2>(),
+        entry<12, 8, 2, 2>(),
+    };
+    for (const auto &e : table)
+        if (e.r == r && e.rz == rz) return &e;
+    return nullptr;
+}
+
+// ============================================================ aux kernels
+// user [nk][nyl][nx] -> internal rows [y][z][x] (base = interior row 0), planes k0..
+__global__ void k_user_to_internal(const float *__restrict__ src, float *__restrict__ dst, int nk, int nyl, int nx,
+                                   int nz, int nxp, int k0)
+{
+    const int64_t n = (int64_t)nk * nyl * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const int64_t r = t / nx;
+        const int y = (int)(r % nyl);
+        const int k = (int)(r / nyl);
+        dst[((int64_t)y * nz + (k0 + k)) * nxp + x] = src ? src[t] : 0.f;
+    }
+}
+
+__global__ void k_internal_to_user(const float *__restrict__ src, float *__restrict__ dst, int nk, int nyl, int nx,
+                                   int nz, int nxp, int k0)
+{
+    const int64_t n = (int64_t)nk * nyl * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const int64_t r = t / nx;
+        const int y = (int)(r % nyl);
+        const int k = (int)(r / nyl);
+        dst[t] = src[((int64_t)y * nz + (k0 + k)) * nxp + x];
+    }
+}
+
+// counters: [0] vz2 <= 0 or non-finite, [1] vx2/vn2 non-finite, [2] vn2 > vx2 -- over internal rows,
+// planes k0..k0+nk, columns < nx
+__global__ void k_check_model(const float *__restrict__ vx2, const float *__restrict__ vn2,
+                              const float *__restrict__ vz2, int nyl, int nz, int nxp, int nx, int k0, int nk,
+                              unsigned long long *counters)
+{
+    unsigned long long bad = 0, nonfin = 0, aniso = 0;
+    const int64_t n = (int64_t)nyl * nk * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const int64_t r = t / nx;
+        const int k = (int)(r % nk);
+        const int y = (int)(r / nk);
+        const int64_t a = ((int64_t)y * nz + k0 + k) * nxp + x;
+        const float vx = vx2[a], vn = vn2[a], vz = vz2[a];
+        bad += !(vz > 0.f) || !isfinite(vz);
+        nonfin += !isfinite(vx) || !isfinite(vn);
+        aniso += vn > vx;
+    }
+    if (bad) atomicAdd(&counters[0], bad);
+    if (nonfin) atomicAdd(&counters[1], nonfin);
+    if (aniso) atomicAdd(&counters[2], aniso);
+}
+
+// non-finite test of u^n (p, q) over internal interior rows, columns < nx
+__global__ void k_check_finite(const float *__restrict__ p, const float *__restrict__ q, int nyl, int nz, int nxp,
+                               int nx, unsigned int *flag)
+{
+    bool bad = false;
+    const int64_t n = (int64_t)nyl * nz * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const int64_t a = (t / nx) * nxp + x;
+        bad |= !isfinite(p[a]) || !isfinite(q[a]);
+    }
+    if (bad) atomicOr(flag, 1u);
+}
+
+// ============================================================ handle
+struct vti_s {
+    vti_config cfg{};
+    std::string err;
+    int R = 0, RZ = 0;
+    int y0 = 0, nyl = 0, nxp = 0;
+    int ntx = 0, nty = 0;
+    const KernelEntry *K = nullptr;
+    int smem_bytes = 0;
+    int sms = 0, ctas_per_sm = 0;
+    int zchunk = 0, nzc = 0, grid = 0;
+    int tune_zchunk = 0, tune_ctas = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_edge = nullptr, ev_comm = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    float *pbuf[2] = {nullptr, nullptr};   // (nyl + 2R) rows each
+    float *qbuf[2] = {nullptr, nullptr};   // nyl rows
+    float *vx2 = nullptr, *vn2 = nullptr, *vz2 = nullptr;
+    float *zrow = nullptr, *gx = nullptr, *gy = nullptr;
+    float *staging = nullptr;
+    size_t staging_floats = 0;
+    unsigned long long *counters = nullptr;
+    unsigned int *flag = nullptr;
+    int64_t device_bytes = 0;
+    CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
+    float cxy[MAX_R + 1] = {0};
+    float dt2 = 0.f;
+    int cur = 0;           // pbuf[cur], qbuf[cur] hold u^n
+    int64_t n = 0;         // time index
+    bool model_set = false;
+    int64_t model_planes_set = 0;
+    int64_t aniso_warn = 0;
+    bool has_src = false;
+    int src_i = 0, src_j = 0, src_k = 0, src_mask = 0;
+    double src_f = 15.0, src_t0 = 0.0, src_amp = 1.0;
+    ncclComm_t comm_nccl = nullptr;
+    bool group_mode = false;
+    bool halo_dirty = false;
+
+    size_t row_floats() const { return (size_t)cfg.nz * nxp; }
+    float *p_int(int b) const { return pbuf[b] + (size_t)R * row_floats(); }
+};
+
+static std::mutex g_err_mu;
+static std::string g_create_err;
+
+static vti_status fail(vti_s *h, vti_status s, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (h) {
+        h->err = buf;
+    } else {
+        std::lock_guard<std::mutex> g(g_err_mu);
+        g_create_err = buf;
+    }
+    return s;
+}
+
+#define CU(h, call)                                                                                   \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess) return fail(h, VTI_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+static double damping(int idx, int n, int W, double alpha)
+{
+    // Cerjan taper: g = exp(-(alpha (W - d))^2), d = distance to the nearest face.
+    int d = idx < n - 1 - idx ? idx : n - 1 - idx;
+    if (d >= W) return 1.0;
+    double a = alpha * (double)(W - d);
+    return exp(-(a * a));
+}
+
+static double ricker(double t, double f, double t0)
+{
+    // s = (1 - 2 pi^2 f^2 t^2) exp(-pi^2 f^2 t^2), evaluated as x = pi f tau, a = x^2.
+    double x = M_PI * f * (t - t0);
+    double a = x * x;
+    return (1.0 - 2.0 * a) * exp(-a);
+}
+
+static bool is_device_ptr(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static vti_status encode(vti_s *h, CUtensorMap *tm, float *base, int rows, int bx, int by)
+{
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t dims[3] = {(cuuint64_t)h->cfg.nx, (cuuint64_t)h->cfg.nz, (cuuint64_t)rows};
+    cuuint64_t strides[2] = {(cuuint64_t)h->nxp * 4, (cuuint64_t)h->row_floats() * 4};
+    cuuint32_t box[3] = {(cuuint32_t)bx, 1u, (cuuint32_t)by};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);   // NONE = zero fill: the paper's zero exterior
+    if (r != CUDA_SUCCESS) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return VTI_OK;
+}
+
+static void choose_schedule(vti_s *h)
+{
+    const int slots = h->sms * h->ctas_per_sm;
+    const int tiles = h->ntx * h->nty;
+    const int nz = h->cfg.nz;
+    if (h->tune_zchunk > 0) {
+        h->zchunk = std::min(h->tune_zchunk, nz);
+    } else {
+        // maximise wave efficiency, penalising the 2Rz-plane q re-read of each extra chunk
+        double best = -1;
+        int best_zc = nz;
+        for (int nzc = 1; nzc <= std::max(1, nz / 16); ++nzc) {
+            const int zc = (nz + nzc - 1) / nzc;
+            const int nzc_eff = (nz + zc - 1) / zc;
+            const long items = (long)tiles * nzc_eff;
+            const long rounds = (items + slots - 1) / slots;
+            const double eff = (double)items / (double)(rounds * slots);
+            const double over = 1.0 + (2.0 * h->RZ * 4.0) / (36.0 * zc);
+            const double score = eff / over;
+            if (score > best + 1e-9) {
+                best = score;
+                best_zc = zc;
+            }
+        }
+        h->zchunk = best_zc;
+    }
+    h->nzc = (nz + h->zchunk - 1) / h->zchunk;
+    const long items = (long)tiles * h->nzc;
+    h->grid = (int)std::min<long>(items, slots);
+}
+
+static vti_status check_cfg(const vti_config *c)
+{
+    if (!c) return VTI_E_PARAM;
+    if (c->r_xy < 1 || c->r_z < 1 || c->r_xy > MAX_R || !(c->h > 0) || !(c->dt > 0) || c->damp_width < 0)
+        return VTI_E_PARAM;
+    if (c->nx < 1 || c->ny < 1 || c->nz < 1) return VTI_E_GEOMETRY;
+    if (c->nz < 2 * c->r_z + 1) return VTI_E_GEOMETRY;   // too few planes
+    if (c->damp_width > 0 && (2 * c->damp_width >= c->nx || 2 * c->damp_width >= c->ny || 2 * c->damp_width >= c->nz))
+        return VTI_E_GEOMETRY;
+    if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return VTI_E_PARAM;
+    if (c->ny / c->nranks < c->r_xy) return VTI_E_GEOMETRY;   // slab thinner than the halo
+    return VTI_OK;
+}
+
+// ============================================================ C ABI
+extern "C" {
+
+int32_t vti_abi_version(void) { return VTI_ABI_VERSION; }
+
+const char *vti_status_string(vti_status s)
+{
+    switch (s) {
+    case VTI_OK: return "ok";
+    case VTI_E_PARAM: return "bad parameter";
+    case VTI_E_GEOMETRY: return "bad geometry";
+    case VTI_E_MODEL: return "bad model";
+    case VTI_E_ANISO: return "anisotropy condition violated";
+    case VTI_E_INSTABILITY: return "non-finite wavefield (instability)";
+    case VTI_E_INDEX: return "index out of range";
+    case VTI_E_CUDA: return "CUDA error";
+    case VTI_E_COMM: return "communication error";
+    case VTI_E_STATE: return "invalid state";
+    case VTI_E_UNSUPPORTED: return "unsupported radius pair";
+    }
+    return "unknown status";
+}
+
+vti_status vti_slab(const vti_config *cfg, int32_t *y0, int32_t *ny_local)
+{
+    if (!cfg || !y0 || !ny_local || cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks || cfg->ny < 1)
+        return VTI_E_PARAM;
+    const int base = cfg->ny / cfg->nranks, extra = cfg->ny % cfg->nranks;
+    *ny_local = base + (cfg->rank < extra ? 1 : 0);
+    *y0 = cfg->rank * base + std::min(cfg->rank, extra);
+    return VTI_OK;
+}
+
+vti_status vti_nccl_unique_id(void *out128)
+{
+    if (!out128) return fail(nullptr, VTI_E_PARAM, "NULL output");
+    NcclApi &api = nccl();
+    if (!api.ok) return fail(nullptr, VTI_E_COMM, "%s", api.err.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, VTI_E_COMM, "ncclGetUniqueId: %s", api.GetErrorString(r));
+    memcpy(out128, &id, sizeof id);
+    return VTI_OK;
+}
+
+vti_status vti_destroy(vti_t h)
+{
+    if (!h) return VTI_OK;
+    if (h->device_bytes || h->stream) cudaSetDevice(h->cfg.device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm) cudaStreamSynchronize(h->comm);
+    if (h->comm_nccl && nccl().ok) nccl().CommDestroy(h->comm_nccl);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(h->pbuf[b]);
+        cudaFree(h->qbuf[b]);
+    }
+    cudaFree(h->vx2);
+    cudaFree(h->vn2);
+    cudaFree(h->vz2);
+    cudaFree(h->zrow);
+    cudaFree(h->gx);
+    cudaFree(h->gy);
+    cudaFree(h->staging);
+    cudaFree(h->counters);
+    cudaFree(h->flag);
+    for (cudaEvent_t e : {h->ev_edge, h->ev_comm, h->ev_t0, h->ev_t1})
+        if (e) cudaEventDestroy(e);
+    if (h->comm) cudaStreamDestroy(h->comm);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return VTI_OK;
+}
+
+static vti_status alloc(vti_s *h, void **p, size_t bytes)
+{
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+    e = cudaMemsetAsync(*p, 0, bytes, h->stream);
+    if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "cudaMemset: %s", cudaGetErrorString(e));
+    h->device_bytes += (int64_t)bytes;
+    return VTI_OK;
+}
+
+static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy, const float *w_z)
+{
+    vti_status st = check_cfg(cfg);
+    if (st != VTI_OK) return fail(h, st, "invalid configuration (%s)", vti_status_string(st));
+    if (!w_xy || !w_z) return fail(h, VTI_E_PARAM, "NULL weights");
+    h->cfg = *cfg;
+    h->R = cfg->r_xy;
+    h->RZ = cfg->r_z;
+    h->K = find_kernel(h->R, h->RZ);
+    if (!h->K) return fail(h, VTI_E_UNSUPPORTED, "(r_xy, r_z) = (%d, %d) not compiled", h->R, h->RZ);
+    vti_slab(cfg, &h->y0, &h->nyl);
+    h->nxp = (cfg->nx + 31) / 32 * 32;
+    h->ntx = (cfg->nx + TX - 1) / TX;
+    h->nty = (h->nyl + TY - 1) / TY;
+    for (int l = 0; l <= h->R; ++l) {
+        if (!std::isfinite(w_xy[l])) return fail(h, VTI_E_PARAM, "non-finite w_xy[%d]", l);
+        h->cxy[l] = (float)((double)w_xy[l] / (cfg->h * cfg->h));   // reading c3
+    }
+    h->dt2 = (float)(cfg->dt * cfg->dt);
+
+    CU(h, cudaSetDevice(cfg->device));
+    if (cfg->stream) {
+        h->stream = (cudaStream_t)cfg->stream;
+    } else {
+        CU(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    int prio_lo, prio_hi;
+    CU(h, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CU(h, cudaStreamCreateWithPriority(&h->comm, cudaStreamNonBlocking, prio_hi));
+    CU(h, cudaEventCreateWithFlags(&h->ev_edge, cudaEventDisableTiming));
+    CU(h, cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
+    CU(h, cudaEventCreate(&h->ev_t0));
+    CU(h, cudaEventCreate(&h->ev_t1));
+    CU(h, cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cfg->device));
+
+    h->smem_bytes = h->K->stages * h->K->stage_bytes + 2 * h->K->stages * 8;
+    CU(h, cudaFuncSetAttribute((const void *)h->K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+    CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)h->K->fn, NTHREADS,
+                                                        h->smem_bytes));
+    if (h->ctas_per_sm < 1) return fail(h, VTI_E_CUDA, "step kernel cannot be resident (smem %d B)", h->smem_bytes);
+    choose_schedule(h);
+
+    const size_t rowf = h->row_floats();
+    const size_t pfl = (size_t)(h->nyl + 2 * h->R) * rowf, qfl = (size_t)h->nyl * rowf;
+    vti_status s;
+    for (int b = 0; b < 2; ++b) {
+        if ((s = alloc(h, (void **)&h->pbuf[b], pfl * 4)) != VTI_OK) return s;
+        if ((s = alloc(h, (void **)&h->qbuf[b], qfl * 4)) != VTI_OK) return s;
+    }
+    if ((s = alloc(h, (void **)&h->vx2, qfl * 4)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->vn2, qfl * 4)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->vz2, qfl * 4)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->counters, 4 * sizeof(unsigned long long))) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->flag, sizeof(unsigned int))) != VTI_OK) return s;
+
+    // per-plane z rows: w^z[k][0..2Rz], gz[k], zero pad (host double -> float once)
+    const int NQ = 2 * h->RZ + 1, ZR = h->K->zrow;
+    std::vector<float> zr((size_t)cfg->nz * ZR, 0.f);
+    for (int k = 0; k < cfg->nz; ++k) {
+        for (int m = 0; m < NQ; ++m) {
+            float v = w_z[(size_t)k * NQ + m];
+            if (!std::isfinite(v)) return fail(h, VTI_E_PARAM, "non-finite w_z[%d][%d]", k, m);
+            zr[(size_t)k * ZR + m] = v;
+        }
+        zr[(size_t)k * ZR + NQ] = (float)damping(k, cfg->nz, cfg->damp_width, cfg->damp_alpha);
+    }
+    std::vector<float> gxv((size_t)h->ntx * TX, 1.f), gyv(h->nyl);
+    for (int i = 0; i < cfg->nx; ++i) gxv[i] = (float)damping(i, cfg->nx, cfg->damp_width, cfg->damp_alpha);
+    for (int j = 0; j < h->nyl; ++j) gyv[j] = (float)damping(h->y0 + j, cfg->ny, cfg->damp_width, cfg->damp_alpha);
+    if ((s = alloc(h, (void **)&h->zrow, zr.size() * 4)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->gx, gxv.size() * 4)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->gy, gyv.size() * 4)) != VTI_OK) return s;
+    CU(h, cudaMemcpyAsync(h->zrow, zr.data(), zr.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    CU(h, cudaMemcpyAsync(h->gx, gxv.data(), gxv.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    CU(h, cudaMemcpyAsync(h->gy, gyv.data(), gyv.size() * 4, cudaMemcpyHostToDevice, h->stream));
+
+    const int RA = (h->R + 3) / 4 * 4;   // 16-byte aligned x apron (see Cfg::RA)
+    const int PW = TX + 2 * RA, PH = TY + 2 * h->R;
+    for (int b = 0; b < 2; ++b) {
+        if ((s = encode(h, &h->tm_ph[b], h->pbuf[b], h->nyl + 2 * h->R, PW, PH)) != VTI_OK) return s;
+        if ((s = encode(h, &h->tm_pi[b], h->p_int(b), h->nyl, TX, TY)) != VTI_OK) return s;
+        if ((s = encode(h, &h->tm_q[b], h->qbuf[b], h->nyl, TX, TY)) != VTI_OK) return s;
+    }
+    if ((s = encode(h, &h->tm_vx, h->vx2, h->nyl, TX, TY)) != VTI_OK) return s;
+    if ((s = encode(h, &h->tm_vn, h->vn2, h->nyl, TX, TY)) != VTI_OK) return s;
+    if ((s = encode(h, &h->tm_vz, h->vz2, h->nyl, TX, TY)) != VTI_OK) return s;
+
+    if (cfg->nranks > 1) {
+        if (cfg->nccl_id) {
+            NcclApi &api = nccl();
+            if (!api.ok) return fail(h, VTI_E_COMM, "%s", api.err.c_str());
+            ncclUniqueId id;
+            memcpy(&id, cfg->nccl_id, sizeof id);
+            ncclResult_t r = api.CommInitRank(&h->comm_nccl, cfg->nranks, id, cfg->rank);
+            if (r != ncclSuccess) return fail(h, VTI_E_COMM, "ncclCommInitRank: %s", api.GetErrorString(r));
+        } else {
+            h->group_mode = true;
+        }
+    }
+    CU(h, cudaStreamSynchronize(h->stream));
+    return VTI_OK;
+}
+
+vti_status vti_create(vti_t *out, const vti_config *cfg, const float *w_xy, const float *w_z)
+{
+    if (!out) return fail(nullptr, VTI_E_PARAM, "NULL output handle");
+    *out = nullptr;
+    vti_s *h = new vti_s();
+    vti_status s = create_impl(h, cfg, w_xy, w_z);
+    if (s != VTI_OK) {
+        {
+            std::lock_guard<std::mutex> g(g_err_mu);
+            g_create_err = h->err;
+        }
+        vti_destroy(h);
+        return s;
+    }
+    *out = h;
+    return VTI_OK;
+}
+
+const char *vti_last_error(vti_t h)
+{
+    if (h) return h->err.c_str();
+    std::lock_guard<std::mutex> g(g_err_mu);
+    return g_create_err.c_str();
+}
+
+// Copy planes [k0, k0+nk) of a user-layout array (host or device) into internal rows.
+static vti_status upload_planes(vti_s *h, float *dst_rows, const float *src, int k0, int nk)
+{
+    const int nx = h->cfg.nx, nyl = h->nyl;
+    const size_t plane = (size_t)nyl * nx;
+    if (!src) {
+        k_user_to_internal<<<4 * h->sms, 256, 0, h->stream>>>(nullptr, dst_rows, nk, nyl, nx, h->cfg.nz, h->nxp, k0);
+        CU(h, cudaGetLastError());
+        return VTI_OK;
+    }
+    if (is_device_ptr(src)) {
+        k_user_to_internal<<<4 * h->sms, 256, 0, h->stream>>>(src, dst_rows, nk, nyl, nx, h->cfg.nz, h->nxp, k0);
+        CU(h, cudaGetLastError());
+        return VTI_OK;
+    }
+    // host source: bounce through a device staging buffer in chunks of planes
+    const size_t want = std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20));
+    if (h->staging_floats < want) {
+        cudaFree(h->staging);
+        h->staging = nullptr;
+        h->staging_floats = 0;
+        CU(h, cudaMalloc(&h->staging, want * 4));
+        h->staging_floats = want;
+    }
+    const int chunk = (int)std::max<size_t>(1, h->staging_floats / plane);
+    for (int k = 0; k < nk; k += chunk) {
+        const int m = std::min(chunk, nk - k);
+        CU(h, cudaMemcpyAsync(h->staging, src + (size_t)k * plane, (size_t)m * plane * 4, cudaMemcpyHostToDevice,
+                              h->stream));
+        k_user_to_internal<<<4 * h->sms, 256, 0, h->stream>>>(h->staging, dst_rows, m, nyl, nx, h->cfg.nz, h->nxp,
+                                                               k0 + k);
+        CU(h, cudaGetLastError());
+    }
+    CU(h, cudaStreamSynchronize(h->stream));   // staging is reused; host buffer may be freed after return
+    return VTI_OK;
+}
+
+static vti_status download_planes(vti_s *h, float *dst, const float *src_rows, int k0, int nk)
+{
+    const int nx = h->cfg.nx, nyl = h->nyl;
+    const size_t plane = (size_t)nyl * nx;
+    if (is_device_ptr(dst)) {
+        k_internal_to_user<<<4 * h->sms, 256, 0, h->stream>>>(src_rows, dst, nk, nyl, nx, h->cfg.nz, h->nxp, k0);
+        CU(h, cudaGetLastError());
+        CU(h, cudaStreamSynchronize(h->stream));
+        return VTI_OK;
+    }
+    const size_t want = std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20));
+    if (h->staging_floats < want) {
+        cudaFree(h->staging);
+        h->staging = nullptr;
+        h->staging_floats = 0;
+        CU(h, cudaMalloc(&h->staging, want * 4));
+        h->staging_floats = want;
+    }
+    const int chunk = (int)std::max<size_t>(1, h->staging_floats / plane);
+    for (int k = 0; k < nk; k += chunk) {
+        const int m = std::min(chunk, nk - k);
+        k_internal_to_user<<<4 * h->sms, 256, 0, h->stream>>>(src_rows, h->staging, m, nyl, nx, h->cfg.nz, h->nxp,
+                                                               k0 + k);
+        CU(h, cudaGetLastError());
+        CU(h, cudaMemcpyAsync(dst + (size_t)k * plane, h->staging, (size_t)m * plane * 4, cudaMemcpyDeviceToHost,
+                              h->stream));
+    }
+    CU(h, cudaStreamSynchronize(h->stream));
+    return VTI_OK;
+}
+
+vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx2, const float *vn2,
+                                const float *vz2)
+{
+    if (!h) return VTI_E_PARAM;
+    if (!vx2 || !vn2 || !vz2) return fail(h, VTI_E_PARAM, "NULL model array");
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz) return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    CU(h, cudaSetDevice(h->cfg.device));
+    vti_status s;
+    if ((s = upload_planes(h, h->vx2, vx2, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->vn2, vn2, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->vz2, vz2, k0, nk)) != VTI_OK) return s;
+    // validate on the device: vz2 > 0 and finite, vx2/vn2 finite, count vn2 > vx2 (reading c5)
+    CU(h, cudaMemsetAsync(h->counters, 0, 4 * sizeof(unsigned long long), h->stream));
+    k_check_model<<<4 * h->sms, 256, 0, h->stream>>>(h->vx2, h->vn2, h->vz2, h->nyl, h->cfg.nz, h->nxp, h->cfg.nx,
+                                                     k0, nk, h->counters);
+    CU(h, cudaGetLastError());
+    unsigned long long cnt[3];
+    CU(h, cudaMemcpyAsync(cnt, h->counters, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    if (cnt[0]) return fail(h, VTI_E_MODEL, "%llu points with vz2 <= 0 or non-finite", cnt[0]);
+    if (cnt[1]) return fail(h, VTI_E_MODEL, "%llu points with non-finite vx2/vn2", cnt[1]);
+    h->aniso_warn += (int64_t)cnt[2];
+    if (k0 == 0 && nk == h->cfg.nz) h->model_set = true;
+    else h->model_planes_set += nk;
+    if (h->model_planes_set >= h->cfg.nz) h->model_set = true;
+    return VTI_OK;
+}
+
+}  // extern "C"
+
+// ============================================================ stepping
+static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int nty_sel)
+{
+    const int c = h->cur, o = 1 - c;
+    P.tm_p = h->tm_ph[c];
+    P.tm_q = h->tm_q[c];
+    P.tm_pm = h->tm_pi[o];
+    P.tm_qm = h->tm_q[o];
+    P.tm_vx = h->tm_vx;
+    P.tm_vn = h->tm_vn;
+    P.tm_vz = h->tm_vz;
+    P.p_out = h->p_int(o);
+    P.q_out = h->qbuf[o];
+    P.zrow = h->zrow;
+    P.gx = h->gx;
+    P.gy = h->gy;
+    for (int l = 0; l <= MAX_R; ++l) P.cxy[l] = l <= h->R ? h->cxy[l] : 0.f;
+    P.dt2 = h->dt2;
+    const bool owned = h->has_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
+    // s(t^n), t^n = n dt, double on the host, rounded once (reading c7)
+    P.s = owned ? (float)(h->src_amp * ricker((double)h->n * h->cfg.dt, h->src_f, h->src_t0)) : 0.f;
+    P.src_i = h->src_i;
+    P.src_j = owned ? h->src_j - h->y0 : -1;
+    P.src_k = h->src_k;
+    P.src_mask = owned ? h->src_mask : 0;
+    P.nx = h->cfg.nx;
+    P.nyl = h->nyl;
+    P.nz = h->cfg.nz;
+    P.nxp = h->nxp;
+    P.ntx = h->ntx;
+    P.ty_begin = ty_begin;
+    P.ty_step = ty_step;
+    P.nty = nty_sel;
+    P.zchunk = h->zchunk;
+    P.nzc = h->nzc;
+    P.items = h->ntx * nty_sel * h->nzc;
+}
+
+static vti_status launch_rows(vti_s *h, int ty_begin, int ty_step, int nty_sel)
+{
+    if (nty_sel <= 0) return VTI_OK;
+    StepParams P;
+    fill_params(h, P, ty_begin, ty_step, nty_sel);
+    const int grid = std::min(P.items, h->sms * h->ctas_per_sm);
+    void *args[] = {&P};
+    CU(h, cudaLaunchKernel((const void *)h->K->fn, dim3(grid), dim3(NTHREADS), args, h->smem_bytes, h->stream));
+    return VTI_OK;
+}
+
+// p rows exchanged with the neighbours: buffer b, R rows each way (contiguous in [y][z][x])
+static size_t halo_floats(const vti_s *h) { return (size_t)h->R * h->row_floats(); }
+static float *send_lo(const vti_s *h, int b) { return h->pbuf[b] + (size_t)h->R * h->row_floats(); }
+static float *send_hi(const vti_s *h, int b) { return h->pbuf[b] + (size_t)h->nyl * h->row_floats(); }
+static float *recv_lo(const vti_s *h, int b) { return h->pbuf[b]; }
+static float *recv_hi(const vti_s *h, int b) { return h->pbuf[b] + (size_t)(h->nyl + h->R) * h->row_floats(); }
+
+// NCCL halo exchange of buffer b on the comm stream after ev_edge; records ev_comm.
+static vti_status exchange_nccl(vti_s *h, int b)
+{
+    NcclApi &api = nccl();
+    CU(h, cudaStreamWaitEvent(h->comm, h->ev_edge, 0));
+    const size_t cnt = halo_floats(h);
+    const int r = h->cfg.rank, nr = h->cfg.nranks;
+    ncclResult_t e = api.GroupStart();
+    if (e == ncclSuccess && r > 0) {
+        e = api.Send(send_lo(h, b), cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
+        if (e == ncclSuccess) e = api.Recv(recv_lo(h, b), cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
+    }
+    if (e == ncclSuccess && r < nr - 1) {
+        e = api.Send(send_hi(h, b), cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
+        if (e == ncclSuccess) e = api.Recv(recv_hi(h, b), cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
+    }
+    ncclResult_t e2 = api.GroupEnd();
+    if (e != ncclSuccess || e2 != ncclSuccess)
+        return fail(h, VTI_E_COMM, "NCCL halo exchange: %s", api.GetErrorString(e != ncclSuccess ? e : e2));
+    CU(h, cudaEventRecord(h->ev_comm, h->comm));
+    return VTI_OK;
+}
+
+static vti_status check_finite(vti_s *h)
+{
+    CU(h, cudaMemsetAsync(h->flag, 0, sizeof(unsigned int), h->stream));
+    k_check_finite<<<4 * h->sms, 256, 0, h->stream>>>(h->p_int(h->cur), h->qbuf[h->cur], h->nyl, h->cfg.nz, h->nxp,
+                                                      h->cfg.nx, h->flag);
+    CU(h, cudaGetLastError());
+    unsigned int f = 0;
+    CU(h, cudaMemcpyAsync(&f, h->flag, sizeof f, cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    if (f) return fail(h, VTI_E_INSTABILITY, "non-finite wavefield at time index %lld", (long long)h->n);
+    return VTI_OK;
+}
+
+extern "C" {
+
+vti_status vti_set_model(vti_t h, const float *vx2, const float *vn2, const float *vz2)
+{
+    if (!h) return VTI_E_PARAM;
+    h->model_planes_set = 0;
+    return vti_set_model_planes(h, 0, h->cfg.nz, vx2, vn2, vz2);
+}
+
+int64_t vti_model_warnings(vti_t h) { return h ? h->aniso_warn : -1; }
+
+vti_status vti_add_source(vti_t h, int32_t i, int32_t j, int32_t k, double f, double t0, double amp,
+                          int32_t field_mask)
+{
+    if (!h) return VTI_E_PARAM;
+    if (field_mask < 1 || field_mask > 3) return fail(h, VTI_E_PARAM, "field_mask must be 1, 2 or 3");
+    if (!std::isfinite(f) || !std::isfinite(t0) || !std::isfinite(amp)) return fail(h, VTI_E_PARAM, "non-finite source parameter");
+    if (i < 0 || i >= h->cfg.nx || j < 0 || j >= h->cfg.ny || k < 0 || k >= h->cfg.nz)
+        return fail(h, VTI_E_INDEX, "source (%d,%d,%d) outside the %dx%dx%d grid", i, j, k, h->cfg.nx, h->cfg.ny,
+                    h->cfg.nz);
+    h->has_src = true;
+    h->src_i = i;
+    h->src_j = j;
+    h->src_k = k;
+    h->src_f = f;
+    h->src_t0 = t0;
+    h->src_amp = amp;
+    h->src_mask = field_mask;
+    return VTI_OK;
+}
+
+vti_status vti_set_fields_planes(vti_t h, int32_t k0, int32_t nk, const float *p, const float *q, const float *pm,
+                                 const float *qm)
+{
+    if (!h) return VTI_E_PARAM;
+    if (!p || !q) return fail(h, VTI_E_PARAM, "NULL p or q");
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz) return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->comm));
+    const int c = h->cur, o = 1 - c;
+    vti_status s;
+    if ((s = upload_planes(h, h->p_int(c), p, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->qbuf[c], q, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->p_int(o), pm, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->qbuf[o], qm, k0, nk)) != VTI_OK) return s;
+    CU(h, cudaStreamSynchronize(h->stream));
+    h->halo_dirty = h->cfg.nranks > 1;
+    return VTI_OK;
+}
+
+vti_status vti_set_fields(vti_t h, const float *p, const float *q, const float *pm, const float *qm,
+                          int64_t time_index)
+{
+    if (!h) return VTI_E_PARAM;
+    vti_status s = vti_set_fields_planes(h, 0, h->cfg.nz, p, q, pm, qm);
+    if (s == VTI_OK) h->n = time_index;
+    return s;
+}
+
+static vti_status step_single(vti_s *h)
+{
+    vti_status s = launch_rows(h, 0, 1, h->nty);
+    if (s != VTI_OK) return s;
+    h->cur = 1 - h->cur;
+    h->n += 1;
+    return VTI_OK;
+}
+
+vti_status vti_step(vti_t h, int32_t nsteps)
+{
+    if (!h) return VTI_E_PARAM;
+    if (nsteps < 0) return fail(h, VTI_E_PARAM, "nsteps < 0");
+    if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
+    if (h->group_mode) return fail(h, VTI_E_STATE, "local-group handle: use vti_group_step");
+    CU(h, cudaSetDevice(h->cfg.device));
+    const bool multi = h->cfg.nranks > 1;
+    vti_status s;
+    if (multi && h->halo_dirty) {
+        CU(h, cudaEventRecord(h->ev_edge, h->stream));
+        if ((s = exchange_nccl(h, h->cur)) != VTI_OK) return s;
+        CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
+        h->halo_dirty = false;
+    }
+    for (int it = 0; it < nsteps; ++it) {
+        if (!multi) {
+            if ((s = step_single(h)) != VTI_OK) return s;
+        } else {
+            const int o = 1 - h->cur;
+            // edge tile rows first, so the rows the neighbours need are ready early
+            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty))) != VTI_OK) return s;
+            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+            if ((s = exchange_nccl(h, o)) != VTI_OK) return s;
+            if ((s = launch_rows(h, 1, 1, h->nty - 2)) != VTI_OK) return s;   // interior rows overlap the exchange
+            CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
+            h->cur = o;
+            h->n += 1;
+        }
+        if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0)
+            if ((s = check_finite(h)) != VTI_OK) return s;
+    }
+    CU(h, cudaGetLastError());
+    return VTI_OK;
+}
+
+vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms)
+{
+    if (!h || !ms) return h ? fail(h, VTI_E_PARAM, "NULL ms") : VTI_E_PARAM;
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaEventRecord(h->ev_t0, h->stream));
+    vti_status s = vti_step(h, nsteps);
+    if (s != VTI_OK) return s;
+    CU(h, cudaEventRecord(h->ev_t1, h->stream));
+    CU(h, cudaEventSynchronize(h->ev_t1));
+    CU(h, cudaEventElapsedTime(ms, h->ev_t0, h->ev_t1));
+    return VTI_OK;
+}
+
+// Local group: device-to-device halo copies between handles of one process.
+static vti_status group_exchange(vti_t *hs, int n, int b_of_all_cur)
+{
+    // every handle's ev_edge marks "rows to send are written"; copies run on the receiver's comm stream
+    for (int i = 0; i < n; ++i) {
+        vti_s *h = hs[i];
+        const int b = b_of_all_cur ? h->cur : 1 - h->cur;
+        CU(h, cudaSetDevice(h->cfg.device));
+        const size_t bytes = halo_floats(h) * 4;
+        if (i > 0) {
+            vti_s *g = hs[i - 1];
+            const int bg = b_of_all_cur ? g->cur : 1 - g->cur;
+            CU(h, cudaStreamWaitEvent(h->comm, g->ev_edge, 0));
+            CU(h, cudaMemcpyPeerAsync(recv_lo(h, b), h->cfg.device, send_hi(g, bg), g->cfg.device, bytes, h->comm));
+        }
+        if (i < n - 1) {
+            vti_s *g = hs[i + 1];
+            const int bg = b_of_all_cur ? g->cur : 1 - g->cur;
+            CU(h, cudaStreamWaitEvent(h->comm, g->ev_edge, 0));
+            CU(h, cudaMemcpyPeerAsync(recv_hi(h, b), h->cfg.device, send_lo(g, bg), g->cfg.device, bytes, h->comm));
+        }
+        CU(h, cudaEventRecord(h->ev_comm, h->comm));
+    }
+    return VTI_OK;
+}
+
+static vti_status group_wait(vti_t *hs, int n)
+{
+    // a handle's next writes may overwrite rows its neighbours copy from: wait for theirs too
+    for (int i = 0; i < n; ++i) {
+        vti_s *h = hs[i];
+        CU(h, cudaSetDevice(h->cfg.device));
+        for (int j = std::max(0, i - 1); j <= std::min(n - 1, i + 1); ++j)
+            CU(h, cudaStreamWaitEvent(h->stream, hs[j]->ev_comm, 0));
+    }
+    return VTI_OK;
+}
+
+vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
+{
+    if (!hs || n < 1 || nsteps < 0) return VTI_E_PARAM;
+    for (int i = 0; i < n; ++i) {
+        if (!hs[i]) return VTI_E_PARAM;
+        if (hs[i]->cfg.nranks != n || hs[i]->cfg.rank != i)
+            return fail(hs[i], VTI_E_STATE, "group handle %d has rank %d / nranks %d", i, hs[i]->cfg.rank,
+                        hs[i]->cfg.nranks);
+        if (n > 1 && !hs[i]->group_mode) return fail(hs[i], VTI_E_STATE, "handle not created for local-group mode");
+        if (!hs[i]->model_set) return fail(hs[i], VTI_E_STATE, "model not set");
+        if (hs[i]->n != hs[0]->n) return fail(hs[i], VTI_E_STATE, "time indices differ inside the group");
+    }
+    if (n == 1) return vti_step(hs[0], nsteps);
+    vti_status s;
+    bool dirty = false;
+    for (int i = 0; i < n; ++i) dirty |= hs[i]->halo_dirty;
+    if (dirty) {
+        for (int i = 0; i < n; ++i) {
+            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+            CU(hs[i], cudaEventRecord(hs[i]->ev_edge, hs[i]->stream));
+        }
+        if ((s = group_exchange(hs, n, 1)) != VTI_OK) return s;
+        if ((s = group_wait(hs, n)) != VTI_OK) return s;
+        for (int i = 0; i < n; ++i) hs[i]->halo_dirty = false;
+    }
+    for (int it = 0; it < nsteps; ++it) {
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty))) != VTI_OK) return s;
+            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+        }
+        if ((s = group_exchange(hs, n, 0)) != VTI_OK) return s;
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            if ((s = launch_rows(h, 1, 1, h->nty - 2)) != VTI_OK) return s;
+        }
+        if ((s = group_wait(hs, n)) != VTI_OK) return s;
+        for (int i = 0; i < n; ++i) {
+            hs[i]->cur = 1 - hs[i]->cur;
+            hs[i]->n += 1;
+        }
+    }
+    return VTI_OK;
+}
+
+vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level)
+{
+    if (!h) return VTI_E_PARAM;
+    if (level != 0 && level != 1) return fail(h, VTI_E_PARAM, "level must be 0 (u^n) or 1 (u^{n-1})");
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz) return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->comm));
+    const int b = level == 0 ? h->cur : 1 - h->cur;
+    vti_status s;
+    if (p && (s = download_planes(h, p, h->p_int(b), k0, nk)) != VTI_OK) return s;
+    if (q && (s = download_planes(h, q, h->qbuf[b], k0, nk)) != VTI_OK) return s;
+    return VTI_OK;
+}
+
+vti_status vti_get_fields(vti_t h, float *p, float *q, int32_t level)
+{
+    if (!h) return VTI_E_PARAM;
+    return vti_get_fields_planes(h, 0, h->cfg.nz, p, q, level);
+}
+
+vti_status vti_sync(vti_t h)
+{
+    if (!h) return VTI_E_PARAM;
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    CU(h, cudaStreamSynchronize(h->comm));
+    CU(h, cudaGetLastError());
+    return VTI_OK;
+}
+
+int64_t vti_time_index(vti_t h) { return h ? h->n : -1; }
+
+void *vti_stream(vti_t h) { return h ? (void *)h->stream : nullptr; }
+
+vti_status vti_query(vti_t h, vti_info *info)
+{
+    if (!h || !info) return VTI_E_PARAM;
+    info->y0 = h->y0;
+    info->ny_local = h->nyl;
+    info->nx_pad = h->nxp;
+    info->tile_x = TX;
+    info->tile_y = TY;
+    info->zchunk = h->zchunk;
+    info->grid = std::min(h->ntx * h->nty * h->nzc, h->sms * h->ctas_per_sm);
+    info->work_items = h->ntx * h->nty * h->nzc;
+    info->launches_per_step = h->cfg.nranks > 1 ? (h->nty > 2 ? 2 : 1) : 1;
+    info->device_bytes = h->device_bytes;
+    info->time_index = h->n;
+    return VTI_OK;
+}
+
+vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm)
+{
+    if (!h) return VTI_E_PARAM;
+    if (zchunk < 0 || ctas_per_sm < 0) return fail(h, VTI_E_PARAM, "negative tuning value");
+    h->tune_zchunk = zchunk;
+    if (ctas_per_sm > 0) {
+        int maxb = 0;
+        CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, (const void *)h->K->fn, NTHREADS, h->smem_bytes));
+        h->ctas_per_sm = std::min(ctas_per_sm, maxb);
+    }
+    choose_schedule(h);
+    return VTI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Gate (BASELINE.json north_star): max relative L2 <= 1e-5 in fp32. Both sides
+implement the same canonical fp32 operation order (reading c12),
+so the expected difference is exactly zero; the bitwise assertions below
+document that, the 1e-5 gate is the contract.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from synth import fields as SF
+from synth import weights as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-30))
+
+
+def make(cfg, dt, wxy, wz, **kw):
+    from paper_1410_1387_b200 import VTI
+    return VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], cfg["r_xy"], cfg["r_z"], dt, wxy, wz,
+               damp_width=cfg["damp_width"], damp_alpha=cfg["damp_alpha"], device=0, **kw)
+
+
+def random_state(cfg, seed=7, amp=1e-3):
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    return [SF.random_planes(nx, ny, 0, nz, seed, s, amp).numpy() for s in range(4)]
+
+
+def random_model(cfg, seed=3):
+    """Pointwise random VTI model, eps >= delta (stable)."""
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    u = [SF.random_planes(nx, ny, 0, nz, seed, 10 + s, 1.0).numpy().astype(np.float64) * 0.5 + 0.5
+         for s in range(3)]
+    vz2 = (2.0e6 + 7.0e6 * u[0]).astype(np.float32)
+    eps = 0.25 * u[1]
+    dl = eps * u[2]
+    vx2 = (vz2.astype(np.float64) * (1 + 2 * eps)).astype(np.float32)
+    vn2 = (vz2.astype(np.float64) * (1 + 2 * dl)).astype(np.float32)
+    return vx2, vn2, vz2
+
+
+def small_cfg(nx, ny, nz, r, rz, damp=4, src=None, mask=1, t0=0.02, dz=(6.0, 14.0)):
+    c = synth.scaled(synth.CONFIGS["C2"](), nx, ny, nz, r_xy=r, r_z=rz, damp_width=damp, dz=dz, t0=t0,
+                     mask=mask)
+    if src is not None:
+        c["src"] = src
+    return c
+
+
+def run_both(cfg, nsteps, state=None, model=None, with_source=True, n0=0):
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    if model is None:
+        model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    with make(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        if with_source:
+            v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
+        if state is not None:
+            v.set_fields(*state, time_index=n0)
+        v.step(nsteps)
+        assert v.time_index == n0 + nsteps
+        g = v.get_fields(0) + v.get_fields(1)
+    P = oracle.params(cfg, dt, src=cfg["src"] if with_source else None)
+    o = oracle.run(P, wxy, wz, *model, state, n0=n0, nsteps=nsteps)[:4]
+    return g, o
+
+
+def assert_parity(g, o, bitwise=True):
+    for a, b in zip(g, o):
+        assert np.isfinite(a).all()
+        assert rel_l2(a, b) <= TOL
+        if bitwise:
+            assert np.array_equal(a, b), f"max |diff| {np.abs(a - b).max():.3e}"
+
+
+def test_c1_full_run():
+    """BASELINE configs[0]: 64^3, R=(4,4), homogeneous eps=0.2 delta=0.1, 100 steps, source (32,32,32)."""
+    cfg = synth.CONFIGS["C1"]()
+    g, o = run_both(cfg, cfg["steps"])
+    assert np.abs(o[0]).max() > 0
+    assert_parity(g, o)
+
+
+def test_c1_without_damping():
+    cfg = dict(synth.CONFIGS["C1"](), damp_width=0)
+    g, o = run_both(cfg, 60)
+    assert_parity(g, o)
+
+
+@pytest.mark.parametrize("r,rz", [(4, 4), (8, 4), (6, 6), (12, 8)])
+@pytest.mark.parametrize("shape", [(61, 33, 47), (24, 24, 24), (130, 17, 40), (64, 32, 17)])
+def test_random_state_ragged_shapes(r, rz, shape):
+    """Random u^n, u^{n-1} and model on ragged grids (partial tiles in x, y and z), 3 steps."""
+    nx, ny, nz = shape
+    if nz < 2 * rz + 1 or ny < r:
+        pytest.skip("grid smaller than the stencil")
+    cfg = small_cfg(nx, ny, nz, r, rz, damp=min(4, (min(shape) - 1) // 2), src=(nx // 3, ny // 2, nz // 2))
+    st = random_state(cfg)
+    g, o = run_both(cfg, 3, state=st, model=random_model(cfg), n0=5)
+    assert_parity(g, o)
+
+
+@pytest.mark.parametrize("mask", [1, 2, 3])
+def test_layered_source_masks(mask):
+    cfg = small_cfg(72, 70, 66, 4, 4, damp=10, mask=mask, src=(30, 41, 29))
+    g, o = run_both(cfg, 40)
+    assert np.abs(o[0]).max() > 0 or np.abs(o[1]).max() > 0
+    assert_parity(g, o)
+
+
+def test_source_at_grid_corner_and_edges():
+    cfg = small_cfg(40, 36, 30, 4, 4, damp=0, src=(0, 35, 29))
+    g, o = run_both(cfg, 12)
+    assert_parity(g, o)
+
+
+def test_isotropic_limit_p_equals_q():
+    """eps = delta = 0 with dual injection: p == q bitwise on the GPU (SURVEY 8(c) isotropic pin)."""
+    cfg = synth.scaled(synth.CONFIGS["C5"](), 48, 40, 44, steps=30, damp_width=6, mask=3)
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    vx2, vn2, vz2 = (a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    assert np.array_equal(vx2, vn2)
+    with make(cfg, dt, wxy, wz) as v:
+        v.set_model(vx2, vn2, vz2)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], mask=3)
+        v.step(30)
+        p, q = v.get_fields(0)
+    assert np.abs(p).max() > 0 and np.array_equal(p, q)
+
+
+def test_split_steps_and_time_index():
+    cfg = small_cfg(50, 40, 36, 4, 4, damp=5, src=(20, 20, 18))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    out = []
+    for chunks in ([25], [7, 11, 7]):
+        with make(cfg, dt, wxy, wz) as v:
+            v.set_model(*model)
+            v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+            for c in chunks:
+                v.step(c)
+            out.append(v.get_fields(0))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_device_pointer_io_matches_host_io():
+    cfg = small_cfg(40, 33, 30, 4, 4, damp=4)
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    st = random_state(cfg)
+    res = []
+    for dev in (False, True):
+        conv = (lambda a: torch.from_numpy(a).cuda()) if dev else (lambda a: a)
+        with make(cfg, dt, wxy, wz) as v:
+            v.set_model(*[conv(a) for a in model])
+            v.set_fields(*[conv(a) for a in st])
+            v.step(4)
+            if dev:
+                p = torch.empty(cfg["nz"], cfg["ny"], cfg["nx"], device="cuda")
+                q = torch.empty_like(p)
+                v.get_fields(0, p, q)
+                res.append((p.cpu().numpy(), q.cpu().numpy()))
+            else:
+                res.append(v.get_fields(0))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+def test_planes_api_roundtrip():
+    cfg = small_cfg(40, 20, 30, 4, 4, damp=0)
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    st = random_state(cfg)
+    with make(cfg, dt, wxy, wz) as v:
+        for k0 in range(0, 30, 7):
+            sl = slice(k0, min(30, k0 + 7))
+            v.set_model_planes(k0, *[a[sl] for a in model])
+            v.set_fields_planes(k0, *[a[sl] for a in st])
+        p, q = v.get_fields(0)
+        pm, qm = v.get_fields(1)
+        assert np.array_equal(p, st[0]) and np.array_equal(q, st[1])
+        assert np.array_equal(pm, st[2]) and np.array_equal(qm, st[3])
+        p2, _ = v.get_fields(0, planes=(5, 9))
+        assert np.array_equal(p2, st[0][5:14])
+
+
+def test_errors_on_gpu_handle():
+    from paper_1410_1387_b200 import VTIError
+    cfg = small_cfg(40, 20, 30, 4, 4, damp=0)
+    wxy, wz, _ = synth.weights_f32(cfg)
+    with make(cfg, 1e-4, wxy, wz) as v:
+        with pytest.raises(VTIError) as e:
+            v.step(1)
+        assert e.value.name == "VTI_E_STATE"
+        with pytest.raises(VTIError) as e:
+            v.add_source(40, 0, 0)
+        assert e.value.name == "VTI_E_INDEX"
+        with pytest.raises(VTIError) as e:
+            v.add_source(1, 1, 1, mask=4)
+        assert e.value.name == "VTI_E_PARAM"
+        bad = np.ones((30, 20, 40), np.float32)
+        with pytest.raises(VTIError) as e:
+            v.set_model(bad, bad, -bad)
+        assert e.value.name == "VTI_E_MODEL"
+        v.set_model(bad, 2 * bad, bad)
+        assert v.model_warnings() == 30 * 20 * 40   # eps < delta everywhere: warn-only
+
+
+def test_check_every_detects_instability():
+    from paper_1410_1387_b200 import VTIError
+    cfg = small_cfg(32, 32, 32, 4, 4, damp=0, src=(16, 16, 16))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = 5 * synth.stable_dt(cfg, wxy, wz)   # far beyond the CFL bound
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    with make(cfg, dt, wxy, wz, check_every=25) as v:
+        v.set_model(*model)
+        v.set_fields(*random_state(cfg, amp=1.0))
+        with pytest.raises(VTIError) as e:
+            v.step(2000)
+        assert e.value.name == "VTI_E_INSTABILITY"
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_local_group_slabs_bitwise_equal_single(nranks):
+    """y-slab decomposition with device-to-device halo copies == one slab, bitwise."""
+    from paper_1410_1387_b200 import VTI, group_step
+    cfg = small_cfg(70, 75, 40, 4, 4, damp=6, src=(30, 37, 20))
+    if nranks == 2:
+        cfg["src"] = (30, 38, 20)   # first row of rank 1: source on a slab boundary
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    st = random_state(cfg, amp=1e-4)
+    g, o = run_both(cfg, 9, state=st, model=model)
+    assert_parity(g, o)
+    hs = [VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], 4, 4, dt, wxy, wz, damp_width=cfg["damp_width"],
+              damp_alpha=cfg["damp_alpha"], device=0, rank=r, nranks=nranks) for r in range(nranks)]
+    for h in hs:
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_model(*[np.ascontiguousarray(a[:, sl]) for a in model])
+        h.set_fields(*[np.ascontiguousarray(a[:, sl]) for a in st])
+        h.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+    group_step(hs, 4)
+    group_step(hs, 5)
+    parts = [h.get_fields(0) + h.get_fields(1) for h in hs]
+    for f in range(4):
+        full = np.concatenate([p[f] for p in parts], axis=1)
+        assert np.array_equal(full, g[f])
+    for h in hs:
+        h.close()
