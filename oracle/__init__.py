@@ -82,8 +82,12 @@ def lib():
     return _lib
 
 
-def params(cfg: dict, dt: float, src=None, mask=None, damp_width=None) -> Params:
-    s = cfg["src"] if src is None else src
+_FROM_CFG = object()
+
+
+def params(cfg: dict, dt: float, src=_FROM_CFG, mask=None, damp_width=None) -> Params:
+    """Oracle parameters; ``src`` defaults to cfg["src"], ``src=None`` means no source."""
+    s = cfg.get("src") if src is _FROM_CFG else src
     return Params(
         nx=cfg["nx"], ny=cfg["ny"], nz=cfg["nz"], r_xy=cfg["r_xy"], r_z=cfg["r_z"],
         h=cfg["h"], dt=float(np.float32(dt)),
