@@ -17,7 +17,9 @@
  *  - Ownership: the library owns all device memory behind a vti_t. Caller
  *    buffers are borrowed for the duration of the call only (copied in/out).
  *    Pointers may be host memory or device memory (UVA): the library detects
- *    which with cudaPointerGetAttributes.
+ *    which with cudaPointerGetAttributes. Before reading or writing a caller's
+ *    device buffer the library synchronises the device, so buffers produced
+ *    on any stream are safe to pass; such calls are setup-time, not hot-path.
  *  - User layout of every 3-D array: [z][y][x], x fastest,
  *    interior points only (no halo, no padding). With nranks > 1 an array
  *    covers this rank's y-slab only: [nz][ny_local][nx] (see vti_slab).
@@ -72,6 +74,7 @@ typedef struct {
 typedef struct {
     int32_t y0, ny_local;   /* this rank's rows [y0, y0 + ny_local) of the global grid */
     int32_t nx_pad;         /* padded x stride (floats) of the internal layout */
+    int32_t layout;         /* 0: internal [z][y][x] (default), 1: [y][z][x] (env VTI_LAYOUT=yzx) */
     int32_t tile_x, tile_y; /* CTA tile of the step kernel */
     int32_t zchunk;         /* planes per work item */
     int32_t grid;           /* CTAs launched per step (persistent) */

@@ -32,14 +32,15 @@
 namespace vti {
 
 constexpr int TX = 64;               // tile width in x (points) = 16 threads x float4
-constexpr int TY = 16;               // tile height in y (rows)
-constexpr int NCONS_WARPS = 8;       // consumer warps: 16 x 16 threads
-constexpr int NTHREADS = (NCONS_WARPS + 1) * 32;
 constexpr int MAX_R = 12;
+
+// Tile height TY (16 or 32 rows): 16 threads per row, TY/2 consumer warps + 1 producer warp.
+__host__ __device__ constexpr int cons_warps(int ty) { return ty / 2; }
+__host__ __device__ constexpr int nthreads(int ty) { return (ty / 2 + 1) * 32; }
 
 __host__ __device__ constexpr int align128(int b) { return (b + 127) / 128 * 128; }
 
-template <int R, int RZ>
+template <int R, int RZ, int TY>
 struct Cfg {
     // x apron rounded up to 4 floats: the TMA box must start on a 16-byte
     // boundary in x (x0 - RA), and every shared-memory read is then a float4.
@@ -65,16 +66,19 @@ struct Cfg {
     static_assert(PW <= 256 && PH <= 256, "TMA box limit");
 };
 
+// All arrays share one geometry: nz planes x (nyl + 2R) rows x nxp floats with
+// strides ys (row) and zs (plane) in floats; R halo rows on both y sides (only
+// p's are ever non-zero). Tensor-map dims are ordered (x, y, z).
 struct StepParams {
-    CUtensorMap tm_p;    // p^n  : dims {nx, nz, nyl + 2R} (y-halo rows), box {TX + 2RA, 1, TY + 2R}
-    CUtensorMap tm_q;    // q^n  : dims {nx, nz, nyl}, box {TX, 1, TY}
-    CUtensorMap tm_pm;   // p^{n-1}: interior rows of the other p buffer
+    CUtensorMap tm_p;    // p^n  : halo'd view dims {nx, nyl + 2R, nz}, box {TX + 2RA, TY + 2R, 1}
+    CUtensorMap tm_q;    // q^n  : interior view dims {nx, nyl, nz}, box {TX, TY, 1}
+    CUtensorMap tm_pm;   // p^{n-1}: interior view of the other p buffer
     CUtensorMap tm_qm;   // q^{n-1}
     CUtensorMap tm_vx;   // vx2
     CUtensorMap tm_vn;   // vn2
     CUtensorMap tm_vz;   // vz2
-    float *p_out;        // p^{n+1}: interior row 0 of the other p buffer
-    float *q_out;        // q^{n+1}
+    float *p_out;        // p^{n+1}: interior row 0, plane 0 of the other p buffer
+    float *q_out;        // q^{n+1}: interior row 0, plane 0 of the other q buffer
     const float *zrow;   // [nz][ZROW]: w^z[k][0..2Rz], gz[k], 0 ...
     const float *gx;     // [ntx * TX] (1 beyond nx)
     const float *gy;     // [nyl] local rows
@@ -82,7 +86,8 @@ struct StepParams {
     float dt2;
     float s;             // s(t^n) this step
     int src_i, src_j, src_k, src_mask;   // local indices; src_mask = 0: no source here
-    int nx, nyl, nz, nxp;
+    int nx, nyl, nz;
+    long long ys, zs;                    // row / plane strides (floats)
     int ntx;                             // tiles along x
     int ty_begin, ty_step, nty;          // tile rows ty_begin + t * ty_step, t < nty
     int zchunk, nzc;                     // planes per chunk, chunks
@@ -156,6 +161,7 @@ __device__ __forceinline__ float f4(const float4 &v, int c)
     return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
+template <int TY>
 __device__ __forceinline__ void decode_item(const StepParams &P, int item, int &x0, int &y0, int &kb, int &ke)
 {
     const int tx = item % P.ntx;
@@ -169,10 +175,11 @@ __device__ __forceinline__ void decode_item(const StepParams &P, int item, int &
 }
 
 // ---------------------------------------------------------------- the kernel
-template <int R, int RZ, int STAGES, int MINB>
-__global__ void __launch_bounds__(NTHREADS, MINB) vti_step_kernel(const __grid_constant__ StepParams P)
+template <int R, int RZ, int TY, int STAGES, int MINB>
+__global__ void __launch_bounds__(nthreads(TY), MINB) vti_step_kernel(const __grid_constant__ StepParams P)
 {
-    using C = Cfg<R, RZ>;
+    using C = Cfg<R, RZ, TY>;
+    constexpr int NCONS_WARPS = cons_warps(TY);
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(NTHREADS, MINB) vti_step_kernel(const __grid_c
             uint32_t phase = 0;
             for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
                 int x0, y0, kb, ke;
-                decode_item(P, item, x0, y0, kb, ke);
+                decode_item<TY>(P, item, x0, y0, kb, ke);
                 const int nload = (ke - kb) + 2 * RZ;
                 for (int t = 0; t < nload; ++t) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -215,19 +222,19 @@ __global__ void __launch_bounds__(NTHREADS, MINB) vti_step_kernel(const __grid_c
                     if (t < 2 * RZ) {
                         // priming: q^n planes kb-Rz .. kb+Rz-1 (OOB planes -> 0)
                         mbar_arrive_expect_tx(bar, C::PRIME_TX);
-                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, kb - RZ + t, y0, bar);
+                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, y0, kb - RZ + t, bar);
                     } else {
                         const int k = kb + t - 2 * RZ;
                         mbar_arrive_expect_tx(bar, C::FULL_TX);
                         // p^n plane with R-point apron; y coordinate is the halo'd row
                         // index, whose row y0 is local row y0 - R.
-                        tma_load_3d(st + C::OFF_P, &P.tm_p, x0 - RA, k, y0, bar);
-                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, k + RZ, y0, bar);
-                        tma_load_3d(st + C::OFF_PM, &P.tm_pm, x0, k, y0, bar);
-                        tma_load_3d(st + C::OFF_QM, &P.tm_qm, x0, k, y0, bar);
-                        tma_load_3d(st + C::OFF_VX, &P.tm_vx, x0, k, y0, bar);
-                        tma_load_3d(st + C::OFF_VN, &P.tm_vn, x0, k, y0, bar);
-                        tma_load_3d(st + C::OFF_VZ, &P.tm_vz, x0, k, y0, bar);
+                        tma_load_3d(st + C::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
+                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, y0, k + RZ, bar);
+                        tma_load_3d(st + C::OFF_PM, &P.tm_pm, x0, y0, k, bar);
+                        tma_load_3d(st + C::OFF_QM, &P.tm_qm, x0, y0, k, bar);
+                        tma_load_3d(st + C::OFF_VX, &P.tm_vx, x0, y0, k, bar);
+                        tma_load_3d(st + C::OFF_VN, &P.tm_vn, x0, y0, k, bar);
+                        tma_load_3d(st + C::OFF_VZ, &P.tm_vz, x0, y0, k, bar);
                         bulk_load(st + C::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * 4, bar);
                     }
                     if (++stage == STAGES) {
@@ -240,16 +247,15 @@ __global__ void __launch_bounds__(NTHREADS, MINB) vti_step_kernel(const __grid_c
         return;
     }
 
-    // ======================= consumers: 16 x 16 threads, 4 x-points each =======================
+    // ======================= consumers: 16 x TY threads, 4 x-points each =======================
     const int tx = threadIdx.x & 15;
     const int ty = threadIdx.x >> 4;
     int stage = 0;
     uint32_t phase = 0;
-    const size_t row_stride = (size_t)P.nz * P.nxp;   // floats between y rows
 
     for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
         int x0, y0, kb, ke;
-        decode_item(P, item, x0, y0, kb, ke);
+        decode_item<TY>(P, item, x0, y0, kb, ke);
         const int xg = x0 + 4 * tx;      // first of this thread's 4 columns
         const int yl = y0 + ty;          // local row
         const bool store_ok = (yl < P.nyl) && (xg < P.nx);
@@ -264,8 +270,8 @@ __global__ void __launch_bounds__(NTHREADS, MINB) vti_step_kernel(const __grid_c
         }
         const bool src_col = P.src_mask != 0 && P.src_j == yl && P.src_i >= xg && P.src_i < xg + 4;
         const int src_c = P.src_i - xg;
-        float *pout = P.p_out + (size_t)yl * row_stride + xg;
-        float *qout = P.q_out + (size_t)yl * row_stride + xg;
+        float *pout = P.p_out + (long long)yl * P.ys + xg;
+        float *qout = P.q_out + (long long)yl * P.ys + xg;
         const int sidx = ty * TX + 4 * tx;   // this thread's float offset in a stream tile
 
         float4 q[NQ];
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(NTHREADS, MINB) vti_step_kernel(const __grid_c
                         qn[c] = g * __fmaf_rn(P.dt2, Fq, __fmaf_rn(-g, f4(qm4, c), 2.0f * f4(q[(u + RZ) % NQ], c)));
                     }
                     if (store_ok) {
-                        const size_t off = (size_t)k * P.nxp;
+                        const long long off = (long long)k * P.zs;
                         *reinterpret_cast<float4 *>(pout + off) = make_float4(pn[0], pn[1], pn[2], pn[3]);
                         *reinterpret_cast<float4 *>(qout + off) = make_float4(qn[0], qn[1], qn[2], qn[3]);
                     }

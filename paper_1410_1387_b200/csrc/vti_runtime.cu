@@ -1,12 +1,14 @@
 // vti_runtime.cu -- host runtime behind include/vti.h (B200 / sm_100a).
 //
-// Owns device buffers in the internal layout [y][z][x] (x padded to a
-// multiple of 32 floats, p with R_xy halo rows on both y sides so the
-// multi-GPU halo rows are contiguous), builds the TMA tensor maps, the
-// per-plane w^z + gz table and the 1-D Cerjan profiles, evaluates the Ricker
-// sample per step on the host, and launches the step kernel(s). With
-// nranks > 1 it exchanges p's R_xy boundary rows after each step, over NCCL
-// (one process per GPU) or with device-to-device copies (local group).
+// Owns the device arrays (all seven share one geometry: nz planes x
+// (ny_local + 2R) rows x nx_pad floats, internal layout [z][y][x] by default,
+// R_xy halo rows on both y sides of which only p's are ever non-zero), builds
+// the TMA tensor maps, the per-plane w^z + gz table and the 1-D Cerjan
+// profiles, evaluates the Ricker sample per step on the host, and launches the
+// step kernel(s). With nranks > 1 it packs p's R_xy boundary rows after the
+// edge tiles, exchanges them over NCCL (one process per GPU) or with
+// device-to-device copies (local group), and unpacks them into the halo rows
+// while the interior tiles run.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -103,34 +105,39 @@ static PFN_encodeTiled get_encode()
 
 // ============================================================ kernel table
 struct KernelEntry {
-    int r, rz, stages, minb, stage_bytes;
+    int r, rz, ty, stages, minb, stage_bytes;
     void (*fn)(StepParams);
     int zrow;
+    int threads;
 };
 
-template <int R, int RZ, int S, int B>
+template <int R, int RZ, int TY, int S, int B>
 static KernelEntry entry()
 {
-    return KernelEntry{R, RZ, S, B, Cfg<R, RZ>::STAGE, vti_step_kernel<R, RZ, S, B>, Cfg<R, RZ>::ZROW};
+    return KernelEntry{R, RZ, TY, S, B, Cfg<R, RZ, TY>::STAGE, vti_step_kernel<R, RZ, TY, S, B>,
+                       Cfg<R, RZ, TY>::ZROW, nthreads(TY)};
 }
 
-static const KernelEntry *find_kernel(int r, int rz)
+// Compiled variants. ty = 0 picks the default tile height for the pair.
+static const KernelEntry *find_kernel(int r, int rz, int ty)
 {
     static const KernelEntry table[] = {
-        entry<4, 4, 3, 2>(),
-        entry<8, 4, 3, 2>(),
-        entry<6, 6, 3, 2>(),
-        entry<12, 8, 2, 2>(),
+        entry<4, 4, 32, 3, 1>(), entry<4, 4, 16, 3, 2>(),
+        entry<8, 4, 32, 3, 1>(), entry<8, 4, 16, 3, 2>(),
+        entry<6, 6, 32, 3, 1>(), entry<6, 6, 16, 3, 2>(),
+        entry<12, 8, 32, 2, 1>(), entry<12, 8, 16, 2, 2>(),
     };
     for (const auto &e : table)
-        if (e.r == r && e.rz == rz) return &e;
+        if (e.r == r && e.rz == rz && (ty == 0 || e.ty == ty)) return &e;
     return nullptr;
 }
 
 // ============================================================ aux kernels
-// user [nk][nyl][nx] -> internal rows [y][z][x] (base = interior row 0), planes k0..
+// Internal element (x, y, k) of an interior view lives at base[y * ys + k * zs + x].
+
+// user [nk][nyl][nx] (or zero when src == NULL) -> internal planes k0..k0+nk
 __global__ void k_user_to_internal(const float *__restrict__ src, float *__restrict__ dst, int nk, int nyl, int nx,
-                                   int nz, int nxp, int k0)
+                                   long long ys, long long zs, int k0)
 {
     const int64_t n = (int64_t)nk * nyl * nx;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
@@ -138,12 +145,12 @@ __global__ void k_user_to_internal(const float *__restrict__ src, float *__restr
         const int64_t r = t / nx;
         const int y = (int)(r % nyl);
         const int k = (int)(r / nyl);
-        dst[((int64_t)y * nz + (k0 + k)) * nxp + x] = src ? src[t] : 0.f;
+        dst[y * ys + (k0 + k) * zs + x] = src ? src[t] : 0.f;
     }
 }
 
 __global__ void k_internal_to_user(const float *__restrict__ src, float *__restrict__ dst, int nk, int nyl, int nx,
-                                   int nz, int nxp, int k0)
+                                   long long ys, long long zs, int k0)
 {
     const int64_t n = (int64_t)nk * nyl * nx;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
@@ -151,24 +158,23 @@ __global__ void k_internal_to_user(const float *__restrict__ src, float *__restr
         const int64_t r = t / nx;
         const int y = (int)(r % nyl);
         const int k = (int)(r / nyl);
-        dst[t] = src[((int64_t)y * nz + (k0 + k)) * nxp + x];
+        dst[t] = src[y * ys + (k0 + k) * zs + x];
     }
 }
 
-// counters: [0] vz2 <= 0 or non-finite, [1] vx2/vn2 non-finite, [2] vn2 > vx2 -- over internal rows,
-// planes k0..k0+nk, columns < nx
+// counters: [0] vz2 <= 0 or non-finite, [1] vx2/vn2 non-finite, [2] vn2 > vx2, over planes k0..k0+nk
 __global__ void k_check_model(const float *__restrict__ vx2, const float *__restrict__ vn2,
-                              const float *__restrict__ vz2, int nyl, int nz, int nxp, int nx, int k0, int nk,
-                              unsigned long long *counters)
+                              const float *__restrict__ vz2, int nyl, int nx, long long ys, long long zs, int k0,
+                              int nk, unsigned long long *counters)
 {
     unsigned long long bad = 0, nonfin = 0, aniso = 0;
     const int64_t n = (int64_t)nyl * nk * nx;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int x = (int)(t % nx);
         const int64_t r = t / nx;
-        const int k = (int)(r % nk);
-        const int y = (int)(r / nk);
-        const int64_t a = ((int64_t)y * nz + k0 + k) * nxp + x;
+        const int y = (int)(r % nyl);
+        const int k = (int)(r / nyl);
+        const int64_t a = y * ys + (k0 + k) * zs + x;
         const float vx = vx2[a], vn = vn2[a], vz = vz2[a];
         bad += !(vz > 0.f) || !isfinite(vz);
         nonfin += !isfinite(vx) || !isfinite(vn);
@@ -179,26 +185,59 @@ __global__ void k_check_model(const float *__restrict__ vx2, const float *__rest
     if (aniso) atomicAdd(&counters[2], aniso);
 }
 
-// non-finite test of u^n (p, q) over internal interior rows, columns < nx
-__global__ void k_check_finite(const float *__restrict__ p, const float *__restrict__ q, int nyl, int nz, int nxp,
-                               int nx, unsigned int *flag)
+// non-finite test of u^n (p, q) over the interior
+__global__ void k_check_finite(const float *__restrict__ p, const float *__restrict__ q, int nyl, int nz, int nx,
+                               long long ys, long long zs, unsigned int *flag)
 {
     bool bad = false;
     const int64_t n = (int64_t)nyl * nz * nx;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int x = (int)(t % nx);
-        const int64_t a = (t / nx) * nxp + x;
+        const int64_t r = t / nx;
+        const int y = (int)(r % nyl);
+        const int k = (int)(r / nyl);
+        const int64_t a = y * ys + k * zs + x;
         bad |= !isfinite(p[a]) || !isfinite(q[a]);
     }
     if (bad) atomicOr(flag, 1u);
+}
+
+// Halo transport of p: rows [row0, row0 + R) of a halo'd buffer (row index
+// counted from the first halo row) <-> a contiguous [nz][R][nx] buffer.
+__global__ void k_pack_rows(const float *__restrict__ buf, float *__restrict__ out, int row0, int R, int nz, int nx,
+                            long long ys, long long zs)
+{
+    const int64_t n = (int64_t)nz * R * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const int64_t r = t / nx;
+        const int y = (int)(r % R);
+        const int k = (int)(r / R);
+        out[t] = buf[(row0 + y) * ys + k * zs + x];
+    }
+}
+
+__global__ void k_unpack_rows(const float *__restrict__ in, float *__restrict__ buf, int row0, int R, int nz, int nx,
+                              long long ys, long long zs)
+{
+    const int64_t n = (int64_t)nz * R * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const int64_t r = t / nx;
+        const int y = (int)(r % R);
+        const int k = (int)(r / R);
+        buf[(row0 + y) * ys + k * zs + x] = in[t];
+    }
 }
 
 // ============================================================ handle
 struct vti_s {
     vti_config cfg{};
     std::string err;
-    int R = 0, RZ = 0;
-    int y0 = 0, nyl = 0, nxp = 0;
+    int R = 0, RZ = 0, TY = 16;
+    int y0 = 0, nyl = 0, nxp = 0, rows = 0;   // rows = nyl + 2R (halo'd)
+    long long ys = 0, zs = 0;                 // row / plane strides (floats)
+    bool layout_zyx = true;                   // [z][y][x] (default) or [y][z][x]
     int ntx = 0, nty = 0;
     const KernelEntry *K = nullptr;
     int smem_bytes = 0;
@@ -209,9 +248,11 @@ struct vti_s {
     bool own_stream = false;
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_edge = nullptr, ev_comm = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
-    float *pbuf[2] = {nullptr, nullptr};   // (nyl + 2R) rows each
-    float *qbuf[2] = {nullptr, nullptr};   // nyl rows
+    float *pbuf[2] = {nullptr, nullptr};   // halo'd arrays (base = first halo row)
+    float *qbuf[2] = {nullptr, nullptr};
     float *vx2 = nullptr, *vn2 = nullptr, *vz2 = nullptr;
+    float *sbuf[2] = {nullptr, nullptr};   // packed send rows: [0] to rank-1, [1] to rank+1
+    float *rbuf[2] = {nullptr, nullptr};   // packed recv rows: [0] from rank-1, [1] from rank+1
     float *zrow = nullptr, *gx = nullptr, *gy = nullptr;
     float *staging = nullptr;
     size_t staging_floats = 0;
@@ -233,8 +274,10 @@ struct vti_s {
     bool group_mode = false;
     bool halo_dirty = false;
 
-    size_t row_floats() const { return (size_t)cfg.nz * nxp; }
-    float *p_int(int b) const { return pbuf[b] + (size_t)R * row_floats(); }
+    size_t total_floats() const { return (size_t)cfg.nz * rows * nxp; }
+    float *in(float *base) const { return base + (long long)R * ys; }   // interior view
+    float *p_int(int b) const { return in(pbuf[b]); }
+    float *q_int(int b) const { return in(qbuf[b]); }
 };
 
 static std::mutex g_err_mu;
@@ -290,21 +333,29 @@ static bool is_device_ptr(const void *p)
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-static vti_status encode(vti_s *h, CUtensorMap *tm, float *base, int rows, int bx, int by)
+// 3-D tensor map over (x, y, z) of an array with this handle's strides.
+static vti_status encode(vti_s *h, CUtensorMap *tm, float *base, int rows, int bx, int by,
+                         CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B)
 {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-    cuuint64_t dims[3] = {(cuuint64_t)h->cfg.nx, (cuuint64_t)h->cfg.nz, (cuuint64_t)rows};
-    cuuint64_t strides[2] = {(cuuint64_t)h->nxp * 4, (cuuint64_t)h->row_floats() * 4};
-    cuuint32_t box[3] = {(cuuint32_t)bx, 1u, (cuuint32_t)by};
+    cuuint64_t dims[3] = {(cuuint64_t)h->cfg.nx, (cuuint64_t)rows, (cuuint64_t)h->cfg.nz};
+    cuuint64_t strides[2] = {(cuuint64_t)h->ys * 4, (cuuint64_t)h->zs * 4};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1u};
     cuuint32_t estr[3] = {1u, 1u, 1u};
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);   // NONE = zero fill: the paper's zero exterior
     if (r != CUDA_SUCCESS) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return VTI_OK;
 }
 
+// Work items are (tile, z-chunk). Measured on B200 (profiles/):
+// full z columns marching in lockstep keep the p apron re-reads in L2 and
+// avoid the 2Rz-plane q priming of every chunk, and beat finer chunking even
+// with some SMs idle (C2: 128 columns on 148 SMs > 1024 chunks). So: one chunk
+// per column unless there are fewer than half as many tiles as CTA slots; then
+// split z just enough to give every slot an item.
 static void choose_schedule(vti_s *h)
 {
     const int slots = h->sms * h->ctas_per_sm;
@@ -312,24 +363,11 @@ static void choose_schedule(vti_s *h)
     const int nz = h->cfg.nz;
     if (h->tune_zchunk > 0) {
         h->zchunk = std::min(h->tune_zchunk, nz);
+    } else if (2 * tiles >= slots) {
+        h->zchunk = nz;
     } else {
-        // maximise wave efficiency, penalising the 2Rz-plane q re-read of each extra chunk
-        double best = -1;
-        int best_zc = nz;
-        for (int nzc = 1; nzc <= std::max(1, nz / 16); ++nzc) {
-            const int zc = (nz + nzc - 1) / nzc;
-            const int nzc_eff = (nz + zc - 1) / zc;
-            const long items = (long)tiles * nzc_eff;
-            const long rounds = (items + slots - 1) / slots;
-            const double eff = (double)items / (double)(rounds * slots);
-            const double over = 1.0 + (2.0 * h->RZ * 4.0) / (36.0 * zc);
-            const double score = eff / over;
-            if (score > best + 1e-9) {
-                best = score;
-                best_zc = zc;
-            }
-        }
-        h->zchunk = best_zc;
+        const int nzc = std::min((slots + tiles - 1) / tiles, std::max(1, nz / (4 * h->RZ)));
+        h->zchunk = (nz + nzc - 1) / nzc;
     }
     h->nzc = (nz + h->zchunk - 1) / h->zchunk;
     const long items = (long)tiles * h->nzc;
@@ -349,6 +387,16 @@ static vti_status check_cfg(const vti_config *c)
     if (c->ny / c->nranks < c->r_xy) return VTI_E_GEOMETRY;   // slab thinner than the halo
     return VTI_OK;
 }
+
+// Device pointers handed in or out by the caller may have been produced or be
+// consumed on another stream: order the library's stream after all prior work.
+static vti_status order_after_caller(vti_s *h)
+{
+    CU(h, cudaDeviceSynchronize());
+    return VTI_OK;
+}
+
+static int launch_grid(const vti_s *h) { return 4 * h->sms; }
 
 // ============================================================ C ABI
 extern "C" {
@@ -405,6 +453,8 @@ vti_status vti_destroy(vti_t h)
     for (int b = 0; b < 2; ++b) {
         cudaFree(h->pbuf[b]);
         cudaFree(h->qbuf[b]);
+        cudaFree(h->sbuf[b]);
+        cudaFree(h->rbuf[b]);
     }
     cudaFree(h->vx2);
     cudaFree(h->vn2);
@@ -441,12 +491,26 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     h->cfg = *cfg;
     h->R = cfg->r_xy;
     h->RZ = cfg->r_z;
-    h->K = find_kernel(h->R, h->RZ);
+    int want_ty = 0;
+    if (const char *e = getenv("VTI_TY")) want_ty = atoi(e);
+    h->K = find_kernel(h->R, h->RZ, want_ty);
+    if (!h->K && want_ty) h->K = find_kernel(h->R, h->RZ, 0);
     if (!h->K) return fail(h, VTI_E_UNSUPPORTED, "(r_xy, r_z) = (%d, %d) not compiled", h->R, h->RZ);
+    h->TY = h->K->ty;
     vti_slab(cfg, &h->y0, &h->nyl);
     h->nxp = (cfg->nx + 31) / 32 * 32;
+    h->rows = h->nyl + 2 * h->R;
+    const char *lay = getenv("VTI_LAYOUT");
+    h->layout_zyx = !(lay && strcmp(lay, "yzx") == 0);
+    if (h->layout_zyx) {   // [z][y][x]: a tile plane is one contiguous run of rows
+        h->ys = h->nxp;
+        h->zs = (long long)h->rows * h->nxp;
+    } else {               // [y][z][x]
+        h->ys = (long long)cfg->nz * h->nxp;
+        h->zs = h->nxp;
+    }
     h->ntx = (cfg->nx + TX - 1) / TX;
-    h->nty = (h->nyl + TY - 1) / TY;
+    h->nty = (h->nyl + h->TY - 1) / h->TY;
     for (int l = 0; l <= h->R; ++l) {
         if (!std::isfinite(w_xy[l])) return fail(h, VTI_E_PARAM, "non-finite w_xy[%d]", l);
         h->cxy[l] = (float)((double)w_xy[l] / (cfg->h * cfg->h));   // reading c3
@@ -471,23 +535,29 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
 
     h->smem_bytes = h->K->stages * h->K->stage_bytes + 2 * h->K->stages * 8;
     CU(h, cudaFuncSetAttribute((const void *)h->K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
-    CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)h->K->fn, NTHREADS,
+    CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)h->K->fn, h->K->threads,
                                                         h->smem_bytes));
     if (h->ctas_per_sm < 1) return fail(h, VTI_E_CUDA, "step kernel cannot be resident (smem %d B)", h->smem_bytes);
     choose_schedule(h);
 
-    const size_t rowf = h->row_floats();
-    const size_t pfl = (size_t)(h->nyl + 2 * h->R) * rowf, qfl = (size_t)h->nyl * rowf;
+    const size_t bytes = h->total_floats() * 4;
     vti_status s;
     for (int b = 0; b < 2; ++b) {
-        if ((s = alloc(h, (void **)&h->pbuf[b], pfl * 4)) != VTI_OK) return s;
-        if ((s = alloc(h, (void **)&h->qbuf[b], qfl * 4)) != VTI_OK) return s;
+        if ((s = alloc(h, (void **)&h->pbuf[b], bytes)) != VTI_OK) return s;
+        if ((s = alloc(h, (void **)&h->qbuf[b], bytes)) != VTI_OK) return s;
     }
-    if ((s = alloc(h, (void **)&h->vx2, qfl * 4)) != VTI_OK) return s;
-    if ((s = alloc(h, (void **)&h->vn2, qfl * 4)) != VTI_OK) return s;
-    if ((s = alloc(h, (void **)&h->vz2, qfl * 4)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->vx2, bytes)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->vn2, bytes)) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->vz2, bytes)) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->counters, 4 * sizeof(unsigned long long))) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->flag, sizeof(unsigned int))) != VTI_OK) return s;
+    if (cfg->nranks > 1) {
+        const size_t hb = (size_t)cfg->nz * h->R * cfg->nx * 4;
+        for (int b = 0; b < 2; ++b) {
+            if ((s = alloc(h, (void **)&h->sbuf[b], hb)) != VTI_OK) return s;
+            if ((s = alloc(h, (void **)&h->rbuf[b], hb)) != VTI_OK) return s;
+        }
+    }
 
     // per-plane z rows: w^z[k][0..2Rz], gz[k], zero pad (host double -> float once)
     const int NQ = 2 * h->RZ + 1, ZR = h->K->zrow;
@@ -511,15 +581,22 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     CU(h, cudaMemcpyAsync(h->gy, gyv.data(), gyv.size() * 4, cudaMemcpyHostToDevice, h->stream));
 
     const int RA = (h->R + 3) / 4 * 4;   // 16-byte aligned x apron (see Cfg::RA)
-    const int PW = TX + 2 * RA, PH = TY + 2 * h->R;
-    for (int b = 0; b < 2; ++b) {
-        if ((s = encode(h, &h->tm_ph[b], h->pbuf[b], h->nyl + 2 * h->R, PW, PH)) != VTI_OK) return s;
-        if ((s = encode(h, &h->tm_pi[b], h->p_int(b), h->nyl, TX, TY)) != VTI_OK) return s;
-        if ((s = encode(h, &h->tm_q[b], h->qbuf[b], h->nyl, TX, TY)) != VTI_OK) return s;
+    const int PW = TX + 2 * RA, PH = h->TY + 2 * h->R;
+    // L2 promotion of the halo'd p box (its x apron is not 256-B aligned): env VTI_P_PROMO=none|64|128|256
+    CUtensorMapL2promotion ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    if (const char *e = getenv("VTI_P_PROMO")) {
+        if (!strcmp(e, "none")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+        else if (!strcmp(e, "64")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        else if (!strcmp(e, "128")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     }
-    if ((s = encode(h, &h->tm_vx, h->vx2, h->nyl, TX, TY)) != VTI_OK) return s;
-    if ((s = encode(h, &h->tm_vn, h->vn2, h->nyl, TX, TY)) != VTI_OK) return s;
-    if ((s = encode(h, &h->tm_vz, h->vz2, h->nyl, TX, TY)) != VTI_OK) return s;
+    for (int b = 0; b < 2; ++b) {
+        if ((s = encode(h, &h->tm_ph[b], h->pbuf[b], h->rows, PW, PH, ppromo)) != VTI_OK) return s;
+        if ((s = encode(h, &h->tm_pi[b], h->p_int(b), h->nyl, TX, h->TY)) != VTI_OK) return s;
+        if ((s = encode(h, &h->tm_q[b], h->q_int(b), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    }
+    if ((s = encode(h, &h->tm_vx, h->in(h->vx2), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    if ((s = encode(h, &h->tm_vn, h->in(h->vn2), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    if ((s = encode(h, &h->tm_vz, h->in(h->vz2), h->nyl, TX, h->TY)) != VTI_OK) return s;
 
     if (cfg->nranks > 1) {
         if (cfg->nccl_id) {
@@ -562,66 +639,58 @@ const char *vti_last_error(vti_t h)
     return g_create_err.c_str();
 }
 
-// Copy planes [k0, k0+nk) of a user-layout array (host or device) into internal rows.
-static vti_status upload_planes(vti_s *h, float *dst_rows, const float *src, int k0, int nk)
+static vti_status ensure_staging(vti_s *h, size_t want)
+{
+    if (h->staging_floats >= want) return VTI_OK;
+    cudaFree(h->staging);
+    h->staging = nullptr;
+    h->staging_floats = 0;
+    CU(h, cudaMalloc(&h->staging, want * 4));
+    h->staging_floats = want;
+    return VTI_OK;
+}
+
+// Planes [k0, k0+nk) of a user-layout array (host, device, or NULL = zero) -> interior view dst.
+static vti_status upload_planes(vti_s *h, float *dst, const float *src, int k0, int nk)
 {
     const int nx = h->cfg.nx, nyl = h->nyl;
     const size_t plane = (size_t)nyl * nx;
-    if (!src) {
-        k_user_to_internal<<<4 * h->sms, 256, 0, h->stream>>>(nullptr, dst_rows, nk, nyl, nx, h->cfg.nz, h->nxp, k0);
-        CU(h, cudaGetLastError());
-        return VTI_OK;
-    }
-    if (is_device_ptr(src)) {
-        k_user_to_internal<<<4 * h->sms, 256, 0, h->stream>>>(src, dst_rows, nk, nyl, nx, h->cfg.nz, h->nxp, k0);
+    if (!src || is_device_ptr(src)) {
+        k_user_to_internal<<<launch_grid(h), 256, 0, h->stream>>>(src, dst, nk, nyl, nx, h->ys, h->zs, k0);
         CU(h, cudaGetLastError());
         return VTI_OK;
     }
     // host source: bounce through a device staging buffer in chunks of planes
-    const size_t want = std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20));
-    if (h->staging_floats < want) {
-        cudaFree(h->staging);
-        h->staging = nullptr;
-        h->staging_floats = 0;
-        CU(h, cudaMalloc(&h->staging, want * 4));
-        h->staging_floats = want;
-    }
+    vti_status s = ensure_staging(h, std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20)));
+    if (s != VTI_OK) return s;
     const int chunk = (int)std::max<size_t>(1, h->staging_floats / plane);
     for (int k = 0; k < nk; k += chunk) {
         const int m = std::min(chunk, nk - k);
         CU(h, cudaMemcpyAsync(h->staging, src + (size_t)k * plane, (size_t)m * plane * 4, cudaMemcpyHostToDevice,
                               h->stream));
-        k_user_to_internal<<<4 * h->sms, 256, 0, h->stream>>>(h->staging, dst_rows, m, nyl, nx, h->cfg.nz, h->nxp,
-                                                               k0 + k);
+        k_user_to_internal<<<launch_grid(h), 256, 0, h->stream>>>(h->staging, dst, m, nyl, nx, h->ys, h->zs, k0 + k);
         CU(h, cudaGetLastError());
     }
     CU(h, cudaStreamSynchronize(h->stream));   // staging is reused; host buffer may be freed after return
     return VTI_OK;
 }
 
-static vti_status download_planes(vti_s *h, float *dst, const float *src_rows, int k0, int nk)
+static vti_status download_planes(vti_s *h, float *dst, const float *src, int k0, int nk)
 {
     const int nx = h->cfg.nx, nyl = h->nyl;
     const size_t plane = (size_t)nyl * nx;
     if (is_device_ptr(dst)) {
-        k_internal_to_user<<<4 * h->sms, 256, 0, h->stream>>>(src_rows, dst, nk, nyl, nx, h->cfg.nz, h->nxp, k0);
+        k_internal_to_user<<<launch_grid(h), 256, 0, h->stream>>>(src, dst, nk, nyl, nx, h->ys, h->zs, k0);
         CU(h, cudaGetLastError());
         CU(h, cudaStreamSynchronize(h->stream));
         return VTI_OK;
     }
-    const size_t want = std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20));
-    if (h->staging_floats < want) {
-        cudaFree(h->staging);
-        h->staging = nullptr;
-        h->staging_floats = 0;
-        CU(h, cudaMalloc(&h->staging, want * 4));
-        h->staging_floats = want;
-    }
+    vti_status s = ensure_staging(h, std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20)));
+    if (s != VTI_OK) return s;
     const int chunk = (int)std::max<size_t>(1, h->staging_floats / plane);
     for (int k = 0; k < nk; k += chunk) {
         const int m = std::min(chunk, nk - k);
-        k_internal_to_user<<<4 * h->sms, 256, 0, h->stream>>>(src_rows, h->staging, m, nyl, nx, h->cfg.nz, h->nxp,
-                                                               k0 + k);
+        k_internal_to_user<<<launch_grid(h), 256, 0, h->stream>>>(src, h->staging, m, nyl, nx, h->ys, h->zs, k0 + k);
         CU(h, cudaGetLastError());
         CU(h, cudaMemcpyAsync(dst + (size_t)k * plane, h->staging, (size_t)m * plane * 4, cudaMemcpyDeviceToHost,
                               h->stream));
@@ -630,21 +699,30 @@ static vti_status download_planes(vti_s *h, float *dst, const float *src_rows, i
     return VTI_OK;
 }
 
+static bool any_device(std::initializer_list<const void *> ps)
+{
+    for (const void *p : ps)
+        if (is_device_ptr(p)) return true;
+    return false;
+}
+
 vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx2, const float *vn2,
                                 const float *vz2)
 {
     if (!h) return VTI_E_PARAM;
     if (!vx2 || !vn2 || !vz2) return fail(h, VTI_E_PARAM, "NULL model array");
-    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz) return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
+        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
     CU(h, cudaSetDevice(h->cfg.device));
     vti_status s;
-    if ((s = upload_planes(h, h->vx2, vx2, k0, nk)) != VTI_OK) return s;
-    if ((s = upload_planes(h, h->vn2, vn2, k0, nk)) != VTI_OK) return s;
-    if ((s = upload_planes(h, h->vz2, vz2, k0, nk)) != VTI_OK) return s;
+    if (any_device({vx2, vn2, vz2}) && (s = order_after_caller(h)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->in(h->vx2), vx2, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->in(h->vn2), vn2, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->in(h->vz2), vz2, k0, nk)) != VTI_OK) return s;
     // validate on the device: vz2 > 0 and finite, vx2/vn2 finite, count vn2 > vx2 (reading c5)
     CU(h, cudaMemsetAsync(h->counters, 0, 4 * sizeof(unsigned long long), h->stream));
-    k_check_model<<<4 * h->sms, 256, 0, h->stream>>>(h->vx2, h->vn2, h->vz2, h->nyl, h->cfg.nz, h->nxp, h->cfg.nx,
-                                                     k0, nk, h->counters);
+    k_check_model<<<launch_grid(h), 256, 0, h->stream>>>(h->in(h->vx2), h->in(h->vn2), h->in(h->vz2), h->nyl,
+                                                          h->cfg.nx, h->ys, h->zs, k0, nk, h->counters);
     CU(h, cudaGetLastError());
     unsigned long long cnt[3];
     CU(h, cudaMemcpyAsync(cnt, h->counters, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
@@ -672,7 +750,7 @@ static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int 
     P.tm_vn = h->tm_vn;
     P.tm_vz = h->tm_vz;
     P.p_out = h->p_int(o);
-    P.q_out = h->qbuf[o];
+    P.q_out = h->q_int(o);
     P.zrow = h->zrow;
     P.gx = h->gx;
     P.gy = h->gy;
@@ -688,7 +766,8 @@ static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int 
     P.nx = h->cfg.nx;
     P.nyl = h->nyl;
     P.nz = h->cfg.nz;
-    P.nxp = h->nxp;
+    P.ys = h->ys;
+    P.zs = h->zs;
     P.ntx = h->ntx;
     P.ty_begin = ty_begin;
     P.ty_step = ty_step;
@@ -705,18 +784,43 @@ static vti_status launch_rows(vti_s *h, int ty_begin, int ty_step, int nty_sel)
     fill_params(h, P, ty_begin, ty_step, nty_sel);
     const int grid = std::min(P.items, h->sms * h->ctas_per_sm);
     void *args[] = {&P};
-    CU(h, cudaLaunchKernel((const void *)h->K->fn, dim3(grid), dim3(NTHREADS), args, h->smem_bytes, h->stream));
+    CU(h, cudaLaunchKernel((const void *)h->K->fn, dim3(grid), dim3(h->K->threads), args, h->smem_bytes, h->stream));
     return VTI_OK;
 }
 
-// p rows exchanged with the neighbours: buffer b, R rows each way (contiguous in [y][z][x])
-static size_t halo_floats(const vti_s *h) { return (size_t)h->R * h->row_floats(); }
-static float *send_lo(const vti_s *h, int b) { return h->pbuf[b] + (size_t)h->R * h->row_floats(); }
-static float *send_hi(const vti_s *h, int b) { return h->pbuf[b] + (size_t)h->nyl * h->row_floats(); }
-static float *recv_lo(const vti_s *h, int b) { return h->pbuf[b]; }
-static float *recv_hi(const vti_s *h, int b) { return h->pbuf[b] + (size_t)(h->nyl + h->R) * h->row_floats(); }
+// ---- halo transport of p (y-slab decomposition)
+// Halo'd row index: [0, R) rows from rank-1, [R, R+nyl) own rows, [R+nyl, 2R+nyl) rows from rank+1.
+static size_t halo_floats(const vti_s *h) { return (size_t)h->cfg.nz * h->R * h->cfg.nx; }
 
-// NCCL halo exchange of buffer b on the comm stream after ev_edge; records ev_comm.
+// On the main stream: pack this rank's boundary rows of buffer b into sbuf[0] (-> rank-1) and sbuf[1] (-> rank+1).
+static vti_status pack_send(vti_s *h, int b)
+{
+    const int r = h->cfg.rank, nr = h->cfg.nranks;
+    if (r > 0)
+        k_pack_rows<<<launch_grid(h), 256, 0, h->stream>>>(h->pbuf[b], h->sbuf[0], h->R, h->R, h->cfg.nz, h->cfg.nx,
+                                                          h->ys, h->zs);
+    if (r < nr - 1)
+        k_pack_rows<<<launch_grid(h), 256, 0, h->stream>>>(h->pbuf[b], h->sbuf[1], h->nyl, h->R, h->cfg.nz,
+                                                          h->cfg.nx, h->ys, h->zs);
+    CU(h, cudaGetLastError());
+    return VTI_OK;
+}
+
+// On the comm stream: unpack rbuf[0] (from rank-1) and rbuf[1] (from rank+1) into the halo rows of buffer b.
+static vti_status unpack_recv(vti_s *h, int b)
+{
+    const int r = h->cfg.rank, nr = h->cfg.nranks;
+    if (r > 0)
+        k_unpack_rows<<<launch_grid(h), 256, 0, h->comm>>>(h->rbuf[0], h->pbuf[b], 0, h->R, h->cfg.nz, h->cfg.nx,
+                                                          h->ys, h->zs);
+    if (r < nr - 1)
+        k_unpack_rows<<<launch_grid(h), 256, 0, h->comm>>>(h->rbuf[1], h->pbuf[b], h->nyl + h->R, h->R, h->cfg.nz,
+                                                          h->cfg.nx, h->ys, h->zs);
+    CU(h, cudaGetLastError());
+    return VTI_OK;
+}
+
+// NCCL transport on the comm stream after ev_edge, then unpack; records ev_comm.
 static vti_status exchange_nccl(vti_s *h, int b)
 {
     NcclApi &api = nccl();
@@ -725,16 +829,18 @@ static vti_status exchange_nccl(vti_s *h, int b)
     const int r = h->cfg.rank, nr = h->cfg.nranks;
     ncclResult_t e = api.GroupStart();
     if (e == ncclSuccess && r > 0) {
-        e = api.Send(send_lo(h, b), cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
-        if (e == ncclSuccess) e = api.Recv(recv_lo(h, b), cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
+        e = api.Send(h->sbuf[0], cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
+        if (e == ncclSuccess) e = api.Recv(h->rbuf[0], cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
     }
     if (e == ncclSuccess && r < nr - 1) {
-        e = api.Send(send_hi(h, b), cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
-        if (e == ncclSuccess) e = api.Recv(recv_hi(h, b), cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
+        e = api.Send(h->sbuf[1], cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
+        if (e == ncclSuccess) e = api.Recv(h->rbuf[1], cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
     }
     ncclResult_t e2 = api.GroupEnd();
     if (e != ncclSuccess || e2 != ncclSuccess)
         return fail(h, VTI_E_COMM, "NCCL halo exchange: %s", api.GetErrorString(e != ncclSuccess ? e : e2));
+    vti_status s = unpack_recv(h, b);
+    if (s != VTI_OK) return s;
     CU(h, cudaEventRecord(h->ev_comm, h->comm));
     return VTI_OK;
 }
@@ -742,8 +848,8 @@ static vti_status exchange_nccl(vti_s *h, int b)
 static vti_status check_finite(vti_s *h)
 {
     CU(h, cudaMemsetAsync(h->flag, 0, sizeof(unsigned int), h->stream));
-    k_check_finite<<<4 * h->sms, 256, 0, h->stream>>>(h->p_int(h->cur), h->qbuf[h->cur], h->nyl, h->cfg.nz, h->nxp,
-                                                      h->cfg.nx, h->flag);
+    k_check_finite<<<launch_grid(h), 256, 0, h->stream>>>(h->p_int(h->cur), h->q_int(h->cur), h->nyl, h->cfg.nz,
+                                                           h->cfg.nx, h->ys, h->zs, h->flag);
     CU(h, cudaGetLastError());
     unsigned int f = 0;
     CU(h, cudaMemcpyAsync(&f, h->flag, sizeof f, cudaMemcpyDeviceToHost, h->stream));
@@ -768,7 +874,8 @@ vti_status vti_add_source(vti_t h, int32_t i, int32_t j, int32_t k, double f, do
 {
     if (!h) return VTI_E_PARAM;
     if (field_mask < 1 || field_mask > 3) return fail(h, VTI_E_PARAM, "field_mask must be 1, 2 or 3");
-    if (!std::isfinite(f) || !std::isfinite(t0) || !std::isfinite(amp)) return fail(h, VTI_E_PARAM, "non-finite source parameter");
+    if (!std::isfinite(f) || !std::isfinite(t0) || !std::isfinite(amp))
+        return fail(h, VTI_E_PARAM, "non-finite source parameter");
     if (i < 0 || i >= h->cfg.nx || j < 0 || j >= h->cfg.ny || k < 0 || k >= h->cfg.nz)
         return fail(h, VTI_E_INDEX, "source (%d,%d,%d) outside the %dx%dx%d grid", i, j, k, h->cfg.nx, h->cfg.ny,
                     h->cfg.nz);
@@ -788,15 +895,17 @@ vti_status vti_set_fields_planes(vti_t h, int32_t k0, int32_t nk, const float *p
 {
     if (!h) return VTI_E_PARAM;
     if (!p || !q) return fail(h, VTI_E_PARAM, "NULL p or q");
-    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz) return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
+        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaStreamSynchronize(h->comm));
-    const int c = h->cur, o = 1 - c;
     vti_status s;
+    if (any_device({p, q, pm, qm}) && (s = order_after_caller(h)) != VTI_OK) return s;
+    const int c = h->cur, o = 1 - c;
     if ((s = upload_planes(h, h->p_int(c), p, k0, nk)) != VTI_OK) return s;
-    if ((s = upload_planes(h, h->qbuf[c], q, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->q_int(c), q, k0, nk)) != VTI_OK) return s;
     if ((s = upload_planes(h, h->p_int(o), pm, k0, nk)) != VTI_OK) return s;
-    if ((s = upload_planes(h, h->qbuf[o], qm, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->q_int(o), qm, k0, nk)) != VTI_OK) return s;
     CU(h, cudaStreamSynchronize(h->stream));
     h->halo_dirty = h->cfg.nranks > 1;
     return VTI_OK;
@@ -811,15 +920,6 @@ vti_status vti_set_fields(vti_t h, const float *p, const float *q, const float *
     return s;
 }
 
-static vti_status step_single(vti_s *h)
-{
-    vti_status s = launch_rows(h, 0, 1, h->nty);
-    if (s != VTI_OK) return s;
-    h->cur = 1 - h->cur;
-    h->n += 1;
-    return VTI_OK;
-}
-
 vti_status vti_step(vti_t h, int32_t nsteps)
 {
     if (!h) return VTI_E_PARAM;
@@ -829,7 +929,8 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     CU(h, cudaSetDevice(h->cfg.device));
     const bool multi = h->cfg.nranks > 1;
     vti_status s;
-    if (multi && h->halo_dirty) {
+    if (multi && h->halo_dirty) {   // halos of a state set by the caller
+        if ((s = pack_send(h, h->cur)) != VTI_OK) return s;
         CU(h, cudaEventRecord(h->ev_edge, h->stream));
         if ((s = exchange_nccl(h, h->cur)) != VTI_OK) return s;
         CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
@@ -837,18 +938,19 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     }
     for (int it = 0; it < nsteps; ++it) {
         if (!multi) {
-            if ((s = step_single(h)) != VTI_OK) return s;
+            if ((s = launch_rows(h, 0, 1, h->nty)) != VTI_OK) return s;
         } else {
             const int o = 1 - h->cur;
             // edge tile rows first, so the rows the neighbours need are ready early
             if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty))) != VTI_OK) return s;
+            if ((s = pack_send(h, o)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
             if ((s = exchange_nccl(h, o)) != VTI_OK) return s;
             if ((s = launch_rows(h, 1, 1, h->nty - 2)) != VTI_OK) return s;   // interior rows overlap the exchange
             CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
-            h->cur = o;
-            h->n += 1;
         }
+        h->cur = 1 - h->cur;
+        h->n += 1;
         if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0)
             if ((s = check_finite(h)) != VTI_OK) return s;
     }
@@ -858,7 +960,8 @@ vti_status vti_step(vti_t h, int32_t nsteps)
 
 vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms)
 {
-    if (!h || !ms) return h ? fail(h, VTI_E_PARAM, "NULL ms") : VTI_E_PARAM;
+    if (!h) return VTI_E_PARAM;
+    if (!ms) return fail(h, VTI_E_PARAM, "NULL ms");
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaEventRecord(h->ev_t0, h->stream));
     vti_status s = vti_step(h, nsteps);
@@ -869,27 +972,26 @@ vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms)
     return VTI_OK;
 }
 
-// Local group: device-to-device halo copies between handles of one process.
-static vti_status group_exchange(vti_t *hs, int n, int b_of_all_cur)
+// Local group: the same pack / transport / unpack schedule, transport = peer copies of the packed rows.
+static vti_status group_exchange(vti_t *hs, int n, bool current)
 {
-    // every handle's ev_edge marks "rows to send are written"; copies run on the receiver's comm stream
     for (int i = 0; i < n; ++i) {
         vti_s *h = hs[i];
-        const int b = b_of_all_cur ? h->cur : 1 - h->cur;
+        const int b = current ? h->cur : 1 - h->cur;
         CU(h, cudaSetDevice(h->cfg.device));
         const size_t bytes = halo_floats(h) * 4;
-        if (i > 0) {
+        if (i > 0) {   // my rows from rank-1 = its packed rows for rank+1
             vti_s *g = hs[i - 1];
-            const int bg = b_of_all_cur ? g->cur : 1 - g->cur;
             CU(h, cudaStreamWaitEvent(h->comm, g->ev_edge, 0));
-            CU(h, cudaMemcpyPeerAsync(recv_lo(h, b), h->cfg.device, send_hi(g, bg), g->cfg.device, bytes, h->comm));
+            CU(h, cudaMemcpyPeerAsync(h->rbuf[0], h->cfg.device, g->sbuf[1], g->cfg.device, bytes, h->comm));
         }
         if (i < n - 1) {
             vti_s *g = hs[i + 1];
-            const int bg = b_of_all_cur ? g->cur : 1 - g->cur;
             CU(h, cudaStreamWaitEvent(h->comm, g->ev_edge, 0));
-            CU(h, cudaMemcpyPeerAsync(recv_hi(h, b), h->cfg.device, send_lo(g, bg), g->cfg.device, bytes, h->comm));
+            CU(h, cudaMemcpyPeerAsync(h->rbuf[1], h->cfg.device, g->sbuf[0], g->cfg.device, bytes, h->comm));
         }
+        vti_status s = unpack_recv(h, b);
+        if (s != VTI_OK) return s;
         CU(h, cudaEventRecord(h->ev_comm, h->comm));
     }
     return VTI_OK;
@@ -897,7 +999,7 @@ static vti_status group_exchange(vti_t *hs, int n, int b_of_all_cur)
 
 static vti_status group_wait(vti_t *hs, int n)
 {
-    // a handle's next writes may overwrite rows its neighbours copy from: wait for theirs too
+    // a handle's next pack overwrites rows its neighbours copy from: wait for their copies too
     for (int i = 0; i < n; ++i) {
         vti_s *h = hs[i];
         CU(h, cudaSetDevice(h->cfg.device));
@@ -926,9 +1028,10 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
     if (dirty) {
         for (int i = 0; i < n; ++i) {
             CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+            if ((s = pack_send(hs[i], hs[i]->cur)) != VTI_OK) return s;
             CU(hs[i], cudaEventRecord(hs[i]->ev_edge, hs[i]->stream));
         }
-        if ((s = group_exchange(hs, n, 1)) != VTI_OK) return s;
+        if ((s = group_exchange(hs, n, true)) != VTI_OK) return s;
         if ((s = group_wait(hs, n)) != VTI_OK) return s;
         for (int i = 0; i < n; ++i) hs[i]->halo_dirty = false;
     }
@@ -937,9 +1040,10 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
             if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty))) != VTI_OK) return s;
+            if ((s = pack_send(h, 1 - h->cur)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
         }
-        if ((s = group_exchange(hs, n, 0)) != VTI_OK) return s;
+        if ((s = group_exchange(hs, n, false)) != VTI_OK) return s;
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
@@ -958,13 +1062,15 @@ vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, floa
 {
     if (!h) return VTI_E_PARAM;
     if (level != 0 && level != 1) return fail(h, VTI_E_PARAM, "level must be 0 (u^n) or 1 (u^{n-1})");
-    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz) return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
+        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaStreamSynchronize(h->comm));
-    const int b = level == 0 ? h->cur : 1 - h->cur;
     vti_status s;
+    if (any_device({p, q}) && (s = order_after_caller(h)) != VTI_OK) return s;
+    const int b = level == 0 ? h->cur : 1 - h->cur;
     if (p && (s = download_planes(h, p, h->p_int(b), k0, nk)) != VTI_OK) return s;
-    if (q && (s = download_planes(h, q, h->qbuf[b], k0, nk)) != VTI_OK) return s;
+    if (q && (s = download_planes(h, q, h->q_int(b), k0, nk)) != VTI_OK) return s;
     return VTI_OK;
 }
 
@@ -994,8 +1100,9 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->y0 = h->y0;
     info->ny_local = h->nyl;
     info->nx_pad = h->nxp;
+    info->layout = h->layout_zyx ? 0 : 1;
     info->tile_x = TX;
-    info->tile_y = TY;
+    info->tile_y = h->TY;
     info->zchunk = h->zchunk;
     info->grid = std::min(h->ntx * h->nty * h->nzc, h->sms * h->ctas_per_sm);
     info->work_items = h->ntx * h->nty * h->nzc;
@@ -1012,7 +1119,8 @@ vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm)
     h->tune_zchunk = zchunk;
     if (ctas_per_sm > 0) {
         int maxb = 0;
-        CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, (const void *)h->K->fn, NTHREADS, h->smem_bytes));
+        CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, (const void *)h->K->fn, h->K->threads,
+                                                            h->smem_bytes));
         h->ctas_per_sm = std::min(ctas_per_sm, maxb);
     }
     choose_schedule(h);
