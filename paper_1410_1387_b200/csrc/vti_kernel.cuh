@@ -14,13 +14,16 @@
 // (x-y tile in shared memory + z register rolling), made
 // B200-native:
 //  * a persistent grid of CTAs pulls work items (64x16 x-y tile, z-chunk);
-//  * warp 8 is a TMA producer: per z plane it issues cp.async.bulk.tensor
-//    loads of the halo'd p^n plane tile, the q^n plane Rz ahead, p^{n-1},
-//    q^{n-1}, vx2, vn2, vz2 and a 1-D bulk copy of the plane's w^z row + gz,
-//    all completing on one mbarrier of an S-stage ring; out-of-bounds box
+//  * one elected lane (warp 0, lane 0) drives a STAGES-deep TMA ring: per z
+//    plane it issues cp.async.bulk.tensor loads of the halo'd p^n plane tile,
+//    the q^n plane Rz ahead, p^{n-1}, q^{n-1}, vx2, vn2, vz2 and a 1-D bulk
+//    copy of the plane's w^z row + gz, all completing on one mbarrier; load
+//    j + STAGES is issued as soon as every warp has released load j (empty
+//    mbarrier), so STAGES - 1 planes are always in flight. Out-of-bounds box
 //    elements are zero-filled by TMA, which IS the paper's zero exterior
-//    (l.89-90) in x, y and z;
-//  * warps 0-7 consume: each thread owns 4 consecutive x points (float4) of
+//    (l.89-90) in x, y and z. (No dedicated producer warp: 16 warps per CTA
+//    keep 4 warps per SM sub-partition, i.e. 128 registers per thread.)
+//  * all warps consume: each thread owns 4 consecutive x points (float4) of
 //    one row, keeps a (2Rz+1)-deep float4 register queue of q along z, reads
 //    the p cross from shared memory and writes p^{n+1}, q^{n+1} with 16-byte
 //    stores in place over p^{n-1}, q^{n-1}.
@@ -34,9 +37,10 @@ namespace vti {
 constexpr int TX = 64;               // tile width in x (points) = 16 threads x float4
 constexpr int MAX_R = 12;
 
-// Tile height TY (16 or 32 rows): 16 threads per row, TY/2 consumer warps + 1 producer warp.
-__host__ __device__ constexpr int cons_warps(int ty) { return ty / 2; }
-__host__ __device__ constexpr int nthreads(int ty) { return (ty / 2 + 1) * 32; }
+// Tile height TY (16 or 32 rows), RPT rows per thread (1 or 2): 16 threads per
+// row group, TY / (2 RPT) consumer warps, plus one producer warp when WP = 1.
+__host__ __device__ constexpr int cons_warps(int ty, int rpt) { return ty / (2 * rpt); }
+__host__ __device__ constexpr int nthreads(int ty, int rpt, int wp) { return (cons_warps(ty, rpt) + wp) * 32; }
 
 __host__ __device__ constexpr int align128(int b) { return (b + 127) / 128 * 128; }
 
@@ -174,14 +178,82 @@ __device__ __forceinline__ void decode_item(const StepParams &P, int item, int &
     ke = min(P.nz, kb + P.zchunk);
 }
 
+// The flat sequence of stage loads of one CTA: for each of its work items,
+// 2Rz priming loads (q only) then one full load per plane. Driven by a
+// single thread; load j goes to stage j % STAGES.
+template <int R, int RZ, int TY, int STAGES>
+struct Producer {
+    int item, t, nload, x0, y0, kb, ke;
+    int stage;
+    uint32_t phase;
+
+    __device__ __forceinline__ void start(const StepParams &P)
+    {
+        item = blockIdx.x;
+        t = 0;
+        stage = 0;
+        phase = 0;
+        if (item < P.items) {
+            decode_item<TY>(P, item, x0, y0, kb, ke);
+            nload = (ke - kb) + 2 * RZ;
+        }
+    }
+
+    __device__ __forceinline__ void issue(const StepParams &P, uint8_t *smem, uint64_t *full, uint64_t *empty)
+    {
+        using C = Cfg<R, RZ, TY>;
+        constexpr int RA = C::RA;
+        if (item >= P.items) return;
+        mbar_wait(&empty[stage], phase ^ 1);   // every warp released the previous load of this stage
+        uint8_t *st = smem + stage * C::STAGE;
+        uint64_t *bar = &full[stage];
+        if (t < 2 * RZ) {
+            // priming: q^n planes kb-Rz .. kb+Rz-1 (OOB planes -> 0)
+            mbar_arrive_expect_tx(bar, C::PRIME_TX);
+            tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, y0, kb - RZ + t, bar);
+        } else {
+            const int k = kb + t - 2 * RZ;
+            mbar_arrive_expect_tx(bar, C::FULL_TX);
+            // p^n plane with its apron; the y coordinate is the halo'd row index,
+            // whose row y0 is local row y0 - R.
+            tma_load_3d(st + C::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
+            tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, y0, k + RZ, bar);
+            tma_load_3d(st + C::OFF_PM, &P.tm_pm, x0, y0, k, bar);
+            tma_load_3d(st + C::OFF_QM, &P.tm_qm, x0, y0, k, bar);
+            tma_load_3d(st + C::OFF_VX, &P.tm_vx, x0, y0, k, bar);
+            tma_load_3d(st + C::OFF_VN, &P.tm_vn, x0, y0, k, bar);
+            tma_load_3d(st + C::OFF_VZ, &P.tm_vz, x0, y0, k, bar);
+            bulk_load(st + C::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * 4, bar);
+        }
+        if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+        }
+        if (++t == nload) {
+            item += gridDim.x;
+            t = 0;
+            if (item < P.items) {
+                decode_item<TY>(P, item, x0, y0, kb, ke);
+                nload = (ke - kb) + 2 * RZ;
+            }
+        }
+    }
+};
+
 // ---------------------------------------------------------------- the kernel
-template <int R, int RZ, int TY, int STAGES, int MINB>
-__global__ void __launch_bounds__(nthreads(TY), MINB) vti_step_kernel(const __grid_constant__ StepParams P)
+// WP = 1: a dedicated producer warp issues every load (consumers never stall
+//         on the ring); 17 warps per TY=32 CTA cap registers at 96.
+// WP = 0: the CTA's first thread issues load j + STAGES right after releasing
+//         load j; 16 warps allow 128 registers (needed for the R_z >= 6 queues).
+template <int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB>
+__global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(const __grid_constant__ StepParams P)
 {
     using C = Cfg<R, RZ, TY>;
-    constexpr int NCONS_WARPS = cons_warps(TY);
+    constexpr int NCONS_WARPS = cons_warps(TY, RPT);
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
+    constexpr int NW = 4 + 2 * RA;   // x window of one row (floats)
+    static_assert(TY % (2 * RPT) == 0, "tile rows must split into 16-thread row groups");
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE);
     uint64_t *empty = full + STAGES;
@@ -189,6 +261,8 @@ __global__ void __launch_bounds__(nthreads(TY), MINB) vti_step_kernel(const __gr
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
+    const bool leader = (WP == 0) && threadIdx.x == 0;
+    Producer<R, RZ, TY, STAGES> prod;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -196,93 +270,71 @@ __global__ void __launch_bounds__(nthreads(TY), MINB) vti_step_kernel(const __gr
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        prefetch_tmap(&P.tm_p);
+        prefetch_tmap(&P.tm_q);
+        prefetch_tmap(&P.tm_pm);
+        prefetch_tmap(&P.tm_qm);
+        prefetch_tmap(&P.tm_vx);
+        prefetch_tmap(&P.tm_vn);
+        prefetch_tmap(&P.tm_vz);
     }
     __syncthreads();
-
-    if (warp == NCONS_WARPS) {
-        // ======================= TMA producer (one elected lane) =======================
-        if (lane == 0) {
-            prefetch_tmap(&P.tm_p);
-            prefetch_tmap(&P.tm_q);
-            prefetch_tmap(&P.tm_pm);
-            prefetch_tmap(&P.tm_qm);
-            prefetch_tmap(&P.tm_vx);
-            prefetch_tmap(&P.tm_vn);
-            prefetch_tmap(&P.tm_vz);
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
-                int x0, y0, kb, ke;
-                decode_item<TY>(P, item, x0, y0, kb, ke);
-                const int nload = (ke - kb) + 2 * RZ;
-                for (int t = 0; t < nload; ++t) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t *st = smem + stage * C::STAGE;
-                    uint64_t *bar = &full[stage];
-                    if (t < 2 * RZ) {
-                        // priming: q^n planes kb-Rz .. kb+Rz-1 (OOB planes -> 0)
-                        mbar_arrive_expect_tx(bar, C::PRIME_TX);
-                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, y0, kb - RZ + t, bar);
-                    } else {
-                        const int k = kb + t - 2 * RZ;
-                        mbar_arrive_expect_tx(bar, C::FULL_TX);
-                        // p^n plane with R-point apron; y coordinate is the halo'd row
-                        // index, whose row y0 is local row y0 - R.
-                        tma_load_3d(st + C::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
-                        tma_load_3d(st + C::OFF_Q, &P.tm_q, x0, y0, k + RZ, bar);
-                        tma_load_3d(st + C::OFF_PM, &P.tm_pm, x0, y0, k, bar);
-                        tma_load_3d(st + C::OFF_QM, &P.tm_qm, x0, y0, k, bar);
-                        tma_load_3d(st + C::OFF_VX, &P.tm_vx, x0, y0, k, bar);
-                        tma_load_3d(st + C::OFF_VN, &P.tm_vn, x0, y0, k, bar);
-                        tma_load_3d(st + C::OFF_VZ, &P.tm_vz, x0, y0, k, bar);
-                        bulk_load(st + C::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * 4, bar);
-                    }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
+    if constexpr (WP == 1) {
+        if (warp == NCONS_WARPS) {   // dedicated producer warp: one lane walks the whole load sequence
+            if (lane == 0) {
+                prod.start(P);
+                while (prod.item < P.items) prod.issue(P, smem, full, empty);
             }
+            return;
         }
-        return;
+    } else {
+        if (leader) {
+            prod.start(P);
+            for (int s = 0; s < STAGES; ++s) prod.issue(P, smem, full, empty);   // fill the ring
+        }
     }
 
-    // ======================= consumers: 16 x TY threads, 4 x-points each =======================
+    // ======================= all warps consume: 16 x (TY / RPT) threads, 4 x RPT points each =======================
     const int tx = threadIdx.x & 15;
-    const int ty = threadIdx.x >> 4;
+    const int tg = threadIdx.x >> 4;   // row group: tile rows tg*RPT .. tg*RPT + RPT - 1
     int stage = 0;
     uint32_t phase = 0;
 
     for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
         int x0, y0, kb, ke;
         decode_item<TY>(P, item, x0, y0, kb, ke);
-        const int xg = x0 + 4 * tx;      // first of this thread's 4 columns
-        const int yl = y0 + ty;          // local row
-        const bool store_ok = (yl < P.nyl) && (xg < P.nx);
-        float gxy[4];
-        {
+        const int xg = x0 + 4 * tx;   // first of this thread's 4 columns
+        const float4 g4 = *reinterpret_cast<const float4 *>(P.gx + xg);
+        float gxy[RPT][4];
+        bool store_ok[RPT], src_col[RPT];
+        float *pout[RPT], *qout[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int yl = y0 + tg * RPT + r;   // local row
             const float gyv = (yl < P.nyl) ? P.gy[yl] : 0.f;
-            const float4 g4 = *reinterpret_cast<const float4 *>(P.gx + xg);
-            gxy[0] = g4.x * gyv;
-            gxy[1] = g4.y * gyv;
-            gxy[2] = g4.z * gyv;
-            gxy[3] = g4.w * gyv;
+            gxy[r][0] = g4.x * gyv;
+            gxy[r][1] = g4.y * gyv;
+            gxy[r][2] = g4.z * gyv;
+            gxy[r][3] = g4.w * gyv;
+            store_ok[r] = (yl < P.nyl) && (xg < P.nx);
+            src_col[r] = P.src_mask != 0 && P.src_j == yl && P.src_i >= xg && P.src_i < xg + 4;
+            pout[r] = P.p_out + (long long)yl * P.ys + xg;
+            qout[r] = P.q_out + (long long)yl * P.ys + xg;
         }
-        const bool src_col = P.src_mask != 0 && P.src_j == yl && P.src_i >= xg && P.src_i < xg + 4;
         const int src_c = P.src_i - xg;
-        float *pout = P.p_out + (long long)yl * P.ys + xg;
-        float *qout = P.q_out + (long long)yl * P.ys + xg;
-        const int sidx = ty * TX + 4 * tx;   // this thread's float offset in a stream tile
+        const int sidx = tg * RPT * TX + 4 * tx;   // float offset of row 0 in a stream tile
 
-        float4 q[NQ];
+        float4 q[RPT][NQ];
         // prime the queue with q(kb - Rz .. kb + Rz - 1)
 #pragma unroll
         for (int t = 0; t < 2 * RZ; ++t) {
             mbar_wait(&full[stage], phase);
             const float *st = reinterpret_cast<const float *>(smem + stage * C::STAGE);
-            q[t] = lds4(st + C::OFF_Q / 4 + sidx);
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) q[r][t] = lds4(st + C::OFF_Q / 4 + sidx + r * TX);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
+            if (leader) prod.issue(P, smem, full, empty);
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
@@ -296,71 +348,93 @@ __global__ void __launch_bounds__(nthreads(TY), MINB) vti_step_kernel(const __gr
                 if (k < ke) {
                     mbar_wait(&full[stage], phase);
                     const float *st = reinterpret_cast<const float *>(smem + stage * C::STAGE);
-                    q[(u + 2 * RZ) % NQ] = lds4(st + C::OFF_Q / 4 + sidx);   // q^n(k + Rz)
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r)
+                        q[r][(u + 2 * RZ) % NQ] = lds4(st + C::OFF_Q / 4 + sidx + r * TX);   // q^n(k + Rz)
                     const float *ps = st + C::OFF_P / 4;
-                    const float *prow = ps + (ty + R) * C::PW + 4 * tx;      // window start x0+4tx-RA
-                    float w[4 + 2 * RA];
-#pragma unroll
-                    for (int v = 0; v < (4 + 2 * RA) / 4; ++v) {
-                        const float4 t4 = lds4(prow + 4 * v);
-                        w[4 * v + 0] = t4.x;
-                        w[4 * v + 1] = t4.y;
-                        w[4 * v + 2] = t4.z;
-                        w[4 * v + 3] = t4.w;
-                    }
-                    const float *zr = st + C::OFF_ZR / 4;
-                    float zw[NQ + 1];
-#pragma unroll
-                    for (int m = 0; m < NQ + 1; ++m) zw[m] = zr[m];
+                    // smem row of tile row tg*RPT - R is tg*RPT; x window starts at x0 + 4tx - RA
+                    const float *pbase = ps + tg * RPT * C::PW + 4 * tx;
                     // Eq. 4 / h^2, canonical order: L = c0 p; L = fma(c_l, xpair + ypair, L)
-                    float L[4];
+                    float L[RPT][4];
+                    float pc[RPT][4];   // p^n at the points (2 u^n term)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) L[c] = P.cxy[0] * w[RA + c];
+                    for (int r = 0; r < RPT; ++r) {
+                        float w[NW];
+                        const float *prow = pbase + (r + R) * C::PW;
 #pragma unroll
-                    for (int l = 1; l <= R; ++l) {
-                        const float4 yp = lds4(prow + l * C::PW + RA);
-                        const float4 ym = lds4(prow - l * C::PW + RA);
+                        for (int v = 0; v < NW / 4; ++v) {
+                            const float4 t4 = lds4(prow + 4 * v);
+                            w[4 * v + 0] = t4.x;
+                            w[4 * v + 1] = t4.y;
+                            w[4 * v + 2] = t4.z;
+                            w[4 * v + 3] = t4.w;
+                        }
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            const float xpair = w[RA + c + l] + w[RA + c - l];
-                            const float ypair = f4(yp, c) + f4(ym, c);
-                            L[c] = __fmaf_rn(P.cxy[l], xpair + ypair, L[c]);
+                            pc[r][c] = w[RA + c];
+                            L[r][c] = P.cxy[0] * w[RA + c];
+                        }
+#pragma unroll
+                        for (int l = 1; l <= R; ++l) {
+                            // y neighbours of row r at distance l: shared column rows r+R+l, r+R-l
+                            const float4 yp = lds4(pbase + (r + R + l) * C::PW + RA);
+                            const float4 ym = lds4(pbase + (r + R - l) * C::PW + RA);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                const float xpair = w[RA + c + l] + w[RA + c - l];
+                                const float ypair = f4(yp, c) + f4(ym, c);
+                                L[r][c] = __fmaf_rn(P.cxy[l], xpair + ypair, L[r][c]);
+                            }
                         }
                     }
-                    const float4 pm4 = lds4(st + C::OFF_PM / 4 + sidx);
-                    const float4 qm4 = lds4(st + C::OFF_QM / 4 + sidx);
-                    const float4 vx4 = lds4(st + C::OFF_VX / 4 + sidx);
-                    const float4 vn4 = lds4(st + C::OFF_VN / 4 + sidx);
-                    const float4 vz4 = lds4(st + C::OFF_VZ / 4 + sidx);
+                    // stage data below is read at the point of use (register pressure at
+                    // R_z >= 6); the stage is released after the last shared-memory read
+                    const float *zr = st + C::OFF_ZR / 4;
+                    const float gz = zr[NQ];
+                    float pn[RPT][4], qn[RPT][4];
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        const float4 pm4 = lds4(st + C::OFF_PM / 4 + sidx + r * TX);
+                        const float4 qm4 = lds4(st + C::OFF_QM / 4 + sidx + r * TX);
+                        const float4 vx4 = lds4(st + C::OFF_VX / 4 + sidx + r * TX);
+                        const float4 vn4 = lds4(st + C::OFF_VN / 4 + sidx + r * TX);
+                        const float4 vz4 = lds4(st + C::OFF_VZ / 4 + sidx + r * TX);
+                        const bool src_here = src_col[r] && (k == P.src_k);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
+                            float D = zr[0] * f4(q[r][u % NQ], c);
+#pragma unroll
+                            for (int m = 1; m < NQ; ++m) D = __fmaf_rn(zr[m], f4(q[r][(u + m) % NQ], c), D);
+                            const float vD = f4(vz4, c) * D;
+                            float Fp = __fmaf_rn(f4(vx4, c), L[r][c], vD);
+                            float Fq = __fmaf_rn(f4(vn4, c), L[r][c], vD);
+                            if (src_here && c == src_c) {
+                                if (P.src_mask & 1) Fp = Fp + P.s;
+                                if (P.src_mask & 2) Fq = Fq + P.s;
+                            }
+                            const float g = gxy[r][c] * gz;   // (gx gy) gz
+                            pn[r][c] = g * __fmaf_rn(P.dt2, Fp, __fmaf_rn(-g, f4(pm4, c), 2.0f * pc[r][c]));
+                            qn[r][c] = g * __fmaf_rn(P.dt2, Fq,
+                                                     __fmaf_rn(-g, f4(qm4, c), 2.0f * f4(q[r][(u + RZ) % NQ], c)));
+                        }
+                    }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[stage]);
+                    if (leader) prod.issue(P, smem, full, empty);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
-                    const bool src_here = src_col && (k == P.src_k);
-                    float pn[4], qn[4];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
-                        float D = zw[0] * f4(q[u % NQ], c);
-#pragma unroll
-                        for (int m = 1; m < NQ; ++m) D = __fmaf_rn(zw[m], f4(q[(u + m) % NQ], c), D);
-                        const float vD = f4(vz4, c) * D;
-                        float Fp = __fmaf_rn(f4(vx4, c), L[c], vD);
-                        float Fq = __fmaf_rn(f4(vn4, c), L[c], vD);
-                        if (src_here && c == src_c) {
-                            if (P.src_mask & 1) Fp = Fp + P.s;
-                            if (P.src_mask & 2) Fq = Fq + P.s;
+                    for (int r = 0; r < RPT; ++r) {
+                        if (store_ok[r]) {
+                            const long long off = (long long)k * P.zs;
+                            *reinterpret_cast<float4 *>(pout[r] + off) =
+                                make_float4(pn[r][0], pn[r][1], pn[r][2], pn[r][3]);
+                            *reinterpret_cast<float4 *>(qout[r] + off) =
+                                make_float4(qn[r][0], qn[r][1], qn[r][2], qn[r][3]);
                         }
-                        const float g = gxy[c] * zw[NQ];   // (gx gy) gz
-                        pn[c] = g * __fmaf_rn(P.dt2, Fp, __fmaf_rn(-g, f4(pm4, c), 2.0f * w[RA + c]));
-                        qn[c] = g * __fmaf_rn(P.dt2, Fq, __fmaf_rn(-g, f4(qm4, c), 2.0f * f4(q[(u + RZ) % NQ], c)));
-                    }
-                    if (store_ok) {
-                        const long long off = (long long)k * P.zs;
-                        *reinterpret_cast<float4 *>(pout + off) = make_float4(pn[0], pn[1], pn[2], pn[3]);
-                        *reinterpret_cast<float4 *>(qout + off) = make_float4(qn[0], qn[1], qn[2], qn[3]);
                     }
                 }
             }

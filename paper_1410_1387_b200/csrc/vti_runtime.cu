@@ -105,30 +105,31 @@ static PFN_encodeTiled get_encode()
 
 // ============================================================ kernel table
 struct KernelEntry {
-    int r, rz, ty, stages, minb, stage_bytes;
+    int r, rz, ty, rpt, wp, stages, minb, stage_bytes;
     void (*fn)(StepParams);
     int zrow;
     int threads;
 };
 
-template <int R, int RZ, int TY, int S, int B>
+template <int R, int RZ, int TY, int RPT, int WP, int S, int B>
 static KernelEntry entry()
 {
-    return KernelEntry{R, RZ, TY, S, B, Cfg<R, RZ, TY>::STAGE, vti_step_kernel<R, RZ, TY, S, B>,
-                       Cfg<R, RZ, TY>::ZROW, nthreads(TY)};
+    return KernelEntry{R, RZ, TY, RPT, WP, S, B, Cfg<R, RZ, TY>::STAGE, vti_step_kernel<R, RZ, TY, RPT, WP, S, B>,
+                       Cfg<R, RZ, TY>::ZROW, nthreads(TY, RPT, WP)};
 }
 
-// Compiled variants. ty = 0 picks the default tile height for the pair.
-static const KernelEntry *find_kernel(int r, int rz, int ty)
+// Compiled variants; the first match is the default for a radius pair.
+// -1 = any (env VTI_TY, VTI_WP select the others for experiments).
+static const KernelEntry *find_kernel(int r, int rz, int ty, int wp)
 {
     static const KernelEntry table[] = {
-        entry<4, 4, 32, 3, 1>(), entry<4, 4, 16, 3, 2>(),
-        entry<8, 4, 32, 3, 1>(), entry<8, 4, 16, 3, 2>(),
-        entry<6, 6, 32, 3, 1>(), entry<6, 6, 16, 3, 2>(),
-        entry<12, 8, 32, 2, 1>(), entry<12, 8, 16, 2, 2>(),
+        entry<4, 4, 32, 1, 1, 3, 1>(),  entry<4, 4, 32, 1, 0, 3, 1>(),  entry<4, 4, 16, 1, 1, 3, 2>(),
+        entry<8, 4, 32, 1, 1, 3, 1>(),  entry<8, 4, 32, 1, 0, 3, 1>(),  entry<8, 4, 16, 1, 1, 3, 2>(),
+        entry<6, 6, 32, 1, 0, 3, 1>(),  entry<6, 6, 32, 1, 1, 3, 1>(),  entry<6, 6, 16, 1, 0, 3, 2>(),
+        entry<12, 8, 32, 1, 0, 2, 1>(), entry<12, 8, 32, 1, 1, 2, 1>(), entry<12, 8, 16, 1, 0, 2, 2>(),
     };
     for (const auto &e : table)
-        if (e.r == r && e.rz == rz && (ty == 0 || e.ty == ty)) return &e;
+        if (e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp)) return &e;
     return nullptr;
 }
 
@@ -491,10 +492,11 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     h->cfg = *cfg;
     h->R = cfg->r_xy;
     h->RZ = cfg->r_z;
-    int want_ty = 0;
+    int want_ty = -1, want_wp = -1;
     if (const char *e = getenv("VTI_TY")) want_ty = atoi(e);
-    h->K = find_kernel(h->R, h->RZ, want_ty);
-    if (!h->K && want_ty) h->K = find_kernel(h->R, h->RZ, 0);
+    if (const char *e = getenv("VTI_WP")) want_wp = atoi(e);
+    h->K = find_kernel(h->R, h->RZ, want_ty, want_wp);
+    if (!h->K) h->K = find_kernel(h->R, h->RZ, -1, -1);
     if (!h->K) return fail(h, VTI_E_UNSUPPORTED, "(r_xy, r_z) = (%d, %d) not compiled", h->R, h->RZ);
     h->TY = h->K->ty;
     vti_slab(cfg, &h->y0, &h->nyl);

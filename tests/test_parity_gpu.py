@@ -260,3 +260,15 @@ def test_local_group_slabs_bitwise_equal_single(nranks):
         assert np.array_equal(full, g[f])
     for h in hs:
         h.close()
+
+
+@pytest.mark.parametrize("r,rz", [(4, 4), (8, 4), (6, 6), (12, 8)])
+@pytest.mark.parametrize("ty,wp", [(32, 1), (32, 0), (16, -1)])
+def test_every_compiled_variant(r, rz, ty, wp, monkeypatch):
+    """Each (tile height, producer-warp) instantiation is bitwise equal to the oracle."""
+    monkeypatch.setenv("VTI_TY", str(ty))
+    monkeypatch.setenv("VTI_WP", str(wp))
+    cfg = small_cfg(77, 45, 41, r, rz, damp=5, src=(30, 22, 20))
+    st = random_state(cfg, seed=9)
+    g, o = run_both(cfg, 4, state=st, model=random_model(cfg, seed=5), n0=2)
+    assert_parity(g, o)
