@@ -243,7 +243,8 @@ struct vti_s {
     const KernelEntry *K = nullptr;
     int smem_bytes = 0;
     int sms = 0, ctas_per_sm = 0;
-    int zchunk = 0, nzc = 0, grid = 0;
+    int zchunk = 0, nzc = 0, grid = 0;   // single-launch schedule
+    int zchunk_edge = 0, zchunk_inner = 0;   // nranks > 1: per-launch chunking
     int tune_zchunk = 0, tune_ctas = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -351,28 +352,51 @@ static vti_status encode(vti_s *h, CUtensorMap *tm, float *base, int rows, int b
     return VTI_OK;
 }
 
-// Work items are (tile, z-chunk). Measured on B200 (profiles/):
-// full z columns marching in lockstep keep the p apron re-reads in L2 and
-// avoid the 2Rz-plane q priming of every chunk, and beat finer chunking even
-// with some SMs idle (C2: 128 columns on 148 SMs > 1024 chunks). So: one chunk
-// per column unless there are fewer than half as many tiles as CTA slots; then
-// split z just enough to give every slot an item.
+// Work items are (tile, z-chunk). Measured on B200: full z
+// columns marching in lockstep keep the p apron re-reads in L2 and avoid the
+// 2Rz-plane q priming of each chunk, and ~110 resident CTAs already saturate
+// HBM (C2: 128 columns on 148 SMs beat 1024 chunks). The chunk count per
+// launch minimises a wave cost: each round of a active CTAs costs
+// zchunk * a / min(a, SAT), times the priming overhead 1 + 8 Rz / (36 zchunk).
+static int choose_zchunk(const vti_s *h, int tiles)
+{
+    const int nz = h->cfg.nz;
+    if (h->tune_zchunk > 0) return std::min(h->tune_zchunk, nz);
+    if (tiles <= 0) return nz;
+    const int slots = h->sms * h->ctas_per_sm;
+    double sat = 110.0 * h->ctas_per_sm;
+    if (const char *e = getenv("VTI_SAT")) sat = atof(e);
+    sat = std::max(1.0, std::min(sat, (double)slots));
+    double best = 1e300;
+    int best_zc = nz;
+    const int max_nzc = std::max(1, nz / (4 * h->RZ));
+    for (int nzc = 1; nzc <= max_nzc; ++nzc) {
+        const int zc = (nz + nzc - 1) / nzc;
+        if ((nz + zc - 1) / zc != nzc) continue;   // same chunking as a smaller nzc
+        const long items = (long)tiles * nzc;
+        const long full = items / slots, last = items % slots;
+        double cost = (double)full * zc * slots / std::min<double>(slots, sat);
+        if (last) cost += (double)zc * last / std::min<double>(last, sat);
+        cost *= 1.0 + (8.0 * h->RZ) / (36.0 * zc);
+        if (cost < best * (1.0 - 1e-3)) {
+            best = cost;
+            best_zc = zc;
+        }
+    }
+    return best_zc;
+}
+
+// Default schedule: one launch over all tile rows (single slab), or an edge
+// launch (first and last tile rows) plus an interior launch (nranks > 1).
 static void choose_schedule(vti_s *h)
 {
-    const int slots = h->sms * h->ctas_per_sm;
-    const int tiles = h->ntx * h->nty;
-    const int nz = h->cfg.nz;
-    if (h->tune_zchunk > 0) {
-        h->zchunk = std::min(h->tune_zchunk, nz);
-    } else if (2 * tiles >= slots) {
-        h->zchunk = nz;
-    } else {
-        const int nzc = std::min((slots + tiles - 1) / tiles, std::max(1, nz / (4 * h->RZ)));
-        h->zchunk = (nz + nzc - 1) / nzc;
-    }
-    h->nzc = (nz + h->zchunk - 1) / h->zchunk;
-    const long items = (long)tiles * h->nzc;
-    h->grid = (int)std::min<long>(items, slots);
+    const int edge_rows = std::min(2, h->nty), inner_rows = std::max(0, h->nty - 2);
+    h->zchunk = choose_zchunk(h, h->ntx * h->nty);
+    h->zchunk_edge = choose_zchunk(h, h->ntx * edge_rows);
+    h->zchunk_inner = choose_zchunk(h, h->ntx * inner_rows);
+    h->nzc = (h->cfg.nz + h->zchunk - 1) / h->zchunk;
+    const long items = (long)h->ntx * h->nty * h->nzc;
+    h->grid = (int)std::min<long>(items, (long)h->sms * h->ctas_per_sm);
 }
 
 static vti_status check_cfg(const vti_config *c)
@@ -741,7 +765,7 @@ vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx
 }  // extern "C"
 
 // ============================================================ stepping
-static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int nty_sel)
+static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int nty_sel, int zchunk)
 {
     const int c = h->cur, o = 1 - c;
     P.tm_p = h->tm_ph[c];
@@ -774,16 +798,16 @@ static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int 
     P.ty_begin = ty_begin;
     P.ty_step = ty_step;
     P.nty = nty_sel;
-    P.zchunk = h->zchunk;
-    P.nzc = h->nzc;
-    P.items = h->ntx * nty_sel * h->nzc;
+    P.zchunk = zchunk;
+    P.nzc = (h->cfg.nz + zchunk - 1) / zchunk;
+    P.items = h->ntx * nty_sel * P.nzc;
 }
 
-static vti_status launch_rows(vti_s *h, int ty_begin, int ty_step, int nty_sel)
+static vti_status launch_rows(vti_s *h, int ty_begin, int ty_step, int nty_sel, int zchunk)
 {
     if (nty_sel <= 0) return VTI_OK;
     StepParams P;
-    fill_params(h, P, ty_begin, ty_step, nty_sel);
+    fill_params(h, P, ty_begin, ty_step, nty_sel, zchunk);
     const int grid = std::min(P.items, h->sms * h->ctas_per_sm);
     void *args[] = {&P};
     CU(h, cudaLaunchKernel((const void *)h->K->fn, dim3(grid), dim3(h->K->threads), args, h->smem_bytes, h->stream));
@@ -940,15 +964,17 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     }
     for (int it = 0; it < nsteps; ++it) {
         if (!multi) {
-            if ((s = launch_rows(h, 0, 1, h->nty)) != VTI_OK) return s;
+            if ((s = launch_rows(h, 0, 1, h->nty, h->zchunk)) != VTI_OK) return s;
         } else {
             const int o = 1 - h->cur;
             // edge tile rows first, so the rows the neighbours need are ready early
-            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty))) != VTI_OK) return s;
+            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty), h->zchunk_edge)) != VTI_OK)
+                return s;
             if ((s = pack_send(h, o)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
             if ((s = exchange_nccl(h, o)) != VTI_OK) return s;
-            if ((s = launch_rows(h, 1, 1, h->nty - 2)) != VTI_OK) return s;   // interior rows overlap the exchange
+            if ((s = launch_rows(h, 1, 1, h->nty - 2, h->zchunk_inner)) != VTI_OK)   // overlaps the exchange
+                return s;
             CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         }
         h->cur = 1 - h->cur;
@@ -1041,7 +1067,8 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
-            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty))) != VTI_OK) return s;
+            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty), h->zchunk_edge)) != VTI_OK)
+                return s;
             if ((s = pack_send(h, 1 - h->cur)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
         }
@@ -1049,7 +1076,7 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
-            if ((s = launch_rows(h, 1, 1, h->nty - 2)) != VTI_OK) return s;
+            if ((s = launch_rows(h, 1, 1, h->nty - 2, h->zchunk_inner)) != VTI_OK) return s;
         }
         if ((s = group_wait(hs, n)) != VTI_OK) return s;
         for (int i = 0; i < n; ++i) {
