@@ -252,7 +252,6 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
     constexpr int NCONS_WARPS = cons_warps(TY, RPT);
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
-    constexpr int NW = 4 + 2 * RA;   // x window of one row (floats)
     static_assert(TY % (2 * RPT) == 0, "tile rows must split into 16-thread row groups");
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE);
@@ -359,29 +358,24 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                     float pc[RPT][4];   // p^n at the points (2 u^n term)
 #pragma unroll
                     for (int r = 0; r < RPT; ++r) {
-                        float w[NW];
+                        // x window of row r: floats [4tx, 4tx + 4 + 2RA) of smem row r + R, read
+                        // as float4 chunks at the point of use (identical loads are CSE'd), so
+                        // only the chunks of the current radius stay live
                         const float *prow = pbase + (r + R) * C::PW;
-#pragma unroll
-                        for (int v = 0; v < NW / 4; ++v) {
-                            const float4 t4 = lds4(prow + 4 * v);
-                            w[4 * v + 0] = t4.x;
-                            w[4 * v + 1] = t4.y;
-                            w[4 * v + 2] = t4.z;
-                            w[4 * v + 3] = t4.w;
-                        }
+                        auto wx = [&](int i) { return f4(lds4(prow + 4 * (i / 4)), i % 4); };
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            pc[r][c] = w[RA + c];
-                            L[r][c] = P.cxy[0] * w[RA + c];
+                            pc[r][c] = wx(RA + c);
+                            L[r][c] = P.cxy[0] * pc[r][c];
                         }
 #pragma unroll
                         for (int l = 1; l <= R; ++l) {
-                            // y neighbours of row r at distance l: shared column rows r+R+l, r+R-l
+                            // y neighbours of row r at distance l: smem rows r+R+l, r+R-l at x offset RA
                             const float4 yp = lds4(pbase + (r + R + l) * C::PW + RA);
                             const float4 ym = lds4(pbase + (r + R - l) * C::PW + RA);
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                const float xpair = w[RA + c + l] + w[RA + c - l];
+                                const float xpair = wx(RA + c + l) + wx(RA + c - l);
                                 const float ypair = f4(yp, c) + f4(ym, c);
                                 L[r][c] = __fmaf_rn(P.cxy[l], xpair + ypair, L[r][c]);
                             }

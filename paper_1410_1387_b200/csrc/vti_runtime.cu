@@ -126,7 +126,7 @@ static const KernelEntry *find_kernel(int r, int rz, int ty, int wp)
         entry<4, 4, 32, 1, 1, 3, 1>(),  entry<4, 4, 32, 1, 0, 3, 1>(),  entry<4, 4, 16, 1, 1, 3, 2>(),
         entry<8, 4, 32, 1, 1, 3, 1>(),  entry<8, 4, 32, 1, 0, 3, 1>(),  entry<8, 4, 16, 1, 1, 3, 2>(),
         entry<6, 6, 32, 1, 0, 3, 1>(),  entry<6, 6, 32, 1, 1, 3, 1>(),  entry<6, 6, 16, 1, 0, 3, 2>(),
-        entry<12, 8, 32, 1, 0, 2, 1>(), entry<12, 8, 32, 1, 1, 2, 1>(), entry<12, 8, 16, 1, 0, 2, 2>(),
+        entry<12, 8, 32, 1, 1, 3, 1>(), entry<12, 8, 32, 1, 0, 3, 1>(), entry<12, 8, 16, 1, 0, 2, 2>(),
     };
     for (const auto &e : table)
         if (e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp)) return &e;
@@ -1135,7 +1135,12 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->zchunk = h->zchunk;
     info->grid = std::min(h->ntx * h->nty * h->nzc, h->sms * h->ctas_per_sm);
     info->work_items = h->ntx * h->nty * h->nzc;
-    info->launches_per_step = h->cfg.nranks > 1 ? (h->nty > 2 ? 2 : 1) : 1;
+    if (h->cfg.nranks > 1) {   // edge + interior step kernels, then pack + unpack per neighbour
+        const int neighbours = (h->cfg.rank > 0) + (h->cfg.rank < h->cfg.nranks - 1);
+        info->launches_per_step = (h->nty > 2 ? 2 : 1) + 2 * neighbours;
+    } else {
+        info->launches_per_step = 1;
+    }
     info->device_bytes = h->device_bytes;
     info->time_index = h->n;
     return VTI_OK;

@@ -62,7 +62,15 @@ def C5(n_gpus=1):
                  dz=(5.0, 15.0), notes="1024^3 per GPU, R=6/6, eps=delta=0, weak scaling")
 
 
-CONFIGS = {"C1": C1, "C2": C2, "C3": C3, "C4": C4, "C5": C5}
+def N1():
+    """the paper's benchmark radii R_xy=12, R_z=8 ("92 flops per
+    point", 1000 steps) on the C2 grid and model (the paper
+    states no grid)."""
+    return _base("N1", 512, 512, 512, 12, 8, layered(8), 1000, dz=(5.0, 15.0),
+                 notes="paper benchmark radii (12,8) on the C2 512^3 layered model, 1000 steps")
+
+
+CONFIGS = {"C1": C1, "C2": C2, "C3": C3, "C4": C4, "C5": C5, "N1": N1}
 
 
 def scaled(cfg: dict, nx=None, ny=None, nz=None, steps=None, **kw) -> dict:
