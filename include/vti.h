@@ -182,6 +182,27 @@ vti_status vti_query(vti_t h, vti_info *info);
 /* Tuning knobs (0 = library default): planes per work item, CTAs per SM. */
 vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm);
 
+/* Select a compiled step-kernel variant: tile height (32 or 16 rows) and
+ * dedicated TMA producer warp (1) or in-line producer (0); -1 = any. The
+ * arithmetic (and so every result bit) is identical across variants.
+ * Errors: UNSUPPORTED if no such variant is compiled for (r_xy, r_z). */
+vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp);
+
+typedef struct {
+    int32_t tile_y, producer_warp;  /* chosen variant */
+    int32_t zchunk;                 /* chosen planes per work item */
+    float ms_per_step;              /* its measured device time per step */
+    int32_t candidates;             /* (variant, z-chunk) pairs timed */
+} vti_tune_result;
+
+/* SURVEY.md 8(f) N2 autotuner (the paper tuned its CPU blocking the same way,
+ * PAPER.md l.242-243): time every compiled variant x z-chunk candidate for
+ * probe_steps steps on this handle's own grid and keep the fastest. Needs the
+ * model set and the initial zero state (before any vti_step / vti_set_fields):
+ * probes inject no source, so the state stays zero and the time index is reset
+ * to 0. out may be NULL. Errors: STATE, PARAM, CUDA. */
+vti_status vti_autotune(vti_t h, int32_t probe_steps, vti_tune_result *out);
+
 /* Last error message of the handle (or of the last failed vti_create when h is NULL). */
 const char *vti_last_error(vti_t h);
 

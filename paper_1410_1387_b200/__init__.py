@@ -18,7 +18,7 @@ import numpy as np
 
 from ._build import LIB, build  # noqa: F401
 
-__all__ = ["VTI", "VTIError", "Config", "Info", "lib", "slab", "nccl_unique_id", "group_step"]
+__all__ = ["VTI", "VTIError", "Config", "Info", "TuneResult", "lib", "slab", "nccl_unique_id", "group_step"]
 
 STATUS = {
     0: "VTI_OK", 1: "VTI_E_PARAM", 2: "VTI_E_GEOMETRY", 3: "VTI_E_MODEL", 4: "VTI_E_ANISO",
@@ -43,6 +43,14 @@ class Config(C.Structure):
         ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
         ("nccl_id", C.c_void_p), ("check_every", C.c_int32),
     ]
+
+
+class TuneResult(C.Structure):
+    _fields_ = [("tile_y", C.c_int32), ("producer_warp", C.c_int32), ("zchunk", C.c_int32),
+                ("ms_per_step", C.c_float), ("candidates", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class Info(C.Structure):
@@ -88,6 +96,8 @@ def _load():
         "vti_stream": (C.c_void_p, [H]),
         "vti_query": (st, [H, C.POINTER(Info)]),
         "vti_set_tuning": (st, [H, C.c_int32, C.c_int32]),
+        "vti_set_variant": (st, [H, C.c_int32, C.c_int32]),
+        "vti_autotune": (st, [H, C.c_int32, C.POINTER(TuneResult)]),
         "vti_last_error": (C.c_char_p, [H]),
         "vti_destroy": (st, [H]),
     }
@@ -253,6 +263,14 @@ class VTI:
 
     def set_tuning(self, zchunk=0, ctas_per_sm=0):
         _check(self.h, lib.vti_set_tuning(self.h, zchunk, ctas_per_sm))
+
+    def set_variant(self, tile_y=-1, producer_warp=-1):
+        _check(self.h, lib.vti_set_variant(self.h, tile_y, producer_warp))
+
+    def autotune(self, probe_steps=5) -> dict:
+        r = TuneResult()
+        _check(self.h, lib.vti_autotune(self.h, probe_steps, C.byref(r)))
+        return r.as_dict()
 
 
 def group_step(handles, nsteps=1):

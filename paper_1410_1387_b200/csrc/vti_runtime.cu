@@ -133,6 +133,16 @@ static const KernelEntry *find_kernel(int r, int rz, int ty, int wp)
     return nullptr;
 }
 
+static std::vector<const KernelEntry *> all_kernels(int r, int rz)
+{
+    std::vector<const KernelEntry *> v;
+    for (int ty : {32, 16})
+        for (int wp : {1, 0})
+            if (const KernelEntry *e = find_kernel(r, rz, ty, wp))
+                if (e->ty == ty && e->wp == wp) v.push_back(e);
+    return v;
+}
+
 // ============================================================ aux kernels
 // Internal element (x, y, k) of an interior view lives at base[y * ys + k * zs + x].
 
@@ -245,7 +255,7 @@ struct vti_s {
     int sms = 0, ctas_per_sm = 0;
     int zchunk = 0, nzc = 0, grid = 0;   // single-launch schedule
     int zchunk_edge = 0, zchunk_inner = 0;   // nranks > 1: per-launch chunking
-    int tune_zchunk = 0, tune_ctas = 0;
+    int tune_zchunk = 0, tune_ctas = 0;   // vti_set_tuning / vti_autotune overrides (0 = model)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaStream_t comm = nullptr;
@@ -275,6 +285,8 @@ struct vti_s {
     ncclComm_t comm_nccl = nullptr;
     bool group_mode = false;
     bool halo_dirty = false;
+    bool suppress_src = false;   // autotune probes inject nothing
+    bool fields_touched = false; // vti_set_fields* called (state may be non-zero)
 
     size_t total_floats() const { return (size_t)cfg.nz * rows * nxp; }
     float *in(float *base) const { return base + (long long)R * ys; }   // interior view
@@ -508,6 +520,42 @@ static vti_status alloc(vti_s *h, void **p, size_t bytes)
     return VTI_OK;
 }
 
+// Make K the step kernel of the handle: tile height, shared memory, occupancy,
+// default schedule and the TMA tensor maps (whose boxes depend on TY).
+static vti_status select_variant(vti_s *h, const KernelEntry *K)
+{
+    h->K = K;
+    h->TY = K->ty;
+    h->nty = (h->nyl + h->TY - 1) / h->TY;
+    h->smem_bytes = K->stages * K->stage_bytes + 2 * K->stages * 8;
+    CU(h, cudaFuncSetAttribute((const void *)K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+    CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)K->fn, K->threads,
+                                                        h->smem_bytes));
+    if (h->ctas_per_sm < 1) return fail(h, VTI_E_CUDA, "step kernel cannot be resident (smem %d B)", h->smem_bytes);
+    if (h->tune_ctas > 0) h->ctas_per_sm = std::min(h->ctas_per_sm, h->tune_ctas);
+    choose_schedule(h);
+
+    // L2 promotion of the halo'd p box (its x apron is not 256-B aligned): env VTI_P_PROMO=none|64|128|256
+    CUtensorMapL2promotion ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    if (const char *e = getenv("VTI_P_PROMO")) {
+        if (!strcmp(e, "none")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+        else if (!strcmp(e, "64")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        else if (!strcmp(e, "256")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
+    const int RA = (h->R + 3) / 4 * 4;   // 16-byte aligned x apron (see Cfg::RA)
+    const int PW = TX + 2 * RA, PH = h->TY + 2 * h->R;
+    vti_status s;
+    for (int b = 0; b < 2; ++b) {
+        if ((s = encode(h, &h->tm_ph[b], h->pbuf[b], h->rows, PW, PH, ppromo)) != VTI_OK) return s;
+        if ((s = encode(h, &h->tm_pi[b], h->p_int(b), h->nyl, TX, h->TY)) != VTI_OK) return s;
+        if ((s = encode(h, &h->tm_q[b], h->q_int(b), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    }
+    if ((s = encode(h, &h->tm_vx, h->in(h->vx2), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    if ((s = encode(h, &h->tm_vn, h->in(h->vn2), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    if ((s = encode(h, &h->tm_vz, h->in(h->vz2), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    return VTI_OK;
+}
+
 static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy, const float *w_z)
 {
     vti_status st = check_cfg(cfg);
@@ -536,7 +584,6 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
         h->zs = h->nxp;
     }
     h->ntx = (cfg->nx + TX - 1) / TX;
-    h->nty = (h->nyl + h->TY - 1) / h->TY;
     for (int l = 0; l <= h->R; ++l) {
         if (!std::isfinite(w_xy[l])) return fail(h, VTI_E_PARAM, "non-finite w_xy[%d]", l);
         h->cxy[l] = (float)((double)w_xy[l] / (cfg->h * cfg->h));   // reading c3
@@ -558,13 +605,6 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     CU(h, cudaEventCreate(&h->ev_t0));
     CU(h, cudaEventCreate(&h->ev_t1));
     CU(h, cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cfg->device));
-
-    h->smem_bytes = h->K->stages * h->K->stage_bytes + 2 * h->K->stages * 8;
-    CU(h, cudaFuncSetAttribute((const void *)h->K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
-    CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)h->K->fn, h->K->threads,
-                                                        h->smem_bytes));
-    if (h->ctas_per_sm < 1) return fail(h, VTI_E_CUDA, "step kernel cannot be resident (smem %d B)", h->smem_bytes);
-    choose_schedule(h);
 
     const size_t bytes = h->total_floats() * 4;
     vti_status s;
@@ -606,23 +646,7 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     CU(h, cudaMemcpyAsync(h->gx, gxv.data(), gxv.size() * 4, cudaMemcpyHostToDevice, h->stream));
     CU(h, cudaMemcpyAsync(h->gy, gyv.data(), gyv.size() * 4, cudaMemcpyHostToDevice, h->stream));
 
-    const int RA = (h->R + 3) / 4 * 4;   // 16-byte aligned x apron (see Cfg::RA)
-    const int PW = TX + 2 * RA, PH = h->TY + 2 * h->R;
-    // L2 promotion of the halo'd p box (its x apron is not 256-B aligned): env VTI_P_PROMO=none|64|128|256
-    CUtensorMapL2promotion ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    if (const char *e = getenv("VTI_P_PROMO")) {
-        if (!strcmp(e, "none")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
-        else if (!strcmp(e, "64")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
-        else if (!strcmp(e, "128")) ppromo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    }
-    for (int b = 0; b < 2; ++b) {
-        if ((s = encode(h, &h->tm_ph[b], h->pbuf[b], h->rows, PW, PH, ppromo)) != VTI_OK) return s;
-        if ((s = encode(h, &h->tm_pi[b], h->p_int(b), h->nyl, TX, h->TY)) != VTI_OK) return s;
-        if ((s = encode(h, &h->tm_q[b], h->q_int(b), h->nyl, TX, h->TY)) != VTI_OK) return s;
-    }
-    if ((s = encode(h, &h->tm_vx, h->in(h->vx2), h->nyl, TX, h->TY)) != VTI_OK) return s;
-    if ((s = encode(h, &h->tm_vn, h->in(h->vn2), h->nyl, TX, h->TY)) != VTI_OK) return s;
-    if ((s = encode(h, &h->tm_vz, h->in(h->vz2), h->nyl, TX, h->TY)) != VTI_OK) return s;
+    if ((s = select_variant(h, h->K)) != VTI_OK) return s;
 
     if (cfg->nranks > 1) {
         if (cfg->nccl_id) {
@@ -782,7 +806,7 @@ static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int 
     P.gy = h->gy;
     for (int l = 0; l <= MAX_R; ++l) P.cxy[l] = l <= h->R ? h->cxy[l] : 0.f;
     P.dt2 = h->dt2;
-    const bool owned = h->has_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
+    const bool owned = h->has_src && !h->suppress_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
     // s(t^n), t^n = n dt, double on the host, rounded once (reading c7)
     P.s = owned ? (float)(h->src_amp * ricker((double)h->n * h->cfg.dt, h->src_f, h->src_t0)) : 0.f;
     P.src_i = h->src_i;
@@ -934,6 +958,7 @@ vti_status vti_set_fields_planes(vti_t h, int32_t k0, int32_t nk, const float *p
     if ((s = upload_planes(h, h->q_int(o), qm, k0, nk)) != VTI_OK) return s;
     CU(h, cudaStreamSynchronize(h->stream));
     h->halo_dirty = h->cfg.nranks > 1;
+    h->fields_touched = true;
     return VTI_OK;
 }
 
@@ -1151,13 +1176,74 @@ vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm)
     if (!h) return VTI_E_PARAM;
     if (zchunk < 0 || ctas_per_sm < 0) return fail(h, VTI_E_PARAM, "negative tuning value");
     h->tune_zchunk = zchunk;
-    if (ctas_per_sm > 0) {
-        int maxb = 0;
-        CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, (const void *)h->K->fn, h->K->threads,
-                                                            h->smem_bytes));
-        h->ctas_per_sm = std::min(ctas_per_sm, maxb);
+    h->tune_ctas = ctas_per_sm;
+    CU(h, cudaSetDevice(h->cfg.device));
+    return select_variant(h, h->K);
+}
+
+vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp)
+{
+    if (!h) return VTI_E_PARAM;
+    const KernelEntry *K = find_kernel(h->R, h->RZ, tile_y, producer_warp);
+    if (!K) return fail(h, VTI_E_UNSUPPORTED, "no compiled variant (r_xy %d, r_z %d, tile_y %d, producer_warp %d)",
+                        h->R, h->RZ, tile_y, producer_warp);
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    return select_variant(h, K);
+}
+
+vti_status vti_autotune(vti_t h, int32_t probe_steps, vti_tune_result *out)
+{
+    if (!h) return VTI_E_PARAM;
+    if (probe_steps < 1) return fail(h, VTI_E_PARAM, "probe_steps must be >= 1");
+    if (!h->model_set) return fail(h, VTI_E_STATE, "model not set");
+    if (h->group_mode) return fail(h, VTI_E_STATE, "autotune is per handle; not for local-group handles");
+    if (h->n != 0 || h->fields_touched)
+        return fail(h, VTI_E_STATE, "autotune needs the initial zero state (call it before stepping or set_fields)");
+    CU(h, cudaSetDevice(h->cfg.device));
+    const KernelEntry *keep = h->K;
+    const int keep_zc = h->tune_zchunk;
+    float best_ms = 1e30f;
+    const KernelEntry *best_k = keep;
+    int best_zc = 0, ncand = 0;
+    h->suppress_src = true;   // zero state, no injection: every probe step leaves u == 0
+    for (const KernelEntry *K : all_kernels(h->R, h->RZ)) {
+        h->tune_zchunk = 0;
+        vti_status s = select_variant(h, K);
+        if (s != VTI_OK) continue;   // e.g. not resident on this device
+        std::vector<int> zcs = {0, h->cfg.nz, (h->cfg.nz + 1) / 2, (h->cfg.nz + 3) / 4};
+        for (int zc : zcs) {
+            if (zc != 0 && zc < 4 * h->RZ) continue;
+            h->tune_zchunk = zc;
+            choose_schedule(h);
+            float ms = 0.f;
+            if ((s = vti_step(h, 2)) != VTI_OK) break;                       // warm-up
+            if ((s = vti_step_timed(h, probe_steps, &ms)) != VTI_OK) break;
+            ++ncand;
+            if (ms < best_ms) {
+                best_ms = ms;
+                best_k = K;
+                best_zc = zc;
+            }
+        }
+        if (s != VTI_OK) {
+            h->suppress_src = false;
+            return s;
+        }
     }
-    choose_schedule(h);
+    h->suppress_src = false;
+    h->n = 0;   // probes stepped a zero state; restore the time origin
+    h->tune_zchunk = best_zc;
+    vti_status s = select_variant(h, best_k ? best_k : keep);
+    if (s != VTI_OK) return s;
+    (void)keep_zc;
+    if (out) {
+        out->tile_y = h->K->ty;
+        out->producer_warp = h->K->wp;
+        out->zchunk = h->zchunk;
+        out->ms_per_step = best_ms / probe_steps;
+        out->candidates = ncand;
+    }
     return VTI_OK;
 }
 

@@ -272,3 +272,53 @@ def test_every_compiled_variant(r, rz, ty, wp, monkeypatch):
     st = random_state(cfg, seed=9)
     g, o = run_both(cfg, 4, state=st, model=random_model(cfg, seed=5), n0=2)
     assert_parity(g, o)
+
+
+@pytest.mark.parametrize("r,rz", [(4, 4), (6, 6)])
+def test_autotune_then_parity(r, rz):
+    """vti_autotune probes every variant on the zero state, then the run is still bitwise exact."""
+    from paper_1410_1387_b200 import VTIError
+    cfg = small_cfg(96, 70, 60, r, rz, damp=6, src=(40, 33, 30))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    with make(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        res = v.autotune(probe_steps=2)
+        assert res["candidates"] >= 3 and res["tile_y"] in (16, 32) and res["ms_per_step"] > 0
+        assert v.time_index == 0
+        p0, q0 = v.get_fields(0)
+        assert not p0.any() and not q0.any()          # probes left the zero state untouched
+        info = v.info()
+        assert info["tile_y"] == res["tile_y"] and info["zchunk"] == res["zchunk"]
+        v.step(15)
+        p, q = v.get_fields(0)
+        with pytest.raises(VTIError) as e:
+            v.autotune(2)                              # not the initial state any more
+        assert e.value.name == "VTI_E_STATE"
+    po, qo, _, _, _ = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=15)
+    assert np.abs(po).max() > 0
+    assert np.array_equal(p, po) and np.array_equal(q, qo)
+
+
+def test_set_variant_switches_kernel_mid_run():
+    """Switching the compiled variant between steps keeps the result bitwise identical."""
+    from paper_1410_1387_b200 import VTIError
+    cfg = small_cfg(70, 50, 40, 4, 4, damp=5, src=(30, 25, 20))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    with make(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        for ty, wp in ((32, 1), (16, -1), (32, 0), (32, 1)):
+            v.set_variant(ty, wp)
+            assert v.info()["tile_y"] == ty
+            v.step(4)
+        with pytest.raises(VTIError) as e:
+            v.set_variant(8, 1)
+        assert e.value.name == "VTI_E_UNSUPPORTED"
+        p, q = v.get_fields(0)
+    po, qo, _, _, _ = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=16)
+    assert np.array_equal(p, po) and np.array_equal(q, qo)
