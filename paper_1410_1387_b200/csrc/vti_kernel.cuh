@@ -96,6 +96,12 @@ struct StepParams {
     int ty_begin, ty_step, nty;          // tile rows ty_begin + t * ty_step, t < nty
     int zchunk, nzc;                     // planes per chunk, chunks
     int items;                           // ntx * nty * nzc
+    // Round alignment (cooperative launch only): CTAs arrive on *sync_ctr after
+    // each non-final round r and wait until it reaches sync_base + (r+1) * grid,
+    // so all CTAs start round r+1 together and neighbouring tiles stay within
+    // the L2 window of each other's p rows. NULL = no alignment.
+    unsigned long long *sync_ctr;
+    unsigned long long sync_base;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -150,6 +156,18 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
                      smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
@@ -299,7 +317,17 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
     int stage = 0;
     uint32_t phase = 0;
 
-    for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+    const int rounds = (P.items + gridDim.x - 1) / gridDim.x;
+    for (int item = blockIdx.x, round = 0; item < P.items; item += gridDim.x, ++round) {
+        if (round > 0 && P.sync_ctr) {
+            // align with every other CTA before the next round (see StepParams::sync_ctr)
+            named_bar_sync(1, NCONS_WARPS * 32);
+            if (threadIdx.x == 0) {
+                const unsigned long long target = P.sync_base + (unsigned long long)round * gridDim.x;
+                while (ld_acquire_u64(P.sync_ctr) < target) __nanosleep(64);
+            }
+            named_bar_sync(1, NCONS_WARPS * 32);
+        }
         int x0, y0, kb, ke;
         decode_item<TY>(P, item, x0, y0, kb, ke);
         const int xg = x0 + 4 * tx;   // first of this thread's 4 columns
@@ -432,6 +460,11 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                     }
                 }
             }
+        }
+        if (P.sync_ctr && round < rounds - 1) {
+            // every CTA arrives once per non-final round, whether or not it has another item
+            named_bar_sync(1, NCONS_WARPS * 32);
+            if (threadIdx.x == 0) atomicAdd(P.sync_ctr, 1ULL);
         }
     }
 }

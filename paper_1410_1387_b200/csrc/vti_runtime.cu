@@ -270,6 +270,9 @@ struct vti_s {
     size_t staging_floats = 0;
     unsigned long long *counters = nullptr;
     unsigned int *flag = nullptr;
+    unsigned long long *sync_ctr = nullptr;   // round-alignment counter (monotone across launches)
+    unsigned long long sync_value = 0;        // its value once all launched work has finished
+    bool align_rounds = true;                 // env VTI_ALIGN=0 disables
     int64_t device_bytes = 0;
     CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
     float cxy[MAX_R + 1] = {0};
@@ -502,6 +505,7 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->staging);
     cudaFree(h->counters);
     cudaFree(h->flag);
+    cudaFree(h->sync_ctr);
     for (cudaEvent_t e : {h->ev_edge, h->ev_comm, h->ev_t0, h->ev_t1})
         if (e) cudaEventDestroy(e);
     if (h->comm) cudaStreamDestroy(h->comm);
@@ -617,6 +621,8 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     if ((s = alloc(h, (void **)&h->vz2, bytes)) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->counters, 4 * sizeof(unsigned long long))) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->flag, sizeof(unsigned int))) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->sync_ctr, sizeof(unsigned long long))) != VTI_OK) return s;
+    if (const char *e = getenv("VTI_ALIGN")) h->align_rounds = atoi(e) != 0;
     if (cfg->nranks > 1) {
         const size_t hb = (size_t)cfg->nz * h->R * cfg->nx * 4;
         for (int b = 0; b < 2; ++b) {
@@ -833,8 +839,26 @@ static vti_status launch_rows(vti_s *h, int ty_begin, int ty_step, int nty_sel, 
     StepParams P;
     fill_params(h, P, ty_begin, ty_step, nty_sel, zchunk);
     const int grid = std::min(P.items, h->sms * h->ctas_per_sm);
-    void *args[] = {&P};
-    CU(h, cudaLaunchKernel((const void *)h->K->fn, dim3(grid), dim3(h->K->threads), args, h->smem_bytes, h->stream));
+    const int rounds = (P.items + grid - 1) / grid;
+    P.sync_ctr = nullptr;
+    P.sync_base = 0;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(h->K->threads);
+    lc.dynamicSmemBytes = h->smem_bytes;
+    lc.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    if (rounds > 1 && h->align_rounds) {
+        // all CTAs must be co-resident for the in-kernel round barrier: cooperative launch
+        P.sync_ctr = h->sync_ctr;
+        P.sync_base = h->sync_value;
+        h->sync_value += (unsigned long long)grid * (rounds - 1);
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+    }
+    CU(h, cudaLaunchKernelEx(&lc, h->K->fn, P));
     return VTI_OK;
 }
 
