@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--zchunk", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--precision", type=int, default=32, choices=[32, 64],
+                    help="64 = the fp64 path (SURVEY.md 8(f) N3, 72 B/point)")
     return ap.parse_args()
 
 
@@ -69,7 +71,7 @@ def workload(args, world):
     return cfg, scaling
 
 
-def describe(cfg, world, scaling):
+def describe(cfg, world, scaling, bpp=BYTES_PER_POINT):
     return {
         "workload": f"{cfg['name']}: {cfg['nx']}x{cfg['ny']}x{cfg['nz']} global, R_xy={cfg['r_xy']} R_z={cfg['r_z']}, "
                     f"{cfg['model']['kind']} VTI, W={cfg['damp_width']}, Ricker f={cfg['f']:g} Hz at the centre",
@@ -77,8 +79,8 @@ def describe(cfg, world, scaling):
         "r_xy": cfg["r_xy"], "r_z": cfg["r_z"], "config_steps": cfg["steps"],
         "decomposition": f"y-slabs x{world}" if world > 1 else "single GPU",
         "scaling": scaling,
-        "l2_flush": "not needed: per-step working set (36 B/pt) >> 126 MB L2",
-        "bytes_per_point": BYTES_PER_POINT,
+        "l2_flush": f"not needed: per-step working set ({bpp} B/pt) >> 126 MB L2",
+        "bytes_per_point": bpp,
     }
 
 
@@ -157,7 +159,7 @@ def ncu_traffic(cfg):
     return None
 
 
-def cpu_baseline(cfg, budget_s=12.0):
+def cpu_baseline(cfg, budget_s=12.0, precision=32):
     """The oracle as it stands, on this host's cores, on a bounded sample of the same workload."""
     import numpy as np
     import torch
@@ -166,8 +168,9 @@ def cpu_baseline(cfg, budget_s=12.0):
     import synth
     from synth import fields as SF
     oracle.build()
-    wxy, wz, _ = synth.weights_f32(cfg)
-    dt = synth.stable_dt(cfg, wxy, wz)
+    wxy, wz = weights(cfg, precision)
+    dt = synth.stable_dt(cfg)
+    dt_np = np.float32 if precision == 32 else np.float64
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     nz = cfg["nz"]
     model = [a.cpu().numpy() for a in SF.model_planes(cfg, 0, nz, device=dev)]
@@ -175,13 +178,13 @@ def cpu_baseline(cfg, budget_s=12.0):
              for s in range(4)]
     P = oracle.params(cfg, dt)
     npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    _, _, _, _, t1 = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=1)
+    _, _, _, _, t1 = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=1, dtype=dt_np)
     k = int(max(1, min(50, budget_s / max(t1, 1e-3))))
-    _, _, _, _, tk = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=k)
+    _, _, _, _, tk = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=k, dtype=dt_np)
     del model, state
     return {"value": round(npts * k / tk / 1e9, 6), "unit": "Gpoints/s", "cores": oracle.max_threads(),
             "kind": "oracle",
-            "sample": f"oracle fp32 (C, OpenMP) on the full {cfg['nx']}x{cfg['ny']}x{cfg['nz']} {cfg['name']} grid, "
+            "sample": f"oracle fp{precision} (C, OpenMP) on the full {cfg['nx']}x{cfg['ny']}x{cfg['nz']} {cfg['name']} grid, "
                       f"{k} time steps from a seeded random state (step loop only, {tk:.1f} s)"}
 
 
@@ -237,11 +240,24 @@ def run_reference(args):
     return 0
 
 
-def make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id):
+def make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id, precision=32):
     from paper_1410_1387_b200 import VTI
     return VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], cfg["r_xy"], cfg["r_z"], dt, wxy, wz,
                damp_width=cfg["damp_width"], damp_alpha=cfg["damp_alpha"], device=local, rank=rank,
-               nranks=world, nccl_id=nccl_id)
+               nranks=world, nccl_id=nccl_id, precision=precision)
+
+
+def weights(cfg, precision):
+    """float32 weights (the BASELINE path) or float64 weights for the fp64 path."""
+    import numpy as np
+
+    import synth
+    from synth import weights as W
+    if precision == 32:
+        wxy, wz, _ = synth.weights_f32(cfg)
+        return wxy, wz
+    zc = W.z_coords_ramp(cfg["nz"], cfg["r_z"], cfg["dz"][0], cfg["dz"][1])
+    return W.xy_weights(cfg["r_xy"]), np.ascontiguousarray(W.z_weights(zc, cfg["r_z"]))
 
 
 def set_model_from_device(v, cfg, chunk=64):
@@ -251,6 +267,8 @@ def set_model_from_device(v, cfg, chunk=64):
     for k0 in range(0, cfg["nz"], chunk):
         nk = min(chunk, cfg["nz"] - k0)
         m = SF.model_planes(cfg, k0, nk, device="cuda", j0=v.y0, nyl=v.ny_local)
+        if v.precision == 64:
+            m = [a.double() for a in m]
         v.set_model_planes(k0, *[a.contiguous() for a in m])
         del m
     torch.cuda.synchronize()
@@ -270,8 +288,10 @@ def run_native(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, scaling = workload(args, world)
-    wxy, wz, _ = synth.weights_f32(cfg)
-    dt = synth.stable_dt(cfg, wxy, wz)
+    prec = args.precision
+    bpp = BYTES_PER_POINT * prec // 32   # 36 B/point in fp32, 72 in fp64
+    wxy, wz = weights(cfg, prec)
+    dt = synth.stable_dt(cfg)
 
     nccl_id = None
     if world > 1:
@@ -292,7 +312,7 @@ def run_native(args):
         return float(t.item())
 
     npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    v = make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id)
+    v = make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id, prec)
     if args.zchunk or args.ctas_per_sm:
         v.set_tuning(args.zchunk, args.ctas_per_sm)
     set_model_from_device(v, cfg)
@@ -314,15 +334,16 @@ def run_native(args):
     pts_rank = cfg["nx"] * info["ny_local"] * cfg["nz"]
     # dominant kernel: the step kernel; at N = 1 one launch per step covers every point
     kern_ms = ms / args.steps
-    achieved = BYTES_PER_POINT * pts_rank / (kern_ms * 1e-3) / 1e9
+    achieved = bpp * pts_rank / (kern_ms * 1e-3) / 1e9
     peak, peak_src = peak_hbm()
-    traffic = ncu_traffic(cfg) if world == 1 else None
+    traffic = ncu_traffic(cfg) if world == 1 and prec == 32 else None
     v.close()
 
     e2e = None
     if not args.no_e2e:
         # through the public API with HOST buffers (pinned): model upload, K steps, read back u^K
-        pin = lambda shape: torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        tdt = torch.float32 if prec == 32 else torch.float64
+        pin = lambda shape: torch.empty(shape, dtype=tdt, pin_memory=True)
         shape = (cfg["nz"], info["ny_local"], cfg["nx"])
         host_model = [pin(shape) for _ in range(3)]
         from synth import fields as SF
@@ -332,7 +353,7 @@ def run_native(args):
             for dst, src in zip(host_model, m):
                 dst[k0:k0 + nk].copy_(src)
         out_p, out_q = pin(shape), pin(shape)
-        w = make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id)
+        w = make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id, prec)
         if args.zchunk or args.ctas_per_sm:
             w.set_tuning(args.zchunk, args.ctas_per_sm)
         barrier()
@@ -346,7 +367,7 @@ def run_native(args):
         barrier()
         te = max_over_ranks(te)
         w.close()
-        nbytes = 4 * cfg["nx"] * cfg["ny"] * cfg["nz"]
+        nbytes = (prec // 8) * cfg["nx"] * cfg["ny"] * cfg["nz"]
         e2e = {"value": round(npts * args.steps / te / 1e9, 4), "unit": "Gpoints/s",
                "h2d_bytes_per_step": int(3 * nbytes / args.steps), "d2h_bytes_per_step": int(2 * nbytes / args.steps),
                "what": "vti_set_model (pinned host) + vti_add_source + vti_step(K) + vti_get_fields(u^K to pinned host), wall clock, max over ranks"}
@@ -354,19 +375,19 @@ def run_native(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
+        cpu = cpu_baseline(cfg, precision=prec)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": "Gpoints/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 5),
-            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": f"f{prec}",
             "data": "synthetic (seeded layered VTI model generated on device; zero initial state + Ricker source)",
-            "config": describe(cfg, world, scaling),
+            "config": describe(cfg, world, scaling, bpp),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "vti::vti_step_kernel<4,4>" if cfg["r_xy"] == 4 else f"vti::vti_step_kernel<{cfg['r_xy']},{cfg['r_z']}>",
-                         "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts_rank},
+                         "algorithmic_bytes_per_launch": bpp * pts_rank},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,

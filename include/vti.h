@@ -23,8 +23,12 @@
  *  - User layout of every 3-D array: [z][y][x], x fastest,
  *    interior points only (no halo, no padding). With nranks > 1 an array
  *    covers this rank's y-slab only: [nz][ny_local][nx] (see vti_slab).
- *  - Precision: fp32 storage and arithmetic in a fixed "canonical" operation
- *    order (reading c12), so results are bitwise reproducible.
+ *  - Precision: fp32 (default; the BASELINE.json path) or fp64 (cfg.precision
+ *    = 64) storage and arithmetic, in one fixed "canonical"
+ *    operation order (reading c12), so results are bitwise
+ *    reproducible. Array entry points come in pairs: the plain name takes
+ *    float*, the _f64 name double*; calling the other precision's entry point
+ *    is VTI_E_PARAM.
  *  - Threading: a handle is single-writer; calls on one handle must not race.
  *  - Asynchrony: vti_step enqueues work on the handle's stream and returns;
  *    vti_get_fields / vti_sync synchronise.
@@ -38,7 +42,7 @@
 extern "C" {
 #endif
 
-#define VTI_ABI_VERSION 1
+#define VTI_ABI_VERSION 2
 
 typedef struct vti_s *vti_t;
 
@@ -69,6 +73,7 @@ typedef struct {
     const void *nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (nranks > 1);
                                NULL with nranks > 1 = "local group" mode (vti_group_step) */
     int32_t check_every;    /* > 0: test for non-finite values every this many steps */
+    int32_t precision;      /* 32 (or 0) = fp32, 64 = fp64 */
 } vti_config;
 
 typedef struct {
@@ -109,6 +114,10 @@ vti_status vti_nccl_unique_id(void *out128);
  */
 vti_status vti_create(vti_t *out, const vti_config *cfg, const float *w_xy, const float *w_z);
 
+/* Same with double weights; needs cfg->precision = 64 (with vti_create an
+ * fp64 handle gets the float weights widened exactly). */
+vti_status vti_create_f64(vti_t *out, const vti_config *cfg, const double *w_xy, const double *w_z);
+
 /* Upload this rank's model slab (vx2 = nu_x^2, vn2 = nu_n^2, vz2 = nu_z^2 [m^2/s^2],
  * PAPER.md l.39-43), each [nz][ny_local][nx]. Errors: PARAM (NULL), MODEL
  * (vz2 <= 0 or non-finite anywhere), CUDA. vn2 > vx2 (eps < delta) is
@@ -118,6 +127,9 @@ vti_status vti_set_model(vti_t h, const float *vx2, const float *vn2, const floa
 /* Same for planes [k0, k0+nk) only: arrays are [nk][ny_local][nx]. */
 vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx2,
                                 const float *vn2, const float *vz2);
+vti_status vti_set_model_f64(vti_t h, const double *vx2, const double *vn2, const double *vz2);
+vti_status vti_set_model_planes_f64(vti_t h, int32_t k0, int32_t nk, const double *vx2,
+                                    const double *vn2, const double *vz2);
 
 /* Points with vn2 > vx2 (eps < delta) seen by vti_set_model* so far. */
 int64_t vti_model_warnings(vti_t h);
@@ -142,6 +154,10 @@ vti_status vti_set_fields(vti_t h, const float *p, const float *q, const float *
 /* Planes [k0, k0+nk) of the state (time index unchanged; pm/qm may be NULL = zero). */
 vti_status vti_set_fields_planes(vti_t h, int32_t k0, int32_t nk, const float *p, const float *q,
                                  const float *pm, const float *qm);
+vti_status vti_set_fields_f64(vti_t h, const double *p, const double *q, const double *pm,
+                              const double *qm, int64_t time_index);
+vti_status vti_set_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, const double *p, const double *q,
+                                     const double *pm, const double *qm);
 
 /* Advance nsteps time steps (async on the handle's stream). With nranks > 1
  * and an nccl_id, every rank must call it with the same nsteps (NCCL halo
@@ -166,6 +182,8 @@ vti_status vti_get_fields(vti_t h, float *p, float *q, int32_t level);
 
 /* Planes [k0, k0+nk) of vti_get_fields. */
 vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level);
+vti_status vti_get_fields_f64(vti_t h, double *p, double *q, int32_t level);
+vti_status vti_get_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, double *p, double *q, int32_t level);
 
 /* Block until all work on the handle's stream(s) is done. */
 vti_status vti_sync(vti_t h);

@@ -41,7 +41,7 @@ class Config(C.Structure):
         ("h", C.c_double), ("r_xy", C.c_int32), ("r_z", C.c_int32), ("dt", C.c_double),
         ("damp_width", C.c_int32), ("damp_alpha", C.c_double), ("device", C.c_int32),
         ("stream", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
-        ("nccl_id", C.c_void_p), ("check_every", C.c_int32),
+        ("nccl_id", C.c_void_p), ("check_every", C.c_int32), ("precision", C.c_int32),
     ]
 
 
@@ -79,6 +79,13 @@ def _load():
         "vti_slab": (st, [C.POINTER(Config), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "vti_nccl_unique_id": (st, [P]),
         "vti_create": (st, [C.POINTER(H), C.POINTER(Config), P, P]),
+        "vti_create_f64": (st, [C.POINTER(H), C.POINTER(Config), P, P]),
+        "vti_set_model_f64": (st, [H, P, P, P]),
+        "vti_set_model_planes_f64": (st, [H, C.c_int32, C.c_int32, P, P, P]),
+        "vti_set_fields_f64": (st, [H, P, P, P, P, C.c_int64]),
+        "vti_set_fields_planes_f64": (st, [H, C.c_int32, C.c_int32, P, P, P, P]),
+        "vti_get_fields_f64": (st, [H, P, P, C.c_int32]),
+        "vti_get_fields_planes_f64": (st, [H, C.c_int32, C.c_int32, P, P, C.c_int32]),
         "vti_set_model": (st, [H, P, P, P]),
         "vti_set_model_planes": (st, [H, C.c_int32, C.c_int32, P, P, P]),
         "vti_model_warnings": (C.c_int64, [H]),
@@ -113,26 +120,27 @@ for _n in EXPORTS:
     globals()[_n] = getattr(lib, _n)
 
 
-def _ptr(a, nelem: int | None = None, writable: bool = False):
-    """Raw pointer of a float32 C-contiguous numpy array or torch tensor (None -> NULL)."""
+def _ptr(a, nelem: int | None = None, writable: bool = False, dtype=np.float32):
+    """Raw pointer of a C-contiguous numpy array or torch tensor of ``dtype`` (None -> NULL)."""
     if a is None:
         return None, None
     try:
         import torch
         if isinstance(a, torch.Tensor):
-            if a.dtype != torch.float32 or not a.is_contiguous():
-                raise TypeError("torch tensors must be float32 and contiguous")
+            tdt = torch.float32 if dtype == np.float32 else torch.float64
+            if a.dtype != tdt or not a.is_contiguous():
+                raise TypeError(f"torch tensors must be {tdt} and contiguous")
             if nelem is not None and a.numel() != nelem:
                 raise ValueError(f"expected {nelem} elements, got {a.numel()}")
             return a.data_ptr(), a
     except ImportError:
         pass
     if writable:
-        if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous):
-            raise TypeError("output arrays must be float32 C-contiguous numpy arrays or torch tensors")
+        if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous):
+            raise TypeError(f"output arrays must be {np.dtype(dtype).name} C-contiguous numpy arrays or torch tensors")
         arr = a
     else:
-        arr = np.ascontiguousarray(a, dtype=np.float32)
+        arr = np.ascontiguousarray(a, dtype=dtype)
     if nelem is not None and arr.size != nelem:
         raise ValueError(f"expected {nelem} elements, got {arr.size}")
     return arr.ctypes.data, arr
@@ -163,18 +171,27 @@ class VTI:
 
     def __init__(self, nx, ny, nz, h, r_xy, r_z, dt, w_xy, w_z, damp_width=20, damp_alpha=0.015,
                  device=0, stream=None, rank=0, nranks=1, nccl_id: bytes | None = None,
-                 check_every=0):
+                 check_every=0, precision=32):
+        if precision not in (32, 64):
+            raise ValueError("precision must be 32 or 64")
+        self.precision = precision
+        self.dtype = np.float32 if precision == 32 else np.float64
+        self._sfx = "" if precision == 32 else "_f64"
         self._id_buf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         self.cfg = Config(nx=nx, ny=ny, nz=nz, h=h, r_xy=r_xy, r_z=r_z, dt=dt, damp_width=damp_width,
                           damp_alpha=damp_alpha, device=device, stream=stream, rank=rank, nranks=nranks,
                           nccl_id=C.cast(self._id_buf, C.c_void_p) if self._id_buf is not None else None,
-                          check_every=check_every)
-        wxy_p, self._wxy = _ptr(w_xy, r_xy + 1)
-        wz_p, self._wz = _ptr(w_z, nz * (2 * r_z + 1))
+                          check_every=check_every, precision=precision)
+        wxy_p, self._wxy = _ptr(w_xy, r_xy + 1, dtype=self.dtype)
+        wz_p, self._wz = _ptr(w_z, nz * (2 * r_z + 1), dtype=self.dtype)
         self.h = C.c_void_p()
-        _check(None, lib.vti_create(C.byref(self.h), C.byref(self.cfg), wxy_p, wz_p))
+        create = lib.vti_create if precision == 32 else lib.vti_create_f64
+        _check(None, create(C.byref(self.h), C.byref(self.cfg), wxy_p, wz_p))
         self.y0, self.ny_local = slab(ny, rank, nranks)
         self.nx, self.ny, self.nz = nx, ny, nz
+
+    def _fn(self, name):
+        return getattr(lib, name + self._sfx)
 
     # -- lifecycle
     def close(self):
@@ -199,13 +216,13 @@ class VTI:
         return (self.nz if nk is None else nk) * self.ny_local * self.nx
 
     def set_model(self, vx2, vn2, vz2):
-        a = [_ptr(x, self._n()) for x in (vx2, vn2, vz2)]
-        _check(self.h, lib.vti_set_model(self.h, a[0][0], a[1][0], a[2][0]))
+        a = [_ptr(x, self._n(), dtype=self.dtype) for x in (vx2, vn2, vz2)]
+        _check(self.h, self._fn("vti_set_model")(self.h, a[0][0], a[1][0], a[2][0]))
 
     def set_model_planes(self, k0, vx2, vn2, vz2):
         nk = (vx2.shape[0] if hasattr(vx2, "shape") else len(vx2))
-        a = [_ptr(x, self._n(nk)) for x in (vx2, vn2, vz2)]
-        _check(self.h, lib.vti_set_model_planes(self.h, k0, nk, a[0][0], a[1][0], a[2][0]))
+        a = [_ptr(x, self._n(nk), dtype=self.dtype) for x in (vx2, vn2, vz2)]
+        _check(self.h, self._fn("vti_set_model_planes")(self.h, k0, nk, a[0][0], a[1][0], a[2][0]))
 
     def model_warnings(self) -> int:
         return lib.vti_model_warnings(self.h)
@@ -214,13 +231,13 @@ class VTI:
         _check(self.h, lib.vti_add_source(self.h, i, j, k, f, t0, amp, mask))
 
     def set_fields(self, p, q, pm=None, qm=None, time_index=0):
-        a = [_ptr(x, self._n()) for x in (p, q, pm, qm)]
-        _check(self.h, lib.vti_set_fields(self.h, a[0][0], a[1][0], a[2][0], a[3][0], time_index))
+        a = [_ptr(x, self._n(), dtype=self.dtype) for x in (p, q, pm, qm)]
+        _check(self.h, self._fn("vti_set_fields")(self.h, a[0][0], a[1][0], a[2][0], a[3][0], time_index))
 
     def set_fields_planes(self, k0, p, q, pm=None, qm=None):
         nk = p.shape[0]
-        a = [_ptr(x, self._n(nk)) for x in (p, q, pm, qm)]
-        _check(self.h, lib.vti_set_fields_planes(self.h, k0, nk, a[0][0], a[1][0], a[2][0], a[3][0]))
+        a = [_ptr(x, self._n(nk), dtype=self.dtype) for x in (p, q, pm, qm)]
+        _check(self.h, self._fn("vti_set_fields_planes")(self.h, k0, nk, a[0][0], a[1][0], a[2][0], a[3][0]))
 
     # -- stepping
     def step(self, nsteps=1):
@@ -240,12 +257,12 @@ class VTI:
         k0, nk = (0, self.nz) if planes is None else planes
         shape = (nk, self.ny_local, self.nx)
         if p is None:
-            p = np.empty(shape, dtype=np.float32)
+            p = np.empty(shape, dtype=self.dtype)
         if q is None:
-            q = np.empty(shape, dtype=np.float32)
-        pp, _ = _ptr(p, self._n(nk), writable=True)
-        qp, _ = _ptr(q, self._n(nk), writable=True)
-        _check(self.h, lib.vti_get_fields_planes(self.h, k0, nk, pp, qp, level))
+            q = np.empty(shape, dtype=self.dtype)
+        pp, _ = _ptr(p, self._n(nk), writable=True, dtype=self.dtype)
+        qp, _ = _ptr(q, self._n(nk), writable=True, dtype=self.dtype)
+        _check(self.h, self._fn("vti_get_fields_planes")(self.h, k0, nk, pp, qp, level))
         return p, q
 
     @property

@@ -44,17 +44,19 @@ __host__ __device__ constexpr int nthreads(int ty, int rpt, int wp) { return (co
 
 __host__ __device__ constexpr int align128(int b) { return (b + 127) / 128 * 128; }
 
-template <int R, int RZ, int TY>
+// T = float (the fp32 path of BASELINE.json) or double.
+template <typename T, int R, int RZ, int TY>
 struct Cfg {
-    // x apron rounded up to 4 floats: the TMA box must start on a 16-byte
-    // boundary in x (x0 - RA), and every shared-memory read is then a float4.
+    // x apron rounded up to 4 elements: the TMA box must start on a 16-byte
+    // boundary in x (x0 - RA), and every shared-memory read is then a 4-vector.
     static constexpr int RA = (R + 3) / 4 * 4;
+    static constexpr int ES = (int)sizeof(T);
     static constexpr int PW = TX + 2 * RA;                // p tile row length (floats)
     static constexpr int PH = TY + 2 * R;                 // p tile rows
     static constexpr int NQ = 2 * RZ + 1;                 // q queue depth
-    static constexpr int ZROW = ((NQ + 1 + 3) / 4) * 4;   // w^z row + gz, padded to 16 B
-    static constexpr int P_BYTES = PW * PH * 4;
-    static constexpr int S_BYTES = TX * TY * 4;
+    static constexpr int ZROW = ((NQ + 1 + 3) / 4) * 4;   // w^z row + gz, padded to 4 elements
+    static constexpr int P_BYTES = PW * PH * ES;
+    static constexpr int S_BYTES = TX * TY * ES;
     static constexpr int OFF_P = 0;
     static constexpr int OFF_Q = align128(P_BYTES);
     static constexpr int OFF_PM = OFF_Q + S_BYTES;
@@ -63,16 +65,17 @@ struct Cfg {
     static constexpr int OFF_VN = OFF_VX + S_BYTES;
     static constexpr int OFF_VZ = OFF_VN + S_BYTES;
     static constexpr int OFF_ZR = OFF_VZ + S_BYTES;
-    static constexpr int STAGE = align128(OFF_ZR + ZROW * 4);
-    static constexpr uint32_t FULL_TX = P_BYTES + 6 * S_BYTES + ZROW * 4;
+    static constexpr int STAGE = align128(OFF_ZR + ZROW * ES);
+    static constexpr uint32_t FULL_TX = P_BYTES + 6 * S_BYTES + ZROW * ES;
     static constexpr uint32_t PRIME_TX = S_BYTES;
-    static_assert(PW % 4 == 0, "p tile rows must be 16-byte multiples");
+    static_assert(PW % 4 == 0, "p tile rows must be whole 4-vectors");
     static_assert(PW <= 256 && PH <= 256, "TMA box limit");
 };
 
 // All arrays share one geometry: nz planes x (nyl + 2R) rows x nxp floats with
 // strides ys (row) and zs (plane) in floats; R halo rows on both y sides (only
 // p's are ever non-zero). Tensor-map dims are ordered (x, y, z).
+template <typename T>
 struct StepParams {
     CUtensorMap tm_p;    // p^n  : halo'd view dims {nx, nyl + 2R, nz}, box {TX + 2RA, TY + 2R, 1}
     CUtensorMap tm_q;    // q^n  : interior view dims {nx, nyl, nz}, box {TX, TY, 1}
@@ -81,21 +84,21 @@ struct StepParams {
     CUtensorMap tm_vx;   // vx2
     CUtensorMap tm_vn;   // vn2
     CUtensorMap tm_vz;   // vz2
-    float *p_out;        // p^{n+1}: interior row 0, plane 0 of the other p buffer
-    float *q_out;        // q^{n+1}: interior row 0, plane 0 of the other q buffer
-    const float *zrow;   // [nz][ZROW]: w^z[k][0..2Rz], gz[k], 0 ...
-    const float *gx;     // [ntx * TX] (1 beyond nx)
-    const float *gy;     // [nyl] local rows
-    float cxy[MAX_R + 1];
-    float dt2;
-    float s;             // s(t^n) this step
+    T *p_out;            // p^{n+1}: interior row 0, plane 0 of the other p buffer
+    T *q_out;            // q^{n+1}: interior row 0, plane 0 of the other q buffer
+    const T *zrow;       // [nz][ZROW]: w^z[k][0..2Rz], gz[k], 0 ...
+    const T *gx;         // [ntx * TX] (1 beyond nx)
+    const T *gy;         // [nyl] local rows
+    T cxy[MAX_R + 1];
+    T dt2;
+    T s;                 // s(t^n) this step
     int src_i, src_j, src_k, src_mask;   // local indices; src_mask = 0: no source here
     int nx, nyl, nz;
-    long long ys, zs;                    // row / plane strides (floats)
+    long long ys, zs;                    // row / plane strides (elements)
     int ntx;                             // tiles along x
-    int ty_begin, ty_step, nty;          // tile rows ty_begin + t * ty_step, t < nty
+    int tr0, ntr0, tr1, ntr1;            // tile rows [tr0, tr0+ntr0) then [tr1, tr1+ntr1)
     int zchunk, nzc;                     // planes per chunk, chunks
-    int items;                           // ntx * nty * nzc
+    int items;                           // ntx * (ntr0 + ntr1) * nzc
     // Round alignment (cooperative launch only): CTAs arrive on *sync_ctr after
     // each non-final round r and wait until it reaches sync_base + (r+1) * grid,
     // so all CTAs start round r+1 together and neighbouring tiles stay within
@@ -175,23 +178,49 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
 }
 
-__device__ __forceinline__ float4 lds4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
-__device__ __forceinline__ float2 lds2(const float *p) { return *reinterpret_cast<const float2 *>(p); }
+// 4 consecutive elements: one float4, or two double2 (32 B) for fp64.
+template <typename T> struct V4;
+template <> struct V4<float> {
+    float4 v;
+    __device__ __forceinline__ float operator[](int c) const { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
+};
+template <> struct V4<double> {
+    double2 a, b;
+    __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : c == 1 ? a.y : c == 2 ? b.x : b.y; }
+};
 
-__device__ __forceinline__ float f4(const float4 &v, int c)
+__device__ __forceinline__ V4<float> lds4(const float *p) { return V4<float>{*reinterpret_cast<const float4 *>(p)}; }
+__device__ __forceinline__ V4<double> lds4(const double *p)
 {
-    return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+    return V4<double>{reinterpret_cast<const double2 *>(p)[0], reinterpret_cast<const double2 *>(p)[1]};
 }
-
-template <int TY>
-__device__ __forceinline__ void decode_item(const StepParams &P, int item, int &x0, int &y0, int &kb, int &ke)
+__device__ __forceinline__ V4<float> ldg4(const float *p) { return V4<float>{*reinterpret_cast<const float4 *>(p)}; }
+__device__ __forceinline__ V4<double> ldg4(const double *p)
 {
+    return V4<double>{reinterpret_cast<const double2 *>(p)[0], reinterpret_cast<const double2 *>(p)[1]};
+}
+__device__ __forceinline__ void stg4(float *p, const float (&v)[4])
+{
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void stg4(double *p, const double (&v)[4])
+{
+    reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <int TY, typename PP>
+__device__ __forceinline__ void decode_item(const PP &P, int item, int &x0, int &y0, int &kb, int &ke)
+{
+    const int nsel = P.ntr0 + P.ntr1;
     const int tx = item % P.ntx;
     const int rest = item / P.ntx;
-    const int t = rest % P.nty;
-    const int zc = rest / P.nty;
+    const int t = rest % nsel;
+    const int zc = rest / nsel;
     x0 = tx * TX;
-    y0 = (P.ty_begin + t * P.ty_step) * TY;   // local row of the tile's first row
+    y0 = (t < P.ntr0 ? P.tr0 + t : P.tr1 + (t - P.ntr0)) * TY;   // local row of the tile's first row
     kb = zc * P.zchunk;
     ke = min(P.nz, kb + P.zchunk);
 }
@@ -199,13 +228,13 @@ __device__ __forceinline__ void decode_item(const StepParams &P, int item, int &
 // The flat sequence of stage loads of one CTA: for each of its work items,
 // 2Rz priming loads (q only) then one full load per plane. Driven by a
 // single thread; load j goes to stage j % STAGES.
-template <int R, int RZ, int TY, int STAGES>
+template <typename T, int R, int RZ, int TY, int STAGES>
 struct Producer {
     int item, t, nload, x0, y0, kb, ke;
     int stage;
     uint32_t phase;
 
-    __device__ __forceinline__ void start(const StepParams &P)
+    __device__ __forceinline__ void start(const StepParams<T> &P)
     {
         item = blockIdx.x;
         t = 0;
@@ -217,9 +246,9 @@ struct Producer {
         }
     }
 
-    __device__ __forceinline__ void issue(const StepParams &P, uint8_t *smem, uint64_t *full, uint64_t *empty)
+    __device__ __forceinline__ void issue(const StepParams<T> &P, uint8_t *smem, uint64_t *full, uint64_t *empty)
     {
-        using C = Cfg<R, RZ, TY>;
+        using C = Cfg<T, R, RZ, TY>;
         constexpr int RA = C::RA;
         if (item >= P.items) return;
         mbar_wait(&empty[stage], phase ^ 1);   // every warp released the previous load of this stage
@@ -241,7 +270,7 @@ struct Producer {
             tma_load_3d(st + C::OFF_VX, &P.tm_vx, x0, y0, k, bar);
             tma_load_3d(st + C::OFF_VN, &P.tm_vn, x0, y0, k, bar);
             tma_load_3d(st + C::OFF_VZ, &P.tm_vz, x0, y0, k, bar);
-            bulk_load(st + C::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * 4, bar);
+            bulk_load(st + C::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * C::ES, bar);
         }
         if (++stage == STAGES) {
             stage = 0;
@@ -263,10 +292,10 @@ struct Producer {
 //         on the ring); 17 warps per TY=32 CTA cap registers at 96.
 // WP = 0: the CTA's first thread issues load j + STAGES right after releasing
 //         load j; 16 warps allow 128 registers (needed for the R_z >= 6 queues).
-template <int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB>
-__global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(const __grid_constant__ StepParams P)
+template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB>
+__global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(const __grid_constant__ StepParams<T> P)
 {
-    using C = Cfg<R, RZ, TY>;
+    using C = Cfg<T, R, RZ, TY>;
     constexpr int NCONS_WARPS = cons_warps(TY, RPT);
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
@@ -279,7 +308,7 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
     const int lane = threadIdx.x & 31;
 
     const bool leader = (WP == 0) && threadIdx.x == 0;
-    Producer<R, RZ, TY, STAGES> prod;
+    Producer<T, R, RZ, TY, STAGES> prod;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -331,18 +360,16 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
         int x0, y0, kb, ke;
         decode_item<TY>(P, item, x0, y0, kb, ke);
         const int xg = x0 + 4 * tx;   // first of this thread's 4 columns
-        const float4 g4 = *reinterpret_cast<const float4 *>(P.gx + xg);
-        float gxy[RPT][4];
+        const V4<T> g4 = ldg4(P.gx + xg);
+        T gxy[RPT][4];
         bool store_ok[RPT], src_col[RPT];
-        float *pout[RPT], *qout[RPT];
+        T *pout[RPT], *qout[RPT];
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
             const int yl = y0 + tg * RPT + r;   // local row
-            const float gyv = (yl < P.nyl) ? P.gy[yl] : 0.f;
-            gxy[r][0] = g4.x * gyv;
-            gxy[r][1] = g4.y * gyv;
-            gxy[r][2] = g4.z * gyv;
-            gxy[r][3] = g4.w * gyv;
+            const T gyv = (yl < P.nyl) ? P.gy[yl] : T(0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) gxy[r][c] = g4[c] * gyv;
             store_ok[r] = (yl < P.nyl) && (xg < P.nx);
             src_col[r] = P.src_mask != 0 && P.src_j == yl && P.src_i >= xg && P.src_i < xg + 4;
             pout[r] = P.p_out + (long long)yl * P.ys + xg;
@@ -351,14 +378,14 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
         const int src_c = P.src_i - xg;
         const int sidx = tg * RPT * TX + 4 * tx;   // float offset of row 0 in a stream tile
 
-        float4 q[RPT][NQ];
+        V4<T> q[RPT][NQ];
         // prime the queue with q(kb - Rz .. kb + Rz - 1)
 #pragma unroll
         for (int t = 0; t < 2 * RZ; ++t) {
             mbar_wait(&full[stage], phase);
-            const float *st = reinterpret_cast<const float *>(smem + stage * C::STAGE);
+            const T *st = reinterpret_cast<const T *>(smem + stage * C::STAGE);
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) q[r][t] = lds4(st + C::OFF_Q / 4 + sidx + r * TX);
+            for (int r = 0; r < RPT; ++r) q[r][t] = lds4(st + C::OFF_Q / C::ES + sidx + r * TX);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (leader) prod.issue(P, smem, full, empty);
@@ -374,23 +401,23 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                 const int k = kbase + u;
                 if (k < ke) {
                     mbar_wait(&full[stage], phase);
-                    const float *st = reinterpret_cast<const float *>(smem + stage * C::STAGE);
+                    const T *st = reinterpret_cast<const T *>(smem + stage * C::STAGE);
 #pragma unroll
                     for (int r = 0; r < RPT; ++r)
-                        q[r][(u + 2 * RZ) % NQ] = lds4(st + C::OFF_Q / 4 + sidx + r * TX);   // q^n(k + Rz)
-                    const float *ps = st + C::OFF_P / 4;
+                        q[r][(u + 2 * RZ) % NQ] = lds4(st + C::OFF_Q / C::ES + sidx + r * TX);   // q^n(k + Rz)
+                    const T *ps = st + C::OFF_P / C::ES;
                     // smem row of tile row tg*RPT - R is tg*RPT; x window starts at x0 + 4tx - RA
-                    const float *pbase = ps + tg * RPT * C::PW + 4 * tx;
+                    const T *pbase = ps + tg * RPT * C::PW + 4 * tx;
                     // Eq. 4 / h^2, canonical order: L = c0 p; L = fma(c_l, xpair + ypair, L)
-                    float L[RPT][4];
-                    float pc[RPT][4];   // p^n at the points (2 u^n term)
+                    T L[RPT][4];
+                    T pc[RPT][4];   // p^n at the points (2 u^n term)
 #pragma unroll
                     for (int r = 0; r < RPT; ++r) {
                         // x window of row r: floats [4tx, 4tx + 4 + 2RA) of smem row r + R, read
                         // as float4 chunks at the point of use (identical loads are CSE'd), so
                         // only the chunks of the current radius stay live
-                        const float *prow = pbase + (r + R) * C::PW;
-                        auto wx = [&](int i) { return f4(lds4(prow + 4 * (i / 4)), i % 4); };
+                        const T *prow = pbase + (r + R) * C::PW;
+                        auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             pc[r][c] = wx(RA + c);
@@ -399,46 +426,45 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
 #pragma unroll
                         for (int l = 1; l <= R; ++l) {
                             // y neighbours of row r at distance l: smem rows r+R+l, r+R-l at x offset RA
-                            const float4 yp = lds4(pbase + (r + R + l) * C::PW + RA);
-                            const float4 ym = lds4(pbase + (r + R - l) * C::PW + RA);
+                            const V4<T> yp = lds4(pbase + (r + R + l) * C::PW + RA);
+                            const V4<T> ym = lds4(pbase + (r + R - l) * C::PW + RA);
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
-                                const float xpair = wx(RA + c + l) + wx(RA + c - l);
-                                const float ypair = f4(yp, c) + f4(ym, c);
-                                L[r][c] = __fmaf_rn(P.cxy[l], xpair + ypair, L[r][c]);
+                                const T xpair = wx(RA + c + l) + wx(RA + c - l);
+                                const T ypair = yp[c] + ym[c];
+                                L[r][c] = fma_rn(P.cxy[l], xpair + ypair, L[r][c]);
                             }
                         }
                     }
                     // stage data below is read at the point of use (register pressure at
                     // R_z >= 6); the stage is released after the last shared-memory read
-                    const float *zr = st + C::OFF_ZR / 4;
-                    const float gz = zr[NQ];
-                    float pn[RPT][4], qn[RPT][4];
+                    const T *zr = st + C::OFF_ZR / C::ES;
+                    const T gz = zr[NQ];
+                    T pn[RPT][4], qn[RPT][4];
 #pragma unroll
                     for (int r = 0; r < RPT; ++r) {
-                        const float4 pm4 = lds4(st + C::OFF_PM / 4 + sidx + r * TX);
-                        const float4 qm4 = lds4(st + C::OFF_QM / 4 + sidx + r * TX);
-                        const float4 vx4 = lds4(st + C::OFF_VX / 4 + sidx + r * TX);
-                        const float4 vn4 = lds4(st + C::OFF_VN / 4 + sidx + r * TX);
-                        const float4 vz4 = lds4(st + C::OFF_VZ / 4 + sidx + r * TX);
+                        const V4<T> pm4 = lds4(st + C::OFF_PM / C::ES + sidx + r * TX);
+                        const V4<T> qm4 = lds4(st + C::OFF_QM / C::ES + sidx + r * TX);
+                        const V4<T> vx4 = lds4(st + C::OFF_VX / C::ES + sidx + r * TX);
+                        const V4<T> vn4 = lds4(st + C::OFF_VN / C::ES + sidx + r * TX);
+                        const V4<T> vz4 = lds4(st + C::OFF_VZ / C::ES + sidx + r * TX);
                         const bool src_here = src_col[r] && (k == P.src_k);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
-                            float D = zr[0] * f4(q[r][u % NQ], c);
+                            T D = zr[0] * q[r][u % NQ][c];
 #pragma unroll
-                            for (int m = 1; m < NQ; ++m) D = __fmaf_rn(zr[m], f4(q[r][(u + m) % NQ], c), D);
-                            const float vD = f4(vz4, c) * D;
-                            float Fp = __fmaf_rn(f4(vx4, c), L[r][c], vD);
-                            float Fq = __fmaf_rn(f4(vn4, c), L[r][c], vD);
+                            for (int m = 1; m < NQ; ++m) D = fma_rn(zr[m], q[r][(u + m) % NQ][c], D);
+                            const T vD = vz4[c] * D;
+                            T Fp = fma_rn(vx4[c], L[r][c], vD);
+                            T Fq = fma_rn(vn4[c], L[r][c], vD);
                             if (src_here && c == src_c) {
                                 if (P.src_mask & 1) Fp = Fp + P.s;
                                 if (P.src_mask & 2) Fq = Fq + P.s;
                             }
-                            const float g = gxy[r][c] * gz;   // (gx gy) gz
-                            pn[r][c] = g * __fmaf_rn(P.dt2, Fp, __fmaf_rn(-g, f4(pm4, c), 2.0f * pc[r][c]));
-                            qn[r][c] = g * __fmaf_rn(P.dt2, Fq,
-                                                     __fmaf_rn(-g, f4(qm4, c), 2.0f * f4(q[r][(u + RZ) % NQ], c)));
+                            const T g = gxy[r][c] * gz;   // (gx gy) gz
+                            pn[r][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[r][c]));
+                            qn[r][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * q[r][(u + RZ) % NQ][c]));
                         }
                     }
                     __syncwarp();
@@ -452,10 +478,8 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                     for (int r = 0; r < RPT; ++r) {
                         if (store_ok[r]) {
                             const long long off = (long long)k * P.zs;
-                            *reinterpret_cast<float4 *>(pout[r] + off) =
-                                make_float4(pn[r][0], pn[r][1], pn[r][2], pn[r][3]);
-                            *reinterpret_cast<float4 *>(qout[r] + off) =
-                                make_float4(qn[r][0], qn[r][1], qn[r][2], qn[r][3]);
+                            stg4(pout[r] + off, pn[r]);
+                            stg4(qout[r] + off, qn[r]);
                         }
                     }
                 }

@@ -33,7 +33,7 @@ typedef struct {
     char internal[128];
 } ncclUniqueId;
 typedef enum { ncclSuccess = 0 } ncclResult_t;
-typedef enum { ncclFloat32 = 7 } ncclDataType_t;
+typedef enum { ncclFloat32 = 7, ncclFloat64 = 8 } ncclDataType_t;
 
 struct NcclApi {
     bool ok = false;
@@ -103,42 +103,57 @@ static PFN_encodeTiled get_encode()
     return fn;
 }
 
+
 // ============================================================ kernel table
+// Element-type-erased entry: fn is a vti_step_kernel<T, ...> instantiation,
+// launched through cudaLaunchKernelExC with a StepParams<T> argument.
 struct KernelEntry {
-    int r, rz, ty, rpt, wp, stages, minb, stage_bytes;
-    void (*fn)(StepParams);
+    int esize, r, rz, ty, rpt, wp, stages, minb, stage_bytes;
+    const void *fn;
     int zrow;
     int threads;
 };
 
-template <int R, int RZ, int TY, int RPT, int WP, int S, int B>
+template <typename T, int R, int RZ, int TY, int RPT, int WP, int S, int B>
 static KernelEntry entry()
 {
-    return KernelEntry{R, RZ, TY, RPT, WP, S, B, Cfg<R, RZ, TY>::STAGE, vti_step_kernel<R, RZ, TY, RPT, WP, S, B>,
-                       Cfg<R, RZ, TY>::ZROW, nthreads(TY, RPT, WP)};
+    return KernelEntry{(int)sizeof(T), R, RZ, TY, RPT, WP, S, B, Cfg<T, R, RZ, TY>::STAGE,
+                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B>, Cfg<T, R, RZ, TY>::ZROW,
+                       nthreads(TY, RPT, WP)};
 }
 
-// Compiled variants; the first match is the default for a radius pair.
-// -1 = any (env VTI_TY, VTI_WP select the others for experiments).
-static const KernelEntry *find_kernel(int r, int rz, int ty, int wp)
+// Compiled variants; the first match is the default for (precision, radius pair).
+// -1 = any (env VTI_TY, VTI_WP or vti_set_variant select the others).
+static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp)
 {
     static const KernelEntry table[] = {
-        entry<4, 4, 32, 1, 1, 3, 1>(),  entry<4, 4, 32, 1, 0, 3, 1>(),  entry<4, 4, 16, 1, 1, 3, 2>(),
-        entry<8, 4, 32, 1, 1, 3, 1>(),  entry<8, 4, 32, 1, 0, 3, 1>(),  entry<8, 4, 16, 1, 1, 3, 2>(),
-        entry<6, 6, 32, 1, 0, 3, 1>(),  entry<6, 6, 32, 1, 1, 3, 1>(),  entry<6, 6, 16, 1, 0, 3, 2>(),
-        entry<12, 8, 32, 1, 1, 3, 1>(), entry<12, 8, 32, 1, 0, 3, 1>(), entry<12, 8, 16, 1, 0, 2, 2>(),
+        // fp32 (BASELINE.json configs)
+        entry<float, 4, 4, 32, 1, 1, 3, 1>(),   entry<float, 4, 4, 32, 1, 0, 3, 1>(),
+        entry<float, 4, 4, 16, 1, 1, 3, 2>(),
+        entry<float, 8, 4, 32, 1, 1, 3, 1>(),   entry<float, 8, 4, 32, 1, 0, 3, 1>(),
+        entry<float, 8, 4, 16, 1, 1, 3, 2>(),
+        entry<float, 6, 6, 32, 1, 0, 3, 1>(),   entry<float, 6, 6, 32, 1, 1, 3, 1>(),
+        entry<float, 6, 6, 16, 1, 0, 3, 2>(),
+        entry<float, 12, 8, 32, 1, 1, 3, 1>(),  entry<float, 12, 8, 32, 1, 0, 3, 1>(),
+        entry<float, 12, 8, 16, 1, 0, 2, 2>(),
+        // fp64: 16-row tiles so three stages fit in shared memory
+        entry<double, 4, 4, 16, 1, 1, 3, 1>(),  entry<double, 4, 4, 16, 1, 0, 3, 1>(),
+        entry<double, 8, 4, 16, 1, 1, 3, 1>(),  entry<double, 8, 4, 16, 1, 0, 3, 1>(),
+        entry<double, 6, 6, 16, 1, 0, 3, 1>(),  entry<double, 6, 6, 16, 1, 1, 3, 1>(),
+        entry<double, 12, 8, 16, 1, 1, 2, 1>(), entry<double, 12, 8, 16, 1, 0, 2, 1>(),
     };
     for (const auto &e : table)
-        if (e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp)) return &e;
+        if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp))
+            return &e;
     return nullptr;
 }
 
-static std::vector<const KernelEntry *> all_kernels(int r, int rz)
+static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
     for (int ty : {32, 16})
         for (int wp : {1, 0})
-            if (const KernelEntry *e = find_kernel(r, rz, ty, wp))
+            if (const KernelEntry *e = find_kernel(esize, r, rz, ty, wp))
                 if (e->ty == ty && e->wp == wp) v.push_back(e);
     return v;
 }
@@ -147,7 +162,8 @@ static std::vector<const KernelEntry *> all_kernels(int r, int rz)
 // Internal element (x, y, k) of an interior view lives at base[y * ys + k * zs + x].
 
 // user [nk][nyl][nx] (or zero when src == NULL) -> internal planes k0..k0+nk
-__global__ void k_user_to_internal(const float *__restrict__ src, float *__restrict__ dst, int nk, int nyl, int nx,
+template <typename T>
+__global__ void k_user_to_internal(const T *__restrict__ src, T *__restrict__ dst, int nk, int nyl, int nx,
                                    long long ys, long long zs, int k0)
 {
     const int64_t n = (int64_t)nk * nyl * nx;
@@ -156,11 +172,12 @@ __global__ void k_user_to_internal(const float *__restrict__ src, float *__restr
         const int64_t r = t / nx;
         const int y = (int)(r % nyl);
         const int k = (int)(r / nyl);
-        dst[y * ys + (k0 + k) * zs + x] = src ? src[t] : 0.f;
+        dst[y * ys + (k0 + k) * zs + x] = src ? src[t] : T(0);
     }
 }
 
-__global__ void k_internal_to_user(const float *__restrict__ src, float *__restrict__ dst, int nk, int nyl, int nx,
+template <typename T>
+__global__ void k_internal_to_user(const T *__restrict__ src, T *__restrict__ dst, int nk, int nyl, int nx,
                                    long long ys, long long zs, int k0)
 {
     const int64_t n = (int64_t)nk * nyl * nx;
@@ -174,9 +191,10 @@ __global__ void k_internal_to_user(const float *__restrict__ src, float *__restr
 }
 
 // counters: [0] vz2 <= 0 or non-finite, [1] vx2/vn2 non-finite, [2] vn2 > vx2, over planes k0..k0+nk
-__global__ void k_check_model(const float *__restrict__ vx2, const float *__restrict__ vn2,
-                              const float *__restrict__ vz2, int nyl, int nx, long long ys, long long zs, int k0,
-                              int nk, unsigned long long *counters)
+template <typename T>
+__global__ void k_check_model(const T *__restrict__ vx2, const T *__restrict__ vn2, const T *__restrict__ vz2,
+                              int nyl, int nx, long long ys, long long zs, int k0, int nk,
+                              unsigned long long *counters)
 {
     unsigned long long bad = 0, nonfin = 0, aniso = 0;
     const int64_t n = (int64_t)nyl * nk * nx;
@@ -186,8 +204,8 @@ __global__ void k_check_model(const float *__restrict__ vx2, const float *__rest
         const int y = (int)(r % nyl);
         const int k = (int)(r / nyl);
         const int64_t a = y * ys + (k0 + k) * zs + x;
-        const float vx = vx2[a], vn = vn2[a], vz = vz2[a];
-        bad += !(vz > 0.f) || !isfinite(vz);
+        const T vx = vx2[a], vn = vn2[a], vz = vz2[a];
+        bad += !(vz > T(0)) || !isfinite(vz);
         nonfin += !isfinite(vx) || !isfinite(vn);
         aniso += vn > vx;
     }
@@ -197,7 +215,8 @@ __global__ void k_check_model(const float *__restrict__ vx2, const float *__rest
 }
 
 // non-finite test of u^n (p, q) over the interior
-__global__ void k_check_finite(const float *__restrict__ p, const float *__restrict__ q, int nyl, int nz, int nx,
+template <typename T>
+__global__ void k_check_finite(const T *__restrict__ p, const T *__restrict__ q, int nyl, int nz, int nx,
                                long long ys, long long zs, unsigned int *flag)
 {
     bool bad = false;
@@ -215,7 +234,8 @@ __global__ void k_check_finite(const float *__restrict__ p, const float *__restr
 
 // Halo transport of p: rows [row0, row0 + R) of a halo'd buffer (row index
 // counted from the first halo row) <-> a contiguous [nz][R][nx] buffer.
-__global__ void k_pack_rows(const float *__restrict__ buf, float *__restrict__ out, int row0, int R, int nz, int nx,
+template <typename T>
+__global__ void k_pack_rows(const T *__restrict__ buf, T *__restrict__ out, int row0, int R, int nz, int nx,
                             long long ys, long long zs)
 {
     const int64_t n = (int64_t)nz * R * nx;
@@ -228,7 +248,8 @@ __global__ void k_pack_rows(const float *__restrict__ buf, float *__restrict__ o
     }
 }
 
-__global__ void k_unpack_rows(const float *__restrict__ in, float *__restrict__ buf, int row0, int R, int nz, int nx,
+template <typename T>
+__global__ void k_unpack_rows(const T *__restrict__ in, T *__restrict__ buf, int row0, int R, int nz, int nx,
                               long long ys, long long zs)
 {
     const int64_t n = (int64_t)nz * R * nx;
@@ -245,29 +266,30 @@ __global__ void k_unpack_rows(const float *__restrict__ in, float *__restrict__ 
 struct vti_s {
     vti_config cfg{};
     std::string err;
+    int es = 4;                               // element size: 4 (fp32) or 8 (fp64)
     int R = 0, RZ = 0, TY = 16;
     int y0 = 0, nyl = 0, nxp = 0, rows = 0;   // rows = nyl + 2R (halo'd)
-    long long ys = 0, zs = 0;                 // row / plane strides (floats)
+    long long ys = 0, zs = 0;                 // row / plane strides (elements)
     bool layout_zyx = true;                   // [z][y][x] (default) or [y][z][x]
     int ntx = 0, nty = 0;
     const KernelEntry *K = nullptr;
     int smem_bytes = 0;
     int sms = 0, ctas_per_sm = 0;
-    int zchunk = 0, nzc = 0, grid = 0;   // single-launch schedule
-    int zchunk_edge = 0, zchunk_inner = 0;   // nranks > 1: per-launch chunking
-    int tune_zchunk = 0, tune_ctas = 0;   // vti_set_tuning / vti_autotune overrides (0 = model)
+    int zchunk = 0, nzc = 0, grid = 0;        // single-launch schedule
+    int zchunk_edge = 0, zchunk_inner = 0;    // nranks > 1: per-launch chunking
+    int tune_zchunk = 0, tune_ctas = 0;       // vti_set_tuning / vti_autotune overrides (0 = model)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_edge = nullptr, ev_comm = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
-    float *pbuf[2] = {nullptr, nullptr};   // halo'd arrays (base = first halo row)
-    float *qbuf[2] = {nullptr, nullptr};
-    float *vx2 = nullptr, *vn2 = nullptr, *vz2 = nullptr;
-    float *sbuf[2] = {nullptr, nullptr};   // packed send rows: [0] to rank-1, [1] to rank+1
-    float *rbuf[2] = {nullptr, nullptr};   // packed recv rows: [0] from rank-1, [1] from rank+1
-    float *zrow = nullptr, *gx = nullptr, *gy = nullptr;
-    float *staging = nullptr;
-    size_t staging_floats = 0;
+    void *pbuf[2] = {nullptr, nullptr};       // halo'd arrays (base = first halo row)
+    void *qbuf[2] = {nullptr, nullptr};
+    void *vx2 = nullptr, *vn2 = nullptr, *vz2 = nullptr;
+    void *sbuf[2] = {nullptr, nullptr};       // packed send rows: [0] to rank-1, [1] to rank+1
+    void *rbuf[2] = {nullptr, nullptr};       // packed recv rows: [0] from rank-1, [1] from rank+1
+    void *zrow = nullptr, *gx = nullptr, *gy = nullptr;
+    void *staging = nullptr;
+    size_t staging_bytes = 0;
     unsigned long long *counters = nullptr;
     unsigned int *flag = nullptr;
     unsigned long long *sync_ctr = nullptr;   // round-alignment counter (monotone across launches)
@@ -275,10 +297,9 @@ struct vti_s {
     bool align_rounds = true;                 // env VTI_ALIGN=0 disables
     int64_t device_bytes = 0;
     CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
-    float cxy[MAX_R + 1] = {0};
-    float dt2 = 0.f;
-    int cur = 0;           // pbuf[cur], qbuf[cur] hold u^n
-    int64_t n = 0;         // time index
+    double cxy[MAX_R + 1] = {0};              // w^xy / h^2 in double; rounded to T at launch (reading c3)
+    int cur = 0;                              // pbuf[cur], qbuf[cur] hold u^n
+    int64_t n = 0;                            // time index
     bool model_set = false;
     int64_t model_planes_set = 0;
     int64_t aniso_warn = 0;
@@ -288,13 +309,13 @@ struct vti_s {
     ncclComm_t comm_nccl = nullptr;
     bool group_mode = false;
     bool halo_dirty = false;
-    bool suppress_src = false;   // autotune probes inject nothing
-    bool fields_touched = false; // vti_set_fields* called (state may be non-zero)
+    bool suppress_src = false;                // autotune probes inject nothing
+    bool fields_touched = false;              // vti_set_fields* called (state may be non-zero)
 
-    size_t total_floats() const { return (size_t)cfg.nz * rows * nxp; }
-    float *in(float *base) const { return base + (long long)R * ys; }   // interior view
-    float *p_int(int b) const { return in(pbuf[b]); }
-    float *q_int(int b) const { return in(qbuf[b]); }
+    size_t total_elems() const { return (size_t)cfg.nz * rows * nxp; }
+    char *in(void *base) const { return (char *)base + (long long)R * ys * es; }   // interior view
+    char *p_int(int b) const { return in(pbuf[b]); }
+    char *q_int(int b) const { return in(qbuf[b]); }
 };
 
 static std::mutex g_err_mu;
@@ -351,17 +372,18 @@ static bool is_device_ptr(const void *p)
 }
 
 // 3-D tensor map over (x, y, z) of an array with this handle's strides.
-static vti_status encode(vti_s *h, CUtensorMap *tm, float *base, int rows, int bx, int by,
+static vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx, int by,
                          CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B)
 {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     cuuint64_t dims[3] = {(cuuint64_t)h->cfg.nx, (cuuint64_t)rows, (cuuint64_t)h->cfg.nz};
-    cuuint64_t strides[2] = {(cuuint64_t)h->ys * 4, (cuuint64_t)h->zs * 4};
+    cuuint64_t strides[2] = {(cuuint64_t)(h->ys * h->es), (cuuint64_t)(h->zs * h->es)};
     cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1u};
     cuuint32_t estr[3] = {1u, 1u, 1u};
-    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+    const CUtensorMapDataType dt = h->es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    CUresult r = enc(tm, dt, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);   // NONE = zero fill: the paper's zero exterior
     if (r != CUDA_SUCCESS) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return VTI_OK;
@@ -401,11 +423,22 @@ static int choose_zchunk(const vti_s *h, int tiles)
     return best_zc;
 }
 
+// nranks > 1: the edge launch covers every tile row that intersects the first
+// or the last R_xy rows of the slab (the rows the neighbours receive), i.e.
+// tile rows [0, e1) and [e2, nty); the interior launch covers [e1, e2).
+static void edge_rows(const vti_s *h, int &e1, int &e2)
+{
+    e1 = std::min(h->nty, (h->R + h->TY - 1) / h->TY);
+    e2 = std::max(e1, std::min(h->nty, (h->nyl - h->R) / h->TY));
+}
+
 // Default schedule: one launch over all tile rows (single slab), or an edge
-// launch (first and last tile rows) plus an interior launch (nranks > 1).
+// launch plus an interior launch (nranks > 1).
 static void choose_schedule(vti_s *h)
 {
-    const int edge_rows = std::min(2, h->nty), inner_rows = std::max(0, h->nty - 2);
+    int e1, e2;
+    edge_rows(h, e1, e2);
+    const int edge_rows = e1 + (h->nty - e2), inner_rows = e2 - e1;
     h->zchunk = choose_zchunk(h, h->ntx * h->nty);
     h->zchunk_edge = choose_zchunk(h, h->ntx * edge_rows);
     h->zchunk_inner = choose_zchunk(h, h->ntx * inner_rows);
@@ -414,11 +447,14 @@ static void choose_schedule(vti_s *h)
     h->grid = (int)std::min<long>(items, (long)h->sms * h->ctas_per_sm);
 }
 
+static int precision_bits(const vti_config *c) { return c->precision == 0 ? 32 : c->precision; }
+
 static vti_status check_cfg(const vti_config *c)
 {
     if (!c) return VTI_E_PARAM;
     if (c->r_xy < 1 || c->r_z < 1 || c->r_xy > MAX_R || !(c->h > 0) || !(c->dt > 0) || c->damp_width < 0)
         return VTI_E_PARAM;
+    if (precision_bits(c) != 32 && precision_bits(c) != 64) return VTI_E_PARAM;
     if (c->nx < 1 || c->ny < 1 || c->nz < 1) return VTI_E_GEOMETRY;
     if (c->nz < 2 * c->r_z + 1) return VTI_E_GEOMETRY;   // too few planes
     if (c->damp_width > 0 && (2 * c->damp_width >= c->nx || 2 * c->damp_width >= c->ny || 2 * c->damp_width >= c->nz))
@@ -437,6 +473,52 @@ static vti_status order_after_caller(vti_s *h)
 }
 
 static int launch_grid(const vti_s *h) { return 4 * h->sms; }
+
+// Typed launch helpers for the auxiliary kernels.
+template <typename T>
+static void launch_u2i(vti_s *h, const void *src, void *dst, int nk, int k0)
+{
+    k_user_to_internal<T><<<launch_grid(h), 256, 0, h->stream>>>((const T *)src, (T *)dst, nk, h->nyl, h->cfg.nx,
+                                                                   h->ys, h->zs, k0);
+}
+template <typename T>
+static void launch_i2u(vti_s *h, const void *src, void *dst, int nk, int k0)
+{
+    k_internal_to_user<T><<<launch_grid(h), 256, 0, h->stream>>>((const T *)src, (T *)dst, nk, h->nyl, h->cfg.nx,
+                                                                   h->ys, h->zs, k0);
+}
+static void u2i(vti_s *h, const void *src, void *dst, int nk, int k0)
+{
+    if (h->es == 8) launch_u2i<double>(h, src, dst, nk, k0);
+    else launch_u2i<float>(h, src, dst, nk, k0);
+}
+static void i2u(vti_s *h, const void *src, void *dst, int nk, int k0)
+{
+    if (h->es == 8) launch_i2u<double>(h, src, dst, nk, k0);
+    else launch_i2u<float>(h, src, dst, nk, k0);
+}
+template <typename T>
+static void launch_pack(vti_s *h, const void *buf, void *out, int row0, cudaStream_t st)
+{
+    k_pack_rows<T><<<launch_grid(h), 256, 0, st>>>((const T *)buf, (T *)out, row0, h->R, h->cfg.nz, h->cfg.nx, h->ys,
+                                                   h->zs);
+}
+template <typename T>
+static void launch_unpack(vti_s *h, const void *in, void *buf, int row0, cudaStream_t st)
+{
+    k_unpack_rows<T><<<launch_grid(h), 256, 0, st>>>((const T *)in, (T *)buf, row0, h->R, h->cfg.nz, h->cfg.nx, h->ys,
+                                                     h->zs);
+}
+static void pack(vti_s *h, const void *buf, void *out, int row0, cudaStream_t st)
+{
+    if (h->es == 8) launch_pack<double>(h, buf, out, row0, st);
+    else launch_pack<float>(h, buf, out, row0, st);
+}
+static void unpack(vti_s *h, const void *in, void *buf, int row0, cudaStream_t st)
+{
+    if (h->es == 8) launch_unpack<double>(h, in, buf, row0, st);
+    else launch_unpack<float>(h, in, buf, row0, st);
+}
 
 // ============================================================ C ABI
 extern "C" {
@@ -496,13 +578,7 @@ vti_status vti_destroy(vti_t h)
         cudaFree(h->sbuf[b]);
         cudaFree(h->rbuf[b]);
     }
-    cudaFree(h->vx2);
-    cudaFree(h->vn2);
-    cudaFree(h->vz2);
-    cudaFree(h->zrow);
-    cudaFree(h->gx);
-    cudaFree(h->gy);
-    cudaFree(h->staging);
+    for (void *p : {h->vx2, h->vn2, h->vz2, h->zrow, h->gx, h->gy, h->staging}) cudaFree(p);
     cudaFree(h->counters);
     cudaFree(h->flag);
     cudaFree(h->sync_ctr);
@@ -524,6 +600,8 @@ static vti_status alloc(vti_s *h, void **p, size_t bytes)
     return VTI_OK;
 }
 
+}  // extern "C"
+
 // Make K the step kernel of the handle: tile height, shared memory, occupancy,
 // default schedule and the TMA tensor maps (whose boxes depend on TY).
 static vti_status select_variant(vti_s *h, const KernelEntry *K)
@@ -532,9 +610,8 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
     h->TY = K->ty;
     h->nty = (h->nyl + h->TY - 1) / h->TY;
     h->smem_bytes = K->stages * K->stage_bytes + 2 * K->stages * 8;
-    CU(h, cudaFuncSetAttribute((const void *)K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
-    CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, (const void *)K->fn, K->threads,
-                                                        h->smem_bytes));
+    CU(h, cudaFuncSetAttribute(K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+    CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, K->fn, K->threads, h->smem_bytes));
     if (h->ctas_per_sm < 1) return fail(h, VTI_E_CUDA, "step kernel cannot be resident (smem %d B)", h->smem_bytes);
     if (h->tune_ctas > 0) h->ctas_per_sm = std::min(h->ctas_per_sm, h->tune_ctas);
     choose_schedule(h);
@@ -560,21 +637,38 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
     return VTI_OK;
 }
 
-static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy, const float *w_z)
+// Upload a host table converting double -> T (one rounding for fp32).
+static vti_status upload_table(vti_s *h, void **dst, const std::vector<double> &v)
+{
+    vti_status s = alloc(h, dst, v.size() * h->es);
+    if (s != VTI_OK) return s;
+    if (h->es == 8) {
+        CU(h, cudaMemcpy(*dst, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> f(v.size());
+        for (size_t i = 0; i < v.size(); ++i) f[i] = (float)v[i];
+        CU(h, cudaMemcpy(*dst, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    }
+    return VTI_OK;
+}
+
+// w_xy / w_z as double (exact widening of float weights for the fp32 entry point).
+static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_xy, const double *w_z)
 {
     vti_status st = check_cfg(cfg);
     if (st != VTI_OK) return fail(h, st, "invalid configuration (%s)", vti_status_string(st));
     if (!w_xy || !w_z) return fail(h, VTI_E_PARAM, "NULL weights");
     h->cfg = *cfg;
+    h->es = precision_bits(cfg) / 8;
     h->R = cfg->r_xy;
     h->RZ = cfg->r_z;
     int want_ty = -1, want_wp = -1;
     if (const char *e = getenv("VTI_TY")) want_ty = atoi(e);
     if (const char *e = getenv("VTI_WP")) want_wp = atoi(e);
-    h->K = find_kernel(h->R, h->RZ, want_ty, want_wp);
-    if (!h->K) h->K = find_kernel(h->R, h->RZ, -1, -1);
-    if (!h->K) return fail(h, VTI_E_UNSUPPORTED, "(r_xy, r_z) = (%d, %d) not compiled", h->R, h->RZ);
-    h->TY = h->K->ty;
+    h->K = find_kernel(h->es, h->R, h->RZ, want_ty, want_wp);
+    if (!h->K) h->K = find_kernel(h->es, h->R, h->RZ, -1, -1);
+    if (!h->K)
+        return fail(h, VTI_E_UNSUPPORTED, "(r_xy, r_z) = (%d, %d) not compiled for fp%d", h->R, h->RZ, 8 * h->es);
     vti_slab(cfg, &h->y0, &h->nyl);
     h->nxp = (cfg->nx + 31) / 32 * 32;
     h->rows = h->nyl + 2 * h->R;
@@ -590,9 +684,8 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     h->ntx = (cfg->nx + TX - 1) / TX;
     for (int l = 0; l <= h->R; ++l) {
         if (!std::isfinite(w_xy[l])) return fail(h, VTI_E_PARAM, "non-finite w_xy[%d]", l);
-        h->cxy[l] = (float)((double)w_xy[l] / (cfg->h * cfg->h));   // reading c3
+        h->cxy[l] = w_xy[l] / (cfg->h * cfg->h);   // reading c3; rounded once to T at launch
     }
-    h->dt2 = (float)(cfg->dt * cfg->dt);
 
     CU(h, cudaSetDevice(cfg->device));
     if (cfg->stream) {
@@ -610,47 +703,45 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     CU(h, cudaEventCreate(&h->ev_t1));
     CU(h, cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cfg->device));
 
-    const size_t bytes = h->total_floats() * 4;
+    const size_t bytes = h->total_elems() * h->es;
     vti_status s;
     for (int b = 0; b < 2; ++b) {
-        if ((s = alloc(h, (void **)&h->pbuf[b], bytes)) != VTI_OK) return s;
-        if ((s = alloc(h, (void **)&h->qbuf[b], bytes)) != VTI_OK) return s;
+        if ((s = alloc(h, &h->pbuf[b], bytes)) != VTI_OK) return s;
+        if ((s = alloc(h, &h->qbuf[b], bytes)) != VTI_OK) return s;
     }
-    if ((s = alloc(h, (void **)&h->vx2, bytes)) != VTI_OK) return s;
-    if ((s = alloc(h, (void **)&h->vn2, bytes)) != VTI_OK) return s;
-    if ((s = alloc(h, (void **)&h->vz2, bytes)) != VTI_OK) return s;
+    if ((s = alloc(h, &h->vx2, bytes)) != VTI_OK) return s;
+    if ((s = alloc(h, &h->vn2, bytes)) != VTI_OK) return s;
+    if ((s = alloc(h, &h->vz2, bytes)) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->counters, 4 * sizeof(unsigned long long))) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->flag, sizeof(unsigned int))) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->sync_ctr, sizeof(unsigned long long))) != VTI_OK) return s;
     if (const char *e = getenv("VTI_ALIGN")) h->align_rounds = atoi(e) != 0;
     if (cfg->nranks > 1) {
-        const size_t hb = (size_t)cfg->nz * h->R * cfg->nx * 4;
+        const size_t hb = (size_t)cfg->nz * h->R * cfg->nx * h->es;
         for (int b = 0; b < 2; ++b) {
-            if ((s = alloc(h, (void **)&h->sbuf[b], hb)) != VTI_OK) return s;
-            if ((s = alloc(h, (void **)&h->rbuf[b], hb)) != VTI_OK) return s;
+            if ((s = alloc(h, &h->sbuf[b], hb)) != VTI_OK) return s;
+            if ((s = alloc(h, &h->rbuf[b], hb)) != VTI_OK) return s;
         }
     }
 
-    // per-plane z rows: w^z[k][0..2Rz], gz[k], zero pad (host double -> float once)
+    // per-plane z rows: w^z[k][0..2Rz], gz[k], zero pad; 1-D Cerjan profiles (double -> T once)
     const int NQ = 2 * h->RZ + 1, ZR = h->K->zrow;
-    std::vector<float> zr((size_t)cfg->nz * ZR, 0.f);
+    std::vector<double> zr((size_t)cfg->nz * ZR, 0.0);
     for (int k = 0; k < cfg->nz; ++k) {
         for (int m = 0; m < NQ; ++m) {
-            float v = w_z[(size_t)k * NQ + m];
+            const double v = w_z[(size_t)k * NQ + m];
             if (!std::isfinite(v)) return fail(h, VTI_E_PARAM, "non-finite w_z[%d][%d]", k, m);
             zr[(size_t)k * ZR + m] = v;
         }
-        zr[(size_t)k * ZR + NQ] = (float)damping(k, cfg->nz, cfg->damp_width, cfg->damp_alpha);
+        zr[(size_t)k * ZR + NQ] = damping(k, cfg->nz, cfg->damp_width, cfg->damp_alpha);
     }
-    std::vector<float> gxv((size_t)h->ntx * TX, 1.f), gyv(h->nyl);
-    for (int i = 0; i < cfg->nx; ++i) gxv[i] = (float)damping(i, cfg->nx, cfg->damp_width, cfg->damp_alpha);
-    for (int j = 0; j < h->nyl; ++j) gyv[j] = (float)damping(h->y0 + j, cfg->ny, cfg->damp_width, cfg->damp_alpha);
-    if ((s = alloc(h, (void **)&h->zrow, zr.size() * 4)) != VTI_OK) return s;
-    if ((s = alloc(h, (void **)&h->gx, gxv.size() * 4)) != VTI_OK) return s;
-    if ((s = alloc(h, (void **)&h->gy, gyv.size() * 4)) != VTI_OK) return s;
-    CU(h, cudaMemcpyAsync(h->zrow, zr.data(), zr.size() * 4, cudaMemcpyHostToDevice, h->stream));
-    CU(h, cudaMemcpyAsync(h->gx, gxv.data(), gxv.size() * 4, cudaMemcpyHostToDevice, h->stream));
-    CU(h, cudaMemcpyAsync(h->gy, gyv.data(), gyv.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    std::vector<double> gxv((size_t)h->ntx * TX, 1.0), gyv(h->nyl);
+    for (int i = 0; i < cfg->nx; ++i) gxv[i] = damping(i, cfg->nx, cfg->damp_width, cfg->damp_alpha);
+    for (int j = 0; j < h->nyl; ++j) gyv[j] = damping(h->y0 + j, cfg->ny, cfg->damp_width, cfg->damp_alpha);
+    CU(h, cudaStreamSynchronize(h->stream));
+    if ((s = upload_table(h, &h->zrow, zr)) != VTI_OK) return s;
+    if ((s = upload_table(h, &h->gx, gxv)) != VTI_OK) return s;
+    if ((s = upload_table(h, &h->gy, gyv)) != VTI_OK) return s;
 
     if ((s = select_variant(h, h->K)) != VTI_OK) return s;
 
@@ -670,10 +761,8 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const float *w_xy
     return VTI_OK;
 }
 
-vti_status vti_create(vti_t *out, const vti_config *cfg, const float *w_xy, const float *w_z)
+static vti_status create_common(vti_t *out, const vti_config *cfg, const double *w_xy, const double *w_z)
 {
-    if (!out) return fail(nullptr, VTI_E_PARAM, "NULL output handle");
-    *out = nullptr;
     vti_s *h = new vti_s();
     vti_status s = create_impl(h, cfg, w_xy, w_z);
     if (s != VTI_OK) {
@@ -688,67 +777,58 @@ vti_status vti_create(vti_t *out, const vti_config *cfg, const float *w_xy, cons
     return VTI_OK;
 }
 
-const char *vti_last_error(vti_t h)
+static vti_status ensure_staging(vti_s *h, size_t want_bytes)
 {
-    if (h) return h->err.c_str();
-    std::lock_guard<std::mutex> g(g_err_mu);
-    return g_create_err.c_str();
-}
-
-static vti_status ensure_staging(vti_s *h, size_t want)
-{
-    if (h->staging_floats >= want) return VTI_OK;
+    if (h->staging_bytes >= want_bytes) return VTI_OK;
     cudaFree(h->staging);
     h->staging = nullptr;
-    h->staging_floats = 0;
-    CU(h, cudaMalloc(&h->staging, want * 4));
-    h->staging_floats = want;
+    h->staging_bytes = 0;
+    CU(h, cudaMalloc(&h->staging, want_bytes));
+    h->staging_bytes = want_bytes;
     return VTI_OK;
 }
 
 // Planes [k0, k0+nk) of a user-layout array (host, device, or NULL = zero) -> interior view dst.
-static vti_status upload_planes(vti_s *h, float *dst, const float *src, int k0, int nk)
+static vti_status upload_planes(vti_s *h, void *dst, const void *src, int k0, int nk)
 {
-    const int nx = h->cfg.nx, nyl = h->nyl;
-    const size_t plane = (size_t)nyl * nx;
+    const size_t plane = (size_t)h->nyl * h->cfg.nx * h->es;   // bytes
     if (!src || is_device_ptr(src)) {
-        k_user_to_internal<<<launch_grid(h), 256, 0, h->stream>>>(src, dst, nk, nyl, nx, h->ys, h->zs, k0);
+        u2i(h, src, dst, nk, k0);
         CU(h, cudaGetLastError());
         return VTI_OK;
     }
     // host source: bounce through a device staging buffer in chunks of planes
-    vti_status s = ensure_staging(h, std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20)));
+    vti_status s = ensure_staging(h, std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)256 << 20)));
     if (s != VTI_OK) return s;
-    const int chunk = (int)std::max<size_t>(1, h->staging_floats / plane);
+    const int chunk = (int)std::max<size_t>(1, h->staging_bytes / plane);
     for (int k = 0; k < nk; k += chunk) {
         const int m = std::min(chunk, nk - k);
-        CU(h, cudaMemcpyAsync(h->staging, src + (size_t)k * plane, (size_t)m * plane * 4, cudaMemcpyHostToDevice,
-                              h->stream));
-        k_user_to_internal<<<launch_grid(h), 256, 0, h->stream>>>(h->staging, dst, m, nyl, nx, h->ys, h->zs, k0 + k);
+        CU(h, cudaMemcpyAsync(h->staging, (const char *)src + (size_t)k * plane, (size_t)m * plane,
+                              cudaMemcpyHostToDevice, h->stream));
+        u2i(h, h->staging, dst, m, k0 + k);
         CU(h, cudaGetLastError());
     }
     CU(h, cudaStreamSynchronize(h->stream));   // staging is reused; host buffer may be freed after return
     return VTI_OK;
 }
 
-static vti_status download_planes(vti_s *h, float *dst, const float *src, int k0, int nk)
+static vti_status download_planes(vti_s *h, void *dst, const void *src, int k0, int nk)
 {
-    const int nx = h->cfg.nx, nyl = h->nyl;
-    const size_t plane = (size_t)nyl * nx;
+    const size_t plane = (size_t)h->nyl * h->cfg.nx * h->es;
     if (is_device_ptr(dst)) {
-        k_internal_to_user<<<launch_grid(h), 256, 0, h->stream>>>(src, dst, nk, nyl, nx, h->ys, h->zs, k0);
+        i2u(h, src, dst, nk, k0);
         CU(h, cudaGetLastError());
         CU(h, cudaStreamSynchronize(h->stream));
         return VTI_OK;
     }
-    vti_status s = ensure_staging(h, std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)64 << 20)));
+    vti_status s = ensure_staging(h, std::min<size_t>((size_t)nk * plane, std::max<size_t>(plane, (size_t)256 << 20)));
     if (s != VTI_OK) return s;
-    const int chunk = (int)std::max<size_t>(1, h->staging_floats / plane);
+    const int chunk = (int)std::max<size_t>(1, h->staging_bytes / plane);
     for (int k = 0; k < nk; k += chunk) {
         const int m = std::min(chunk, nk - k);
-        k_internal_to_user<<<launch_grid(h), 256, 0, h->stream>>>(src, h->staging, m, nyl, nx, h->ys, h->zs, k0 + k);
+        i2u(h, src, h->staging, m, k0 + k);
         CU(h, cudaGetLastError());
-        CU(h, cudaMemcpyAsync(dst + (size_t)k * plane, h->staging, (size_t)m * plane * 4, cudaMemcpyDeviceToHost,
+        CU(h, cudaMemcpyAsync((char *)dst + (size_t)k * plane, h->staging, (size_t)m * plane, cudaMemcpyDeviceToHost,
                               h->stream));
     }
     CU(h, cudaStreamSynchronize(h->stream));
@@ -762,23 +842,38 @@ static bool any_device(std::initializer_list<const void *> ps)
     return false;
 }
 
-vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx2, const float *vn2,
-                                const float *vz2)
+static vti_status check_precision(vti_s *h, int es, const char *fn)
+{
+    if (h->es != es)
+        return fail(h, VTI_E_PARAM, "%s: handle is fp%d, call is fp%d (use the %s entry point)", fn, 8 * h->es, 8 * es,
+                    h->es == 8 ? "_f64" : "fp32");
+    return VTI_OK;
+}
+
+static vti_status set_model_planes(vti_s *h, int es, int32_t k0, int32_t nk, const void *vx2, const void *vn2,
+                                   const void *vz2)
 {
     if (!h) return VTI_E_PARAM;
+    vti_status s = check_precision(h, es, "vti_set_model");
+    if (s != VTI_OK) return s;
     if (!vx2 || !vn2 || !vz2) return fail(h, VTI_E_PARAM, "NULL model array");
     if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
         return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
     CU(h, cudaSetDevice(h->cfg.device));
-    vti_status s;
     if (any_device({vx2, vn2, vz2}) && (s = order_after_caller(h)) != VTI_OK) return s;
     if ((s = upload_planes(h, h->in(h->vx2), vx2, k0, nk)) != VTI_OK) return s;
     if ((s = upload_planes(h, h->in(h->vn2), vn2, k0, nk)) != VTI_OK) return s;
     if ((s = upload_planes(h, h->in(h->vz2), vz2, k0, nk)) != VTI_OK) return s;
     // validate on the device: vz2 > 0 and finite, vx2/vn2 finite, count vn2 > vx2 (reading c5)
     CU(h, cudaMemsetAsync(h->counters, 0, 4 * sizeof(unsigned long long), h->stream));
-    k_check_model<<<launch_grid(h), 256, 0, h->stream>>>(h->in(h->vx2), h->in(h->vn2), h->in(h->vz2), h->nyl,
-                                                          h->cfg.nx, h->ys, h->zs, k0, nk, h->counters);
+    if (h->es == 8)
+        k_check_model<double><<<launch_grid(h), 256, 0, h->stream>>>(
+            (const double *)h->in(h->vx2), (const double *)h->in(h->vn2), (const double *)h->in(h->vz2), h->nyl,
+            h->cfg.nx, h->ys, h->zs, k0, nk, h->counters);
+    else
+        k_check_model<float><<<launch_grid(h), 256, 0, h->stream>>>(
+            (const float *)h->in(h->vx2), (const float *)h->in(h->vn2), (const float *)h->in(h->vz2), h->nyl,
+            h->cfg.nx, h->ys, h->zs, k0, nk, h->counters);
     CU(h, cudaGetLastError());
     unsigned long long cnt[3];
     CU(h, cudaMemcpyAsync(cnt, h->counters, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
@@ -792,10 +887,49 @@ vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx
     return VTI_OK;
 }
 
-}  // extern "C"
+static vti_status set_fields_planes(vti_s *h, int es, int32_t k0, int32_t nk, const void *p, const void *q,
+                                    const void *pm, const void *qm)
+{
+    if (!h) return VTI_E_PARAM;
+    vti_status s = check_precision(h, es, "vti_set_fields");
+    if (s != VTI_OK) return s;
+    if (!p || !q) return fail(h, VTI_E_PARAM, "NULL p or q");
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
+        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->comm));
+    if (any_device({p, q, pm, qm}) && (s = order_after_caller(h)) != VTI_OK) return s;
+    const int c = h->cur, o = 1 - c;
+    if ((s = upload_planes(h, h->p_int(c), p, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->q_int(c), q, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->p_int(o), pm, k0, nk)) != VTI_OK) return s;
+    if ((s = upload_planes(h, h->q_int(o), qm, k0, nk)) != VTI_OK) return s;
+    CU(h, cudaStreamSynchronize(h->stream));
+    h->halo_dirty = h->cfg.nranks > 1;
+    h->fields_touched = true;
+    return VTI_OK;
+}
+
+static vti_status get_fields_planes(vti_s *h, int es, int32_t k0, int32_t nk, void *p, void *q, int32_t level)
+{
+    if (!h) return VTI_E_PARAM;
+    vti_status s = check_precision(h, es, "vti_get_fields");
+    if (s != VTI_OK) return s;
+    if (level != 0 && level != 1) return fail(h, VTI_E_PARAM, "level must be 0 (u^n) or 1 (u^{n-1})");
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
+        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->comm));
+    if (any_device({p, q}) && (s = order_after_caller(h)) != VTI_OK) return s;
+    const int b = level == 0 ? h->cur : 1 - h->cur;
+    if (p && (s = download_planes(h, p, h->p_int(b), k0, nk)) != VTI_OK) return s;
+    if (q && (s = download_planes(h, q, h->q_int(b), k0, nk)) != VTI_OK) return s;
+    return VTI_OK;
+}
 
 // ============================================================ stepping
-static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int nty_sel, int zchunk)
+template <typename T>
+static void fill_params(vti_s *h, StepParams<T> &P, int tr0, int ntr0, int tr1, int ntr1, int zchunk)
 {
     const int c = h->cur, o = 1 - c;
     P.tm_p = h->tm_ph[c];
@@ -805,16 +939,16 @@ static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int 
     P.tm_vx = h->tm_vx;
     P.tm_vn = h->tm_vn;
     P.tm_vz = h->tm_vz;
-    P.p_out = h->p_int(o);
-    P.q_out = h->q_int(o);
-    P.zrow = h->zrow;
-    P.gx = h->gx;
-    P.gy = h->gy;
-    for (int l = 0; l <= MAX_R; ++l) P.cxy[l] = l <= h->R ? h->cxy[l] : 0.f;
-    P.dt2 = h->dt2;
+    P.p_out = (T *)h->p_int(o);
+    P.q_out = (T *)h->q_int(o);
+    P.zrow = (const T *)h->zrow;
+    P.gx = (const T *)h->gx;
+    P.gy = (const T *)h->gy;
+    for (int l = 0; l <= MAX_R; ++l) P.cxy[l] = l <= h->R ? (T)h->cxy[l] : T(0);
+    P.dt2 = (T)(h->cfg.dt * h->cfg.dt);
     const bool owned = h->has_src && !h->suppress_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
-    // s(t^n), t^n = n dt, double on the host, rounded once (reading c7)
-    P.s = owned ? (float)(h->src_amp * ricker((double)h->n * h->cfg.dt, h->src_f, h->src_t0)) : 0.f;
+    // s(t^n), t^n = n dt, double on the host, rounded once to T (reading c7)
+    P.s = owned ? (T)(h->src_amp * ricker((double)h->n * h->cfg.dt, h->src_f, h->src_t0)) : T(0);
     P.src_i = h->src_i;
     P.src_j = owned ? h->src_j - h->y0 : -1;
     P.src_k = h->src_k;
@@ -825,19 +959,20 @@ static void fill_params(vti_s *h, StepParams &P, int ty_begin, int ty_step, int 
     P.ys = h->ys;
     P.zs = h->zs;
     P.ntx = h->ntx;
-    P.ty_begin = ty_begin;
-    P.ty_step = ty_step;
-    P.nty = nty_sel;
+    P.tr0 = tr0;
+    P.ntr0 = ntr0;
+    P.tr1 = tr1;
+    P.ntr1 = ntr1;
     P.zchunk = zchunk;
     P.nzc = (h->cfg.nz + zchunk - 1) / zchunk;
-    P.items = h->ntx * nty_sel * P.nzc;
+    P.items = h->ntx * (ntr0 + ntr1) * P.nzc;
 }
 
-static vti_status launch_rows(vti_s *h, int ty_begin, int ty_step, int nty_sel, int zchunk)
+template <typename T>
+static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk)
 {
-    if (nty_sel <= 0) return VTI_OK;
-    StepParams P;
-    fill_params(h, P, ty_begin, ty_step, nty_sel, zchunk);
+    StepParams<T> P;
+    fill_params<T>(h, P, tr0, ntr0, tr1, ntr1, zchunk);
     const int grid = std::min(P.items, h->sms * h->ctas_per_sm);
     const int rounds = (P.items + grid - 1) / grid;
     P.sync_ctr = nullptr;
@@ -858,24 +993,43 @@ static vti_status launch_rows(vti_s *h, int ty_begin, int ty_step, int nty_sel, 
         lc.attrs = attr;
         lc.numAttrs = 1;
     }
-    CU(h, cudaLaunchKernelEx(&lc, h->K->fn, P));
+    void *args[] = {&P};
+    CU(h, cudaLaunchKernelExC(&lc, h->K->fn, args));
     return VTI_OK;
+}
+
+// Tile rows [tr0, tr0+ntr0) then [tr1, tr1+ntr1) of this slab, z-chunks of zchunk planes.
+static vti_status launch_rows(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk)
+{
+    if (ntr0 + ntr1 <= 0) return VTI_OK;
+    return h->es == 8 ? launch_rows_t<double>(h, tr0, ntr0, tr1, ntr1, zchunk)
+                      : launch_rows_t<float>(h, tr0, ntr0, tr1, ntr1, zchunk);
+}
+
+static vti_status launch_edge(vti_s *h)
+{
+    int e1, e2;
+    edge_rows(h, e1, e2);
+    return launch_rows(h, 0, e1, e2, h->nty - e2, h->zchunk_edge);
+}
+
+static vti_status launch_interior(vti_s *h)
+{
+    int e1, e2;
+    edge_rows(h, e1, e2);
+    return launch_rows(h, e1, e2 - e1, 0, 0, h->zchunk_inner);
 }
 
 // ---- halo transport of p (y-slab decomposition)
 // Halo'd row index: [0, R) rows from rank-1, [R, R+nyl) own rows, [R+nyl, 2R+nyl) rows from rank+1.
-static size_t halo_floats(const vti_s *h) { return (size_t)h->cfg.nz * h->R * h->cfg.nx; }
+static size_t halo_elems(const vti_s *h) { return (size_t)h->cfg.nz * h->R * h->cfg.nx; }
 
 // On the main stream: pack this rank's boundary rows of buffer b into sbuf[0] (-> rank-1) and sbuf[1] (-> rank+1).
 static vti_status pack_send(vti_s *h, int b)
 {
     const int r = h->cfg.rank, nr = h->cfg.nranks;
-    if (r > 0)
-        k_pack_rows<<<launch_grid(h), 256, 0, h->stream>>>(h->pbuf[b], h->sbuf[0], h->R, h->R, h->cfg.nz, h->cfg.nx,
-                                                          h->ys, h->zs);
-    if (r < nr - 1)
-        k_pack_rows<<<launch_grid(h), 256, 0, h->stream>>>(h->pbuf[b], h->sbuf[1], h->nyl, h->R, h->cfg.nz,
-                                                          h->cfg.nx, h->ys, h->zs);
+    if (r > 0) pack(h, h->pbuf[b], h->sbuf[0], h->R, h->stream);
+    if (r < nr - 1) pack(h, h->pbuf[b], h->sbuf[1], h->nyl, h->stream);
     CU(h, cudaGetLastError());
     return VTI_OK;
 }
@@ -884,12 +1038,8 @@ static vti_status pack_send(vti_s *h, int b)
 static vti_status unpack_recv(vti_s *h, int b)
 {
     const int r = h->cfg.rank, nr = h->cfg.nranks;
-    if (r > 0)
-        k_unpack_rows<<<launch_grid(h), 256, 0, h->comm>>>(h->rbuf[0], h->pbuf[b], 0, h->R, h->cfg.nz, h->cfg.nx,
-                                                          h->ys, h->zs);
-    if (r < nr - 1)
-        k_unpack_rows<<<launch_grid(h), 256, 0, h->comm>>>(h->rbuf[1], h->pbuf[b], h->nyl + h->R, h->R, h->cfg.nz,
-                                                          h->cfg.nx, h->ys, h->zs);
+    if (r > 0) unpack(h, h->rbuf[0], h->pbuf[b], 0, h->comm);
+    if (r < nr - 1) unpack(h, h->rbuf[1], h->pbuf[b], h->nyl + h->R, h->comm);
     CU(h, cudaGetLastError());
     return VTI_OK;
 }
@@ -899,16 +1049,17 @@ static vti_status exchange_nccl(vti_s *h, int b)
 {
     NcclApi &api = nccl();
     CU(h, cudaStreamWaitEvent(h->comm, h->ev_edge, 0));
-    const size_t cnt = halo_floats(h);
+    const size_t cnt = halo_elems(h);
+    const ncclDataType_t dt = h->es == 8 ? ncclFloat64 : ncclFloat32;
     const int r = h->cfg.rank, nr = h->cfg.nranks;
     ncclResult_t e = api.GroupStart();
     if (e == ncclSuccess && r > 0) {
-        e = api.Send(h->sbuf[0], cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
-        if (e == ncclSuccess) e = api.Recv(h->rbuf[0], cnt, ncclFloat32, r - 1, h->comm_nccl, h->comm);
+        e = api.Send(h->sbuf[0], cnt, dt, r - 1, h->comm_nccl, h->comm);
+        if (e == ncclSuccess) e = api.Recv(h->rbuf[0], cnt, dt, r - 1, h->comm_nccl, h->comm);
     }
     if (e == ncclSuccess && r < nr - 1) {
-        e = api.Send(h->sbuf[1], cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
-        if (e == ncclSuccess) e = api.Recv(h->rbuf[1], cnt, ncclFloat32, r + 1, h->comm_nccl, h->comm);
+        e = api.Send(h->sbuf[1], cnt, dt, r + 1, h->comm_nccl, h->comm);
+        if (e == ncclSuccess) e = api.Recv(h->rbuf[1], cnt, dt, r + 1, h->comm_nccl, h->comm);
     }
     ncclResult_t e2 = api.GroupEnd();
     if (e != ncclSuccess || e2 != ncclSuccess)
@@ -922,8 +1073,14 @@ static vti_status exchange_nccl(vti_s *h, int b)
 static vti_status check_finite(vti_s *h)
 {
     CU(h, cudaMemsetAsync(h->flag, 0, sizeof(unsigned int), h->stream));
-    k_check_finite<<<launch_grid(h), 256, 0, h->stream>>>(h->p_int(h->cur), h->q_int(h->cur), h->nyl, h->cfg.nz,
-                                                           h->cfg.nx, h->ys, h->zs, h->flag);
+    if (h->es == 8)
+        k_check_finite<double><<<launch_grid(h), 256, 0, h->stream>>>(
+            (const double *)h->p_int(h->cur), (const double *)h->q_int(h->cur), h->nyl, h->cfg.nz, h->cfg.nx, h->ys,
+            h->zs, h->flag);
+    else
+        k_check_finite<float><<<launch_grid(h), 256, 0, h->stream>>>(
+            (const float *)h->p_int(h->cur), (const float *)h->q_int(h->cur), h->nyl, h->cfg.nz, h->cfg.nx, h->ys,
+            h->zs, h->flag);
     CU(h, cudaGetLastError());
     unsigned int f = 0;
     CU(h, cudaMemcpyAsync(&f, h->flag, sizeof f, cudaMemcpyDeviceToHost, h->stream));
@@ -934,11 +1091,62 @@ static vti_status check_finite(vti_s *h)
 
 extern "C" {
 
+vti_status vti_create(vti_t *out, const vti_config *cfg, const float *w_xy, const float *w_z)
+{
+    if (!out) return fail(nullptr, VTI_E_PARAM, "NULL output handle");
+    *out = nullptr;
+    vti_status st = check_cfg(cfg);
+    if (st != VTI_OK) return fail(nullptr, st, "invalid configuration (%s)", vti_status_string(st));
+    if (!w_xy || !w_z) return fail(nullptr, VTI_E_PARAM, "NULL weights");
+    const int NQ = 2 * cfg->r_z + 1;
+    std::vector<double> wxy(cfg->r_xy + 1), wz((size_t)cfg->nz * NQ);
+    for (size_t i = 0; i < wxy.size(); ++i) wxy[i] = (double)w_xy[i];   // exact widening
+    for (size_t i = 0; i < wz.size(); ++i) wz[i] = (double)w_z[i];
+    return create_common(out, cfg, wxy.data(), wz.data());
+}
+
+vti_status vti_create_f64(vti_t *out, const vti_config *cfg, const double *w_xy, const double *w_z)
+{
+    if (!out) return fail(nullptr, VTI_E_PARAM, "NULL output handle");
+    *out = nullptr;
+    vti_status st = check_cfg(cfg);
+    if (st != VTI_OK) return fail(nullptr, st, "invalid configuration (%s)", vti_status_string(st));
+    if (precision_bits(cfg) != 64) return fail(nullptr, VTI_E_PARAM, "vti_create_f64 needs cfg->precision = 64");
+    if (!w_xy || !w_z) return fail(nullptr, VTI_E_PARAM, "NULL weights");
+    return create_common(out, cfg, w_xy, w_z);
+}
+
+const char *vti_last_error(vti_t h)
+{
+    if (h) return h->err.c_str();
+    std::lock_guard<std::mutex> g(g_err_mu);
+    return g_create_err.c_str();
+}
+
+vti_status vti_set_model_planes(vti_t h, int32_t k0, int32_t nk, const float *vx2, const float *vn2,
+                                const float *vz2)
+{
+    return set_model_planes(h, 4, k0, nk, vx2, vn2, vz2);
+}
+
+vti_status vti_set_model_planes_f64(vti_t h, int32_t k0, int32_t nk, const double *vx2, const double *vn2,
+                                    const double *vz2)
+{
+    return set_model_planes(h, 8, k0, nk, vx2, vn2, vz2);
+}
+
 vti_status vti_set_model(vti_t h, const float *vx2, const float *vn2, const float *vz2)
 {
     if (!h) return VTI_E_PARAM;
     h->model_planes_set = 0;
-    return vti_set_model_planes(h, 0, h->cfg.nz, vx2, vn2, vz2);
+    return set_model_planes(h, 4, 0, h->cfg.nz, vx2, vn2, vz2);
+}
+
+vti_status vti_set_model_f64(vti_t h, const double *vx2, const double *vn2, const double *vz2)
+{
+    if (!h) return VTI_E_PARAM;
+    h->model_planes_set = 0;
+    return set_model_planes(h, 8, 0, h->cfg.nz, vx2, vn2, vz2);
 }
 
 int64_t vti_model_warnings(vti_t h) { return h ? h->aniso_warn : -1; }
@@ -967,32 +1175,53 @@ vti_status vti_add_source(vti_t h, int32_t i, int32_t j, int32_t k, double f, do
 vti_status vti_set_fields_planes(vti_t h, int32_t k0, int32_t nk, const float *p, const float *q, const float *pm,
                                  const float *qm)
 {
-    if (!h) return VTI_E_PARAM;
-    if (!p || !q) return fail(h, VTI_E_PARAM, "NULL p or q");
-    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
-        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
-    CU(h, cudaSetDevice(h->cfg.device));
-    CU(h, cudaStreamSynchronize(h->comm));
-    vti_status s;
-    if (any_device({p, q, pm, qm}) && (s = order_after_caller(h)) != VTI_OK) return s;
-    const int c = h->cur, o = 1 - c;
-    if ((s = upload_planes(h, h->p_int(c), p, k0, nk)) != VTI_OK) return s;
-    if ((s = upload_planes(h, h->q_int(c), q, k0, nk)) != VTI_OK) return s;
-    if ((s = upload_planes(h, h->p_int(o), pm, k0, nk)) != VTI_OK) return s;
-    if ((s = upload_planes(h, h->q_int(o), qm, k0, nk)) != VTI_OK) return s;
-    CU(h, cudaStreamSynchronize(h->stream));
-    h->halo_dirty = h->cfg.nranks > 1;
-    h->fields_touched = true;
-    return VTI_OK;
+    return set_fields_planes(h, 4, k0, nk, p, q, pm, qm);
+}
+
+vti_status vti_set_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, const double *p, const double *q,
+                                     const double *pm, const double *qm)
+{
+    return set_fields_planes(h, 8, k0, nk, p, q, pm, qm);
 }
 
 vti_status vti_set_fields(vti_t h, const float *p, const float *q, const float *pm, const float *qm,
                           int64_t time_index)
 {
     if (!h) return VTI_E_PARAM;
-    vti_status s = vti_set_fields_planes(h, 0, h->cfg.nz, p, q, pm, qm);
+    vti_status s = set_fields_planes(h, 4, 0, h->cfg.nz, p, q, pm, qm);
     if (s == VTI_OK) h->n = time_index;
     return s;
+}
+
+vti_status vti_set_fields_f64(vti_t h, const double *p, const double *q, const double *pm, const double *qm,
+                              int64_t time_index)
+{
+    if (!h) return VTI_E_PARAM;
+    vti_status s = set_fields_planes(h, 8, 0, h->cfg.nz, p, q, pm, qm);
+    if (s == VTI_OK) h->n = time_index;
+    return s;
+}
+
+vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level)
+{
+    return get_fields_planes(h, 4, k0, nk, p, q, level);
+}
+
+vti_status vti_get_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, double *p, double *q, int32_t level)
+{
+    return get_fields_planes(h, 8, k0, nk, p, q, level);
+}
+
+vti_status vti_get_fields(vti_t h, float *p, float *q, int32_t level)
+{
+    if (!h) return VTI_E_PARAM;
+    return get_fields_planes(h, 4, 0, h->cfg.nz, p, q, level);
+}
+
+vti_status vti_get_fields_f64(vti_t h, double *p, double *q, int32_t level)
+{
+    if (!h) return VTI_E_PARAM;
+    return get_fields_planes(h, 8, 0, h->cfg.nz, p, q, level);
 }
 
 vti_status vti_step(vti_t h, int32_t nsteps)
@@ -1013,17 +1242,15 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     }
     for (int it = 0; it < nsteps; ++it) {
         if (!multi) {
-            if ((s = launch_rows(h, 0, 1, h->nty, h->zchunk)) != VTI_OK) return s;
+            if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk)) != VTI_OK) return s;
         } else {
             const int o = 1 - h->cur;
             // edge tile rows first, so the rows the neighbours need are ready early
-            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty), h->zchunk_edge)) != VTI_OK)
-                return s;
+            if ((s = launch_edge(h)) != VTI_OK) return s;
             if ((s = pack_send(h, o)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
             if ((s = exchange_nccl(h, o)) != VTI_OK) return s;
-            if ((s = launch_rows(h, 1, 1, h->nty - 2, h->zchunk_inner)) != VTI_OK)   // overlaps the exchange
-                return s;
+            if ((s = launch_interior(h)) != VTI_OK) return s;   // overlaps the exchange
             CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         }
         h->cur = 1 - h->cur;
@@ -1056,7 +1283,7 @@ static vti_status group_exchange(vti_t *hs, int n, bool current)
         vti_s *h = hs[i];
         const int b = current ? h->cur : 1 - h->cur;
         CU(h, cudaSetDevice(h->cfg.device));
-        const size_t bytes = halo_floats(h) * 4;
+        const size_t bytes = halo_elems(h) * h->es;
         if (i > 0) {   // my rows from rank-1 = its packed rows for rank+1
             vti_s *g = hs[i - 1];
             CU(h, cudaStreamWaitEvent(h->comm, g->ev_edge, 0));
@@ -1116,8 +1343,7 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
-            if ((s = launch_rows(h, 0, std::max(1, h->nty - 1), std::min(2, h->nty), h->zchunk_edge)) != VTI_OK)
-                return s;
+            if ((s = launch_edge(h)) != VTI_OK) return s;
             if ((s = pack_send(h, 1 - h->cur)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
         }
@@ -1125,7 +1351,7 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
-            if ((s = launch_rows(h, 1, 1, h->nty - 2, h->zchunk_inner)) != VTI_OK) return s;
+            if ((s = launch_interior(h)) != VTI_OK) return s;
         }
         if ((s = group_wait(hs, n)) != VTI_OK) return s;
         for (int i = 0; i < n; ++i) {
@@ -1134,28 +1360,6 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         }
     }
     return VTI_OK;
-}
-
-vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level)
-{
-    if (!h) return VTI_E_PARAM;
-    if (level != 0 && level != 1) return fail(h, VTI_E_PARAM, "level must be 0 (u^n) or 1 (u^{n-1})");
-    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
-        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
-    CU(h, cudaSetDevice(h->cfg.device));
-    CU(h, cudaStreamSynchronize(h->comm));
-    vti_status s;
-    if (any_device({p, q}) && (s = order_after_caller(h)) != VTI_OK) return s;
-    const int b = level == 0 ? h->cur : 1 - h->cur;
-    if (p && (s = download_planes(h, p, h->p_int(b), k0, nk)) != VTI_OK) return s;
-    if (q && (s = download_planes(h, q, h->q_int(b), k0, nk)) != VTI_OK) return s;
-    return VTI_OK;
-}
-
-vti_status vti_get_fields(vti_t h, float *p, float *q, int32_t level)
-{
-    if (!h) return VTI_E_PARAM;
-    return vti_get_fields_planes(h, 0, h->cfg.nz, p, q, level);
 }
 
 vti_status vti_sync(vti_t h)
@@ -1186,7 +1390,9 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->work_items = h->ntx * h->nty * h->nzc;
     if (h->cfg.nranks > 1) {   // edge + interior step kernels, then pack + unpack per neighbour
         const int neighbours = (h->cfg.rank > 0) + (h->cfg.rank < h->cfg.nranks - 1);
-        info->launches_per_step = (h->nty > 2 ? 2 : 1) + 2 * neighbours;
+        int e1, e2;
+        edge_rows(h, e1, e2);
+        info->launches_per_step = 1 + (e2 > e1 ? 1 : 0) + 2 * neighbours;
     } else {
         info->launches_per_step = 1;
     }
@@ -1208,7 +1414,7 @@ vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm)
 vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp)
 {
     if (!h) return VTI_E_PARAM;
-    const KernelEntry *K = find_kernel(h->R, h->RZ, tile_y, producer_warp);
+    const KernelEntry *K = find_kernel(h->es, h->R, h->RZ, tile_y, producer_warp);
     if (!K) return fail(h, VTI_E_UNSUPPORTED, "no compiled variant (r_xy %d, r_z %d, tile_y %d, producer_warp %d)",
                         h->R, h->RZ, tile_y, producer_warp);
     CU(h, cudaSetDevice(h->cfg.device));
@@ -1231,7 +1437,7 @@ vti_status vti_autotune(vti_t h, int32_t probe_steps, vti_tune_result *out)
     const KernelEntry *best_k = keep;
     int best_zc = 0, ncand = 0;
     h->suppress_src = true;   // zero state, no injection: every probe step leaves u == 0
-    for (const KernelEntry *K : all_kernels(h->R, h->RZ)) {
+    for (const KernelEntry *K : all_kernels(h->es, h->R, h->RZ)) {
         h->tune_zchunk = 0;
         vti_status s = select_variant(h, K);
         if (s != VTI_OK) continue;   // e.g. not resident on this device

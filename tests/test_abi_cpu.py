@@ -43,7 +43,8 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version_and_status_strings():
-    assert V.lib.vti_abi_version() == 1
+    hdr = open(HEADER).read()
+    assert f"#define VTI_ABI_VERSION {V.lib.vti_abi_version()}" in hdr
     for code in range(11):
         s = V.lib.vti_status_string(code)
         assert s and s.decode()
@@ -69,7 +70,7 @@ def test_slab_rejects_bad_rank():
 
 def _cfg(**kw):
     d = dict(nx=64, ny=64, nz=64, h=10.0, r_xy=4, r_z=4, dt=1e-3, damp_width=20, damp_alpha=0.015, device=0,
-             stream=None, rank=0, nranks=1, nccl_id=None, check_every=0)
+             stream=None, rank=0, nranks=1, nccl_id=None, check_every=0, precision=32)
     d.update(kw)
     return V.Config(**d)
 
@@ -95,6 +96,7 @@ def _create(cfg, wxy=True, wz=True):
     (dict(ny=12, nranks=4, damp_width=0), "VTI_E_GEOMETRY"),   # slab thinner than R_xy
     (dict(rank=2, nranks=2), "VTI_E_PARAM"),
     (dict(damp_width=-1), "VTI_E_PARAM"),
+    (dict(precision=16), "VTI_E_PARAM"),
 ])
 def test_create_validation_needs_no_gpu(kw, expect):
     assert V.STATUS[_create(_cfg(**kw))] == expect
@@ -132,3 +134,27 @@ def test_binding_rejects_wrong_dtype_or_size():
         V._ptr(np.zeros(3, np.float32), nelem=4)
     with pytest.raises(TypeError):
         V._ptr(np.zeros(4, np.float64), nelem=4, writable=True)
+
+
+def test_create_f64_requires_precision_64():
+    cfg = _cfg()
+    h = C.c_void_p()
+    a = np.zeros(5, np.float64)
+    b = np.zeros(64 * 9, np.float64)
+    assert V.STATUS[V.lib.vti_create_f64(C.byref(h), C.byref(cfg), a.ctypes.data, b.ctypes.data)] == "VTI_E_PARAM"
+    assert b"precision" in V.lib.vti_last_error(None)
+
+
+def test_config_struct_matches_header():
+    """ctypes mirror of vti_config / vti_info has the header's field order."""
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    for struct, cls in (("vti_config", V.Config), ("vti_info", V.Info), ("vti_tune_result", V.TuneResult)):
+        body = re.search(r"typedef struct \{([^{}]*)\}\s*" + struct + ";", src).group(1)
+        names = []
+        for decl in body.split(";"):
+            decl = decl.strip()
+            if not decl:
+                continue
+            decl = re.sub(r"^(const\s+)?[a-z0-9_]+\s*\*?\s*", "", decl)
+            names += [n.strip().lstrip("*") for n in decl.split(",")]
+        assert names == [f for f, _ in cls._fields_], struct

@@ -322,3 +322,34 @@ def test_set_variant_switches_kernel_mid_run():
         p, q = v.get_fields(0)
     po, qo, _, _, _ = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=16)
     assert np.array_equal(p, po) and np.array_equal(q, qo)
+
+
+@pytest.mark.parametrize("ty", [16, 32])
+@pytest.mark.parametrize("ny,nranks", [(66, 2), (67, 2), (100, 3), (98, 2), (140, 4)])
+def test_local_group_short_last_tiles(ty, ny, nranks, monkeypatch):
+    """Slabs whose last tile row is shorter than R_xy: the rows a neighbour receives span
+    two tile rows, and all of them must be in the edge launch (multi-step, bitwise)."""
+    from paper_1410_1387_b200 import VTI, group_step
+    monkeypatch.setenv("VTI_TY", str(ty))
+    cfg = small_cfg(70, ny, 30, 4, 4, damp=5, src=(30, ny // 2, 15))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    st = random_state(cfg, amp=1e-4)
+    g, o = run_both(cfg, 6, state=st, model=model)
+    assert_parity(g, o)
+    hs = [VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], 4, 4, dt, wxy, wz, damp_width=cfg["damp_width"],
+              damp_alpha=cfg["damp_alpha"], rank=r, nranks=nranks) for r in range(nranks)]
+    for h in hs:
+        assert h.info()["tile_y"] == ty
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_model(*[np.ascontiguousarray(a[:, sl]) for a in model])
+        h.set_fields(*[np.ascontiguousarray(a[:, sl]) for a in st])
+        h.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+    group_step(hs, 2)
+    group_step(hs, 4)
+    parts = [h.get_fields(0) + h.get_fields(1) for h in hs]
+    for f in range(4):
+        assert np.array_equal(np.concatenate([p[f] for p in parts], axis=1), g[f])
+    for h in hs:
+        h.close()
