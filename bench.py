@@ -293,11 +293,12 @@ def run_native(args):
     wxy, wz = weights(cfg, prec)
     dt = synth.stable_dt(cfg)
 
-    nccl_id = None
-    if world > 1:
-        obj = [vti.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+    from paper_1410_1387_b200 import multi
+
+    def fresh_nccl_id():
+        return multi.broadcast_nccl_id(dist, rank, world)
+
+    nccl_id = fresh_nccl_id()
 
     def barrier():
         if world > 1:
@@ -305,11 +306,7 @@ def run_native(args):
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return multi.max_over_ranks(dist, world, x, device="cuda")
 
     npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
     v = make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id, prec)
@@ -353,7 +350,7 @@ def run_native(args):
             for dst, src in zip(host_model, m):
                 dst[k0:k0 + nk].copy_(src)
         out_p, out_q = pin(shape), pin(shape)
-        w = make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id, prec)
+        w = make_handle(cfg, dt, wxy, wz, rank, world, local, fresh_nccl_id(), prec)
         if args.zchunk or args.ctas_per_sm:
             w.set_tuning(args.zchunk, args.ctas_per_sm)
         barrier()

@@ -8,8 +8,8 @@ steps its slab with the oracle on an (ny_local + 2R)-row subgrid, exchanging
 halos through torch.distributed (gloo) send/recv in the same neighbour
 pattern as the library's NCCL group, and the gathered result must equal a
 single-domain oracle run bitwise. Also covered: per-rank model-slab
-generation equals the global model's rows, NCCL-id broadcast and the
-max-over-ranks timing reduction used by bench.py.
+generation equals the global model's rows, and bench.py's bootstrap
+(paper_1410_1387_b200.multi: library ncclUniqueId broadcast, max over ranks).
 """
 import os
 import socket
@@ -94,13 +94,15 @@ def _worker(rank, world, port, nsteps, q):
             _exchange(p, R, nyl, rank, world)      # p^{n+1} boundary rows to the neighbours
         mine = [a[:, R:R + nyl] for a in (p, qf, pm, qm)]
 
-        # NCCL-id style broadcast and max-over-ranks timing reduction (bench.py)
-        obj = [b"\x07" * 128 if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        assert obj[0] == b"\x07" * 128
-        t = torch.tensor([float(rank + 1)], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        assert t.item() == float(world)
+        # bench.py's N > 1 bootstrap: a real ncclUniqueId from the library on rank 0,
+        # identical on every rank after the broadcast; fresh per call; max over ranks
+        from paper_1410_1387_b200 import multi
+        ids = [multi.broadcast_nccl_id(dist, rank, world) for _ in range(2)]
+        assert all(len(i) == 128 for i in ids) and ids[0] != ids[1]
+        allids = [None] * world
+        dist.all_gather_object(allids, ids[0])
+        assert all(i == ids[0] for i in allids)
+        assert multi.max_over_ranks(dist, world, float(rank + 1)) == float(world)
 
         gathered = [None] * world
         dist.all_gather_object(gathered, (y0, [m.copy() for m in mine]))
