@@ -185,6 +185,39 @@ vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, floa
 vti_status vti_get_fields_f64(vti_t h, double *p, double *q, int32_t level);
 vti_status vti_get_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, double *p, double *q, int32_t level);
 
+/*
+ * Receivers (the trace-extraction hook of RTM/FWI,
+ * PAPER.md l.18-19): after every subsequent step, the wavefield(s) in
+ * field_mask (1 = p, 2 = q, 3 = both) at the n GLOBAL grid points ijk[3r..3r+2]
+ * are gathered into a device trace buffer, up to capacity_steps rows
+ * (recording then stops silently). Only the receivers inside this rank's slab
+ * are kept (vti_receiver_info lists them). A new call replaces the set and
+ * restarts the recording. n = 0 removes all receivers. Errors: PARAM, INDEX, CUDA.
+ */
+vti_status vti_set_receivers(vti_t h, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t capacity_steps);
+
+/* Local receiver count, rows recorded so far, and (ids != NULL, n_local entries)
+ * the caller's index of each local receiver. */
+vti_status vti_receiver_info(vti_t h, int32_t *n_local, int32_t *steps_recorded, int32_t *ids);
+
+/* Copy the recorded traces, [steps_recorded][n_local][nf] (nf = fields in the
+ * mask, p before q), to out (host or device). Synchronises. */
+vti_status vti_get_traces(vti_t h, float *out);
+vti_status vti_get_traces_f64(vti_t h, double *out);
+
+/*
+ * Time reversal (N4, the backward propagation of RTM): swap the two stored
+ * levels, so the next vti_step applies Eq. 3 backwards,
+ * u^{n-1} = g (2 u^n - g u^{n+1} + dt^2 F(u^n)), with s(t^n) at the current
+ * level and the time index decreasing. Without damping (W = 0) this is the
+ * exact inverse of forward stepping up to rounding; calling it again restores
+ * forward stepping. vti_time_index() is the current level throughout.
+ */
+vti_status vti_reverse(vti_t h);
+
+/* +1 (forward) or -1 (after an odd number of vti_reverse calls). */
+int32_t vti_direction(vti_t h);
+
 /* Block until all work on the handle's stream(s) is done. */
 vti_status vti_sync(vti_t h);
 

@@ -104,6 +104,12 @@ def _load():
         "vti_query": (st, [H, C.POINTER(Info)]),
         "vti_set_tuning": (st, [H, C.c_int32, C.c_int32]),
         "vti_set_variant": (st, [H, C.c_int32, C.c_int32]),
+        "vti_set_receivers": (st, [H, C.c_int32, P, C.c_int32, C.c_int32]),
+        "vti_receiver_info": (st, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32), P]),
+        "vti_get_traces": (st, [H, P]),
+        "vti_get_traces_f64": (st, [H, P]),
+        "vti_reverse": (st, [H]),
+        "vti_direction": (C.c_int32, [H]),
         "vti_autotune": (st, [H, C.c_int32, C.POINTER(TuneResult)]),
         "vti_last_error": (C.c_char_p, [H]),
         "vti_destroy": (st, [H]),
@@ -264,6 +270,37 @@ class VTI:
         qp, _ = _ptr(q, self._n(nk), writable=True, dtype=self.dtype)
         _check(self.h, self._fn("vti_get_fields_planes")(self.h, k0, nk, pp, qp, level))
         return p, q
+
+    # -- receivers and time reversal
+    def set_receivers(self, ijk, fields=1, capacity_steps=1000):
+        """ijk: (n, 3) global (i, j, k) receiver points; fields: 1 = p, 2 = q, 3 = both."""
+        a = np.ascontiguousarray(np.asarray(ijk, dtype=np.int32).reshape(-1, 3))
+        _check(self.h, lib.vti_set_receivers(self.h, a.shape[0], a.ctypes.data if a.size else None, fields,
+                                             capacity_steps))
+        self._rec_fields = (fields & 1) + ((fields >> 1) & 1)
+
+    def receiver_info(self):
+        n, t = C.c_int32(), C.c_int32()
+        _check(self.h, lib.vti_receiver_info(self.h, C.byref(n), C.byref(t), None))
+        ids = np.zeros(n.value, np.int32)
+        if n.value:
+            _check(self.h, lib.vti_receiver_info(self.h, None, None, ids.ctypes.data))
+        return ids, t.value
+
+    def get_traces(self):
+        """(ids, traces[steps][n_local][nf]) of this rank's receivers."""
+        ids, steps = self.receiver_info()
+        out = np.zeros((steps, len(ids), getattr(self, "_rec_fields", 1)), dtype=self.dtype)
+        if out.size:
+            _check(self.h, self._fn("vti_get_traces")(self.h, out.ctypes.data))
+        return ids, out
+
+    def reverse(self):
+        _check(self.h, lib.vti_reverse(self.h))
+
+    @property
+    def direction(self) -> int:
+        return lib.vti_direction(self.h)
 
     @property
     def time_index(self) -> int:

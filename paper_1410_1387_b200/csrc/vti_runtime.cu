@@ -262,6 +262,20 @@ __global__ void k_unpack_rows(const T *__restrict__ in, T *__restrict__ buf, int
     }
 }
 
+// Receivers: after each step, gather u^n at the receiver
+// points (interior-view element offsets) into trace row t: out[t][r][f].
+template <typename T>
+__global__ void k_record(const T *__restrict__ p, const T *__restrict__ q, const long long *__restrict__ off, int n,
+                         int mask, T *__restrict__ out)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int nf = (mask & 1) + ((mask >> 1) & 1);
+    int f = 0;
+    if (mask & 1) out[(size_t)r * nf + f++] = p[off[r]];
+    if (mask & 2) out[(size_t)r * nf + f] = q[off[r]];
+}
+
 // ============================================================ handle
 struct vti_s {
     vti_config cfg{};
@@ -311,6 +325,12 @@ struct vti_s {
     bool halo_dirty = false;
     bool suppress_src = false;                // autotune probes inject nothing
     bool fields_touched = false;              // vti_set_fields* called (state may be non-zero)
+    int dir = 1;                              // +1 forward in time, -1 after vti_reverse
+    // receivers (this slab's subset, in the caller's order)
+    int nrec = 0, rec_mask = 0, rec_cap = 0, rec_steps = 0;
+    long long *rec_off = nullptr;             // device: element offsets in an interior view
+    void *traces = nullptr;                   // device: [rec_cap][nrec][nf] of T
+    std::vector<int32_t> rec_ids;             // global receiver index of each local receiver
 
     size_t total_elems() const { return (size_t)cfg.nz * rows * nxp; }
     char *in(void *base) const { return (char *)base + (long long)R * ys * es; }   // interior view
@@ -582,6 +602,8 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->counters);
     cudaFree(h->flag);
     cudaFree(h->sync_ctr);
+    cudaFree(h->rec_off);
+    cudaFree(h->traces);
     for (cudaEvent_t e : {h->ev_edge, h->ev_comm, h->ev_t0, h->ev_t1})
         if (e) cudaEventDestroy(e);
     if (h->comm) cudaStreamDestroy(h->comm);
@@ -1089,7 +1111,108 @@ static vti_status check_finite(vti_s *h)
     return VTI_OK;
 }
 
+// Gather the receivers' u^n (just written) into the next trace row; silently
+// stops when the capacity is reached (vti_get_traces reports the count).
+static vti_status record(vti_s *h)
+{
+    if (h->nrec == 0 || h->rec_steps >= h->rec_cap || h->suppress_src) return VTI_OK;   // not during autotune probes
+    const int nf = (h->rec_mask & 1) + ((h->rec_mask >> 1) & 1);
+    const size_t row = (size_t)h->nrec * nf * h->es;
+    char *dst = (char *)h->traces + (size_t)h->rec_steps * row;
+    const int threads = 128, blocks = (h->nrec + threads - 1) / threads;
+    if (h->es == 8)
+        k_record<double><<<blocks, threads, 0, h->stream>>>((const double *)h->p_int(h->cur),
+                                                            (const double *)h->q_int(h->cur), h->rec_off, h->nrec,
+                                                            h->rec_mask, (double *)dst);
+    else
+        k_record<float><<<blocks, threads, 0, h->stream>>>((const float *)h->p_int(h->cur),
+                                                           (const float *)h->q_int(h->cur), h->rec_off, h->nrec,
+                                                           h->rec_mask, (float *)dst);
+    CU(h, cudaGetLastError());
+    h->rec_steps += 1;
+    return VTI_OK;
+}
+
 extern "C" {
+
+vti_status vti_set_receivers(vti_t h, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t capacity_steps)
+{
+    if (!h) return VTI_E_PARAM;
+    if (n < 0 || capacity_steps < 0 || (n > 0 && !ijk)) return fail(h, VTI_E_PARAM, "bad receiver arguments");
+    if (n > 0 && (field_mask < 1 || field_mask > 3)) return fail(h, VTI_E_PARAM, "field_mask must be 1, 2 or 3");
+    std::vector<long long> off;
+    std::vector<int32_t> ids;
+    for (int r = 0; r < n; ++r) {
+        const int i = ijk[3 * r], j = ijk[3 * r + 1], k = ijk[3 * r + 2];
+        if (i < 0 || i >= h->cfg.nx || j < 0 || j >= h->cfg.ny || k < 0 || k >= h->cfg.nz)
+            return fail(h, VTI_E_INDEX, "receiver %d (%d,%d,%d) outside the grid", r, i, j, k);
+        if (j < h->y0 || j >= h->y0 + h->nyl) continue;   // another rank's slab
+        off.push_back((long long)(j - h->y0) * h->ys + (long long)k * h->zs + i);
+        ids.push_back(r);
+    }
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    cudaFree(h->rec_off);
+    cudaFree(h->traces);
+    h->rec_off = nullptr;
+    h->traces = nullptr;
+    h->nrec = (int)off.size();
+    h->rec_ids = ids;
+    h->rec_mask = field_mask;
+    h->rec_cap = capacity_steps;
+    h->rec_steps = 0;
+    if (h->nrec > 0 && capacity_steps > 0) {
+        const int nf = (field_mask & 1) + ((field_mask >> 1) & 1);
+        CU(h, cudaMalloc((void **)&h->rec_off, off.size() * sizeof(long long)));
+        CU(h, cudaMemcpy(h->rec_off, off.data(), off.size() * sizeof(long long), cudaMemcpyHostToDevice));
+        CU(h, cudaMalloc(&h->traces, (size_t)capacity_steps * h->nrec * nf * h->es));
+    }
+    return VTI_OK;
+}
+
+vti_status vti_receiver_info(vti_t h, int32_t *n_local, int32_t *steps_recorded, int32_t *ids)
+{
+    if (!h) return VTI_E_PARAM;
+    if (n_local) *n_local = h->nrec;
+    if (steps_recorded) *steps_recorded = h->rec_steps;
+    if (ids)
+        for (int r = 0; r < h->nrec; ++r) ids[r] = h->rec_ids[r];
+    return VTI_OK;
+}
+
+static vti_status get_traces(vti_s *h, int es, void *out)
+{
+    if (!h) return VTI_E_PARAM;
+    vti_status s = check_precision(h, es, "vti_get_traces");
+    if (s != VTI_OK) return s;
+    if (!out) return fail(h, VTI_E_PARAM, "NULL output");
+    if (h->nrec == 0 || h->rec_steps == 0) return VTI_OK;
+    const int nf = (h->rec_mask & 1) + ((h->rec_mask >> 1) & 1);
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    CU(h, cudaMemcpy(out, h->traces, (size_t)h->rec_steps * h->nrec * nf * h->es, cudaMemcpyDefault));
+    return VTI_OK;
+}
+
+vti_status vti_get_traces(vti_t h, float *out) { return get_traces(h, 4, out); }
+vti_status vti_get_traces_f64(vti_t h, double *out) { return get_traces(h, 8, out); }
+
+vti_status vti_reverse(vti_t h)
+{
+    if (!h) return VTI_E_PARAM;
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    CU(h, cudaStreamSynchronize(h->comm));
+    // the stored levels (u^n, u^{n-dir}) become (u^{n-dir}, u^n): the next step applies Eq. 3
+    // at level n - dir and produces level n - 2 dir
+    h->cur = 1 - h->cur;
+    h->n -= h->dir;
+    h->dir = -h->dir;
+    h->halo_dirty = h->cfg.nranks > 1;   // re-exchange the new current level's halo rows
+    return VTI_OK;
+}
+
+int32_t vti_direction(vti_t h) { return h ? h->dir : 0; }
 
 vti_status vti_create(vti_t *out, const vti_config *cfg, const float *w_xy, const float *w_z)
 {
@@ -1254,7 +1377,8 @@ vti_status vti_step(vti_t h, int32_t nsteps)
             CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         }
         h->cur = 1 - h->cur;
-        h->n += 1;
+        h->n += h->dir;
+        if ((s = record(h)) != VTI_OK) return s;
         if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0)
             if ((s = check_finite(h)) != VTI_OK) return s;
     }
@@ -1356,7 +1480,8 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         if ((s = group_wait(hs, n)) != VTI_OK) return s;
         for (int i = 0; i < n; ++i) {
             hs[i]->cur = 1 - hs[i]->cur;
-            hs[i]->n += 1;
+            hs[i]->n += hs[i]->dir;
+            if ((s = record(hs[i])) != VTI_OK) return s;
         }
     }
     return VTI_OK;
