@@ -124,12 +124,14 @@ static KernelEntry entry()
 
 // Compiled variants; the first match is the default for (precision, radius pair).
 // -1 = any (env VTI_TY, VTI_WP or vti_set_variant select the others).
-static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp)
+static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, int rpt = -1)
 {
     static const KernelEntry table[] = {
-        // fp32 (BASELINE.json configs)
+        // fp32 (BASELINE.json configs). RPT = 2 rows per thread halves the y-neighbour
+        // shared-memory reads (8 warps, up to 255 registers); measured slower than
+        // RPT = 1 on every config (C2 187 vs 193), kept for (4,4) as an autotune candidate
         entry<float, 4, 4, 32, 1, 1, 3, 1>(),   entry<float, 4, 4, 32, 1, 0, 3, 1>(),
-        entry<float, 4, 4, 16, 1, 1, 3, 2>(),
+        entry<float, 4, 4, 32, 2, 0, 3, 1>(),   entry<float, 4, 4, 16, 1, 1, 3, 2>(),
         entry<float, 8, 4, 32, 1, 1, 3, 1>(),   entry<float, 8, 4, 32, 1, 0, 3, 1>(),
         entry<float, 8, 4, 16, 1, 1, 3, 2>(),
         entry<float, 6, 6, 32, 1, 0, 3, 1>(),   entry<float, 6, 6, 32, 1, 1, 3, 1>(),
@@ -143,7 +145,8 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp)
         entry<double, 12, 8, 16, 1, 1, 2, 1>(), entry<double, 12, 8, 16, 1, 0, 2, 1>(),
     };
     for (const auto &e : table)
-        if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp))
+        if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp) &&
+            (rpt < 0 || e.rpt == rpt))
             return &e;
     return nullptr;
 }
@@ -151,10 +154,11 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp)
 static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
+    const KernelEntry *e;
     for (int ty : {32, 16})
         for (int wp : {1, 0})
-            if (const KernelEntry *e = find_kernel(esize, r, rz, ty, wp))
-                if (e->ty == ty && e->wp == wp) v.push_back(e);
+            for (int rpt : {1, 2})
+                if ((e = find_kernel(esize, r, rz, ty, wp, rpt)) != nullptr) v.push_back(e);
     return v;
 }
 
@@ -684,10 +688,11 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     h->es = precision_bits(cfg) / 8;
     h->R = cfg->r_xy;
     h->RZ = cfg->r_z;
-    int want_ty = -1, want_wp = -1;
+    int want_ty = -1, want_wp = -1, want_rpt = -1;
     if (const char *e = getenv("VTI_TY")) want_ty = atoi(e);
     if (const char *e = getenv("VTI_WP")) want_wp = atoi(e);
-    h->K = find_kernel(h->es, h->R, h->RZ, want_ty, want_wp);
+    if (const char *e = getenv("VTI_RPT")) want_rpt = atoi(e);
+    h->K = find_kernel(h->es, h->R, h->RZ, want_ty, want_wp, want_rpt);
     if (!h->K) h->K = find_kernel(h->es, h->R, h->RZ, -1, -1);
     if (!h->K)
         return fail(h, VTI_E_UNSUPPORTED, "(r_xy, r_z) = (%d, %d) not compiled for fp%d", h->R, h->RZ, 8 * h->es);
@@ -1510,6 +1515,8 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->layout = h->layout_zyx ? 0 : 1;
     info->tile_x = TX;
     info->tile_y = h->TY;
+    info->rows_per_thread = h->K->rpt;
+    info->producer_warp = h->K->wp;
     info->zchunk = h->zchunk;
     info->grid = std::min(h->ntx * h->nty * h->nzc, h->sms * h->ctas_per_sm);
     info->work_items = h->ntx * h->nty * h->nzc;
@@ -1536,12 +1543,13 @@ vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm)
     return select_variant(h, h->K);
 }
 
-vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp)
+vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp, int32_t rows_per_thread)
 {
     if (!h) return VTI_E_PARAM;
-    const KernelEntry *K = find_kernel(h->es, h->R, h->RZ, tile_y, producer_warp);
-    if (!K) return fail(h, VTI_E_UNSUPPORTED, "no compiled variant (r_xy %d, r_z %d, tile_y %d, producer_warp %d)",
-                        h->R, h->RZ, tile_y, producer_warp);
+    const KernelEntry *K = find_kernel(h->es, h->R, h->RZ, tile_y, producer_warp, rows_per_thread);
+    if (!K)
+        return fail(h, VTI_E_UNSUPPORTED, "no compiled variant (fp%d, r_xy %d, r_z %d, tile_y %d, producer_warp %d, rpt %d)",
+                    8 * h->es, h->R, h->RZ, tile_y, producer_warp, rows_per_thread);
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaStreamSynchronize(h->stream));
     return select_variant(h, K);
@@ -1595,6 +1603,7 @@ vti_status vti_autotune(vti_t h, int32_t probe_steps, vti_tune_result *out)
     if (out) {
         out->tile_y = h->K->ty;
         out->producer_warp = h->K->wp;
+        out->rows_per_thread = h->K->rpt;
         out->zchunk = h->zchunk;
         out->ms_per_step = best_ms / probe_steps;
         out->candidates = ncand;

@@ -70,7 +70,7 @@ def check(g, o):
 def test_fp64_random_state_ragged(r, rz, wp):
     cfg = cfg_of(77, 45, 41, r, rz, src=(30, 22, 20))
     model, st = inputs(cfg)
-    g, o = run64(cfg, 4, st, model, variant=(16, wp))
+    g, o = run64(cfg, 4, st, model, variant=(16, wp, 1))
     check(g, o)
 
 

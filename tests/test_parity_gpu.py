@@ -263,11 +263,13 @@ def test_local_group_slabs_bitwise_equal_single(nranks):
 
 
 @pytest.mark.parametrize("r,rz", [(4, 4), (8, 4), (6, 6), (12, 8)])
-@pytest.mark.parametrize("ty,wp", [(32, 1), (32, 0), (16, -1)])
-def test_every_compiled_variant(r, rz, ty, wp, monkeypatch):
-    """Each (tile height, producer-warp) instantiation is bitwise equal to the oracle."""
+@pytest.mark.parametrize("ty,wp,rpt", [(32, 1, 1), (32, 0, 1), (32, 0, 2), (16, -1, 1)])
+def test_every_compiled_variant(r, rz, ty, wp, rpt, monkeypatch):
+    """Each (tile height, producer-warp, rows-per-thread) instantiation is bitwise equal to the oracle
+    (a combination not compiled for the pair falls back to the default, also checked)."""
     monkeypatch.setenv("VTI_TY", str(ty))
     monkeypatch.setenv("VTI_WP", str(wp))
+    monkeypatch.setenv("VTI_RPT", str(rpt))
     cfg = small_cfg(77, 45, 41, r, rz, damp=5, src=(30, 22, 20))
     st = random_state(cfg, seed=9)
     g, o = run_both(cfg, 4, state=st, model=random_model(cfg, seed=5), n0=2)
@@ -316,11 +318,14 @@ def test_set_variant_switches_kernel_mid_run():
             v.set_variant(ty, wp)
             assert v.info()["tile_y"] == ty
             v.step(4)
+        v.set_variant(32, 0, 2)
+        assert v.info()["rows_per_thread"] == 2
+        v.step(3)
         with pytest.raises(VTIError) as e:
             v.set_variant(8, 1)
         assert e.value.name == "VTI_E_UNSUPPORTED"
         p, q = v.get_fields(0)
-    po, qo, _, _, _ = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=16)
+    po, qo, _, _, _ = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=19)
     assert np.array_equal(p, po) and np.array_equal(q, qo)
 
 
