@@ -43,7 +43,11 @@ def launches(path):
 
 
 def raw(report):
-    txt = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Counters of a --set full capture: an .ncu-rep (exported here) or its raw-page CSV export."""
+    if report.endswith(".csv"):
+        txt = open(report).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -70,6 +74,7 @@ def main():
     ap.add_argument("--grid", type=int, nargs=3, required=True)
     ap.add_argument("--round", default="r01")
     ap.add_argument("--bytes-per-point", type=float, default=36.0)
+    ap.add_argument("--key", default=None, help="entry name in profiles/ncu_summary.json (default --name)")
     a = ap.parse_args()
     out = {"config": a.name, "grid": a.grid, "round": a.round}
     npts = a.grid[0] * a.grid[1] * a.grid[2]
@@ -95,12 +100,13 @@ def main():
                 "traffic_over_algorithmic": (rd + wr) / (a.bytes_per_point * npts),
                 "dram_bytes_per_point": (rd + wr) / npts, "duration_s": t, "dram_GBps": (rd + wr) / t / 1e9,
             }
-    path = os.path.join("profiles", f"ncu_{a.name}_{a.round}.json")
+    key = a.key or a.name
+    path = os.path.join("profiles", f"ncu_{key}_{a.round}.json")
     json.dump(out, open(path, "w"), indent=1)
     summ = os.path.join("profiles", "ncu_summary.json")
     s = json.load(open(summ)) if os.path.exists(summ) else {}
     if "step_kernel" in out:
-        s[a.name] = {"grid": a.grid, "round": a.round, "dram_bytes_per_launch": out["step_kernel"]["dram_bytes_per_launch"],
+        s[key] = {"grid": a.grid, "round": a.round, "dram_bytes_per_launch": out["step_kernel"]["dram_bytes_per_launch"],
                      "source": os.path.basename(path)}
         json.dump(s, open(summ, "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "full_set"}, indent=1))
