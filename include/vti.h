@@ -49,7 +49,7 @@ typedef struct vti_s *vti_t;
 typedef enum {
     VTI_OK = 0,
     VTI_E_PARAM = 1,        /* bad scalar argument: radius, h, dt, mask, NULL pointer */
-    VTI_E_GEOMETRY = 2,     /* bad extents: too few planes, 2W >= extent, slab thinner than R_xy (l.59, l.136) */
+    VTI_E_GEOMETRY = 2,     /* bad extents: nz < 2R_z+1, 2W >= extent, y-slabs thinner than R_xy (l.59, l.136) */
     VTI_E_MODEL = 3,        /* vz2 <= 0 or non-finite model value */
     VTI_E_ANISO = 4,        /* reserved: strict eps >= delta check (warn-only by default) */
     VTI_E_INSTABILITY = 5,  /* non-finite wavefield detected (check_every > 0) */

@@ -484,7 +484,7 @@ static vti_status check_cfg(const vti_config *c)
     if (c->damp_width > 0 && (2 * c->damp_width >= c->nx || 2 * c->damp_width >= c->ny || 2 * c->damp_width >= c->nz))
         return VTI_E_GEOMETRY;
     if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return VTI_E_PARAM;
-    if (c->ny / c->nranks < c->r_xy) return VTI_E_GEOMETRY;   // slab thinner than the halo
+    if (c->nranks > 1 && c->ny / c->nranks < c->r_xy) return VTI_E_GEOMETRY;   // slab thinner than the halo
     return VTI_OK;
 }
 

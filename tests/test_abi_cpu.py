@@ -94,6 +94,7 @@ def _create(cfg, wxy=True, wz=True):
     (dict(nz=8), "VTI_E_GEOMETRY"),              # fewer than 2 Rz + 1 planes
     (dict(damp_width=32), "VTI_E_GEOMETRY"),     # 2W >= extent
     (dict(ny=12, nranks=4, damp_width=0), "VTI_E_GEOMETRY"),   # slab thinner than R_xy
+    (dict(nx=1, ny=1, nz=8, damp_width=0), "VTI_E_GEOMETRY"),  # nz < 2 R_z + 1 (thin x, y are fine)
     (dict(rank=2, nranks=2), "VTI_E_PARAM"),
     (dict(damp_width=-1), "VTI_E_PARAM"),
     (dict(precision=16), "VTI_E_PARAM"),

@@ -358,3 +358,34 @@ def test_local_group_short_last_tiles(ty, ny, nranks, monkeypatch):
         assert np.array_equal(np.concatenate([p[f] for p in parts], axis=1), g[f])
     for h in hs:
         h.close()
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 9), (1, 40, 9), (37, 1, 12), (1, 1, 17), (5, 3, 9)])
+def test_degenerate_thin_grids(shape):
+    """Grids thinner than the stencil in x and/or y (the zero exterior does all the work)."""
+    nx, ny, nz = shape
+    cfg = small_cfg(nx, ny, nz, 4, 4, damp=0, src=(nx // 2, ny // 2, nz // 2))
+    st = random_state(cfg, amp=1e-2)
+    g, o = run_both(cfg, 7, state=st, model=random_model(cfg))
+    assert_parity(g, o)
+
+
+def test_zero_steps_and_zero_amplitude():
+    cfg = small_cfg(40, 30, 20, 4, 4, damp=3)
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    st = random_state(cfg)
+    with make(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.set_fields(*st, time_index=7)
+        v.step(0)                                   # no-op
+        assert v.time_index == 7
+        p, q = v.get_fields(0)
+        assert np.array_equal(p, st[0]) and np.array_equal(q, st[1])
+    with make(cfg, dt, wxy, wz) as v:               # zero state, zero-amplitude source: stays exactly zero
+        v.set_model(*model)
+        v.add_source(*cfg["src"], amp=0.0)
+        v.step(10)
+        p, q = v.get_fields(0)
+        assert not p.any() and not q.any()
