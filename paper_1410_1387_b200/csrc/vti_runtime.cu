@@ -131,13 +131,15 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, 
         // shared-memory reads (8 warps, up to 255 registers); measured slower than
         // RPT = 1 on every config (C2 187 vs 193), kept for (4,4) as an autotune candidate
         entry<float, 4, 4, 32, 1, 1, 3, 1>(),   entry<float, 4, 4, 32, 1, 0, 3, 1>(),
-        entry<float, 4, 4, 32, 2, 0, 3, 1>(),   entry<float, 4, 4, 16, 1, 1, 3, 2>(),
+        entry<float, 4, 4, 30, 1, 1, 3, 1>(),   entry<float, 4, 4, 32, 2, 0, 3, 1>(),
+        entry<float, 4, 4, 16, 1, 1, 3, 2>(),
         entry<float, 8, 4, 32, 1, 1, 3, 1>(),   entry<float, 8, 4, 32, 1, 0, 3, 1>(),
-        entry<float, 8, 4, 16, 1, 1, 3, 2>(),
-        entry<float, 6, 6, 32, 1, 0, 3, 1>(),   entry<float, 6, 6, 32, 1, 1, 3, 1>(),
-        entry<float, 6, 6, 16, 1, 0, 3, 2>(),
-        entry<float, 12, 8, 32, 1, 1, 3, 1>(),  entry<float, 12, 8, 32, 1, 0, 3, 1>(),
-        entry<float, 12, 8, 16, 1, 0, 2, 2>(),
+        entry<float, 8, 4, 30, 1, 1, 3, 1>(),   entry<float, 8, 4, 16, 1, 1, 3, 2>(),
+        // TY = 30 + producer warp: 16 warps -> 128 registers without the in-line producer
+        entry<float, 6, 6, 30, 1, 1, 3, 1>(),   entry<float, 6, 6, 32, 1, 0, 3, 1>(),
+        entry<float, 6, 6, 32, 1, 1, 3, 1>(),   entry<float, 6, 6, 16, 1, 0, 3, 2>(),
+        entry<float, 12, 8, 30, 1, 1, 3, 1>(),  entry<float, 12, 8, 32, 1, 1, 3, 1>(),
+        entry<float, 12, 8, 32, 1, 0, 3, 1>(),  entry<float, 12, 8, 16, 1, 0, 2, 2>(),
         // fp64: 16-row tiles so three stages fit in shared memory
         entry<double, 4, 4, 16, 1, 1, 3, 1>(),  entry<double, 4, 4, 16, 1, 0, 3, 1>(),
         entry<double, 8, 4, 16, 1, 1, 3, 1>(),  entry<double, 8, 4, 16, 1, 0, 3, 1>(),
@@ -155,7 +157,7 @@ static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
     const KernelEntry *e;
-    for (int ty : {32, 16})
+    for (int ty : {32, 30, 16})
         for (int wp : {1, 0})
             for (int rpt : {1, 2})
                 if ((e = find_kernel(esize, r, rz, ty, wp, rpt)) != nullptr) v.push_back(e);

@@ -288,7 +288,7 @@ def test_autotune_then_parity(r, rz):
         v.set_model(*model)
         v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
         res = v.autotune(probe_steps=2)
-        assert res["candidates"] >= 3 and res["tile_y"] in (16, 32) and res["ms_per_step"] > 0
+        assert res["candidates"] >= 3 and res["tile_y"] in (16, 30, 32) and res["ms_per_step"] > 0
         assert v.time_index == 0
         p0, q0 = v.get_fields(0)
         assert not p0.any() and not q0.any()          # probes left the zero state untouched
