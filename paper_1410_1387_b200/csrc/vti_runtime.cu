@@ -140,11 +140,16 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, 
         entry<float, 6, 6, 32, 1, 1, 3, 1>(),   entry<float, 6, 6, 16, 1, 0, 3, 2>(),
         entry<float, 12, 8, 30, 1, 1, 3, 1>(),  entry<float, 12, 8, 32, 1, 1, 3, 1>(),
         entry<float, 12, 8, 32, 1, 0, 3, 1>(),  entry<float, 12, 8, 16, 1, 0, 2, 2>(),
-        // fp64: 16-row tiles so three stages fit in shared memory
+        // fp64: 16- or 14-row tiles so three stages fit in shared
+        // memory; TY = 14 + producer warp = 8 warps -> up to 255 registers (R_z >= 6 queues)
         entry<double, 4, 4, 16, 1, 1, 3, 1>(),  entry<double, 4, 4, 16, 1, 0, 3, 1>(),
+        entry<double, 4, 4, 14, 1, 1, 3, 1>(),
         entry<double, 8, 4, 16, 1, 1, 3, 1>(),  entry<double, 8, 4, 16, 1, 0, 3, 1>(),
-        entry<double, 6, 6, 16, 1, 0, 3, 1>(),  entry<double, 6, 6, 16, 1, 1, 3, 1>(),
-        entry<double, 12, 8, 16, 1, 1, 2, 1>(), entry<double, 12, 8, 16, 1, 0, 2, 1>(),
+        entry<double, 8, 4, 14, 1, 1, 3, 1>(),
+        entry<double, 6, 6, 14, 1, 1, 3, 1>(),  entry<double, 6, 6, 16, 1, 0, 3, 1>(),
+        entry<double, 6, 6, 16, 1, 1, 3, 1>(),
+        entry<double, 12, 8, 14, 1, 1, 3, 1>(), entry<double, 12, 8, 16, 1, 1, 2, 1>(),
+        entry<double, 12, 8, 16, 1, 0, 2, 1>(),
     };
     for (const auto &e : table)
         if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp) &&
@@ -157,7 +162,7 @@ static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
     const KernelEntry *e;
-    for (int ty : {32, 30, 16})
+    for (int ty : {32, 30, 16, 14})
         for (int wp : {1, 0})
             for (int rpt : {1, 2})
                 if ((e = find_kernel(esize, r, rz, ty, wp, rpt)) != nullptr) v.push_back(e);
