@@ -101,6 +101,23 @@ const char *vti_status_string(vti_status s);
  * ranks getting one extra row. Host-only; never touches the GPU. */
 vti_status vti_slab(const vti_config *cfg, int32_t *y0, int32_t *ny_local);
 
+typedef struct {
+    int32_t y0, ny_local;            /* this rank's slab (vti_slab) */
+    int32_t ntx, nty;                /* 64 x tile_y tiles over the slab */
+    int32_t edge_lo, edge_hi;        /* nranks > 1: tile rows [0, edge_lo) and [edge_hi, nty) are the edge launch
+                                        (every tile row touching the first or last r_xy rows); [edge_lo, edge_hi)
+                                        the interior launch */
+    int32_t zchunk;                  /* planes per work item, single launch over all tile rows */
+    int32_t zchunk_edge, zchunk_inner; /* the same for the edge / interior launches */
+    int32_t items, grid;             /* work items and CTAs of the single launch */
+} vti_plan_info;
+
+/* The schedule the library would use for cfg with tile height tile_y on a GPU
+ * with `sms` multiprocessors and `ctas_per_sm` resident step CTAs per SM.
+ * Host-only (never touches the GPU): the same functions vti_create uses.
+ * Errors: PARAM / GEOMETRY as vti_create's validation. */
+vti_status vti_plan(const vti_config *cfg, int32_t tile_y, int32_t sms, int32_t ctas_per_sm, vti_plan_info *out);
+
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 calls it, then broadcasts).
  * VTI_E_COMM if NCCL cannot be loaded. */
 vti_status vti_nccl_unique_id(void *out128);

@@ -54,6 +54,15 @@ class TuneResult(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class PlanInfo(C.Structure):
+    _fields_ = [("y0", C.c_int32), ("ny_local", C.c_int32), ("ntx", C.c_int32), ("nty", C.c_int32),
+                ("edge_lo", C.c_int32), ("edge_hi", C.c_int32), ("zchunk", C.c_int32),
+                ("zchunk_edge", C.c_int32), ("zchunk_inner", C.c_int32), ("items", C.c_int32), ("grid", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Info(C.Structure):
     _fields_ = [
         ("y0", C.c_int32), ("ny_local", C.c_int32), ("nx_pad", C.c_int32), ("layout", C.c_int32),
@@ -80,6 +89,7 @@ def _load():
         "vti_status_string": (C.c_char_p, [st]),
         "vti_slab": (st, [C.POINTER(Config), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "vti_nccl_unique_id": (st, [P]),
+        "vti_plan": (st, [C.POINTER(Config), C.c_int32, C.c_int32, C.c_int32, C.POINTER(PlanInfo)]),
         "vti_create": (st, [C.POINTER(H), C.POINTER(Config), P, P]),
         "vti_create_f64": (st, [C.POINTER(H), C.POINTER(Config), P, P]),
         "vti_set_model_f64": (st, [H, P, P, P]),
@@ -166,6 +176,15 @@ def slab(ny: int, rank: int, nranks: int):
     y0, n = C.c_int32(), C.c_int32()
     _check(None, lib.vti_slab(C.byref(c), C.byref(y0), C.byref(n)))
     return y0.value, n.value
+
+
+def plan(nx, ny, nz, r_xy, r_z, tile_y=32, sms=148, ctas_per_sm=1, rank=0, nranks=1, damp_width=0) -> dict:
+    """The library's host-side schedule for a configuration (no GPU needed)."""
+    c = Config(nx=nx, ny=ny, nz=nz, h=10.0, r_xy=r_xy, r_z=r_z, dt=1e-3, damp_width=damp_width, damp_alpha=0.015,
+               rank=rank, nranks=nranks, precision=32)
+    out = PlanInfo()
+    _check(None, lib.vti_plan(C.byref(c), tile_y, sms, ctas_per_sm, C.byref(out)))
+    return out.as_dict()
 
 
 def nccl_unique_id() -> bytes:

@@ -420,24 +420,28 @@ static vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx
     return VTI_OK;
 }
 
+// ---- host-side planning (pure functions; exported for tests as vti_plan)
 // Work items are (tile, z-chunk). Measured on B200: full z
 // columns marching in lockstep keep the p apron re-reads in L2 and avoid the
 // 2Rz-plane q priming of each chunk, and ~110 resident CTAs already saturate
 // HBM (C2: 128 columns on 148 SMs beat 1024 chunks). The chunk count per
 // launch minimises a wave cost: each round of a active CTAs costs
 // zchunk * a / min(a, SAT), times the priming overhead 1 + 8 Rz / (36 zchunk).
-static int choose_zchunk(const vti_s *h, int tiles)
+static double sat_ctas(int ctas_per_sm)
 {
-    const int nz = h->cfg.nz;
-    if (h->tune_zchunk > 0) return std::min(h->tune_zchunk, nz);
-    if (tiles <= 0) return nz;
-    const int slots = h->sms * h->ctas_per_sm;
-    double sat = 110.0 * h->ctas_per_sm;
+    double sat = 110.0 * ctas_per_sm;
     if (const char *e = getenv("VTI_SAT")) sat = atof(e);
+    return sat;
+}
+
+static int plan_zchunk(int nz, int rz, int tiles, int slots, double sat, int tune_zchunk)
+{
+    if (tune_zchunk > 0) return std::min(tune_zchunk, nz);
+    if (tiles <= 0 || slots <= 0) return nz;
     sat = std::max(1.0, std::min(sat, (double)slots));
     double best = 1e300;
     int best_zc = nz;
-    const int max_nzc = std::max(1, nz / (4 * h->RZ));
+    const int max_nzc = std::max(1, nz / (4 * rz));
     for (int nzc = 1; nzc <= max_nzc; ++nzc) {
         const int zc = (nz + nzc - 1) / nzc;
         if ((nz + zc - 1) / zc != nzc) continue;   // same chunking as a smaller nzc
@@ -445,7 +449,7 @@ static int choose_zchunk(const vti_s *h, int tiles)
         const long full = items / slots, last = items % slots;
         double cost = (double)full * zc * slots / std::min<double>(slots, sat);
         if (last) cost += (double)zc * last / std::min<double>(last, sat);
-        cost *= 1.0 + (8.0 * h->RZ) / (36.0 * zc);
+        cost *= 1.0 + (8.0 * rz) / (36.0 * zc);
         if (cost < best * (1.0 - 1e-3)) {
             best = cost;
             best_zc = zc;
@@ -457,11 +461,18 @@ static int choose_zchunk(const vti_s *h, int tiles)
 // nranks > 1: the edge launch covers every tile row that intersects the first
 // or the last R_xy rows of the slab (the rows the neighbours receive), i.e.
 // tile rows [0, e1) and [e2, nty); the interior launch covers [e1, e2).
-static void edge_rows(const vti_s *h, int &e1, int &e2)
+static void plan_edge_rows(int nty, int r, int ty, int nyl, int &e1, int &e2)
 {
-    e1 = std::min(h->nty, (h->R + h->TY - 1) / h->TY);
-    e2 = std::max(e1, std::min(h->nty, (h->nyl - h->R) / h->TY));
+    e1 = std::min(nty, (r + ty - 1) / ty);
+    e2 = std::max(e1, std::min(nty, (nyl - r) / ty));
 }
+
+static int choose_zchunk(const vti_s *h, int tiles)
+{
+    return plan_zchunk(h->cfg.nz, h->RZ, tiles, h->sms * h->ctas_per_sm, sat_ctas(h->ctas_per_sm), h->tune_zchunk);
+}
+
+static void edge_rows(const vti_s *h, int &e1, int &e2) { plan_edge_rows(h->nty, h->R, h->TY, h->nyl, e1, e2); }
 
 // Default schedule: one launch over all tile rows (single slab), or an edge
 // launch plus an interior launch (nranks > 1).
@@ -581,6 +592,29 @@ vti_status vti_slab(const vti_config *cfg, int32_t *y0, int32_t *ny_local)
     const int base = cfg->ny / cfg->nranks, extra = cfg->ny % cfg->nranks;
     *ny_local = base + (cfg->rank < extra ? 1 : 0);
     *y0 = cfg->rank * base + std::min(cfg->rank, extra);
+    return VTI_OK;
+}
+
+vti_status vti_plan(const vti_config *cfg, int32_t tile_y, int32_t sms, int32_t ctas_per_sm, vti_plan_info *out)
+{
+    if (!cfg || !out || tile_y < 1 || sms < 1 || ctas_per_sm < 1) return VTI_E_PARAM;
+    vti_status st = check_cfg(cfg);
+    if (st != VTI_OK) return st;
+    vti_slab(cfg, &out->y0, &out->ny_local);
+    out->ntx = (cfg->nx + TX - 1) / TX;
+    out->nty = (out->ny_local + tile_y - 1) / tile_y;
+    int e1, e2;
+    plan_edge_rows(out->nty, cfg->r_xy, tile_y, out->ny_local, e1, e2);
+    out->edge_lo = e1;
+    out->edge_hi = e2;
+    const int slots = sms * ctas_per_sm;
+    const double sat = sat_ctas(ctas_per_sm);
+    out->zchunk = plan_zchunk(cfg->nz, cfg->r_z, out->ntx * out->nty, slots, sat, 0);
+    out->zchunk_edge = plan_zchunk(cfg->nz, cfg->r_z, out->ntx * (e1 + out->nty - e2), slots, sat, 0);
+    out->zchunk_inner = plan_zchunk(cfg->nz, cfg->r_z, out->ntx * (e2 - e1), slots, sat, 0);
+    const long items = (long)out->ntx * out->nty * ((cfg->nz + out->zchunk - 1) / out->zchunk);
+    out->items = (int32_t)items;
+    out->grid = (int32_t)std::min<long>(items, slots);
     return VTI_OK;
 }
 

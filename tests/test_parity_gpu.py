@@ -389,3 +389,16 @@ def test_zero_steps_and_zero_amplitude():
         v.step(10)
         p, q = v.get_fields(0)
         assert not p.any() and not q.any()
+
+
+def test_handle_schedule_equals_host_plan():
+    """vti_query on a GPU handle reports the schedule vti_plan predicts on the host."""
+    import torch
+    from paper_1410_1387_b200 import plan
+    cfg = small_cfg(300, 200, 96, 4, 4, damp=4)
+    wxy, wz, _ = synth.weights_f32(cfg)
+    with make(cfg, 1e-4, wxy, wz) as v:
+        info = v.info()
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        p = plan(300, 200, 96, 4, 4, tile_y=info["tile_y"], sms=sms, ctas_per_sm=info["grid"] // min(info["grid"], sms) or 1)
+        assert (info["zchunk"], info["work_items"]) == (p["zchunk"], p["items"])
