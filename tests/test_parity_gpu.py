@@ -400,5 +400,6 @@ def test_handle_schedule_equals_host_plan():
     with make(cfg, 1e-4, wxy, wz) as v:
         info = v.info()
         sms = torch.cuda.get_device_properties(0).multi_processor_count
-        p = plan(300, 200, 96, 4, 4, tile_y=info["tile_y"], sms=sms, ctas_per_sm=info["grid"] // min(info["grid"], sms) or 1)
-        assert (info["zchunk"], info["work_items"]) == (p["zchunk"], p["items"])
+        assert info["tile_y"] == 32                     # default (4,4) variant: one CTA per SM
+        p = plan(300, 200, 96, 4, 4, tile_y=32, sms=sms, ctas_per_sm=1)
+        assert (info["zchunk"], info["work_items"], info["grid"]) == (p["zchunk"], p["items"], p["grid"])
