@@ -9,8 +9,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libvti.so")
-SOURCES = [os.path.join(CSRC, "vti_runtime.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "vti_kernel.cuh"), os.path.join(ROOT, "include", "vti.h")]
+SOURCES = [os.path.join(CSRC, "vti_runtime.cu")] + sorted(
+    os.path.join(CSRC, "variants", f) for f in os.listdir(os.path.join(CSRC, "variants")) if f.endswith(".cu"))
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("vti_kernel.cuh", "vti_entry.cuh", "vti_variants.h")] + [
+    os.path.join(ROOT, "include", "vti.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -28,18 +30,42 @@ def nvcc() -> str:
     return cand if os.path.exists(cand) else "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+    """Compile every translation unit (kernel variants in parallel) and link libvti.so."""
     os.makedirs(LIBDIR, exist_ok=True)
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in DEPS):
             return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), *SOURCES, "-o", tmp, "-ldl"]
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        compile_flags = ["-Xptxas=-v"] + compile_flags
+    cmds, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.relpath(src, CSRC).replace(os.sep, "_").replace(".cu", ".o"))
+        cmds.append([nvcc(), *compile_flags, *inc, "-c", src, "-o", obj])
+        objs.append(obj)
+    jobs = jobs or max(1, min(len(cmds), os.cpu_count() or 1))
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(cmd):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return cmd, r
+
+    with ThreadPoolExecutor(jobs) as ex:
+        for cmd, r in ex.map(run, cmds):
+            if verbose or r.returncode:
+                print(" ".join(cmd))
+                print(r.stdout + r.stderr)
+            if r.returncode:
+                raise subprocess.CalledProcessError(r.returncode, cmd, r.stdout, r.stderr)
+    tmp = LIB + ".tmp"
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", *objs,
+            "-o", tmp, "-ldl"]
+    subprocess.check_call(link)
     os.replace(tmp, LIB)
     return LIB
 

@@ -1,0 +1,21 @@
+// vti_entry.cuh -- build a KernelEntry from one vti_step_kernel instantiation.
+#pragma once
+
+#include "vti_kernel.cuh"
+#include "vti_variants.h"
+
+template <typename T, int R, int RZ, int TY, int RPT, int WP, int S, int B>
+static KernelEntry entry()
+{
+    using namespace vti;
+    return KernelEntry{(int)sizeof(T), R, RZ, TY, RPT, WP, S, B, Cfg<T, R, RZ, TY>::STAGE,
+                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B>, Cfg<T, R, RZ, TY>::ZROW,
+                       nthreads(TY, RPT, WP)};
+}
+
+#define VTI_TABLE(name, ...)                                     \
+    VariantTable name()                                          \
+    {                                                            \
+        static const KernelEntry t[] = {__VA_ARGS__};            \
+        return VariantTable{t, (int)(sizeof t / sizeof t[0])};   \
+    }

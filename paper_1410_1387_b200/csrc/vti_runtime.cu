@@ -24,6 +24,7 @@
 
 #include "vti.h"
 #include "vti_kernel.cuh"
+#include "vti_variants.h"
 
 using namespace vti;
 
@@ -105,56 +106,21 @@ static PFN_encodeTiled get_encode()
 
 
 // ============================================================ kernel table
-// Element-type-erased entry: fn is a vti_step_kernel<T, ...> instantiation,
-// launched through cudaLaunchKernelExC with a StepParams<T> argument.
-struct KernelEntry {
-    int esize, r, rz, ty, rpt, wp, stages, minb, stage_bytes;
-    const void *fn;
-    int zrow;
-    int threads;
-};
-
-template <typename T, int R, int RZ, int TY, int RPT, int WP, int S, int B>
-static KernelEntry entry()
-{
-    return KernelEntry{(int)sizeof(T), R, RZ, TY, RPT, WP, S, B, Cfg<T, R, RZ, TY>::STAGE,
-                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B>, Cfg<T, R, RZ, TY>::ZROW,
-                       nthreads(TY, RPT, WP)};
-}
-
-// Compiled variants; the first match is the default for (precision, radius pair).
-// -1 = any (env VTI_TY, VTI_WP or vti_set_variant select the others).
+// Compiled variants live in csrc/variants/*.cu (see vti_variants.h); the first
+// match is the default for (precision, radius pair). -1 = any (env VTI_TY,
+// VTI_WP, VTI_RPT or vti_set_variant select the others).
 static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, int rpt = -1)
 {
-    static const KernelEntry table[] = {
-        // fp32 (BASELINE.json configs). RPT = 2 rows per thread halves the y-neighbour
-        // shared-memory reads (8 warps, up to 255 registers); measured slower than
-        // RPT = 1 on every config (C2 187 vs 193), kept for (4,4) as an autotune candidate
-        entry<float, 4, 4, 32, 1, 1, 3, 1>(),   entry<float, 4, 4, 32, 1, 0, 3, 1>(),
-        entry<float, 4, 4, 30, 1, 1, 3, 1>(),   entry<float, 4, 4, 32, 2, 0, 3, 1>(),
-        entry<float, 4, 4, 16, 1, 1, 3, 2>(),
-        entry<float, 8, 4, 32, 1, 1, 3, 1>(),   entry<float, 8, 4, 32, 1, 0, 3, 1>(),
-        entry<float, 8, 4, 30, 1, 1, 3, 1>(),   entry<float, 8, 4, 16, 1, 1, 3, 2>(),
-        // TY = 30 + producer warp: 16 warps -> 128 registers without the in-line producer
-        entry<float, 6, 6, 30, 1, 1, 3, 1>(),   entry<float, 6, 6, 32, 1, 0, 3, 1>(),
-        entry<float, 6, 6, 32, 1, 1, 3, 1>(),   entry<float, 6, 6, 16, 1, 0, 3, 2>(),
-        entry<float, 12, 8, 30, 1, 1, 3, 1>(),  entry<float, 12, 8, 32, 1, 1, 3, 1>(),
-        entry<float, 12, 8, 32, 1, 0, 3, 1>(),  entry<float, 12, 8, 16, 1, 0, 2, 2>(),
-        // fp64: 16- or 14-row tiles so three stages fit in shared
-        // memory; TY = 14 + producer warp = 8 warps -> up to 255 registers (R_z >= 6 queues)
-        entry<double, 4, 4, 16, 1, 1, 3, 1>(),  entry<double, 4, 4, 16, 1, 0, 3, 1>(),
-        entry<double, 4, 4, 14, 1, 1, 3, 1>(),
-        entry<double, 8, 4, 16, 1, 1, 3, 1>(),  entry<double, 8, 4, 16, 1, 0, 3, 1>(),
-        entry<double, 8, 4, 14, 1, 1, 3, 1>(),
-        entry<double, 6, 6, 14, 1, 1, 3, 1>(),  entry<double, 6, 6, 16, 1, 0, 3, 1>(),
-        entry<double, 6, 6, 16, 1, 1, 3, 1>(),
-        entry<double, 12, 8, 14, 1, 1, 3, 1>(), entry<double, 12, 8, 16, 1, 1, 2, 1>(),
-        entry<double, 12, 8, 16, 1, 0, 2, 1>(),
-    };
-    for (const auto &e : table)
-        if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp) &&
-            (rpt < 0 || e.rpt == rpt))
-            return &e;
+    static const VariantTable tables[] = {vti_variants_f32_r4(),  vti_variants_f32_r8(),  vti_variants_f32_r6(),
+                                          vti_variants_f32_r12(), vti_variants_f64_r48(), vti_variants_f64_r6(),
+                                          vti_variants_f64_r12()};
+    for (const VariantTable &t : tables)
+        for (int i = 0; i < t.n; ++i) {
+            const KernelEntry &e = t.e[i];
+            if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp) &&
+                (rpt < 0 || e.rpt == rpt))
+                return &e;
+        }
     return nullptr;
 }
 

@@ -1,0 +1,28 @@
+// vti_variants.h -- the table of compiled step-kernel variants.
+//
+// Each translation unit under csrc/variants/ instantiates a few
+// vti_step_kernel<T, R, RZ, TY, RPT, WP, STAGES, MINB> variants and exports
+// them as a VariantTable, so the instantiations compile in parallel. The
+// runtime scans the tables in vti_variant_tables() order; the first entry that
+// matches (precision, r_xy, r_z) is the default for that pair.
+#pragma once
+
+struct KernelEntry {
+    int esize, r, rz, ty, rpt, wp, stages, minb, stage_bytes;
+    const void *fn;   // host stub of the instantiation (cudaLaunchKernelExC with a StepParams<T> argument)
+    int zrow;
+    int threads;
+};
+
+struct VariantTable {
+    const KernelEntry *e;
+    int n;
+};
+
+VariantTable vti_variants_f32_r4();    // (4,4)
+VariantTable vti_variants_f32_r8();    // (8,4)
+VariantTable vti_variants_f32_r6();    // (6,6)
+VariantTable vti_variants_f32_r12();   // (12,8)
+VariantTable vti_variants_f64_r48();   // (4,4), (8,4)
+VariantTable vti_variants_f64_r6();    // (6,6)
+VariantTable vti_variants_f64_r12();   // (12,8)
