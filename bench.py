@@ -289,7 +289,8 @@ def run_native(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, scaling = workload(args, world)
     prec = args.precision
-    bpp = BYTES_PER_POINT * prec // 32   # 36 B/point in fp32, 72 in fp64
+    from paper_1410_1387_b200 import perfmodel
+    bpp = perfmodel.bytes_per_point(prec)   # 36 B/point in fp32, 72 in fp64
     wxy, wz = weights(cfg, prec)
     dt = synth.stable_dt(cfg)
 
@@ -384,7 +385,10 @@ def run_native(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "vti::vti_step_kernel<4,4>" if cfg["r_xy"] == 4 else f"vti::vti_step_kernel<{cfg['r_xy']},{cfg['r_z']}>",
-                         "algorithmic_bytes_per_launch": bpp * pts_rank},
+                         "algorithmic_bytes_per_launch": bpp * pts_rank,
+                         "flops_per_point": {"paper_count": perfmodel.flops_per_point(cfg["r_xy"], cfg["r_z"]),
+                                             "canonical_order": perfmodel.step_flops_per_point(cfg["r_xy"], cfg["r_z"])},
+                         "gflops": round(perfmodel.step_flops_per_point(cfg["r_xy"], cfg["r_z"]) * value, 1)},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
