@@ -27,8 +27,9 @@ def peak_fraction(r_xy: int, r_z: int, peak_gflops: float, bw_gbytes: float, gib
     """Roofline bound on the fraction of peak flops: CI x bandwidth / peak.
 
     The paper's "47 %" for 666 GF / 102.4 GB/s is reproduced only when the
-    bandwidth is read as GiB/s (gib=True); with GB/s it is 50.5 %."""
-    bw = bw_gbytes * (2 ** 30 if gib else 1e9)
+    bandwidth is converted as 102.4e9 B/s / 2^30 = 95.4 "G"B/s (gib=True, the
+    slip SURVEY.md 2d E3 identifies); with GB/s it is 50.5 %."""
+    bw = bw_gbytes * 1e9 * (1e9 / 2 ** 30 if gib else 1.0)
     return ci_optimistic(r_xy, r_z) * bw / (peak_gflops * 1e9)
 
 
