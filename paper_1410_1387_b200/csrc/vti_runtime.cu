@@ -391,8 +391,13 @@ static vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx
 // columns marching in lockstep keep the p apron re-reads in L2 and avoid the
 // 2Rz-plane q priming of each chunk, and ~110 resident CTAs already saturate
 // HBM (C2: 128 columns on 148 SMs beat 1024 chunks). The chunk count per
-// launch minimises a wave cost: each round of a active CTAs costs
-// zchunk * a / min(a, SAT), times the priming overhead 1 + 8 Rz / (36 zchunk).
+// launch minimises a wave cost, in units of one saturated plane-time: a round
+// of a active CTAs costs the larger of its bandwidth time
+//   zchunk * (1 + 8 Rz / (36 zchunk)) * a / min(a, SAT)   (q priming re-reads)
+// and its latency time (zchunk + 2 Rz) * LAT (each item walks its stage loads
+// in order; ~0.7 plane-times per dependent load, measured on C1 where 8 CTAs
+// of 24 loads took 18.9 us). Small grids therefore get short chunks and many
+// CTAs, large grids long columns.
 static double sat_ctas(int ctas_per_sm)
 {
     double sat = 110.0 * ctas_per_sm;
@@ -400,22 +405,31 @@ static double sat_ctas(int ctas_per_sm)
     return sat;
 }
 
+static double lat_planes()
+{
+    double lat = 0.7;
+    if (const char *e = getenv("VTI_LAT")) lat = atof(e);
+    return lat;
+}
+
 static int plan_zchunk(int nz, int rz, int tiles, int slots, double sat, int tune_zchunk)
 {
     if (tune_zchunk > 0) return std::min(tune_zchunk, nz);
     if (tiles <= 0 || slots <= 0) return nz;
     sat = std::max(1.0, std::min(sat, (double)slots));
+    const double lat = lat_planes();
     double best = 1e300;
     int best_zc = nz;
-    const int max_nzc = std::max(1, nz / (4 * rz));
-    for (int nzc = 1; nzc <= max_nzc; ++nzc) {
+    for (int nzc = 1; nzc <= nz; ++nzc) {
         const int zc = (nz + nzc - 1) / nzc;
         if ((nz + zc - 1) / zc != nzc) continue;   // same chunking as a smaller nzc
         const long items = (long)tiles * nzc;
         const long full = items / slots, last = items % slots;
-        double cost = (double)full * zc * slots / std::min<double>(slots, sat);
-        if (last) cost += (double)zc * last / std::min<double>(last, sat);
-        cost *= 1.0 + (8.0 * rz) / (36.0 * zc);
+        const double prime = 1.0 + (8.0 * rz) / (36.0 * zc);
+        const double lat_round = (zc + 2.0 * rz) * lat;
+        auto round_cost = [&](long a) { return std::max(zc * prime * a / std::min<double>(a, sat), lat_round); };
+        double cost = (double)full * round_cost(slots);
+        if (last) cost += round_cost(last);
         if (cost < best * (1.0 - 1e-3)) {
             best = cost;
             best_zc = zc;

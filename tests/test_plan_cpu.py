@@ -41,7 +41,7 @@ def test_plan_rejects_invalid_config():
 def test_zchunk_choice_properties(nx, ny, nz, r, rz):
     p = V.plan(nx, ny, nz, r, rz, tile_y=32, sms=148, ctas_per_sm=1)
     tiles = p["ntx"] * p["nty"]
-    assert 4 * rz <= p["zchunk"] <= nz
+    assert 4 * rz <= p["zchunk"] <= nz       # big grids: no short chunks (q priming re-reads)
     nzc = -(-nz // p["zchunk"])
     assert p["items"] == tiles * nzc and p["grid"] == min(p["items"], 148)
     if tiles >= 128:              # enough tiles: long z columns (L2 reuse, no extra q priming)
@@ -57,3 +57,10 @@ def test_c2_weak_scaling_rank_plan():
     assert edge_tiles == 16
     assert edge_tiles * (-(-512 // p["zchunk_edge"])) >= 100   # the edge launch fills most SMs
     assert p["zchunk_inner"] == 512
+
+
+def test_small_grid_gets_short_chunks_and_many_ctas():
+    """C1 (64^3, two 64x32 tiles): latency-bound, so z is cut into short chunks."""
+    p = V.plan(64, 64, 64, 4, 4, tile_y=32, sms=148, ctas_per_sm=1)
+    assert p["ntx"] * p["nty"] == 2
+    assert p["grid"] >= 64 and p["zchunk"] <= 4
