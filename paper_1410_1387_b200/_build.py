@@ -37,8 +37,9 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in DEPS):
             return LIB
-    objdir = os.path.join(LIBDIR, "obj")
-    os.makedirs(objdir, exist_ok=True)
+    import shutil
+    import tempfile
+    objdir = tempfile.mkdtemp(prefix="vti_obj_")   # intermediates stay out of the tree
     inc = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     if verbose:
@@ -65,7 +66,10 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     tmp = LIB + ".tmp"
     link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", *objs,
             "-o", tmp, "-ldl"]
-    subprocess.check_call(link)
+    try:
+        subprocess.check_call(link)
+    finally:
+        shutil.rmtree(objdir, ignore_errors=True)
     os.replace(tmp, LIB)
     return LIB
 
