@@ -56,17 +56,17 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         r = subprocess.run(cmd, capture_output=True, text=True)
         return cmd, r
 
-    with ThreadPoolExecutor(jobs) as ex:
-        for cmd, r in ex.map(run, cmds):
-            if verbose or r.returncode:
-                print(" ".join(cmd))
-                print(r.stdout + r.stderr)
-            if r.returncode:
-                raise subprocess.CalledProcessError(r.returncode, cmd, r.stdout, r.stderr)
     tmp = LIB + ".tmp"
     link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", *objs,
             "-o", tmp, "-ldl"]
     try:
+        with ThreadPoolExecutor(jobs) as ex:
+            for cmd, r in ex.map(run, cmds):
+                if verbose or r.returncode:
+                    print(" ".join(cmd))
+                    print(r.stdout + r.stderr)
+                if r.returncode:
+                    raise subprocess.CalledProcessError(r.returncode, cmd, r.stdout, r.stderr)
         subprocess.check_call(link)
     finally:
         shutil.rmtree(objdir, ignore_errors=True)
