@@ -91,7 +91,9 @@ struct StepParams {
     const T *gy;         // [nyl] local rows
     T cxy[MAX_R + 1];
     T dt2;
-    T s;                 // s(t^n) this step
+    T s;                 // s(t^n) this step (direct launches)
+    const T *s_table;    // CUDA-graph launches: s(t^n) = s_table[s_index], refilled before each replay
+    int s_index;
     int src_i, src_j, src_k, src_mask;   // local indices; src_mask = 0: no source here
     int nx, nyl, nz;
     long long ys, zs;                    // row / plane strides (elements)
@@ -459,8 +461,9 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                             T Fp = fma_rn(vx4[c], L[r][c], vD);
                             T Fq = fma_rn(vn4[c], L[r][c], vD);
                             if (src_here && c == src_c) {
-                                if (P.src_mask & 1) Fp = Fp + P.s;
-                                if (P.src_mask & 2) Fq = Fq + P.s;
+                                const T sv = P.s_table ? P.s_table[P.s_index] : P.s;
+                                if (P.src_mask & 1) Fp = Fp + sv;
+                                if (P.src_mask & 2) Fq = Fq + sv;
                             }
                             const T g = gxy[r][c] * gz;   // (gx gy) gz
                             pn[r][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[r][c]));

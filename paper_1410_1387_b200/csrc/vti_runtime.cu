@@ -303,6 +303,13 @@ struct vti_s {
     bool suppress_src = false;                // autotune probes inject nothing
     bool fields_touched = false;              // vti_set_fields* called (state may be non-zero)
     int dir = 1;                              // +1 forward in time, -1 after vti_reverse
+    // CUDA graphs of GRAPH_STEPS single-slab steps (launch-bound small grids)
+    bool graph_enabled = true;                // env VTI_GRAPH=0 disables
+    bool capturing = false;
+    int capture_index = 0;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // by starting parity (cur)
+    void *s_graph = nullptr;                  // device: GRAPH_STEPS source samples of T
+    std::vector<double> s_host;
     // receivers (this slab's subset, in the caller's order)
     int nrec = 0, rec_mask = 0, rec_cap = 0, rec_steps = 0;
     long long *rec_off = nullptr;             // device: element offsets in an interior view
@@ -629,6 +636,9 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->sync_ctr);
     cudaFree(h->rec_off);
     cudaFree(h->traces);
+    for (int b = 0; b < 2; ++b)
+        if (h->gexec[b]) cudaGraphExecDestroy(h->gexec[b]);
+    cudaFree(h->s_graph);
     for (cudaEvent_t e : {h->ev_edge, h->ev_comm, h->ev_t0, h->ev_t1})
         if (e) cudaEventDestroy(e);
     if (h->comm) cudaStreamDestroy(h->comm);
@@ -651,8 +661,18 @@ static vti_status alloc(vti_s *h, void **p, size_t bytes)
 
 // Make K the step kernel of the handle: tile height, shared memory, occupancy,
 // default schedule and the TMA tensor maps (whose boxes depend on TY).
+static void invalidate_graphs(vti_s *h)
+{
+    for (int b = 0; b < 2; ++b)
+        if (h->gexec[b]) {
+            cudaGraphExecDestroy(h->gexec[b]);
+            h->gexec[b] = nullptr;
+        }
+}
+
 static vti_status select_variant(vti_s *h, const KernelEntry *K)
 {
+    invalidate_graphs(h);
     h->K = K;
     h->TY = K->ty;
     h->nty = (h->nyl + h->TY - 1) / h->TY;
@@ -764,6 +784,7 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     if ((s = alloc(h, (void **)&h->flag, sizeof(unsigned int))) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->sync_ctr, sizeof(unsigned long long))) != VTI_OK) return s;
     if (const char *e = getenv("VTI_ALIGN")) h->align_rounds = atoi(e) != 0;
+    if (const char *e = getenv("VTI_GRAPH")) h->graph_enabled = atoi(e) != 0;
     if (cfg->nranks > 1) {
         const size_t hb = (size_t)cfg->nz * h->R * cfg->nx * h->es;
         for (int b = 0; b < 2; ++b) {
@@ -997,6 +1018,8 @@ static void fill_params(vti_s *h, StepParams<T> &P, int tr0, int ntr0, int tr1, 
     const bool owned = h->has_src && !h->suppress_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
     // s(t^n), t^n = n dt, double on the host, rounded once to T (reading c7)
     P.s = owned ? (T)(h->src_amp * ricker((double)h->n * h->cfg.dt, h->src_f, h->src_t0)) : T(0);
+    P.s_table = nullptr;   // set by graph capture
+    P.s_index = 0;
     P.src_i = h->src_i;
     P.src_j = owned ? h->src_j - h->y0 : -1;
     P.src_k = h->src_k;
@@ -1021,6 +1044,10 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
 {
     StepParams<T> P;
     fill_params<T>(h, P, tr0, ntr0, tr1, ntr1, zchunk);
+    if (h->capturing) {   // graph node: the source sample comes from the graph's table
+        P.s_table = (const T *)h->s_graph;
+        P.s_index = h->capture_index;
+    }
     const int grid = std::min(P.items, h->sms * h->ctas_per_sm);
     const int rounds = (P.items + grid - 1) / grid;
     P.sync_ctr = nullptr;
@@ -1180,6 +1207,9 @@ vti_status vti_set_receivers(vti_t h, int32_t n, const int32_t *ijk, int32_t fie
     CU(h, cudaStreamSynchronize(h->stream));
     cudaFree(h->rec_off);
     cudaFree(h->traces);
+    for (int b = 0; b < 2; ++b)
+        if (h->gexec[b]) cudaGraphExecDestroy(h->gexec[b]);
+    cudaFree(h->s_graph);
     h->rec_off = nullptr;
     h->traces = nullptr;
     h->nrec = (int)off.size();
@@ -1310,6 +1340,7 @@ vti_status vti_add_source(vti_t h, int32_t i, int32_t j, int32_t k, double f, do
     if (i < 0 || i >= h->cfg.nx || j < 0 || j >= h->cfg.ny || k < 0 || k >= h->cfg.nz)
         return fail(h, VTI_E_INDEX, "source (%d,%d,%d) outside the %dx%dx%d grid", i, j, k, h->cfg.nx, h->cfg.ny,
                     h->cfg.nz);
+    invalidate_graphs(h);   // the source position and mask are baked into graph nodes
     h->has_src = true;
     h->src_i = i;
     h->src_j = j;
@@ -1373,6 +1404,69 @@ vti_status vti_get_fields_f64(vti_t h, double *p, double *q, int32_t level)
     return get_fields_planes(h, 8, 0, h->cfg.nz, p, q, level);
 }
 
+// ---- CUDA graphs for launch-bound small grids (single slab, one round per step)
+static constexpr int GRAPH_STEPS = 32;   // even: a replay returns to its starting parity
+
+static bool graph_eligible(const vti_s *h)
+{
+    if (!h->graph_enabled || h->cfg.nranks > 1 || h->nrec > 0 || h->cfg.check_every > 0 || h->suppress_src)
+        return false;
+    const long items = (long)h->ntx * h->nty * h->nzc;
+    if (items > (long)h->sms * h->ctas_per_sm) return false;          // multi-round: cooperative launches
+    const double pts = (double)h->cfg.nx * h->nyl * h->cfg.nz;
+    return pts <= 64.0 * 1024 * 1024;   // beyond that a step is long enough that launch gaps do not matter
+}
+
+// Capture GRAPH_STEPS steps starting at parity c into h->gexec[c].
+static vti_status build_graph(vti_s *h, int c)
+{
+    if (!h->s_graph) CU(h, cudaMalloc(&h->s_graph, GRAPH_STEPS * 8));
+    const int keep_cur = h->cur;
+    cudaGraph_t g = nullptr;
+    CU(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    h->capturing = true;
+    vti_status s = VTI_OK;
+    for (int i = 0; i < GRAPH_STEPS && s == VTI_OK; ++i) {
+        h->cur = (c + i) & 1;
+        h->capture_index = i;
+        s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk);
+    }
+    h->capturing = false;
+    h->cur = keep_cur;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (s != VTI_OK) {
+        if (g) cudaGraphDestroy(g);
+        return s;
+    }
+    if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&h->gexec[c], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    return VTI_OK;
+}
+
+// Replay GRAPH_STEPS steps: refill the source table (stream-ordered, from pageable
+// host memory so the host buffer is free on return), then launch the graph.
+static vti_status replay_graph(vti_s *h)
+{
+    vti_status s;
+    if (!h->gexec[h->cur] && (s = build_graph(h, h->cur)) != VTI_OK) return s;
+    const bool owned = h->has_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
+    h->s_host.assign(GRAPH_STEPS, 0.0);
+    for (int i = 0; i < GRAPH_STEPS && owned; ++i)
+        h->s_host[i] = h->src_amp * ricker((double)(h->n + (int64_t)i * h->dir) * h->cfg.dt, h->src_f, h->src_t0);
+    if (h->es == 8) {
+        CU(h, cudaMemcpyAsync(h->s_graph, h->s_host.data(), GRAPH_STEPS * 8, cudaMemcpyHostToDevice, h->stream));
+    } else {
+        float f[GRAPH_STEPS];
+        for (int i = 0; i < GRAPH_STEPS; ++i) f[i] = (float)h->s_host[i];   // rounded once, as P.s
+        CU(h, cudaMemcpyAsync(h->s_graph, f, sizeof f, cudaMemcpyHostToDevice, h->stream));
+    }
+    CU(h, cudaGraphLaunch(h->gexec[h->cur], h->stream));
+    h->n += (int64_t)GRAPH_STEPS * h->dir;   // parity (cur) is unchanged after an even number of steps
+    return VTI_OK;
+}
+
 vti_status vti_step(vti_t h, int32_t nsteps)
 {
     if (!h) return VTI_E_PARAM;
@@ -1389,7 +1483,18 @@ vti_status vti_step(vti_t h, int32_t nsteps)
         CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         h->halo_dirty = false;
     }
-    for (int it = 0; it < nsteps; ++it) {
+    int it = 0;
+    if (!multi && nsteps >= GRAPH_STEPS && graph_eligible(h)) {
+        for (; it + GRAPH_STEPS <= nsteps; it += GRAPH_STEPS)
+            if ((s = replay_graph(h)) != VTI_OK) {
+                // capture is not possible on this stream (e.g. the legacy default stream): launch directly
+                cudaGetLastError();
+                h->graph_enabled = false;
+                invalidate_graphs(h);
+                break;
+            }
+    }
+    for (; it < nsteps; ++it) {
         if (!multi) {
             if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk)) != VTI_OK) return s;
         } else {

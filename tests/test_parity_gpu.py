@@ -403,3 +403,28 @@ def test_handle_schedule_equals_host_plan():
         assert info["tile_y"] == 32                     # default (4,4) variant: one CTA per SM
         p = plan(300, 200, 96, 4, 4, tile_y=32, sms=sms, ctas_per_sm=1)
         assert (info["zchunk"], info["work_items"], info["grid"]) == (p["zchunk"], p["items"], p["grid"])
+
+
+def test_graph_replays_equal_direct_launches(monkeypatch):
+    """Launch-bound grids step through CUDA-graph replays (32 steps each); the result is
+    bitwise the direct-launch result, across a source change, an odd remainder and reversal."""
+    cfg = small_cfg(60, 44, 40, 4, 4, damp=5, src=(20, 20, 20))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    out = []
+    for graph in ("1", "0"):
+        monkeypatch.setenv("VTI_GRAPH", graph)
+        with make(cfg, dt, wxy, wz) as v:
+            v.set_model(*model)
+            v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+            v.step(70)                                   # 2 replays + 6 direct steps
+            v.add_source(40, 10, 30, f=cfg["f"], t0=0.0, mask=3)   # invalidates the graphs
+            v.step(33)
+            v.reverse()
+            v.step(64)
+            assert v.time_index == 70 + 33 - 1 - 64
+            out.append(v.get_fields(0) + v.get_fields(1))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
+    assert np.abs(out[0][0]).max() > 0
