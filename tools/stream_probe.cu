@@ -3,6 +3,7 @@
 // loops. Prints TB/s for several launch shapes; compare with the step kernel's
 // ncu DRAM rate. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/sp tools/stream_probe.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void mix(const float4 *__restrict__ a, const float4 *__restrict__ b, const float4 *__restrict__ c,
@@ -16,9 +17,11 @@ __global__ void mix(const float4 *__restrict__ a, const float4 *__restrict__ b, 
     }
 }
 
-int main()
+int main(int argc, char **argv)
 {
-    const size_t n = 512ull * 512 * 512, n4 = n / 4;
+    // points per stream: 512^3 (C2) by default, or argv[1] (e.g. 4294967296 for C4's 2048^2 x 1024)
+    const size_t n = argc > 1 ? (size_t)atoll(argv[1]) : 512ull * 512 * 512, n4 = n / 4;
+    printf("points per stream: %zu (%.1f GB over 9 streams)\n", n, 36.0 * n / 1e9);
     float4 *p[9];
     for (int i = 0; i < 9; ++i) {
         cudaMalloc(&p[i], n * 4);
@@ -34,7 +37,7 @@ int main()
         const int grid = sms * sh[0], block = sh[1];
         for (int w = 0; w < 3; ++w) mix<<<grid, block>>>(p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8], n4);
         cudaEventRecord(t0);
-        const int reps = 20;
+        const int reps = n > (1ull << 30) ? 3 : 20;
         for (int r = 0; r < reps; ++r) mix<<<grid, block>>>(p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8], n4);
         cudaEventRecord(t1);
         cudaEventSynchronize(t1);
