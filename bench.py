@@ -71,13 +71,14 @@ def workload(args, world):
     return cfg, scaling
 
 
-def describe(cfg, world, scaling, bpp=BYTES_PER_POINT):
+def describe(cfg, world, scaling, bpp=BYTES_PER_POINT, transport="none"):
     return {
         "workload": f"{cfg['name']}: {cfg['nx']}x{cfg['ny']}x{cfg['nz']} global, R_xy={cfg['r_xy']} R_z={cfg['r_z']}, "
                     f"{cfg['model']['kind']} VTI, W={cfg['damp_width']}, Ricker f={cfg['f']:g} Hz at the centre",
         "grid": [cfg["nx"], cfg["ny"], cfg["nz"]],
         "r_xy": cfg["r_xy"], "r_z": cfg["r_z"], "config_steps": cfg["steps"],
         "decomposition": f"y-slabs x{world}" if world > 1 else "single GPU",
+        "halo_transport": transport,
         "scaling": scaling,
         "l2_flush": f"not needed: per-step working set ({bpp} B/pt) >> 126 MB L2",
         "bytes_per_point": bpp,
@@ -299,7 +300,17 @@ def run_native(args):
     def fresh_nccl_id():
         return multi.broadcast_nccl_id(dist, rank, world)
 
-    nccl_id = fresh_nccl_id()
+    halo = os.environ.get("VTI_HALO", "copy-engine") if world > 1 else "none"
+
+    def open_handle():
+        """A rank's handle with its halo transport: copy engine over CUDA IPC by default,
+        NCCL if requested or if any rank cannot connect (collective fallback)."""
+        if world > 1 and halo != "nccl":
+            h = make_handle(cfg, dt, wxy, wz, rank, world, local, None, prec)
+            if multi.connect_copy_engine(dist, h, rank, world):
+                return h
+            h.close()
+        return make_handle(cfg, dt, wxy, wz, rank, world, local, fresh_nccl_id(), prec)
 
     def barrier():
         if world > 1:
@@ -310,7 +321,8 @@ def run_native(args):
         return multi.max_over_ranks(dist, world, x, device="cuda")
 
     npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    v = make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id, prec)
+    v = open_handle()
+    transport = v.halo_transport
     if args.zchunk or args.ctas_per_sm:
         v.set_tuning(args.zchunk, args.ctas_per_sm)
     set_model_from_device(v, cfg)
@@ -319,6 +331,8 @@ def run_native(args):
 
     # warm-up (untimed), then exactly K timed steps bracketed by barrier + synchronize
     v.step(args.warmup)
+    if world > 1:   # the first exchanges prove the transport; fail loudly rather than hang
+        multi.sync_or_die(v, 120.0, f"warm-up ({transport} halo transport)")
     v.sync()
     barrier()
     with Clocks(local) as clk:
@@ -351,7 +365,7 @@ def run_native(args):
             for dst, src in zip(host_model, m):
                 dst[k0:k0 + nk].copy_(src)
         out_p, out_q = pin(shape), pin(shape)
-        w = make_handle(cfg, dt, wxy, wz, rank, world, local, fresh_nccl_id(), prec)
+        w = open_handle()
         if args.zchunk or args.ctas_per_sm:
             w.set_tuning(args.zchunk, args.ctas_per_sm)
         barrier()
@@ -381,7 +395,7 @@ def run_native(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 5),
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": f"f{prec}",
             "data": "synthetic (seeded layered VTI model generated on device; zero initial state + Ricker source)",
-            "config": describe(cfg, world, scaling, bpp),
+            "config": describe(cfg, world, scaling, bpp, transport),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "vti::vti_step_kernel<4,4>" if cfg["r_xy"] == 4 else f"vti::vti_step_kernel<{cfg['r_xy']},{cfg['r_z']}>",

@@ -42,7 +42,8 @@
 extern "C" {
 #endif
 
-#define VTI_ABI_VERSION 2
+#define VTI_ABI_VERSION 3
+#define VTI_IPC_BYTES 512   /* size of a vti_ipc_export blob */
 
 typedef struct vti_s *vti_t;
 
@@ -55,7 +56,7 @@ typedef enum {
     VTI_E_INSTABILITY = 5,  /* non-finite wavefield detected (check_every > 0) */
     VTI_E_INDEX = 6,        /* source or plane range outside the domain */
     VTI_E_CUDA = 7,         /* CUDA runtime / driver failure (message has the CUDA error) */
-    VTI_E_COMM = 8,         /* NCCL failure or NCCL unavailable for nranks > 1 */
+    VTI_E_COMM = 8,         /* halo transport failure: NCCL, CUDA IPC or stream memory operations (nranks > 1) */
     VTI_E_STATE = 9,        /* call not valid in the handle's current state */
     VTI_E_UNSUPPORTED = 10  /* (r_xy, r_z) pair not compiled into this library */
 } vti_status;
@@ -235,6 +236,25 @@ vti_status vti_reverse(vti_t h);
 
 /* +1 (forward) or -1 (after an odd number of vti_reverse calls). */
 int32_t vti_direction(vti_t h);
+
+/*
+ * Copy-engine halo transport for nranks > 1 (no NCCL, no SMs): p's packed
+ * boundary rows are copied straight into the neighbours' receive buffers over
+ * NVLink (CUDA IPC peer pointers) and ordered with flag words written and
+ * waited on by stream memory operations. vti_ipc_export writes this rank's
+ * VTI_IPC_BYTES blob; after exchanging blobs (e.g. all-gather over the job's
+ * process group) every rank calls vti_ipc_connect with the blob of rank-1 (lo)
+ * and rank+1 (hi), NULL at the ends. A handle created with an nccl_id that is
+ * then connected uses this transport instead of NCCL. Both calls are
+ * collective in effect: all ranks must connect before the next vti_step.
+ * Errors: STATE (nranks < 2), PARAM (wrong blob), COMM (IPC / stream memory
+ * operations unavailable), CUDA.
+ */
+vti_status vti_ipc_export(vti_t h, void *out);
+vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi);
+
+/* 0: none (single slab), 1: NCCL, 2: copy engine (local group or CUDA IPC). */
+int32_t vti_halo_transport(vti_t h);
 
 /* Block until all work on the handle's stream(s) is done. */
 vti_status vti_sync(vti_t h);

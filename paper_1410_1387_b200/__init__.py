@@ -121,6 +121,9 @@ def _load():
         "vti_get_traces": (st, [H, P]),
         "vti_get_traces_f64": (st, [H, P]),
         "vti_reverse": (st, [H]),
+        "vti_ipc_export": (st, [H, P]),
+        "vti_ipc_connect": (st, [H, P, P]),
+        "vti_halo_transport": (C.c_int32, [H]),
         "vti_direction": (C.c_int32, [H]),
         "vti_autotune": (st, [H, C.c_int32, C.POINTER(TuneResult)]),
         "vti_last_error": (C.c_char_p, [H]),
@@ -315,6 +318,23 @@ class VTI:
         if out.size:
             _check(self.h, self._fn("vti_get_traces")(self.h, out.ctypes.data))
         return ids, out
+
+    # -- multi-process copy-engine halo transport (CUDA IPC)
+    IPC_BYTES = 512
+
+    def ipc_export(self) -> bytes:
+        buf = C.create_string_buffer(self.IPC_BYTES)
+        _check(self.h, lib.vti_ipc_export(self.h, buf))
+        return buf.raw
+
+    def ipc_connect(self, lo: bytes | None, hi: bytes | None):
+        lo_b = C.create_string_buffer(lo, self.IPC_BYTES) if lo is not None else None
+        hi_b = C.create_string_buffer(hi, self.IPC_BYTES) if hi is not None else None
+        _check(self.h, lib.vti_ipc_connect(self.h, lo_b, hi_b))
+
+    @property
+    def halo_transport(self) -> str:
+        return {0: "none", 1: "nccl", 2: "copy-engine"}.get(lib.vti_halo_transport(self.h), "?")
 
     def reverse(self):
         _check(self.h, lib.vti_reverse(self.h))

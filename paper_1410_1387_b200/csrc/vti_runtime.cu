@@ -105,6 +105,30 @@ static PFN_encodeTiled get_encode()
 }
 
 
+// Stream memory operations (the copy-engine halo transport's flags).
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct StreamMemOps {
+    PFN_streamValue32 wait = nullptr, write = nullptr;
+};
+
+static const StreamMemOps &stream_mem_ops()
+{
+    static StreamMemOps ops;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.wait = reinterpret_cast<PFN_streamValue32>(p);
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.write = reinterpret_cast<PFN_streamValue32>(p);
+    });
+    return ops;
+}
+
 // ============================================================ kernel table
 // Compiled variants live in csrc/variants/*.cu (see vti_variants.h); the first
 // match is the default for (precision, radius pair). -1 = any (env VTI_TY,
@@ -299,6 +323,15 @@ struct vti_s {
     double src_f = 15.0, src_t0 = 0.0, src_amp = 1.0;
     ncclComm_t comm_nccl = nullptr;
     bool group_mode = false;
+    // copy-engine halo transport (local group, or multi-process after vti_ipc_connect):
+    // flags[] = {DATA_LO, DATA_HI, ACK_LO, ACK_HI}, written by the neighbours
+    bool p2p = false;
+    unsigned int *flags = nullptr;
+    void *peer_rbuf[2] = {nullptr, nullptr};          // [0]: rank-1's rbuf[1], [1]: rank+1's rbuf[0]
+    unsigned int *peer_flags[2] = {nullptr, nullptr}; // the neighbours' flags
+    void *ipc_opened[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // cudaIpcCloseMemHandle on destroy
+    unsigned int xseq = 0;                            // exchanges so far (the flag values)
+    bool flush_remote = false;                        // CU_STREAM_WAIT_VALUE_FLUSH supported
     bool halo_dirty = false;
     bool suppress_src = false;                // autotune probes inject nothing
     bool fields_touched = false;              // vti_set_fields* called (state may be non-zero)
@@ -634,6 +667,9 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->counters);
     cudaFree(h->flag);
     cudaFree(h->sync_ctr);
+    for (void *p : h->ipc_opened)
+        if (p) cudaIpcCloseMemHandle(p);
+    cudaFree(h->flags);
     cudaFree(h->rec_off);
     cudaFree(h->traces);
     for (int b = 0; b < 2; ++b)
@@ -791,6 +827,11 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
             if ((s = alloc(h, &h->sbuf[b], hb)) != VTI_OK) return s;
             if ((s = alloc(h, &h->rbuf[b], hb)) != VTI_OK) return s;
         }
+        if ((s = alloc(h, (void **)&h->flags, 4 * sizeof(unsigned int))) != VTI_OK) return s;
+        int flush = 0;
+        if (cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, cfg->device) == cudaSuccess)
+            h->flush_remote = flush != 0;
+        cudaGetLastError();
     }
 
     // per-plane z rows: w^z[k][0..2Rz], gz[k], zero pad; 1-D Cerjan profiles (double -> T once)
@@ -1145,6 +1186,75 @@ static vti_status exchange_nccl(vti_s *h, int b)
     return VTI_OK;
 }
 
+// Copy-engine transport (no SMs, no NCCL): after the edge launch and the pack,
+// the comm stream copies each packed boundary block straight into the
+// neighbour's receive buffer over NVLink (UVA / CUDA-IPC peer pointer) and then
+// bumps the neighbour's DATA flag; it waits for its own DATA flags, unpacks, and
+// bumps the neighbours' ACK flags; before the next copy into a neighbour's
+// buffer it waits for that neighbour's ACK of the previous one. Flags are
+// monotone exchange counters; cuStreamWaitValue32/WriteValue32 order them with
+// the copies on the GPU front end. Records ev_comm.
+//
+// Enqueue order matters: streams share a small pool of in-order hardware
+// channels, so a value-wait may only wait on a write that was ENQUEUED EARLIER
+// (the same rule that makes event waits safe). The send half (ACK wait of the
+// previous exchange, copy, DATA write) and the receive half (DATA wait, unpack,
+// ACK write) are therefore separate calls, and a local group enqueues every
+// handle's send half before any receive half.
+enum { F_DATA_LO = 0, F_DATA_HI = 1, F_ACK_LO = 2, F_ACK_HI = 3 };
+
+static CUdeviceptr dev_ptr(const void *p) { return (CUdeviceptr)(uintptr_t)p; }
+
+static vti_status exchange_p2p_send(vti_s *h)
+{
+    const StreamMemOps &ops = stream_mem_ops();
+    if (!ops.wait || !ops.write) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
+    const unsigned int k = ++h->xseq;
+    const size_t bytes = halo_elems(h) * h->es;
+    CUstream cs = (CUstream)h->comm;
+    CU(h, cudaStreamWaitEvent(h->comm, h->ev_edge, 0));
+    for (int side = 0; side < 2; ++side) {   // 0: our first R rows -> rank-1, 1: our last R rows -> rank+1
+        if (side == 0 ? h->cfg.rank == 0 : h->cfg.rank == h->cfg.nranks - 1) continue;
+        if (ops.wait(cs, dev_ptr(h->flags + (side == 0 ? F_ACK_LO : F_ACK_HI)), k - 1, CU_STREAM_WAIT_VALUE_GEQ) !=
+            CUDA_SUCCESS)
+            return fail(h, VTI_E_COMM, "cuStreamWaitValue32 failed");
+        CU(h, cudaMemcpyAsync(h->peer_rbuf[side], h->sbuf[side], bytes, cudaMemcpyDefault, h->comm));
+        if (ops.write(cs, dev_ptr(h->peer_flags[side] + (side == 0 ? F_DATA_HI : F_DATA_LO)), k,
+                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return fail(h, VTI_E_COMM, "cuStreamWriteValue32 failed");
+    }
+    return VTI_OK;
+}
+
+static vti_status exchange_p2p_recv(vti_s *h, int b)
+{
+    const StreamMemOps &ops = stream_mem_ops();
+    const unsigned int k = h->xseq;
+    CUstream cs = (CUstream)h->comm;
+    const unsigned wait_flags = h->flush_remote ? CU_STREAM_WAIT_VALUE_GEQ | CU_STREAM_WAIT_VALUE_FLUSH
+                                                : CU_STREAM_WAIT_VALUE_GEQ;
+    for (int side = 0; side < 2; ++side) {   // 0: rows from rank-1 -> halo rows [0,R), 1: from rank+1
+        if (side == 0 ? h->cfg.rank == 0 : h->cfg.rank == h->cfg.nranks - 1) continue;
+        if (ops.wait(cs, dev_ptr(h->flags + (side == 0 ? F_DATA_LO : F_DATA_HI)), k, wait_flags) != CUDA_SUCCESS)
+            return fail(h, VTI_E_COMM, "cuStreamWaitValue32 failed");
+        unpack(h, h->rbuf[side], h->pbuf[b], side == 0 ? 0 : h->nyl + h->R, h->comm);
+        CU(h, cudaGetLastError());
+        if (ops.write(cs, dev_ptr(h->peer_flags[side] + (side == 0 ? F_ACK_HI : F_ACK_LO)), k,
+                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return fail(h, VTI_E_COMM, "cuStreamWriteValue32 failed");
+    }
+    CU(h, cudaEventRecord(h->ev_comm, h->comm));
+    return VTI_OK;
+}
+
+static vti_status exchange_p2p(vti_s *h, int b)
+{
+    vti_status s = exchange_p2p_send(h);
+    return s != VTI_OK ? s : exchange_p2p_recv(h, b);
+}
+
+static vti_status exchange(vti_s *h, int b) { return h->p2p ? exchange_p2p(h, b) : exchange_nccl(h, b); }
+
 static vti_status check_finite(vti_s *h)
 {
     CU(h, cudaMemsetAsync(h->flag, 0, sizeof(unsigned int), h->stream));
@@ -1252,6 +1362,70 @@ static vti_status get_traces(vti_s *h, int es, void *out)
 
 vti_status vti_get_traces(vti_t h, float *out) { return get_traces(h, 4, out); }
 vti_status vti_get_traces_f64(vti_t h, double *out) { return get_traces(h, 8, out); }
+
+// ---- multi-process copy-engine transport over CUDA IPC
+struct IpcBlob {
+    uint32_t magic, version;
+    int32_t rank, nranks;
+    cudaIpcMemHandle_t rbuf[2], flags;
+};
+static_assert(sizeof(IpcBlob) <= VTI_IPC_BYTES, "IPC blob too large");
+static const uint32_t IPC_MAGIC = 0x56544931u;   // "VTI1"
+
+vti_status vti_ipc_export(vti_t h, void *out)
+{
+    if (!h || !out) return VTI_E_PARAM;
+    if (h->cfg.nranks < 2 || !h->flags) return fail(h, VTI_E_STATE, "vti_ipc_export needs nranks > 1");
+    CU(h, cudaSetDevice(h->cfg.device));
+    IpcBlob b;
+    memset(&b, 0, sizeof b);
+    b.magic = IPC_MAGIC;
+    b.version = VTI_ABI_VERSION;
+    b.rank = h->cfg.rank;
+    b.nranks = h->cfg.nranks;
+    CU(h, cudaIpcGetMemHandle(&b.rbuf[0], h->rbuf[0]));
+    CU(h, cudaIpcGetMemHandle(&b.rbuf[1], h->rbuf[1]));
+    CU(h, cudaIpcGetMemHandle(&b.flags, h->flags));
+    memset(out, 0, VTI_IPC_BYTES);
+    memcpy(out, &b, sizeof b);
+    return VTI_OK;
+}
+
+vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
+{
+    if (!h) return VTI_E_PARAM;
+    const int r = h->cfg.rank, nr = h->cfg.nranks;
+    if (nr < 2) return fail(h, VTI_E_STATE, "vti_ipc_connect needs nranks > 1");
+    if ((r > 0) != (lo != nullptr) || (r < nr - 1) != (hi != nullptr))
+        return fail(h, VTI_E_PARAM, "pass the blob of rank-1 (lo) and rank+1 (hi), NULL at the ends");
+    const StreamMemOps &ops = stream_mem_ops();
+    if (!ops.wait || !ops.write) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
+    CU(h, cudaSetDevice(h->cfg.device));
+    const void *blobs[2] = {lo, hi};
+    for (int side = 0; side < 2; ++side) {
+        if (!blobs[side]) continue;
+        IpcBlob b;
+        memcpy(&b, blobs[side], sizeof b);
+        if (b.magic != IPC_MAGIC || b.version != (uint32_t)VTI_ABI_VERSION || b.nranks != nr ||
+            b.rank != (side == 0 ? r - 1 : r + 1))
+            return fail(h, VTI_E_PARAM, "IPC blob of the wrong rank, job or library version");
+        void *rb = nullptr, *fl = nullptr;
+        // rank-1 receives our first rows in its rbuf[1]; rank+1 our last rows in its rbuf[0]
+        cudaError_t e = cudaIpcOpenMemHandle(&rb, b.rbuf[side == 0 ? 1 : 0], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+        h->ipc_opened[3 * side] = rb;
+        e = cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+        h->ipc_opened[3 * side + 1] = fl;
+        h->peer_rbuf[side] = rb;
+        h->peer_flags[side] = (unsigned int *)fl;
+    }
+    h->p2p = true;
+    h->group_mode = false;
+    return VTI_OK;
+}
+
+int32_t vti_halo_transport(vti_t h) { return !h ? -1 : h->cfg.nranks < 2 ? 0 : h->p2p ? 2 : h->comm_nccl ? 1 : 0; }
 
 vti_status vti_reverse(vti_t h)
 {
@@ -1473,13 +1647,15 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     if (nsteps < 0) return fail(h, VTI_E_PARAM, "nsteps < 0");
     if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
     if (h->group_mode) return fail(h, VTI_E_STATE, "local-group handle: use vti_group_step");
+    if (h->cfg.nranks > 1 && !h->p2p && !h->comm_nccl)
+        return fail(h, VTI_E_STATE, "nranks > 1 needs an nccl_id at create time or vti_ipc_connect");
     CU(h, cudaSetDevice(h->cfg.device));
     const bool multi = h->cfg.nranks > 1;
     vti_status s;
     if (multi && h->halo_dirty) {   // halos of a state set by the caller
         if ((s = pack_send(h, h->cur)) != VTI_OK) return s;
         CU(h, cudaEventRecord(h->ev_edge, h->stream));
-        if ((s = exchange_nccl(h, h->cur)) != VTI_OK) return s;
+        if ((s = exchange(h, h->cur)) != VTI_OK) return s;
         CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         h->halo_dirty = false;
     }
@@ -1503,7 +1679,7 @@ vti_status vti_step(vti_t h, int32_t nsteps)
             if ((s = launch_edge(h)) != VTI_OK) return s;
             if ((s = pack_send(h, o)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
-            if ((s = exchange_nccl(h, o)) != VTI_OK) return s;
+            if ((s = exchange(h, o)) != VTI_OK) return s;
             if ((s = launch_interior(h)) != VTI_OK) return s;   // overlaps the exchange
             CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         }
@@ -1532,38 +1708,46 @@ vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms)
 }
 
 // Local group: the same pack / transport / unpack schedule, transport = peer copies of the packed rows.
-static vti_status group_exchange(vti_t *hs, int n, bool current)
+// Local group: the copy-engine transport between handles of one process (peer
+// pointers are the neighbours' own device buffers), the same protocol as the
+// multi-process CUDA-IPC transport.
+static void group_connect(vti_t *hs, int n)
 {
     for (int i = 0; i < n; ++i) {
         vti_s *h = hs[i];
-        const int b = current ? h->cur : 1 - h->cur;
-        CU(h, cudaSetDevice(h->cfg.device));
-        const size_t bytes = halo_elems(h) * h->es;
-        if (i > 0) {   // my rows from rank-1 = its packed rows for rank+1
-            vti_s *g = hs[i - 1];
-            CU(h, cudaStreamWaitEvent(h->comm, g->ev_edge, 0));
-            CU(h, cudaMemcpyPeerAsync(h->rbuf[0], h->cfg.device, g->sbuf[1], g->cfg.device, bytes, h->comm));
-        }
-        if (i < n - 1) {
-            vti_s *g = hs[i + 1];
-            CU(h, cudaStreamWaitEvent(h->comm, g->ev_edge, 0));
-            CU(h, cudaMemcpyPeerAsync(h->rbuf[1], h->cfg.device, g->sbuf[0], g->cfg.device, bytes, h->comm));
-        }
-        vti_status s = unpack_recv(h, b);
+        h->p2p = true;
+        h->peer_rbuf[0] = i > 0 ? hs[i - 1]->rbuf[1] : nullptr;
+        h->peer_flags[0] = i > 0 ? hs[i - 1]->flags : nullptr;
+        h->peer_rbuf[1] = i < n - 1 ? hs[i + 1]->rbuf[0] : nullptr;
+        h->peer_flags[1] = i < n - 1 ? hs[i + 1]->flags : nullptr;
+    }
+}
+
+static vti_status group_exchange(vti_t *hs, int n, bool current)
+{
+    // every handle's send half before any receive half (see exchange_p2p_send)
+    for (int i = 0; i < n; ++i) {
+        CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+        vti_status s = exchange_p2p_send(hs[i]);
         if (s != VTI_OK) return s;
-        CU(h, cudaEventRecord(h->ev_comm, h->comm));
+    }
+    for (int i = 0; i < n; ++i) {
+        vti_s *h = hs[i];
+        CU(h, cudaSetDevice(h->cfg.device));
+        vti_status s = exchange_p2p_recv(h, current ? h->cur : 1 - h->cur);
+        if (s != VTI_OK) return s;
     }
     return VTI_OK;
 }
 
 static vti_status group_wait(vti_t *hs, int n)
 {
-    // a handle's next pack overwrites rows its neighbours copy from: wait for their copies too
+    // the next step's pack overwrites sbuf and its kernels read the unpacked halos: ev_comm
+    // covers both (the neighbours' buffers are protected by the ACK flags)
     for (int i = 0; i < n; ++i) {
         vti_s *h = hs[i];
         CU(h, cudaSetDevice(h->cfg.device));
-        for (int j = std::max(0, i - 1); j <= std::min(n - 1, i + 1); ++j)
-            CU(h, cudaStreamWaitEvent(h->stream, hs[j]->ev_comm, 0));
+        CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
     }
     return VTI_OK;
 }
@@ -1581,6 +1765,9 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         if (hs[i]->n != hs[0]->n) return fail(hs[i], VTI_E_STATE, "time indices differ inside the group");
     }
     if (n == 1) return vti_step(hs[0], nsteps);
+    for (int i = 0; i < n; ++i)
+        if (hs[i]->xseq != hs[0]->xseq) return fail(hs[i], VTI_E_STATE, "exchange counters differ inside the group");
+    group_connect(hs, n);
     vti_status s;
     bool dirty = false;
     for (int i = 0; i < n; ++i) dirty |= hs[i]->halo_dirty;

@@ -26,3 +26,50 @@ def max_over_ranks(dist, world: int, x: float, device="cpu") -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def connect_copy_engine(dist, handle, rank: int, world: int) -> bool:
+    """Connect a rank's handle to its y-neighbours for the copy-engine halo transport
+    (vti_ipc_export / vti_ipc_connect): every rank publishes its CUDA-IPC blob, then
+    opens the blobs of rank-1 and rank+1. Returns True on every rank only if every
+    rank succeeded (the decision is collective, so nobody waits on a peer that fell
+    back to NCCL)."""
+    if world == 1:
+        return False
+    blob = handle.ipc_export()
+    blobs = [None] * world
+    dist.all_gather_object(blobs, blob)
+    ok = 1
+    try:
+        handle.ipc_connect(blobs[rank - 1] if rank > 0 else None, blobs[rank + 1] if rank < world - 1 else None)
+    except Exception:
+        ok = 0
+    import torch
+    t = torch.tensor([ok], dtype=torch.int32)
+    try:
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    except RuntimeError:   # process groups whose backend needs device tensors
+        t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(int(t.item()))
+
+
+def sync_or_die(handle, timeout_s: float, what: str = "halo exchange") -> None:
+    """Wait for the handle's enqueued steps, polling its stream, and exit the process
+    loudly if they do not finish within timeout_s (a peer that never delivers its halo
+    must fail the run, not hang it). The main stream waits on every exchange, so its
+    completion covers the comm stream's work too."""
+    import os
+    import sys
+    import time
+
+    import torch
+    s = torch.cuda.ExternalStream(handle.stream())
+    t0 = time.monotonic()
+    while not s.query():
+        if time.monotonic() - t0 > timeout_s:
+            print(f"error: {what} did not complete within {timeout_s:.0f} s "
+                  f"(transport {handle.halo_transport}); aborting", file=sys.stderr, flush=True)
+            os._exit(3)
+        time.sleep(0.01)
+    handle.sync()
