@@ -300,14 +300,14 @@ def run_native(args):
     def fresh_nccl_id():
         return multi.broadcast_nccl_id(dist, rank, world)
 
-    halo = os.environ.get("VTI_HALO", "copy-engine") if world > 1 else "none"
+    halo = os.environ.get("VTI_HALO", "peer") if world > 1 else "none"
 
     def open_handle():
-        """A rank's handle with its halo transport: copy engine over CUDA IPC by default,
+        """A rank's handle with its halo transport: peer stores over CUDA IPC by default,
         NCCL if requested or if any rank cannot connect (collective fallback)."""
         if world > 1 and halo != "nccl":
             h = make_handle(cfg, dt, wxy, wz, rank, world, local, None, prec)
-            if multi.connect_copy_engine(dist, h, rank, world):
+            if multi.connect_peer(dist, h, rank, world):
                 return h
             h.close()
         return make_handle(cfg, dt, wxy, wz, rank, world, local, fresh_nccl_id(), prec)

@@ -238,22 +238,26 @@ vti_status vti_reverse(vti_t h);
 int32_t vti_direction(vti_t h);
 
 /*
- * Copy-engine halo transport for nranks > 1 (no NCCL, no SMs): p's packed
- * boundary rows are copied straight into the neighbours' receive buffers over
- * NVLink (CUDA IPC peer pointers) and ordered with flag words written and
- * waited on by stream memory operations. vti_ipc_export writes this rank's
- * VTI_IPC_BYTES blob; after exchanging blobs (e.g. all-gather over the job's
- * process group) every rank calls vti_ipc_connect with the blob of rank-1 (lo)
- * and rank+1 (hi), NULL at the ends. A handle created with an nccl_id that is
- * then connected uses this transport instead of NCCL. Both calls are
- * collective in effect: all ranks must connect before the next vti_step.
- * Errors: STATE (nranks < 2), PARAM (wrong blob), COMM (IPC / stream memory
+ * Fused peer-memory halo transport for nranks > 1 (no NCCL, no pack, copy or
+ * unpack): the edge step launch stores p^{n+1} of this slab's first / last R_xy
+ * rows both locally and straight into rank-1's top / rank+1's bottom halo rows
+ * through CUDA-IPC peer pointers (NVLink), and flag words written and waited on
+ * with stream memory operations order the steps.
+ * vti_ipc_export writes this rank's VTI_IPC_BYTES blob (IPC handles of both p
+ * buffers and the flag words, plus the slab geometry). After exchanging blobs
+ * (e.g. an all-gather over the job's process group), every rank calls
+ * vti_ipc_connect with the blob of rank-1 (lo) and rank+1 (hi), NULL at the
+ * ends. A handle created with an nccl_id that is then connected uses this
+ * transport instead of NCCL. Both calls are collective in effect: all ranks
+ * must connect before the next vti_step, and all ranks must then step together.
+ * Errors: STATE (nranks < 2, local-group handle), PARAM (blob of the wrong rank,
+ * job, geometry, precision, layout or version), COMM (IPC or stream memory
  * operations unavailable), CUDA.
  */
 vti_status vti_ipc_export(vti_t h, void *out);
 vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi);
 
-/* 0: none (single slab), 1: NCCL, 2: copy engine (local group or CUDA IPC). */
+/* 0: none (single slab), 1: NCCL, 2: fused peer stores (local group or CUDA IPC). */
 int32_t vti_halo_transport(vti_t h);
 
 /* Block until all work on the handle's stream(s) is done. */

@@ -319,7 +319,7 @@ class VTI:
             _check(self.h, self._fn("vti_get_traces")(self.h, out.ctypes.data))
         return ids, out
 
-    # -- multi-process copy-engine halo transport (CUDA IPC)
+    # -- multi-process fused peer-memory halo transport (CUDA IPC)
     IPC_BYTES = 512
 
     def ipc_export(self) -> bytes:
@@ -334,7 +334,7 @@ class VTI:
 
     @property
     def halo_transport(self) -> str:
-        return {0: "none", 1: "nccl", 2: "copy-engine"}.get(lib.vti_halo_transport(self.h), "?")
+        return {0: "none", 1: "nccl", 2: "peer"}.get(lib.vti_halo_transport(self.h), "?")
 
     def reverse(self):
         _check(self.h, lib.vti_reverse(self.h))

@@ -9,7 +9,8 @@ static KernelEntry entry()
 {
     using namespace vti;
     return KernelEntry{(int)sizeof(T), R, RZ, TY, RPT, WP, S, B, Cfg<T, R, RZ, TY>::STAGE,
-                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B>, Cfg<T, R, RZ, TY>::ZROW,
+                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B, false>,
+                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B, true>, Cfg<T, R, RZ, TY>::ZROW,
                        nthreads(TY, RPT, WP)};
 }
 

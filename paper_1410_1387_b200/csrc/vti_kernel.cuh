@@ -86,6 +86,13 @@ struct StepParams {
     CUtensorMap tm_vz;   // vz2
     T *p_out;            // p^{n+1}: interior row 0, plane 0 of the other p buffer
     T *q_out;            // q^{n+1}: interior row 0, plane 0 of the other q buffer
+    // Fused halo transport (y-slabs, peer memory): p^{n+1} of local rows [0, R) is also
+    // stored at rows [0, R) of peer_lo (rank-1's buffer from its top halo row, plane 0),
+    // and of local rows [nyl - R, nyl) at rows [0, R) of peer_hi (rank+1's buffer from
+    // its bottom halo row); peer_zs_* are the neighbours' plane strides. NULL = no peer.
+    T *peer_lo;
+    T *peer_hi;
+    long long peer_zs_lo, peer_zs_hi;
     const T *zrow;       // [nz][ZROW]: w^z[k][0..2Rz], gz[k], 0 ...
     const T *gx;         // [ntx * TX] (1 beyond nx)
     const T *gy;         // [nyl] local rows
@@ -294,7 +301,10 @@ struct Producer {
 //         on the ring); 17 warps per TY=32 CTA cap registers at 96.
 // WP = 0: the CTA's first thread issues load j + STAGES right after releasing
 //         load j; 16 warps allow 128 registers (needed for the R_z >= 6 queues).
-template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB>
+// PEER: also store the boundary rows into the neighbours' halo rows (StepParams::peer_*);
+// only the edge launch of a peer-connected slab uses it, so the other launches keep
+// the register allocation of the plain kernel.
+template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB, bool PEER>
 __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(const __grid_constant__ StepParams<T> P)
 {
     using C = Cfg<T, R, RZ, TY>;
@@ -483,6 +493,17 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                             const long long off = (long long)k * P.zs;
                             stg4(pout[r] + off, pn[r]);
                             stg4(qout[r] + off, qn[r]);
+                            if constexpr (PEER) {
+                                // the neighbours' halo rows, straight over NVLink (edge tile rows
+                                // only; a row goes to both sides when nyl < 2R)
+                                const int yl = y0 + tg * RPT + r;
+                                if (P.peer_lo != nullptr && yl < R)
+                                    stg4(P.peer_lo + (long long)k * P.peer_zs_lo + (long long)yl * P.ys + xg, pn[r]);
+                                if (P.peer_hi != nullptr && yl >= P.nyl - R)
+                                    stg4(P.peer_hi + (long long)k * P.peer_zs_hi +
+                                             (long long)(yl - (P.nyl - R)) * P.ys + xg,
+                                         pn[r]);
+                            }
                         }
                     }
                 }

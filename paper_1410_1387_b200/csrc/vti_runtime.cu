@@ -323,14 +323,17 @@ struct vti_s {
     double src_f = 15.0, src_t0 = 0.0, src_amp = 1.0;
     ncclComm_t comm_nccl = nullptr;
     bool group_mode = false;
-    // copy-engine halo transport (local group, or multi-process after vti_ipc_connect):
+    // fused peer-memory halo transport (local group, or multi-process after vti_ipc_connect):
+    // the edge launch stores p^{n+1}'s boundary rows straight into the neighbours' halo rows;
     // flags[] = {DATA_LO, DATA_HI, ACK_LO, ACK_HI}, written by the neighbours
-    bool p2p = false;
+    bool peer = false;
     unsigned int *flags = nullptr;
-    void *peer_rbuf[2] = {nullptr, nullptr};          // [0]: rank-1's rbuf[1], [1]: rank+1's rbuf[0]
+    void *peer_p[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][b]: neighbour's pbuf[b] at the
+                                                                      // first halo row this rank writes
+    long long peer_zs[2] = {0, 0};                    // the neighbours' plane strides (elements)
     unsigned int *peer_flags[2] = {nullptr, nullptr}; // the neighbours' flags
     void *ipc_opened[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // cudaIpcCloseMemHandle on destroy
-    unsigned int xseq = 0;                            // exchanges so far (the flag values)
+    unsigned int xseq = 0;                            // halo publications so far (the flag values)
     bool flush_remote = false;                        // CU_STREAM_WAIT_VALUE_FLUSH supported
     bool halo_dirty = false;
     bool suppress_src = false;                // autotune probes inject nothing
@@ -714,6 +717,7 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
     h->nty = (h->nyl + h->TY - 1) / h->TY;
     h->smem_bytes = K->stages * K->stage_bytes + 2 * K->stages * 8;
     CU(h, cudaFuncSetAttribute(K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+    CU(h, cudaFuncSetAttribute(K->fn_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
     CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, K->fn, K->threads, h->smem_bytes));
     if (h->ctas_per_sm < 1) return fail(h, VTI_E_CUDA, "step kernel cannot be resident (smem %d B)", h->smem_bytes);
     if (h->tune_ctas > 0) h->ctas_per_sm = std::min(h->ctas_per_sm, h->tune_ctas);
@@ -1051,6 +1055,10 @@ static void fill_params(vti_s *h, StepParams<T> &P, int tr0, int ntr0, int tr1, 
     P.tm_vz = h->tm_vz;
     P.p_out = (T *)h->p_int(o);
     P.q_out = (T *)h->q_int(o);
+    P.peer_lo = h->peer ? (T *)h->peer_p[0][o] : nullptr;
+    P.peer_hi = h->peer ? (T *)h->peer_p[1][o] : nullptr;
+    P.peer_zs_lo = h->peer_zs[0];
+    P.peer_zs_hi = h->peer_zs[1];
     P.zrow = (const T *)h->zrow;
     P.gx = (const T *)h->gx;
     P.gy = (const T *)h->gy;
@@ -1110,7 +1118,10 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
         lc.numAttrs = 1;
     }
     void *args[] = {&P};
-    CU(h, cudaLaunchKernelExC(&lc, h->K->fn, args));
+    // only tile rows within R of the slab edges store into the neighbours (edge launches)
+    const bool peer_rows = (P.peer_lo || P.peer_hi) && (tr0 * h->TY < h->R || (tr0 + ntr0) * h->TY > h->nyl - h->R ||
+                                                        (ntr1 > 0 && (tr1 + ntr1) * h->TY > h->nyl - h->R));
+    CU(h, cudaLaunchKernelExC(&lc, peer_rows ? h->K->fn_peer : h->K->fn, args));
     return VTI_OK;
 }
 
@@ -1186,74 +1197,112 @@ static vti_status exchange_nccl(vti_s *h, int b)
     return VTI_OK;
 }
 
-// Copy-engine transport (no SMs, no NCCL): after the edge launch and the pack,
-// the comm stream copies each packed boundary block straight into the
-// neighbour's receive buffer over NVLink (UVA / CUDA-IPC peer pointer) and then
-// bumps the neighbour's DATA flag; it waits for its own DATA flags, unpacks, and
-// bumps the neighbours' ACK flags; before the next copy into a neighbour's
-// buffer it waits for that neighbour's ACK of the previous one. Flags are
-// monotone exchange counters; cuStreamWaitValue32/WriteValue32 order them with
-// the copies on the GPU front end. Records ev_comm.
-//
-// Enqueue order matters: streams share a small pool of in-order hardware
-// channels, so a value-wait may only wait on a write that was ENQUEUED EARLIER
-// (the same rule that makes event waits safe). The send half (ACK wait of the
-// previous exchange, copy, DATA write) and the receive half (DATA wait, unpack,
-// ACK write) are therefore separate calls, and a local group enqueues every
-// handle's send half before any receive half.
+// Fused peer-memory transport (no NCCL, no pack/copy/unpack): the edge launch
+// itself stores p^{n+1} of this slab's first / last R rows into rank-1's top /
+// rank+1's bottom halo rows through peer pointers (NVLink; the neighbours' own
+// buffers in a local group, CUDA-IPC mappings across processes), so the halo
+// travels tile by tile while the edge tiles are computed. Publication j is the
+// halo of the level the next step reads; flags[] are monotone counters written
+// by the neighbours with cuStreamWriteValue32 (which fences the kernel's peer
+// stores before the flag) and waited on with cuStreamWaitValue32, all on the
+// main stream:
+//   before the edge launch that consumes publication j:
+//     DATA >= j    the neighbours' rows of this level are in our halo
+//     ACK  >= j-1  the neighbours have read the halo we are about to overwrite
+//                  (publication j+1 lands in the buffer parity of j-1)
+//   after it: the neighbours' ACK = j (only the edge launch reads halo rows)
+//             and DATA = j+1.
+// Enqueue-order rule: streams share a small pool of in-order hardware channels,
+// so a value-wait may only wait on a write ENQUEUED EARLIER (the rule that makes
+// event waits safe); a local group therefore enqueues every handle's step j
+// writes before any handle's step j+1 waits, and splits a re-publication into
+// a release half and a publish half.
 enum { F_DATA_LO = 0, F_DATA_HI = 1, F_ACK_LO = 2, F_ACK_HI = 3 };
 
 static CUdeviceptr dev_ptr(const void *p) { return (CUdeviceptr)(uintptr_t)p; }
+static bool has_side(const vti_s *h, int side) { return side == 0 ? h->cfg.rank > 0 : h->cfg.rank < h->cfg.nranks - 1; }
 
-static vti_status exchange_p2p_send(vti_s *h)
+static vti_status flag_wait(vti_s *h, int idx, unsigned int v, bool remote_data)
 {
     const StreamMemOps &ops = stream_mem_ops();
-    if (!ops.wait || !ops.write) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
-    const unsigned int k = ++h->xseq;
-    const size_t bytes = halo_elems(h) * h->es;
-    CUstream cs = (CUstream)h->comm;
-    CU(h, cudaStreamWaitEvent(h->comm, h->ev_edge, 0));
-    for (int side = 0; side < 2; ++side) {   // 0: our first R rows -> rank-1, 1: our last R rows -> rank+1
-        if (side == 0 ? h->cfg.rank == 0 : h->cfg.rank == h->cfg.nranks - 1) continue;
-        if (ops.wait(cs, dev_ptr(h->flags + (side == 0 ? F_ACK_LO : F_ACK_HI)), k - 1, CU_STREAM_WAIT_VALUE_GEQ) !=
-            CUDA_SUCCESS)
-            return fail(h, VTI_E_COMM, "cuStreamWaitValue32 failed");
-        CU(h, cudaMemcpyAsync(h->peer_rbuf[side], h->sbuf[side], bytes, cudaMemcpyDefault, h->comm));
-        if (ops.write(cs, dev_ptr(h->peer_flags[side] + (side == 0 ? F_DATA_HI : F_DATA_LO)), k,
-                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-            return fail(h, VTI_E_COMM, "cuStreamWriteValue32 failed");
+    if (!ops.wait) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
+    unsigned fl = CU_STREAM_WAIT_VALUE_GEQ;
+    if (remote_data && h->flush_remote) fl |= CU_STREAM_WAIT_VALUE_FLUSH;
+    if (ops.wait((CUstream)h->stream, dev_ptr(h->flags + idx), v, fl) != CUDA_SUCCESS)
+        return fail(h, VTI_E_COMM, "cuStreamWaitValue32 failed");
+    return VTI_OK;
+}
+
+// the neighbour on `side` sees flag `idx` (its own numbering) become v
+static vti_status flag_write(vti_s *h, int side, int idx, unsigned int v)
+{
+    const StreamMemOps &ops = stream_mem_ops();
+    if (!ops.write) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
+    if (ops.write((CUstream)h->stream, dev_ptr(h->peer_flags[side] + idx), v, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+        CUDA_SUCCESS)
+        return fail(h, VTI_E_COMM, "cuStreamWriteValue32 failed");
+    return VTI_OK;
+}
+
+static vti_status peer_pre_step(vti_s *h)
+{
+    const unsigned int j = h->xseq;
+    vti_status s;
+    for (int side = 0; side < 2; ++side) {
+        if (!has_side(h, side)) continue;
+        if ((s = flag_wait(h, side == 0 ? F_DATA_LO : F_DATA_HI, j, true)) != VTI_OK) return s;
+        if (j >= 1 && (s = flag_wait(h, side == 0 ? F_ACK_LO : F_ACK_HI, j - 1, false)) != VTI_OK) return s;
     }
     return VTI_OK;
 }
 
-static vti_status exchange_p2p_recv(vti_s *h, int b)
+static vti_status peer_post_edge(vti_s *h)
 {
-    const StreamMemOps &ops = stream_mem_ops();
-    const unsigned int k = h->xseq;
-    CUstream cs = (CUstream)h->comm;
-    const unsigned wait_flags = h->flush_remote ? CU_STREAM_WAIT_VALUE_GEQ | CU_STREAM_WAIT_VALUE_FLUSH
-                                                : CU_STREAM_WAIT_VALUE_GEQ;
-    for (int side = 0; side < 2; ++side) {   // 0: rows from rank-1 -> halo rows [0,R), 1: from rank+1
-        if (side == 0 ? h->cfg.rank == 0 : h->cfg.rank == h->cfg.nranks - 1) continue;
-        if (ops.wait(cs, dev_ptr(h->flags + (side == 0 ? F_DATA_LO : F_DATA_HI)), k, wait_flags) != CUDA_SUCCESS)
-            return fail(h, VTI_E_COMM, "cuStreamWaitValue32 failed");
-        unpack(h, h->rbuf[side], h->pbuf[b], side == 0 ? 0 : h->nyl + h->R, h->comm);
-        CU(h, cudaGetLastError());
-        if (ops.write(cs, dev_ptr(h->peer_flags[side] + (side == 0 ? F_ACK_HI : F_ACK_LO)), k,
-                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-            return fail(h, VTI_E_COMM, "cuStreamWriteValue32 failed");
+    const unsigned int j = h->xseq;
+    vti_status s;
+    for (int side = 0; side < 2; ++side) {
+        if (!has_side(h, side)) continue;
+        if ((s = flag_write(h, side, side == 0 ? F_ACK_HI : F_ACK_LO, j)) != VTI_OK) return s;
+        if ((s = flag_write(h, side, side == 0 ? F_DATA_HI : F_DATA_LO, j + 1)) != VTI_OK) return s;
     }
-    CU(h, cudaEventRecord(h->ev_comm, h->comm));
+    h->xseq = j + 1;
     return VTI_OK;
 }
 
-static vti_status exchange_p2p(vti_s *h, int b)
+// Re-publication of the current level (state set by the caller, vti_reverse). Release
+// half: everything published so far is consumed or abandoned (stream-ordered after
+// this rank's last read of its halo).
+static vti_status peer_release(vti_s *h)
 {
-    vti_status s = exchange_p2p_send(h);
-    return s != VTI_OK ? s : exchange_p2p_recv(h, b);
+    vti_status s;
+    for (int side = 0; side < 2; ++side)
+        if (has_side(h, side) && (s = flag_write(h, side, side == 0 ? F_ACK_HI : F_ACK_LO, h->xseq)) != VTI_OK)
+            return s;
+    return VTI_OK;
 }
 
-static vti_status exchange(vti_s *h, int b) { return h->p2p ? exchange_p2p(h, b) : exchange_nccl(h, b); }
+// Publish half: once the neighbours released every earlier publication, copy this
+// rank's boundary rows of the current level into their halo rows (R contiguous
+// rows per plane on both sides: one 2-D copy per neighbour), then DATA.
+static vti_status peer_publish(vti_s *h)
+{
+    const unsigned int j = ++h->xseq;
+    vti_status s;
+    // [z][y][x]: R rows are contiguous within each plane; [y][z][x]: the R rows of every plane are one block
+    const size_t width = (size_t)h->R * h->ys * h->es;
+    const size_t height = h->layout_zyx ? (size_t)h->cfg.nz : 1;
+    for (int side = 0; side < 2; ++side) {
+        if (!has_side(h, side)) continue;
+        if ((s = flag_wait(h, side == 0 ? F_ACK_LO : F_ACK_HI, j - 1, false)) != VTI_OK) return s;
+        const char *src = (const char *)h->pbuf[h->cur] + (size_t)(side == 0 ? h->R : h->nyl) * h->ys * h->es;
+        const size_t spitch = h->layout_zyx ? (size_t)h->zs * h->es : width;
+        const size_t dpitch = h->layout_zyx ? (size_t)h->peer_zs[side] * h->es : width;
+        CU(h, cudaMemcpy2DAsync(h->peer_p[side][h->cur], dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                h->stream));
+        if ((s = flag_write(h, side, side == 0 ? F_DATA_HI : F_DATA_LO, j)) != VTI_OK) return s;
+    }
+    return VTI_OK;
+}
 
 static vti_status check_finite(vti_s *h)
 {
@@ -1363,14 +1412,14 @@ static vti_status get_traces(vti_s *h, int es, void *out)
 vti_status vti_get_traces(vti_t h, float *out) { return get_traces(h, 4, out); }
 vti_status vti_get_traces_f64(vti_t h, double *out) { return get_traces(h, 8, out); }
 
-// ---- multi-process copy-engine transport over CUDA IPC
+// ---- multi-process fused peer transport over CUDA IPC
 struct IpcBlob {
     uint32_t magic, version;
-    int32_t rank, nranks;
-    cudaIpcMemHandle_t rbuf[2], flags;
+    int32_t rank, nranks, nyl, nxp, R, es, zyx;
+    cudaIpcMemHandle_t pbuf[2], flags;
 };
 static_assert(sizeof(IpcBlob) <= VTI_IPC_BYTES, "IPC blob too large");
-static const uint32_t IPC_MAGIC = 0x56544931u;   // "VTI1"
+static const uint32_t IPC_MAGIC = 0x56544932u;   // "VTI2"
 
 vti_status vti_ipc_export(vti_t h, void *out)
 {
@@ -1383,8 +1432,13 @@ vti_status vti_ipc_export(vti_t h, void *out)
     b.version = VTI_ABI_VERSION;
     b.rank = h->cfg.rank;
     b.nranks = h->cfg.nranks;
-    CU(h, cudaIpcGetMemHandle(&b.rbuf[0], h->rbuf[0]));
-    CU(h, cudaIpcGetMemHandle(&b.rbuf[1], h->rbuf[1]));
+    b.nyl = h->nyl;
+    b.nxp = h->nxp;
+    b.R = h->R;
+    b.es = h->es;
+    b.zyx = h->layout_zyx;
+    CU(h, cudaIpcGetMemHandle(&b.pbuf[0], h->pbuf[0]));
+    CU(h, cudaIpcGetMemHandle(&b.pbuf[1], h->pbuf[1]));
     CU(h, cudaIpcGetMemHandle(&b.flags, h->flags));
     memset(out, 0, VTI_IPC_BYTES);
     memcpy(out, &b, sizeof b);
@@ -1396,6 +1450,7 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
     if (!h) return VTI_E_PARAM;
     const int r = h->cfg.rank, nr = h->cfg.nranks;
     if (nr < 2) return fail(h, VTI_E_STATE, "vti_ipc_connect needs nranks > 1");
+    if (h->group_mode) return fail(h, VTI_E_STATE, "local-group handles connect through vti_group_step");
     if ((r > 0) != (lo != nullptr) || (r < nr - 1) != (hi != nullptr))
         return fail(h, VTI_E_PARAM, "pass the blob of rank-1 (lo) and rank+1 (hi), NULL at the ends");
     const StreamMemOps &ops = stream_mem_ops();
@@ -1407,25 +1462,30 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
         IpcBlob b;
         memcpy(&b, blobs[side], sizeof b);
         if (b.magic != IPC_MAGIC || b.version != (uint32_t)VTI_ABI_VERSION || b.nranks != nr ||
-            b.rank != (side == 0 ? r - 1 : r + 1))
-            return fail(h, VTI_E_PARAM, "IPC blob of the wrong rank, job or library version");
-        void *rb = nullptr, *fl = nullptr;
-        // rank-1 receives our first rows in its rbuf[1]; rank+1 our last rows in its rbuf[0]
-        cudaError_t e = cudaIpcOpenMemHandle(&rb, b.rbuf[side == 0 ? 1 : 0], cudaIpcMemLazyEnablePeerAccess);
+            b.rank != (side == 0 ? r - 1 : r + 1) || b.nxp != h->nxp || b.R != h->R || b.es != h->es ||
+            b.zyx != (int32_t)h->layout_zyx)
+            return fail(h, VTI_E_PARAM, "IPC blob of the wrong rank, job, geometry or library version");
+        void *pb[2] = {nullptr, nullptr}, *fl = nullptr;
+        for (int k = 0; k < 2; ++k) {
+            cudaError_t e = cudaIpcOpenMemHandle(&pb[k], b.pbuf[k], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+            h->ipc_opened[3 * side + k] = pb[k];
+        }
+        cudaError_t e = cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-        h->ipc_opened[3 * side] = rb;
-        e = cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess);
-        if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-        h->ipc_opened[3 * side + 1] = fl;
-        h->peer_rbuf[side] = rb;
+        h->ipc_opened[3 * side + 2] = fl;
+        // rank-1: our first rows go to its top halo (row R + nyl); rank+1: our last rows to its row 0.
+        // Same layout on both sides, so the row stride is ours (h->ys); the plane stride is theirs.
+        const size_t row0 = side == 0 ? (size_t)b.R + b.nyl : 0;
+        for (int k = 0; k < 2; ++k) h->peer_p[side][k] = (char *)pb[k] + row0 * h->ys * (size_t)b.es;
+        h->peer_zs[side] = b.zyx ? (long long)(b.nyl + 2 * b.R) * b.nxp : (long long)b.nxp;
         h->peer_flags[side] = (unsigned int *)fl;
     }
-    h->p2p = true;
-    h->group_mode = false;
+    h->peer = true;
     return VTI_OK;
 }
 
-int32_t vti_halo_transport(vti_t h) { return !h ? -1 : h->cfg.nranks < 2 ? 0 : h->p2p ? 2 : h->comm_nccl ? 1 : 0; }
+int32_t vti_halo_transport(vti_t h) { return !h ? -1 : h->cfg.nranks < 2 ? 0 : h->peer ? 2 : h->comm_nccl ? 1 : 0; }
 
 vti_status vti_reverse(vti_t h)
 {
@@ -1647,16 +1707,20 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     if (nsteps < 0) return fail(h, VTI_E_PARAM, "nsteps < 0");
     if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
     if (h->group_mode) return fail(h, VTI_E_STATE, "local-group handle: use vti_group_step");
-    if (h->cfg.nranks > 1 && !h->p2p && !h->comm_nccl)
+    if (h->cfg.nranks > 1 && !h->peer && !h->comm_nccl)
         return fail(h, VTI_E_STATE, "nranks > 1 needs an nccl_id at create time or vti_ipc_connect");
     CU(h, cudaSetDevice(h->cfg.device));
     const bool multi = h->cfg.nranks > 1;
     vti_status s;
     if (multi && h->halo_dirty) {   // halos of a state set by the caller
-        if ((s = pack_send(h, h->cur)) != VTI_OK) return s;
-        CU(h, cudaEventRecord(h->ev_edge, h->stream));
-        if ((s = exchange(h, h->cur)) != VTI_OK) return s;
-        CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
+        if (h->peer) {
+            if ((s = peer_release(h)) != VTI_OK || (s = peer_publish(h)) != VTI_OK) return s;
+        } else {
+            if ((s = pack_send(h, h->cur)) != VTI_OK) return s;
+            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+            if ((s = exchange_nccl(h, h->cur)) != VTI_OK) return s;
+            CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
+        }
         h->halo_dirty = false;
     }
     int it = 0;
@@ -1673,13 +1737,19 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     for (; it < nsteps; ++it) {
         if (!multi) {
             if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk)) != VTI_OK) return s;
+        } else if (h->peer) {
+            // the edge launch stores the neighbours' halo rows itself; the interior overlaps their edges
+            if ((s = peer_pre_step(h)) != VTI_OK) return s;
+            if ((s = launch_edge(h)) != VTI_OK) return s;
+            if ((s = peer_post_edge(h)) != VTI_OK) return s;
+            if ((s = launch_interior(h)) != VTI_OK) return s;
         } else {
             const int o = 1 - h->cur;
             // edge tile rows first, so the rows the neighbours need are ready early
             if ((s = launch_edge(h)) != VTI_OK) return s;
             if ((s = pack_send(h, o)) != VTI_OK) return s;
             CU(h, cudaEventRecord(h->ev_edge, h->stream));
-            if ((s = exchange(h, o)) != VTI_OK) return s;
+            if ((s = exchange_nccl(h, o)) != VTI_OK) return s;
             if ((s = launch_interior(h)) != VTI_OK) return s;   // overlaps the exchange
             CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         }
@@ -1707,49 +1777,23 @@ vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms)
     return VTI_OK;
 }
 
-// Local group: the same pack / transport / unpack schedule, transport = peer copies of the packed rows.
-// Local group: the copy-engine transport between handles of one process (peer
-// pointers are the neighbours' own device buffers), the same protocol as the
-// multi-process CUDA-IPC transport.
+// Local group: the fused peer-memory transport between handles of one process
+// (peer pointers are the neighbours' own device buffers), the same protocol as the
+// multi-process CUDA-IPC form.
 static void group_connect(vti_t *hs, int n)
 {
     for (int i = 0; i < n; ++i) {
         vti_s *h = hs[i];
-        h->p2p = true;
-        h->peer_rbuf[0] = i > 0 ? hs[i - 1]->rbuf[1] : nullptr;
-        h->peer_flags[0] = i > 0 ? hs[i - 1]->flags : nullptr;
-        h->peer_rbuf[1] = i < n - 1 ? hs[i + 1]->rbuf[0] : nullptr;
-        h->peer_flags[1] = i < n - 1 ? hs[i + 1]->flags : nullptr;
+        h->peer = true;
+        for (int side = 0; side < 2; ++side) {
+            const vti_s *nb = side == 0 ? (i > 0 ? hs[i - 1] : nullptr) : (i < n - 1 ? hs[i + 1] : nullptr);
+            for (int b = 0; b < 2; ++b)
+                h->peer_p[side][b] = !nb ? nullptr
+                                         : (char *)nb->pbuf[b] + (size_t)(side == 0 ? nb->R + nb->nyl : 0) * nb->ys * nb->es;
+            h->peer_zs[side] = nb ? nb->zs : 0;
+            h->peer_flags[side] = nb ? nb->flags : nullptr;
+        }
     }
-}
-
-static vti_status group_exchange(vti_t *hs, int n, bool current)
-{
-    // every handle's send half before any receive half (see exchange_p2p_send)
-    for (int i = 0; i < n; ++i) {
-        CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
-        vti_status s = exchange_p2p_send(hs[i]);
-        if (s != VTI_OK) return s;
-    }
-    for (int i = 0; i < n; ++i) {
-        vti_s *h = hs[i];
-        CU(h, cudaSetDevice(h->cfg.device));
-        vti_status s = exchange_p2p_recv(h, current ? h->cur : 1 - h->cur);
-        if (s != VTI_OK) return s;
-    }
-    return VTI_OK;
-}
-
-static vti_status group_wait(vti_t *hs, int n)
-{
-    // the next step's pack overwrites sbuf and its kernels read the unpacked halos: ev_comm
-    // covers both (the neighbours' buffers are protected by the ACK flags)
-    for (int i = 0; i < n; ++i) {
-        vti_s *h = hs[i];
-        CU(h, cudaSetDevice(h->cfg.device));
-        CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
-    }
-    return VTI_OK;
 }
 
 vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
@@ -1766,40 +1810,38 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
     }
     if (n == 1) return vti_step(hs[0], nsteps);
     for (int i = 0; i < n; ++i)
-        if (hs[i]->xseq != hs[0]->xseq) return fail(hs[i], VTI_E_STATE, "exchange counters differ inside the group");
+        if (hs[i]->xseq != hs[0]->xseq || hs[i]->cur != hs[0]->cur)
+            return fail(hs[i], VTI_E_STATE, "halo publications or buffer parity differ inside the group");
     group_connect(hs, n);
     vti_status s;
     bool dirty = false;
     for (int i = 0; i < n; ++i) dirty |= hs[i]->halo_dirty;
-    if (dirty) {
+    if (dirty) {   // every release before any publish (enqueue-order rule)
         for (int i = 0; i < n; ++i) {
             CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
-            if ((s = pack_send(hs[i], hs[i]->cur)) != VTI_OK) return s;
-            CU(hs[i], cudaEventRecord(hs[i]->ev_edge, hs[i]->stream));
+            if ((s = peer_release(hs[i])) != VTI_OK) return s;
         }
-        if ((s = group_exchange(hs, n, true)) != VTI_OK) return s;
-        if ((s = group_wait(hs, n)) != VTI_OK) return s;
-        for (int i = 0; i < n; ++i) hs[i]->halo_dirty = false;
+        for (int i = 0; i < n; ++i) {
+            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+            if ((s = peer_publish(hs[i])) != VTI_OK) return s;
+            hs[i]->halo_dirty = false;
+        }
     }
     for (int it = 0; it < nsteps; ++it) {
-        for (int i = 0; i < n; ++i) {
+        for (int i = 0; i < n; ++i) {   // waits on the previous step's writes only
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
+            if ((s = peer_pre_step(h)) != VTI_OK) return s;
             if ((s = launch_edge(h)) != VTI_OK) return s;
-            if ((s = pack_send(h, 1 - h->cur)) != VTI_OK) return s;
-            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+            if ((s = peer_post_edge(h)) != VTI_OK) return s;
         }
-        if ((s = group_exchange(hs, n, false)) != VTI_OK) return s;
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
             if ((s = launch_interior(h)) != VTI_OK) return s;
-        }
-        if ((s = group_wait(hs, n)) != VTI_OK) return s;
-        for (int i = 0; i < n; ++i) {
-            hs[i]->cur = 1 - hs[i]->cur;
-            hs[i]->n += hs[i]->dir;
-            if ((s = record(hs[i])) != VTI_OK) return s;
+            h->cur = 1 - h->cur;
+            h->n += h->dir;
+            if ((s = record(h)) != VTI_OK) return s;
         }
     }
     return VTI_OK;
@@ -1833,11 +1875,11 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->zchunk = h->zchunk;
     info->grid = std::min(h->ntx * h->nty * h->nzc, h->sms * h->ctas_per_sm);
     info->work_items = h->ntx * h->nty * h->nzc;
-    if (h->cfg.nranks > 1) {   // edge + interior step kernels, then pack + unpack per neighbour
+    if (h->cfg.nranks > 1) {   // edge + interior step kernels (+ pack and unpack per neighbour with NCCL)
         const int neighbours = (h->cfg.rank > 0) + (h->cfg.rank < h->cfg.nranks - 1);
         int e1, e2;
         edge_rows(h, e1, e2);
-        info->launches_per_step = 1 + (e2 > e1 ? 1 : 0) + 2 * neighbours;
+        info->launches_per_step = 1 + (e2 > e1 ? 1 : 0) + (h->peer || h->group_mode ? 0 : 2 * neighbours);
     } else {
         info->launches_per_step = 1;
     }

@@ -9,7 +9,8 @@
 
 struct KernelEntry {
     int esize, r, rz, ty, rpt, wp, stages, minb, stage_bytes;
-    const void *fn;   // host stub of the instantiation (cudaLaunchKernelExC with a StepParams<T> argument)
+    const void *fn;        // host stub of the instantiation (cudaLaunchKernelExC with a StepParams<T> argument)
+    const void *fn_peer;   // the same with the fused peer-halo stores (edge launches of peer-connected slabs)
     int zrow;
     int threads;
 };

@@ -28,8 +28,8 @@ def max_over_ranks(dist, world: int, x: float, device="cpu") -> float:
     return float(t.item())
 
 
-def connect_copy_engine(dist, handle, rank: int, world: int) -> bool:
-    """Connect a rank's handle to its y-neighbours for the copy-engine halo transport
+def connect_peer(dist, handle, rank: int, world: int) -> bool:
+    """Connect a rank's handle to its y-neighbours for the fused peer-memory halo transport
     (vti_ipc_export / vti_ipc_connect): every rank publishes its CUDA-IPC blob, then
     opens the blobs of rank-1 and rank+1. Returns True on every rank only if every
     rank succeeded (the decision is collective, so nobody waits on a peer that fell

@@ -104,7 +104,7 @@ def _worker(rank, world, port, nsteps, q):
         assert all(i == ids[0] for i in allids)
         assert multi.max_over_ranks(dist, world, float(rank + 1)) == float(world)
 
-        # copy-engine transport bootstrap: each rank connects to the blobs of rank-1 / rank+1,
+        # peer transport bootstrap: each rank connects to the blobs of rank-1 / rank+1,
         # and one rank failing makes every rank fall back (collective decision)
         class MockHandle:
             def __init__(self, fail):
@@ -119,10 +119,10 @@ def _worker(rank, world, port, nsteps, q):
                     raise RuntimeError("no peer access")
 
         h = MockHandle(fail=False)
-        assert multi.connect_copy_engine(dist, h, rank, world)
+        assert multi.connect_peer(dist, h, rank, world)
         assert h.got == (b"blob-%d" % (rank - 1) if rank > 0 else None,
                          b"blob-%d" % (rank + 1) if rank < world - 1 else None)
-        assert not multi.connect_copy_engine(dist, MockHandle(fail=(rank == world - 1)), rank, world)
+        assert not multi.connect_peer(dist, MockHandle(fail=(rank == world - 1)), rank, world)
 
         gathered = [None] * world
         dist.all_gather_object(gathered, (y0, [m.copy() for m in mine]))

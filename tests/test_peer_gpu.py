@@ -1,0 +1,194 @@
+"""GPU tests of the fused peer-memory halo transport.
+
+The edge launch of a y-slab stores p^{n+1} of its first / last R_xy rows into
+the neighbours' halo rows itself (a separate PEER instantiation of every
+compiled variant), and stream flag operations order the steps. A local group
+(several handles in one process on cuda:0) runs exactly that protocol with the
+neighbours' own buffers as peer memory, so every case here is a multi-slab run
+compared bitwise with the single-domain oracle (or, for time reversal, with the
+single-slab library run that tests/test_n4_gpu.py pins to the oracle).
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import fields as SF
+
+from test_parity_gpu import random_state, small_cfg
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def compiled_variants():
+    """(precision, r, rz, ty, wp, rpt) of every entry<...> in csrc/variants/*.cu."""
+    out = []
+    d = os.path.join(ROOT, "paper_1410_1387_b200", "csrc", "variants")
+    for f in sorted(os.listdir(d)):
+        if f.endswith(".cu"):
+            for m in re.finditer(r"entry<(float|double),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),", open(os.path.join(d, f)).read()):
+                t, r, rz, ty, rpt, wp = m.groups()
+                out.append((32 if t == "float" else 64, int(r), int(rz), int(ty), int(wp), int(rpt)))
+    return out
+
+
+def handles(cfg, dt, wxy, wz, nranks, precision=32):
+    from paper_1410_1387_b200 import VTI
+    return [VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], cfg["r_xy"], cfg["r_z"], dt, wxy, wz,
+                damp_width=cfg["damp_width"], damp_alpha=cfg["damp_alpha"], device=0, rank=r, nranks=nranks,
+                precision=precision) for r in range(nranks)]
+
+
+def load(hs, model, state=None, n0=0, cfg=None):
+    for h in hs:
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_model(*[np.ascontiguousarray(a[:, sl]) for a in model])
+        if state is not None:
+            h.set_fields(*[np.ascontiguousarray(a[:, sl]) for a in state], time_index=n0)
+        if cfg is not None:
+            h.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+
+
+def gather(hs):
+    parts = [h.get_fields(0) + h.get_fields(1) for h in hs]
+    return [np.concatenate([p[f] for p in parts], axis=1) for f in range(4)]
+
+
+def close(hs):
+    for h in hs:
+        h.close()
+
+
+def f32_inputs(cfg, seed=7):
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    return wxy, wz, dt, model, random_state(cfg, seed=seed, amp=1e-4)
+
+
+def f64_inputs(cfg, seed=7):
+    from test_fp64_gpu import inputs, weights64
+    wxy, wz = weights64(cfg)
+    model, st = inputs(cfg, seed=seed)
+    return wxy, wz, synth.stable_dt(cfg), tuple(model), st
+
+
+@pytest.mark.parametrize("prec,r,rz,ty,wp,rpt", compiled_variants())
+def test_every_peer_instantiation(prec, r, rz, ty, wp, rpt):
+    """3 slabs (source on a slab boundary, interior tile rows present) in every compiled
+    variant: the PEER edge instantiation and the plain interior one, bitwise == oracle."""
+    ny = 3 * max(2 * ty + 2 * r, 40)
+    cfg = small_cfg(70, ny, 2 * rz + 12, r, rz, damp=5)
+    cfg["src"] = (30, ny // 3, cfg["nz"] // 2)   # first row of rank 1
+    wxy, wz, dt, model, st = (f64_inputs if prec == 64 else f32_inputs)(cfg)
+    hs = handles(cfg, dt, wxy, wz, 3, prec)
+    for h in hs:
+        h.set_variant(ty, wp, rpt)
+        info = h.info()
+        assert (info["tile_y"], info["producer_warp"], info["rows_per_thread"]) == (ty, wp, rpt)
+    load(hs, model, st, 2, cfg)
+    from paper_1410_1387_b200 import group_step
+    group_step(hs, 5)
+    got = gather(hs)
+    assert hs[1].halo_transport == "peer"
+    close(hs)
+    P = oracle.params(cfg, dt)
+    ref = oracle.run(P, wxy, wz, *model, st, n0=2, nsteps=5, dtype=np.float64 if prec == 64 else np.float32)[:4]
+    for f in range(4):
+        assert np.abs(ref[f]).max() > 0
+        assert np.array_equal(got[f], ref[f]), f"field {f}"
+
+
+@pytest.mark.parametrize("r,rz,ny,nranks", [(8, 4, 40, 4), (12, 8, 39, 3), (4, 4, 30, 5)])
+def test_slabs_thinner_than_two_radii(r, rz, ny, nranks):
+    """nyl < 2R: a boundary row is in both neighbours' halos (stored to both sides)."""
+    from paper_1410_1387_b200 import group_step
+    cfg = small_cfg(64, ny, 2 * rz + 8, r, rz, damp=3, src=(20, ny // 2, rz + 4))
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    hs = handles(cfg, dt, wxy, wz, nranks)
+    assert all(r <= h.ny_local < 2 * r for h in hs)
+    load(hs, model, st, 0, cfg)
+    group_step(hs, 4)
+    group_step(hs, 3)
+    got = gather(hs)
+    close(hs)
+    ref = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, st, nsteps=7)[:4]
+    for f in range(4):
+        assert np.array_equal(got[f], ref[f]), f"field {f}"
+
+
+def test_set_fields_mid_run_republishes():
+    """Steps, then a new state from the caller (halos re-published after the last step's
+    publication was abandoned), then more steps: bitwise == oracle from the new state."""
+    from paper_1410_1387_b200 import group_step
+    cfg = small_cfg(70, 90, 30, 4, 4, damp=5, src=(30, 45, 15))
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    hs = handles(cfg, dt, wxy, wz, 3)
+    load(hs, model, st, 0, cfg)
+    group_step(hs, 3)
+    st2 = random_state(cfg, seed=11, amp=1e-4)
+    for h in hs:
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_fields(*[np.ascontiguousarray(a[:, sl]) for a in st2], time_index=3)
+    group_step(hs, 4)
+    got = gather(hs)
+    close(hs)
+    ref = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, st2, n0=3, nsteps=4)[:4]
+    for f in range(4):
+        assert np.array_equal(got[f], ref[f]), f"field {f}"
+
+
+def test_reverse_in_a_group_equals_single_slab():
+    """Forward, vti_reverse (re-publication of the swapped level), backward: the group run
+    equals the single-slab run of the same calls bitwise."""
+    from paper_1410_1387_b200 import group_step
+    cfg = small_cfg(70, 80, 30, 4, 4, damp=5, src=(30, 40, 15))
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    (one,) = handles(cfg, dt, wxy, wz, 1)
+    load([one], model, st, 0, cfg)
+    one.step(6)
+    one.reverse()
+    one.step(4)
+    ref = one.get_fields(0) + one.get_fields(1)
+    one.close()
+    hs = handles(cfg, dt, wxy, wz, 2)
+    load(hs, model, st, 0, cfg)
+    group_step(hs, 6)
+    for h in hs:
+        h.reverse()
+    group_step(hs, 4)
+    got = gather(hs)
+    close(hs)
+    for f in range(4):
+        assert np.array_equal(got[f], ref[f]), f"field {f}"
+
+
+def test_yzx_layout_group(monkeypatch):
+    """The [y][z][x] layout: different row / plane strides for the peer stores and the
+    re-publication copy."""
+    from paper_1410_1387_b200 import group_step
+    monkeypatch.setenv("VTI_LAYOUT", "yzx")
+    cfg = small_cfg(70, 75, 26, 4, 4, damp=5, src=(30, 37, 13))
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    hs = handles(cfg, dt, wxy, wz, 3)
+    assert hs[0].info()["layout"] == 1
+    load(hs, model, st, 0, cfg)
+    group_step(hs, 5)
+    got = gather(hs)
+    close(hs)
+    ref = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, st, nsteps=5)[:4]
+    for f in range(4):
+        assert np.array_equal(got[f], ref[f]), f"field {f}"
+
+
+def test_peer_group_launches_two_kernels_per_step():
+    cfg = small_cfg(70, 450, 26, 4, 4, damp=5, src=(30, 100, 13))   # 150-row slabs: edge + interior
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    hs = handles(cfg, dt, wxy, wz, 3)
+    assert [h.info()["launches_per_step"] for h in hs] == [2, 2, 2]
+    close(hs)
