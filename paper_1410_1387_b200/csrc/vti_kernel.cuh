@@ -32,6 +32,13 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <type_traits>
+
+// fp32 arithmetic on packed pairs (FFMA2 / FADD2 / FMUL2, sm_100a); 0 = scalar form (A/B builds)
+#ifndef VTI_PACKED_F32
+#define VTI_PACKED_F32 1
+#endif
+
 namespace vti {
 
 constexpr int TX = 64;               // tile width in x (points) = 16 threads x float4
@@ -308,6 +315,7 @@ template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MI
 __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(const __grid_constant__ StepParams<T> P)
 {
     using C = Cfg<T, R, RZ, TY>;
+    constexpr bool PACKED = VTI_PACKED_F32 && std::is_same<T, float>::value;
     constexpr int NCONS_WARPS = cons_warps(TY, RPT);
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
@@ -420,64 +428,149 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                     const T *ps = st + C::OFF_P / C::ES;
                     // smem row of tile row tg*RPT - R is tg*RPT; x window starts at x0 + 4tx - RA
                     const T *pbase = ps + tg * RPT * C::PW + 4 * tx;
-                    // Eq. 4 / h^2, canonical order: L = c0 p; L = fma(c_l, xpair + ypair, L)
-                    T L[RPT][4];
-                    T pc[RPT][4];   // p^n at the points (2 u^n term)
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r) {
-                        // x window of row r: floats [4tx, 4tx + 4 + 2RA) of smem row r + R, read
-                        // as float4 chunks at the point of use (identical loads are CSE'd), so
-                        // only the chunks of the current radius stay live
-                        const T *prow = pbase + (r + R) * C::PW;
-                        auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            pc[r][c] = wx(RA + c);
-                            L[r][c] = P.cxy[0] * pc[r][c];
-                        }
-#pragma unroll
-                        for (int l = 1; l <= R; ++l) {
-                            // y neighbours of row r at distance l: smem rows r+R+l, r+R-l at x offset RA
-                            const V4<T> yp = lds4(pbase + (r + R + l) * C::PW + RA);
-                            const V4<T> ym = lds4(pbase + (r + R - l) * C::PW + RA);
-#pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                const T xpair = wx(RA + c + l) + wx(RA + c - l);
-                                const T ypair = yp[c] + ym[c];
-                                L[r][c] = fma_rn(P.cxy[l], xpair + ypair, L[r][c]);
-                            }
-                        }
-                    }
-                    // stage data below is read at the point of use (register pressure at
-                    // R_z >= 6); the stage is released after the last shared-memory read
                     const T *zr = st + C::OFF_ZR / C::ES;
                     const T gz = zr[NQ];
                     T pn[RPT][4], qn[RPT][4];
+                    if constexpr (PACKED) {
+                        // fp32: the same canonical operation order, lane for lane, on packed pairs
+                        // (c0,c1), (c2,c3) -- FADD2 / FMUL2 / FFMA2 round each lane exactly like
+                        // the scalar instruction, so results are bitwise those of the scalar form
+                        // with half the FP instructions. Scalar weights are broadcast operands.
+                        float2 L2[RPT][2], pc2[RPT][2];
 #pragma unroll
-                    for (int r = 0; r < RPT; ++r) {
-                        const V4<T> pm4 = lds4(st + C::OFF_PM / C::ES + sidx + r * TX);
-                        const V4<T> qm4 = lds4(st + C::OFF_QM / C::ES + sidx + r * TX);
-                        const V4<T> vx4 = lds4(st + C::OFF_VX / C::ES + sidx + r * TX);
-                        const V4<T> vn4 = lds4(st + C::OFF_VN / C::ES + sidx + r * TX);
-                        const V4<T> vz4 = lds4(st + C::OFF_VZ / C::ES + sidx + r * TX);
-                        const bool src_here = src_col[r] && (k == P.src_k);
+                        for (int r = 0; r < RPT; ++r) {
+                            const float *prow = pbase + (r + R) * C::PW;
+                            // (w[i], w[i+1]) of the x window; i odd straddles two registers pairs
+                            auto wpair = [&](int i) -> float2 {
+                                const V4<float> a4 = lds4(prow + 4 * (i / 4));
+                                if (i % 4 != 3) return make_float2(a4[i % 4], a4[i % 4 + 1]);
+                                return make_float2(a4[3], lds4(prow + 4 * (i / 4 + 1))[0]);
+                            };
+                            const float2 c0 = make_float2(P.cxy[0], P.cxy[0]);
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
-                            T D = zr[0] * q[r][u % NQ][c];
-#pragma unroll
-                            for (int m = 1; m < NQ; ++m) D = fma_rn(zr[m], q[r][(u + m) % NQ][c], D);
-                            const T vD = vz4[c] * D;
-                            T Fp = fma_rn(vx4[c], L[r][c], vD);
-                            T Fq = fma_rn(vn4[c], L[r][c], vD);
-                            if (src_here && c == src_c) {
-                                const T sv = P.s_table ? P.s_table[P.s_index] : P.s;
-                                if (P.src_mask & 1) Fp = Fp + sv;
-                                if (P.src_mask & 2) Fq = Fq + sv;
+                            for (int hp = 0; hp < 2; ++hp) {
+                                pc2[r][hp] = wpair(RA + 2 * hp);
+                                L2[r][hp] = __fmul2_rn(c0, pc2[r][hp]);
                             }
-                            const T g = gxy[r][c] * gz;   // (gx gy) gz
-                            pn[r][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[r][c]));
-                            qn[r][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * q[r][(u + RZ) % NQ][c]));
+#pragma unroll
+                            for (int l = 1; l <= R; ++l) {
+                                const V4<float> yp = lds4(pbase + (r + R + l) * C::PW + RA);
+                                const V4<float> ym = lds4(pbase + (r + R - l) * C::PW + RA);
+                                const float2 cl = make_float2(P.cxy[l], P.cxy[l]);
+#pragma unroll
+                                for (int hp = 0; hp < 2; ++hp) {
+                                    const float2 xpair = __fadd2_rn(wpair(RA + 2 * hp + l), wpair(RA + 2 * hp - l));
+                                    const float2 ypair = __fadd2_rn(make_float2(yp[2 * hp], yp[2 * hp + 1]),
+                                                                    make_float2(ym[2 * hp], ym[2 * hp + 1]));
+                                    L2[r][hp] = __ffma2_rn(cl, __fadd2_rn(xpair, ypair), L2[r][hp]);
+                                }
+                            }
+                        }
+                        const float2 gz2 = make_float2(gz, gz), ngz2 = make_float2(-gz, -gz);
+                        const float2 dt22 = make_float2(P.dt2, P.dt2);
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) {
+                            const V4<float> pm4 = lds4(st + C::OFF_PM / C::ES + sidx + r * TX);
+                            const V4<float> qm4 = lds4(st + C::OFF_QM / C::ES + sidx + r * TX);
+                            const V4<float> vx4 = lds4(st + C::OFF_VX / C::ES + sidx + r * TX);
+                            const V4<float> vn4 = lds4(st + C::OFF_VN / C::ES + sidx + r * TX);
+                            const V4<float> vz4 = lds4(st + C::OFF_VZ / C::ES + sidx + r * TX);
+                            const bool src_here = src_col[r] && (k == P.src_k);
+#pragma unroll
+                            for (int hp = 0; hp < 2; ++hp) {
+                                const int c = 2 * hp;
+                                auto qp = [&](int slot) {
+                                    const V4<float> &qq = q[r][slot];
+                                    return make_float2(qq[c], qq[c + 1]);
+                                };
+                                // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
+                                float2 D = __fmul2_rn(make_float2(zr[0], zr[0]), qp(u % NQ));
+#pragma unroll
+                                for (int m = 1; m < NQ; ++m)
+                                    D = __ffma2_rn(make_float2(zr[m], zr[m]), qp((u + m) % NQ), D);
+                                const float2 vD = __fmul2_rn(make_float2(vz4[c], vz4[c + 1]), D);
+                                float2 Fp = __ffma2_rn(make_float2(vx4[c], vx4[c + 1]), L2[r][hp], vD);
+                                float2 Fq = __ffma2_rn(make_float2(vn4[c], vn4[c + 1]), L2[r][hp], vD);
+                                if (src_here && (src_c >> 1) == hp) {
+                                    const float sv = P.s_table ? P.s_table[P.s_index] : P.s;
+                                    if (src_c & 1) {
+                                        if (P.src_mask & 1) Fp.y = __fadd_rn(Fp.y, sv);
+                                        if (P.src_mask & 2) Fq.y = __fadd_rn(Fq.y, sv);
+                                    } else {
+                                        if (P.src_mask & 1) Fp.x = __fadd_rn(Fp.x, sv);
+                                        if (P.src_mask & 2) Fq.x = __fadd_rn(Fq.x, sv);
+                                    }
+                                }
+                                const float2 gxy2 = make_float2(gxy[r][c], gxy[r][c + 1]);
+                                const float2 g = __fmul2_rn(gxy2, gz2);     // (gx gy) gz
+                                const float2 ng = __fmul2_rn(gxy2, ngz2);   // -g exactly (sign-symmetric RN)
+                                const float2 pc = pc2[r][hp], qc = qp((u + RZ) % NQ);
+                                // 2 u^n as u + u (exact, equal to 2 * u)
+                                const float2 pnv = __fmul2_rn(g, __ffma2_rn(dt22, Fp, __ffma2_rn(ng, make_float2(pm4[c], pm4[c + 1]), __fadd2_rn(pc, pc))));
+                                const float2 qnv = __fmul2_rn(g, __ffma2_rn(dt22, Fq, __ffma2_rn(ng, make_float2(qm4[c], qm4[c + 1]), __fadd2_rn(qc, qc))));
+                                pn[r][c] = pnv.x;
+                                pn[r][c + 1] = pnv.y;
+                                qn[r][c] = qnv.x;
+                                qn[r][c + 1] = qnv.y;
+                            }
+                        }
+                    } else {
+                        // Eq. 4 / h^2, canonical order: L = c0 p; L = fma(c_l, xpair + ypair, L)
+                        T L[RPT][4];
+                        T pc[RPT][4];   // p^n at the points (2 u^n term)
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) {
+                            // x window of row r: floats [4tx, 4tx + 4 + 2RA) of smem row r + R, read
+                            // as float4 chunks at the point of use (identical loads are CSE'd), so
+                            // only the chunks of the current radius stay live
+                            const T *prow = pbase + (r + R) * C::PW;
+                            auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                pc[r][c] = wx(RA + c);
+                                L[r][c] = P.cxy[0] * pc[r][c];
+                            }
+#pragma unroll
+                            for (int l = 1; l <= R; ++l) {
+                                // y neighbours of row r at distance l: smem rows r+R+l, r+R-l at x offset RA
+                                const V4<T> yp = lds4(pbase + (r + R + l) * C::PW + RA);
+                                const V4<T> ym = lds4(pbase + (r + R - l) * C::PW + RA);
+#pragma unroll
+                                for (int c = 0; c < 4; ++c) {
+                                    const T xpair = wx(RA + c + l) + wx(RA + c - l);
+                                    const T ypair = yp[c] + ym[c];
+                                    L[r][c] = fma_rn(P.cxy[l], xpair + ypair, L[r][c]);
+                                }
+                            }
+                        }
+                        // stage data below is read at the point of use (register pressure at
+                        // R_z >= 6); the stage is released after the last shared-memory read
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) {
+                            const V4<T> pm4 = lds4(st + C::OFF_PM / C::ES + sidx + r * TX);
+                            const V4<T> qm4 = lds4(st + C::OFF_QM / C::ES + sidx + r * TX);
+                            const V4<T> vx4 = lds4(st + C::OFF_VX / C::ES + sidx + r * TX);
+                            const V4<T> vn4 = lds4(st + C::OFF_VN / C::ES + sidx + r * TX);
+                            const V4<T> vz4 = lds4(st + C::OFF_VZ / C::ES + sidx + r * TX);
+                            const bool src_here = src_col[r] && (k == P.src_k);
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
+                                T D = zr[0] * q[r][u % NQ][c];
+#pragma unroll
+                                for (int m = 1; m < NQ; ++m) D = fma_rn(zr[m], q[r][(u + m) % NQ][c], D);
+                                const T vD = vz4[c] * D;
+                                T Fp = fma_rn(vx4[c], L[r][c], vD);
+                                T Fq = fma_rn(vn4[c], L[r][c], vD);
+                                if (src_here && c == src_c) {
+                                    const T sv = P.s_table ? P.s_table[P.s_index] : P.s;
+                                    if (P.src_mask & 1) Fp = Fp + sv;
+                                    if (P.src_mask & 2) Fq = Fq + sv;
+                                }
+                                const T g = gxy[r][c] * gz;   // (gx gy) gz
+                                pn[r][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[r][c]));
+                                qn[r][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * q[r][(u + RZ) % NQ][c]));
+                            }
                         }
                     }
                     __syncwarp();
