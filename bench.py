@@ -407,7 +407,8 @@ def run_native(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
-            "schedule": {k: info[k] for k in ("tile_x", "tile_y", "zchunk", "grid", "work_items")},
+            "schedule": {k: info[k] for k in ("tile_x", "tile_y", "producer_warp", "rows_per_thread", "points_per_thread",
+                                              "zchunk", "grid", "work_items")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -47,7 +47,7 @@ class Config(C.Structure):
 
 class TuneResult(C.Structure):
     _fields_ = [("tile_y", C.c_int32), ("producer_warp", C.c_int32), ("rows_per_thread", C.c_int32),
-                ("zchunk", C.c_int32),
+                ("points_per_thread", C.c_int32), ("zchunk", C.c_int32),
                 ("ms_per_step", C.c_float), ("candidates", C.c_int32)]
 
     def as_dict(self):
@@ -67,7 +67,7 @@ class Info(C.Structure):
     _fields_ = [
         ("y0", C.c_int32), ("ny_local", C.c_int32), ("nx_pad", C.c_int32), ("layout", C.c_int32),
         ("tile_x", C.c_int32), ("tile_y", C.c_int32), ("rows_per_thread", C.c_int32), ("producer_warp", C.c_int32),
-        ("zchunk", C.c_int32), ("grid", C.c_int32),
+        ("points_per_thread", C.c_int32), ("zchunk", C.c_int32), ("grid", C.c_int32),
         ("work_items", C.c_int32), ("launches_per_step", C.c_int32),
         ("device_bytes", C.c_int64), ("time_index", C.c_int64),
     ]
@@ -115,7 +115,7 @@ def _load():
         "vti_stream": (C.c_void_p, [H]),
         "vti_query": (st, [H, C.POINTER(Info)]),
         "vti_set_tuning": (st, [H, C.c_int32, C.c_int32]),
-        "vti_set_variant": (st, [H, C.c_int32, C.c_int32, C.c_int32]),
+        "vti_set_variant": (st, [H, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
         "vti_set_receivers": (st, [H, C.c_int32, P, C.c_int32, C.c_int32]),
         "vti_receiver_info": (st, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32), P]),
         "vti_get_traces": (st, [H, P]),
@@ -359,8 +359,8 @@ class VTI:
     def set_tuning(self, zchunk=0, ctas_per_sm=0):
         _check(self.h, lib.vti_set_tuning(self.h, zchunk, ctas_per_sm))
 
-    def set_variant(self, tile_y=-1, producer_warp=-1, rows_per_thread=-1):
-        _check(self.h, lib.vti_set_variant(self.h, tile_y, producer_warp, rows_per_thread))
+    def set_variant(self, tile_y=-1, producer_warp=-1, rows_per_thread=-1, points_per_thread=-1):
+        _check(self.h, lib.vti_set_variant(self.h, tile_y, producer_warp, rows_per_thread, points_per_thread))
 
     def autotune(self, probe_steps=5) -> dict:
         r = TuneResult()

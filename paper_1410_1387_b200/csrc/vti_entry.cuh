@@ -4,14 +4,14 @@
 #include "vti_kernel.cuh"
 #include "vti_variants.h"
 
-template <typename T, int R, int RZ, int TY, int RPT, int WP, int S, int B>
+template <typename T, int R, int RZ, int TY, int RPT, int WP, int S, int B, int PX = 4>
 static KernelEntry entry()
 {
     using namespace vti;
-    return KernelEntry{(int)sizeof(T), R, RZ, TY, RPT, WP, S, B, Cfg<T, R, RZ, TY>::STAGE,
-                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B, false>,
-                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B, true>, Cfg<T, R, RZ, TY>::ZROW,
-                       nthreads(TY, RPT, WP)};
+    return KernelEntry{(int)sizeof(T), R, RZ, TY, RPT, WP, S, B, Cfg<T, R, RZ, TY>::STAGE, PX,
+                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B, false, PX>,
+                       (const void *)vti_step_kernel<T, R, RZ, TY, RPT, WP, S, B, true, PX>, Cfg<T, R, RZ, TY>::ZROW,
+                       nthreads(TY, RPT, WP, PX)};
 }
 
 #define VTI_TABLE(name, ...)                                     \

@@ -41,13 +41,17 @@
 
 namespace vti {
 
-constexpr int TX = 64;               // tile width in x (points) = 16 threads x float4
+constexpr int TX = 64;               // tile width in x (points)
 constexpr int MAX_R = 12;
 
-// Tile height TY (16 or 32 rows), RPT rows per thread (1 or 2): 16 threads per
-// row group, TY / (2 RPT) consumer warps, plus one producer warp when WP = 1.
-__host__ __device__ constexpr int cons_warps(int ty, int rpt) { return ty / (2 * rpt); }
-__host__ __device__ constexpr int nthreads(int ty, int rpt, int wp) { return (cons_warps(ty, rpt) + wp) * 32; }
+// Tile height TY, RPT rows per thread (1 or 2), PX consecutive x points per
+// thread (4: one float4 / two double2; 2: one double2): TX / PX threads per row
+// group, TY * (TX / PX) / (32 RPT) consumer warps, plus one producer warp when WP = 1.
+__host__ __device__ constexpr int cons_warps(int ty, int rpt, int px) { return ty * (TX / px) / (32 * rpt); }
+__host__ __device__ constexpr int nthreads(int ty, int rpt, int wp, int px)
+{
+    return (cons_warps(ty, rpt, px) + wp) * 32;
+}
 
 __host__ __device__ constexpr int align128(int b) { return (b + 127) / 128 * 128; }
 
@@ -194,35 +198,53 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
 }
 
-// 4 consecutive elements: one float4, or two double2 (32 B) for fp64.
-template <typename T> struct V4;
-template <> struct V4<float> {
+// N consecutive elements held in 16-byte vectors: float4 (float, 4), two double2
+// (double, 4) or one double2 (double, 2).
+template <typename T, int N> struct Vec;
+template <> struct Vec<float, 4> {
     float4 v;
     __device__ __forceinline__ float operator[](int c) const { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
 };
-template <> struct V4<double> {
+template <> struct Vec<double, 4> {
     double2 a, b;
     __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : c == 1 ? a.y : c == 2 ? b.x : b.y; }
 };
+template <> struct Vec<double, 2> {
+    double2 a;
+    __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : a.y; }
+};
+template <typename T> using V4 = Vec<T, 4>;
 
-__device__ __forceinline__ V4<float> lds4(const float *p) { return V4<float>{*reinterpret_cast<const float4 *>(p)}; }
-__device__ __forceinline__ V4<double> lds4(const double *p)
+// loads of N elements (16-byte aligned), shared or global memory (generic addressing)
+template <int N> __device__ __forceinline__ Vec<float, N> ldv(const float *p);
+template <> __device__ __forceinline__ Vec<float, 4> ldv<4>(const float *p)
 {
-    return V4<double>{reinterpret_cast<const double2 *>(p)[0], reinterpret_cast<const double2 *>(p)[1]};
+    return Vec<float, 4>{*reinterpret_cast<const float4 *>(p)};
 }
-__device__ __forceinline__ V4<float> ldg4(const float *p) { return V4<float>{*reinterpret_cast<const float4 *>(p)}; }
-__device__ __forceinline__ V4<double> ldg4(const double *p)
+template <int N> __device__ __forceinline__ Vec<double, N> ldv(const double *p);
+template <> __device__ __forceinline__ Vec<double, 4> ldv<4>(const double *p)
 {
-    return V4<double>{reinterpret_cast<const double2 *>(p)[0], reinterpret_cast<const double2 *>(p)[1]};
+    return Vec<double, 4>{reinterpret_cast<const double2 *>(p)[0], reinterpret_cast<const double2 *>(p)[1]};
 }
-__device__ __forceinline__ void stg4(float *p, const float (&v)[4])
+template <> __device__ __forceinline__ Vec<double, 2> ldv<2>(const double *p)
+{
+    return Vec<double, 2>{*reinterpret_cast<const double2 *>(p)};
+}
+__device__ __forceinline__ V4<float> lds4(const float *p) { return ldv<4>(p); }
+__device__ __forceinline__ V4<double> lds4(const double *p) { return ldv<4>(p); }
+
+__device__ __forceinline__ void stv(float *p, const float (&v)[4])
 {
     *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
-__device__ __forceinline__ void stg4(double *p, const double (&v)[4])
+__device__ __forceinline__ void stv(double *p, const double (&v)[4])
 {
     reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
     reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ void stv(double *p, const double (&v)[2])
+{
+    *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
 }
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
@@ -311,15 +333,20 @@ struct Producer {
 // PEER: also store the boundary rows into the neighbours' halo rows (StepParams::peer_*);
 // only the edge launch of a peer-connected slab uses it, so the other launches keep
 // the register allocation of the plain kernel.
-template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB, bool PEER>
-__global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(const __grid_constant__ StepParams<T> P)
+template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB, bool PEER, int PX>
+__global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
+    vti_step_kernel(const __grid_constant__ StepParams<T> P)
 {
     using C = Cfg<T, R, RZ, TY>;
-    constexpr bool PACKED = VTI_PACKED_F32 && std::is_same<T, float>::value;
-    constexpr int NCONS_WARPS = cons_warps(TY, RPT);
+    using VP = Vec<T, PX>;
+    constexpr bool PACKED = VTI_PACKED_F32 && std::is_same<T, float>::value && PX == 4;
+    constexpr int NCONS_WARPS = cons_warps(TY, RPT, PX);
+    constexpr int TPR = TX / PX;   // threads per tile row
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
-    static_assert(TY % (2 * RPT) == 0, "tile rows must split into 16-thread row groups");
+    static_assert(PX == 4 || (PX == 2 && sizeof(T) == 8), "PX = 2 is the fp64 (double2) mapping");
+    static_assert((TY * TPR) % (32 * RPT) == 0, "tile rows must split into whole warps");
+    static_assert(RA % PX == 0, "x apron must be whole vectors");
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE);
     uint64_t *empty = full + STAGES;
@@ -360,9 +387,9 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
         }
     }
 
-    // ======================= all warps consume: 16 x (TY / RPT) threads, 4 x RPT points each =======================
-    const int tx = threadIdx.x & 15;
-    const int tg = threadIdx.x >> 4;   // row group: tile rows tg*RPT .. tg*RPT + RPT - 1
+    // =============== all warps consume: TPR x (TY / RPT) threads, PX x RPT points each ===============
+    const int tx = threadIdx.x % TPR;
+    const int tg = threadIdx.x / TPR;   // row group: tile rows tg*RPT .. tg*RPT + RPT - 1
     int stage = 0;
     uint32_t phase = 0;
 
@@ -379,9 +406,9 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
         }
         int x0, y0, kb, ke;
         decode_item<TY>(P, item, x0, y0, kb, ke);
-        const int xg = x0 + 4 * tx;   // first of this thread's 4 columns
-        const V4<T> g4 = ldg4(P.gx + xg);
-        T gxy[RPT][4];
+        const int xg = x0 + PX * tx;   // first of this thread's PX columns
+        const VP g4 = ldv<PX>(P.gx + xg);
+        T gxy[RPT][PX];
         bool store_ok[RPT], src_col[RPT];
         T *pout[RPT], *qout[RPT];
 #pragma unroll
@@ -389,23 +416,23 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
             const int yl = y0 + tg * RPT + r;   // local row
             const T gyv = (yl < P.nyl) ? P.gy[yl] : T(0);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) gxy[r][c] = g4[c] * gyv;
+            for (int c = 0; c < PX; ++c) gxy[r][c] = g4[c] * gyv;
             store_ok[r] = (yl < P.nyl) && (xg < P.nx);
-            src_col[r] = P.src_mask != 0 && P.src_j == yl && P.src_i >= xg && P.src_i < xg + 4;
+            src_col[r] = P.src_mask != 0 && P.src_j == yl && P.src_i >= xg && P.src_i < xg + PX;
             pout[r] = P.p_out + (long long)yl * P.ys + xg;
             qout[r] = P.q_out + (long long)yl * P.ys + xg;
         }
         const int src_c = P.src_i - xg;
-        const int sidx = tg * RPT * TX + 4 * tx;   // float offset of row 0 in a stream tile
+        const int sidx = tg * RPT * TX + PX * tx;   // element offset of row 0 in a stream tile
 
-        V4<T> q[RPT][NQ];
+        VP q[RPT][NQ];
         // prime the queue with q(kb - Rz .. kb + Rz - 1)
 #pragma unroll
         for (int t = 0; t < 2 * RZ; ++t) {
             mbar_wait(&full[stage], phase);
             const T *st = reinterpret_cast<const T *>(smem + stage * C::STAGE);
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) q[r][t] = lds4(st + C::OFF_Q / C::ES + sidx + r * TX);
+            for (int r = 0; r < RPT; ++r) q[r][t] = ldv<PX>(st + C::OFF_Q / C::ES + sidx + r * TX);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (leader) prod.issue(P, smem, full, empty);
@@ -424,13 +451,13 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                     const T *st = reinterpret_cast<const T *>(smem + stage * C::STAGE);
 #pragma unroll
                     for (int r = 0; r < RPT; ++r)
-                        q[r][(u + 2 * RZ) % NQ] = lds4(st + C::OFF_Q / C::ES + sidx + r * TX);   // q^n(k + Rz)
+                        q[r][(u + 2 * RZ) % NQ] = ldv<PX>(st + C::OFF_Q / C::ES + sidx + r * TX);   // q^n(k + Rz)
                     const T *ps = st + C::OFF_P / C::ES;
                     // smem row of tile row tg*RPT - R is tg*RPT; x window starts at x0 + 4tx - RA
-                    const T *pbase = ps + tg * RPT * C::PW + 4 * tx;
+                    const T *pbase = ps + tg * RPT * C::PW + PX * tx;
                     const T *zr = st + C::OFF_ZR / C::ES;
                     const T gz = zr[NQ];
-                    T pn[RPT][4], qn[RPT][4];
+                    T pn[RPT][PX], qn[RPT][PX];
                     if constexpr (PACKED) {
                         // fp32: the same canonical operation order, lane for lane, on packed pairs
                         // (c0,c1), (c2,c3) -- FADD2 / FMUL2 / FFMA2 round each lane exactly like
@@ -516,27 +543,27 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                         }
                     } else {
                         // Eq. 4 / h^2, canonical order: L = c0 p; L = fma(c_l, xpair + ypair, L)
-                        T L[RPT][4];
-                        T pc[RPT][4];   // p^n at the points (2 u^n term)
+                        T L[RPT][PX];
+                        T pc[RPT][PX];   // p^n at the points (2 u^n term)
 #pragma unroll
                         for (int r = 0; r < RPT; ++r) {
-                            // x window of row r: floats [4tx, 4tx + 4 + 2RA) of smem row r + R, read
-                            // as float4 chunks at the point of use (identical loads are CSE'd), so
+                            // x window of row r: elements [PX tx, PX tx + PX + 2RA) of smem row r + R, read
+                            // as PX-vectors at the point of use (identical loads are CSE'd), so
                             // only the chunks of the current radius stay live
                             const T *prow = pbase + (r + R) * C::PW;
-                            auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
+                            auto wx = [&](int i) { return ldv<PX>(prow + PX * (i / PX))[i % PX]; };
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) {
+                            for (int c = 0; c < PX; ++c) {
                                 pc[r][c] = wx(RA + c);
                                 L[r][c] = P.cxy[0] * pc[r][c];
                             }
 #pragma unroll
                             for (int l = 1; l <= R; ++l) {
                                 // y neighbours of row r at distance l: smem rows r+R+l, r+R-l at x offset RA
-                                const V4<T> yp = lds4(pbase + (r + R + l) * C::PW + RA);
-                                const V4<T> ym = lds4(pbase + (r + R - l) * C::PW + RA);
+                                const VP yp = ldv<PX>(pbase + (r + R + l) * C::PW + RA);
+                                const VP ym = ldv<PX>(pbase + (r + R - l) * C::PW + RA);
 #pragma unroll
-                                for (int c = 0; c < 4; ++c) {
+                                for (int c = 0; c < PX; ++c) {
                                     const T xpair = wx(RA + c + l) + wx(RA + c - l);
                                     const T ypair = yp[c] + ym[c];
                                     L[r][c] = fma_rn(P.cxy[l], xpair + ypair, L[r][c]);
@@ -547,14 +574,14 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                         // R_z >= 6); the stage is released after the last shared-memory read
 #pragma unroll
                         for (int r = 0; r < RPT; ++r) {
-                            const V4<T> pm4 = lds4(st + C::OFF_PM / C::ES + sidx + r * TX);
-                            const V4<T> qm4 = lds4(st + C::OFF_QM / C::ES + sidx + r * TX);
-                            const V4<T> vx4 = lds4(st + C::OFF_VX / C::ES + sidx + r * TX);
-                            const V4<T> vn4 = lds4(st + C::OFF_VN / C::ES + sidx + r * TX);
-                            const V4<T> vz4 = lds4(st + C::OFF_VZ / C::ES + sidx + r * TX);
+                            const VP pm4 = ldv<PX>(st + C::OFF_PM / C::ES + sidx + r * TX);
+                            const VP qm4 = ldv<PX>(st + C::OFF_QM / C::ES + sidx + r * TX);
+                            const VP vx4 = ldv<PX>(st + C::OFF_VX / C::ES + sidx + r * TX);
+                            const VP vn4 = ldv<PX>(st + C::OFF_VN / C::ES + sidx + r * TX);
+                            const VP vz4 = ldv<PX>(st + C::OFF_VZ / C::ES + sidx + r * TX);
                             const bool src_here = src_col[r] && (k == P.src_k);
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) {
+                            for (int c = 0; c < PX; ++c) {
                                 // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
                                 T D = zr[0] * q[r][u % NQ][c];
 #pragma unroll
@@ -584,16 +611,16 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP), MINB) vti_step_kernel(c
                     for (int r = 0; r < RPT; ++r) {
                         if (store_ok[r]) {
                             const long long off = (long long)k * P.zs;
-                            stg4(pout[r] + off, pn[r]);
-                            stg4(qout[r] + off, qn[r]);
+                            stv(pout[r] + off, pn[r]);
+                            stv(qout[r] + off, qn[r]);
                             if constexpr (PEER) {
                                 // the neighbours' halo rows, straight over NVLink (edge tile rows
                                 // only; a row goes to both sides when nyl < 2R)
                                 const int yl = y0 + tg * RPT + r;
                                 if (P.peer_lo != nullptr && yl < R)
-                                    stg4(P.peer_lo + (long long)k * P.peer_zs_lo + (long long)yl * P.ys + xg, pn[r]);
+                                    stv(P.peer_lo + (long long)k * P.peer_zs_lo + (long long)yl * P.ys + xg, pn[r]);
                                 if (P.peer_hi != nullptr && yl >= P.nyl - R)
-                                    stg4(P.peer_hi + (long long)k * P.peer_zs_hi +
+                                    stv(P.peer_hi + (long long)k * P.peer_zs_hi +
                                              (long long)(yl - (P.nyl - R)) * P.ys + xg,
                                          pn[r]);
                             }

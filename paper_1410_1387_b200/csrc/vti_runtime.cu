@@ -132,8 +132,8 @@ static const StreamMemOps &stream_mem_ops()
 // ============================================================ kernel table
 // Compiled variants live in csrc/variants/*.cu (see vti_variants.h); the first
 // match is the default for (precision, radius pair). -1 = any (env VTI_TY,
-// VTI_WP, VTI_RPT or vti_set_variant select the others).
-static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, int rpt = -1)
+// VTI_WP, VTI_RPT, VTI_PX or vti_set_variant select the others).
+static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, int rpt = -1, int px = -1)
 {
     static const VariantTable tables[] = {vti_variants_f32_r4(),  vti_variants_f32_r8(),  vti_variants_f32_r6(),
                                           vti_variants_f32_r12(), vti_variants_f64_r48(), vti_variants_f64_r6(),
@@ -142,7 +142,7 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, 
         for (int i = 0; i < t.n; ++i) {
             const KernelEntry &e = t.e[i];
             if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp) &&
-                (rpt < 0 || e.rpt == rpt))
+                (rpt < 0 || e.rpt == rpt) && (px < 0 || e.px == px))
                 return &e;
         }
     return nullptr;
@@ -152,10 +152,11 @@ static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
     const KernelEntry *e;
-    for (int ty : {32, 30, 16, 14})
+    for (int ty : {32, 30, 16, 15, 14})
         for (int wp : {1, 0})
             for (int rpt : {1, 2})
-                if ((e = find_kernel(esize, r, rz, ty, wp, rpt)) != nullptr) v.push_back(e);
+                for (int px : {4, 2})
+                    if ((e = find_kernel(esize, r, rz, ty, wp, rpt, px)) != nullptr) v.push_back(e);
     return v;
 }
 
@@ -769,11 +770,12 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     h->es = precision_bits(cfg) / 8;
     h->R = cfg->r_xy;
     h->RZ = cfg->r_z;
-    int want_ty = -1, want_wp = -1, want_rpt = -1;
+    int want_ty = -1, want_wp = -1, want_rpt = -1, want_px = -1;
     if (const char *e = getenv("VTI_TY")) want_ty = atoi(e);
     if (const char *e = getenv("VTI_WP")) want_wp = atoi(e);
     if (const char *e = getenv("VTI_RPT")) want_rpt = atoi(e);
-    h->K = find_kernel(h->es, h->R, h->RZ, want_ty, want_wp, want_rpt);
+    if (const char *e = getenv("VTI_PX")) want_px = atoi(e);
+    h->K = find_kernel(h->es, h->R, h->RZ, want_ty, want_wp, want_rpt, want_px);
     if (!h->K) h->K = find_kernel(h->es, h->R, h->RZ, -1, -1);
     if (!h->K)
         return fail(h, VTI_E_UNSUPPORTED, "(r_xy, r_z) = (%d, %d) not compiled for fp%d", h->R, h->RZ, 8 * h->es);
@@ -1872,6 +1874,7 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->tile_y = h->TY;
     info->rows_per_thread = h->K->rpt;
     info->producer_warp = h->K->wp;
+    info->points_per_thread = h->K->px;
     info->zchunk = h->zchunk;
     info->grid = std::min(h->ntx * h->nty * h->nzc, h->sms * h->ctas_per_sm);
     info->work_items = h->ntx * h->nty * h->nzc;
@@ -1898,13 +1901,15 @@ vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm)
     return select_variant(h, h->K);
 }
 
-vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp, int32_t rows_per_thread)
+vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp, int32_t rows_per_thread,
+                           int32_t points_per_thread)
 {
     if (!h) return VTI_E_PARAM;
-    const KernelEntry *K = find_kernel(h->es, h->R, h->RZ, tile_y, producer_warp, rows_per_thread);
+    const KernelEntry *K = find_kernel(h->es, h->R, h->RZ, tile_y, producer_warp, rows_per_thread, points_per_thread);
     if (!K)
-        return fail(h, VTI_E_UNSUPPORTED, "no compiled variant (fp%d, r_xy %d, r_z %d, tile_y %d, producer_warp %d, rpt %d)",
-                    8 * h->es, h->R, h->RZ, tile_y, producer_warp, rows_per_thread);
+        return fail(h, VTI_E_UNSUPPORTED,
+                    "no compiled variant (fp%d, r_xy %d, r_z %d, tile_y %d, producer_warp %d, rpt %d, px %d)", 8 * h->es,
+                    h->R, h->RZ, tile_y, producer_warp, rows_per_thread, points_per_thread);
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaStreamSynchronize(h->stream));
     return select_variant(h, K);
@@ -1959,6 +1964,7 @@ vti_status vti_autotune(vti_t h, int32_t probe_steps, vti_tune_result *out)
         out->tile_y = h->K->ty;
         out->producer_warp = h->K->wp;
         out->rows_per_thread = h->K->rpt;
+        out->points_per_thread = h->K->px;
         out->zchunk = h->zchunk;
         out->ms_per_step = best_ms / probe_steps;
         out->candidates = ncand;

@@ -9,6 +9,7 @@
 
 struct KernelEntry {
     int esize, r, rz, ty, rpt, wp, stages, minb, stage_bytes;
+    int px;                // points per thread along x (4, or 2 for the fp64 double2 mapping)
     const void *fn;        // host stub of the instantiation (cudaLaunchKernelExC with a StepParams<T> argument)
     const void *fn_peer;   // the same with the fused peer-halo stores (edge launches of peer-connected slabs)
     int zrow;

@@ -66,16 +66,16 @@ def check(g, o):
 
 
 @pytest.mark.parametrize("r,rz", [(4, 4), (8, 4), (6, 6), (12, 8)])
-@pytest.mark.parametrize("ty,wp", [(16, 1), (16, 0), (14, 1)])
-def test_fp64_random_state_ragged(r, rz, ty, wp):
+@pytest.mark.parametrize("ty,wp,px", [(16, 1, 4), (16, 0, 4), (14, 1, 4), (15, 1, 2), (16, 0, 2), (16, 1, 2)])
+def test_fp64_random_state_ragged(r, rz, ty, wp, px):
     from paper_1410_1387_b200 import VTIError
     cfg = cfg_of(77, 45, 41, r, rz, src=(30, 22, 20))
     model, st = inputs(cfg)
     try:
-        g, o = run64(cfg, 4, st, model, variant=(ty, wp, 1))
+        g, o = run64(cfg, 4, st, model, variant=(ty, wp, 1, px))
     except VTIError as e:
         assert e.name == "VTI_E_UNSUPPORTED"
-        pytest.skip(f"variant ({ty}, {wp}) not compiled for ({r}, {rz})")
+        pytest.skip(f"variant ({ty}, {wp}, px {px}) not compiled for ({r}, {rz})")
     check(g, o)
 
 

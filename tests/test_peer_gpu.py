@@ -26,14 +26,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def compiled_variants():
-    """(precision, r, rz, ty, wp, rpt) of every entry<...> in csrc/variants/*.cu."""
+    """(precision, r, rz, ty, wp, rpt, px) of every entry<...> in csrc/variants/*.cu."""
     out = []
     d = os.path.join(ROOT, "paper_1410_1387_b200", "csrc", "variants")
     for f in sorted(os.listdir(d)):
         if f.endswith(".cu"):
-            for m in re.finditer(r"entry<(float|double),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),", open(os.path.join(d, f)).read()):
-                t, r, rz, ty, rpt, wp = m.groups()
-                out.append((32 if t == "float" else 64, int(r), int(rz), int(ty), int(wp), int(rpt)))
+            src = open(os.path.join(d, f)).read()
+            pat = r"entry<(float|double),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*\d+,\s*\d+(?:,\s*(\d+))?>"
+            for m in re.finditer(pat, src):
+                t, r, rz, ty, rpt, wp, px = m.groups()
+                out.append((32 if t == "float" else 64, int(r), int(rz), int(ty), int(wp), int(rpt), int(px or 4)))
     return out
 
 
@@ -78,8 +80,8 @@ def f64_inputs(cfg, seed=7):
     return wxy, wz, synth.stable_dt(cfg), tuple(model), st
 
 
-@pytest.mark.parametrize("prec,r,rz,ty,wp,rpt", compiled_variants())
-def test_every_peer_instantiation(prec, r, rz, ty, wp, rpt):
+@pytest.mark.parametrize("prec,r,rz,ty,wp,rpt,px", compiled_variants())
+def test_every_peer_instantiation(prec, r, rz, ty, wp, rpt, px):
     """3 slabs (source on a slab boundary, interior tile rows present) in every compiled
     variant: the PEER edge instantiation and the plain interior one, bitwise == oracle."""
     ny = 3 * max(2 * ty + 2 * r, 40)
@@ -88,9 +90,10 @@ def test_every_peer_instantiation(prec, r, rz, ty, wp, rpt):
     wxy, wz, dt, model, st = (f64_inputs if prec == 64 else f32_inputs)(cfg)
     hs = handles(cfg, dt, wxy, wz, 3, prec)
     for h in hs:
-        h.set_variant(ty, wp, rpt)
+        h.set_variant(ty, wp, rpt, px)
         info = h.info()
-        assert (info["tile_y"], info["producer_warp"], info["rows_per_thread"]) == (ty, wp, rpt)
+        assert (info["tile_y"], info["producer_warp"], info["rows_per_thread"], info["points_per_thread"]) == \
+            (ty, wp, rpt, px)
     load(hs, model, st, 2, cfg)
     from paper_1410_1387_b200 import group_step
     group_step(hs, 5)
