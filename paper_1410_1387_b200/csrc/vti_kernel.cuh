@@ -205,6 +205,10 @@ template <> struct Vec<float, 4> {
     float4 v;
     __device__ __forceinline__ float operator[](int c) const { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }
 };
+template <> struct Vec<float, 2> {
+    float2 v;
+    __device__ __forceinline__ float operator[](int c) const { return c == 0 ? v.x : v.y; }
+};
 template <> struct Vec<double, 4> {
     double2 a, b;
     __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : c == 1 ? a.y : c == 2 ? b.x : b.y; }
@@ -220,6 +224,10 @@ template <int N> __device__ __forceinline__ Vec<float, N> ldv(const float *p);
 template <> __device__ __forceinline__ Vec<float, 4> ldv<4>(const float *p)
 {
     return Vec<float, 4>{*reinterpret_cast<const float4 *>(p)};
+}
+template <> __device__ __forceinline__ Vec<float, 2> ldv<2>(const float *p)
+{
+    return Vec<float, 2>{*reinterpret_cast<const float2 *>(p)};
 }
 template <int N> __device__ __forceinline__ Vec<double, N> ldv(const double *p);
 template <> __device__ __forceinline__ Vec<double, 4> ldv<4>(const double *p)
@@ -237,6 +245,7 @@ __device__ __forceinline__ void stv(float *p, const float (&v)[4])
 {
     *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
+__device__ __forceinline__ void stv(float *p, const float (&v)[2]) { *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]); }
 __device__ __forceinline__ void stv(double *p, const double (&v)[4])
 {
     reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
@@ -339,12 +348,12 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
 {
     using C = Cfg<T, R, RZ, TY>;
     using VP = Vec<T, PX>;
-    constexpr bool PACKED = VTI_PACKED_F32 && std::is_same<T, float>::value && PX == 4;
+    constexpr bool PACKED = VTI_PACKED_F32 && std::is_same<T, float>::value;
     constexpr int NCONS_WARPS = cons_warps(TY, RPT, PX);
     constexpr int TPR = TX / PX;   // threads per tile row
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
-    static_assert(PX == 4 || (PX == 2 && sizeof(T) == 8), "PX = 2 is the fp64 (double2) mapping");
+    static_assert(PX == 4 || PX == 2, "4 or 2 x points per thread");
     static_assert((TY * TPR) % (32 * RPT) == 0, "tile rows must split into whole warps");
     static_assert(RA % PX == 0, "x apron must be whole vectors");
     extern __shared__ __align__(128) uint8_t smem[];
@@ -463,29 +472,30 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
                         // (c0,c1), (c2,c3) -- FADD2 / FMUL2 / FFMA2 round each lane exactly like
                         // the scalar instruction, so results are bitwise those of the scalar form
                         // with half the FP instructions. Scalar weights are broadcast operands.
-                        float2 L2[RPT][2], pc2[RPT][2];
+                        constexpr int NPAIR = PX / 2;
+                        float2 L2[RPT][NPAIR], pc2[RPT][NPAIR];
 #pragma unroll
                         for (int r = 0; r < RPT; ++r) {
                             const float *prow = pbase + (r + R) * C::PW;
-                            // (w[i], w[i+1]) of the x window; i odd straddles two registers pairs
+                            // (w[i], w[i+1]) of the x window; i odd straddles two register pairs
                             auto wpair = [&](int i) -> float2 {
-                                const V4<float> a4 = lds4(prow + 4 * (i / 4));
-                                if (i % 4 != 3) return make_float2(a4[i % 4], a4[i % 4 + 1]);
-                                return make_float2(a4[3], lds4(prow + 4 * (i / 4 + 1))[0]);
+                                const Vec<float, PX> a4 = ldv<PX>(prow + PX * (i / PX));
+                                if (i % PX != PX - 1) return make_float2(a4[i % PX], a4[i % PX + 1]);
+                                return make_float2(a4[PX - 1], ldv<PX>(prow + PX * (i / PX + 1))[0]);
                             };
                             const float2 c0 = make_float2(P.cxy[0], P.cxy[0]);
 #pragma unroll
-                            for (int hp = 0; hp < 2; ++hp) {
+                            for (int hp = 0; hp < NPAIR; ++hp) {
                                 pc2[r][hp] = wpair(RA + 2 * hp);
                                 L2[r][hp] = __fmul2_rn(c0, pc2[r][hp]);
                             }
 #pragma unroll
                             for (int l = 1; l <= R; ++l) {
-                                const V4<float> yp = lds4(pbase + (r + R + l) * C::PW + RA);
-                                const V4<float> ym = lds4(pbase + (r + R - l) * C::PW + RA);
+                                const Vec<float, PX> yp = ldv<PX>(pbase + (r + R + l) * C::PW + RA);
+                                const Vec<float, PX> ym = ldv<PX>(pbase + (r + R - l) * C::PW + RA);
                                 const float2 cl = make_float2(P.cxy[l], P.cxy[l]);
 #pragma unroll
-                                for (int hp = 0; hp < 2; ++hp) {
+                                for (int hp = 0; hp < NPAIR; ++hp) {
                                     const float2 xpair = __fadd2_rn(wpair(RA + 2 * hp + l), wpair(RA + 2 * hp - l));
                                     const float2 ypair = __fadd2_rn(make_float2(yp[2 * hp], yp[2 * hp + 1]),
                                                                     make_float2(ym[2 * hp], ym[2 * hp + 1]));
@@ -497,17 +507,17 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
                         const float2 dt22 = make_float2(P.dt2, P.dt2);
 #pragma unroll
                         for (int r = 0; r < RPT; ++r) {
-                            const V4<float> pm4 = lds4(st + C::OFF_PM / C::ES + sidx + r * TX);
-                            const V4<float> qm4 = lds4(st + C::OFF_QM / C::ES + sidx + r * TX);
-                            const V4<float> vx4 = lds4(st + C::OFF_VX / C::ES + sidx + r * TX);
-                            const V4<float> vn4 = lds4(st + C::OFF_VN / C::ES + sidx + r * TX);
-                            const V4<float> vz4 = lds4(st + C::OFF_VZ / C::ES + sidx + r * TX);
+                            const VP pm4 = ldv<PX>(st + C::OFF_PM / C::ES + sidx + r * TX);
+                            const VP qm4 = ldv<PX>(st + C::OFF_QM / C::ES + sidx + r * TX);
+                            const VP vx4 = ldv<PX>(st + C::OFF_VX / C::ES + sidx + r * TX);
+                            const VP vn4 = ldv<PX>(st + C::OFF_VN / C::ES + sidx + r * TX);
+                            const VP vz4 = ldv<PX>(st + C::OFF_VZ / C::ES + sidx + r * TX);
                             const bool src_here = src_col[r] && (k == P.src_k);
 #pragma unroll
-                            for (int hp = 0; hp < 2; ++hp) {
+                            for (int hp = 0; hp < NPAIR; ++hp) {
                                 const int c = 2 * hp;
                                 auto qp = [&](int slot) {
-                                    const V4<float> &qq = q[r][slot];
+                                    const VP &qq = q[r][slot];
                                     return make_float2(qq[c], qq[c + 1]);
                                 };
                                 // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)

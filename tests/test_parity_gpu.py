@@ -263,13 +263,15 @@ def test_local_group_slabs_bitwise_equal_single(nranks):
 
 
 @pytest.mark.parametrize("r,rz", [(4, 4), (8, 4), (6, 6), (12, 8)])
-@pytest.mark.parametrize("ty,wp,rpt", [(32, 1, 1), (32, 0, 1), (32, 0, 2), (16, -1, 1)])
-def test_every_compiled_variant(r, rz, ty, wp, rpt, monkeypatch):
-    """Each (tile height, producer-warp, rows-per-thread) instantiation is bitwise equal to the oracle
-    (a combination not compiled for the pair falls back to the default, also checked)."""
+@pytest.mark.parametrize("ty,wp,rpt,px", [(32, 1, 1, 4), (32, 0, 1, 4), (32, 0, 2, 4), (16, -1, 1, 4),
+                                         (30, 1, 2, 2), (32, 1, 2, 2)])
+def test_every_compiled_variant(r, rz, ty, wp, rpt, px, monkeypatch):
+    """Each (tile height, producer-warp, rows-per-thread, points-per-thread) instantiation is bitwise
+    equal to the oracle (a combination not compiled for the pair falls back to the default, also checked)."""
     monkeypatch.setenv("VTI_TY", str(ty))
     monkeypatch.setenv("VTI_WP", str(wp))
     monkeypatch.setenv("VTI_RPT", str(rpt))
+    monkeypatch.setenv("VTI_PX", str(px))
     cfg = small_cfg(77, 45, 41, r, rz, damp=5, src=(30, 22, 20))
     st = random_state(cfg, seed=9)
     g, o = run_both(cfg, 4, state=st, model=random_model(cfg, seed=5), n0=2)
