@@ -147,12 +147,12 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(cfg):
+def ncu_traffic(cfg, precision=32):
     """dram bytes per launch from the committed ncu --set full summary, if one matches this workload."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         d = json.load(open(p))
-        e = d.get(cfg["name"])
+        e = d.get(cfg["name"] if precision == 32 else cfg["name"] + "_f64")
         if e and e.get("grid") == [cfg["nx"], cfg["ny"], cfg["nz"]]:
             return e.get("dram_bytes_per_launch")
     except (OSError, ValueError):
@@ -348,7 +348,7 @@ def run_native(args):
     kern_ms = ms / args.steps
     achieved = bpp * pts_rank / (kern_ms * 1e-3) / 1e9
     peak, peak_src = peak_hbm()
-    traffic = ncu_traffic(cfg) if world == 1 and prec == 32 else None
+    traffic = ncu_traffic(cfg, prec) if world == 1 else None
     v.close()
 
     e2e = None

@@ -1,16 +1,17 @@
 # round profile pass: every ncu command line first exits 0 without ncu; reports are
-# exported to CSV on the box (raw + details pages) and only the C2 fp32 .ncu-rep is kept
+# exported to CSV on the box (raw + details pages) and the .ncu-rep files are dropped
+# (gpurun_out/ is capped at 64 MiB)
 set -u
 out=gpurun_out
 B="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline"
 $B > $out/plain_l.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"vti|k_" -c 200 --csv --log-file $out/launches_C2.csv $B > $out/ncu_l.log 2>&1; echo "launches rc=$?"
-for spec in "C2 32" "C3 32" "C4 32" "C5 32" "N1 32" "C2 64"; do
+for spec in "C2 32" "C3 32" "C4 32" "C5 32" "N1 32" "C2 64" "C3 64" "C5 64" "N1 64"; do
   set -- $spec
   B="python bench.py --config $1 --precision $2 --steps 4 --warmup 3 --no-e2e --no-cpu-baseline"
   rep=$out/prof_$1_f$2
   $B > $out/plain_$1_$2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:vti_step_kernel -s 3 -c 1 -o $rep $B > $out/ncu_$1_$2.log 2>&1; echo "ncu $1 f$2 rc=$?"
   ncu -i $rep.ncu-rep --page raw --csv > ${rep}_raw.csv 2>/dev/null
   ncu -i $rep.ncu-rep --page details --csv > ${rep}_details.csv 2>/dev/null
-  if [ "$1$2" != "C232" ]; then rm -f $rep.ncu-rep; fi
+  rm -f $rep.ncu-rep
 done
 du -sh $out
