@@ -1,0 +1,56 @@
+"""The bench.py JSON-line contract the driver reads (task contract).
+
+CPU: the reference arm (`--impl reference`, the oracle on host cores) on the small
+C1 workload. GPU: the native arm on C1 with e2e and cpu_baseline, checking every key
+the contract names -- roofline, cpu_baseline, e2e, clocks, gpu_launches.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config"}
+
+
+def run_bench(*args, timeout=600):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT, capture_output=True,
+                         text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = run_bench("--impl", "reference", "--config", "C1", "--steps", "2", "--warmup", "3")
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 1
+    assert d["steps"] == 2 and d["warmup"] == 3
+    assert d["config"]["workload"].startswith("C1")
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["metric"] == json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+
+
+@pytest.mark.gpu
+def test_native_arm_line():
+    d = run_bench("--config", "C1", "--steps", "40", "--warmup", "3")
+    assert BASE_KEYS <= set(d)
+    assert d["metric"] == json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 40 and d["warmup"] == 3
+    assert d["dtype"] == "f32" and d["higher_is_better"] is True
+    assert abs(d["ms_per_step"] - 64 ** 3 / (d["value"] * 1e9) * 1e3) < 1e-3 * d["ms_per_step"] + 1e-6
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+    assert d["gpu_launches"] >= 40
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
