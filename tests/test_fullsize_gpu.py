@@ -1,9 +1,10 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times
 (default schedule of a fresh handle).
 
-* C2 512^3 (R 4/4) and C3 1024x1024x512 (R 8/4), C5 1024^3 (R 6/6): the whole
-  grid against the full-grid oracle, from seeded random states (every point
-  non-trivial) and, for C2, from the bench's own start (zero state + source).
+* C2 512^3 (R 4/4) and C3 1024x1024x512 (R 8/4), C5 1024^3 (R 6/6), N1 512^3
+  (R 12/8, the float2 x 2-row default): the whole grid against the full-grid
+  oracle, from seeded random states (every point non-trivial) and, for C2, from
+  the bench's own start (zero state + source); C2 also in fp64 (double2 default).
 * C4 2048x2048x1024 (R 4/4, 4.3 G points, 120 GB on the GPU): too large for the
   host oracle, so one step from a seeded random state is compared at ~3000
   sampled points (tile, chunk, slab and domain edges included), each evaluated
@@ -56,7 +57,7 @@ def compare(a, b):
     assert np.array_equal(a, b), f"max |diff| {np.abs(a - b).max():.3e}"
 
 
-@pytest.mark.parametrize("name,nsteps", [("C2", 3), ("C3", 2), ("C5", 1)])
+@pytest.mark.parametrize("name,nsteps", [("C2", 3), ("C3", 2), ("C5", 1), ("N1", 2)])
 def test_full_grid_random_state(name, nsteps):
     cfg = synth.CONFIGS[name]()
     wxy, wz, _ = synth.weights_f32(cfg)
@@ -161,3 +162,29 @@ def test_c4_sampled_points_one_step():
         gp, gq = got[(i, j, k)]
         bad += (gp != po) + (gq != qo)
     assert bad == 0, f"{bad} mismatching values over {len(pts)} points"
+
+
+def test_c2_fp64_full_grid():
+    """The fp64 path (N3) at the C2 size, whole grid, against the oracle's fp64 mode."""
+    from synth import weights as W
+    from paper_1410_1387_b200 import VTI
+    cfg = synth.CONFIGS["C2"]()
+    wxy = W.xy_weights(cfg["r_xy"])
+    zc = W.z_coords_ramp(cfg["nz"], cfg["r_z"], cfg["dz"][0], cfg["dz"][1])
+    wz = np.ascontiguousarray(W.z_weights(zc, cfg["r_z"]))
+    dt = synth.stable_dt(cfg)
+    model, st = host_inputs(cfg, seed=23)
+    model = [a.astype(np.float64) for a in model]
+    st = [a.astype(np.float64) for a in st]
+    with VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], cfg["r_xy"], cfg["r_z"], dt, wxy, wz,
+             damp_width=cfg["damp_width"], damp_alpha=cfg["damp_alpha"], device=0, precision=64) as v:
+        assert v.info()["points_per_thread"] == 2
+        v.set_model(*model)
+        v.set_fields(*st)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        v.step(2)
+        g = v.get_fields(0) + v.get_fields(1)
+    o = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, st, nsteps=2, dtype=np.float64)[:4]
+    for a, b in zip(g, o):
+        assert a.dtype == np.float64 and np.isfinite(a).all()
+        assert np.array_equal(a, b), f"max |diff| {np.abs(a - b).max():.3e}"
