@@ -180,9 +180,11 @@ vti_status vti_set_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, const doub
                                      const double *pm, const double *qm);
 
 /* Advance nsteps time steps (async on the handle's stream). With nranks > 1
- * and an nccl_id, every rank must call it with the same nsteps (NCCL halo
- * exchange of p's R_xy boundary rows each step). Errors: STATE (model unset,
- * or local-group handle), INSTABILITY (check_every), CUDA, COMM. */
+ * every rank must call it with the same nsteps: p's R_xy boundary rows are
+ * exchanged every step, through the neighbours' halo rows directly after
+ * vti_ipc_connect (the edge launch stores them over NVLink), else with NCCL
+ * (nccl_id at create time). Errors: STATE (model unset, local-group handle,
+ * or nranks > 1 with neither transport), INSTABILITY (check_every), CUDA, COMM. */
 vti_status vti_step(vti_t h, int32_t nsteps);
 
 /* vti_step bracketed by CUDA events on the handle's stream; *ms = device time
@@ -191,7 +193,8 @@ vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms);
 
 /* Local group: n handles created with the same cfg except rank = 0..n-1,
  * nranks = n and nccl_id = NULL (any devices, one process). Steps them in
- * lockstep with device-to-device halo copies instead of NCCL. */
+ * lockstep with the fused peer-memory halo transport between the handles'
+ * own buffers (the protocol of vti_ipc_connect, without IPC). */
 vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps);
 
 /* Copy out u^n (level 0) or the stored u^{n-1} (level 1) of this slab into
