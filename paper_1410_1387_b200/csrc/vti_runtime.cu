@@ -1645,7 +1645,8 @@ static constexpr int GRAPH_STEPS = 32;   // even: a replay returns to its starti
 
 static bool graph_eligible(const vti_s *h)
 {
-    if (!h->graph_enabled || h->cfg.nranks > 1 || h->nrec > 0 || h->cfg.check_every > 0 || h->suppress_src)
+    if (!h->graph_enabled || h->cfg.nranks > 1 || h->nrec > 0 || h->cfg.check_every > 0 || h->suppress_src ||
+        getenv("VTI_FORCE_SPLIT"))
         return false;
     const long items = (long)h->ntx * h->nty * h->nzc;
     if (items > (long)h->sms * h->ctas_per_sm) return false;          // multi-round: cooperative launches
@@ -1736,8 +1737,13 @@ vti_status vti_step(vti_t h, int32_t nsteps)
                 break;
             }
     }
+    // diagnostic: VTI_FORCE_SPLIT=1 runs a single slab with the multi-GPU two-launch schedule
+    // (edge tile rows, then interior; no transport) to time what one rank's GPU does per step
+    static const bool force_split = getenv("VTI_FORCE_SPLIT") && atoi(getenv("VTI_FORCE_SPLIT")) != 0;
     for (; it < nsteps; ++it) {
-        if (!multi) {
+        if (!multi && force_split) {
+            if ((s = launch_edge(h)) != VTI_OK || (s = launch_interior(h)) != VTI_OK) return s;
+        } else if (!multi) {
             if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk)) != VTI_OK) return s;
         } else if (h->peer) {
             // the edge launch stores the neighbours' halo rows itself; the interior overlaps their edges

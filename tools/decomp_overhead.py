@@ -1,11 +1,15 @@
 #!/usr/bin/env python
 """Cost of the y-slab decomposition on ONE GPU (not a scaling number).
 
-Runs the C2 grid as 1, 2 and 4 local-group slabs in one process on cuda:0
-(vti_group_step: edge tile rows, pack, device-to-device halo copy, unpack,
-interior rows -- the same schedule as the NCCL path with a copy transport)
-and prints Gpoints/s for each, so the overhead of the multi-slab step itself
-(extra launches, edge/interior split, halo traffic) is visible.
+Default: the C2 grid split into 1, 2 and 4 local-group slabs in one process
+on cuda:0. --weak: n slabs of the full C2 ny each (grid nx x n*ny x nz, the
+bench's weak-scaling workload per GPU), n = 1, 2, 4, 8.
+
+Both run vti_group_step, i.e. the multi-GPU step schedule: edge tile rows with
+the fused peer stores into the neighbours' halo rows, flag waits and writes,
+then the interior rows. They print Gpoints/s, so the overhead of the
+multi-slab step itself is visible: extra launch, edge/interior split, halo
+stores. NVLink and the other GPUs are not part of it.
 """
 import json
 import os
@@ -51,11 +55,20 @@ def run(cfg, nslabs, steps, warmup):
 
 
 if __name__ == "__main__":
-    name = sys.argv[1] if len(sys.argv) > 1 else "C2"
-    cfg = synth.CONFIGS[name]()
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    weak = "--weak" in sys.argv
+    name = args[0] if args else "C2"
+    base = synth.CONFIGS[name]()
     out = {}
-    for n in (1, 2, 4):
-        v, info = run(cfg, n, 200, 10)
+    for n in ((1, 2, 4, 8) if weak else (1, 2, 4)):
+        cfg = base
+        if weak:   # the bench's weak-scaling workload: n slabs of the base ny rows each
+            cfg = synth.scaled(base, base["nx"], base["ny"] * n, base["nz"])
+            cfg["src"] = base["src"]
+        v, info = run(cfg, n, 200 if not weak else max(50, 200 // n), 10)
         out[n] = {"gpoints_s": round(v, 2), "rank0_launches_per_step": info["launches_per_step"]}
+        if weak:
+            out[n]["efficiency_vs_1"] = round(v / out[1]["gpoints_s"], 4)
         print(n, out[n], flush=True)
-    print(json.dumps({"config": name, "slabs_on_one_gpu": out}))
+    print(json.dumps({"config": name, "mode": "weak (n slabs of ny rows)" if weak else "split one grid",
+                      "slabs_on_one_gpu": out}))
