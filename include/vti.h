@@ -254,7 +254,7 @@ int32_t vti_direction(vti_t h);
  * ends. A handle created with an nccl_id that is then connected uses this
  * transport instead of NCCL. Both calls are collective in effect: all ranks
  * must connect before the next vti_step, and all ranks must then step together.
- * Errors: STATE (nranks < 2, local-group handle), PARAM (blob of the wrong rank,
+ * Errors: STATE (nranks < 2), PARAM (blob of the wrong rank,
  * job, geometry, precision, layout or version), COMM (IPC or stream memory
  * operations unavailable), CUDA.
  */

@@ -661,6 +661,8 @@ vti_status vti_destroy(vti_t h)
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm) cudaStreamSynchronize(h->comm);
     if (h->comm_nccl && nccl().ok) nccl().CommDestroy(h->comm_nccl);
+    for (void *p : h->ipc_opened)   // the neighbours' mappings first
+        if (p) cudaIpcCloseMemHandle(p);
     for (int b = 0; b < 2; ++b) {
         cudaFree(h->pbuf[b]);
         cudaFree(h->qbuf[b]);
@@ -671,8 +673,6 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->counters);
     cudaFree(h->flag);
     cudaFree(h->sync_ctr);
-    for (void *p : h->ipc_opened)
-        if (p) cudaIpcCloseMemHandle(p);
     cudaFree(h->flags);
     cudaFree(h->rec_off);
     cudaFree(h->traces);
@@ -1452,7 +1452,6 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
     if (!h) return VTI_E_PARAM;
     const int r = h->cfg.rank, nr = h->cfg.nranks;
     if (nr < 2) return fail(h, VTI_E_STATE, "vti_ipc_connect needs nranks > 1");
-    if (h->group_mode) return fail(h, VTI_E_STATE, "local-group handles connect through vti_group_step");
     if ((r > 0) != (lo != nullptr) || (r < nr - 1) != (hi != nullptr))
         return fail(h, VTI_E_PARAM, "pass the blob of rank-1 (lo) and rank+1 (hi), NULL at the ends");
     const StreamMemOps &ops = stream_mem_ops();
@@ -1484,6 +1483,7 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
         h->peer_flags[side] = (unsigned int *)fl;
     }
     h->peer = true;
+    h->group_mode = false;   // created with nccl_id = NULL; now a multi-process peer rank stepped by vti_step
     return VTI_OK;
 }
 

@@ -1,0 +1,80 @@
+"""Multi-process bootstrap of the fused peer transport over CUDA IPC.
+
+Two processes on cuda:0, each owning one y-slab handle (nranks = 2, nccl_id = NULL),
+run bench.py's own connect path (paper_1410_1387_b200.multi.connect_peer over a gloo
+group): export the IPC blobs, all-gather them, open the neighbour's buffers and flag
+words. The handles must then report the peer transport and the two-launch step.
+Nothing is stepped: ranks that wait on one another must not share one GPU
+(B200_PROFILING.md), so the stepping protocol itself is covered by the local-group
+GPU tests (same kernels and flag sequence) and the CPU model check
+(tests/test_peer_protocol_cpu.py).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1410_1387_b200 import VTI, VTIError, multi
+        nz = 20
+        h = VTI(64, 192, nz, 10.0, 4, 4, 1e-3, np.zeros(5, np.float32), np.zeros(nz * 9, np.float32),
+                damp_width=0, device=0, rank=rank, nranks=world)
+        before = h.halo_transport
+        ok = multi.connect_peer(dist, h, rank, world)
+        res = {"before": before, "ok": ok, "after": h.halo_transport, "launches": h.info()["launches_per_step"]}
+        # a blob of the wrong rank is refused
+        try:
+            h.ipc_connect(h.ipc_export() if rank > 0 else None, h.ipc_export() if rank < world - 1 else None)
+            res["self_blob"] = "accepted"
+        except VTIError as e:
+            res["self_blob"] = e.name
+        dist.barrier()
+        h.close()
+        dist.barrier()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_ipc_connect():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        got = dict(q.get(timeout=240) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    for r in range(world):
+        assert got[r]["before"] == "none", got
+        assert got[r]["ok"] is True, got
+        assert got[r]["after"] == "peer", got
+        assert got[r]["launches"] == 2, got
+        assert got[r]["self_blob"] == "VTI_E_PARAM", got
+    for p in procs:
+        assert p.exitcode == 0
