@@ -58,17 +58,19 @@ if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     weak = "--weak" in sys.argv
     name = args[0] if args else "C2"
+    slabs = tuple(int(x) for x in args[1].split(",")) if len(args) > 1 else ((1, 2, 4, 8) if weak else (1, 2, 4))
+    steps = int(args[2]) if len(args) > 2 else 200
     base = synth.CONFIGS[name]()
     out = {}
-    for n in ((1, 2, 4, 8) if weak else (1, 2, 4)):
+    for n in slabs:
         cfg = base
         if weak:   # the bench's weak-scaling workload: n slabs of the base ny rows each
             cfg = synth.scaled(base, base["nx"], base["ny"] * n, base["nz"])
             cfg["src"] = base["src"]
-        v, info = run(cfg, n, 200 if not weak else max(50, 200 // n), 10)
+        v, info = run(cfg, n, steps if not weak else max(25, steps // n), 5)
         out[n] = {"gpoints_s": round(v, 2), "rank0_launches_per_step": info["launches_per_step"]}
-        if weak:
-            out[n]["efficiency_vs_1"] = round(v / out[1]["gpoints_s"], 4)
+        if 1 in out:
+            out[n]["vs_1_slab"] = round(v / out[1]["gpoints_s"], 4)
         print(n, out[n], flush=True)
     print(json.dumps({"config": name, "mode": "weak (n slabs of ny rows)" if weak else "split one grid",
                       "slabs_on_one_gpu": out}))
