@@ -147,6 +147,20 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def mix_ceiling():
+    """Best streaming rate of the step's own DRAM mix (7 streams read, 2 written) measured by
+    tools/stream_probe.cu (profiles/stream_probe_r01.txt): the practical ceiling of this kernel,
+    above the 1:1 copy figure of MEASURED_PEAKS.json. Context for roofline.frac > 1."""
+    import re
+    p = os.path.join(ROOT, "profiles", "stream_probe_r01.txt")
+    try:
+        vals = [float(m.group(1)) for line in open(p) if line.startswith("grid")
+                for m in [re.search(r"([0-9.]+) TB/s", line)] if m]
+        return max(vals) * 1000.0 if vals else None
+    except OSError:
+        return None
+
+
 def ncu_traffic(cfg, precision=32):
     """dram bytes per launch from the committed ncu --set full summary, if one matches this workload."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -398,6 +412,9 @@ def run_native(args):
             "config": describe(cfg, world, scaling, bpp, transport),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "mix_ceiling": ({"gbs": mc, "frac": round(achieved / mc, 4),
+                                          "source": "profiles/stream_probe_r01.txt (7 read + 2 write float4 streams)"}
+                                         if (mc := mix_ceiling()) else None),
                          "kernel": "vti::vti_step_kernel<4,4>" if cfg["r_xy"] == 4 else f"vti::vti_step_kernel<{cfg['r_xy']},{cfg['r_z']}>",
                          "algorithmic_bytes_per_launch": bpp * pts_rank,
                          "flops_per_point": {"paper_count": perfmodel.flops_per_point(cfg["r_xy"], cfg["r_z"]),
