@@ -63,7 +63,9 @@ def dist_env():
 def workload(args, world):
     import synth
     base = synth.CONFIGS[args.config]() if args.config != "C5" else synth.CONFIGS["C5"](world)
-    scaling = args.scaling or ("strong" if args.config == "C4" else "weak")
+    # C3 = y-slabs of 1024/G rows and C4 = strong scaling (fixed grid); C2 = 512^3
+    # per GPU and C5 = 1024 x 1024G x 1024 (weak)
+    scaling = args.scaling or ("strong" if args.config in ("C3", "C4") else "weak")
     if world > 1 and scaling == "weak" and args.config != "C5":
         cfg = synth.scaled(base, base["nx"], base["ny"] * world, base["nz"])
     else:
