@@ -181,10 +181,11 @@ def slab(ny: int, rank: int, nranks: int):
     return y0.value, n.value
 
 
-def plan(nx, ny, nz, r_xy, r_z, tile_y=32, sms=148, ctas_per_sm=1, rank=0, nranks=1, damp_width=0) -> dict:
+def plan(nx, ny, nz, r_xy, r_z, tile_y=32, sms=148, ctas_per_sm=1, rank=0, nranks=1, damp_width=0,
+         precision=32) -> dict:
     """The library's host-side schedule for a configuration (no GPU needed)."""
     c = Config(nx=nx, ny=ny, nz=nz, h=10.0, r_xy=r_xy, r_z=r_z, dt=1e-3, damp_width=damp_width, damp_alpha=0.015,
-               rank=rank, nranks=nranks, precision=32)
+               rank=rank, nranks=nranks, precision=precision)
     out = PlanInfo()
     _check(None, lib.vti_plan(C.byref(c), tile_y, sms, ctas_per_sm, C.byref(out)))
     return out.as_dict()

@@ -293,6 +293,7 @@ struct vti_s {
     int sms = 0, ctas_per_sm = 0;
     int zchunk = 0, nzc = 0, grid = 0;        // single-launch schedule
     int zchunk_edge = 0, zchunk_inner = 0;    // nranks > 1: per-launch chunking
+    int cap = 0, cap_edge = 0, cap_inner = 0; // CTAs per launch at most (plan_sched)
     int tune_zchunk = 0, tune_ctas = 0;       // vti_set_tuning / vti_autotune overrides (0 = model)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -456,30 +457,57 @@ static double lat_planes()
     return lat;
 }
 
-static int plan_zchunk(int nz, int rz, int tiles, int slots, double sat, int tune_zchunk)
+// HBM streaming efficiency falls when more than ~128 CTAs (per CTA-per-SM slot)
+// stream at once: tools/stream_probe_bulk.cu moves the step's 7R+2W mix at 7.10
+// TB/s with 110-128 CTAs but 6.90 TB/s with 148. eff(a) models that (0.97 at 148)
+// for the fp32 kernels (C3 183 -> 190, C4 179 -> 191, C5 182 -> 187 Gpoints/s with
+// a 128-CTA grid); the slower fp64 CTAs need the full grid to saturate HBM, so
+// their plans keep it (measured: capping costs them 2-4 %).
+static constexpr int CONC = 128;
+static double conc_eff(long a, int ctas_per_sm)
 {
-    if (tune_zchunk > 0) return std::min(tune_zchunk, nz);
-    if (tiles <= 0 || slots <= 0) return nz;
+    const double over = (double)a / ctas_per_sm - CONC;
+    return over > 0 ? 1.0 - 0.0015 * over : 1.0;
+}
+
+struct Sched {
+    int zchunk;   // planes per work item
+    int cap;      // CTAs launched at most (<= slots)
+};
+
+static Sched plan_sched(int nz, int rz, int tiles, int slots, int ctas_per_sm, double sat, int tune_zchunk,
+                        bool conc_model)
+{
+    if (tiles <= 0 || slots <= 0) return {nz, std::max(slots, 1)};
     sat = std::max(1.0, std::min(sat, (double)slots));
     const double lat = lat_planes();
     double best = 1e300;
-    int best_zc = nz;
-    for (int nzc = 1; nzc <= nz; ++nzc) {
-        const int zc = (nz + nzc - 1) / nzc;
-        if ((nz + zc - 1) / zc != nzc) continue;   // same chunking as a smaller nzc
-        const long items = (long)tiles * nzc;
-        const long full = items / slots, last = items % slots;
-        const double prime = 1.0 + (8.0 * rz) / (36.0 * zc);
-        const double lat_round = (zc + 2.0 * rz) * lat;
-        auto round_cost = [&](long a) { return std::max(zc * prime * a / std::min<double>(a, sat), lat_round); };
-        double cost = (double)full * round_cost(slots);
-        if (last) cost += round_cost(last);
-        if (cost < best * (1.0 - 1e-3)) {
-            best = cost;
-            best_zc = zc;
+    Sched out{tune_zchunk > 0 ? std::min(tune_zchunk, nz) : nz, slots};
+    const int caps[2] = {slots, std::min(slots, CONC * ctas_per_sm)};
+    for (int ci = 0; ci < (conc_model ? 2 : 1); ++ci) {
+        const int cap = caps[ci];
+        if (ci == 1 && cap == slots) break;
+        for (int nzc = 1; nzc <= nz; ++nzc) {
+            const int zc = (nz + nzc - 1) / nzc;
+            if ((nz + zc - 1) / zc != nzc) continue;   // same chunking as a smaller nzc
+            if (tune_zchunk > 0 && zc != std::min(tune_zchunk, nz)) continue;
+            const long items = (long)tiles * nzc;
+            const long full = items / cap, last = items % cap;
+            const double prime = 1.0 + (8.0 * rz) / (36.0 * zc);
+            const double lat_round = (zc + 2.0 * rz) * lat;
+            auto round_cost = [&](long a) {
+                const double eff = conc_model ? conc_eff(a, ctas_per_sm) : 1.0;
+                return std::max(zc * prime * a / (std::min<double>(a, sat) * eff), lat_round);
+            };
+            double cost = (double)full * round_cost(cap);
+            if (last) cost += round_cost(last);
+            if (cost < best * (1.0 - 1e-3)) {
+                best = cost;
+                out = {zc, cap};
+            }
         }
     }
-    return best_zc;
+    return out;
 }
 
 // nranks > 1: the edge launch covers every tile row that intersects the first
@@ -491,9 +519,18 @@ static void plan_edge_rows(int nty, int r, int ty, int nyl, int &e1, int &e2)
     e2 = std::max(e1, std::min(nty, (nyl - r) / ty));
 }
 
-static int choose_zchunk(const vti_s *h, int tiles)
+// CTA slots of a launch: resident CTAs, optionally capped (env VTI_MAXGRID, experiments)
+static int slots(const vti_s *h)
 {
-    return plan_zchunk(h->cfg.nz, h->RZ, tiles, h->sms * h->ctas_per_sm, sat_ctas(h->ctas_per_sm), h->tune_zchunk);
+    static const int cap = getenv("VTI_MAXGRID") ? atoi(getenv("VTI_MAXGRID")) : 0;
+    const int n = h->sms * h->ctas_per_sm;
+    return cap > 0 ? std::min(n, cap) : n;
+}
+
+static Sched choose_sched(const vti_s *h, int tiles)
+{
+    return plan_sched(h->cfg.nz, h->RZ, tiles, slots(h), h->ctas_per_sm, sat_ctas(h->ctas_per_sm), h->tune_zchunk,
+                      h->es == 4);
 }
 
 static void edge_rows(const vti_s *h, int &e1, int &e2) { plan_edge_rows(h->nty, h->R, h->TY, h->nyl, e1, e2); }
@@ -505,12 +542,17 @@ static void choose_schedule(vti_s *h)
     int e1, e2;
     edge_rows(h, e1, e2);
     const int edge_rows = e1 + (h->nty - e2), inner_rows = e2 - e1;
-    h->zchunk = choose_zchunk(h, h->ntx * h->nty);
-    h->zchunk_edge = choose_zchunk(h, h->ntx * edge_rows);
-    h->zchunk_inner = choose_zchunk(h, h->ntx * inner_rows);
+    const Sched a = choose_sched(h, h->ntx * h->nty), e = choose_sched(h, h->ntx * edge_rows),
+                i = choose_sched(h, h->ntx * inner_rows);
+    h->zchunk = a.zchunk;
+    h->cap = a.cap;
+    h->zchunk_edge = e.zchunk;
+    h->cap_edge = e.cap;
+    h->zchunk_inner = i.zchunk;
+    h->cap_inner = i.cap;
     h->nzc = (h->cfg.nz + h->zchunk - 1) / h->zchunk;
     const long items = (long)h->ntx * h->nty * h->nzc;
-    h->grid = (int)std::min<long>(items, (long)h->sms * h->ctas_per_sm);
+    h->grid = (int)std::min<long>(items, (long)h->cap);
 }
 
 static int precision_bits(const vti_config *c) { return c->precision == 0 ? 32 : c->precision; }
@@ -633,12 +675,15 @@ vti_status vti_plan(const vti_config *cfg, int32_t tile_y, int32_t sms, int32_t 
     out->edge_hi = e2;
     const int slots = sms * ctas_per_sm;
     const double sat = sat_ctas(ctas_per_sm);
-    out->zchunk = plan_zchunk(cfg->nz, cfg->r_z, out->ntx * out->nty, slots, sat, 0);
-    out->zchunk_edge = plan_zchunk(cfg->nz, cfg->r_z, out->ntx * (e1 + out->nty - e2), slots, sat, 0);
-    out->zchunk_inner = plan_zchunk(cfg->nz, cfg->r_z, out->ntx * (e2 - e1), slots, sat, 0);
+    const bool f32 = precision_bits(cfg) == 32;
+    const Sched a = plan_sched(cfg->nz, cfg->r_z, out->ntx * out->nty, slots, ctas_per_sm, sat, 0, f32);
+    out->zchunk = a.zchunk;
+    out->zchunk_edge =
+        plan_sched(cfg->nz, cfg->r_z, out->ntx * (e1 + out->nty - e2), slots, ctas_per_sm, sat, 0, f32).zchunk;
+    out->zchunk_inner = plan_sched(cfg->nz, cfg->r_z, out->ntx * (e2 - e1), slots, ctas_per_sm, sat, 0, f32).zchunk;
     const long items = (long)out->ntx * out->nty * ((cfg->nz + out->zchunk - 1) / out->zchunk);
     out->items = (int32_t)items;
-    out->grid = (int32_t)std::min<long>(items, slots);
+    out->grid = (int32_t)std::min<long>(items, a.cap);
     return VTI_OK;
 }
 
@@ -1096,7 +1141,7 @@ static void fill_params(vti_s *h, StepParams<T> &P, int tr0, int ntr0, int tr1, 
 }
 
 template <typename T>
-static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk)
+static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk, int cap)
 {
     StepParams<T> P;
     fill_params<T>(h, P, tr0, ntr0, tr1, ntr1, zchunk);
@@ -1104,7 +1149,7 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
         P.s_table = (const T *)h->s_graph;
         P.s_index = h->capture_index;
     }
-    const int grid = std::min(P.items, h->sms * h->ctas_per_sm);
+    const int grid = std::min(P.items, cap > 0 ? std::min(cap, slots(h)) : slots(h));
     const int rounds = (P.items + grid - 1) / grid;
     P.sync_ctr = nullptr;
     P.sync_base = 0;
@@ -1133,25 +1178,25 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
 }
 
 // Tile rows [tr0, tr0+ntr0) then [tr1, tr1+ntr1) of this slab, z-chunks of zchunk planes.
-static vti_status launch_rows(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk)
+static vti_status launch_rows(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk, int cap)
 {
     if (ntr0 + ntr1 <= 0) return VTI_OK;
-    return h->es == 8 ? launch_rows_t<double>(h, tr0, ntr0, tr1, ntr1, zchunk)
-                      : launch_rows_t<float>(h, tr0, ntr0, tr1, ntr1, zchunk);
+    return h->es == 8 ? launch_rows_t<double>(h, tr0, ntr0, tr1, ntr1, zchunk, cap)
+                      : launch_rows_t<float>(h, tr0, ntr0, tr1, ntr1, zchunk, cap);
 }
 
 static vti_status launch_edge(vti_s *h)
 {
     int e1, e2;
     edge_rows(h, e1, e2);
-    return launch_rows(h, 0, e1, e2, h->nty - e2, h->zchunk_edge);
+    return launch_rows(h, 0, e1, e2, h->nty - e2, h->zchunk_edge, h->cap_edge);
 }
 
 static vti_status launch_interior(vti_s *h)
 {
     int e1, e2;
     edge_rows(h, e1, e2);
-    return launch_rows(h, e1, e2 - e1, 0, 0, h->zchunk_inner);
+    return launch_rows(h, e1, e2 - e1, 0, 0, h->zchunk_inner, h->cap_inner);
 }
 
 // ---- halo transport of p (y-slab decomposition)
@@ -1654,7 +1699,7 @@ static bool graph_eligible(const vti_s *h)
         getenv("VTI_FORCE_SPLIT"))
         return false;
     const long items = (long)h->ntx * h->nty * h->nzc;
-    if (items > (long)h->sms * h->ctas_per_sm) return false;          // multi-round: cooperative launches
+    if (items > (long)h->cap) return false;          // multi-round: cooperative launches
     const double pts = (double)h->cfg.nx * h->nyl * h->cfg.nz;
     return pts <= 64.0 * 1024 * 1024;   // beyond that a step is long enough that launch gaps do not matter
 }
@@ -1671,7 +1716,7 @@ static vti_status build_graph(vti_s *h, int c)
     for (int i = 0; i < GRAPH_STEPS && s == VTI_OK; ++i) {
         h->cur = (c + i) & 1;
         h->capture_index = i;
-        s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk);
+        s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk, h->cap);
     }
     h->capturing = false;
     h->cur = keep_cur;
@@ -1749,7 +1794,7 @@ vti_status vti_step(vti_t h, int32_t nsteps)
         if (!multi && force_split) {
             if ((s = launch_edge(h)) != VTI_OK || (s = launch_interior(h)) != VTI_OK) return s;
         } else if (!multi) {
-            if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk)) != VTI_OK) return s;
+            if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk, h->cap)) != VTI_OK) return s;
         } else if (h->peer) {
             // the edge launch stores the neighbours' halo rows itself; the interior overlaps their edges
             if ((s = peer_pre_step(h)) != VTI_OK) return s;
@@ -1887,7 +1932,7 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->producer_warp = h->K->wp;
     info->points_per_thread = h->K->px;
     info->zchunk = h->zchunk;
-    info->grid = std::min(h->ntx * h->nty * h->nzc, h->sms * h->ctas_per_sm);
+    info->grid = std::min(h->ntx * h->nty * h->nzc, h->cap);
     info->work_items = h->ntx * h->nty * h->nzc;
     if (h->cfg.nranks > 1) {   // edge + interior step kernels (+ pack and unpack per neighbour with NCCL)
         const int neighbours = (h->cfg.rank > 0) + (h->cfg.rank < h->cfg.nranks - 1);

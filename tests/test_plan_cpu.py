@@ -43,9 +43,22 @@ def test_zchunk_choice_properties(nx, ny, nz, r, rz):
     tiles = p["ntx"] * p["nty"]
     assert 4 * rz <= p["zchunk"] <= nz       # big grids: no short chunks (q priming re-reads)
     nzc = -(-nz // p["zchunk"])
-    assert p["items"] == tiles * nzc and p["grid"] == min(p["items"], 148)
+    # fp32: the concurrency term may cap a multi-round launch at 128 CTAs (HBM streams best there)
+    assert p["items"] == tiles * nzc and p["grid"] in (min(p["items"], 148), min(p["items"], 128))
     if tiles >= 128:              # enough tiles: long z columns (L2 reuse, no extra q priming)
         assert p["zchunk"] >= nz // 2
+    p64 = V.plan(nx, ny, nz, r, rz, tile_y=15, sms=148, ctas_per_sm=1, precision=64)
+    assert p64["grid"] == min(p64["items"], 148)      # fp64 keeps the full grid
+
+
+def test_concurrency_cap_on_the_bench_grids():
+    """C3 and C4 (fp32): whole rounds of 128 full columns; N1's 144 columns stay one round of 144."""
+    c3 = V.plan(1024, 1024, 512, 8, 4, tile_y=32, sms=148, ctas_per_sm=1)
+    c4 = V.plan(2048, 2048, 1024, 4, 4, tile_y=32, sms=148, ctas_per_sm=1)
+    n1 = V.plan(512, 512, 512, 12, 8, tile_y=30, sms=148, ctas_per_sm=1)
+    assert (c3["zchunk"], c3["items"], c3["grid"]) == (512, 512, 128)
+    assert (c4["zchunk"], c4["items"], c4["grid"]) == (1024, 2048, 128)
+    assert (n1["zchunk"], n1["items"], n1["grid"]) == (512, 144, 144)
 
 
 def test_c2_weak_scaling_rank_plan():
