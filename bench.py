@@ -150,17 +150,19 @@ def peak_hbm():
 
 
 def mix_ceiling():
-    """Best streaming rate of the step's own DRAM mix (7 streams read, 2 written) measured by
-    tools/stream_probe.cu (profiles/stream_probe_r01.txt): the practical ceiling of this kernel,
-    above the 1:1 copy figure of MEASURED_PEAKS.json. Context for roofline.frac > 1."""
+    """Best streaming rate of the step's own DRAM mix (7 streams read, 2 written), measured by
+    tools/stream_probe.cu (plain loads) and tools/stream_probe_bulk.cu (TMA bulk loads, the way
+    the kernel moves data) -- profiles/stream_probe*_r01.txt: the practical ceiling of this
+    kernel, above the 1:1 copy figure of MEASURED_PEAKS.json. Context for roofline.frac > 1."""
+    import glob
     import re
-    p = os.path.join(ROOT, "profiles", "stream_probe_r01.txt")
-    try:
-        vals = [float(m.group(1)) for line in open(p) if line.startswith("grid")
-                for m in [re.search(r"([0-9.]+) TB/s", line)] if m]
-        return max(vals) * 1000.0 if vals else None
-    except OSError:
-        return None
+    vals = []
+    for p in glob.glob(os.path.join(ROOT, "profiles", "stream_probe*_r01.txt")):
+        for line in open(p):
+            m = None if line.startswith("#") else re.search(r"([0-9.]+) TB/s", line)
+            if m:
+                vals.append(float(m.group(1)))
+    return max(vals) * 1000.0 if vals else None
 
 
 def ncu_traffic(cfg, precision=32):
@@ -415,7 +417,8 @@ def run_native(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "mix_ceiling": ({"gbs": mc, "frac": round(achieved / mc, 4),
-                                          "source": "profiles/stream_probe_r01.txt (7 read + 2 write float4 streams)"}
+                                          "source": "profiles/stream_probe*_r01.txt (7 read + 2 write streams, "
+                                                    "best of plain and TMA-bulk loads)"}
                                          if (mc := mix_ceiling()) else None),
                          "kernel": "vti::vti_step_kernel<4,4>" if cfg["r_xy"] == 4 else f"vti::vti_step_kernel<{cfg['r_xy']},{cfg['r_z']}>",
                          "algorithmic_bytes_per_launch": bpp * pts_rank,
