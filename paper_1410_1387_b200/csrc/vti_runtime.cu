@@ -5,85 +5,11 @@
 // R_xy halo rows on both y sides of which only p's are ever non-zero), builds
 // the TMA tensor maps, the per-plane w^z + gz table and the 1-D Cerjan
 // profiles, evaluates the Ricker sample per step on the host, and launches the
-// step kernel(s). With nranks > 1 it packs p's R_xy boundary rows after the
-// edge tiles, exchanges them over NCCL (one process per GPU) or with
-// device-to-device copies (local group), and unpacks them into the halo rows
-// while the interior tiles run.
-#include <cuda.h>
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdarg>
-#include <cstdio>
-#include <cstring>
-#include <mutex>
-#include <string>
-#include <vector>
-
-#include "vti.h"
-#include "vti_kernel.cuh"
-#include "vti_variants.h"
-
-using namespace vti;
-
-// ============================================================ NCCL (dlopen'ed)
-typedef struct ncclComm *ncclComm_t;
-typedef struct {
-    char internal[128];
-} ncclUniqueId;
-typedef enum { ncclSuccess = 0 } ncclResult_t;
-typedef enum { ncclFloat32 = 7, ncclFloat64 = 8 } ncclDataType_t;
-
-struct NcclApi {
-    bool ok = false;
-    std::string err;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*GroupStart)() = nullptr;
-    ncclResult_t (*GroupEnd)() = nullptr;
-    const char *(*GetErrorString)(ncclResult_t) = nullptr;
-};
-
-static NcclApi &nccl()
-{
-    static NcclApi api;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        const char *env = getenv("VTI_NCCL_LIB");
-        const char *names[] = {env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
-        void *h = nullptr;
-        for (const char *n : names) {
-            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
-            if (h) break;
-        }
-        if (!h) {
-            api.err = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
-            return;
-        }
-#define LOADSYM(field, name)                                                   \
-    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));        \
-    if (!api.field) {                                                          \
-        api.err = std::string("missing NCCL symbol ") + name;                  \
-        return;                                                                \
-    }
-        LOADSYM(GetUniqueId, "ncclGetUniqueId");
-        LOADSYM(CommInitRank, "ncclCommInitRank");
-        LOADSYM(CommDestroy, "ncclCommDestroy");
-        LOADSYM(Send, "ncclSend");
-        LOADSYM(Recv, "ncclRecv");
-        LOADSYM(GroupStart, "ncclGroupStart");
-        LOADSYM(GroupEnd, "ncclGroupEnd");
-        LOADSYM(GetErrorString, "ncclGetErrorString");
-#undef LOADSYM
-        api.ok = true;
-    });
-    return api;
-}
+// step kernel(s): one launch per step on a single slab, or with nranks > 1 an
+// edge launch (whose PEER kernel stores the boundary rows into the neighbours'
+// halos) and an interior launch, with the transport of vti_transport.cu between
+// them. Scheduling lives in vti_schedule.cu (see vti_internal.h).
+#include "vti_internal.h"
 
 // ============================================================ driver entry point
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -104,30 +30,6 @@ static PFN_encodeTiled get_encode()
     return fn;
 }
 
-
-// Stream memory operations (the copy-engine halo transport's flags).
-typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-struct StreamMemOps {
-    PFN_streamValue32 wait = nullptr, write = nullptr;
-};
-
-static const StreamMemOps &stream_mem_ops()
-{
-    static StreamMemOps ops;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            ops.wait = reinterpret_cast<PFN_streamValue32>(p);
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            ops.write = reinterpret_cast<PFN_streamValue32>(p);
-    });
-    return ops;
-}
 
 // ============================================================ kernel table
 // Compiled variants live in csrc/variants/*.cu (see vti_variants.h); the first
@@ -236,34 +138,6 @@ __global__ void k_check_finite(const T *__restrict__ p, const T *__restrict__ q,
 
 // Halo transport of p: rows [row0, row0 + R) of a halo'd buffer (row index
 // counted from the first halo row) <-> a contiguous [nz][R][nx] buffer.
-template <typename T>
-__global__ void k_pack_rows(const T *__restrict__ buf, T *__restrict__ out, int row0, int R, int nz, int nx,
-                            long long ys, long long zs)
-{
-    const int64_t n = (int64_t)nz * R * nx;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(t % nx);
-        const int64_t r = t / nx;
-        const int y = (int)(r % R);
-        const int k = (int)(r / R);
-        out[t] = buf[(row0 + y) * ys + k * zs + x];
-    }
-}
-
-template <typename T>
-__global__ void k_unpack_rows(const T *__restrict__ in, T *__restrict__ buf, int row0, int R, int nz, int nx,
-                              long long ys, long long zs)
-{
-    const int64_t n = (int64_t)nz * R * nx;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(t % nx);
-        const int64_t r = t / nx;
-        const int y = (int)(r % R);
-        const int k = (int)(r / R);
-        buf[(row0 + y) * ys + k * zs + x] = in[t];
-    }
-}
-
 // Receivers: after each step, gather u^n at the receiver
 // points (interior-view element offsets) into trace row t: out[t][r][f].
 template <typename T>
@@ -278,92 +152,10 @@ __global__ void k_record(const T *__restrict__ p, const T *__restrict__ q, const
     if (mask & 2) out[(size_t)r * nf + f] = q[off[r]];
 }
 
-// ============================================================ handle
-struct vti_s {
-    vti_config cfg{};
-    std::string err;
-    int es = 4;                               // element size: 4 (fp32) or 8 (fp64)
-    int R = 0, RZ = 0, TY = 16;
-    int y0 = 0, nyl = 0, nxp = 0, rows = 0;   // rows = nyl + 2R (halo'd)
-    long long ys = 0, zs = 0;                 // row / plane strides (elements)
-    bool layout_zyx = true;                   // [z][y][x] (default) or [y][z][x]
-    int ntx = 0, nty = 0;
-    const KernelEntry *K = nullptr;
-    int smem_bytes = 0;
-    int sms = 0, ctas_per_sm = 0;
-    int zchunk = 0, nzc = 0, grid = 0;        // single-launch schedule
-    int zchunk_edge = 0, zchunk_inner = 0;    // nranks > 1: per-launch chunking
-    int cap = 0, cap_edge = 0, cap_inner = 0; // CTAs per launch at most (plan_sched)
-    int tune_zchunk = 0, tune_ctas = 0;       // vti_set_tuning / vti_autotune overrides (0 = model)
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    cudaStream_t comm = nullptr;
-    cudaEvent_t ev_edge = nullptr, ev_comm = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
-    void *pbuf[2] = {nullptr, nullptr};       // halo'd arrays (base = first halo row)
-    void *qbuf[2] = {nullptr, nullptr};
-    void *vx2 = nullptr, *vn2 = nullptr, *vz2 = nullptr;
-    void *sbuf[2] = {nullptr, nullptr};       // packed send rows: [0] to rank-1, [1] to rank+1
-    void *rbuf[2] = {nullptr, nullptr};       // packed recv rows: [0] from rank-1, [1] from rank+1
-    void *zrow = nullptr, *gx = nullptr, *gy = nullptr;
-    void *staging = nullptr;
-    size_t staging_bytes = 0;
-    unsigned long long *counters = nullptr;
-    unsigned int *flag = nullptr;
-    unsigned long long *sync_ctr = nullptr;   // round-alignment counter (monotone across launches)
-    unsigned long long sync_value = 0;        // its value once all launched work has finished
-    bool align_rounds = true;                 // env VTI_ALIGN=0 disables
-    int64_t device_bytes = 0;
-    CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
-    double cxy[MAX_R + 1] = {0};              // w^xy / h^2 in double; rounded to T at launch (reading c3)
-    int cur = 0;                              // pbuf[cur], qbuf[cur] hold u^n
-    int64_t n = 0;                            // time index
-    bool model_set = false;
-    int64_t model_planes_set = 0;
-    int64_t aniso_warn = 0;
-    bool has_src = false;
-    int src_i = 0, src_j = 0, src_k = 0, src_mask = 0;
-    double src_f = 15.0, src_t0 = 0.0, src_amp = 1.0;
-    ncclComm_t comm_nccl = nullptr;
-    bool group_mode = false;
-    // fused peer-memory halo transport (local group, or multi-process after vti_ipc_connect):
-    // the edge launch stores p^{n+1}'s boundary rows straight into the neighbours' halo rows;
-    // flags[] = {DATA_LO, DATA_HI, ACK_LO, ACK_HI}, written by the neighbours
-    bool peer = false;
-    unsigned int *flags = nullptr;
-    void *peer_p[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][b]: neighbour's pbuf[b] at the
-                                                                      // first halo row this rank writes
-    long long peer_zs[2] = {0, 0};                    // the neighbours' plane strides (elements)
-    unsigned int *peer_flags[2] = {nullptr, nullptr}; // the neighbours' flags
-    void *ipc_opened[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // cudaIpcCloseMemHandle on destroy
-    unsigned int xseq = 0;                            // halo publications so far (the flag values)
-    bool flush_remote = false;                        // CU_STREAM_WAIT_VALUE_FLUSH supported
-    bool halo_dirty = false;
-    bool suppress_src = false;                // autotune probes inject nothing
-    bool fields_touched = false;              // vti_set_fields* called (state may be non-zero)
-    int dir = 1;                              // +1 forward in time, -1 after vti_reverse
-    // CUDA graphs of GRAPH_STEPS single-slab steps (launch-bound small grids)
-    bool graph_enabled = true;                // env VTI_GRAPH=0 disables
-    bool capturing = false;
-    int capture_index = 0;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // by starting parity (cur)
-    void *s_graph = nullptr;                  // device: GRAPH_STEPS source samples of T
-    std::vector<double> s_host;
-    // receivers (this slab's subset, in the caller's order)
-    int nrec = 0, rec_mask = 0, rec_cap = 0, rec_steps = 0;
-    long long *rec_off = nullptr;             // device: element offsets in an interior view
-    void *traces = nullptr;                   // device: [rec_cap][nrec][nf] of T
-    std::vector<int32_t> rec_ids;             // global receiver index of each local receiver
-
-    size_t total_elems() const { return (size_t)cfg.nz * rows * nxp; }
-    char *in(void *base) const { return (char *)base + (long long)R * ys * es; }   // interior view
-    char *p_int(int b) const { return in(pbuf[b]); }
-    char *q_int(int b) const { return in(qbuf[b]); }
-};
-
 static std::mutex g_err_mu;
 static std::string g_create_err;
 
-static vti_status fail(vti_s *h, vti_status s, const char *fmt, ...)
+vti_status fail(vti_s *h, vti_status s, const char *fmt, ...)
 {
     char buf[1024];
     va_list ap;
@@ -379,11 +171,6 @@ static vti_status fail(vti_s *h, vti_status s, const char *fmt, ...)
     return s;
 }
 
-#define CU(h, call)                                                                                   \
-    do {                                                                                              \
-        cudaError_t e_ = (call);                                                                      \
-        if (e_ != cudaSuccess) return fail(h, VTI_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
-    } while (0)
 
 static double damping(int idx, int n, int W, double alpha)
 {
@@ -431,147 +218,6 @@ static vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx
     return VTI_OK;
 }
 
-// ---- host-side planning (pure functions; exported for tests as vti_plan)
-// Work items are (tile, z-chunk). Measured on B200: full z
-// columns marching in lockstep keep the p apron re-reads in L2 and avoid the
-// 2Rz-plane q priming of each chunk, and ~110 resident CTAs already saturate
-// HBM (C2: 128 columns on 148 SMs beat 1024 chunks). The chunk count per
-// launch minimises a wave cost, in units of one saturated plane-time: a round
-// of a active CTAs costs the larger of its bandwidth time
-//   zchunk * (1 + 8 Rz / (36 zchunk)) * a / min(a, SAT)   (q priming re-reads)
-// and its latency time (zchunk + 2 Rz) * LAT (each item walks its stage loads
-// in order; ~0.7 plane-times per dependent load, measured on C1 where 8 CTAs
-// of 24 loads took 18.9 us). Small grids therefore get short chunks and many
-// CTAs, large grids long columns.
-static double sat_ctas(int ctas_per_sm)
-{
-    double sat = 110.0 * ctas_per_sm;
-    if (const char *e = getenv("VTI_SAT")) sat = atof(e);
-    return sat;
-}
-
-static double lat_planes()
-{
-    double lat = 0.7;
-    if (const char *e = getenv("VTI_LAT")) lat = atof(e);
-    return lat;
-}
-
-// HBM streaming efficiency falls when more than ~128 CTAs (per CTA-per-SM slot)
-// stream at once: tools/stream_probe_bulk.cu moves the step's 7R+2W mix at 7.10
-// TB/s with 110-128 CTAs but 6.90 TB/s with 148. eff(a) models that (0.97 at 148)
-// for the fp32 kernels (C3 183 -> 190, C4 179 -> 191, C5 182 -> 187 Gpoints/s with
-// a 128-CTA grid); the slower fp64 CTAs need the full grid to saturate HBM, so
-// their plans keep it (measured: capping costs them 2-4 %).
-static constexpr int CONC = 128;
-static double conc_eff(long a, int ctas_per_sm)
-{
-    const double over = (double)a / ctas_per_sm - CONC;
-    return over > 0 ? 1.0 - 0.0015 * over : 1.0;
-}
-
-struct Sched {
-    int zchunk;   // planes per work item
-    int cap;      // CTAs launched at most (<= slots)
-};
-
-static Sched plan_sched(int nz, int rz, int tiles, int slots, int ctas_per_sm, double sat, int tune_zchunk,
-                        bool conc_model)
-{
-    if (tiles <= 0 || slots <= 0) return {nz, std::max(slots, 1)};
-    sat = std::max(1.0, std::min(sat, (double)slots));
-    const double lat = lat_planes();
-    double best = 1e300;
-    Sched out{tune_zchunk > 0 ? std::min(tune_zchunk, nz) : nz, slots};
-    const int caps[2] = {slots, std::min(slots, CONC * ctas_per_sm)};
-    for (int ci = 0; ci < (conc_model ? 2 : 1); ++ci) {
-        const int cap = caps[ci];
-        if (ci == 1 && cap == slots) break;
-        for (int nzc = 1; nzc <= nz; ++nzc) {
-            const int zc = (nz + nzc - 1) / nzc;
-            if ((nz + zc - 1) / zc != nzc) continue;   // same chunking as a smaller nzc
-            if (tune_zchunk > 0 && zc != std::min(tune_zchunk, nz)) continue;
-            const long items = (long)tiles * nzc;
-            const long full = items / cap, last = items % cap;
-            const double prime = 1.0 + (8.0 * rz) / (36.0 * zc);
-            const double lat_round = (zc + 2.0 * rz) * lat;
-            auto round_cost = [&](long a) {
-                const double eff = conc_model ? conc_eff(a, ctas_per_sm) : 1.0;
-                return std::max(zc * prime * a / (std::min<double>(a, sat) * eff), lat_round);
-            };
-            double cost = (double)full * round_cost(cap);
-            if (last) cost += round_cost(last);
-            if (cost < best * (1.0 - 1e-3)) {
-                best = cost;
-                out = {zc, cap};
-            }
-        }
-    }
-    return out;
-}
-
-// nranks > 1: the edge launch covers every tile row that intersects the first
-// or the last R_xy rows of the slab (the rows the neighbours receive), i.e.
-// tile rows [0, e1) and [e2, nty); the interior launch covers [e1, e2).
-static void plan_edge_rows(int nty, int r, int ty, int nyl, int &e1, int &e2)
-{
-    e1 = std::min(nty, (r + ty - 1) / ty);
-    e2 = std::max(e1, std::min(nty, (nyl - r) / ty));
-}
-
-// CTA slots of a launch: resident CTAs, optionally capped (env VTI_MAXGRID, experiments)
-static int slots(const vti_s *h)
-{
-    static const int cap = getenv("VTI_MAXGRID") ? atoi(getenv("VTI_MAXGRID")) : 0;
-    const int n = h->sms * h->ctas_per_sm;
-    return cap > 0 ? std::min(n, cap) : n;
-}
-
-static Sched choose_sched(const vti_s *h, int tiles)
-{
-    return plan_sched(h->cfg.nz, h->RZ, tiles, slots(h), h->ctas_per_sm, sat_ctas(h->ctas_per_sm), h->tune_zchunk,
-                      h->es == 4);
-}
-
-static void edge_rows(const vti_s *h, int &e1, int &e2) { plan_edge_rows(h->nty, h->R, h->TY, h->nyl, e1, e2); }
-
-// Default schedule: one launch over all tile rows (single slab), or an edge
-// launch plus an interior launch (nranks > 1).
-static void choose_schedule(vti_s *h)
-{
-    int e1, e2;
-    edge_rows(h, e1, e2);
-    const int edge_rows = e1 + (h->nty - e2), inner_rows = e2 - e1;
-    const Sched a = choose_sched(h, h->ntx * h->nty), e = choose_sched(h, h->ntx * edge_rows),
-                i = choose_sched(h, h->ntx * inner_rows);
-    h->zchunk = a.zchunk;
-    h->cap = a.cap;
-    h->zchunk_edge = e.zchunk;
-    h->cap_edge = e.cap;
-    h->zchunk_inner = i.zchunk;
-    h->cap_inner = i.cap;
-    h->nzc = (h->cfg.nz + h->zchunk - 1) / h->zchunk;
-    const long items = (long)h->ntx * h->nty * h->nzc;
-    h->grid = (int)std::min<long>(items, (long)h->cap);
-}
-
-static int precision_bits(const vti_config *c) { return c->precision == 0 ? 32 : c->precision; }
-
-static vti_status check_cfg(const vti_config *c)
-{
-    if (!c) return VTI_E_PARAM;
-    if (c->r_xy < 1 || c->r_z < 1 || c->r_xy > MAX_R || !(c->h > 0) || !(c->dt > 0) || c->damp_width < 0)
-        return VTI_E_PARAM;
-    if (precision_bits(c) != 32 && precision_bits(c) != 64) return VTI_E_PARAM;
-    if (c->nx < 1 || c->ny < 1 || c->nz < 1) return VTI_E_GEOMETRY;
-    if (c->nz < 2 * c->r_z + 1) return VTI_E_GEOMETRY;   // too few planes
-    if (c->damp_width > 0 && (2 * c->damp_width >= c->nx || 2 * c->damp_width >= c->ny || 2 * c->damp_width >= c->nz))
-        return VTI_E_GEOMETRY;
-    if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return VTI_E_PARAM;
-    if (c->nranks > 1 && c->ny / c->nranks < c->r_xy) return VTI_E_GEOMETRY;   // slab thinner than the halo
-    return VTI_OK;
-}
-
 // Device pointers handed in or out by the caller may have been produced or be
 // consumed on another stream: order the library's stream after all prior work.
 static vti_status order_after_caller(vti_s *h)
@@ -580,7 +226,6 @@ static vti_status order_after_caller(vti_s *h)
     return VTI_OK;
 }
 
-static int launch_grid(const vti_s *h) { return 4 * h->sms; }
 
 // Typed launch helpers for the auxiliary kernels.
 template <typename T>
@@ -605,29 +250,6 @@ static void i2u(vti_s *h, const void *src, void *dst, int nk, int k0)
     if (h->es == 8) launch_i2u<double>(h, src, dst, nk, k0);
     else launch_i2u<float>(h, src, dst, nk, k0);
 }
-template <typename T>
-static void launch_pack(vti_s *h, const void *buf, void *out, int row0, cudaStream_t st)
-{
-    k_pack_rows<T><<<launch_grid(h), 256, 0, st>>>((const T *)buf, (T *)out, row0, h->R, h->cfg.nz, h->cfg.nx, h->ys,
-                                                   h->zs);
-}
-template <typename T>
-static void launch_unpack(vti_s *h, const void *in, void *buf, int row0, cudaStream_t st)
-{
-    k_unpack_rows<T><<<launch_grid(h), 256, 0, st>>>((const T *)in, (T *)buf, row0, h->R, h->cfg.nz, h->cfg.nx, h->ys,
-                                                     h->zs);
-}
-static void pack(vti_s *h, const void *buf, void *out, int row0, cudaStream_t st)
-{
-    if (h->es == 8) launch_pack<double>(h, buf, out, row0, st);
-    else launch_pack<float>(h, buf, out, row0, st);
-}
-static void unpack(vti_s *h, const void *in, void *buf, int row0, cudaStream_t st)
-{
-    if (h->es == 8) launch_unpack<double>(h, in, buf, row0, st);
-    else launch_unpack<float>(h, in, buf, row0, st);
-}
-
 // ============================================================ C ABI
 extern "C" {
 
@@ -649,54 +271,6 @@ const char *vti_status_string(vti_status s)
     case VTI_E_UNSUPPORTED: return "unsupported radius pair";
     }
     return "unknown status";
-}
-
-vti_status vti_slab(const vti_config *cfg, int32_t *y0, int32_t *ny_local)
-{
-    if (!cfg || !y0 || !ny_local || cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks || cfg->ny < 1)
-        return VTI_E_PARAM;
-    const int base = cfg->ny / cfg->nranks, extra = cfg->ny % cfg->nranks;
-    *ny_local = base + (cfg->rank < extra ? 1 : 0);
-    *y0 = cfg->rank * base + std::min(cfg->rank, extra);
-    return VTI_OK;
-}
-
-vti_status vti_plan(const vti_config *cfg, int32_t tile_y, int32_t sms, int32_t ctas_per_sm, vti_plan_info *out)
-{
-    if (!cfg || !out || tile_y < 1 || sms < 1 || ctas_per_sm < 1) return VTI_E_PARAM;
-    vti_status st = check_cfg(cfg);
-    if (st != VTI_OK) return st;
-    vti_slab(cfg, &out->y0, &out->ny_local);
-    out->ntx = (cfg->nx + TX - 1) / TX;
-    out->nty = (out->ny_local + tile_y - 1) / tile_y;
-    int e1, e2;
-    plan_edge_rows(out->nty, cfg->r_xy, tile_y, out->ny_local, e1, e2);
-    out->edge_lo = e1;
-    out->edge_hi = e2;
-    const int slots = sms * ctas_per_sm;
-    const double sat = sat_ctas(ctas_per_sm);
-    const bool f32 = precision_bits(cfg) == 32;
-    const Sched a = plan_sched(cfg->nz, cfg->r_z, out->ntx * out->nty, slots, ctas_per_sm, sat, 0, f32);
-    out->zchunk = a.zchunk;
-    out->zchunk_edge =
-        plan_sched(cfg->nz, cfg->r_z, out->ntx * (e1 + out->nty - e2), slots, ctas_per_sm, sat, 0, f32).zchunk;
-    out->zchunk_inner = plan_sched(cfg->nz, cfg->r_z, out->ntx * (e2 - e1), slots, ctas_per_sm, sat, 0, f32).zchunk;
-    const long items = (long)out->ntx * out->nty * ((cfg->nz + out->zchunk - 1) / out->zchunk);
-    out->items = (int32_t)items;
-    out->grid = (int32_t)std::min<long>(items, a.cap);
-    return VTI_OK;
-}
-
-vti_status vti_nccl_unique_id(void *out128)
-{
-    if (!out128) return fail(nullptr, VTI_E_PARAM, "NULL output");
-    NcclApi &api = nccl();
-    if (!api.ok) return fail(nullptr, VTI_E_COMM, "%s", api.err.c_str());
-    ncclUniqueId id;
-    ncclResult_t r = api.GetUniqueId(&id);
-    if (r != ncclSuccess) return fail(nullptr, VTI_E_COMM, "ncclGetUniqueId: %s", api.GetErrorString(r));
-    memcpy(out128, &id, sizeof id);
-    return VTI_OK;
 }
 
 vti_status vti_destroy(vti_t h)
@@ -1185,175 +759,18 @@ static vti_status launch_rows(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, in
                       : launch_rows_t<float>(h, tr0, ntr0, tr1, ntr1, zchunk, cap);
 }
 
-static vti_status launch_edge(vti_s *h)
+vti_status launch_edge(vti_s *h)
 {
     int e1, e2;
     edge_rows(h, e1, e2);
     return launch_rows(h, 0, e1, e2, h->nty - e2, h->zchunk_edge, h->cap_edge);
 }
 
-static vti_status launch_interior(vti_s *h)
+vti_status launch_interior(vti_s *h)
 {
     int e1, e2;
     edge_rows(h, e1, e2);
     return launch_rows(h, e1, e2 - e1, 0, 0, h->zchunk_inner, h->cap_inner);
-}
-
-// ---- halo transport of p (y-slab decomposition)
-// Halo'd row index: [0, R) rows from rank-1, [R, R+nyl) own rows, [R+nyl, 2R+nyl) rows from rank+1.
-static size_t halo_elems(const vti_s *h) { return (size_t)h->cfg.nz * h->R * h->cfg.nx; }
-
-// On the main stream: pack this rank's boundary rows of buffer b into sbuf[0] (-> rank-1) and sbuf[1] (-> rank+1).
-static vti_status pack_send(vti_s *h, int b)
-{
-    const int r = h->cfg.rank, nr = h->cfg.nranks;
-    if (r > 0) pack(h, h->pbuf[b], h->sbuf[0], h->R, h->stream);
-    if (r < nr - 1) pack(h, h->pbuf[b], h->sbuf[1], h->nyl, h->stream);
-    CU(h, cudaGetLastError());
-    return VTI_OK;
-}
-
-// On the comm stream: unpack rbuf[0] (from rank-1) and rbuf[1] (from rank+1) into the halo rows of buffer b.
-static vti_status unpack_recv(vti_s *h, int b)
-{
-    const int r = h->cfg.rank, nr = h->cfg.nranks;
-    if (r > 0) unpack(h, h->rbuf[0], h->pbuf[b], 0, h->comm);
-    if (r < nr - 1) unpack(h, h->rbuf[1], h->pbuf[b], h->nyl + h->R, h->comm);
-    CU(h, cudaGetLastError());
-    return VTI_OK;
-}
-
-// NCCL transport on the comm stream after ev_edge, then unpack; records ev_comm.
-static vti_status exchange_nccl(vti_s *h, int b)
-{
-    NcclApi &api = nccl();
-    CU(h, cudaStreamWaitEvent(h->comm, h->ev_edge, 0));
-    const size_t cnt = halo_elems(h);
-    const ncclDataType_t dt = h->es == 8 ? ncclFloat64 : ncclFloat32;
-    const int r = h->cfg.rank, nr = h->cfg.nranks;
-    ncclResult_t e = api.GroupStart();
-    if (e == ncclSuccess && r > 0) {
-        e = api.Send(h->sbuf[0], cnt, dt, r - 1, h->comm_nccl, h->comm);
-        if (e == ncclSuccess) e = api.Recv(h->rbuf[0], cnt, dt, r - 1, h->comm_nccl, h->comm);
-    }
-    if (e == ncclSuccess && r < nr - 1) {
-        e = api.Send(h->sbuf[1], cnt, dt, r + 1, h->comm_nccl, h->comm);
-        if (e == ncclSuccess) e = api.Recv(h->rbuf[1], cnt, dt, r + 1, h->comm_nccl, h->comm);
-    }
-    ncclResult_t e2 = api.GroupEnd();
-    if (e != ncclSuccess || e2 != ncclSuccess)
-        return fail(h, VTI_E_COMM, "NCCL halo exchange: %s", api.GetErrorString(e != ncclSuccess ? e : e2));
-    vti_status s = unpack_recv(h, b);
-    if (s != VTI_OK) return s;
-    CU(h, cudaEventRecord(h->ev_comm, h->comm));
-    return VTI_OK;
-}
-
-// Fused peer-memory transport (no NCCL, no pack/copy/unpack): the edge launch
-// itself stores p^{n+1} of this slab's first / last R rows into rank-1's top /
-// rank+1's bottom halo rows through peer pointers (NVLink; the neighbours' own
-// buffers in a local group, CUDA-IPC mappings across processes), so the halo
-// travels tile by tile while the edge tiles are computed. Publication j is the
-// halo of the level the next step reads; flags[] are monotone counters written
-// by the neighbours with cuStreamWriteValue32 (which fences the kernel's peer
-// stores before the flag) and waited on with cuStreamWaitValue32, all on the
-// main stream:
-//   before the edge launch that consumes publication j:
-//     DATA >= j    the neighbours' rows of this level are in our halo
-//     ACK  >= j-1  the neighbours have read the halo we are about to overwrite
-//                  (publication j+1 lands in the buffer parity of j-1)
-//   after it: the neighbours' ACK = j (only the edge launch reads halo rows)
-//             and DATA = j+1.
-// Enqueue-order rule: streams share a small pool of in-order hardware channels,
-// so a value-wait may only wait on a write ENQUEUED EARLIER (the rule that makes
-// event waits safe); a local group therefore enqueues every handle's step j
-// writes before any handle's step j+1 waits, and splits a re-publication into
-// a release half and a publish half.
-enum { F_DATA_LO = 0, F_DATA_HI = 1, F_ACK_LO = 2, F_ACK_HI = 3 };
-
-static CUdeviceptr dev_ptr(const void *p) { return (CUdeviceptr)(uintptr_t)p; }
-static bool has_side(const vti_s *h, int side) { return side == 0 ? h->cfg.rank > 0 : h->cfg.rank < h->cfg.nranks - 1; }
-
-static vti_status flag_wait(vti_s *h, int idx, unsigned int v, bool remote_data)
-{
-    const StreamMemOps &ops = stream_mem_ops();
-    if (!ops.wait) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
-    unsigned fl = CU_STREAM_WAIT_VALUE_GEQ;
-    if (remote_data && h->flush_remote) fl |= CU_STREAM_WAIT_VALUE_FLUSH;
-    if (ops.wait((CUstream)h->stream, dev_ptr(h->flags + idx), v, fl) != CUDA_SUCCESS)
-        return fail(h, VTI_E_COMM, "cuStreamWaitValue32 failed");
-    return VTI_OK;
-}
-
-// the neighbour on `side` sees flag `idx` (its own numbering) become v
-static vti_status flag_write(vti_s *h, int side, int idx, unsigned int v)
-{
-    const StreamMemOps &ops = stream_mem_ops();
-    if (!ops.write) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
-    if (ops.write((CUstream)h->stream, dev_ptr(h->peer_flags[side] + idx), v, CU_STREAM_WRITE_VALUE_DEFAULT) !=
-        CUDA_SUCCESS)
-        return fail(h, VTI_E_COMM, "cuStreamWriteValue32 failed");
-    return VTI_OK;
-}
-
-static vti_status peer_pre_step(vti_s *h)
-{
-    const unsigned int j = h->xseq;
-    vti_status s;
-    for (int side = 0; side < 2; ++side) {
-        if (!has_side(h, side)) continue;
-        if ((s = flag_wait(h, side == 0 ? F_DATA_LO : F_DATA_HI, j, true)) != VTI_OK) return s;
-        if (j >= 1 && (s = flag_wait(h, side == 0 ? F_ACK_LO : F_ACK_HI, j - 1, false)) != VTI_OK) return s;
-    }
-    return VTI_OK;
-}
-
-static vti_status peer_post_edge(vti_s *h)
-{
-    const unsigned int j = h->xseq;
-    vti_status s;
-    for (int side = 0; side < 2; ++side) {
-        if (!has_side(h, side)) continue;
-        if ((s = flag_write(h, side, side == 0 ? F_ACK_HI : F_ACK_LO, j)) != VTI_OK) return s;
-        if ((s = flag_write(h, side, side == 0 ? F_DATA_HI : F_DATA_LO, j + 1)) != VTI_OK) return s;
-    }
-    h->xseq = j + 1;
-    return VTI_OK;
-}
-
-// Re-publication of the current level (state set by the caller, vti_reverse). Release
-// half: everything published so far is consumed or abandoned (stream-ordered after
-// this rank's last read of its halo).
-static vti_status peer_release(vti_s *h)
-{
-    vti_status s;
-    for (int side = 0; side < 2; ++side)
-        if (has_side(h, side) && (s = flag_write(h, side, side == 0 ? F_ACK_HI : F_ACK_LO, h->xseq)) != VTI_OK)
-            return s;
-    return VTI_OK;
-}
-
-// Publish half: once the neighbours released every earlier publication, copy this
-// rank's boundary rows of the current level into their halo rows (R contiguous
-// rows per plane on both sides: one 2-D copy per neighbour), then DATA.
-static vti_status peer_publish(vti_s *h)
-{
-    const unsigned int j = ++h->xseq;
-    vti_status s;
-    // [z][y][x]: R rows are contiguous within each plane; [y][z][x]: the R rows of every plane are one block
-    const size_t width = (size_t)h->R * h->ys * h->es;
-    const size_t height = h->layout_zyx ? (size_t)h->cfg.nz : 1;
-    for (int side = 0; side < 2; ++side) {
-        if (!has_side(h, side)) continue;
-        if ((s = flag_wait(h, side == 0 ? F_ACK_LO : F_ACK_HI, j - 1, false)) != VTI_OK) return s;
-        const char *src = (const char *)h->pbuf[h->cur] + (size_t)(side == 0 ? h->R : h->nyl) * h->ys * h->es;
-        const size_t spitch = h->layout_zyx ? (size_t)h->zs * h->es : width;
-        const size_t dpitch = h->layout_zyx ? (size_t)h->peer_zs[side] * h->es : width;
-        CU(h, cudaMemcpy2DAsync(h->peer_p[side][h->cur], dpitch, src, spitch, width, height, cudaMemcpyDefault,
-                                h->stream));
-        if ((s = flag_write(h, side, side == 0 ? F_DATA_HI : F_DATA_LO, j)) != VTI_OK) return s;
-    }
-    return VTI_OK;
 }
 
 static vti_status check_finite(vti_s *h)
@@ -1377,7 +794,7 @@ static vti_status check_finite(vti_s *h)
 
 // Gather the receivers' u^n (just written) into the next trace row; silently
 // stops when the capacity is reached (vti_get_traces reports the count).
-static vti_status record(vti_s *h)
+vti_status record(vti_s *h)
 {
     if (h->nrec == 0 || h->rec_steps >= h->rec_cap || h->suppress_src) return VTI_OK;   // not during autotune probes
     const int nf = (h->rec_mask & 1) + ((h->rec_mask >> 1) & 1);
@@ -1463,81 +880,6 @@ static vti_status get_traces(vti_s *h, int es, void *out)
 
 vti_status vti_get_traces(vti_t h, float *out) { return get_traces(h, 4, out); }
 vti_status vti_get_traces_f64(vti_t h, double *out) { return get_traces(h, 8, out); }
-
-// ---- multi-process fused peer transport over CUDA IPC
-struct IpcBlob {
-    uint32_t magic, version;
-    int32_t rank, nranks, nyl, nxp, R, es, zyx;
-    cudaIpcMemHandle_t pbuf[2], flags;
-};
-static_assert(sizeof(IpcBlob) <= VTI_IPC_BYTES, "IPC blob too large");
-static const uint32_t IPC_MAGIC = 0x56544932u;   // "VTI2"
-
-vti_status vti_ipc_export(vti_t h, void *out)
-{
-    if (!h || !out) return VTI_E_PARAM;
-    if (h->cfg.nranks < 2 || !h->flags) return fail(h, VTI_E_STATE, "vti_ipc_export needs nranks > 1");
-    CU(h, cudaSetDevice(h->cfg.device));
-    IpcBlob b;
-    memset(&b, 0, sizeof b);
-    b.magic = IPC_MAGIC;
-    b.version = VTI_ABI_VERSION;
-    b.rank = h->cfg.rank;
-    b.nranks = h->cfg.nranks;
-    b.nyl = h->nyl;
-    b.nxp = h->nxp;
-    b.R = h->R;
-    b.es = h->es;
-    b.zyx = h->layout_zyx;
-    CU(h, cudaIpcGetMemHandle(&b.pbuf[0], h->pbuf[0]));
-    CU(h, cudaIpcGetMemHandle(&b.pbuf[1], h->pbuf[1]));
-    CU(h, cudaIpcGetMemHandle(&b.flags, h->flags));
-    memset(out, 0, VTI_IPC_BYTES);
-    memcpy(out, &b, sizeof b);
-    return VTI_OK;
-}
-
-vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
-{
-    if (!h) return VTI_E_PARAM;
-    const int r = h->cfg.rank, nr = h->cfg.nranks;
-    if (nr < 2) return fail(h, VTI_E_STATE, "vti_ipc_connect needs nranks > 1");
-    if ((r > 0) != (lo != nullptr) || (r < nr - 1) != (hi != nullptr))
-        return fail(h, VTI_E_PARAM, "pass the blob of rank-1 (lo) and rank+1 (hi), NULL at the ends");
-    const StreamMemOps &ops = stream_mem_ops();
-    if (!ops.wait || !ops.write) return fail(h, VTI_E_COMM, "stream memory operations unavailable");
-    CU(h, cudaSetDevice(h->cfg.device));
-    const void *blobs[2] = {lo, hi};
-    for (int side = 0; side < 2; ++side) {
-        if (!blobs[side]) continue;
-        IpcBlob b;
-        memcpy(&b, blobs[side], sizeof b);
-        if (b.magic != IPC_MAGIC || b.version != (uint32_t)VTI_ABI_VERSION || b.nranks != nr ||
-            b.rank != (side == 0 ? r - 1 : r + 1) || b.nxp != h->nxp || b.R != h->R || b.es != h->es ||
-            b.zyx != (int32_t)h->layout_zyx)
-            return fail(h, VTI_E_PARAM, "IPC blob of the wrong rank, job, geometry or library version");
-        void *pb[2] = {nullptr, nullptr}, *fl = nullptr;
-        for (int k = 0; k < 2; ++k) {
-            cudaError_t e = cudaIpcOpenMemHandle(&pb[k], b.pbuf[k], cudaIpcMemLazyEnablePeerAccess);
-            if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-            h->ipc_opened[3 * side + k] = pb[k];
-        }
-        cudaError_t e = cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess);
-        if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-        h->ipc_opened[3 * side + 2] = fl;
-        // rank-1: our first rows go to its top halo (row R + nyl); rank+1: our last rows to its row 0.
-        // Same layout on both sides, so the row stride is ours (h->ys); the plane stride is theirs.
-        const size_t row0 = side == 0 ? (size_t)b.R + b.nyl : 0;
-        for (int k = 0; k < 2; ++k) h->peer_p[side][k] = (char *)pb[k] + row0 * h->ys * (size_t)b.es;
-        h->peer_zs[side] = b.zyx ? (long long)(b.nyl + 2 * b.R) * b.nxp : (long long)b.nxp;
-        h->peer_flags[side] = (unsigned int *)fl;
-    }
-    h->peer = true;
-    h->group_mode = false;   // created with nccl_id = NULL; now a multi-process peer rank stepped by vti_step
-    return VTI_OK;
-}
-
-int32_t vti_halo_transport(vti_t h) { return !h ? -1 : h->cfg.nranks < 2 ? 0 : h->peer ? 2 : h->comm_nccl ? 1 : 0; }
 
 vti_status vti_reverse(vti_t h)
 {
@@ -1832,76 +1174,6 @@ vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms)
     CU(h, cudaEventRecord(h->ev_t1, h->stream));
     CU(h, cudaEventSynchronize(h->ev_t1));
     CU(h, cudaEventElapsedTime(ms, h->ev_t0, h->ev_t1));
-    return VTI_OK;
-}
-
-// Local group: the fused peer-memory transport between handles of one process
-// (peer pointers are the neighbours' own device buffers), the same protocol as the
-// multi-process CUDA-IPC form.
-static void group_connect(vti_t *hs, int n)
-{
-    for (int i = 0; i < n; ++i) {
-        vti_s *h = hs[i];
-        h->peer = true;
-        for (int side = 0; side < 2; ++side) {
-            const vti_s *nb = side == 0 ? (i > 0 ? hs[i - 1] : nullptr) : (i < n - 1 ? hs[i + 1] : nullptr);
-            for (int b = 0; b < 2; ++b)
-                h->peer_p[side][b] = !nb ? nullptr
-                                         : (char *)nb->pbuf[b] + (size_t)(side == 0 ? nb->R + nb->nyl : 0) * nb->ys * nb->es;
-            h->peer_zs[side] = nb ? nb->zs : 0;
-            h->peer_flags[side] = nb ? nb->flags : nullptr;
-        }
-    }
-}
-
-vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
-{
-    if (!hs || n < 1 || nsteps < 0) return VTI_E_PARAM;
-    for (int i = 0; i < n; ++i) {
-        if (!hs[i]) return VTI_E_PARAM;
-        if (hs[i]->cfg.nranks != n || hs[i]->cfg.rank != i)
-            return fail(hs[i], VTI_E_STATE, "group handle %d has rank %d / nranks %d", i, hs[i]->cfg.rank,
-                        hs[i]->cfg.nranks);
-        if (n > 1 && !hs[i]->group_mode) return fail(hs[i], VTI_E_STATE, "handle not created for local-group mode");
-        if (!hs[i]->model_set) return fail(hs[i], VTI_E_STATE, "model not set");
-        if (hs[i]->n != hs[0]->n) return fail(hs[i], VTI_E_STATE, "time indices differ inside the group");
-    }
-    if (n == 1) return vti_step(hs[0], nsteps);
-    for (int i = 0; i < n; ++i)
-        if (hs[i]->xseq != hs[0]->xseq || hs[i]->cur != hs[0]->cur)
-            return fail(hs[i], VTI_E_STATE, "halo publications or buffer parity differ inside the group");
-    group_connect(hs, n);
-    vti_status s;
-    bool dirty = false;
-    for (int i = 0; i < n; ++i) dirty |= hs[i]->halo_dirty;
-    if (dirty) {   // every release before any publish (enqueue-order rule)
-        for (int i = 0; i < n; ++i) {
-            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
-            if ((s = peer_release(hs[i])) != VTI_OK) return s;
-        }
-        for (int i = 0; i < n; ++i) {
-            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
-            if ((s = peer_publish(hs[i])) != VTI_OK) return s;
-            hs[i]->halo_dirty = false;
-        }
-    }
-    for (int it = 0; it < nsteps; ++it) {
-        for (int i = 0; i < n; ++i) {   // waits on the previous step's writes only
-            vti_s *h = hs[i];
-            CU(h, cudaSetDevice(h->cfg.device));
-            if ((s = peer_pre_step(h)) != VTI_OK) return s;
-            if ((s = launch_edge(h)) != VTI_OK) return s;
-            if ((s = peer_post_edge(h)) != VTI_OK) return s;
-        }
-        for (int i = 0; i < n; ++i) {
-            vti_s *h = hs[i];
-            CU(h, cudaSetDevice(h->cfg.device));
-            if ((s = launch_interior(h)) != VTI_OK) return s;
-            h->cur = 1 - h->cur;
-            h->n += h->dir;
-            if ((s = record(h)) != VTI_OK) return s;
-        }
-    }
     return VTI_OK;
 }
 

@@ -2,7 +2,7 @@
 
 The multi-process form of the transport cannot run on the single GPU of this
 environment, so its ordering logic is checked here on the CPU. The model
-replays, per rank, the operation sequence `vti_runtime.cu` enqueues on the
+replays, per rank, the operation sequence `vti_step` (vti_runtime.cu, vti_transport.cu) enqueues on the
 rank's stream:
 
   step consuming publication j  (peer_pre_step, launch_edge, peer_post_edge):
