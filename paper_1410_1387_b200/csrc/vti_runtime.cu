@@ -54,7 +54,7 @@ static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
     const KernelEntry *e;
-    for (int ty : {32, 30, 16, 15, 14})
+    for (int ty : {32, 30, 16, 15, 14, 12, 10, 8})
         for (int wp : {1, 0})
             for (int rpt : {1, 2})
                 for (int px : {4, 2})
