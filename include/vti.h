@@ -83,7 +83,7 @@ typedef struct {
     int32_t layout;         /* 0: internal [z][y][x] (default), 1: [y][z][x] (env VTI_LAYOUT=yzx) */
     int32_t tile_x, tile_y; /* CTA tile of the step kernel */
     int32_t rows_per_thread, producer_warp; /* step-kernel variant (see vti_set_variant) */
-    int32_t points_per_thread; /* consecutive x points per thread: 4, or 2 (fp64 double2 variants) */
+    int32_t points_per_thread; /* consecutive x points per thread: 4, or 2 (float2 / double2 variants) */
     int32_t zchunk;         /* planes per work item */
     int32_t grid;           /* CTAs launched per step (persistent) */
     int32_t work_items;     /* tiles x z-chunks per step */
@@ -279,10 +279,10 @@ vti_status vti_query(vti_t h, vti_info *info);
 /* Tuning knobs (0 = library default): planes per work item, CTAs per SM. */
 vti_status vti_set_tuning(vti_t h, int32_t zchunk, int32_t ctas_per_sm);
 
-/* Select a compiled step-kernel variant: tile height (32, 30, 16, 15 or 14
- * rows), dedicated TMA producer warp (1) or in-line producer (0), rows per
- * thread (1 or 2), consecutive x points per thread (4, or 2 for fp64); -1 =
- * any. The arithmetic (and so every result bit) is identical across variants.
+/* Select a compiled step-kernel variant: tile height (32, 30, 16, 15, 14, 10
+ * or 8 rows, per precision and radius pair), dedicated TMA producer warp (1) or
+ * in-line producer (0), rows per thread (1 or 2), consecutive x points per
+ * thread (4, or 2: float2 / double2); -1 = any. The arithmetic (and so every result bit) is identical across variants.
  * Errors: UNSUPPORTED if no such variant is compiled for (precision, r_xy, r_z). */
 vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp, int32_t rows_per_thread,
                            int32_t points_per_thread);
