@@ -54,3 +54,15 @@ def test_native_arm_line():
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
     assert d["gpu_launches"] >= 40
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args,dtype,bpp", [(("--config", "C1", "--precision", "64"), "f64", 72),
+                                            (("--config", "N1"), "f32", 36)])
+def test_native_arm_other_workloads(args, dtype, bpp):
+    d = run_bench(*args, "--steps", "20", "--warmup", "3", "--no-e2e", "--no-cpu-baseline")
+    assert BASE_KEYS <= set(d) and d["value"] > 0 and d["dtype"] == dtype
+    assert d["config"]["bytes_per_point"] == bpp
+    assert d["config"]["workload"].startswith(args[1])
+    assert d["roofline"]["peak"] > 0 and d["roofline"]["achieved"] > 0
+    assert d["gpu_launches"] >= 20
