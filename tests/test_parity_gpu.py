@@ -234,7 +234,7 @@ def test_check_every_detects_instability():
 
 @pytest.mark.parametrize("nranks", [2, 3])
 def test_local_group_slabs_bitwise_equal_single(nranks):
-    """y-slab decomposition with device-to-device halo copies == one slab, bitwise."""
+    """y-slab decomposition (local group, fused peer-store halo transport) == one slab, bitwise."""
     from paper_1410_1387_b200 import VTI, group_step
     cfg = small_cfg(70, 75, 40, 4, 4, damp=6, src=(30, 37, 20))
     if nranks == 2:
