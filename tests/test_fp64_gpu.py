@@ -121,3 +121,11 @@ def test_fp64_local_group_equals_single():
         assert np.array_equal(np.concatenate([p[f] for p in parts], axis=1), g[f])
     for h in hs:
         h.close()
+
+
+@pytest.mark.parametrize("r,rz", [(4, 4), (12, 8)])
+def test_fp64_thin_grid_minimum_depth(r, rz):
+    cfg = cfg_of(5, 3, 2 * rz + 1, r, rz, damp=0, src=(2, 1, rz))
+    model, st = inputs(cfg)
+    g, o = run64(cfg, 4, st, model)
+    check(g, o)

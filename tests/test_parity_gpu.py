@@ -430,3 +430,24 @@ def test_graph_replays_equal_direct_launches(monkeypatch):
     for a, b in zip(*out):
         assert np.array_equal(a, b)
     assert np.abs(out[0][0]).max() > 0
+
+
+@pytest.mark.parametrize("r,rz", [(8, 4), (6, 6), (12, 8)])
+@pytest.mark.parametrize("shape", [(1, 1, None), (5, 3, None), (70, 2, None), (3, 37, None)])
+def test_degenerate_thin_grids_every_radius(r, rz, shape):
+    """Thin grids at the smallest legal depth nz = 2 R_z + 1 for every compiled radius pair
+    (the default variant of the pair, including the float2 x 2-row (12,8) mapping)."""
+    nx, ny, _ = shape
+    nz = 2 * rz + 1
+    cfg = small_cfg(nx, ny, nz, r, rz, damp=0, src=(nx // 2, ny // 2, nz // 2))
+    st = random_state(cfg, amp=1e-2)
+    g, o = run_both(cfg, 5, state=st, model=random_model(cfg))
+    assert_parity(g, o)
+
+
+def test_widest_damping_band():
+    """2W = extent - 1 on the smallest axis: every point of that axis is inside the band."""
+    cfg = small_cfg(61, 45, 23, 4, 4, damp=11, src=(30, 22, 11))
+    st = random_state(cfg, amp=1e-3)
+    g, o = run_both(cfg, 6, state=st, model=random_model(cfg))
+    assert_parity(g, o)
