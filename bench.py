@@ -430,6 +430,7 @@ def run_native(args):
             "clocks": clocks,
             "cpu_baseline": cpu,
             "schedule": {k: info[k] for k in ("tile_x", "tile_y", "producer_warp", "rows_per_thread", "points_per_thread",
+                                              "small_kernel",
                                               "zchunk", "grid", "work_items")},
         }
         print(json.dumps(line), flush=True)

@@ -84,6 +84,7 @@ typedef struct {
     int32_t tile_x, tile_y; /* CTA tile of the step kernel */
     int32_t rows_per_thread, producer_warp; /* step-kernel variant (see vti_set_variant) */
     int32_t points_per_thread; /* consecutive x points per thread: 4, or 2 (float2 / double2 variants) */
+    int32_t small_kernel;   /* 1: small-grid kernel (one CTA per tile-plane item, all loads at once) */
     int32_t zchunk;         /* planes per work item */
     int32_t grid;           /* CTAs launched per step (persistent) */
     int32_t work_items;     /* tiles x z-chunks per step */

@@ -67,7 +67,7 @@ class Info(C.Structure):
     _fields_ = [
         ("y0", C.c_int32), ("ny_local", C.c_int32), ("nx_pad", C.c_int32), ("layout", C.c_int32),
         ("tile_x", C.c_int32), ("tile_y", C.c_int32), ("rows_per_thread", C.c_int32), ("producer_warp", C.c_int32),
-        ("points_per_thread", C.c_int32), ("zchunk", C.c_int32), ("grid", C.c_int32),
+        ("points_per_thread", C.c_int32), ("small_kernel", C.c_int32), ("zchunk", C.c_int32), ("grid", C.c_int32),
         ("work_items", C.c_int32), ("launches_per_step", C.c_int32),
         ("device_bytes", C.c_int64), ("time_index", C.c_int64),
     ]

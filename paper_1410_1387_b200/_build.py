@@ -11,7 +11,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libvti.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("vti_runtime.cu", "vti_schedule.cu", "vti_transport.cu")] + sorted(
     os.path.join(CSRC, "variants", f) for f in os.listdir(os.path.join(CSRC, "variants")) if f.endswith(".cu"))
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("vti_kernel.cuh", "vti_entry.cuh", "vti_variants.h",
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("vti_kernel.cuh", "vti_small.cuh", "vti_entry.cuh", "vti_variants.h",
                                                    "vti_internal.h")] + [
     os.path.join(ROOT, "include", "vti.h")]
 

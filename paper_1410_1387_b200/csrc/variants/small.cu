@@ -1,0 +1,20 @@
+// Small-grid step kernels (vti_small.cuh), fp32, 16-row tiles: the tile height the
+// runtime picks for grids of at most 4 M points, for the radius pairs whose default
+// mapping has 4 x points per thread.
+#include "../vti_entry.cuh"
+#include "../vti_small.cuh"
+
+template <typename T, int R, int RZ, int TY>
+static SmallEntry small_entry()
+{
+    using namespace vti;
+    return SmallEntry{(int)sizeof(T), R, RZ, TY, (const void *)vti_small_kernel<T, R, RZ, TY>,
+                      SmallCfg<T, R, RZ, TY>::SMEM, SmallCfg<T, R, RZ, TY>::THREADS};
+}
+
+SmallTable vti_small_kernels()
+{
+    static const SmallEntry t[] = {small_entry<float, 4, 4, 16>(), small_entry<float, 8, 4, 16>(),
+                                   small_entry<float, 6, 6, 16>()};
+    return SmallTable{t, (int)(sizeof t / sizeof t[0])};
+}

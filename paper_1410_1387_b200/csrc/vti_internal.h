@@ -23,6 +23,7 @@
 
 #include "vti.h"
 #include "vti_kernel.cuh"
+#include "vti_small.cuh"
 #include "vti_variants.h"
 
 using namespace vti;
@@ -86,6 +87,9 @@ struct vti_s {
     bool align_rounds = true;                 // env VTI_ALIGN=0 disables
     int64_t device_bytes = 0;
     CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
+    CUtensorMap tm_qcol[2];                   // q^n column views (box depth 2 R_z + 1) for the small-grid kernel
+    const SmallEntry *small = nullptr;        // small-grid kernel in use (single slab, 1-plane items), or NULL
+    bool explicit_variant = false;            // env VTI_TY/WP/RPT/PX or vti_set_variant / vti_autotune chose K
     double cxy[MAX_R + 1] = {0};              // w^xy / h^2 in double; rounded to T at launch (reading c3)
     int cur = 0;                              // pbuf[cur], qbuf[cur] hold u^n
     int64_t n = 0;                            // time index

@@ -50,6 +50,14 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, 
     return nullptr;
 }
 
+static const SmallEntry *find_small(int esize, int r, int rz, int ty)
+{
+    static const SmallTable t = vti_small_kernels();
+    for (int i = 0; i < t.n; ++i)
+        if (t.e[i].esize == esize && t.e[i].r == r && t.e[i].rz == rz && t.e[i].ty == ty) return &t.e[i];
+    return nullptr;
+}
+
 static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
@@ -202,13 +210,13 @@ static bool is_device_ptr(const void *p)
 
 // 3-D tensor map over (x, y, z) of an array with this handle's strides.
 static vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx, int by,
-                         CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B)
+                         CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B, int bz = 1)
 {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     cuuint64_t dims[3] = {(cuuint64_t)h->cfg.nx, (cuuint64_t)rows, (cuuint64_t)h->cfg.nz};
     cuuint64_t strides[2] = {(cuuint64_t)(h->ys * h->es), (cuuint64_t)(h->zs * h->es)};
-    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1u};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
     cuuint32_t estr[3] = {1u, 1u, 1u};
     const CUtensorMapDataType dt = h->es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     CUresult r = enc(tm, dt, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -361,6 +369,20 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
     if ((s = encode(h, &h->tm_vx, h->in(h->vx2), h->nyl, TX, h->TY)) != VTI_OK) return s;
     if ((s = encode(h, &h->tm_vn, h->in(h->vn2), h->nyl, TX, h->TY)) != VTI_OK) return s;
     if ((s = encode(h, &h->tm_vz, h->in(h->vz2), h->nyl, TX, h->TY)) != VTI_OK) return s;
+
+    // small-grid kernel (vti_small.cuh): single slab, fp32, plans of 1-plane items, default variant
+    h->small = nullptr;
+    static const bool small_on = !getenv("VTI_SMALL") || atoi(getenv("VTI_SMALL")) != 0;
+    const SmallEntry *se = find_small(h->es, h->R, h->RZ, h->TY);
+    if (small_on && se && !h->explicit_variant && h->cfg.nranks == 1 && h->zchunk == 1 && h->layout_zyx) {
+        const int NQ = 2 * h->RZ + 1;
+        for (int b = 0; b < 2; ++b)
+            if ((s = encode(h, &h->tm_qcol[b], h->q_int(b), h->nyl, TX, h->TY, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            NQ)) != VTI_OK)
+                return s;
+        CU(h, cudaFuncSetAttribute(se->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, se->smem));
+        h->small = se;
+    }
     return VTI_OK;
 }
 
@@ -394,6 +416,7 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     if (const char *e = getenv("VTI_WP")) want_wp = atoi(e);
     if (const char *e = getenv("VTI_RPT")) want_rpt = atoi(e);
     if (const char *e = getenv("VTI_PX")) want_px = atoi(e);
+    h->explicit_variant = want_ty >= 0 || want_wp >= 0 || want_rpt >= 0 || want_px >= 0;
     h->K = find_kernel(h->es, h->R, h->RZ, want_ty, want_wp, want_rpt, want_px);
     if (!h->K) h->K = find_kernel(h->es, h->R, h->RZ, -1, -1);
     if (!h->K)
@@ -722,6 +745,22 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
     if (h->capturing) {   // graph node: the source sample comes from the graph's table
         P.s_table = (const T *)h->s_graph;
         P.s_index = h->capture_index;
+    }
+    if (h->small && zchunk == 1 && tr0 == 0 && ntr0 == h->nty && ntr1 == 0) {
+        // small-grid kernel: one CTA per (tile, plane) item, every load of the item at once
+        SmallParams<T> S;
+        S.P = P;
+        S.P.sync_ctr = nullptr;
+        S.P.sync_base = 0;
+        S.tm_qcol = h->tm_qcol[h->cur];
+        cudaLaunchConfig_t sl = {};
+        sl.gridDim = dim3(P.items);
+        sl.blockDim = dim3(h->small->threads);
+        sl.dynamicSmemBytes = h->small->smem;
+        sl.stream = h->stream;
+        void *sargs[] = {&S};
+        CU(h, cudaLaunchKernelExC(&sl, h->small->fn, sargs));
+        return VTI_OK;
     }
     const int grid = std::min(P.items, cap > 0 ? std::min(cap, slots(h)) : slots(h));
     const int rounds = (P.items + grid - 1) / grid;
@@ -1203,8 +1242,9 @@ vti_status vti_query(vti_t h, vti_info *info)
     info->rows_per_thread = h->K->rpt;
     info->producer_warp = h->K->wp;
     info->points_per_thread = h->K->px;
+    info->small_kernel = h->small != nullptr;
     info->zchunk = h->zchunk;
-    info->grid = std::min(h->ntx * h->nty * h->nzc, h->cap);
+    info->grid = h->small ? h->ntx * h->nty * h->nzc : std::min(h->ntx * h->nty * h->nzc, h->cap);
     info->work_items = h->ntx * h->nty * h->nzc;
     if (h->cfg.nranks > 1) {   // edge + interior step kernels (+ pack and unpack per neighbour with NCCL)
         const int neighbours = (h->cfg.rank > 0) + (h->cfg.rank < h->cfg.nranks - 1);
@@ -1240,6 +1280,7 @@ vti_status vti_set_variant(vti_t h, int32_t tile_y, int32_t producer_warp, int32
                     h->R, h->RZ, tile_y, producer_warp, rows_per_thread, points_per_thread);
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaStreamSynchronize(h->stream));
+    h->explicit_variant = true;   // the caller picked this kernel: no small-grid substitution
     return select_variant(h, K);
 }
 
@@ -1258,6 +1299,7 @@ vti_status vti_autotune(vti_t h, int32_t probe_steps, vti_tune_result *out)
     const KernelEntry *best_k = keep;
     int best_zc = 0, ncand = 0;
     h->suppress_src = true;   // zero state, no injection: every probe step leaves u == 0
+    h->explicit_variant = true;   // autotune chooses among the compiled step-kernel variants
     for (const KernelEntry *K : all_kernels(h->es, h->R, h->RZ)) {
         h->tune_zchunk = 0;
         vti_status s = select_variant(h, K);

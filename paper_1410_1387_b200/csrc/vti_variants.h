@@ -28,3 +28,15 @@ VariantTable vti_variants_f32_r12();   // (12,8)
 VariantTable vti_variants_f64_r48();   // (4,4), (8,4)
 VariantTable vti_variants_f64_r6();    // (6,6)
 VariantTable vti_variants_f64_r12();   // (12,8)
+
+// Small-grid kernels (vti_small.cuh): one CTA per (tile, plane), all loads of the item at once.
+struct SmallEntry {
+    int esize, r, rz, ty;
+    const void *fn;
+    int smem, threads;
+};
+struct SmallTable {
+    const SmallEntry *e;
+    int n;
+};
+SmallTable vti_small_kernels();

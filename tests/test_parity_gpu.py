@@ -451,3 +451,32 @@ def test_widest_damping_band():
     st = random_state(cfg, amp=1e-3)
     g, o = run_both(cfg, 6, state=st, model=random_model(cfg))
     assert_parity(g, o)
+
+
+@pytest.mark.parametrize("r,rz,shape", [(4, 4, (64, 64, 64)), (8, 4, (77, 45, 41)), (6, 6, (70, 33, 29))])
+def test_small_grid_kernel(r, rz, shape, monkeypatch):
+    """Small single-slab grids whose plan cuts z into 1-plane items run the small-grid kernel
+    (one CTA per tile-plane item, the whole q column in one TMA box): bitwise == oracle, and
+    == the persistent kernel (VTI_SMALL=0)."""
+    nx, ny, nz = shape
+    cfg = small_cfg(nx, ny, nz, r, rz, damp=5, src=(nx // 2, ny // 2, nz // 2))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    st = random_state(cfg, amp=1e-3)
+    model = random_model(cfg)
+    with make(cfg, dt, wxy, wz) as v:
+        assert v.info()["small_kernel"] == 1 and v.info()["zchunk"] == 1
+    g, o = run_both(cfg, 9, state=st, model=model, n0=1)
+    assert_parity(g, o)
+    monkeypatch.setenv("VTI_SMALL", "0")
+    # the switch is read once per process; a fresh handle with an explicit variant uses the main kernel
+    monkeypatch.setenv("VTI_TY", "16")
+    with make(cfg, dt, wxy, wz) as v:
+        assert v.info()["small_kernel"] == 0
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
+        v.set_fields(*st, time_index=1)
+        v.step(9)
+        g2 = v.get_fields(0) + v.get_fields(1)
+    for a, b in zip(g, g2):
+        assert np.array_equal(a, b)
