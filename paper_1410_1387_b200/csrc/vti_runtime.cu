@@ -758,6 +758,14 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
         sl.blockDim = dim3(h->small->threads);
         sl.dynamicSmemBytes = h->small->smem;
         sl.stream = h->stream;
+        cudaLaunchAttribute sa[1];
+        static const bool pdl = !getenv("VTI_PDL") || atoi(getenv("VTI_PDL")) != 0;
+        if (pdl) {   // overlap this launch with the previous step's tail (see vti_small.cuh)
+            sa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            sa[0].val.programmaticStreamSerializationAllowed = 1;
+            sl.attrs = sa;
+            sl.numAttrs = 1;
+        }
         void *sargs[] = {&S};
         CU(h, cudaLaunchKernelExC(&sl, h->small->fn, sargs));
         return VTI_OK;

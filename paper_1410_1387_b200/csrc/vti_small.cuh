@@ -60,6 +60,10 @@ __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // programmatic dependent launch: everything above overlaps the previous step; the
+        // previous grid must complete before this item reads u^n / overwrites u^{n-1}
+        // (no-op without the launch attribute). Every store below follows these loads.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         mbar_arrive_expect_tx(bar, SC::TX_BYTES);
         tma_load_3d(smem + SC::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
         tma_load_3d(smem + SC::OFF_Q, &S.tm_qcol, x0, y0, k - RZ, bar);
