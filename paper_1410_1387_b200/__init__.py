@@ -29,6 +29,7 @@ COMPILED_RADII = ((4, 4), (8, 4), (6, 6), (12, 8))
 
 
 class VTIError(RuntimeError):
+    """Non-OK vti_status from the library; .name is the status name, the message is vti_last_error()."""
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
@@ -36,6 +37,7 @@ class VTIError(RuntimeError):
 
 
 class Config(C.Structure):
+    """ctypes mirror of vti_config (include/vti.h)."""
     _fields_ = [
         ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
         ("h", C.c_double), ("r_xy", C.c_int32), ("r_z", C.c_int32), ("dt", C.c_double),
@@ -46,6 +48,7 @@ class Config(C.Structure):
 
 
 class TuneResult(C.Structure):
+    """ctypes mirror of vti_tune_result."""
     _fields_ = [("tile_y", C.c_int32), ("producer_warp", C.c_int32), ("rows_per_thread", C.c_int32),
                 ("points_per_thread", C.c_int32), ("zchunk", C.c_int32),
                 ("ms_per_step", C.c_float), ("candidates", C.c_int32)]
@@ -55,6 +58,7 @@ class TuneResult(C.Structure):
 
 
 class PlanInfo(C.Structure):
+    """ctypes mirror of vti_plan_info."""
     _fields_ = [("y0", C.c_int32), ("ny_local", C.c_int32), ("ntx", C.c_int32), ("nty", C.c_int32),
                 ("edge_lo", C.c_int32), ("edge_hi", C.c_int32), ("zchunk", C.c_int32),
                 ("zchunk_edge", C.c_int32), ("zchunk_inner", C.c_int32), ("items", C.c_int32), ("grid", C.c_int32)]
@@ -64,6 +68,7 @@ class PlanInfo(C.Structure):
 
 
 class Info(C.Structure):
+    """ctypes mirror of vti_info."""
     _fields_ = [
         ("y0", C.c_int32), ("ny_local", C.c_int32), ("nx_pad", C.c_int32), ("layout", C.c_int32),
         ("tile_x", C.c_int32), ("tile_y", C.c_int32), ("rows_per_thread", C.c_int32), ("producer_warp", C.c_int32),
@@ -192,6 +197,7 @@ def plan(nx, ny, nz, r_xy, r_z, tile_y=32, sms=148, ctas_per_sm=1, rank=0, nrank
 
 
 def nccl_unique_id() -> bytes:
+    """vti_nccl_unique_id: a fresh 128-byte ncclUniqueId (rank 0 creates it, then broadcasts)."""
     buf = C.create_string_buffer(128)
     _check(None, lib.vti_nccl_unique_id(buf))
     return buf.raw
@@ -226,6 +232,7 @@ class VTI:
 
     # -- lifecycle
     def close(self):
+        """vti_destroy: free the handle and its device memory (idempotent)."""
         if self.h:
             lib.vti_destroy(self.h)
             self.h = C.c_void_p()
@@ -247,39 +254,48 @@ class VTI:
         return (self.nz if nk is None else nk) * self.ny_local * self.nx
 
     def set_model(self, vx2, vn2, vz2):
+        """vti_set_model[_f64]: vx2, vn2, vz2 of this rank's slab, [nz][ny_local][nx], host or device."""
         a = [_ptr(x, self._n(), dtype=self.dtype) for x in (vx2, vn2, vz2)]
         _check(self.h, self._fn("vti_set_model")(self.h, a[0][0], a[1][0], a[2][0]))
 
     def set_model_planes(self, k0, vx2, vn2, vz2):
+        """vti_set_model_planes[_f64]: planes [k0, k0 + nk) of the model."""
         nk = (vx2.shape[0] if hasattr(vx2, "shape") else len(vx2))
         a = [_ptr(x, self._n(nk), dtype=self.dtype) for x in (vx2, vn2, vz2)]
         _check(self.h, self._fn("vti_set_model_planes")(self.h, k0, nk, a[0][0], a[1][0], a[2][0]))
 
     def model_warnings(self) -> int:
+        """vti_model_warnings: points with vn2 > vx2 (eps < delta) seen so far."""
         return lib.vti_model_warnings(self.h)
 
     def add_source(self, i, j, k, f=15.0, t0=0.0, amp=1.0, mask=1):
+        """vti_add_source: Ricker point source at GLOBAL (i, j, k); mask 1 = F_p, 2 = F_q, 3 = both."""
         _check(self.h, lib.vti_add_source(self.h, i, j, k, f, t0, amp, mask))
 
     def set_fields(self, p, q, pm=None, qm=None, time_index=0):
+        """vti_set_fields[_f64]: state u^n (p, q) and u^{n-1} (pm, qm; None = zero) at time_index."""
         a = [_ptr(x, self._n(), dtype=self.dtype) for x in (p, q, pm, qm)]
         _check(self.h, self._fn("vti_set_fields")(self.h, a[0][0], a[1][0], a[2][0], a[3][0], time_index))
 
     def set_fields_planes(self, k0, p, q, pm=None, qm=None):
+        """vti_set_fields_planes[_f64]: planes [k0, k0 + nk) of the state."""
         nk = p.shape[0]
         a = [_ptr(x, self._n(nk), dtype=self.dtype) for x in (p, q, pm, qm)]
         _check(self.h, self._fn("vti_set_fields_planes")(self.h, k0, nk, a[0][0], a[1][0], a[2][0], a[3][0]))
 
     # -- stepping
     def step(self, nsteps=1):
+        """vti_step: enqueue nsteps time steps on the handle's stream (asynchronous)."""
         _check(self.h, lib.vti_step(self.h, nsteps))
 
     def step_timed(self, nsteps=1) -> float:
+        """vti_step_timed: nsteps steps bracketed by CUDA events; returns the device milliseconds."""
         ms = C.c_float()
         _check(self.h, lib.vti_step_timed(self.h, nsteps, C.byref(ms)))
         return ms.value
 
     def sync(self):
+        """vti_sync: wait for all work on the handle's stream(s)."""
         _check(self.h, lib.vti_sync(self.h))
 
     # -- outputs
@@ -305,6 +321,7 @@ class VTI:
         self._rec_fields = (fields & 1) + ((fields >> 1) & 1)
 
     def receiver_info(self):
+        """vti_receiver_info: (local receiver ids, rows recorded so far)."""
         n, t = C.c_int32(), C.c_int32()
         _check(self.h, lib.vti_receiver_info(self.h, C.byref(n), C.byref(t), None))
         ids = np.zeros(n.value, np.int32)
@@ -324,46 +341,57 @@ class VTI:
     IPC_BYTES = 512
 
     def ipc_export(self) -> bytes:
+        """vti_ipc_export: this rank's CUDA-IPC blob for the fused peer halo transport."""
         buf = C.create_string_buffer(self.IPC_BYTES)
         _check(self.h, lib.vti_ipc_export(self.h, buf))
         return buf.raw
 
     def ipc_connect(self, lo: bytes | None, hi: bytes | None):
+        """vti_ipc_connect: map the blobs of rank-1 (lo) and rank+1 (hi); None at the ends."""
         lo_b = C.create_string_buffer(lo, self.IPC_BYTES) if lo is not None else None
         hi_b = C.create_string_buffer(hi, self.IPC_BYTES) if hi is not None else None
         _check(self.h, lib.vti_ipc_connect(self.h, lo_b, hi_b))
 
     @property
     def halo_transport(self) -> str:
+        """vti_halo_transport: 'none', 'nccl' or 'peer'."""
         return {0: "none", 1: "nccl", 2: "peer"}.get(lib.vti_halo_transport(self.h), "?")
 
     def reverse(self):
+        """vti_reverse: swap the stored levels; the next steps run backwards in time."""
         _check(self.h, lib.vti_reverse(self.h))
 
     @property
     def direction(self) -> int:
+        """vti_direction: +1 forward, -1 after an odd number of reverse() calls."""
         return lib.vti_direction(self.h)
 
     @property
     def time_index(self) -> int:
+        """vti_time_index: the current level n."""
         return lib.vti_time_index(self.h)
 
     @property
     def stream(self) -> int:
+        """vti_stream: the cudaStream_t (as an int) the step kernels run on."""
         return lib.vti_stream(self.h) or 0
 
     def info(self) -> dict:
+        """vti_query: layout and launch facts of the handle as a dict."""
         i = Info()
         _check(self.h, lib.vti_query(self.h, C.byref(i)))
         return i.as_dict()
 
     def set_tuning(self, zchunk=0, ctas_per_sm=0):
+        """vti_set_tuning: planes per work item and CTAs per SM (0 = library default)."""
         _check(self.h, lib.vti_set_tuning(self.h, zchunk, ctas_per_sm))
 
     def set_variant(self, tile_y=-1, producer_warp=-1, rows_per_thread=-1, points_per_thread=-1):
+        """vti_set_variant: pick a compiled step-kernel variant (-1 = any); results are bitwise identical."""
         _check(self.h, lib.vti_set_variant(self.h, tile_y, producer_warp, rows_per_thread, points_per_thread))
 
     def autotune(self, probe_steps=5) -> dict:
+        """vti_autotune: time every compiled variant x z-chunk on this grid and keep the fastest."""
         r = TuneResult()
         _check(self.h, lib.vti_autotune(self.h, probe_steps, C.byref(r)))
         return r.as_dict()
