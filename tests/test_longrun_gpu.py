@@ -1,0 +1,41 @@
+"""The bench's own workload end to end: C2 (512^3, layered VTI, W = 20, Ricker at the
+centre, zero initial state) for its full 1000 steps, in bench.py's launch
+configuration, against the oracle over the whole grid -- bitwise.
+
+Opt-in (VTI_LONG=1): ~15 minutes, mostly the oracle on 16 host cores (passed: 872 s).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from synth import fields as SF
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(os.environ.get("VTI_LONG", "0") == "0", reason="long run: set VTI_LONG=1")]
+
+
+def test_c2_bench_workload_1000_steps():
+    from paper_1410_1387_b200 import VTI
+    cfg = synth.CONFIGS["C2"]()
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    nsteps = cfg["steps"]
+    assert nsteps == 1000
+    with VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], cfg["r_xy"], cfg["r_z"], dt, wxy, wz,
+             damp_width=cfg["damp_width"], damp_alpha=cfg["damp_alpha"], device=0) as v:
+        for k0 in range(0, cfg["nz"], 64):
+            v.set_model_planes(k0, *[a.contiguous() for a in SF.model_planes(cfg, k0, 64, device="cuda")])
+        torch.cuda.synchronize()
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
+        v.step(nsteps)
+        g = v.get_fields(0) + v.get_fields(1)
+    model = [a.cpu().numpy() for a in SF.model_planes(cfg, 0, cfg["nz"], device="cuda")]
+    torch.cuda.empty_cache()
+    o = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=nsteps)[:4]
+    for a, b in zip(g, o):
+        assert np.abs(b).max() > 0 and np.isfinite(a).all()
+        assert np.array_equal(a, b), f"max |diff| {np.abs(a - b).max():.3e}"
