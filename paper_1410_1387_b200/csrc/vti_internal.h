@@ -161,6 +161,7 @@ void choose_schedule(vti_s *h);                 // z-chunks and CTA caps of the 
 vti_status launch_edge(vti_s *h);               // tile rows the neighbours receive (PEER kernel when connected)
 vti_status launch_interior(vti_s *h);
 vti_status record(vti_s *h);                    // receiver gather after a step
+vti_status check_finite(vti_s *h);              // check_every: INSTABILITY on a non-finite value
 
 // vti_transport.cu
 vti_status pack_send(vti_s *h, int b);          // NCCL: boundary rows of buffer b -> send buffers (main stream)

@@ -820,7 +820,7 @@ vti_status launch_interior(vti_s *h)
     return launch_rows(h, e1, e2 - e1, 0, 0, h->zchunk_inner, h->cap_inner);
 }
 
-static vti_status check_finite(vti_s *h)
+vti_status check_finite(vti_s *h)
 {
     CU(h, cudaMemsetAsync(h->flag, 0, sizeof(unsigned int), h->stream));
     if (h->es == 8)

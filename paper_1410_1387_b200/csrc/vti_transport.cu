@@ -430,6 +430,8 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
             h->cur = 1 - h->cur;
             h->n += h->dir;
             if ((s = record(h)) != VTI_OK) return s;
+            if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0 && (s = check_finite(h)) != VTI_OK)
+                return s;
         }
     }
     return VTI_OK;

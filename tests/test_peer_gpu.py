@@ -195,3 +195,19 @@ def test_peer_group_launches_two_kernels_per_step():
     hs = handles(cfg, dt, wxy, wz, 3)
     assert [h.info()["launches_per_step"] for h in hs] == [2, 2, 2]
     close(hs)
+
+
+def test_group_check_every_detects_instability():
+    """check_every also runs in a local group: a blow-up is reported as VTI_E_INSTABILITY."""
+    from paper_1410_1387_b200 import VTI, VTIError, group_step
+    cfg = small_cfg(70, 80, 30, 4, 4, damp=5, src=(30, 40, 15))
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = 5 * synth.stable_dt(cfg, wxy, wz)   # far beyond the CFL bound
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    hs = [VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], 4, 4, dt, wxy, wz, damp_width=cfg["damp_width"],
+              damp_alpha=cfg["damp_alpha"], rank=r, nranks=2, check_every=25) for r in range(2)]
+    load(hs, model, random_state(cfg, amp=1.0), 0, cfg)
+    with pytest.raises(VTIError) as e:
+        group_step(hs, 2000)
+    assert e.value.name == "VTI_E_INSTABILITY"
+    close(hs)
