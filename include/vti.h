@@ -88,8 +88,9 @@ typedef struct {
     int32_t zchunk;         /* planes per work item */
     int32_t grid;           /* CTAs launched per step (persistent) */
     int32_t work_items;     /* tiles x z-chunks per step */
-    int32_t launches_per_step; /* library kernels per step: 1 (one slab); nranks > 1: edge + interior
-                                  step kernels (+ one pack and one unpack kernel per neighbour with NCCL) */
+    int32_t launches_per_step; /* library kernels per step: 1 (one slab, or a fused peer step); otherwise
+                                  edge + interior step kernels (+ one pack and one unpack kernel per
+                                  neighbour with NCCL) */
     int64_t device_bytes;   /* device memory owned by the handle */
     int64_t time_index;     /* n: fields hold u^n and u^{n-1} */
 } vti_info;

@@ -84,6 +84,13 @@ struct vti_s {
     unsigned int *flag = nullptr;
     unsigned long long *sync_ctr = nullptr;   // round-alignment counter (monotone across launches)
     unsigned long long sync_value = 0;        // its value once all launched work has finished
+    unsigned long long *edge_ctr = nullptr;   // fused multi-GPU step: edge items completed (monotone)
+    unsigned long long edge_value = 0;        // its value once all launched work has finished
+    // peer transport schedule: one fused launch per step (edge items first, device-side flags) or
+    // the edge + interior pair. Default: fused for a multi-process rank (one slab per GPU), the
+    // pair for a local group (slabs sharing a GPU interleave better); env VTI_FUSED_STEP=1/0 forces.
+    int fused_env = -1;
+    bool fused() const { return fused_env >= 0 ? fused_env != 0 : !group_mode; }
     bool align_rounds = true;                 // env VTI_ALIGN=0 disables
     int64_t device_bytes = 0;
     CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
@@ -170,3 +177,8 @@ vti_status peer_pre_step(vti_s *h);             // peer: wait for the halo this 
 vti_status peer_post_edge(vti_s *h);            // peer: after the edge launch, ACK + DATA to the neighbours
 vti_status peer_release(vti_s *h);              // peer re-publication (set_fields, reverse), first half
 vti_status peer_publish(vti_s *h);              // ... second half
+vti_status peer_fused_step(vti_s *h);           // peer: one launch (edge items first, device-side flags)
+
+// vti_runtime.cu: the fused multi-GPU launch -- edge tile rows (items first, PEER stores)
+// then the interior rows; the last edge item stores sig_val[i] to sig[i] (release, system)
+vti_status launch_fused(vti_s *h, unsigned int *const sig[4], const unsigned int sig_val[4]);

@@ -125,6 +125,18 @@ struct StepParams {
     // the L2 window of each other's p rows. NULL = no alignment.
     unsigned long long *sync_ctr;
     unsigned long long sync_base;
+    // Fused multi-GPU step (PEER kernels only): one launch covers the edge tile rows
+    // (tr0.., tr1..; items [0, edge_items)) and then the interior rows [tr2, tr2 + ntr2)
+    // (the remaining items). The CTA that completes the last edge item -- the edge_ctr
+    // counter reaching edge_target after every edge CTA fenced its stores at system
+    // scope -- stores sig_val[i] to *sig[i] with release semantics: the neighbours'
+    // ACK and DATA flag words. edge_items = 0: a plain launch (tile rows tr0.., tr1..).
+    int tr2, ntr2;
+    int edge_items;
+    unsigned long long *edge_ctr;
+    unsigned long long edge_target;
+    unsigned int *sig[4];
+    unsigned int sig_val[4];
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -261,13 +273,16 @@ __device__ __forceinline__ double fma_rn(double a, double b, double c) { return 
 template <int TY, typename PP>
 __device__ __forceinline__ void decode_item(const PP &P, int item, int &x0, int &y0, int &kb, int &ke)
 {
-    const int nsel = P.ntr0 + P.ntr1;
-    const int tx = item % P.ntx;
-    const int rest = item / P.ntx;
+    // edge rows (tr0.., tr1..) first; with edge_items > 0 the interior rows (tr2..) follow
+    const bool edge = P.edge_items == 0 || item < P.edge_items;
+    const int it = edge ? item : item - P.edge_items;
+    const int nsel = edge ? P.ntr0 + P.ntr1 : P.ntr2;
+    const int tx = it % P.ntx;
+    const int rest = it / P.ntx;
     const int t = rest % nsel;
     const int zc = rest / nsel;
     x0 = tx * TX;
-    y0 = (t < P.ntr0 ? P.tr0 + t : P.tr1 + (t - P.ntr0)) * TY;   // local row of the tile's first row
+    y0 = (edge ? (t < P.ntr0 ? P.tr0 + t : P.tr1 + (t - P.ntr0)) : P.tr2 + t) * TY;   // local row of the tile
     kb = zc * P.zchunk;
     ke = min(P.nz, kb + P.zchunk);
 }
@@ -635,6 +650,24 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
                                          pn[r]);
                             }
                         }
+                    }
+                }
+            }
+        }
+        if constexpr (PEER) {
+            if (P.edge_ctr != nullptr && item < P.edge_items) {
+                // fused multi-GPU step: this edge item's stores (own rows and the neighbours'
+                // halo rows) are done; the last edge item to finish raises the neighbours' flags
+                named_bar_sync(1, NCONS_WARPS * 32);
+                if (threadIdx.x == 0) {
+                    __threadfence_system();
+                    if (atomicAdd(P.edge_ctr, 1ULL) + 1 == P.edge_target) {
+                        __threadfence_system();
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (P.sig[i] != nullptr)
+                                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(P.sig[i]), "r"(P.sig_val[i])
+                                             : "memory");
                     }
                 }
             }

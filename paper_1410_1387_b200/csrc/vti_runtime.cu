@@ -300,6 +300,7 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->counters);
     cudaFree(h->flag);
     cudaFree(h->sync_ctr);
+    cudaFree(h->edge_ctr);
     cudaFree(h->flags);
     cudaFree(h->rec_off);
     cudaFree(h->traces);
@@ -472,6 +473,8 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     if ((s = alloc(h, (void **)&h->counters, 4 * sizeof(unsigned long long))) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->flag, sizeof(unsigned int))) != VTI_OK) return s;
     if ((s = alloc(h, (void **)&h->sync_ctr, sizeof(unsigned long long))) != VTI_OK) return s;
+    if ((s = alloc(h, (void **)&h->edge_ctr, sizeof(unsigned long long))) != VTI_OK) return s;
+    if (const char *e = getenv("VTI_FUSED_STEP")) h->fused_env = atoi(e) != 0;
     if (const char *e = getenv("VTI_ALIGN")) h->align_rounds = atoi(e) != 0;
     if (const char *e = getenv("VTI_GRAPH")) h->graph_enabled = atoi(e) != 0;
     if (cfg->nranks > 1) {
@@ -735,13 +738,44 @@ static void fill_params(vti_s *h, StepParams<T> &P, int tr0, int ntr0, int tr1, 
     P.zchunk = zchunk;
     P.nzc = (h->cfg.nz + zchunk - 1) / zchunk;
     P.items = h->ntx * (ntr0 + ntr1) * P.nzc;
+    P.tr2 = 0;
+    P.ntr2 = 0;
+    P.edge_items = 0;
+    P.edge_ctr = nullptr;
+    P.edge_target = 0;
+    for (int i = 0; i < 4; ++i) {
+        P.sig[i] = nullptr;
+        P.sig_val[i] = 0;
+    }
 }
 
+// Fused multi-GPU launch: the interior tile rows after the edge rows, and the flags the
+// last edge item raises (see StepParams::edge_items).
+struct FusedDesc {
+    int tr2, ntr2;
+    unsigned int *sig[4];
+    unsigned int sig_val[4];
+};
+
 template <typename T>
-static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk, int cap)
+static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, int zchunk, int cap,
+                                const FusedDesc *fd = nullptr)
 {
     StepParams<T> P;
     fill_params<T>(h, P, tr0, ntr0, tr1, ntr1, zchunk);
+    if (fd) {
+        P.tr2 = fd->tr2;
+        P.ntr2 = fd->ntr2;
+        P.edge_items = P.items;                       // edge items first
+        P.items += h->ntx * fd->ntr2 * P.nzc;
+        P.edge_ctr = h->edge_ctr;
+        h->edge_value += (unsigned long long)P.edge_items;
+        P.edge_target = h->edge_value;
+        for (int i = 0; i < 4; ++i) {
+            P.sig[i] = fd->sig[i];
+            P.sig_val[i] = fd->sig_val[i];
+        }
+    }
     if (h->capturing) {   // graph node: the source sample comes from the graph's table
         P.s_table = (const T *)h->s_graph;
         P.s_index = h->capture_index;
@@ -796,6 +830,22 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
                                                         (ntr1 > 0 && (tr1 + ntr1) * h->TY > h->nyl - h->R));
     CU(h, cudaLaunchKernelExC(&lc, peer_rows ? h->K->fn_peer : h->K->fn, args));
     return VTI_OK;
+}
+
+vti_status launch_fused(vti_s *h, unsigned int *const sig[4], const unsigned int sig_val[4])
+{
+    int e1, e2;
+    edge_rows(h, e1, e2);
+    FusedDesc fd;
+    fd.tr2 = e1;
+    fd.ntr2 = e2 - e1;
+    for (int i = 0; i < 4; ++i) {
+        fd.sig[i] = sig[i];
+        fd.sig_val[i] = sig_val[i];
+    }
+    // one launch over every tile row: the full-launch plan (z-chunk, CTA cap)
+    return h->es == 8 ? launch_rows_t<double>(h, 0, e1, e2, h->nty - e2, h->zchunk, h->cap, &fd)
+                      : launch_rows_t<float>(h, 0, e1, e2, h->nty - e2, h->zchunk, h->cap, &fd);
 }
 
 // Tile rows [tr0, tr0+ntr0) then [tr1, tr1+ntr1) of this slab, z-chunks of zchunk planes.
@@ -1184,6 +1234,10 @@ vti_status vti_step(vti_t h, int32_t nsteps)
             if ((s = launch_edge(h)) != VTI_OK || (s = launch_interior(h)) != VTI_OK) return s;
         } else if (!multi) {
             if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk, h->cap)) != VTI_OK) return s;
+        } else if (h->peer && h->fused()) {
+            // one launch: edge items first (their PEER stores feed the neighbours' halos), the
+            // last edge item raises the neighbours' flags from the device, the interior follows
+            if ((s = peer_fused_step(h)) != VTI_OK) return s;
         } else if (h->peer) {
             // the edge launch stores the neighbours' halo rows itself; the interior overlaps their edges
             if ((s = peer_pre_step(h)) != VTI_OK) return s;
@@ -1258,7 +1312,9 @@ vti_status vti_query(vti_t h, vti_info *info)
         const int neighbours = (h->cfg.rank > 0) + (h->cfg.rank < h->cfg.nranks - 1);
         int e1, e2;
         edge_rows(h, e1, e2);
-        info->launches_per_step = 1 + (e2 > e1 ? 1 : 0) + (h->peer || h->group_mode ? 0 : 2 * neighbours);
+        const bool peer_path = h->peer || h->group_mode;
+        info->launches_per_step = peer_path && h->fused() ? 1   // one fused launch per step
+                                                          : 1 + (e2 > e1 ? 1 : 0) + (peer_path ? 0 : 2 * neighbours);
     } else {
         info->launches_per_step = 1;
     }

@@ -240,6 +240,32 @@ vti_status peer_post_edge(vti_s *h)
     return VTI_OK;
 }
 
+// The same protocol in one launch: after the pre-step waits, the fused launch's last edge
+// item stores ACK = j and DATA = j + 1 into the neighbours' flag words from the device.
+vti_status peer_fused_step(vti_s *h)
+{
+    const unsigned int j = h->xseq;
+    vti_status s = peer_pre_step(h);
+    if (s != VTI_OK) return s;
+    unsigned int *sig[4] = {nullptr, nullptr, nullptr, nullptr};
+    unsigned int val[4] = {0, 0, 0, 0};
+    if (has_side(h, 0)) {
+        sig[0] = h->peer_flags[0] + F_ACK_HI;
+        val[0] = j;
+        sig[1] = h->peer_flags[0] + F_DATA_HI;
+        val[1] = j + 1;
+    }
+    if (has_side(h, 1)) {
+        sig[2] = h->peer_flags[1] + F_ACK_LO;
+        val[2] = j;
+        sig[3] = h->peer_flags[1] + F_DATA_LO;
+        val[3] = j + 1;
+    }
+    if ((s = launch_fused(h, sig, val)) != VTI_OK) return s;
+    h->xseq = j + 1;
+    return VTI_OK;
+}
+
 // Re-publication of the current level (state set by the caller, vti_reverse). Release
 // half: everything published so far is consumed or abandoned (stream-ordered after
 // this rank's last read of its halo).
@@ -419,6 +445,10 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         for (int i = 0; i < n; ++i) {   // waits on the previous step's writes only
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
+            if (h->fused()) {
+                if ((s = peer_fused_step(h)) != VTI_OK) return s;
+                continue;
+            }
             if ((s = peer_pre_step(h)) != VTI_OK) return s;
             if ((s = launch_edge(h)) != VTI_OK) return s;
             if ((s = peer_post_edge(h)) != VTI_OK) return s;
@@ -426,7 +456,7 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
-            if ((s = launch_interior(h)) != VTI_OK) return s;
+            if (!h->fused() && (s = launch_interior(h)) != VTI_OK) return s;
             h->cur = 1 - h->cur;
             h->n += h->dir;
             if ((s = record(h)) != VTI_OK) return s;

@@ -3,7 +3,7 @@
 Two processes on cuda:0, each owning one y-slab handle (nranks = 2, nccl_id = NULL),
 run bench.py's own connect path (paper_1410_1387_b200.multi.connect_peer over a gloo
 group): export the IPC blobs, all-gather them, open the neighbour's buffers and flag
-words. The handles must then report the peer transport and the two-launch step.
+words. The handles must then report the peer transport and the fused one-launch step.
 Nothing is stepped: ranks that wait on one another must not share one GPU
 (B200_PROFILING.md), so the stepping protocol itself is covered by the local-group
 GPU tests (same kernels and flag sequence) and the CPU model check
@@ -74,7 +74,7 @@ def test_two_process_ipc_connect():
         assert got[r]["before"] == "none", got
         assert got[r]["ok"] is True, got
         assert got[r]["after"] == "peer", got
-        assert got[r]["launches"] == 2, got
+        assert got[r]["launches"] == 1, got   # a multi-process peer rank runs the fused one-launch step
         assert got[r]["self_blob"] == "VTI_E_PARAM", got
     for p in procs:
         assert p.exitcode == 0

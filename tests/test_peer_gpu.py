@@ -193,7 +193,9 @@ def test_peer_group_launches_two_kernels_per_step():
     cfg = small_cfg(70, 450, 26, 4, 4, damp=5, src=(30, 100, 13))   # 150-row slabs: edge + interior
     wxy, wz, dt, model, st = f32_inputs(cfg)
     hs = handles(cfg, dt, wxy, wz, 3)
-    assert [h.info()["launches_per_step"] for h in hs] == [2, 2, 2]
+    # local groups default to the edge + interior pair; VTI_FUSED_STEP=1 forces one fused launch
+    expect = 1 if os.environ.get("VTI_FUSED_STEP", "") == "1" else 2
+    assert [h.info()["launches_per_step"] for h in hs] == [expect] * 3
     close(hs)
 
 
@@ -211,3 +213,47 @@ def test_group_check_every_detects_instability():
         group_step(hs, 2000)
     assert e.value.name == "VTI_E_INSTABILITY"
     close(hs)
+
+
+@pytest.mark.parametrize("nranks,ty,r,rz", [(2, 32, 4, 4), (3, 16, 4, 4), (3, 30, 12, 8), (4, 32, 8, 4)])
+def test_fused_step_bitwise(nranks, ty, r, rz, monkeypatch):
+    """The fused one-launch peer step (edge items first, the last edge CTA raises the
+    neighbours' flags from the device; the default of a multi-process rank), forced in a
+    local group: bitwise == oracle, across a re-publication and a reverse."""
+    from paper_1410_1387_b200 import group_step
+    monkeypatch.setenv("VTI_FUSED_STEP", "1")
+    ny = nranks * 70
+    cfg = small_cfg(70, ny, 2 * rz + 12, r, rz, damp=5)
+    cfg["src"] = (30, ny // nranks, cfg["nz"] // 2)   # first row of rank 1
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    hs = handles(cfg, dt, wxy, wz, nranks)
+    for h in hs:
+        h.set_variant(ty, -1, -1, -1)
+    assert all(h.info()["launches_per_step"] == 1 for h in hs)
+    load(hs, model, st, 0, cfg)
+    group_step(hs, 4)
+    group_step(hs, 3)
+    got = gather(hs)
+    ref = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, st, nsteps=7)[:4]
+    for f in range(4):
+        assert np.array_equal(got[f], ref[f]), f"field {f}"
+    # a state from the caller (re-publication), then reverse: equals the same calls on one slab
+    st2 = random_state(cfg, seed=13, amp=1e-4)
+    for h in hs:
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_fields(*[np.ascontiguousarray(a[:, sl]) for a in st2], time_index=7)
+    group_step(hs, 3)
+    for h in hs:
+        h.reverse()
+    group_step(hs, 2)
+    got2 = gather(hs)
+    close(hs)
+    (one,) = handles(cfg, dt, wxy, wz, 1)
+    load([one], model, st2, 7, cfg)
+    one.step(3)
+    one.reverse()
+    one.step(2)
+    ref2 = one.get_fields(0) + one.get_fields(1)
+    one.close()
+    for f in range(4):
+        assert np.array_equal(got2[f], ref2[f]), f"field {f}"
