@@ -349,6 +349,7 @@ def run_native(args):
 
     # warm-up (untimed), then exactly K timed steps bracketed by barrier + synchronize
     v.step(args.warmup)
+    v.prepare()   # small grids: capture the step graphs now, not inside the timed region
     if world > 1:   # the first exchanges prove the transport; fail loudly rather than hang
         multi.sync_or_die(v, 120.0, f"warm-up ({transport} halo transport)")
     v.sync()

@@ -189,6 +189,13 @@ vti_status vti_set_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, const doub
  * or nranks > 1 with neither transport), INSTABILITY (check_every), CUDA, COMM. */
 vti_status vti_step(vti_t h, int32_t nsteps);
 
+/* Build now whatever vti_step would otherwise build on its first call (the
+ * 32-step CUDA graphs of small single-slab grids, for both level parities), so
+ * a timed region does not pay for graph capture and instantiation. Nothing is
+ * executed; the state and the time index are unchanged. No-op when the handle
+ * does not replay graphs. Errors: STATE (model unset), CUDA. */
+vti_status vti_prepare(vti_t h);
+
 /* vti_step bracketed by CUDA events on the handle's stream; *ms = device time
  * of the nsteps steps (synchronises). */
 vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms);

@@ -118,6 +118,7 @@ def _load():
         "vti_sync": (st, [H]),
         "vti_time_index": (C.c_int64, [H]),
         "vti_stream": (C.c_void_p, [H]),
+        "vti_prepare": (st, [H]),
         "vti_query": (st, [H, C.POINTER(Info)]),
         "vti_set_tuning": (st, [H, C.c_int32, C.c_int32]),
         "vti_set_variant": (st, [H, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
@@ -293,6 +294,10 @@ class VTI:
         ms = C.c_float()
         _check(self.h, lib.vti_step_timed(self.h, nsteps, C.byref(ms)))
         return ms.value
+
+    def prepare(self):
+        """vti_prepare: build the CUDA graphs vti_step would build on first use (nothing runs)."""
+        _check(self.h, lib.vti_prepare(self.h))
 
     def sync(self):
         """vti_sync: wait for all work on the handle's stream(s)."""

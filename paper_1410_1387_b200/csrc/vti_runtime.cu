@@ -1193,6 +1193,18 @@ static vti_status replay_graph(vti_s *h)
     return VTI_OK;
 }
 
+vti_status vti_prepare(vti_t h)
+{
+    if (!h) return VTI_E_PARAM;
+    if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
+    CU(h, cudaSetDevice(h->cfg.device));
+    vti_status s;
+    if (graph_eligible(h))   // capture only: nothing executes, the state is untouched
+        for (int c = 0; c < 2; ++c)
+            if (!h->gexec[c] && (s = build_graph(h, c)) != VTI_OK) return s;
+    return VTI_OK;
+}
+
 vti_status vti_step(vti_t h, int32_t nsteps)
 {
     if (!h) return VTI_E_PARAM;

@@ -480,3 +480,25 @@ def test_small_grid_kernel(r, rz, shape, monkeypatch):
         g2 = v.get_fields(0) + v.get_fields(1)
     for a, b in zip(g, g2):
         assert np.array_equal(a, b)
+
+
+def test_prepare_builds_graphs_without_stepping():
+    """vti_prepare captures the step graphs of a small grid without running anything; the
+    following steps (graph replays) stay bitwise equal to the oracle."""
+    cfg = synth.CONFIGS["C1"]()
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    st = random_state(cfg, seed=5, amp=1e-3)
+    with make(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
+        v.set_fields(*st, time_index=2)
+        v.prepare()
+        assert v.time_index == 2
+        p, q = v.get_fields(0)
+        assert np.array_equal(p, st[0]) and np.array_equal(q, st[1])   # nothing ran
+        v.step(70)                                                      # 2 graph replays + 6 direct steps
+        g = v.get_fields(0) + v.get_fields(1)
+    o = oracle.run(oracle.params(cfg, dt), wxy, wz, *model, st, n0=2, nsteps=70)[:4]
+    assert_parity(g, o)
