@@ -375,7 +375,9 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
     h->small = nullptr;
     static const bool small_on = !getenv("VTI_SMALL") || atoi(getenv("VTI_SMALL")) != 0;
     const SmallEntry *se = find_small(h->es, h->R, h->RZ, h->TY);
-    if (small_on && se && !h->explicit_variant && h->cfg.nranks == 1 && h->zchunk == 1 && h->layout_zyx) {
+    const double pts = (double)h->cfg.nx * h->nyl * h->cfg.nz;
+    if (small_on && se && !h->explicit_variant && h->cfg.nranks == 1 && h->layout_zyx &&
+        (h->zchunk == 1 || pts <= 512.0 * 1024)) {
         const int NQ = 2 * h->RZ + 1;
         for (int b = 0; b < 2; ++b)
             if ((s = encode(h, &h->tm_qcol[b], h->q_int(b), h->nyl, TX, h->TY, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -383,6 +385,9 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
                 return s;
         CU(h, cudaFuncSetAttribute(se->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, se->smem));
         h->small = se;
+        h->zchunk = 1;   // the small kernel's items are (tile, plane)
+        h->nzc = h->cfg.nz;
+        h->grid = h->ntx * h->nty * h->nzc;
     }
     return VTI_OK;
 }
