@@ -1,8 +1,10 @@
-"""The bench's own workload end to end: C2 (512^3, layered VTI, W = 20, Ricker at the
-centre, zero initial state) for its full 1000 steps, in bench.py's launch
-configuration, against the oracle over the whole grid -- bitwise.
+"""The bench's own workloads end to end: C2 (512^3, layered VTI, W = 20, Ricker at the
+centre, zero initial state) and N1 (the same at the paper's radii (12,8)) for their
+full 1000 steps, in bench.py's launch configuration, against the oracle over the
+whole grid -- bitwise.
 
-Opt-in (VTI_LONG=1): ~15 minutes, mostly the oracle on 16 host cores (passed: 872 s).
+Opt-in (VTI_LONG=1): C2 ~15 minutes, N1 longer, mostly the oracle on 16 host cores
+(C2 passed in 872 s).
 """
 import os
 
@@ -18,9 +20,10 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(os.environ.get("VTI_LONG", "0") == "0", reason="long run: set VTI_LONG=1")]
 
 
-def test_c2_bench_workload_1000_steps():
+@pytest.mark.parametrize("name", ["C2", "N1"])
+def test_bench_workload_1000_steps(name):
     from paper_1410_1387_b200 import VTI
-    cfg = synth.CONFIGS["C2"]()
+    cfg = synth.CONFIGS[name]()
     wxy, wz, _ = synth.weights_f32(cfg)
     dt = synth.stable_dt(cfg, wxy, wz)
     nsteps = cfg["steps"]
