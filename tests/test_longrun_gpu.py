@@ -3,8 +3,7 @@ centre, zero initial state) and N1 (the same at the paper's radii (12,8)) for th
 full 1000 steps, in bench.py's launch configuration, against the oracle over the
 whole grid -- bitwise.
 
-Opt-in (VTI_LONG=1): C2 ~15 minutes, N1 longer, mostly the oracle on 16 host cores
-(C2 passed in 872 s).
+Opt-in (VTI_LONG=1): mostly the oracle on 16 host cores (passed: C2 872 s, N1 1755 s).
 """
 import os
 
