@@ -1,10 +1,12 @@
-// fp64 (12,8) variants. Default: two x points per thread (one double2), TY = 10 +
-// producer warp = 11 warps at 168 registers without spills (N1 fp64 28.7 with the
-// 4-point TY = 14 mapping -> 52.4 with TY = 15 at 128 registers (644 B of spills)
-// -> 75.9 Gpoints/s).
+// fp64 (12,8) variants. Default: two x points per thread (one double2), TY = 8 +
+// producer warp = 9 warps, 4-deep TMA ring (N1 fp64 28.7 with the 4-point TY = 14
+// mapping -> 52.4 with TY = 15 at 128 registers (644 B of spills) -> 75.9 Gpoints/s
+// with TY = 10 and 3 stages -> +4.9 % with TY = 8 and 4 stages: 68.4 -> 71.8 on the
+// same box, twice each, 1000 steps; TY = 6 x 5 stages 66.3, TY = 12 55.7, TY = 10
+// x 4 stages 69.7).
 #include "../vti_entry.cuh"
 VTI_TABLE(vti_variants_f64_r12,
-          (entry<double, 12, 8, 10, 1, 1, 3, 1, 2>()), (entry<double, 12, 8, 8, 1, 1, 3, 1, 2>()),
+          (entry<double, 12, 8, 8, 1, 1, 4, 1, 2>()), (entry<double, 12, 8, 10, 1, 1, 3, 1, 2>()),
           (entry<double, 12, 8, 15, 1, 1, 3, 1, 2>()), (entry<double, 12, 8, 16, 1, 0, 2, 1, 2>()),
           (entry<double, 12, 8, 14, 1, 1, 3, 1>()), (entry<double, 12, 8, 16, 1, 1, 2, 1>()),
           (entry<double, 12, 8, 16, 1, 0, 2, 1>()))

@@ -40,11 +40,13 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, 
     static const VariantTable tables[] = {vti_variants_f32_r4(),  vti_variants_f32_r8(),  vti_variants_f32_r6(),
                                           vti_variants_f32_r12(), vti_variants_f64_r48(), vti_variants_f64_r6(),
                                           vti_variants_f64_r12()};
+    // VTI_STAGES=n: only variants with an n-deep TMA ring (a measurement switch)
+    static const int want_stages = getenv("VTI_STAGES") ? atoi(getenv("VTI_STAGES")) : -1;
     for (const VariantTable &t : tables)
         for (int i = 0; i < t.n; ++i) {
             const KernelEntry &e = t.e[i];
             if (e.esize == esize && e.r == r && e.rz == rz && (ty < 0 || e.ty == ty) && (wp < 0 || e.wp == wp) &&
-                (rpt < 0 || e.rpt == rpt) && (px < 0 || e.px == px))
+                (rpt < 0 || e.rpt == rpt) && (px < 0 || e.px == px) && (want_stages < 0 || e.stages == want_stages))
                 return &e;
         }
     return nullptr;
