@@ -1,6 +1,7 @@
 """CPU oracle for the VTI step -- TEST INFRASTRUCTURE ONLY.
 
-Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and the
+Only tests/, tools/oracle_digests.py (writes tests/golden/ digests),
+__graft_entry__.smoke() and bench.py (cpu_baseline leg and the
 ``--impl reference`` arm) may import this package. The product path
 (paper_1410_1387_b200 + include/vti.h) never imports it, and this package
 never imports the product. The arithmetic lives in ``vti_oracle.c`` (plain C
@@ -69,10 +70,12 @@ def lib():
             ct = C.c_float if t is np.float32 else C.c_double
             g.argtypes = [C.POINTER(Params), fp(t), fp(t), C.c_int32, C.c_int32, C.c_int32,
                           C.c_int64, fp(t), fp(t), ct, ct, ct, ct, ct, fp(t)]
+            w = getattr(L, "vto_step_planes_" + sfx)
+            w.restype = C.c_int
+            w.argtypes = [C.POINTER(Params), fp(t), fp(t), C.c_int32, C.c_int32, C.c_int64,
+                          fp(t), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t)]
         L.vto_ricker.restype = C.c_double
         L.vto_ricker.argtypes = [C.c_double, C.c_double, C.c_double]
-        L.vto_source_f32.restype = C.c_float
-        L.vto_source_f32.argtypes = [C.POINTER(Params), C.c_int64]
         L.vto_damping.restype = C.c_double
         L.vto_damping.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double]
         L.vto_damping_profile_f32.restype = None
@@ -136,6 +139,34 @@ def point(P: Params, wxy, wzrow, i, j, k, n, pc, qc, pm, qm, vx2, vn2, vz2, dtyp
     if rc != 0:
         raise ValueError(f"oracle rejected parameters (code {rc})")
     return out[0], out[1]
+
+
+def step_planes(P: Params, wxy, wz, k0: int, p, q, pm, qm, vx2, vn2, vz2, n: int = 0,
+                dtype=np.float32):
+    """One step (level n -> n+1) of planes [k0, k0+nk) of the global grid P from plane windows.
+
+    p, pm, qm, vx2, vn2, vz2: [nk][ny][nx] (planes k0..); q: [nk+2Rz][ny][nx] (planes
+    k0-Rz..; planes outside the grid are ignored = zero exterior); wz: the full
+    [nz][2Rz+1] table. Returns (p^{n+1}, q^{n+1}) on those planes (see vti_oracle.c).
+    """
+    conv = lambda a: np.ascontiguousarray(np.asarray(a, dtype=dtype))
+    p, pm, qm, vx2, vn2, vz2 = (conv(a) for a in (p, pm, qm, vx2, vn2, vz2))
+    q = conv(q)
+    nk = p.shape[0]
+    shape = (nk, P.ny, P.nx)
+    for a in (p, pm, qm, vx2, vn2, vz2):
+        assert a.shape == shape, (a.shape, shape)
+    assert q.shape == (nk + 2 * P.r_z, P.ny, P.nx)
+    wxy = conv(wxy).reshape(-1)
+    wz = conv(wz).reshape(-1)
+    assert wxy.size == P.r_xy + 1 and wz.size == P.nz * (2 * P.r_z + 1)
+    pn = np.empty(shape, dtype=dtype)
+    qn = np.empty(shape, dtype=dtype)
+    f = lib().vto_step_planes_f32 if dtype == np.float32 else lib().vto_step_planes_f64
+    rc = f(C.byref(P), wxy, wz, k0, nk, n, p, q, pm, qm, vx2, vn2, vz2, pn, qn)
+    if rc != 0:
+        raise ValueError(f"oracle rejected parameters (code {rc})")
+    return pn, qn
 
 
 def ricker(t, f, t0):

@@ -1,7 +1,7 @@
 /*
  * oracle/vti_oracle.c -- CPU ORACLE FOR THE VTI STEP.  TEST INFRASTRUCTURE ONLY.
  *
- * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * Only tests/, tools/oracle_digests.py, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
  * arm may load this library. The product path (paper_1410_1387_b200/, the
  * C-ABI in include/vti.h) never calls it and shares no code with it.
  *
@@ -67,12 +67,6 @@ double vto_ricker(double t, double f, double t0)
     double x = M_PI * f * (t - t0);
     double a = x * x;
     return (1.0 - 2.0 * a) * exp(-a);
-}
-
-/* Source sample s(t^n), t^n = n dt, rounded once to float32. */
-float vto_source_f32(const vto_params *P, int64_t n)
-{
-    return (float)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));
 }
 
 /* Cerjan taper value at index idx of an axis with n points (reading c9). */
@@ -166,6 +160,61 @@ int vto_point_##SFX(const vto_params *P, const T *wxy, const T *wzrow, int32_t i
     T s = (T)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));                \
     point_##SFX(R, Rz, cxy, wzrow, dt2, g, pc, qc, pm, qm, vx2, vn2, vz2, bits, s,             \
                 &out2[0], &out2[1]);                                                           \
+    return 0;                                                                                  \
+}                                                                                              \
+                                                                                               \
+/*                                                                                             \
+ * One step (level n -> n+1) on the whole x-y extent of planes [k0, k0+nk) of the GLOBAL       \
+ * grid of P, from caller-supplied plane windows (user layout, x fastest):                     \
+ *   p, pm, qm, vx2, vn2, vz2 : [nk][ny][nx]      planes k0 .. k0+nk-1                         \
+ *   q                        : [nk+2Rz][ny][nx]  planes k0-Rz .. k0+nk+Rz-1; planes outside     \
+ *                              0..nz-1 are never read (zero exterior)                 \
+ *   wz                       : the full [nz][2Rz+1] table (row = global plane)                 \
+ * Outputs pn, qn : [nk][ny][nx] = u^{n+1} on those planes. Same point_ update as vto_run.      \
+ */                                                                                            \
+int vto_step_planes_##SFX(const vto_params *P, const T *wxy, const T *wz, int32_t k0,          \
+                          int32_t nk, int64_t n, const T *p, const T *q, const T *pm,          \
+                          const T *qm, const T *vx2, const T *vn2, const T *vz2, T *pn,        \
+                          T *qn)                                                               \
+{                                                                                              \
+    int rc = check_params(P);                                                                  \
+    if (rc) return rc;                                                                         \
+    const int R = P->r_xy, Rz = P->r_z, nx = P->nx, ny = P->ny, nz = P->nz;                    \
+    if (R >= 64 || Rz >= 64) return 1;                                                         \
+    if (k0 < 0 || nk < 0 || k0 + nk > nz) return 2;                                           \
+    T cxy[64];                                                                                 \
+    for (int l = 0; l <= R; ++l) cxy[l] = (T)((double)wxy[l] / (P->h * P->h));                 \
+    const T dt2 = (T)(P->dt * P->dt);                                                          \
+    const T s = (T)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));          \
+    const int64_t plane = (int64_t)nx * ny;                                                    \
+    _Pragma("omp parallel for collapse(2)")                                                    \
+    for (int kk = 0; kk < nk; ++kk)                                                            \
+        for (int j = 0; j < ny; ++j)                                                           \
+            for (int i = 0; i < nx; ++i) {                                                     \
+                const int k = k0 + kk;                                                         \
+                const int64_t u = (int64_t)kk * plane + (int64_t)j * nx + i;                   \
+                T pc[4 * 64 + 1], qc[2 * 64 + 1];                                              \
+                pc[0] = p[u];                                                                  \
+                for (int l = 1; l <= R; ++l) {                                                 \
+                    pc[l] = i + l < nx ? p[u + l] : (T)0;                                      \
+                    pc[R + l] = i - l >= 0 ? p[u - l] : (T)0;                                  \
+                    pc[2 * R + l] = j + l < ny ? p[u + (int64_t)l * nx] : (T)0;                \
+                    pc[3 * R + l] = j - l >= 0 ? p[u - (int64_t)l * nx] : (T)0;                \
+                }                                                                              \
+                for (int m = 0; m <= 2 * Rz; ++m) {                                            \
+                    const int kq = k - Rz + m;   /* window plane kk + m */                     \
+                    qc[m] = (kq >= 0 && kq < nz) ? q[(int64_t)(kk + m) * plane + (int64_t)j * nx + i] \
+                                                 : (T)0;                                       \
+                }                                                                              \
+                const T gx = (T)vto_damping(i, nx, P->damp_width, P->damp_alpha);              \
+                const T gy = (T)vto_damping(j, ny, P->damp_width, P->damp_alpha);              \
+                const T gz = (T)vto_damping(k, nz, P->damp_width, P->damp_alpha);              \
+                const T g = (gx * gy) * gz;                                                    \
+                const int bits = (P->src_i == i && P->src_j == j && P->src_k == k)             \
+                                     ? P->src_mask : 0;                                        \
+                point_##SFX(R, Rz, cxy, wz + (int64_t)k * (2 * Rz + 1), dt2, g, pc, qc, pm[u], \
+                            qm[u], vx2[u], vn2[u], vz2[u], bits, s, &pn[u], &qn[u]);           \
+            }                                                                                  \
     return 0;                                                                                  \
 }                                                                                              \
                                                                                                \
