@@ -70,6 +70,13 @@ def lib():
             ct = C.c_float if t is np.float32 else C.c_double
             g.argtypes = [C.POINTER(Params), fp(t), fp(t), C.c_int32, C.c_int32, C.c_int32,
                           C.c_int64, fp(t), fp(t), ct, ct, ct, ct, ct, fp(t)]
+            x = getattr(L, "vto_run_ex_" + sfx)
+            x.restype = C.c_int
+            i32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+            x.argtypes = [C.POINTER(Params), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t),
+                          fp(t), fp(t), C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                          C.c_int32, i32, C.c_int32, C.c_int32, C.c_int64, fp(t),
+                          C.c_int32, i32, C.c_int32, fp(t), C.POINTER(C.c_double)]
             w = getattr(L, "vto_step_planes_" + sfx)
             w.restype = C.c_int
             w.argtypes = [C.POINTER(Params), fp(t), fp(t), C.c_int32, C.c_int32, C.c_int64,
@@ -127,6 +134,51 @@ def run(P: Params, wxy, wz, vx2, vn2, vz2, state=None, n0: int = 0, nsteps: int 
     if rc != 0:
         raise ValueError(f"oracle rejected parameters (code {rc})")
     return p, q, pm, qm, secs.value
+
+
+def run_ex(P: Params, wxy, wz, vx2, vn2, vz2, state=None, n0: int = 0, nsteps: int = 1,
+           direction: int = 1, inj=None, rec=None, dtype=np.float32, nthreads: int = 0):
+    """run() with time direction, trace injection and receivers.
+
+    inj = (ijk [n][3] int, mask, t_first, traces [nt][n]) or None;
+    rec = (ijk [m][3] int, mask) or None. direction = -1: state = (u^n, u^{n+1}) and the
+    time index runs n0, n0-1, ... Returns (p, q, pm, qm, rec_traces [nsteps][m][nf] or None, s).
+    """
+    shape = (P.nz, P.ny, P.nx)
+    conv = lambda a: np.ascontiguousarray(np.asarray(a, dtype=dtype))
+    if state is None:
+        p, q, pm, qm = (np.zeros(shape, dtype=dtype) for _ in range(4))
+    else:
+        p, q, pm, qm = (conv(a).copy() for a in state)
+    vx2, vn2, vz2 = (conv(a).reshape(shape) for a in (vx2, vn2, vz2))
+    wxy = conv(wxy).reshape(-1)
+    wz = conv(wz).reshape(-1)
+    dummy_i = np.zeros(3, np.int32)
+    dummy_t = np.zeros(1, dtype)
+    if inj is not None:
+        ijk, imask, t_first, tr = inj
+        ijk = np.ascontiguousarray(np.asarray(ijk, np.int32).reshape(-1, 3))
+        tr = conv(tr).reshape(-1, ijk.shape[0])
+        n_inj, nt = ijk.shape[0], tr.shape[0]
+    else:
+        ijk, imask, t_first, tr, n_inj, nt = dummy_i, 0, 0, dummy_t, 0, 0
+    if rec is not None:
+        rijk, rmask = rec
+        rijk = np.ascontiguousarray(np.asarray(rijk, np.int32).reshape(-1, 3))
+        n_rec = rijk.shape[0]
+        nf = (rmask & 1) + ((rmask >> 1) & 1)
+        out = np.zeros((nsteps, n_rec, nf), dtype=dtype)
+    else:
+        rijk, rmask, n_rec, out = dummy_i, 0, 0, dummy_t
+    secs = C.c_double(0.0)
+    f = lib().vto_run_ex_f32 if dtype == np.float32 else lib().vto_run_ex_f64
+    rc = f(C.byref(P), wxy, wz, vx2, vn2, vz2, p, q, pm, qm, n0, nsteps, direction, nthreads,
+           n_inj, ijk.reshape(-1) if n_inj else dummy_i, imask, nt, t_first, tr.reshape(-1) if n_inj else dummy_t,
+           n_rec, rijk.reshape(-1) if n_rec else dummy_i, rmask, out.reshape(-1) if n_rec else dummy_t,
+           C.byref(secs))
+    if rc != 0:
+        raise ValueError(f"oracle rejected parameters (code {rc})")
+    return p, q, pm, qm, (out if n_rec else None), secs.value
 
 
 def point(P: Params, wxy, wzrow, i, j, k, n, pc, qc, pm, qm, vx2, vn2, vz2, dtype=np.float32):

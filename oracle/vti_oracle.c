@@ -118,7 +118,7 @@ static int check_params(const vto_params *P)
 #define DEFINE_ORACLE(T, SFX, FMA)                                                              \
 static void point_##SFX(int R, int Rz, const T *cxy, const T *wzrow, T dt2, T g,               \
                         const T *pc, const T *qc, T pm, T qm, T vx2, T vn2, T vz2,             \
-                        int src_bits, T s, T *pn, T *qn)                                        \
+                        int src_bits, T s, int inj_bits, T inj, T *pn, T *qn)                  \
 {                                                                                              \
     /* Eq. 4 divided by h^2 (reading c3): L = (p_xx + p_yy) */                                  \
     T L = cxy[0] * pc[0];                                                                      \
@@ -132,8 +132,10 @@ static void point_##SFX(int R, int Rz, const T *cxy, const T *wzrow, T dt2, T g,
     T vD = vz2 * D;                                                                            \
     T Fp = FMA(vx2, L, vD);                                                                    \
     if (src_bits & 1) Fp = Fp + s;                                                             \
+    if (inj_bits & 1) Fp = Fp + inj;  /* injected trace sample (N4), after the source */       \
     T Fq = FMA(vn2, L, vD);                                                                    \
     if (src_bits & 2) Fq = Fq + s;                                                             \
+    if (inj_bits & 2) Fq = Fq + inj;                                                           \
     /* Eq. 3 with Cerjan damping (reading c9) */                                               \
     *pn = g * FMA(dt2, Fp, FMA(-g, pm, (T)2 * pc[0]));                                         \
     *qn = g * FMA(dt2, Fq, FMA(-g, qm, (T)2 * qc[Rz]));                                        \
@@ -158,7 +160,7 @@ int vto_point_##SFX(const vto_params *P, const T *wxy, const T *wzrow, int32_t i
     T g = (gx * gy) * gz;                                                                      \
     int bits = (P->src_i == i && P->src_j == j && P->src_k == k) ? P->src_mask : 0;            \
     T s = (T)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));                \
-    point_##SFX(R, Rz, cxy, wzrow, dt2, g, pc, qc, pm, qm, vx2, vn2, vz2, bits, s,             \
+    point_##SFX(R, Rz, cxy, wzrow, dt2, g, pc, qc, pm, qm, vx2, vn2, vz2, bits, s, 0, (T)0,    \
                 &out2[0], &out2[1]);                                                           \
     return 0;                                                                                  \
 }                                                                                              \
@@ -213,30 +215,63 @@ int vto_step_planes_##SFX(const vto_params *P, const T *wxy, const T *wz, int32_
                 const int bits = (P->src_i == i && P->src_j == j && P->src_k == k)             \
                                      ? P->src_mask : 0;                                        \
                 point_##SFX(R, Rz, cxy, wz + (int64_t)k * (2 * Rz + 1), dt2, g, pc, qc, pm[u], \
-                            qm[u], vx2[u], vn2[u], vz2[u], bits, s, &pn[u], &qn[u]);           \
+                            qm[u], vx2[u], vn2[u], vz2[u], bits, s, 0, (T)0, &pn[u], &qn[u]);  \
             }                                                                                  \
     return 0;                                                                                  \
 }                                                                                              \
                                                                                                \
 /*                                                                                             \
- * Run nsteps steps starting at time level n0. Arrays are interior-only, user                  \
- * layout [z][y][x] (x fastest). On entry p,q = u^{n0}, pm,qm = u^{n0-1}; on                   \
- * exit p,q = u^{n0+nsteps}, pm,qm = u^{n0+nsteps-1}. *seconds (if non-NULL)                   \
- * receives the wall time of the step loop only.                                               \
+ * Run nsteps steps starting at time level n0, time index n0, n0+dir, ... (dir = +1, or -1    \
+ * for the time-reversed recurrence u^{n-1} = g (2u^n - g u^{n+1} + dt^2 F(u^n)), i.e. the    \
+ * same Eq. 3 with the stored level playing u^{n+1}). Arrays are interior-only, user layout    \
+ * [z][y][x] (x fastest). On entry p,q = u^{n0}, pm,qm = u^{n0-dir}; on exit p,q =            \
+ * u^{n0+dir*nsteps}, pm,qm = u^{n0+dir*(nsteps-1)}. *seconds (if non-NULL) receives the wall  \
+ * time of the step loop only.                                                                 \
+ * Trace injection (N4, the backward leg of RTM/FWI): at the step that       \
+ * evaluates F(u^n), if inj_t_first <= n < inj_t_first + inj_nt, the sample                    \
+ * inj_tr[(n - inj_t_first) * n_inj + r] is added into F_p (inj_mask bit 1) and/or F_q (bit 2) \
+ * at the distinct GLOBAL point inj_ijk[3r..3r+2], after the Ricker source.                    \
+ * Receivers: after each step, u^{new} of the fields in rec_mask (p before q) at rec_ijk[3r..]  \
+ * is stored at rec_out[(step * n_rec + r) * nf + f].                                          \
  */                                                                                            \
-int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2,               \
-                  const T *vn2, const T *vz2, T *p, T *q, T *pm, T *qm, int64_t n0,            \
-                  int32_t nsteps, int32_t nthreads, double *seconds)                           \
+int vto_run_ex_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2,            \
+                     const T *vn2, const T *vz2, T *p, T *q, T *pm, T *qm, int64_t n0,         \
+                     int32_t nsteps, int32_t dir, int32_t nthreads, int32_t n_inj,             \
+                     const int32_t *inj_ijk, int32_t inj_mask, int32_t inj_nt,                 \
+                     int64_t inj_t_first, const T *inj_tr, int32_t n_rec,                      \
+                     const int32_t *rec_ijk, int32_t rec_mask, T *rec_out, double *seconds)    \
 {                                                                                              \
     int rc = check_params(P);                                                                  \
     if (rc) return rc;                                                                         \
+    if (dir != 1 && dir != -1) return 1;                                                       \
+    if (n_inj < 0 || n_rec < 0 || (n_inj > 0 && (!inj_ijk || !inj_tr || inj_nt < 0 ||          \
+        inj_mask < 1 || inj_mask > 3)) || (n_rec > 0 && (!rec_ijk || !rec_out ||                \
+        rec_mask < 1 || rec_mask > 3))) return 1;                                              \
     const int R = P->r_xy, Rz = P->r_z, nx = P->nx, ny = P->ny, nz = P->nz;                    \
+    int32_t *inj_at = NULL;  /* interior point -> injection index r, or -1 */                  \
+    if (n_inj > 0) {                                                                           \
+        inj_at = (int32_t *)malloc(sizeof(int32_t) * (size_t)nx * ny * nz);                   \
+        if (!inj_at) return 3;                                                                 \
+        for (int64_t u = 0; u < (int64_t)nx * ny * nz; ++u) inj_at[u] = -1;                    \
+        for (int r = 0; r < n_inj; ++r) {                                                      \
+            const int i = inj_ijk[3 * r], j = inj_ijk[3 * r + 1], k = inj_ijk[3 * r + 2];      \
+            if (i < 0 || i >= nx || j < 0 || j >= ny || k < 0 || k >= nz) { free(inj_at); return 2; } \
+            const int64_t u = ((int64_t)k * ny + j) * nx + i;                                  \
+            if (inj_at[u] >= 0) { free(inj_at); return 1; }  /* points must be distinct */    \
+            inj_at[u] = r;                                                                     \
+        }                                                                                      \
+    }                                                                                          \
+    for (int r = 0; r < n_rec; ++r) {                                                          \
+        const int i = rec_ijk[3 * r], j = rec_ijk[3 * r + 1], k = rec_ijk[3 * r + 2];          \
+        if (i < 0 || i >= nx || j < 0 || j >= ny || k < 0 || k >= nz) { free(inj_at); return 2; } \
+    }                                                                                          \
+    const int rec_nf = (rec_mask & 1) + ((rec_mask >> 1) & 1);                                 \
     const int64_t X = nx + 2 * R, Y = ny + 2 * R, Z = nz + 2 * Rz;                             \
     const int64_t npad = X * Y * Z;                                                            \
     T *buf[4];                                                                                 \
     for (int b = 0; b < 4; ++b) {                                                              \
         buf[b] = (T *)calloc((size_t)npad, sizeof(T));  /* zero exterior */          \
-        if (!buf[b]) { for (int c = 0; c < b; ++c) free(buf[c]); return 3; }                   \
+        if (!buf[b]) { for (int c = 0; c < b; ++c) free(buf[c]); free(inj_at); return 3; }     \
     }                                                                                          \
     T *Pc = buf[0], *Qc = buf[1], *Pm = buf[2], *Qm = buf[3];                                  \
     _Pragma("omp parallel for collapse(2)")                                                    \
@@ -248,7 +283,7 @@ int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2, 
                 Pc[a] = p[u]; Qc[a] = q[u]; Pm[a] = pm[u]; Qm[a] = qm[u];                      \
             }                                                                                  \
     T cxy[64];                                                                                 \
-    if (R >= 64) { for (int b = 0; b < 4; ++b) free(buf[b]); return 1; }                      \
+    if (R >= 64) { for (int b = 0; b < 4; ++b) free(buf[b]); free(inj_at); return 1; }        \
     for (int l = 0; l <= R; ++l) cxy[l] = (T)((double)wxy[l] / (P->h * P->h));                 \
     const T dt2 = (T)(P->dt * P->dt);                                                          \
     T *gx = (T *)malloc(sizeof(T) * nx), *gy = (T *)malloc(sizeof(T) * ny),                    \
@@ -258,8 +293,11 @@ int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2, 
     for (int k = 0; k < nz; ++k) gz[k] = (T)vto_damping(k, nz, P->damp_width, P->damp_alpha);  \
     const int nt = nthreads > 0 ? nthreads : vto_max_threads();                                \
     double t_start = now_s();                                                                  \
-    for (int64_t n = n0; n < n0 + nsteps; ++n) {                                               \
+    for (int32_t step = 0; step < nsteps; ++step) {                                            \
+        const int64_t n = n0 + (int64_t)dir * step;                                            \
         const T s = (T)(P->src_amp * vto_ricker((double)n * P->dt, P->src_f, P->src_t0));      \
+        const int inj_row_ok = n_inj > 0 && n >= inj_t_first && n < inj_t_first + inj_nt;     \
+        const T *inj_row = inj_row_ok ? inj_tr + (n - inj_t_first) * (int64_t)n_inj : NULL;    \
         _Pragma("omp parallel for collapse(2) schedule(static) num_threads(nt)")                \
         for (int k = 0; k < nz; ++k)                                                           \
             for (int j = 0; j < ny; ++j)                                                       \
@@ -278,15 +316,24 @@ int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2, 
                     const T g = (gx[i] * gy[j]) * gz[k];                                       \
                     const int bits = (P->src_i == i && P->src_j == j && P->src_k == k)         \
                                          ? P->src_mask : 0;                                    \
+                    const int ir = inj_row ? inj_at[u] : -1;                                   \
                     T pn, qn;                                                                  \
                     point_##SFX(R, Rz, cxy, wz + (int64_t)k * (2 * Rz + 1), dt2, g, pc, qc,    \
-                                Pm[a], Qm[a], vx2[u], vn2[u], vz2[u], bits, s, &pn, &qn);      \
+                                Pm[a], Qm[a], vx2[u], vn2[u], vz2[u], bits, s,                 \
+                                ir >= 0 ? inj_mask : 0, ir >= 0 ? inj_row[ir] : (T)0, &pn, &qn); \
                     Pm[a] = pn;  /* u^{n+1} overwrites u^{n-1} in place */                     \
                     Qm[a] = qn;                                                                \
                 }                                                                              \
         T *t;                                                                                  \
         t = Pc; Pc = Pm; Pm = t;                                                               \
         t = Qc; Qc = Qm; Qm = t;                                                               \
+        for (int r = 0; r < n_rec; ++r) {   /* receivers: the level just computed */           \
+            const int i = rec_ijk[3 * r], j = rec_ijk[3 * r + 1], k = rec_ijk[3 * r + 2];      \
+            const int64_t a = ((int64_t)(k + Rz) * Y + (j + R)) * X + (i + R);                \
+            T *o = rec_out + ((int64_t)step * n_rec + r) * rec_nf;                             \
+            if (rec_mask & 1) *o++ = Pc[a];                                                    \
+            if (rec_mask & 2) *o = Qc[a];                                                      \
+        }                                                                                      \
     }                                                                                          \
     double t_end = now_s();                                                                    \
     if (seconds) *seconds = t_end - t_start;                                                   \
@@ -299,8 +346,18 @@ int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2, 
                 p[u] = Pc[a]; q[u] = Qc[a]; pm[u] = Pm[a]; qm[u] = Qm[a];                      \
             }                                                                                  \
     free(gx); free(gy); free(gz);                                                              \
+    free(inj_at);                                                                              \
     for (int b = 0; b < 4; ++b) free(buf[b]);                                                  \
     return 0;                                                                                  \
+}                                                                                              \
+                                                                                               \
+/* Forward run, Ricker source only (the path every pin in tests/test_oracle_pins.py drives). */ \
+int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2,               \
+                  const T *vn2, const T *vz2, T *p, T *q, T *pm, T *qm, int64_t n0,            \
+                  int32_t nsteps, int32_t nthreads, double *seconds)                           \
+{                                                                                              \
+    return vto_run_ex_##SFX(P, wxy, wz, vx2, vn2, vz2, p, q, pm, qm, n0, nsteps, 1, nthreads,  \
+                            0, NULL, 0, 0, 0, NULL, 0, NULL, 0, NULL, seconds);                \
 }
 
 DEFINE_ORACLE(float, f32, fmaf)
