@@ -1,23 +1,29 @@
 #!/usr/bin/env python
 """Benchmark: VTI time steps per second on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl native|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--reps R] [--config C4]
+                  [--impl native|reference]
 
 One "step" = one time step of the reduced elastic VTI propagator (PAPER.md
 Eqs. 1-3) over the whole grid: every row of SURVEY.md 8(a) runs inside the
-fused sm_100a kernel (plus, for N > 1, the NCCL halo exchange of p).
+fused sm_100a kernel (for N > 1 the halo exchange of p is fused into it as
+peer stores over NVLink, or NCCL send/recv when CUDA IPC is unavailable).
 
-Workload (N = 1): BASELINE.json configs[1] = C2, 512^3, R_xy = R_z = 4,
-layered VTI with variable dz, Cerjan W = 20, Ricker source at the centre,
-starting from the zero state. N > 1: weak scaling, one 512^3 C2 block per GPU
-stacked along y (global 512 x 512N x 512), one y-slab per rank, NCCL halo
-exchange of p every step. Inputs (4.8 GB/step at N = 1) are far larger than
-the 126 MB L2, so no explicit flush is needed between steps.
+Workload (default at every N): BASELINE.json configs[3] = C4, 2048 x 2048 x
+1024, R_xy = R_z = 4, layered VTI with variable dz, Cerjan W = 20, Ricker source
+at the centre, starting from the zero state -- north_star's ">= 85 % at 8 GPUs
+on a 2048x2048x1024 grid" workload and the largest single-GPU configuration
+(120 GB of HBM at N = 1). N > 1: strong scaling, one y-slab of 2048/N rows per
+rank. --config C1/C2/C3/C5/N1 time the other BASELINE configurations (C2/N1
+and C5 weak-scaled along y for N > 1). Inputs (155 GB/step at N = 1) are far
+larger than the 126 MB L2, so no explicit flush is needed between steps.
 
 Metric: Gpoints/s = (global grid points) x K / t, t = max over ranks of the
-CUDA-event time of the K steps on the library's stream. ``roofline`` uses
-36 algorithmic bytes per point-update against the measured
-HBM copy bandwidth in MEASURED_PEAKS.json.
+CUDA-event time of K steps on the library's stream; the K-step region is timed
+--reps times (default 5, each bracketed by barrier + synchronize) and `value`
+is the median. ``roofline`` uses 36 algorithmic bytes per point-update
+ against the measured HBM copy bandwidth in
+MEASURED_PEAKS.json, with the nominal 8 TB/s fraction alongside.
 """
 from __future__ import annotations
 
@@ -39,12 +45,15 @@ METRIC = "Gpoints/s per VTI step (1/2/4/8 B200) and % of HBM roofline"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "N1"])
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=5, help="timed K-step regions; value = their median")
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5", "N1"])
     ap.add_argument("--scaling", default=None, choices=[None, "weak", "strong"])
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="steps of the end-to-end job (0 = the config's stated step count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--zchunk", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
@@ -74,6 +83,7 @@ def workload(args, world):
 
 
 def describe(cfg, world, scaling, bpp=BYTES_PER_POINT, transport="none"):
+    npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
     return {
         "workload": f"{cfg['name']}: {cfg['nx']}x{cfg['ny']}x{cfg['nz']} global, R_xy={cfg['r_xy']} R_z={cfg['r_z']}, "
                     f"{cfg['model']['kind']} VTI, W={cfg['damp_width']}, Ricker f={cfg['f']:g} Hz at the centre",
@@ -82,7 +92,10 @@ def describe(cfg, world, scaling, bpp=BYTES_PER_POINT, transport="none"):
         "decomposition": f"y-slabs x{world}" if world > 1 else "single GPU",
         "halo_transport": transport,
         "scaling": scaling,
-        "l2_flush": f"not needed: per-step working set ({bpp} B/pt) >> 126 MB L2",
+        "l2_flush": (f"not needed: per-step working set {bpp * npts / 1e9:.1f} GB ({bpp} B/pt) >> 126 MB L2"
+                     if bpp * npts > 4 * 126e6 else
+                     f"none: the whole per-step working set ({bpp * npts / 1e6:.1f} MB) stays L2-resident "
+                     "across steps (a small-grid, latency-bound workload)"),
         "bytes_per_point": bpp,
     }
 
@@ -141,6 +154,9 @@ class Clocks:
                 "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace('.', '', 1).isdigit())}
 
 
+NOMINAL_HBM_GBS = 8000.0   # B200 nominal HBM3e bandwidth (north_star "~8 TB/s")
+
+
 def peak_hbm():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -166,45 +182,73 @@ def mix_ceiling():
 
 
 def ncu_traffic(cfg, precision=32):
-    """dram bytes per launch from the committed ncu --set full summary, if one matches this workload."""
+    """(dram bytes per launch, source) from the committed ncu --set full summary
+    (profiles/ncu_summary.json, tools/ncu_summary.py) if it holds this workload's grid."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         d = json.load(open(p))
         e = d.get(cfg["name"] if precision == 32 else cfg["name"] + "_f64")
         if e and e.get("grid") == [cfg["nx"], cfg["ny"], cfg["nz"]]:
-            return e.get("dram_bytes_per_launch")
+            return e.get("dram_bytes_per_launch"), f"prior ncu --set full capture ({e.get('source', 'profiles/')})"
     except (OSError, ValueError):
         pass
-    return None
+    return None, None
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 def cpu_baseline(cfg, budget_s=12.0, precision=32):
-    """The oracle as it stands, on this host's cores, on a bounded sample of the same workload."""
+    """The oracle as it stands, on this host's cores, on a bounded sample of the same workload:
+    the config's recipe on SURVEY.md 8(d)'s reduced grid (256 x 256 x 128 for C4/C5, the full
+    grid for C1, else at most 256^3), from a seeded random state; all threads, then 1 thread."""
     import numpy as np
-    import torch
 
     import oracle
     import synth
     from synth import fields as SF
     oracle.build()
-    wxy, wz = weights(cfg, precision)
-    dt = synth.stable_dt(cfg)
+    if cfg["nx"] * cfg["ny"] * cfg["nz"] > 256 ** 3:
+        sample = synth.scaled(cfg, min(cfg["nx"], 256), min(cfg["ny"], 256), 128 if cfg["nz"] >= 1024 else
+                              min(cfg["nz"], 256))
+    else:
+        sample = cfg
+    wxy, wz = weights(sample, precision)
+    dt = synth.stable_dt(sample)
     dt_np = np.float32 if precision == 32 else np.float64
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    nz = cfg["nz"]
-    model = [a.cpu().numpy() for a in SF.model_planes(cfg, 0, nz, device=dev)]
-    state = [SF.random_planes(cfg["nx"], cfg["ny"], 0, nz, 11, s, 1e-6, device=dev).cpu().numpy()
-             for s in range(4)]
-    P = oracle.params(cfg, dt)
-    npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    _, _, _, _, t1 = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=1, dtype=dt_np)
-    k = int(max(1, min(50, budget_s / max(t1, 1e-3))))
-    _, _, _, _, tk = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=k, dtype=dt_np)
-    del model, state
-    return {"value": round(npts * k / tk / 1e9, 6), "unit": "Gpoints/s", "cores": oracle.max_threads(),
-            "kind": "oracle",
-            "sample": f"oracle fp{precision} (C, OpenMP) on the full {cfg['nx']}x{cfg['ny']}x{cfg['nz']} {cfg['name']} grid, "
-                      f"{k} time steps from a seeded random state (step loop only, {tk:.1f} s)"}
+    nz = sample["nz"]
+    model = [a.numpy() for a in SF.model_planes(sample, 0, nz)]
+    state = [SF.random_planes(sample["nx"], sample["ny"], 0, nz, 11, s, 1e-6).numpy() for s in range(4)]
+    P = oracle.params(sample, dt)
+    npts = sample["nx"] * sample["ny"] * sample["nz"]
+    threads = host_threads()
+    _, _, _, _, t1 = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=1, dtype=dt_np, nthreads=threads)
+    k = int(max(1, min(400, budget_s / max(t1, 1e-3))))
+    _, _, _, _, tk = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=k, dtype=dt_np, nthreads=threads)
+    k1 = int(max(1, min(10, 0.25 * budget_s / max(t1 * threads, 1e-3))))
+    _, _, _, _, t1t = oracle.run(P, wxy, wz, *model, state, n0=100, nsteps=k1, dtype=dt_np, nthreads=1)
+    return {"value": round(npts * k / tk / 1e9, 6), "unit": "Gpoints/s", "cores": threads,
+            "kind": "oracle", "cpu": cpu_model(),
+            "one_thread": {"value": round(npts * k1 / t1t / 1e9, 6), "steps": k1},
+            "sample": f"oracle fp{precision} (C, OpenMP, {threads} threads) on the {cfg['name']} recipe at "
+                      f"{sample['nx']}x{sample['ny']}x{sample['nz']} (bounded sample of "
+                      f"{cfg['nx']}x{cfg['ny']}x{cfg['nz']}), {k} time steps from a seeded random state "
+                      f"(step loop only, {tk:.1f} s); one_thread: {k1} steps on 1 thread"}
 
 
 def run_reference(args):
@@ -212,8 +256,6 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import numpy as np
-
     import oracle
     import synth
     from synth import fields as SF
@@ -229,8 +271,9 @@ def run_reference(args):
         state = [SF.random_planes(c["nx"], c["ny"], 0, c["nz"], 11, s, 1e-6).numpy() for s in range(4)]
         return oracle.params(c, dt), wxy, wz, model, state
 
+    threads = host_threads()
     P, wxy, wz, model, state = setup(probe)
-    _, _, _, _, t = oracle.run(P, wxy, wz, *model, state, nsteps=2)
+    _, _, _, _, t = oracle.run(P, wxy, wz, *model, state, nsteps=2, nthreads=threads)
     rate = 2 * 128 ** 3 / t
     pts = max(32 ** 3, min(cfg_full["nx"] * cfg_full["ny"] * cfg_full["nz"],
                            int(rate * 120.0 / max(1, args.steps + args.warmup))))
@@ -238,8 +281,8 @@ def run_reference(args):
     side = max(2 * cfg_full["damp_width"] + 2, max(2 * cfg_full["r_z"] + 1, side))
     sample = synth.scaled(cfg_full, side, side, side)
     P, wxy, wz, model, state = setup(sample)
-    st = oracle.run(P, wxy, wz, *model, state, nsteps=args.warmup)[:4] if args.warmup else state
-    _, _, _, _, secs = oracle.run(P, wxy, wz, *model, st, n0=args.warmup, nsteps=args.steps)
+    st = oracle.run(P, wxy, wz, *model, state, nsteps=args.warmup, nthreads=threads)[:4] if args.warmup else state
+    _, _, _, _, secs = oracle.run(P, wxy, wz, *model, st, n0=args.warmup, nsteps=args.steps, nthreads=threads)
     npts = side ** 3
     value = npts * args.steps / secs / 1e9
     line = {
@@ -248,8 +291,8 @@ def run_reference(args):
         "ms_per_step": round(1e3 * secs / args.steps, 4), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
         "config": describe(cfg_full, world, scaling),
-        "cpu_baseline": {"value": round(value, 6), "unit": "Gpoints/s", "cores": oracle.max_threads(),
-                         "kind": "oracle",
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gpoints/s", "cores": threads,
+                         "kind": "oracle", "cpu": cpu_model(),
                          "sample": f"oracle fp32 (C, OpenMP) on the {cfg_full['name']} recipe at {side}^3 "
                                    f"(bounded sample of {cfg_full['nx']}x{cfg_full['ny']}x{cfg_full['nz']}), "
                                    f"{args.warmup} warm-up + {args.steps} timed steps"},
@@ -293,12 +336,112 @@ def set_model_from_device(v, cfg, chunk=64):
     torch.cuda.synchronize()
 
 
+def open_handle(cfg, dt, wxy, wz, rank, world, local, prec, dist, halo="peer"):
+    """A rank's handle with its halo transport: fused peer stores over CUDA IPC by default
+    (multi.connect_peer), NCCL if requested (VTI_HALO=nccl) or if any rank cannot connect
+    (the decision is collective). world == 1: a single-slab handle."""
+    from paper_1410_1387_b200 import multi
+    if world > 1 and halo != "nccl":
+        h = make_handle(cfg, dt, wxy, wz, rank, world, local, None, prec)
+        if multi.connect_peer(dist, h, rank, world):
+            return h
+        h.close()
+    nccl_id = multi.broadcast_nccl_id(dist, rank, world) if world > 1 else None
+    return make_handle(cfg, dt, wxy, wz, rank, world, local, nccl_id, prec)
+
+
+def warm_up(v, steps, world, transport, timeout_s=120.0):
+    """W untimed steps, graph capture for small grids, and -- for N > 1 -- the guard that
+    turns a transport that never delivers into a loud exit instead of a hang."""
+    from paper_1410_1387_b200 import multi
+    v.step(steps)
+    v.prepare()   # small grids: capture the step graphs now, not inside the timed region
+    if world > 1:
+        multi.sync_or_die(v, timeout_s, f"warm-up ({transport} halo transport)")
+    v.sync()
+
+
+def setup_rank(args, cfg, dt, wxy, wz, rank, world, local, dist, halo):
+    """Everything a rank does before the timed region: handle + transport, tuning, model,
+    source and warm-up. Returns (handle, transport name)."""
+    v = open_handle(cfg, dt, wxy, wz, rank, world, local, args.precision, dist, halo)
+    transport = v.halo_transport
+    if args.zchunk or args.ctas_per_sm:
+        v.set_tuning(args.zchunk, args.ctas_per_sm)
+    set_model_from_device(v, cfg)
+    v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
+    warm_up(v, args.warmup, world, transport)
+    return v, transport
+
+
+def end_to_end(args, cfg, dt, wxy, wz, rank, world, local, dist, halo, info, barrier, max_over_ranks):
+    """The config's whole job through the public API with HOST buffers (pinned): model upload,
+    source, e2e_steps steps, read back u^N. Wall clock, max over ranks."""
+    import torch
+
+    from synth import fields as SF
+    import numpy as np
+    prec = args.precision
+    nsteps = args.e2e_steps or cfg["steps"]
+    shape = (cfg["nz"], info["ny_local"], cfg["nx"])
+    rt = torch.cuda.cudart()
+    registered = []
+
+    def pinned():
+        # exact-size page-locked host arrays (cudaHostRegister on numpy memory): torch's pinned
+        # caching allocator rounds large blocks up, which C4 (17 GB per array) cannot afford
+        a = np.empty(shape, np.float32 if prec == 32 else np.float64)
+        err = rt.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+        if int(err) != 0:
+            raise RuntimeError(f"cudaHostRegister({a.nbytes} B) failed: {err}")
+        registered.append(a)
+        return a
+
+    host_model = [pinned() for _ in range(3)]
+    for k0 in range(0, cfg["nz"], 64):
+        nk = min(64, cfg["nz"] - k0)
+        m = SF.model_planes(cfg, k0, nk, device="cuda", j0=info["y0"], nyl=info["ny_local"])
+        for dst, src in zip(host_model, m):
+            torch.from_numpy(dst[k0:k0 + nk]).copy_(src.to(torch.float32 if prec == 32 else torch.float64))
+        del m
+    out_p, out_q = pinned(), pinned()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    w = open_handle(cfg, dt, wxy, wz, rank, world, local, prec, dist, halo)
+    if args.zchunk or args.ctas_per_sm:
+        w.set_tuning(args.zchunk, args.ctas_per_sm)
+    barrier()
+    t0 = time.perf_counter()
+    w.set_model(*host_model)
+    w.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
+    w.step(nsteps)
+    w.get_fields(0, out_p, out_q)
+    w.sync()
+    te = time.perf_counter() - t0
+    barrier()
+    te = max_over_ranks(te)
+    w.close()
+    npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
+    nbytes = (prec // 8) * npts
+    for a in registered:
+        rt.cudaHostUnregister(a.ctypes.data)
+    del host_model, out_p, out_q, registered
+    return {"value": round(npts * nsteps / te / 1e9, 4), "unit": "Gpoints/s", "steps": nsteps,
+            "h2d_bytes_per_step": int(3 * nbytes / nsteps), "d2h_bytes_per_step": int(2 * nbytes / nsteps),
+            "seconds": round(te, 3),
+            "what": f"the config's whole job: vti_set_model (pinned host model, {3 * nbytes / 1e9:.1f} GB) + "
+                    f"vti_add_source + vti_step({nsteps}) + vti_get_fields(u^N, {2 * nbytes / 1e9:.1f} GB to "
+                    "pinned host), wall clock, max over ranks"}
+
+
 def run_native(args):
+    import statistics
+
     import torch
     import torch.distributed as dist
 
     import synth
-    import paper_1410_1387_b200 as vti
+    from paper_1410_1387_b200 import multi, perfmodel
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -308,27 +451,10 @@ def run_native(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, scaling = workload(args, world)
     prec = args.precision
-    from paper_1410_1387_b200 import perfmodel
     bpp = perfmodel.bytes_per_point(prec)   # 36 B/point in fp32, 72 in fp64
     wxy, wz = weights(cfg, prec)
     dt = synth.stable_dt(cfg)
-
-    from paper_1410_1387_b200 import multi
-
-    def fresh_nccl_id():
-        return multi.broadcast_nccl_id(dist, rank, world)
-
     halo = os.environ.get("VTI_HALO", "peer") if world > 1 else "none"
-
-    def open_handle():
-        """A rank's handle with its halo transport: peer stores over CUDA IPC by default,
-        NCCL if requested or if any rank cannot connect (collective fallback)."""
-        if world > 1 and halo != "nccl":
-            h = make_handle(cfg, dt, wxy, wz, rank, world, local, None, prec)
-            if multi.connect_peer(dist, h, rank, world):
-                return h
-            h.close()
-        return make_handle(cfg, dt, wxy, wz, rank, world, local, fresh_nccl_id(), prec)
 
     def barrier():
         if world > 1:
@@ -339,100 +465,73 @@ def run_native(args):
         return multi.max_over_ranks(dist, world, x, device="cuda")
 
     npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    v = open_handle()
-    transport = v.halo_transport
-    if args.zchunk or args.ctas_per_sm:
-        v.set_tuning(args.zchunk, args.ctas_per_sm)
-    set_model_from_device(v, cfg)
-    v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
+    v, transport = setup_rank(args, cfg, dt, wxy, wz, rank, world, local, dist, halo)
     info = v.info()
 
-    # warm-up (untimed), then exactly K timed steps bracketed by barrier + synchronize
-    v.step(args.warmup)
-    v.prepare()   # small grids: capture the step graphs now, not inside the timed region
-    if world > 1:   # the first exchanges prove the transport; fail loudly rather than hang
-        multi.sync_or_die(v, 120.0, f"warm-up ({transport} halo transport)")
-    v.sync()
+    # --reps timed regions of exactly K steps, each bracketed by barrier + synchronize
+    reps = []
     barrier()
     with Clocks(local) as clk:
-        ms = v.step_timed(args.steps)
-    barrier()
-    t_ms = max_over_ranks(ms)
+        for _ in range(max(1, args.reps)):
+            barrier()
+            ms = v.step_timed(args.steps)
+            barrier()
+            reps.append(max_over_ranks(ms))
     clocks = clk.summary()
+    t_ms = statistics.median(reps)
 
     value = npts * args.steps / (t_ms * 1e-3) / 1e9
     launches = info["launches_per_step"] * args.steps
     pts_rank = cfg["nx"] * info["ny_local"] * cfg["nz"]
-    # dominant kernel: the step kernel; at N = 1 one launch per step covers every point
-    kern_ms = ms / args.steps
+    # dominant kernel: the step kernel; one launch per step covers every point of the slab
+    kern_ms = t_ms / args.steps
     achieved = bpp * pts_rank / (kern_ms * 1e-3) / 1e9
     peak, peak_src = peak_hbm()
-    traffic = ncu_traffic(cfg, prec) if world == 1 else None
+    traffic, traffic_src = ncu_traffic(cfg, prec) if world == 1 else (None, None)
     v.close()
+    torch.cuda.empty_cache()
 
     e2e = None
     if not args.no_e2e:
-        # through the public API with HOST buffers (pinned): model upload, K steps, read back u^K
-        tdt = torch.float32 if prec == 32 else torch.float64
-        pin = lambda shape: torch.empty(shape, dtype=tdt, pin_memory=True)
-        shape = (cfg["nz"], info["ny_local"], cfg["nx"])
-        host_model = [pin(shape) for _ in range(3)]
-        from synth import fields as SF
-        for k0 in range(0, cfg["nz"], 64):
-            nk = min(64, cfg["nz"] - k0)
-            m = SF.model_planes(cfg, k0, nk, device="cuda", j0=info["y0"], nyl=info["ny_local"])
-            for dst, src in zip(host_model, m):
-                dst[k0:k0 + nk].copy_(src)
-        out_p, out_q = pin(shape), pin(shape)
-        w = open_handle()
-        if args.zchunk or args.ctas_per_sm:
-            w.set_tuning(args.zchunk, args.ctas_per_sm)
-        barrier()
-        t0 = time.perf_counter()
-        w.set_model(*host_model)
-        w.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=cfg["amp"], mask=cfg["mask"])
-        w.step(args.steps)
-        w.get_fields(0, out_p, out_q)
-        w.sync()
-        te = time.perf_counter() - t0
-        barrier()
-        te = max_over_ranks(te)
-        w.close()
-        nbytes = (prec // 8) * cfg["nx"] * cfg["ny"] * cfg["nz"]
-        e2e = {"value": round(npts * args.steps / te / 1e9, 4), "unit": "Gpoints/s",
-               "h2d_bytes_per_step": int(3 * nbytes / args.steps), "d2h_bytes_per_step": int(2 * nbytes / args.steps),
-               "what": "vti_set_model (pinned host) + vti_add_source + vti_step(K) + vti_get_fields(u^K to pinned host), wall clock, max over ranks"}
-        del host_model
+        e2e = end_to_end(args, cfg, dt, wxy, wz, rank, world, local, dist, halo, info, barrier, max_over_ranks)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, precision=prec)
 
     if rank == 0:
+        mc = mix_ceiling()
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": "Gpoints/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 5),
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": f"f{prec}",
             "data": "synthetic (seeded layered VTI model generated on device; zero initial state + Ricker source)",
             "config": describe(cfg, world, scaling, bpp, transport),
+            "repetitions": {"n": len(reps), "statistic": "median", "ms_per_region": [round(x, 4) for x in reps],
+                            "gpoints_s": [round(npts * args.steps / (x * 1e-3) / 1e9, 3) for x in reps]},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
+                         "nominal": {"peak": NOMINAL_HBM_GBS, "frac": round(achieved / NOMINAL_HBM_GBS, 4),
+                                     "source": "B200 nominal HBM3e bandwidth (north_star ~8 TB/s)"},
                          "mix_ceiling": ({"gbs": mc, "frac": round(achieved / mc, 4),
                                           "source": "profiles/stream_probe*_r01.txt (7 read + 2 write streams, "
-                                                    "best of plain and TMA-bulk loads)"}
-                                         if (mc := mix_ceiling()) else None),
-                         "kernel": "vti::vti_step_kernel<4,4>" if cfg["r_xy"] == 4 else f"vti::vti_step_kernel<{cfg['r_xy']},{cfg['r_z']}>",
+                                                    "best of plain and TMA-bulk loads)"} if mc else None),
+                         "kernel": f"vti::vti_step_kernel<{'float' if prec == 32 else 'double'},"
+                                   f"{cfg['r_xy']},{cfg['r_z']},...>"
+                                   + (" (small-grid kernel vti_small_kernel)" if info["small_kernel"] else ""),
                          "algorithmic_bytes_per_launch": bpp * pts_rank,
+                         "bytes_per_point": bpp, "points_per_launch": pts_rank,
                          "flops_per_point": {"paper_count": perfmodel.flops_per_point(cfg["r_xy"], cfg["r_z"]),
                                              "canonical_order": perfmodel.step_flops_per_point(cfg["r_xy"], cfg["r_z"])},
                          "gflops": round(perfmodel.step_flops_per_point(cfg["r_xy"], cfg["r_z"]) * value, 1)},
             "e2e": e2e,
             "gpu_launches": launches,
+            "timed_regions": len(reps),
             "clocks": clocks,
             "cpu_baseline": cpu,
             "schedule": {k: info[k] for k in ("tile_x", "tile_y", "producer_warp", "rows_per_thread", "points_per_thread",
-                                              "small_kernel",
-                                              "zchunk", "grid", "work_items")},
+                                              "small_kernel", "zchunk", "grid", "work_items", "launches_per_step")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

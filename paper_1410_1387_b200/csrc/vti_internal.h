@@ -101,7 +101,7 @@ struct vti_s {
     int cur = 0;                              // pbuf[cur], qbuf[cur] hold u^n
     int64_t n = 0;                            // time index
     bool model_set = false;
-    int64_t model_planes_set = 0;
+    std::vector<char> model_planes;           // per plane: uploaded by vti_set_model* (model_set = all)
     int64_t aniso_warn = 0;
     bool has_src = false;
     int src_i = 0, src_j = 0, src_k = 0, src_mask = 0;

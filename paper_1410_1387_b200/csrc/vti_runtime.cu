@@ -654,9 +654,11 @@ static vti_status set_model_planes(vti_s *h, int es, int32_t k0, int32_t nk, con
     if (cnt[0]) return fail(h, VTI_E_MODEL, "%llu points with vz2 <= 0 or non-finite", cnt[0]);
     if (cnt[1]) return fail(h, VTI_E_MODEL, "%llu points with non-finite vx2/vn2", cnt[1]);
     h->aniso_warn += (int64_t)cnt[2];
-    if (k0 == 0 && nk == h->cfg.nz) h->model_set = true;
-    else h->model_planes_set += nk;
-    if (h->model_planes_set >= h->cfg.nz) h->model_set = true;
+    // the model counts as set once every plane has been uploaded at least once (planes never
+    // uploaded still hold the zero fill of alloc(), i.e. vz2 = 0, which validation rejects)
+    if ((int)h->model_planes.size() != h->cfg.nz) h->model_planes.assign(h->cfg.nz, 0);
+    std::fill(h->model_planes.begin() + k0, h->model_planes.begin() + k0 + nk, 1);
+    h->model_set = std::all_of(h->model_planes.begin(), h->model_planes.end(), [](char c) { return c != 0; });
     return VTI_OK;
 }
 
@@ -1049,14 +1051,12 @@ vti_status vti_set_model_planes_f64(vti_t h, int32_t k0, int32_t nk, const doubl
 vti_status vti_set_model(vti_t h, const float *vx2, const float *vn2, const float *vz2)
 {
     if (!h) return VTI_E_PARAM;
-    h->model_planes_set = 0;
     return set_model_planes(h, 4, 0, h->cfg.nz, vx2, vn2, vz2);
 }
 
 vti_status vti_set_model_f64(vti_t h, const double *vx2, const double *vn2, const double *vz2)
 {
     if (!h) return VTI_E_PARAM;
-    h->model_planes_set = 0;
     return set_model_planes(h, 8, 0, h->cfg.nz, vx2, vn2, vz2);
 }
 

@@ -24,7 +24,11 @@ def max_over_ranks(dist, world: int, x: float, device="cpu") -> float:
         return x
     import torch
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    try:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    except RuntimeError:   # a backend without device-tensor support (gloo builds): host tensor
+        t = t.cpu()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
@@ -54,22 +58,30 @@ def connect_peer(dist, handle, rank: int, world: int) -> bool:
     return bool(int(t.item()))
 
 
-def sync_or_die(handle, timeout_s: float, what: str = "halo exchange") -> None:
+def sync_or_die(handle, timeout_s: float, what: str = "halo exchange", query=None, die=None) -> None:
     """Wait for the handle's enqueued steps, polling its stream, and exit the process
     loudly if they do not finish within timeout_s (a peer that never delivers its halo
     must fail the run, not hang it). The main stream waits on every exchange, so its
-    completion covers the comm stream's work too."""
+    completion covers the comm stream's work too.
+
+    ``handle.stream`` is the cudaStream_t (an int property, vti_stream). ``query`` /
+    ``die`` default to torch's stream query and os._exit(3); tests substitute them.
+    """
     import os
     import sys
     import time
 
-    import torch
-    s = torch.cuda.ExternalStream(handle.stream())
+    if query is None:
+        import torch
+        query = torch.cuda.ExternalStream(handle.stream).query
+    if die is None:
+        die = os._exit
     t0 = time.monotonic()
-    while not s.query():
+    while not query():
         if time.monotonic() - t0 > timeout_s:
             print(f"error: {what} did not complete within {timeout_s:.0f} s "
                   f"(transport {handle.halo_transport}); aborting", file=sys.stderr, flush=True)
-            os._exit(3)
+            die(3)
+            return
         time.sleep(0.01)
     handle.sync()

@@ -50,10 +50,16 @@ def test_native_arm_line():
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["steps"] == 100   # C1's stated step count: the whole job
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+    assert cb["cpu"] and cb["one_thread"]["value"] > 0
     assert d["gpu_launches"] >= 40
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    reps = d["repetitions"]
+    assert reps["n"] == 5 and reps["statistic"] == "median" and len(reps["ms_per_region"]) == 5
+    assert abs(sorted(reps["ms_per_region"])[2] / 40 - d["ms_per_step"]) < 1e-4
+    assert abs(rf["nominal"]["frac"] - rf["achieved"] / 8000.0) < 1e-3
 
 
 @pytest.mark.gpu
@@ -66,3 +72,23 @@ def test_native_arm_other_workloads(args, dtype, bpp):
     assert d["config"]["workload"].startswith(args[1])
     assert d["roofline"]["peak"] > 0 and d["roofline"]["achieved"] > 0
     assert d["gpu_launches"] >= 20
+
+
+@pytest.mark.gpu
+def test_default_line_is_c4():
+    """The driver's default command (no --config): BASELINE C4 2048x2048x1024 at N = 1, with the
+    end-to-end job (pinned host model in, u^N out), cpu_baseline and the C4 ncu traffic."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < 130e9:
+        pytest.skip(f"C4 needs ~125 GB of device memory, {free / 1e9:.0f} GB free")
+    d = run_bench("--steps", "3", "--warmup", "3", "--reps", "3", timeout=1200)
+    assert BASE_KEYS <= set(d)
+    assert d["config"]["workload"].startswith("C4: 2048x2048x1024") and d["scaling"] == "strong"
+    assert d["value"] > 0 and d["gpu_launches"] == 3 and d["repetitions"]["n"] == 3
+    rf = d["roofline"]
+    assert rf["traffic"] and rf["traffic_source"] and rf["algorithmic_bytes_per_launch"] == 36 * 2048 * 2048 * 1024
+    e = d["e2e"]
+    assert e["steps"] == 200 and e["value"] > 0
+    assert e["h2d_bytes_per_step"] == 3 * 4 * 2048 * 2048 * 1024 // 200
+    assert d["cpu_baseline"]["sample"].count("256x256x128") == 1

@@ -1,10 +1,11 @@
 """Multi-process bootstrap of the fused peer transport over CUDA IPC.
 
 Two processes on cuda:0, each owning one y-slab handle (nranks = 2, nccl_id = NULL),
-run bench.py's own connect path (paper_1410_1387_b200.multi.connect_peer over a gloo
+run bench.py's own rank setup (bench.open_handle -> multi.connect_peer over a gloo
 group): export the IPC blobs, all-gather them, open the neighbour's buffers and flag
-words. The handles must then report the peer transport and the fused one-launch step.
-Nothing is stepped: ranks that wait on one another must not share one GPU
+words. The handles must then report the peer transport and the fused one-launch step,
+and bench.py's N > 1 guards run on them: multi.sync_or_die on the (idle) library stream
+and multi.max_over_ranks with a device tensor. Nothing is stepped: ranks that wait on one another must not share one GPU
 (B200_PROFILING.md), so the stepping protocol itself is covered by the local-group
 GPU tests (same kernels and flag sequence) and the CPU model check
 (tests/test_peer_protocol_cpu.py).
@@ -41,6 +42,16 @@ def _worker(rank, world, port, q):
         before = h.halo_transport
         ok = multi.connect_peer(dist, h, rank, world)
         res = {"before": before, "ok": ok, "after": h.halo_transport, "launches": h.info()["launches_per_step"]}
+        # bench.py's own rank setup and N > 1 guards (no stepping: see the module docstring)
+        import bench
+        import synth
+        cfg = synth.scaled(synth.CONFIGS["C4"](), 64, 192, 24, damp_width=4)
+        wxy, wz, _ = synth.weights_f32(cfg)
+        b = bench.open_handle(cfg, 1e-3, wxy, wz, rank, world, 0, 32, dist, "peer")
+        res["bench_transport"] = b.halo_transport
+        multi.sync_or_die(b, 5.0, "idle stream")   # must return (nothing enqueued)
+        res["max"] = multi.max_over_ranks(dist, world, float(rank) + 0.25, device="cuda")
+        b.close()
         # a blob of the wrong rank is refused
         try:
             h.ipc_connect(h.ipc_export() if rank > 0 else None, h.ipc_export() if rank < world - 1 else None)
@@ -76,5 +87,6 @@ def test_two_process_ipc_connect():
         assert got[r]["after"] == "peer", got
         assert got[r]["launches"] == 1, got   # a multi-process peer rank runs the fused one-launch step
         assert got[r]["self_blob"] == "VTI_E_PARAM", got
+        assert got[r]["bench_transport"] == "peer" and got[r]["max"] == 1.25, got
     for p in procs:
         assert p.exitcode == 0

@@ -196,6 +196,27 @@ def test_planes_api_roundtrip():
         assert np.array_equal(p2, st[0][5:14])
 
 
+def test_model_counts_as_set_only_when_every_plane_was_uploaded():
+    """Uploading the same planes twice must not mark the model set (the
+    never-uploaded planes keep vz2 = 0); the last missing plane completes it."""
+    from paper_1410_1387_b200 import VTIError
+    cfg = small_cfg(40, 20, 30, 4, 4, damp=0)
+    wxy, wz, _ = synth.weights_f32(cfg)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    model = tuple(a.numpy() for a in SF.model_planes(cfg, 0, cfg["nz"]))
+    with make(cfg, dt, wxy, wz) as v:
+        v.set_model_planes(0, *[a[:15] for a in model])
+        v.set_model_planes(0, *[a[:15] for a in model])
+        with pytest.raises(VTIError) as e:
+            v.step(1)
+        assert e.value.name == "VTI_E_STATE"
+        v.set_model_planes(15, *[a[15:29] for a in model])
+        with pytest.raises(VTIError):
+            v.step(1)
+        v.set_model_planes(29, *[a[29:] for a in model])
+        v.step(1)
+
+
 def test_errors_on_gpu_handle():
     from paper_1410_1387_b200 import VTIError
     cfg = small_cfg(40, 20, 30, 4, 4, damp=0)
