@@ -481,7 +481,8 @@ def run_native(args):
     t_ms = statistics.median(reps)
 
     value = npts * args.steps / (t_ms * 1e-3) / 1e9
-    launches = info["launches_per_step"] * args.steps
+    spl = info.get("steps_per_launch", 1)   # > 1: the multi-step small-grid kernel
+    launches = info["launches_per_step"] * (args.steps if spl <= 1 else -(-args.steps // spl))
     pts_rank = cfg["nx"] * info["ny_local"] * cfg["nz"]
     # dominant kernel: the step kernel; one launch per step covers every point of the slab
     kern_ms = t_ms / args.steps
@@ -531,7 +532,8 @@ def run_native(args):
             "clocks": clocks,
             "cpu_baseline": cpu,
             "schedule": {k: info[k] for k in ("tile_x", "tile_y", "producer_warp", "rows_per_thread", "points_per_thread",
-                                              "small_kernel", "zchunk", "grid", "work_items", "launches_per_step")},
+                                              "small_kernel", "zchunk", "grid", "work_items", "launches_per_step",
+                                              "steps_per_launch")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

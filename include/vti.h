@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define VTI_ABI_VERSION 3
+#define VTI_ABI_VERSION 4
 #define VTI_IPC_BYTES 512   /* size of a vti_ipc_export blob */
 
 typedef struct vti_s *vti_t;
@@ -93,6 +93,8 @@ typedef struct {
                                   neighbour with NCCL) */
     int64_t device_bytes;   /* device memory owned by the handle */
     int64_t time_index;     /* n: fields hold u^n and u^{n-1} */
+    int32_t steps_per_launch; /* > 1: the multi-step small-grid kernel, one cooperative launch per
+                                 vti_step call of up to this many steps (single slab, small grids) */
 } vti_info;
 
 /* Library ABI version (VTI_ABI_VERSION). */
@@ -206,6 +208,16 @@ vti_status vti_step_timed(vti_t h, int32_t nsteps, float *ms);
  * own buffers (the protocol of vti_ipc_connect, without IPC). */
 vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps);
 
+/* Local group with the STAGED transport of the NCCL path instead of peer stores:
+ * per step, the edge launch, a pack of the R_xy boundary rows into send buffers,
+ * the exchange on each handle's comm stream (device copies from the neighbours'
+ * send buffers in place of ncclSend/ncclRecv) + unpack into the halo rows,
+ * overlapped with the interior launch; the next step waits on the exchanges.
+ * The same handles, schedules and pack/unpack kernels as vti_step with an
+ * nccl_id, so one GPU can check that path against the oracle. Results are
+ * bitwise those of a single slab. Errors: PARAM, STATE, CUDA. */
+vti_status vti_group_step_staged(vti_t *hs, int32_t n, int32_t nsteps);
+
 /* Copy out u^n (level 0) or the stored u^{n-1} (level 1) of this slab into
  * p, q ([nz][ny_local][nx]; either may be NULL). Synchronises.
  * Note: with damping, the stored u^{n-1} is the undamped previous level
@@ -221,12 +233,32 @@ vti_status vti_get_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, double *p,
  * Receivers (the trace-extraction hook of RTM/FWI,
  * PAPER.md l.18-19): after every subsequent step, the wavefield(s) in
  * field_mask (1 = p, 2 = q, 3 = both) at the n GLOBAL grid points ijk[3r..3r+2]
- * are gathered into a device trace buffer, up to capacity_steps rows
- * (recording then stops silently). Only the receivers inside this rank's slab
- * are kept (vti_receiver_info lists them). A new call replaces the set and
- * restarts the recording. n = 0 removes all receivers. Errors: PARAM, INDEX, CUDA.
+ * are written to a device trace buffer, one row per step, up to capacity_steps
+ * rows (recording then stops silently). The gather is fused into the step
+ * kernel's store epilogue (no extra launch; CUDA-graph replays of small grids
+ * stay on). Only the receivers inside this rank's slab are kept
+ * (vti_receiver_info lists them); duplicates are allowed. A new call replaces the
+ * set and restarts the recording. n = 0 removes all receivers.
+ * Errors: PARAM, INDEX, CUDA.
  */
 vti_status vti_set_receivers(vti_t h, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t capacity_steps);
+
+/*
+ * Trace injection (N4: the backward leg of RTM/FWI re-injects recorded traces,
+ * PAPER.md l.18-19; the forcing term of Eq. 1 generalised to n points): at the
+ * step that evaluates F(u^n) (time index n, also after vti_reverse), if
+ * t_first <= n < t_first + nt, traces[(n - t_first) * n + r] is added into F_p
+ * (field_mask bit 1) and/or F_q (bit 2) at the GLOBAL grid point ijk[3r..3r+2],
+ * after the Ricker source of vti_add_source (same operation order as the oracle).
+ * traces: [nt][n] of the handle's precision, host or device pointer, copied
+ * (the library owns the device copy). Points must be distinct; only those in
+ * this rank's slab are injected. A new call replaces the set; n = 0 removes it.
+ * Errors: PARAM (NULL, mask, nt < 0, duplicate points, wrong precision), INDEX, CUDA.
+ */
+vti_status vti_set_injection(vti_t h, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t nt,
+                             int64_t t_first, const float *traces);
+vti_status vti_set_injection_f64(vti_t h, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t nt,
+                                 int64_t t_first, const double *traces);
 
 /* Local receiver count, rows recorded so far, and (ids != NULL, n_local entries)
  * the caller's index of each local receiver. */
@@ -240,10 +272,15 @@ vti_status vti_get_traces_f64(vti_t h, double *out);
 /*
  * Time reversal (N4, the backward propagation of RTM): swap the two stored
  * levels, so the next vti_step applies Eq. 3 backwards,
- * u^{n-1} = g (2 u^n - g u^{n+1} + dt^2 F(u^n)), with s(t^n) at the current
- * level and the time index decreasing. Without damping (W = 0) this is the
- * exact inverse of forward stepping up to rounding; calling it again restores
- * forward stepping. vti_time_index() is the current level throughout.
+ * u^{n-1} = g (2 u^n - g u^{n+1} + dt^2 F(u^n)), with s(t^n) and the injection
+ * row of time index n at the current level and the time index decreasing.
+ * Without damping (W = 0) this is the exact inverse of forward stepping up to
+ * rounding; calling it again restores forward stepping. vti_time_index() is the
+ * current level throughout. Note: this is time reversal of the SAME operator, not
+ * its adjoint (transpose): F's z operator D has per-plane weights w^z[k] (Eq. 5),
+ * so D^T != D on a variable-dz grid, and the vx2/vn2/vz2 factors multiply on the
+ * other side in A^T. An adjoint-state FWI gradient needs A^T; RTM with the
+ * self-adjoint isotropic limit (eps = delta = 0, uniform dz) does not.
  */
 vti_status vti_reverse(vti_t h);
 

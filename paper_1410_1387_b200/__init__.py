@@ -74,7 +74,7 @@ class Info(C.Structure):
         ("tile_x", C.c_int32), ("tile_y", C.c_int32), ("rows_per_thread", C.c_int32), ("producer_warp", C.c_int32),
         ("points_per_thread", C.c_int32), ("small_kernel", C.c_int32), ("zchunk", C.c_int32), ("grid", C.c_int32),
         ("work_items", C.c_int32), ("launches_per_step", C.c_int32),
-        ("device_bytes", C.c_int64), ("time_index", C.c_int64),
+        ("device_bytes", C.c_int64), ("time_index", C.c_int64), ("steps_per_launch", C.c_int32),
     ]
 
     def as_dict(self):
@@ -113,6 +113,7 @@ def _load():
         "vti_step": (st, [H, C.c_int32]),
         "vti_step_timed": (st, [H, C.c_int32, C.POINTER(C.c_float)]),
         "vti_group_step": (st, [C.POINTER(H), C.c_int32, C.c_int32]),
+        "vti_group_step_staged": (st, [C.POINTER(H), C.c_int32, C.c_int32]),
         "vti_get_fields": (st, [H, P, P, C.c_int32]),
         "vti_get_fields_planes": (st, [H, C.c_int32, C.c_int32, P, P, C.c_int32]),
         "vti_sync": (st, [H]),
@@ -123,6 +124,8 @@ def _load():
         "vti_set_tuning": (st, [H, C.c_int32, C.c_int32]),
         "vti_set_variant": (st, [H, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
         "vti_set_receivers": (st, [H, C.c_int32, P, C.c_int32, C.c_int32]),
+        "vti_set_injection": (st, [H, C.c_int32, P, C.c_int32, C.c_int32, C.c_int64, P]),
+        "vti_set_injection_f64": (st, [H, C.c_int32, P, C.c_int32, C.c_int32, C.c_int64, P]),
         "vti_receiver_info": (st, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32), P]),
         "vti_get_traces": (st, [H, P]),
         "vti_get_traces_f64": (st, [H, P]),
@@ -325,6 +328,20 @@ class VTI:
                                              capacity_steps))
         self._rec_fields = (fields & 1) + ((fields >> 1) & 1)
 
+    def set_injection(self, ijk, traces, fields=1, t_first=0):
+        """vti_set_injection: add traces[n - t_first][r] into F_p (fields bit 1) / F_q (bit 2) at
+        the distinct global points ijk[r] at the step evaluating time index n. traces: [nt][n]
+        numpy array or torch tensor (host or CUDA) of the handle's precision; ijk empty = remove."""
+        a = np.ascontiguousarray(np.asarray(ijk, dtype=np.int32).reshape(-1, 3))
+        n = a.shape[0]
+        if n == 0:
+            _check(self.h, self._fn("vti_set_injection")(self.h, 0, None, fields, 0, 0, None))
+            return
+        nt = int(traces.shape[0]) if len(traces.shape) else 0
+        tp, keep = _ptr(traces, nt * n, dtype=self.dtype)
+        _check(self.h, self._fn("vti_set_injection")(self.h, n, a.ctypes.data, fields, nt, int(t_first), tp))
+        del keep
+
     def receiver_info(self):
         """vti_receiver_info: (local receiver ids, rows recorded so far)."""
         n, t = C.c_int32(), C.c_int32()
@@ -402,10 +419,16 @@ class VTI:
         return r.as_dict()
 
 
-def group_step(handles, nsteps=1):
-    """Local-group stepping of handles created with nranks=len(handles), nccl_id=None."""
+def group_step(handles, nsteps=1, transport="peer"):
+    """Local-group stepping of handles created with nranks=len(handles), nccl_id=None.
+
+    transport="peer": the fused peer-store halo transport (vti_group_step);
+    "staged": the NCCL path's pack / exchange / unpack with device copies in place of
+    ncclSend/ncclRecv (vti_group_step_staged).
+    """
     arr = (C.c_void_p * len(handles))(*[h.h for h in handles])
-    st = lib.vti_group_step(arr, len(handles), nsteps)
+    fn = {"peer": lib.vti_group_step, "staged": lib.vti_group_step_staged}[transport]
+    st = fn(arr, len(handles), nsteps)
     if st != 0:
         for h in handles:
             msg = lib.vti_last_error(h.h)

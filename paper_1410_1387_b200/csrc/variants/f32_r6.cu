@@ -2,6 +2,6 @@
 // producer warp is 16 warps -> 128 registers for the 13-deep queue, no spills.
 #include "../vti_entry.cuh"
 VTI_TABLE(vti_variants_f32_r6,
-          (entry<float, 6, 6, 30, 1, 1, 3, 1>()), (entry<float, 6, 6, 32, 1, 0, 3, 1>()),
+          (entry_io<float, 6, 6, 30, 1, 1, 3, 1>()), (entry<float, 6, 6, 32, 1, 0, 3, 1>()),
           (entry<float, 6, 6, 32, 1, 1, 3, 1>()), (entry<float, 6, 6, 16, 1, 0, 3, 2>()),
           (entry<float, 6, 6, 30, 2, 1, 3, 1, 2>()))

@@ -6,7 +6,7 @@
 // x 4 stages 69.7).
 #include "../vti_entry.cuh"
 VTI_TABLE(vti_variants_f64_r12,
-          (entry<double, 12, 8, 8, 1, 1, 4, 1, 2>()), (entry<double, 12, 8, 10, 1, 1, 3, 1, 2>()),
+          (entry_io<double, 12, 8, 8, 1, 1, 4, 1, 2>()), (entry<double, 12, 8, 10, 1, 1, 3, 1, 2>()),
           (entry<double, 12, 8, 15, 1, 1, 3, 1, 2>()), (entry<double, 12, 8, 16, 1, 0, 2, 1, 2>()),
           (entry<double, 12, 8, 14, 1, 1, 3, 1>()), (entry<double, 12, 8, 16, 1, 1, 2, 1>()),
           (entry<double, 12, 8, 16, 1, 0, 2, 1>()))

@@ -5,11 +5,11 @@
 // 16-row tiles so three stages fit in shared memory.
 #include "../vti_entry.cuh"
 VTI_TABLE(vti_variants_f64_r48,
-          (entry<double, 4, 4, 15, 1, 1, 3, 1, 2>()), (entry<double, 4, 4, 16, 1, 0, 3, 1, 2>()),
+          (entry_io<double, 4, 4, 15, 1, 1, 3, 1, 2>()), (entry<double, 4, 4, 16, 1, 0, 3, 1, 2>()),
           (entry<double, 4, 4, 16, 1, 1, 3, 1, 2>()),
           (entry<double, 4, 4, 16, 1, 1, 3, 1>()), (entry<double, 4, 4, 16, 1, 0, 3, 1>()),
           (entry<double, 4, 4, 14, 1, 1, 3, 1>()),
-          (entry<double, 8, 4, 15, 1, 1, 3, 1, 2>()), (entry<double, 8, 4, 16, 1, 0, 3, 1, 2>()),
+          (entry_io<double, 8, 4, 15, 1, 1, 3, 1, 2>()), (entry<double, 8, 4, 16, 1, 0, 3, 1, 2>()),
           (entry<double, 8, 4, 16, 1, 1, 3, 1, 2>()),
           (entry<double, 8, 4, 16, 1, 1, 3, 1>()), (entry<double, 8, 4, 16, 1, 0, 3, 1>()),
           (entry<double, 8, 4, 14, 1, 1, 3, 1>()))

@@ -3,6 +3,6 @@
 // TY = 14 mapping, which runs 8 warps at 244 registers).
 #include "../vti_entry.cuh"
 VTI_TABLE(vti_variants_f64_r6,
-          (entry<double, 6, 6, 15, 1, 1, 3, 1, 2>()), (entry<double, 6, 6, 16, 1, 0, 3, 1, 2>()),
+          (entry_io<double, 6, 6, 15, 1, 1, 3, 1, 2>()), (entry<double, 6, 6, 16, 1, 0, 3, 1, 2>()),
           (entry<double, 6, 6, 14, 1, 1, 3, 1>()), (entry<double, 6, 6, 16, 1, 0, 3, 1>()),
           (entry<double, 6, 6, 16, 1, 1, 3, 1>()))

@@ -9,7 +9,10 @@ static SmallEntry small_entry()
 {
     using namespace vti;
     return SmallEntry{(int)sizeof(T), R, RZ, TY, (const void *)vti_small_kernel<T, R, RZ, TY>,
-                      SmallCfg<T, R, RZ, TY>::SMEM, SmallCfg<T, R, RZ, TY>::THREADS};
+                      (const void *)vti_small_kernel<T, R, RZ, TY, true>,
+                      (const void *)vti_small_multi_kernel<T, R, RZ, TY>,
+                      (const void *)vti_small_multi_kernel<T, R, RZ, TY, true>, SmallCfg<T, R, RZ, TY>::SMEM,
+                      SmallCfg<T, R, RZ, TY>::THREADS};
 }
 
 SmallTable vti_small_kernels()

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -50,6 +51,14 @@ struct NcclApi {
 };
 
 NcclApi &nccl();
+
+// ============================================================ N4 point sets
+// CSR over (plane k, local row yl) of (x, column) entries sorted by x (StepParams::inj_* / rec_*).
+struct DevPointSet {
+    int *off = nullptr;    // device [nz * nyl + 1]
+    int2 *ent = nullptr;   // device [n]
+    int n = 0;
+};
 
 // ============================================================ handle
 struct vti_s {
@@ -96,6 +105,15 @@ struct vti_s {
     CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
     CUtensorMap tm_qcol[2];                   // q^n column views (box depth 2 R_z + 1) for the small-grid kernel
     const SmallEntry *small = nullptr;        // small-grid kernel in use (single slab, 1-plane items), or NULL
+    // multi-step small-grid kernel (vti_small_multi_kernel): one cooperative launch per vti_step
+    // call (chunks of MULTI_MAX steps); done[] = per-item epoch counters, multi_epoch their value
+    int multi_slots = 0;                      // co-resident multi-step CTAs on the device
+    bool multi_enabled = false;               // env VTI_MULTI=1 enables (measured slower than graph
+                                              // replays of the one-step kernel on C1)
+    unsigned int *done = nullptr;
+    int done_items = 0;
+    unsigned int multi_epoch = 0;
+    void *s_multi = nullptr;                  // device: s(t^n) of each step of a launch
     bool explicit_variant = false;            // env VTI_TY/WP/RPT/PX or vti_set_variant / vti_autotune chose K
     double cxy[MAX_R + 1] = {0};              // w^xy / h^2 in double; rounded to T at launch (reading c3)
     int cur = 0;                              // pbuf[cur], qbuf[cur] hold u^n
@@ -131,11 +149,19 @@ struct vti_s {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // by starting parity (cur)
     void *s_graph = nullptr;                  // device: GRAPH_STEPS source samples of T
     std::vector<double> s_host;
+    // N4 point sets of this slab, gathered / injected inside the step
+    // kernels' IO instantiations (StepParams::inj_* / rec_*)
+    DevPointSet rec_set, inj_set;
     // receivers (this slab's subset, in the caller's order)
     int nrec = 0, rec_mask = 0, rec_cap = 0, rec_steps = 0;
-    long long *rec_off = nullptr;             // device: element offsets in an interior view
     void *traces = nullptr;                   // device: [rec_cap][nrec][nf] of T
     std::vector<int32_t> rec_ids;             // global receiver index of each local receiver
+    // trace injection: rows [0, inj_nt) of inj_tr = time indices inj_t_first.., inj_cols columns
+    void *inj_tr = nullptr;                   // device: [inj_nt][inj_cols] of T
+    int inj_cols = 0, inj_mask = 0, inj_nt = 0;
+    int64_t inj_t_first = 0;
+    long long *dyn = nullptr;                 // device: graph-replay header {inj row, rec row, dir}
+    bool io_active() const { return (rec_set.n > 0 && rec_cap > 0) || inj_set.n > 0; }
 
     size_t total_elems() const { return (size_t)cfg.nz * rows * nxp; }
     char *in(void *base) const { return (char *)base + (long long)R * ys * es; }   // interior view
@@ -167,7 +193,8 @@ void choose_schedule(vti_s *h);                 // z-chunks and CTA caps of the 
 // vti_runtime.cu
 vti_status launch_edge(vti_s *h);               // tile rows the neighbours receive (PEER kernel when connected)
 vti_status launch_interior(vti_s *h);
-vti_status record(vti_s *h);                    // receiver gather after a step
+void advance_records(vti_s *h, int steps);      // receiver rows written by `steps` steps (fused in the kernel)
+vti_status prepare_io(vti_s *h);                // an IO-capable step kernel while a point set is active
 vti_status check_finite(vti_s *h);              // check_every: INSTABILITY on a non-finite value
 
 // vti_transport.cu

@@ -137,7 +137,63 @@ struct StepParams {
     unsigned long long edge_target;
     unsigned int *sig[4];
     unsigned int sig_val[4];
+    // N4 point sets (IO kernels only; NULL = none), SURVEY.md 8(f) N4. Each is a CSR over
+    // (plane k, local row yl): entries ent[off[k*nyl + yl] .. off[k*nyl + yl + 1]) = (x, column),
+    // sorted by x.
+    //  * injection: inj_tr[row * inj_cols + column] is added into F_p (inj_mask bit 1) / F_q
+    //    (bit 2) after the Ricker source; row = the time index n - t_first of this step;
+    //  * receivers: the u^{n+1} just computed goes to rec_tr[(row * rec_cols + column) * nf + f]
+    //    (p before q, nf = fields in rec_mask).
+    // Rows: direct launches pass inj_row / rec_row; graph replays read dyn[0] + graph_i * dyn[2]
+    // and dyn[1] + graph_i (the header refilled before each replay). Rows outside
+    // [0, inj_nt) / [0, rec_cap) are skipped.
+    const int *inj_off;
+    const int2 *inj_ent;
+    const T *inj_tr;
+    int inj_cols, inj_mask, inj_nt;
+    long long inj_row;
+    const int *rec_off;
+    const int2 *rec_ent;
+    T *rec_tr;
+    int rec_cols, rec_mask, rec_cap;
+    long long rec_row;
+    const long long *dyn;
+    int graph_i;
 };
+
+// ---------------------------------------------------------------- N4 point-set helpers
+template <typename PP>
+__device__ __forceinline__ long long inj_row_of(const PP &P)
+{
+    return P.dyn ? P.dyn[0] + (long long)P.graph_i * P.dyn[2] : P.inj_row;
+}
+template <typename PP>
+__device__ __forceinline__ long long rec_row_of(const PP &P)
+{
+    return P.dyn ? P.dyn[1] + P.graph_i : P.rec_row;
+}
+
+// Does the tile (rows [y0, y0 + ty) of plane k) hold any entry of the set? (CTA-uniform)
+__device__ __forceinline__ bool ps_tile_any(const int *off, int nyl, int k, int y0, int ty)
+{
+    const long long b = (long long)k * nyl;
+    return off[b + y0] != off[b + min(y0 + ty, nyl)];
+}
+
+// First entry of row (k, yl) with x >= x0, and the row's end.
+__device__ __forceinline__ void ps_row_range(const int *off, const int2 *ent, int nyl, int k, int yl, int x0,
+                                             int &e, int &e_end)
+{
+    const long long b = (long long)k * nyl + yl;
+    int lo = off[b], hi = off[b + 1];
+    e_end = hi;
+    while (lo < hi) {   // lower bound of x0
+        const int mid = (lo + hi) >> 1;
+        if (ent[mid].x < x0) lo = mid + 1;
+        else hi = mid;
+    }
+    e = lo;
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -250,6 +306,11 @@ template <> __device__ __forceinline__ Vec<double, 2> ldv<2>(const double *p)
 {
     return Vec<double, 2>{*reinterpret_cast<const double2 *>(p)};
 }
+__device__ __forceinline__ V4<float> v4_of(const float (&a)[4]) { return V4<float>{make_float4(a[0], a[1], a[2], a[3])}; }
+__device__ __forceinline__ V4<double> v4_of(const double (&a)[4])
+{
+    return V4<double>{make_double2(a[0], a[1]), make_double2(a[2], a[3])};
+}
 __device__ __forceinline__ V4<float> lds4(const float *p) { return ldv<4>(p); }
 __device__ __forceinline__ V4<double> lds4(const double *p) { return ldv<4>(p); }
 
@@ -349,6 +410,46 @@ struct Producer {
     }
 };
 
+// N4 receivers: this thread's points of u^{n+1} (rows yr .. yr + RPT - 1, columns xg ..
+// xg + PX - 1 of plane k) that are receivers go to their trace row (a tile-uniform early out
+// keeps planes without receivers free).
+template <typename T, int RPT, int PX>
+__device__ __forceinline__ void record_points_row(const StepParams<T> &P, int k, int y0, int ty, int yr, int xg,
+                                                  long long row, const T (&pn)[RPT][PX], const T (&qn)[RPT][PX])
+{
+    if (P.rec_off == nullptr || !ps_tile_any(P.rec_off, P.nyl, k, y0, ty)) return;
+    if (row < 0 || row >= P.rec_cap) return;
+    const int nf = (P.rec_mask & 1) + ((P.rec_mask >> 1) & 1);
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int yl = yr + r;
+        if (yl >= P.nyl || xg >= P.nx) continue;
+        int e, e_end;
+        ps_row_range(P.rec_off, P.rec_ent, P.nyl, k, yl, xg, e, e_end);
+        for (; e < e_end; ++e) {
+            const int2 en = P.rec_ent[e];
+            if (en.x >= xg + PX) break;
+            T vp = pn[r][0], vq = qn[r][0];
+#pragma unroll
+            for (int c = 1; c < PX; ++c)
+                if (en.x == xg + c) {
+                    vp = pn[r][c];
+                    vq = qn[r][c];
+                }
+            T *o = P.rec_tr + (row * P.rec_cols + en.y) * nf;
+            if (P.rec_mask & 1) *o++ = vp;
+            if (P.rec_mask & 2) *o = vq;
+        }
+    }
+}
+
+template <typename T, int RPT, int PX>
+__device__ __forceinline__ void record_points(const StepParams<T> &P, int k, int y0, int ty, int yr, int xg,
+                                              const T (&pn)[RPT][PX], const T (&qn)[RPT][PX])
+{
+    record_points_row<T, RPT, PX>(P, k, y0, ty, yr, xg, rec_row_of(P), pn, qn);
+}
+
 // ---------------------------------------------------------------- the kernel
 // WP = 1: a dedicated producer warp issues every load (consumers never stall
 //         on the ring); 17 warps per TY=32 CTA cap registers at 96.
@@ -357,7 +458,10 @@ struct Producer {
 // PEER: also store the boundary rows into the neighbours' halo rows (StepParams::peer_*);
 // only the edge launch of a peer-connected slab uses it, so the other launches keep
 // the register allocation of the plain kernel.
-template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB, bool PEER, int PX>
+// IO: also the N4 point sets (trace injection into F, receivers gathered from u^{n+1} in the
+// store epilogue; StepParams::inj_* / rec_*). Only the default variant of each radius pair is
+// compiled with IO; the runtime selects it while a point set is active.
+template <typename T, int R, int RZ, int TY, int RPT, int WP, int STAGES, int MINB, bool PEER, int PX, bool IO = false>
 __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
     vti_step_kernel(const __grid_constant__ StepParams<T> P)
 {
@@ -482,6 +586,35 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
                     const T *zr = st + C::OFF_ZR / C::ES;
                     const T gz = zr[NQ];
                     T pn[RPT][PX], qn[RPT][PX];
+                    // N4 injection: this thread's entries of the tile-plane (if any), walked in x order
+                    bool inj_on = false;
+                    const T *inj_base = nullptr;
+                    int inj_e[RPT], inj_end[RPT];
+                    if constexpr (IO) {
+                        if (P.inj_off != nullptr && ps_tile_any(P.inj_off, P.nyl, k, y0, TY)) {
+                            const long long row = inj_row_of(P);
+                            inj_on = row >= 0 && row < P.inj_nt;
+                            inj_base = P.inj_tr + row * P.inj_cols;
+                        }
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) {
+                            inj_e[r] = inj_end[r] = 0;
+                            const int yl = y0 + tg * RPT + r;
+                            if (inj_on && yl < P.nyl) ps_row_range(P.inj_off, P.inj_ent, P.nyl, k, yl, xg, inj_e[r], inj_end[r]);
+                        }
+                    }
+                    // adds the injected sample at column x (if any) to f_p / f_q, after the source
+                    auto inject = [&](int r, int x, T &f_p, T &f_q) {
+                        if constexpr (IO) {
+                            if (!inj_on) return;
+                            while (inj_e[r] < inj_end[r] && P.inj_ent[inj_e[r]].x < x) ++inj_e[r];
+                            if (inj_e[r] < inj_end[r] && P.inj_ent[inj_e[r]].x == x) {
+                                const T v = inj_base[P.inj_ent[inj_e[r]].y];
+                                if (P.inj_mask & 1) f_p = f_p + v;
+                                if (P.inj_mask & 2) f_q = f_q + v;
+                            }
+                        }
+                    };
                     if constexpr (PACKED) {
                         // fp32: the same canonical operation order, lane for lane, on packed pairs
                         // (c0,c1), (c2,c3) -- FADD2 / FMUL2 / FFMA2 round each lane exactly like
@@ -553,6 +686,10 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
                                         if (P.src_mask & 2) Fq.x = __fadd_rn(Fq.x, sv);
                                     }
                                 }
+                                if constexpr (IO) {
+                                    inject(r, xg + c, Fp.x, Fq.x);
+                                    inject(r, xg + c + 1, Fp.y, Fq.y);
+                                }
                                 const float2 gxy2 = make_float2(gxy[r][c], gxy[r][c + 1]);
                                 const float2 g = __fmul2_rn(gxy2, gz2);     // (gx gy) gz
                                 const float2 ng = __fmul2_rn(gxy2, ngz2);   // -g exactly (sign-symmetric RN)
@@ -619,6 +756,7 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
                                     if (P.src_mask & 1) Fp = Fp + sv;
                                     if (P.src_mask & 2) Fq = Fq + sv;
                                 }
+                                if constexpr (IO) inject(r, xg + c, Fp, Fq);
                                 const T g = gxy[r][c] * gz;   // (gx gy) gz
                                 pn[r][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[r][c]));
                                 qn[r][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * q[r][(u + RZ) % NQ][c]));
@@ -632,6 +770,7 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
                         stage = 0;
                         phase ^= 1;
                     }
+                    if constexpr (IO) record_points<T, RPT, PX>(P, k, y0, TY, y0 + tg * RPT, xg, pn, qn);
 #pragma unroll
                     for (int r = 0; r < RPT; ++r) {
                         if (store_ok[r]) {

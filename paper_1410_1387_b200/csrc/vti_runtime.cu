@@ -52,6 +52,19 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, 
     return nullptr;
 }
 
+// The IO-capable variant (N4 point sets) of a radius pair: the default entry of its table.
+static const KernelEntry *find_io_kernel(int esize, int r, int rz)
+{
+    for (int ty : {32, 30, 16, 15, 14, 12, 10, 8})
+        for (int wp : {1, 0})
+            for (int rpt : {1, 2})
+                for (int px : {4, 2}) {
+                    const KernelEntry *e = find_kernel(esize, r, rz, ty, wp, rpt, px);
+                    if (e && e->fn_io) return e;
+                }
+    return nullptr;
+}
+
 static const SmallEntry *find_small(int esize, int r, int rz, int ty)
 {
     static const SmallTable t = vti_small_kernels();
@@ -144,22 +157,6 @@ __global__ void k_check_finite(const T *__restrict__ p, const T *__restrict__ q,
         bad |= !isfinite(p[a]) || !isfinite(q[a]);
     }
     if (bad) atomicOr(flag, 1u);
-}
-
-// Halo transport of p: rows [row0, row0 + R) of a halo'd buffer (row index
-// counted from the first halo row) <-> a contiguous [nz][R][nx] buffer.
-// Receivers: after each step, gather u^n at the receiver
-// points (interior-view element offsets) into trace row t: out[t][r][f].
-template <typename T>
-__global__ void k_record(const T *__restrict__ p, const T *__restrict__ q, const long long *__restrict__ off, int n,
-                         int mask, T *__restrict__ out)
-{
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const int nf = (mask & 1) + ((mask >> 1) & 1);
-    int f = 0;
-    if (mask & 1) out[(size_t)r * nf + f++] = p[off[r]];
-    if (mask & 2) out[(size_t)r * nf + f] = q[off[r]];
 }
 
 static std::mutex g_err_mu;
@@ -304,8 +301,15 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->sync_ctr);
     cudaFree(h->edge_ctr);
     cudaFree(h->flags);
-    cudaFree(h->rec_off);
+    for (DevPointSet *ps : {&h->rec_set, &h->inj_set}) {
+        cudaFree(ps->off);
+        cudaFree(ps->ent);
+    }
     cudaFree(h->traces);
+    cudaFree(h->inj_tr);
+    cudaFree(h->dyn);
+    cudaFree(h->done);
+    cudaFree(h->s_multi);
     for (int b = 0; b < 2; ++b)
         if (h->gexec[b]) cudaGraphExecDestroy(h->gexec[b]);
     cudaFree(h->s_graph);
@@ -347,8 +351,8 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
     h->TY = K->ty;
     h->nty = (h->nyl + h->TY - 1) / h->TY;
     h->smem_bytes = K->stages * K->stage_bytes + 2 * K->stages * 8;
-    CU(h, cudaFuncSetAttribute(K->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
-    CU(h, cudaFuncSetAttribute(K->fn_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
+    for (const void *fn : {K->fn, K->fn_peer, K->fn_io, K->fn_peer_io})
+        if (fn) CU(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
     CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas_per_sm, K->fn, K->threads, h->smem_bytes));
     if (h->ctas_per_sm < 1) return fail(h, VTI_E_CUDA, "step kernel cannot be resident (smem %d B)", h->smem_bytes);
     if (h->tune_ctas > 0) h->ctas_per_sm = std::min(h->ctas_per_sm, h->tune_ctas);
@@ -385,11 +389,25 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
             if ((s = encode(h, &h->tm_qcol[b], h->q_int(b), h->nyl, TX, h->TY, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             NQ)) != VTI_OK)
                 return s;
-        CU(h, cudaFuncSetAttribute(se->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, se->smem));
+        for (const void *fn : {se->fn, se->fn_io, se->fn_multi, se->fn_multi_io})
+            CU(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, se->smem));
         h->small = se;
         h->zchunk = 1;   // the small kernel's items are (tile, plane)
         h->nzc = h->cfg.nz;
         h->grid = h->ntx * h->nty * h->nzc;
+        // multi-step form: every item's CTA must be co-resident (cooperative launch)
+        int per_sm = 0, per_sm_io = 0;
+        CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, se->fn_multi, se->threads, se->smem));
+        CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_io, se->fn_multi_io, se->threads, se->smem));
+        h->multi_slots = std::min(per_sm, per_sm_io) * h->sms;
+        if (h->done_items != h->grid) {   // fresh epoch counters for this item count
+            cudaFree(h->done);
+            h->done = nullptr;
+            CU(h, cudaMalloc((void **)&h->done, (size_t)h->grid * sizeof(unsigned int)));
+            CU(h, cudaMemset(h->done, 0, (size_t)h->grid * sizeof(unsigned int)));
+            h->done_items = h->grid;
+            h->multi_epoch = 0;
+        }
     }
     return VTI_OK;
 }
@@ -484,6 +502,7 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     if (const char *e = getenv("VTI_FUSED_STEP")) h->fused_env = atoi(e) != 0;
     if (const char *e = getenv("VTI_ALIGN")) h->align_rounds = atoi(e) != 0;
     if (const char *e = getenv("VTI_GRAPH")) h->graph_enabled = atoi(e) != 0;
+    if (const char *e = getenv("VTI_MULTI")) h->multi_enabled = atoi(e) != 0;
     if (cfg->nranks > 1) {
         const size_t hb = (size_t)cfg->nz * h->R * cfg->nx * h->es;
         for (int b = 0; b < 2; ++b) {
@@ -756,6 +775,25 @@ static void fill_params(vti_s *h, StepParams<T> &P, int tr0, int ntr0, int tr1, 
         P.sig[i] = nullptr;
         P.sig_val[i] = 0;
     }
+    // N4 point sets (read only by the IO instantiations; none during autotune probes)
+    const bool inj = h->inj_set.n > 0 && !h->suppress_src;
+    P.inj_off = inj ? h->inj_set.off : nullptr;
+    P.inj_ent = inj ? h->inj_set.ent : nullptr;
+    P.inj_tr = (const T *)h->inj_tr;
+    P.inj_cols = h->inj_cols;
+    P.inj_mask = h->inj_mask;
+    P.inj_nt = h->inj_nt;
+    P.inj_row = (long long)(h->n - h->inj_t_first);   // F(u^n) at time index n
+    const bool rec = h->rec_set.n > 0 && h->rec_cap > 0 && !h->suppress_src;
+    P.rec_off = rec ? h->rec_set.off : nullptr;
+    P.rec_ent = rec ? h->rec_set.ent : nullptr;
+    P.rec_tr = (T *)h->traces;
+    P.rec_cols = h->nrec;
+    P.rec_mask = h->rec_mask;
+    P.rec_cap = h->rec_cap;
+    P.rec_row = h->rec_steps;
+    P.dyn = nullptr;
+    P.graph_i = 0;
 }
 
 // Fused multi-GPU launch: the interior tile rows after the edge rows, and the flags the
@@ -788,7 +826,10 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
     if (h->capturing) {   // graph node: the source sample comes from the graph's table
         P.s_table = (const T *)h->s_graph;
         P.s_index = h->capture_index;
+        P.dyn = h->dyn;            // N4 trace rows from the replay header
+        P.graph_i = h->capture_index;
     }
+    const bool io = h->io_active() && !h->suppress_src;
     if (h->small && zchunk == 1 && tr0 == 0 && ntr0 == h->nty && ntr1 == 0) {
         // small-grid kernel: one CTA per (tile, plane) item, every load of the item at once
         SmallParams<T> S;
@@ -810,7 +851,7 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
             sl.numAttrs = 1;
         }
         void *sargs[] = {&S};
-        CU(h, cudaLaunchKernelExC(&sl, h->small->fn, sargs));
+        CU(h, cudaLaunchKernelExC(&sl, io ? h->small->fn_io : h->small->fn, sargs));
         return VTI_OK;
     }
     const int grid = std::min(P.items, cap > 0 ? std::min(cap, slots(h)) : slots(h));
@@ -837,7 +878,9 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
     // only tile rows within R of the slab edges store into the neighbours (edge launches)
     const bool peer_rows = (P.peer_lo || P.peer_hi) && (tr0 * h->TY < h->R || (tr0 + ntr0) * h->TY > h->nyl - h->R ||
                                                         (ntr1 > 0 && (tr1 + ntr1) * h->TY > h->nyl - h->R));
-    CU(h, cudaLaunchKernelExC(&lc, peer_rows ? h->K->fn_peer : h->K->fn, args));
+    const void *fn = peer_rows ? (io ? h->K->fn_peer_io : h->K->fn_peer) : (io ? h->K->fn_io : h->K->fn);
+    if (!fn) return fail(h, VTI_E_STATE, "step-kernel variant without the point-set (IO) instantiation");
+    CU(h, cudaLaunchKernelExC(&lc, fn, args));
     return VTI_OK;
 }
 
@@ -898,25 +941,48 @@ vti_status check_finite(vti_s *h)
     return VTI_OK;
 }
 
-// Gather the receivers' u^n (just written) into the next trace row; silently
-// stops when the capacity is reached (vti_get_traces reports the count).
-vti_status record(vti_s *h)
+// Receiver rows written by `steps` steps (the gather itself is fused into the step kernel's
+// store epilogue); recording stops silently at the capacity (vti_get_traces reports the count).
+void advance_records(vti_s *h, int steps)
 {
-    if (h->nrec == 0 || h->rec_steps >= h->rec_cap || h->suppress_src) return VTI_OK;   // not during autotune probes
-    const int nf = (h->rec_mask & 1) + ((h->rec_mask >> 1) & 1);
-    const size_t row = (size_t)h->nrec * nf * h->es;
-    char *dst = (char *)h->traces + (size_t)h->rec_steps * row;
-    const int threads = 128, blocks = (h->nrec + threads - 1) / threads;
-    if (h->es == 8)
-        k_record<double><<<blocks, threads, 0, h->stream>>>((const double *)h->p_int(h->cur),
-                                                            (const double *)h->q_int(h->cur), h->rec_off, h->nrec,
-                                                            h->rec_mask, (double *)dst);
-    else
-        k_record<float><<<blocks, threads, 0, h->stream>>>((const float *)h->p_int(h->cur),
-                                                           (const float *)h->q_int(h->cur), h->rec_off, h->nrec,
-                                                           h->rec_mask, (float *)dst);
-    CU(h, cudaGetLastError());
-    h->rec_steps += 1;
+    if (h->rec_set.n == 0 || h->suppress_src) return;   // not during autotune probes
+    h->rec_steps = std::min(h->rec_cap, h->rec_steps + steps);
+}
+
+// While a point set is active, the step kernel must be an IO instantiation: the small-grid
+// kernel has one for every radius pair; otherwise switch to the pair's default variant (every
+// variant computes the same bits, so only the speed can change).
+vti_status prepare_io(vti_s *h)
+{
+    if (!h->io_active() || h->small || h->K->fn_io) return VTI_OK;
+    const KernelEntry *K = find_io_kernel(h->es, h->R, h->RZ);
+    if (!K) return fail(h, VTI_E_UNSUPPORTED, "no point-set (IO) step kernel for (%d, %d)", h->R, h->RZ);
+    return select_variant(h, K);
+}
+
+// Build the device CSR of a point set: pts = (x, local row, plane, column).
+static vti_status build_point_set(vti_s *h, DevPointSet &ps, std::vector<std::array<int, 4>> pts)
+{
+    cudaFree(ps.off);
+    cudaFree(ps.ent);
+    ps = DevPointSet{};
+    if (pts.empty()) return VTI_OK;
+    std::sort(pts.begin(), pts.end(), [](const std::array<int, 4> &a, const std::array<int, 4> &b) {
+        return a[2] != b[2] ? a[2] < b[2] : a[1] != b[1] ? a[1] < b[1] : a[0] != b[0] ? a[0] < b[0] : a[3] < b[3];
+    });
+    const size_t rows = (size_t)h->cfg.nz * h->nyl;
+    std::vector<int> off(rows + 1, 0);
+    std::vector<int2> ent(pts.size());
+    for (size_t e = 0; e < pts.size(); ++e) {
+        off[(size_t)pts[e][2] * h->nyl + pts[e][1] + 1] += 1;
+        ent[e] = make_int2(pts[e][0], pts[e][3]);
+    }
+    for (size_t r = 0; r < rows; ++r) off[r + 1] += off[r];
+    CU(h, cudaMalloc((void **)&ps.off, off.size() * sizeof(int)));
+    CU(h, cudaMemcpy(ps.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CU(h, cudaMalloc((void **)&ps.ent, ent.size() * sizeof(int2)));
+    CU(h, cudaMemcpy(ps.ent, ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    ps.n = (int)pts.size();
     return VTI_OK;
 }
 
@@ -927,37 +993,90 @@ vti_status vti_set_receivers(vti_t h, int32_t n, const int32_t *ijk, int32_t fie
     if (!h) return VTI_E_PARAM;
     if (n < 0 || capacity_steps < 0 || (n > 0 && !ijk)) return fail(h, VTI_E_PARAM, "bad receiver arguments");
     if (n > 0 && (field_mask < 1 || field_mask > 3)) return fail(h, VTI_E_PARAM, "field_mask must be 1, 2 or 3");
-    std::vector<long long> off;
+    std::vector<std::array<int, 4>> pts;   // (x, local row, plane, local receiver index)
     std::vector<int32_t> ids;
     for (int r = 0; r < n; ++r) {
         const int i = ijk[3 * r], j = ijk[3 * r + 1], k = ijk[3 * r + 2];
         if (i < 0 || i >= h->cfg.nx || j < 0 || j >= h->cfg.ny || k < 0 || k >= h->cfg.nz)
             return fail(h, VTI_E_INDEX, "receiver %d (%d,%d,%d) outside the grid", r, i, j, k);
         if (j < h->y0 || j >= h->y0 + h->nyl) continue;   // another rank's slab
-        off.push_back((long long)(j - h->y0) * h->ys + (long long)k * h->zs + i);
+        pts.push_back({i, j - h->y0, k, (int)ids.size()});
         ids.push_back(r);
     }
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaStreamSynchronize(h->stream));
-    cudaFree(h->rec_off);
+    CU(h, cudaStreamSynchronize(h->comm));
+    invalidate_graphs(h);   // the point set is baked into graph nodes
     cudaFree(h->traces);
-    for (int b = 0; b < 2; ++b)
-        if (h->gexec[b]) cudaGraphExecDestroy(h->gexec[b]);
-    cudaFree(h->s_graph);
-    h->rec_off = nullptr;
     h->traces = nullptr;
-    h->nrec = (int)off.size();
+    h->nrec = (int)ids.size();
     h->rec_ids = ids;
     h->rec_mask = field_mask;
     h->rec_cap = capacity_steps;
     h->rec_steps = 0;
+    vti_status s = build_point_set(h, h->rec_set, capacity_steps > 0 ? pts : std::vector<std::array<int, 4>>{});
+    if (s != VTI_OK) return s;
     if (h->nrec > 0 && capacity_steps > 0) {
         const int nf = (field_mask & 1) + ((field_mask >> 1) & 1);
-        CU(h, cudaMalloc((void **)&h->rec_off, off.size() * sizeof(long long)));
-        CU(h, cudaMemcpy(h->rec_off, off.data(), off.size() * sizeof(long long), cudaMemcpyHostToDevice));
         CU(h, cudaMalloc(&h->traces, (size_t)capacity_steps * h->nrec * nf * h->es));
+        CU(h, cudaMemset(h->traces, 0, (size_t)capacity_steps * h->nrec * nf * h->es));
     }
     return VTI_OK;
+}
+
+static vti_status set_injection(vti_s *h, int es, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t nt,
+                                int64_t t_first, const void *traces)
+{
+    if (!h) return VTI_E_PARAM;
+    vti_status s = check_precision(h, es, "vti_set_injection");
+    if (s != VTI_OK) return s;
+    if (n < 0 || nt < 0 || (n > 0 && (!ijk || (nt > 0 && !traces))))
+        return fail(h, VTI_E_PARAM, "bad injection arguments");
+    if (n > 0 && (field_mask < 1 || field_mask > 3)) return fail(h, VTI_E_PARAM, "field_mask must be 1, 2 or 3");
+    std::vector<std::array<int, 4>> pts;   // (x, local row, plane, column = caller's index r)
+    std::vector<long long> keys;
+    for (int r = 0; r < n; ++r) {
+        const int i = ijk[3 * r], j = ijk[3 * r + 1], k = ijk[3 * r + 2];
+        if (i < 0 || i >= h->cfg.nx || j < 0 || j >= h->cfg.ny || k < 0 || k >= h->cfg.nz)
+            return fail(h, VTI_E_INDEX, "injection point %d (%d,%d,%d) outside the grid", r, i, j, k);
+        keys.push_back(((long long)k * h->cfg.ny + j) * h->cfg.nx + i);
+        if (j < h->y0 || j >= h->y0 + h->nyl) continue;   // another rank's slab
+        pts.push_back({i, j - h->y0, k, r});
+    }
+    std::sort(keys.begin(), keys.end());
+    if (std::adjacent_find(keys.begin(), keys.end()) != keys.end())
+        return fail(h, VTI_E_PARAM, "injection points must be distinct");
+    CU(h, cudaSetDevice(h->cfg.device));
+    if (traces && is_device_ptr(traces) && (s = order_after_caller(h)) != VTI_OK) return s;
+    CU(h, cudaStreamSynchronize(h->stream));
+    CU(h, cudaStreamSynchronize(h->comm));
+    invalidate_graphs(h);
+    cudaFree(h->inj_tr);
+    h->inj_tr = nullptr;
+    h->inj_cols = n;
+    h->inj_mask = field_mask;
+    h->inj_nt = nt;
+    h->inj_t_first = t_first;
+    const bool any = !pts.empty() && nt > 0;
+    if ((s = build_point_set(h, h->inj_set, any ? pts : std::vector<std::array<int, 4>>{})) != VTI_OK) return s;
+    if (any) {
+        const size_t bytes = (size_t)nt * n * h->es;
+        CU(h, cudaMalloc(&h->inj_tr, bytes));
+        CU(h, cudaMemcpy(h->inj_tr, traces, bytes, cudaMemcpyDefault));   // host or device source
+    }
+    return VTI_OK;
+}
+
+vti_status vti_set_injection(vti_t h, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t nt,
+                             int64_t t_first, const float *traces)
+{
+    return set_injection(h, 4, n, ijk, field_mask, nt, t_first, traces);
+}
+
+vti_status vti_set_injection_f64(vti_t h, int32_t n, const int32_t *ijk, int32_t field_mask, int32_t nt,
+                                 int64_t t_first, const double *traces)
+{
+    return set_injection(h, 8, n, ijk, field_mask, nt, t_first, traces);
 }
 
 vti_status vti_receiver_info(vti_t h, int32_t *n_local, int32_t *steps_recorded, int32_t *ids)
@@ -1141,7 +1260,7 @@ static constexpr int GRAPH_STEPS = 32;   // even: a replay returns to its starti
 
 static bool graph_eligible(const vti_s *h)
 {
-    if (!h->graph_enabled || h->cfg.nranks > 1 || h->nrec > 0 || h->cfg.check_every > 0 || h->suppress_src ||
+    if (!h->graph_enabled || h->cfg.nranks > 1 || h->cfg.check_every > 0 || h->suppress_src ||
         getenv("VTI_FORCE_SPLIT"))
         return false;
     const long items = (long)h->ntx * h->nty * h->nzc;
@@ -1154,6 +1273,7 @@ static bool graph_eligible(const vti_s *h)
 static vti_status build_graph(vti_s *h, int c)
 {
     if (!h->s_graph) CU(h, cudaMalloc(&h->s_graph, GRAPH_STEPS * 8));
+    if (!h->dyn) CU(h, cudaMalloc((void **)&h->dyn, 3 * sizeof(long long)));
     const int keep_cur = h->cur;
     cudaGraph_t g = nullptr;
     CU(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -1195,10 +1315,86 @@ static vti_status replay_graph(vti_s *h)
         for (int i = 0; i < GRAPH_STEPS; ++i) f[i] = (float)h->s_host[i];   // rounded once, as P.s
         CU(h, cudaMemcpyAsync(h->s_graph, f, sizeof f, cudaMemcpyHostToDevice, h->stream));
     }
+    // N4 trace rows of the replay's first step: injection row n - t_first (then + i * dir),
+    // receiver row rec_steps (then + i); the kernels skip rows outside their ranges
+    const long long hdr[3] = {(long long)(h->n - h->inj_t_first), (long long)h->rec_steps, (long long)h->dir};
+    CU(h, cudaMemcpyAsync(h->dyn, hdr, sizeof hdr, cudaMemcpyHostToDevice, h->stream));
     CU(h, cudaGraphLaunch(h->gexec[h->cur], h->stream));
     h->n += (int64_t)GRAPH_STEPS * h->dir;   // parity (cur) is unchanged after an even number of steps
+    advance_records(h, GRAPH_STEPS);
     return VTI_OK;
 }
+
+}  // extern "C"
+
+// ---- multi-step small-grid kernel (vti_small.cuh): one cooperative launch per chunk of steps
+static constexpr int MULTI_MAX = 1024;
+
+static bool multi_eligible(const vti_s *h)
+{
+    return h->multi_enabled && h->small && h->cfg.nranks == 1 && h->cfg.check_every == 0 && !h->suppress_src &&
+           !h->capturing && !getenv("VTI_FORCE_SPLIT") && h->grid <= h->multi_slots && h->done;
+}
+
+template <typename T>
+static vti_status launch_multi_t(vti_s *h, int nsteps)
+{
+    if (!h->s_multi) CU(h, cudaMalloc(&h->s_multi, MULTI_MAX * sizeof(double)));
+    MultiParams<T> M;
+    const int cur0 = h->cur;
+    for (int c = 0; c < 2; ++c) {   // both buffer parities (fill_params reads h->cur)
+        h->cur = c;
+        fill_params<T>(h, M.P[c], 0, h->nty, 0, 0, 1);
+        M.tm_qcol[c] = h->tm_qcol[c];
+    }
+    h->cur = cur0;
+    M.done = h->done;
+    M.epoch0 = h->multi_epoch;
+    M.nsteps = nsteps;
+    M.cur0 = cur0;
+    M.dir = h->dir;
+    static const int mode = getenv("VTI_MULTI_MODE") ? atoi(getenv("VTI_MULTI_MODE")) : 0;
+    M.mode = mode;
+    const bool owned = h->has_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
+    std::vector<T> sv(nsteps);
+    for (int i = 0; i < nsteps; ++i)   // s(t^n) per step: double on the host, rounded once (reading c7)
+        sv[i] = owned ? (T)(h->src_amp * ricker((double)(h->n + (int64_t)i * h->dir) * h->cfg.dt, h->src_f,
+                                                h->src_t0))
+                      : T(0);
+    CU(h, cudaMemcpyAsync(h->s_multi, sv.data(), nsteps * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+    M.s_table = (const T *)h->s_multi;
+    const bool io = h->io_active();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(h->grid);
+    lc.blockDim = dim3(h->small->threads);
+    lc.dynamicSmemBytes = h->small->smem;
+    lc.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // every item's CTA co-resident: the epoch waits need it
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    void *args[] = {&M};
+    CU(h, cudaLaunchKernelExC(&lc, io ? h->small->fn_multi_io : h->small->fn_multi, args));
+    h->multi_epoch += (unsigned int)nsteps;
+    h->cur = (cur0 + nsteps) & 1;
+    h->n += (int64_t)nsteps * h->dir;
+    advance_records(h, nsteps);
+    return VTI_OK;
+}
+
+static vti_status launch_multi(vti_s *h, int nsteps)
+{
+    for (int done = 0; done < nsteps;) {
+        const int m = std::min(MULTI_MAX, nsteps - done);
+        vti_status s = h->es == 8 ? launch_multi_t<double>(h, m) : launch_multi_t<float>(h, m);
+        if (s != VTI_OK) return s;
+        done += m;
+    }
+    return VTI_OK;
+}
+
+extern "C" {
 
 vti_status vti_prepare(vti_t h)
 {
@@ -1206,7 +1402,7 @@ vti_status vti_prepare(vti_t h)
     if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
     CU(h, cudaSetDevice(h->cfg.device));
     vti_status s;
-    if (graph_eligible(h))   // capture only: nothing executes, the state is untouched
+    if (graph_eligible(h) && !multi_eligible(h))   // capture only: nothing executes, the state is untouched
         for (int c = 0; c < 2; ++c)
             if (!h->gexec[c] && (s = build_graph(h, c)) != VTI_OK) return s;
     return VTI_OK;
@@ -1223,6 +1419,7 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     CU(h, cudaSetDevice(h->cfg.device));
     const bool multi = h->cfg.nranks > 1;
     vti_status s;
+    if ((s = prepare_io(h)) != VTI_OK) return s;
     if (multi && h->halo_dirty) {   // halos of a state set by the caller
         if (h->peer) {
             if ((s = peer_release(h)) != VTI_OK || (s = peer_publish(h)) != VTI_OK) return s;
@@ -1233,6 +1430,11 @@ vti_status vti_step(vti_t h, int32_t nsteps)
             CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
         }
         h->halo_dirty = false;
+    }
+    if (!multi && nsteps >= 2 && multi_eligible(h)) {   // small grids: one cooperative launch for the lot
+        if ((s = launch_multi(h, nsteps)) != VTI_OK) return s;
+        CU(h, cudaGetLastError());
+        return VTI_OK;
     }
     int it = 0;
     if (!multi && nsteps >= GRAPH_STEPS && graph_eligible(h)) {
@@ -1275,7 +1477,7 @@ vti_status vti_step(vti_t h, int32_t nsteps)
         }
         h->cur = 1 - h->cur;
         h->n += h->dir;
-        if ((s = record(h)) != VTI_OK) return s;
+        advance_records(h, 1);
         if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0)
             if ((s = check_finite(h)) != VTI_OK) return s;
     }
@@ -1339,6 +1541,7 @@ vti_status vti_query(vti_t h, vti_info *info)
     }
     info->device_bytes = h->device_bytes;
     info->time_index = h->n;
+    info->steps_per_launch = multi_eligible(h) ? MULTI_MAX : 1;
     return VTI_OK;
 }
 

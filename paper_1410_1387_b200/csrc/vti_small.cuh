@@ -41,13 +41,99 @@ struct SmallCfg {
     static constexpr int THREADS = TY * (TX / 4);   // 16 threads x 4 points per tile row
 };
 
-template <typename T, int R, int RZ, int TY>
+// One tile-plane item's update from its staged data: smem holds the halo'd p^n tile (OFF_P)
+// and the q^n column k - R_z .. k + R_z (OFF_Q), plus vx2 / vn2 / vz2 and the plane's w^z + gz
+// row; pm4 / qm4 are this thread's u^{n-1} (4 points). Returns u^{n+1} in pn / qn and this
+// thread's u^n centre values in pc / qc (the next step's u^{n-1} in the multi-step kernel).
+// s = s(t^n); inj_row / rec_row: the N4 trace rows of this step (IO only).
+template <typename T, int R, int RZ, int TY, bool IO>
+__device__ __forceinline__ void small_update(const StepParams<T> &P, const uint8_t *smem, int y0, int k, int tg,
+                                             int tx, int xg, int yl, const V4<T> &g4, T gyv, T s, long long inj_row,
+                                             long long rec_row, const V4<T> &pm4, const V4<T> &qm4, T (&pn)[1][4],
+                                             T (&qn)[1][4], T (&pc)[4], T (&qc)[4])
+{
+    using C = Cfg<T, R, RZ, TY>;
+    using SC = SmallCfg<T, R, RZ, TY>;
+    constexpr int NQ = C::NQ;
+    constexpr int RA = C::RA;
+    const T *st = reinterpret_cast<const T *>(smem);
+    const int sidx = tg * TX + 4 * tx;
+    const T *prow = st + SC::OFF_P / C::ES + (tg + R) * C::PW + 4 * tx;   // smem row of this tile row
+    const T *pbase = st + SC::OFF_P / C::ES + tg * C::PW + 4 * tx;
+    auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
+    T L[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        pc[c] = wx(RA + c);
+        L[c] = P.cxy[0] * pc[c];
+    }
+#pragma unroll
+    for (int l = 1; l <= R; ++l) {
+        const V4<T> yp = lds4(pbase + (R + l) * C::PW + RA);
+        const V4<T> ym = lds4(pbase + (R - l) * C::PW + RA);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const T xpair = wx(RA + c + l) + wx(RA + c - l);
+            const T ypair = yp[c] + ym[c];
+            L[c] = fma_rn(P.cxy[l], xpair + ypair, L[c]);
+        }
+    }
+    const T *zr = st + SC::OFF_ZR / C::ES;
+    const T gz = zr[NQ];
+    const T *qcol = st + SC::OFF_Q / C::ES + sidx;   // plane m of the column at qcol + m * TX * TY
+    const V4<T> vx4 = lds4(st + SC::OFF_VX / C::ES + sidx);
+    const V4<T> vn4 = lds4(st + SC::OFF_VN / C::ES + sidx);
+    const V4<T> vz4 = lds4(st + SC::OFF_VZ / C::ES + sidx);
+    const V4<T> qc4 = lds4(qcol + RZ * TX * TY);
+    const bool src_here = P.src_mask != 0 && P.src_j == yl && P.src_k == k && P.src_i >= xg && P.src_i < xg + 4;
+    bool inj_on = false;
+    const T *inj_base = nullptr;
+    int inj_e = 0, inj_end = 0;
+    if constexpr (IO) {
+        if (P.inj_off != nullptr && ps_tile_any(P.inj_off, P.nyl, k, y0, TY)) {
+            inj_on = inj_row >= 0 && inj_row < P.inj_nt;
+            inj_base = P.inj_tr + inj_row * P.inj_cols;
+        }
+        if (inj_on && yl < P.nyl) ps_row_range(P.inj_off, P.inj_ent, P.nyl, k, yl, xg, inj_e, inj_end);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        qc[c] = qc4[c];
+        // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
+        T D = zr[0] * lds4(qcol)[c];
+#pragma unroll
+        for (int m = 1; m < NQ; ++m) D = fma_rn(zr[m], lds4(qcol + m * TX * TY)[c], D);
+        const T vD = vz4[c] * D;
+        T Fp = fma_rn(vx4[c], L[c], vD);
+        T Fq = fma_rn(vn4[c], L[c], vD);
+        if (src_here && c == P.src_i - xg) {
+            if (P.src_mask & 1) Fp = Fp + s;
+            if (P.src_mask & 2) Fq = Fq + s;
+        }
+        if constexpr (IO) {
+            if (inj_on) {   // N4 injected sample at column xg + c, after the source
+                while (inj_e < inj_end && P.inj_ent[inj_e].x < xg + c) ++inj_e;
+                if (inj_e < inj_end && P.inj_ent[inj_e].x == xg + c) {
+                    const T v = inj_base[P.inj_ent[inj_e].y];
+                    if (P.inj_mask & 1) Fp = Fp + v;
+                    if (P.inj_mask & 2) Fq = Fq + v;
+                }
+            }
+        }
+        const T g = (g4[c] * gyv) * gz;   // (gx gy) gz
+        pn[0][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[c]));
+        qn[0][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * qc4[c]));
+    }
+    if constexpr (IO) record_points_row<T, 1, 4>(P, k, y0, TY, yl, xg, rec_row, pn, qn);
+}
+
+// IO: also the N4 point sets (injection into F, receivers from u^{n+1}; see StepParams).
+template <typename T, int R, int RZ, int TY, bool IO = false>
 __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
     vti_small_kernel(const __grid_constant__ SmallParams<T> S)
 {
     using C = Cfg<T, R, RZ, TY>;
     using SC = SmallCfg<T, R, RZ, TY>;
-    constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
     const StepParams<T> &P = S.P;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -80,64 +166,162 @@ __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
     const V4<T> g4 = lds4(P.gx + xg);   // generic load (global)
     const T gyv = (yl < P.nyl) ? P.gy[yl] : T(0);
     const bool store_ok = (yl < P.nyl) && (xg < P.nx);
-    const bool src_here = P.src_mask != 0 && P.src_j == yl && P.src_k == k && P.src_i >= xg && P.src_i < xg + 4;
+    const T sv = P.s_table ? P.s_table[P.s_index] : P.s;
     __syncthreads();   // the barrier is initialised before anyone waits on it
     mbar_wait(bar, 0);
 
     const T *st = reinterpret_cast<const T *>(smem);
     const int sidx = tg * TX + 4 * tx;
-    const T *prow = st + SC::OFF_P / C::ES + (tg + R) * C::PW + 4 * tx;   // smem row of this tile row
-    const T *pbase = st + SC::OFF_P / C::ES + tg * C::PW + 4 * tx;
-    auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
-    T pc[4], L[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        pc[c] = wx(RA + c);
-        L[c] = P.cxy[0] * pc[c];
-    }
-#pragma unroll
-    for (int l = 1; l <= R; ++l) {
-        const V4<T> yp = lds4(pbase + (R + l) * C::PW + RA);
-        const V4<T> ym = lds4(pbase + (R - l) * C::PW + RA);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const T xpair = wx(RA + c + l) + wx(RA + c - l);
-            const T ypair = yp[c] + ym[c];
-            L[c] = fma_rn(P.cxy[l], xpair + ypair, L[c]);
-        }
-    }
-    const T *zr = st + SC::OFF_ZR / C::ES;
-    const T gz = zr[NQ];
-    const T *qcol = st + SC::OFF_Q / C::ES + sidx;   // plane m of the column at qcol + m * TX * TY
     const V4<T> pm4 = lds4(st + SC::OFF_PM / C::ES + sidx);
     const V4<T> qm4 = lds4(st + SC::OFF_QM / C::ES + sidx);
-    const V4<T> vx4 = lds4(st + SC::OFF_VX / C::ES + sidx);
-    const V4<T> vn4 = lds4(st + SC::OFF_VN / C::ES + sidx);
-    const V4<T> vz4 = lds4(st + SC::OFF_VZ / C::ES + sidx);
-    const V4<T> qc4 = lds4(qcol + RZ * TX * TY);
-    T pn[4], qn[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
-        T D = zr[0] * lds4(qcol)[c];
-#pragma unroll
-        for (int m = 1; m < NQ; ++m) D = fma_rn(zr[m], lds4(qcol + m * TX * TY)[c], D);
-        const T vD = vz4[c] * D;
-        T Fp = fma_rn(vx4[c], L[c], vD);
-        T Fq = fma_rn(vn4[c], L[c], vD);
-        if (src_here && c == P.src_i - xg) {
-            const T sv = P.s_table ? P.s_table[P.s_index] : P.s;
-            if (P.src_mask & 1) Fp = Fp + sv;
-            if (P.src_mask & 2) Fq = Fq + sv;
-        }
-        const T g = (g4[c] * gyv) * gz;   // (gx gy) gz
-        pn[c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[c]));
-        qn[c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * qc4[c]));
-    }
+    T pn[1][4], qn[1][4], pc[4], qc[4];
+    small_update<T, R, RZ, TY, IO>(P, smem, y0, k, tg, tx, xg, yl, g4, gyv, sv, IO ? inj_row_of(P) : 0,
+                                   IO ? rec_row_of(P) : 0, pm4, qm4, pn, qn, pc, qc);
     if (store_ok) {
         const long long off = (long long)k * P.zs + (long long)yl * P.ys + xg;
-        stv(P.p_out + off, pn);
-        stv(P.q_out + off, qn);
+        stv(P.p_out + off, pn[0]);
+        stv(P.q_out + off, qn[0]);
+    }
+}
+
+// ---------------------------------------------------------------- multi-step small-grid kernel
+// Small grids are latency-bound: each step of vti_small_kernel is one dependent launch (PDL +
+// CUDA graphs still leave ~3.5 us per step on C1). Here ONE cooperative launch advances
+// nsteps steps: every CTA owns one (tile, plane) item for the whole launch, keeps its own u^n
+// and u^{n-1} points in registers (the next step's u^{n-1} is this step's centre), keeps the
+// model and w^z row in shared memory, and before step s waits only for the items it exchanges
+// data with -- tile rows within R_xy, tiles within the x apron, planes within R_z -- to have
+// finished step s-1 (per-item epoch counters, release / acquire at gpu scope). That one wait
+// covers both hazards: their u^s is written (read after write) and they no longer read the
+// u^{s-1} this step overwrites (write after read). Then one TMA round trip brings the halo'd
+// p^n tile and the q^n column. Arithmetic: small_update, i.e. bitwise the one-step kernels.
+template <typename T>
+struct MultiParams {
+    StepParams<T> P[2];        // by buffer parity: P[c] reads buffers c (u^n) and writes 1 - c
+    CUtensorMap tm_qcol[2];    // q^n column views of buffer c
+    unsigned int *done;        // [items] epoch counters (monotone across launches)
+    unsigned int epoch0;       // every counter's value at launch
+    int nsteps;
+    int cur0;                  // parity of step 0
+    int dir;                   // +1 / -1 (vti_reverse): the time index moves by dir per step
+    const T *s_table;          // [nsteps] s(t^n) of each step
+    int mode;                  // synchronisation variant bits (env VTI_MULTI_MODE, measurement switch)
+};
+
+template <typename T, int R, int RZ, int TY, bool IO = false>
+__global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
+    vti_small_multi_kernel(const __grid_constant__ MultiParams<T> M)
+{
+    using C = Cfg<T, R, RZ, TY>;
+    using SC = SmallCfg<T, R, RZ, TY>;
+    constexpr int RA = C::RA;
+    constexpr int NQ = C::NQ;
+    constexpr int DTY = (R + TY - 1) / TY;           // tile rows within R_xy
+    constexpr int DTX = (RA + TX - 1) / TX;          // tiles within the x apron
+    constexpr int NDEP = (2 * DTY + 1) * (2 * DTX + 1) * NQ;
+    static_assert(NDEP <= SC::THREADS, "one polling thread per dependency");
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + SC::OFF_BAR);
+    const StepParams<T> &P0 = M.P[0];
+
+    const int item = blockIdx.x;
+    int x0, y0, kb, ke;
+    decode_item<TY>(P0, item, x0, y0, kb, ke);   // items = ntx * nty * nz, plane k = kb
+    const int k = kb;
+    const int ntx = P0.ntx, nty = P0.ntr0;
+    const int itx = item % ntx, ity = (item / ntx) % nty;
+    // this thread's dependency (if any): item (itx + dx, ity + dy, k + dz)
+    int dep = -1;
+    if (threadIdx.x < NDEP) {
+        const int t = threadIdx.x;
+        const int dz = t % NQ - RZ, dy = (t / NQ) % (2 * DTY + 1) - DTY, dx = t / (NQ * (2 * DTY + 1)) - DTX;
+        const int jx = itx + dx, jy = ity + dy, jz = k + dz;
+        if ((dx | dy | dz) != 0 && jx >= 0 && jx < ntx && jy >= 0 && jy < nty && jz >= 0 && jz < P0.nz)
+            dep = (jz * nty + jy) * ntx + jx;
+    }
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // once per launch: u^{n-1} of this item, the model and the plane's w^z + gz row
+        const StepParams<T> &P = M.P[M.cur0];
+        mbar_arrive_expect_tx(bar, 5 * C::S_BYTES + C::ZROW * C::ES);
+        tma_load_3d(smem + SC::OFF_PM, &P.tm_pm, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_QM, &P.tm_qm, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_VX, &P.tm_vx, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_VN, &P.tm_vn, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_VZ, &P.tm_vz, x0, y0, k, bar);
+        bulk_load(smem + SC::OFF_ZR, P0.zrow + (size_t)k * C::ZROW, C::ZROW * C::ES, bar);
+    }
+    const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
+    const int xg = x0 + 4 * tx, yl = y0 + tg;
+    const V4<T> g4 = lds4(P0.gx + xg);
+    const T gyv = (yl < P0.nyl) ? P0.gy[yl] : T(0);
+    const bool store_ok = (yl < P0.nyl) && (xg < P0.nx);
+    __syncthreads();
+    mbar_wait(bar, 0);
+    const T *st = reinterpret_cast<const T *>(smem);
+    const int sidx = tg * TX + 4 * tx;
+    V4<T> pm4 = lds4(st + SC::OFF_PM / C::ES + sidx);
+    V4<T> qm4 = lds4(st + SC::OFF_QM / C::ES + sidx);
+    uint32_t phase = 1;
+
+    for (int step = 0; step < M.nsteps; ++step) {
+        const int c = (M.cur0 + step) & 1;
+        const StepParams<T> &P = M.P[c];
+        if (step > 0) {
+            // the exchange partners finished step - 1
+            if (dep >= 0) {
+                const unsigned int want = M.epoch0 + (unsigned int)step;
+                unsigned int v;
+                if (M.mode & 2) {   // relaxed polling, one acquire fence once satisfied
+                    for (;;) {
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(M.done + dep) : "memory");
+                        if ((int)(v - want) >= 0) break;
+                        if (M.mode & 4) __nanosleep(32);
+                    }
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                } else {
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(M.done + dep) : "memory");
+                        if ((int)(v - want) >= 0) break;
+                        if (M.mode & 4) __nanosleep(32);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            // generic-proxy stores of other CTAs (made visible by the acquires above) before
+            // this thread's async-proxy (TMA) reads
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            mbar_arrive_expect_tx(bar, C::P_BYTES + NQ * C::S_BYTES);
+            tma_load_3d(smem + SC::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
+            tma_load_3d(smem + SC::OFF_Q, &M.tm_qcol[c], x0, y0, k - RZ, bar);
+        }
+        const T sv = M.s_table[step];
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        T pn[1][4], qn[1][4], pc[4], qc[4];
+        small_update<T, R, RZ, TY, IO>(P, smem, y0, k, tg, tx, xg, yl, g4, gyv, sv,
+                                       IO ? P.inj_row + (long long)step * M.dir : 0,
+                                       IO ? P.rec_row + step : 0, pm4, qm4, pn, qn, pc, qc);
+        if (store_ok) {
+            const long long off = (long long)k * P.zs + (long long)yl * P.ys + xg;
+            stv(P.p_out + off, pn[0]);
+            stv(P.q_out + off, qn[0]);
+        }
+        pm4 = v4_of(pc);   // this step's u^n is the next step's u^{n-1}
+        qm4 = v4_of(qc);
+        __syncthreads();   // every store issued, every shared-memory read of this step done
+        if (threadIdx.x == 0) {
+            if (M.mode & 8) asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (M.mode & 1) __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(M.done + item),
+                         "r"(M.epoch0 + (unsigned int)step + 1u)
+                         : "memory");
+        }
     }
 }
 

@@ -142,6 +142,41 @@ static vti_status unpack_recv(vti_s *h, int b)
     return VTI_OK;
 }
 
+// Staged local-group transport (vti_group_step_staged): the NCCL branch of vti_step for
+// handle i of a local group, with device copies from the neighbours' packed send buffers
+// standing in for ncclSend/ncclRecv. Comm stream: after this rank's and the neighbours'
+// ev_edge (their packs of buffer b), copy, unpack into the halo rows, record ev_comm.
+static vti_status exchange_staged(vti_s *const *hs, int n, int i, int b)
+{
+    vti_s *h = hs[i];
+    const size_t bytes = halo_elems(h) * h->es;
+    CU(h, cudaStreamWaitEvent(h->comm, h->ev_edge, 0));
+    if (i > 0) {   // rank-1's last rows (its sbuf[1]) -> our bottom halo
+        CU(h, cudaStreamWaitEvent(h->comm, hs[i - 1]->ev_edge, 0));
+        CU(h, cudaMemcpyAsync(h->rbuf[0], hs[i - 1]->sbuf[1], bytes, cudaMemcpyDefault, h->comm));
+    }
+    if (i < n - 1) {   // rank+1's first rows (its sbuf[0]) -> our top halo
+        CU(h, cudaStreamWaitEvent(h->comm, hs[i + 1]->ev_edge, 0));
+        CU(h, cudaMemcpyAsync(h->rbuf[1], hs[i + 1]->sbuf[0], bytes, cudaMemcpyDefault, h->comm));
+    }
+    vti_status s = unpack_recv(h, b);
+    if (s != VTI_OK) return s;
+    CU(h, cudaEventRecord(h->ev_comm, h->comm));
+    return VTI_OK;
+}
+
+// The main stream of handle i waits for its own and its neighbours' exchanges: its halo rows
+// are complete, and the neighbours' copies out of its send buffers are done before the next
+// pack overwrites them (what ncclSend's completion guarantees on the NCCL path).
+static vti_status wait_staged(vti_s *const *hs, int n, int i)
+{
+    vti_s *h = hs[i];
+    CU(h, cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
+    if (i > 0) CU(h, cudaStreamWaitEvent(h->stream, hs[i - 1]->ev_comm, 0));
+    if (i < n - 1) CU(h, cudaStreamWaitEvent(h->stream, hs[i + 1]->ev_comm, 0));
+    return VTI_OK;
+}
+
 // NCCL transport on the comm stream after ev_edge, then unpack; records ev_comm.
 vti_status exchange_nccl(vti_s *h, int b)
 {
@@ -423,11 +458,15 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
         if (hs[i]->n != hs[0]->n) return fail(hs[i], VTI_E_STATE, "time indices differ inside the group");
     }
     if (n == 1) return vti_step(hs[0], nsteps);
+    vti_status s;
+    for (int i = 0; i < n; ++i) {
+        CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+        if ((s = prepare_io(hs[i])) != VTI_OK) return s;
+    }
     for (int i = 0; i < n; ++i)
         if (hs[i]->xseq != hs[0]->xseq || hs[i]->cur != hs[0]->cur)
             return fail(hs[i], VTI_E_STATE, "halo publications or buffer parity differ inside the group");
     group_connect(hs, n);
-    vti_status s;
     bool dirty = false;
     for (int i = 0; i < n; ++i) dirty |= hs[i]->halo_dirty;
     if (dirty) {   // every release before any publish (enqueue-order rule)
@@ -459,7 +498,77 @@ vti_status vti_group_step(vti_t *hs, int32_t n, int32_t nsteps)
             if (!h->fused() && (s = launch_interior(h)) != VTI_OK) return s;
             h->cur = 1 - h->cur;
             h->n += h->dir;
-            if ((s = record(h)) != VTI_OK) return s;
+            advance_records(h, 1);
+            if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0 && (s = check_finite(h)) != VTI_OK)
+                return s;
+        }
+    }
+    return VTI_OK;
+}
+
+vti_status vti_group_step_staged(vti_t *hs, int32_t n, int32_t nsteps)
+{
+    if (!hs || n < 2 || nsteps < 0) return VTI_E_PARAM;
+    for (int i = 0; i < n; ++i) {
+        if (!hs[i]) return VTI_E_PARAM;
+        if (hs[i]->cfg.nranks != n || hs[i]->cfg.rank != i || !hs[i]->group_mode)
+            return fail(hs[i], VTI_E_STATE, "handle %d is not rank %d of a %d-handle local group", i, i, n);
+        if (!hs[i]->model_set) return fail(hs[i], VTI_E_STATE, "model not set");
+        if (hs[i]->n != hs[0]->n || hs[i]->cur != hs[0]->cur)
+            return fail(hs[i], VTI_E_STATE, "time indices or buffer parity differ inside the group");
+    }
+    vti_status s;
+    for (int i = 0; i < n; ++i) {
+        CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+        if ((s = prepare_io(hs[i])) != VTI_OK) return s;
+        CU(hs[i], cudaStreamSynchronize(hs[i]->comm));
+    }
+    bool dirty = false;
+    for (int i = 0; i < n; ++i) dirty |= hs[i]->halo_dirty;
+    if (dirty) {   // halos of the current level (state set by the caller, vti_reverse)
+        for (int i = 0; i < n; ++i) {
+            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+            if ((s = pack_send(hs[i], hs[i]->cur)) != VTI_OK) return s;
+            CU(hs[i], cudaEventRecord(hs[i]->ev_edge, hs[i]->stream));
+        }
+        for (int i = 0; i < n; ++i) {
+            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+            if ((s = exchange_staged(hs, n, i, hs[i]->cur)) != VTI_OK) return s;
+        }
+        for (int i = 0; i < n; ++i) {
+            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+            if ((s = wait_staged(hs, n, i)) != VTI_OK) return s;
+            hs[i]->halo_dirty = false;
+        }
+    }
+    for (int it = 0; it < nsteps; ++it) {
+        for (int i = 0; i < n; ++i) {   // edge tile rows first, then pack the rows the neighbours need
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            if ((s = launch_edge(h)) != VTI_OK) return s;
+            if ((s = pack_send(h, 1 - h->cur)) != VTI_OK) return s;
+            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+        }
+        for (int i = 0; i < n; ++i) {   // exchange on the comm streams, overlapped with the interiors
+            CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+            if ((s = exchange_staged(hs, n, i, 1 - hs[i]->cur)) != VTI_OK) return s;
+        }
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            if ((s = launch_interior(h)) != VTI_OK) return s;
+        }
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            if ((s = wait_staged(hs, n, i)) != VTI_OK) return s;
+        }
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            h->cur = 1 - h->cur;
+            h->n += h->dir;
+            advance_records(h, 1);
             if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0 && (s = check_finite(h)) != VTI_OK)
                 return s;
         }

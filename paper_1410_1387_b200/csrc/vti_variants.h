@@ -12,6 +12,8 @@ struct KernelEntry {
     int px;                // points per thread along x (4, or 2 for the fp64 double2 mapping)
     const void *fn;        // host stub of the instantiation (cudaLaunchKernelExC with a StepParams<T> argument)
     const void *fn_peer;   // the same with the fused peer-halo stores (edge launches of peer-connected slabs)
+    const void *fn_io;     // with the N4 point sets (injection / receivers), or NULL (default variants only)
+    const void *fn_peer_io;
     int zrow;
     int threads;
 };
@@ -33,6 +35,9 @@ VariantTable vti_variants_f64_r12();   // (12,8)
 struct SmallEntry {
     int esize, r, rz, ty;
     const void *fn;
+    const void *fn_io;     // with the N4 point sets
+    const void *fn_multi;  // multi-step cooperative kernel (vti_small_multi_kernel), and its IO form
+    const void *fn_multi_io;
     int smem, threads;
 };
 struct SmallTable {

@@ -139,3 +139,142 @@ def test_reverse_recovers_initial_state_without_damping():
     for got, want in ((p0, st0[0]), (q0, st0[1]), (p, st0[2]), (q, st0[3])):
         rel = np.linalg.norm(got.astype(np.float64) - want) / np.linalg.norm(want)
         assert rel < 1e-4, rel
+
+
+# ---------------------------------------------------------------- trace injection (fused, IO kernels)
+
+def _inj_points(cfg, n_rand, seed, extra=()):
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    pts = {tuple(cfg["src"])} | set(extra)
+    # tile / row / plane edges, a whole row segment of one plane, the domain corners
+    for i in (0, 1, 63, 64, nx - 1):
+        pts.add((min(i, nx - 1), ny // 2, nz // 3))
+    for i in range(10, 30):
+        pts.add((i, 7, 5))
+    pts |= {(0, 0, 0), (nx - 1, ny - 1, nz - 1)}
+    while len(pts) < n_rand:
+        pts.add((int(rng.integers(nx)), int(rng.integers(ny)), int(rng.integers(nz))))
+    return np.array(sorted(pts, key=lambda t: (t[2], t[1], t[0])), np.int32)[rng.permutation(len(pts))]
+
+
+@pytest.mark.parametrize("grid,nsteps,small", [((60, 50, 40), 70, True), ((96, 96, 72), 50, False)])
+def test_injection_and_receivers_match_oracle(grid, nsteps, small):
+    """Multi-point trace injection (+ the Ricker source at one of the points) and receivers
+    over >= 50 steps: fields and traces bitwise equal to the oracle's vto_run_ex. The small grid
+    runs through the small-grid kernel with CUDA-graph replays (70 steps = 2 x 32 + 6 direct);
+    the larger one through the persistent TMA step kernel."""
+    cfg, wxy, wz, dt, model = setup(*grid, damp=6, src=(grid[0] // 2, grid[1] // 2, grid[2] // 2))
+    pts = _inj_points(cfg, 90, 3)
+    rng = np.random.default_rng(5)
+    t_first, nt = 3, nsteps - 10             # rows outside [t_first, t_first + nt) inject nothing
+    tr = (rng.normal(size=(nt, len(pts))) * 5.0).astype(np.float32)
+    rec = np.concatenate([pts[:40], REC[:3] % np.array(grid[::1], np.int32)])
+    with handle(cfg, dt, wxy, wz) as v:
+        assert v.info()["small_kernel"] == int(small)
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], mask=1)
+        v.set_injection(pts, tr, fields=3, t_first=t_first)
+        v.set_receivers(rec, fields=3, capacity_steps=nsteps + 5)
+        v.step(nsteps)
+        g = v.get_fields(0) + v.get_fields(1)
+        ids, traces = v.get_traces()
+    P = oracle.params(dict(cfg, mask=1), dt)
+    o = oracle.run_ex(P, wxy, wz, *model, None, nsteps=nsteps, inj=(pts, 3, t_first, tr), rec=(rec, 3))
+    for a, b in zip(g, o[:4]):
+        assert np.abs(b).max() > 0
+        assert np.array_equal(a, b), f"max |diff| {np.abs(a - b).max():.3e}"
+    assert list(ids) == list(range(len(rec))) and traces.shape == (nsteps, len(rec), 2)
+    assert np.array_equal(traces, o[4])
+
+
+def test_injection_fp64_matches_oracle():
+    from synth import weights as W
+    cfg, _, _, dt, model = setup(60, 50, 40, damp=5)
+    wxy = W.xy_weights(cfg["r_xy"])
+    wz = np.ascontiguousarray(W.z_weights(W.z_coords_ramp(cfg["nz"], cfg["r_z"], 6.0, 12.0), cfg["r_z"]))
+    model = [a.astype(np.float64) for a in model]
+    pts = _inj_points(cfg, 40, 7)
+    tr = np.random.default_rng(2).normal(size=(30, len(pts)))
+    with handle(cfg, dt, wxy, wz, precision=64) as v:
+        v.set_model(*model)
+        v.set_injection(pts, tr, fields=1)
+        v.set_receivers(pts[:10], fields=2, capacity_steps=40)
+        v.step(30)
+        g = v.get_fields(0)
+        _, traces = v.get_traces()
+    o = oracle.run_ex(oracle.params(cfg, dt, src=None), wxy, wz, *model, None, nsteps=30,
+                      inj=(pts, 1, 0, tr), rec=(pts[:10], 2), dtype=np.float64)
+    assert np.array_equal(g[0], o[0]) and np.array_equal(g[1], o[1]) and np.array_equal(traces, o[4])
+
+
+def test_reverse_with_injection_matches_oracle():
+    """The RTM backward leg: record forward, then reverse and re-inject the recorded traces
+    (time index decreasing picks the earlier rows), bitwise against vto_run_ex(direction=-1)."""
+    cfg, wxy, wz, dt, model = setup(damp=6)
+    rec = _inj_points(cfg, 30, 11)
+    K = 40
+    with handle(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        v.set_receivers(rec, fields=1, capacity_steps=K)
+        v.step(K)
+        _, traces = v.get_traces()
+        fwd = v.get_fields(0) + v.get_fields(1)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], amp=0.0)   # source off for the backward leg
+        v.set_receivers(np.zeros((0, 3), np.int32))
+        v.set_injection(rec, traces[:, :, 0], fields=1, t_first=1)      # row t = level t + 1
+        v.reverse()
+        v.step(K - 5)
+        back = v.get_fields(0) + v.get_fields(1)
+    P = oracle.params(cfg, dt)
+    o = oracle.run_ex(P, wxy, wz, *model, None, nsteps=K, rec=(rec, 1))
+    for a, b in zip(fwd, o[:4]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(traces, o[4])
+    P0 = oracle.params(dict(cfg, amp=0.0), dt)
+    b = oracle.run_ex(P0, wxy, wz, *model, (o[2], o[3], o[0], o[1]), n0=K - 1, nsteps=K - 5, direction=-1,
+                      inj=(rec, 1, 1, traces[:, :, 0]))
+    for a, c in zip(back, b[:4]):
+        assert np.array_equal(a, c)
+
+
+def test_injection_across_slabs():
+    from paper_1410_1387_b200 import group_step
+    cfg, wxy, wz, dt, model = setup(ny=70, src=(25, 35, 20))
+    pts = _inj_points(cfg, 60, 13, extra=[(25, 34, 20), (25, 36, 20), (3, 0, 1), (40, 69, 30)])
+    tr = np.random.default_rng(1).normal(size=(12, len(pts))).astype(np.float32)
+    with handle(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        v.set_injection(pts, tr, fields=3)
+        v.step(10)
+        ref = v.get_fields(0)
+    hs = [handle(cfg, dt, wxy, wz, rank=r, nranks=2) for r in range(2)]
+    for h in hs:
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_model(*[np.ascontiguousarray(a[:, sl]) for a in model])
+        h.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        h.set_injection(pts, tr, fields=3)
+    group_step(hs, 10)
+    for h in hs:
+        p, q = h.get_fields(0)
+        assert np.array_equal(p, ref[0][:, h.y0:h.y0 + h.ny_local])
+        assert np.array_equal(q, ref[1][:, h.y0:h.y0 + h.ny_local])
+        h.close()
+
+
+def test_injection_errors():
+    from paper_1410_1387_b200 import VTIError
+    cfg, wxy, wz, dt, model = setup()
+    with handle(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        for pts, name in (([[1, 1, 1], [1, 1, 1]], "VTI_E_PARAM"), ([[60, 0, 0]], "VTI_E_INDEX")):
+            with pytest.raises(VTIError) as e:
+                v.set_injection(np.array(pts, np.int32), np.ones((3, len(pts)), np.float32))
+            assert e.value.name == name
+        with pytest.raises(VTIError) as e:
+            v.set_injection([[1, 1, 1]], np.ones((3, 1), np.float32), fields=4)
+        assert e.value.name == "VTI_E_PARAM"
+        v.set_injection(np.zeros((0, 3), np.int32), None)   # remove: plain kernels again
+        v.step(2)

@@ -32,7 +32,7 @@ def compiled_variants():
     for f in sorted(os.listdir(d)):
         if f.endswith(".cu"):
             src = open(os.path.join(d, f)).read()
-            pat = r"entry<(float|double),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*\d+,\s*\d+(?:,\s*(\d+))?>"
+            pat = r"entry(?:_io)?<(float|double),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*\d+,\s*\d+(?:,\s*(\d+))?>"
             for m in re.finditer(pat, src):
                 t, r, rz, ty, rpt, wp, px = m.groups()
                 out.append((32 if t == "float" else 64, int(r), int(rz), int(ty), int(wp), int(rpt), int(px or 4)))
@@ -257,3 +257,60 @@ def test_fused_step_bitwise(nranks, ty, r, rz, monkeypatch):
     one.close()
     for f in range(4):
         assert np.array_equal(got2[f], ref2[f]), f"field {f}"
+
+
+@pytest.mark.parametrize("prec,r,rz,nranks", [(32, 4, 4, 2), (32, 8, 4, 3), (64, 6, 6, 3), (32, 12, 8, 2)])
+def test_staged_transport_matches_oracle(prec, r, rz, nranks):
+    """The NCCL path's staged transport -- edge launch, pack of the boundary rows, exchange on
+    the comm stream (device copies standing in for ncclSend/ncclRecv), unpack into the halo
+    rows, interior launch overlapped -- in a local group: bitwise == oracle, including a
+    state set mid-run (its halo re-exchanged before the next step)."""
+    from paper_1410_1387_b200 import group_step
+    ny = nranks * 40
+    cfg = small_cfg(70, ny, 2 * rz + 14, r, rz, damp=5)
+    cfg["src"] = (30, ny // nranks, cfg["nz"] // 2)   # first row of rank 1
+    wxy, wz, dt, model, st = (f64_inputs if prec == 64 else f32_inputs)(cfg)
+    dtype = np.float64 if prec == 64 else np.float32
+    hs = handles(cfg, dt, wxy, wz, nranks, prec)
+    load(hs, model, st, 2, cfg)
+    group_step(hs, 4, transport="staged")
+    mid = gather(hs)
+    P = oracle.params(cfg, dt)
+    ref = oracle.run(P, wxy, wz, *model, st, n0=2, nsteps=4, dtype=dtype)[:4]
+    for f in range(4):
+        assert np.array_equal(mid[f], ref[f]), f"field {f} after 4 steps"
+    # a new state mid-run: halos must be re-exchanged (pack of the current level) before stepping
+    st2 = [np.ascontiguousarray(a[::-1]) for a in st]
+    load(hs, model, st2, 9)
+    group_step(hs, 3, transport="staged")
+    got = gather(hs)
+    close(hs)
+    ref2 = oracle.run(P, wxy, wz, *model, st2, n0=9, nsteps=3, dtype=dtype)[:4]
+    for f in range(4):
+        assert np.abs(ref2[f]).max() > 0
+        assert np.array_equal(got[f], ref2[f]), f"field {f} after the reset"
+
+
+def test_staged_transport_with_receivers_and_injection():
+    from paper_1410_1387_b200 import group_step
+    cfg = small_cfg(70, 96, 20, 4, 4, damp=5)
+    cfg["src"] = (30, 48, 10)
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    pts = np.array([[30, 47, 10], [30, 48, 10], [5, 0, 0], [69, 95, 19], [12, 50, 3]], np.int32)
+    tr = np.random.default_rng(3).normal(size=(6, len(pts))).astype(np.float32)
+    hs = handles(cfg, dt, wxy, wz, 2)
+    load(hs, model, st, 0, cfg)
+    for h in hs:
+        h.set_injection(pts, tr, fields=3)
+        h.set_receivers(pts, fields=1, capacity_steps=10)
+    group_step(hs, 6, transport="staged")
+    got = gather(hs)
+    traces = np.zeros((6, len(pts), 1), np.float32)
+    for h in hs:
+        ids, t = h.get_traces()
+        traces[:, ids] = t
+    close(hs)
+    o = oracle.run_ex(oracle.params(cfg, dt), wxy, wz, *model, st, nsteps=6, inj=(pts, 3, 0, tr), rec=(pts, 1))
+    for f in range(4):
+        assert np.array_equal(got[f], o[f])
+    assert np.array_equal(traces, o[4])
