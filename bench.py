@@ -213,6 +213,37 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+REF_MAX_POINTS = 320 ** 3   # the reference arm's largest sample cube (~1.2 GB of oracle arrays)
+
+
+def reference_side(cfg_full, rate, steps, warmup, budget_s=120.0):
+    """Edge of the reference arm's sample cube: W + K oracle steps in about budget_s at the
+    probed rate (points/s), at most REF_MAX_POINTS (host memory and input generation stay
+    small whatever the config), at least what the damping band and the z stencil need."""
+    pts = max(32 ** 3, min(cfg_full["nx"] * cfg_full["ny"] * cfg_full["nz"], REF_MAX_POINTS,
+                           int(rate * budget_s / max(1, steps + warmup))))
+    side = int(round(pts ** (1.0 / 3.0)))
+    return max(2 * cfg_full["damp_width"] + 2, max(2 * cfg_full["r_z"] + 1, side))
+
+
+def host_inputs(c, chunk=32, dtype=None):
+    """The recipe's model and a seeded random state on the host, generated plane-chunk by
+    plane-chunk into preallocated arrays (bounded temporaries)."""
+    import numpy as np
+
+    from synth import fields as SF
+    shape = (c["nz"], c["ny"], c["nx"])
+    model = [np.empty(shape, np.float32) for _ in range(3)]
+    state = [np.empty(shape, np.float32) for _ in range(4)]
+    for k0 in range(0, c["nz"], chunk):
+        nk = min(chunk, c["nz"] - k0)
+        for dst, src in zip(model, SF.model_planes(c, k0, nk)):
+            dst[k0:k0 + nk] = src.numpy()
+        for s, dst in enumerate(state):
+            dst[k0:k0 + nk] = SF.random_planes(c["nx"], c["ny"], k0, nk, 11, s, 1e-6).numpy()
+    return model, state
+
+
 def cpu_baseline(cfg, budget_s=12.0, precision=32):
     """The oracle as it stands, on this host's cores, on a bounded sample of the same workload:
     the config's recipe on SURVEY.md 8(d)'s reduced grid (256 x 256 x 128 for C4/C5, the full
@@ -221,7 +252,6 @@ def cpu_baseline(cfg, budget_s=12.0, precision=32):
 
     import oracle
     import synth
-    from synth import fields as SF
     oracle.build()
     if cfg["nx"] * cfg["ny"] * cfg["nz"] > 256 ** 3:
         sample = synth.scaled(cfg, min(cfg["nx"], 256), min(cfg["ny"], 256), 128 if cfg["nz"] >= 1024 else
@@ -231,9 +261,7 @@ def cpu_baseline(cfg, budget_s=12.0, precision=32):
     wxy, wz = weights(sample, precision)
     dt = synth.stable_dt(sample)
     dt_np = np.float32 if precision == 32 else np.float64
-    nz = sample["nz"]
-    model = [a.numpy() for a in SF.model_planes(sample, 0, nz)]
-    state = [SF.random_planes(sample["nx"], sample["ny"], 0, nz, 11, s, 1e-6).numpy() for s in range(4)]
+    model, state = host_inputs(sample)
     P = oracle.params(sample, dt)
     npts = sample["nx"] * sample["ny"] * sample["nz"]
     threads = host_threads()
@@ -258,7 +286,6 @@ def run_reference(args):
         return 0
     import oracle
     import synth
-    from synth import fields as SF
     cfg_full, scaling = workload(args, world)
     oracle.build()
     # bounded sample: the same recipe on a smaller grid, sized so W + K steps take ~2 minutes
@@ -267,18 +294,14 @@ def run_reference(args):
     def setup(c):
         wxy, wz, _ = synth.weights_f32(c)
         dt = synth.stable_dt(c, wxy, wz)
-        model = [a.numpy() for a in SF.model_planes(c, 0, c["nz"])]
-        state = [SF.random_planes(c["nx"], c["ny"], 0, c["nz"], 11, s, 1e-6).numpy() for s in range(4)]
+        model, state = host_inputs(c)
         return oracle.params(c, dt), wxy, wz, model, state
 
     threads = host_threads()
     P, wxy, wz, model, state = setup(probe)
     _, _, _, _, t = oracle.run(P, wxy, wz, *model, state, nsteps=2, nthreads=threads)
     rate = 2 * 128 ** 3 / t
-    pts = max(32 ** 3, min(cfg_full["nx"] * cfg_full["ny"] * cfg_full["nz"],
-                           int(rate * 120.0 / max(1, args.steps + args.warmup))))
-    side = int(round(pts ** (1.0 / 3.0)))
-    side = max(2 * cfg_full["damp_width"] + 2, max(2 * cfg_full["r_z"] + 1, side))
+    side = reference_side(cfg_full, rate, args.steps, args.warmup)
     sample = synth.scaled(cfg_full, side, side, side)
     P, wxy, wz, model, state = setup(sample)
     st = oracle.run(P, wxy, wz, *model, state, nsteps=args.warmup, nthreads=threads)[:4] if args.warmup else state

@@ -9,4 +9,7 @@ VTI_TABLE(vti_variants_f64_r12,
           (entry_io<double, 12, 8, 8, 1, 1, 4, 1, 2>()), (entry<double, 12, 8, 10, 1, 1, 3, 1, 2>()),
           (entry<double, 12, 8, 15, 1, 1, 3, 1, 2>()), (entry<double, 12, 8, 16, 1, 0, 2, 1, 2>()),
           (entry<double, 12, 8, 14, 1, 1, 3, 1>()), (entry<double, 12, 8, 16, 1, 1, 2, 1>()),
-          (entry<double, 12, 8, 16, 1, 0, 2, 1>()))
+          (entry<double, 12, 8, 16, 1, 0, 2, 1>()),
+          // one double per thread (PX = 1): twice the warps per tile, half the q queue
+          (entry<double, 12, 8, 8, 1, 1, 4, 1, 1>()), (entry<double, 12, 8, 8, 1, 1, 3, 1, 1>()),
+          (entry<double, 12, 8, 6, 1, 1, 5, 1, 1>()), (entry<double, 12, 8, 4, 1, 1, 4, 2, 1>()))

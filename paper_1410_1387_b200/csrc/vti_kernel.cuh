@@ -281,6 +281,10 @@ template <> struct Vec<double, 4> {
     double2 a, b;
     __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : c == 1 ? a.y : c == 2 ? b.x : b.y; }
 };
+template <> struct Vec<double, 1> {
+    double a;
+    __device__ __forceinline__ double operator[](int) const { return a; }
+};
 template <> struct Vec<double, 2> {
     double2 a;
     __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : a.y; }
@@ -302,6 +306,7 @@ template <> __device__ __forceinline__ Vec<double, 4> ldv<4>(const double *p)
 {
     return Vec<double, 4>{reinterpret_cast<const double2 *>(p)[0], reinterpret_cast<const double2 *>(p)[1]};
 }
+template <> __device__ __forceinline__ Vec<double, 1> ldv<1>(const double *p) { return Vec<double, 1>{*p}; }
 template <> __device__ __forceinline__ Vec<double, 2> ldv<2>(const double *p)
 {
     return Vec<double, 2>{*reinterpret_cast<const double2 *>(p)};
@@ -324,6 +329,7 @@ __device__ __forceinline__ void stv(double *p, const double (&v)[4])
     reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
     reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
 }
+__device__ __forceinline__ void stv(double *p, const double (&v)[1]) { *p = v[0]; }
 __device__ __forceinline__ void stv(double *p, const double (&v)[2])
 {
     *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
     constexpr int TPR = TX / PX;   // threads per tile row
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
-    static_assert(PX == 4 || PX == 2, "4 or 2 x points per thread");
+    static_assert(PX == 4 || PX == 2 || (PX == 1 && !PACKED), "4, 2 (or, scalar fp64, 1) x points per thread");
     static_assert((TY * TPR) % (32 * RPT) == 0, "tile rows must split into whole warps");
     static_assert(RA % PX == 0, "x apron must be whole vectors");
     extern __shared__ __align__(128) uint8_t smem[];

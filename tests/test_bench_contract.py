@@ -94,3 +94,16 @@ def test_default_line_is_c4():
     assert e["steps"] == 200 and e["value"] > 0
     assert e["h2d_bytes_per_step"] == 3 * 4 * 2048 * 2048 * 1024 // 200
     assert d["cpu_baseline"]["sample"].count("256x256x128") == 1
+
+
+def test_reference_arm_sample_is_bounded():
+    """The driver's `--impl reference` at the default config (C4, 4.3 G points): the sample
+    cube stays bounded however fast the host is, and above the damping band's minimum."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    import synth
+    c4 = synth.CONFIGS["C4"]()
+    assert bench.reference_side(c4, rate=1e12, steps=20, warmup=5) ** 3 <= bench.REF_MAX_POINTS
+    assert bench.reference_side(c4, rate=1e3, steps=20, warmup=5) == 2 * c4["damp_width"] + 2
+    assert bench.reference_side(synth.CONFIGS["C1"](), rate=1e12, steps=20, warmup=5) == 64
