@@ -11,7 +11,7 @@ u^{N-1} (pm, qm), plus the digests of the three model arrays so that a GPU-side 
 mismatch is diagnosed separately, and a few scalar summaries. tests/test_digests_gpu.py steps
 the library the same N steps and compares digests (bitwise parity).
 
-  python tools/oracle_digests.py [C2 N1 C3 C5] [--threads T]
+  python tools/oracle_digests.py [C2 N1 C3 C5] [--threads T] [--out PATH]
 
 Runtime on 8 host cores: roughly 0.5-1.5 h per config (x86 subnormal arithmetic in the
 decaying far field dominates); each config is merged into the JSON as soon as it finishes.
@@ -83,18 +83,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("names", nargs="*", default=["C2", "C3", "C5", "N1"])
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--out", default=OUT, help="JSON to merge the entries into (default tests/golden/...)")
     a = ap.parse_args()
     oracle.build()
     for name in a.names:
         ent = run_one(name, a.threads or oracle.max_threads())
-        d = json.load(open(OUT)) if os.path.exists(OUT) else {
+        out = a.out
+        d = json.load(open(out)) if os.path.exists(out) else {
             "what": "sha256 of the oracle's float32 fields after each config's stated step count",
             "written_by": "tools/oracle_digests.py (oracle/ + synth/ only)"}
         d[name] = ent
-        tmp = OUT + ".tmp"
+        tmp = out + ".tmp"
         with open(tmp, "w") as f:
             json.dump(d, f, indent=1)
-        os.replace(tmp, OUT)
+        os.replace(tmp, out)
         print(name, json.dumps(ent), flush=True)
 
 
