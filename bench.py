@@ -384,6 +384,32 @@ def warm_up(v, steps, world, transport, timeout_s=120.0):
     v.sync()
 
 
+class Watchdog:
+    """Exit the process loudly (code 4) if a guarded region outlives timeout_s -- a halo
+    transport that stops delivering mid-run must fail the job, not hang it (N > 1 only;
+    the warm-up is guarded by multi.sync_or_die)."""
+
+    def __init__(self, timeout_s, what, enabled=True):
+        self.timeout_s, self.what, self.enabled, self.t = timeout_s, what, enabled, None
+
+    def _fire(self):
+        print(f"error: {self.what} did not finish within {self.timeout_s:.0f} s; aborting", file=sys.stderr,
+              flush=True)
+        os._exit(4)
+
+    def __enter__(self):
+        if self.enabled:
+            import threading
+            self.t = threading.Timer(self.timeout_s, self._fire)
+            self.t.daemon = True
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.t:
+            self.t.cancel()
+
+
 def setup_rank(args, cfg, dt, wxy, wz, rank, world, local, dist, halo):
     """Everything a rank does before the timed region: handle + transport, tuning, model,
     source and warm-up. Returns (handle, transport name)."""
@@ -494,7 +520,7 @@ def run_native(args):
     # --reps timed regions of exactly K steps, each bracketed by barrier + synchronize
     reps = []
     barrier()
-    with Clocks(local) as clk:
+    with Clocks(local) as clk, Watchdog(600.0 + 2.0 * args.reps * args.steps, "timed region", world > 1):
         for _ in range(max(1, args.reps)):
             barrier()
             ms = v.step_timed(args.steps)
@@ -517,7 +543,8 @@ def run_native(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = end_to_end(args, cfg, dt, wxy, wz, rank, world, local, dist, halo, info, barrier, max_over_ranks)
+        with Watchdog(1800.0, "end-to-end job", world > 1):
+            e2e = end_to_end(args, cfg, dt, wxy, wz, rank, world, local, dist, halo, info, barrier, max_over_ranks)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -13,20 +13,25 @@
 // Design: 2.5-D blocking after the paper's GPU kernel
 // (x-y tile in shared memory + z register rolling), made
 // B200-native:
-//  * a persistent grid of CTAs pulls work items (64x16 x-y tile, z-chunk);
-//  * one elected lane (warp 0, lane 0) drives a STAGES-deep TMA ring: per z
+//  * a persistent grid of CTAs pulls work items (a 64 x TY x-y tile, a z-chunk);
+//    TY, the producer mode, rows and x points per thread are template
+//    parameters (the fp32 (4,4) default: TY = 32, a dedicated producer warp,
+//    4 x points per thread);
+//  * one producer lane -- the dedicated producer warp (WP = 1) or the CTA's
+//    first thread in line (WP = 0) -- drives a STAGES-deep TMA ring: per z
 //    plane it issues cp.async.bulk.tensor loads of the halo'd p^n plane tile,
 //    the q^n plane Rz ahead, p^{n-1}, q^{n-1}, vx2, vn2, vz2 and a 1-D bulk
 //    copy of the plane's w^z row + gz, all completing on one mbarrier; load
-//    j + STAGES is issued as soon as every warp has released load j (empty
-//    mbarrier), so STAGES - 1 planes are always in flight. Out-of-bounds box
-//    elements are zero-filled by TMA, which IS the paper's zero exterior
-//    (l.89-90) in x, y and z. (No dedicated producer warp: 16 warps per CTA
-//    keep 4 warps per SM sub-partition, i.e. 128 registers per thread.)
-//  * all warps consume: each thread owns 4 consecutive x points (float4) of
-//    one row, keeps a (2Rz+1)-deep float4 register queue of q along z, reads
-//    the p cross from shared memory and writes p^{n+1}, q^{n+1} with 16-byte
-//    stores in place over p^{n-1}, q^{n-1}.
+//    j + STAGES is issued as soon as every consumer warp has released load j
+//    (empty mbarrier), so STAGES - 1 planes are always in flight. Out-of-bounds
+//    box elements are zero-filled by TMA, which IS the paper's zero exterior
+//    (l.89-90) in x, y and z;
+//  * the consumer warps: each thread owns PX consecutive x points (float4,
+//    float2 or double2) of RPT rows, keeps a (2Rz+1)-deep register
+//    queue of q along z, reads the p cross from shared memory and writes
+//    p^{n+1}, q^{n+1} with vector stores in place over p^{n-1}, q^{n-1};
+//  * PEER twins also store the slab's boundary rows into the neighbours' halo
+//    rows (multi-GPU), IO twins gather receivers / add injected traces (N4).
 #pragma once
 
 #include <cuda.h>
@@ -281,10 +286,6 @@ template <> struct Vec<double, 4> {
     double2 a, b;
     __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : c == 1 ? a.y : c == 2 ? b.x : b.y; }
 };
-template <> struct Vec<double, 1> {
-    double a;
-    __device__ __forceinline__ double operator[](int) const { return a; }
-};
 template <> struct Vec<double, 2> {
     double2 a;
     __device__ __forceinline__ double operator[](int c) const { return c == 0 ? a.x : a.y; }
@@ -306,7 +307,6 @@ template <> __device__ __forceinline__ Vec<double, 4> ldv<4>(const double *p)
 {
     return Vec<double, 4>{reinterpret_cast<const double2 *>(p)[0], reinterpret_cast<const double2 *>(p)[1]};
 }
-template <> __device__ __forceinline__ Vec<double, 1> ldv<1>(const double *p) { return Vec<double, 1>{*p}; }
 template <> __device__ __forceinline__ Vec<double, 2> ldv<2>(const double *p)
 {
     return Vec<double, 2>{*reinterpret_cast<const double2 *>(p)};
@@ -329,7 +329,6 @@ __device__ __forceinline__ void stv(double *p, const double (&v)[4])
     reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
     reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
 }
-__device__ __forceinline__ void stv(double *p, const double (&v)[1]) { *p = v[0]; }
 __device__ __forceinline__ void stv(double *p, const double (&v)[2])
 {
     *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
@@ -478,7 +477,7 @@ __global__ void __launch_bounds__(nthreads(TY, RPT, WP, PX), MINB)
     constexpr int TPR = TX / PX;   // threads per tile row
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
-    static_assert(PX == 4 || PX == 2 || (PX == 1 && !PACKED), "4, 2 (or, scalar fp64, 1) x points per thread");
+    static_assert(PX == 4 || PX == 2, "4 or 2 x points per thread");
     static_assert((TY * TPR) % (32 * RPT) == 0, "tile rows must split into whole warps");
     static_assert(RA % PX == 0, "x apron must be whole vectors");
     extern __shared__ __align__(128) uint8_t smem[];

@@ -55,10 +55,10 @@ static const KernelEntry *find_kernel(int esize, int r, int rz, int ty, int wp, 
 // The IO-capable variant (N4 point sets) of a radius pair: the default entry of its table.
 static const KernelEntry *find_io_kernel(int esize, int r, int rz)
 {
-    for (int ty : {32, 30, 16, 15, 14, 12, 10, 8, 6, 4})
+    for (int ty : {32, 30, 16, 15, 14, 12, 10, 8})
         for (int wp : {1, 0})
             for (int rpt : {1, 2})
-                for (int px : {4, 2, 1}) {
+                for (int px : {4, 2}) {
                     const KernelEntry *e = find_kernel(esize, r, rz, ty, wp, rpt, px);
                     if (e && e->fn_io) return e;
                 }
@@ -77,10 +77,10 @@ static std::vector<const KernelEntry *> all_kernels(int esize, int r, int rz)
 {
     std::vector<const KernelEntry *> v;
     const KernelEntry *e;
-    for (int ty : {32, 30, 16, 15, 14, 12, 10, 8, 6, 4})
+    for (int ty : {32, 30, 16, 15, 14, 12, 10, 8})
         for (int wp : {1, 0})
             for (int rpt : {1, 2})
-                for (int px : {4, 2, 1})
+                for (int px : {4, 2})
                     if ((e = find_kernel(esize, r, rz, ty, wp, rpt, px)) != nullptr) v.push_back(e);
     return v;
 }

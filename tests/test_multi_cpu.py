@@ -127,3 +127,15 @@ def test_bench_explicit_configs_keep_their_scaling():
     bench, args = _bench_args("--config", "C1")
     cfg, scaling = bench.workload(args, 1)
     assert "L2-resident" in bench.describe(cfg, 1, scaling)["l2_flush"]
+
+
+def test_bench_watchdog_fires_and_cancels():
+    """bench.Watchdog: cancelled on exit; otherwise it ends the process with code 4."""
+    import subprocess
+    import bench
+    with bench.Watchdog(0.5, "quick region"):
+        pass
+    code = ("import sys, time; sys.path.insert(0, %r); import bench\n"
+            "with bench.Watchdog(0.2, 'stuck region'):\n    time.sleep(5)\n" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 4 and "stuck region did not finish" in r.stderr
