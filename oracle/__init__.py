@@ -77,6 +77,12 @@ def lib():
                           fp(t), fp(t), C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                           C.c_int32, i32, C.c_int32, C.c_int32, C.c_int64, fp(t),
                           C.c_int32, i32, C.c_int32, fp(t), C.POINTER(C.c_double)]
+            a = getattr(L, "vto_adjoint_ex_" + sfx)
+            a.restype = C.c_int
+            a.argtypes = [C.POINTER(Params), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t), fp(t),
+                          fp(t), fp(t), C.c_int64, C.c_int32, C.c_int32,
+                          C.c_int32, i32, C.c_int32, C.c_int32, C.c_int64, fp(t),
+                          C.c_int32, i32, C.c_int32, fp(t)]
             w = getattr(L, "vto_step_planes_" + sfx)
             w.restype = C.c_int
             w.argtypes = [C.POINTER(Params), fp(t), fp(t), C.c_int32, C.c_int32, C.c_int64,
@@ -179,6 +185,44 @@ def run_ex(P: Params, wxy, wz, vx2, vn2, vz2, state=None, n0: int = 0, nsteps: i
     if rc != 0:
         raise ValueError(f"oracle rejected parameters (code {rc})")
     return p, q, pm, qm, (out if n_rec else None), secs.value
+
+
+def adjoint_ex(P: Params, wxy, wz, vx2, vn2, vz2, state, m0: int = 0, nsteps: int = 1, inj=None, rec=None,
+               dtype=np.float32, nthreads: int = 0):
+    """The adjoint (transpose) recurrence of the scheme (see vto_adjoint_ex in vti_oracle.c).
+
+    state = (psi_p^m0, psi_q^m0, psi_p^{m0+1}, psi_q^{m0+1}); the time index runs m0, m0-1, ...
+    inj / rec as in run_ex (P's Ricker source is not used). Returns (p, q, pm, qm, rec_traces).
+    """
+    shape = (P.nz, P.ny, P.nx)
+    conv = lambda a: np.ascontiguousarray(np.asarray(a, dtype=dtype))
+    p, q, pm, qm = (conv(a).copy() for a in state)
+    vx2, vn2, vz2 = (conv(a).reshape(shape) for a in (vx2, vn2, vz2))
+    wxy = conv(wxy).reshape(-1)
+    wz = conv(wz).reshape(-1)
+    dummy_i = np.zeros(3, np.int32)
+    dummy_t = np.zeros(1, dtype)
+    if inj is not None:
+        ijk, imask, t_first, tr = inj
+        ijk = np.ascontiguousarray(np.asarray(ijk, np.int32).reshape(-1, 3))
+        tr = conv(tr).reshape(-1, ijk.shape[0])
+        n_inj, nt = ijk.shape[0], tr.shape[0]
+    else:
+        ijk, imask, t_first, tr, n_inj, nt = dummy_i, 0, 0, dummy_t, 0, 0
+    if rec is not None:
+        rijk, rmask = rec
+        rijk = np.ascontiguousarray(np.asarray(rijk, np.int32).reshape(-1, 3))
+        n_rec = rijk.shape[0]
+        out = np.zeros((nsteps, n_rec, (rmask & 1) + ((rmask >> 1) & 1)), dtype=dtype)
+    else:
+        rijk, rmask, n_rec, out = dummy_i, 0, 0, dummy_t
+    f = lib().vto_adjoint_ex_f32 if dtype == np.float32 else lib().vto_adjoint_ex_f64
+    rc = f(C.byref(P), wxy, wz, vx2, vn2, vz2, p, q, pm, qm, m0, nsteps, nthreads,
+           n_inj, ijk.reshape(-1) if n_inj else dummy_i, imask, nt, t_first, tr.reshape(-1) if n_inj else dummy_t,
+           n_rec, rijk.reshape(-1) if n_rec else dummy_i, rmask, out.reshape(-1) if n_rec else dummy_t)
+    if rc != 0:
+        raise ValueError(f"oracle rejected parameters (code {rc})")
+    return p, q, pm, qm, (out if n_rec else None)
 
 
 def point(P: Params, wxy, wzrow, i, j, k, n, pc, qc, pm, qm, vx2, vn2, vz2, dtype=np.float32):

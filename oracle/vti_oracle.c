@@ -351,6 +351,125 @@ int vto_run_ex_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx
     return 0;                                                                                  \
 }                                                                                              \
                                                                                                \
+/*                                                                                             \
+ * Adjoint (transpose) recurrence (the backward leg of adjoint-state FWI).   \
+ * The forward step is X^{n+1} = M X^n on X = (u^n, u^{n-1}), M = [[g(2 + dt^2 A), -g^2],        \
+ * [I, 0]], with A u = (vx2 L p + vz2 D q, vn2 L p + vz2 D q) (Eqs. 1-2, 4-5). Its transpose    \
+ * M^T, written in the damping-scaled adjoint variable psi = g a, has the same form with A^T:    \
+ *   psi^{m-1} = g (2 psi^m - g psi^{m+1} + dt^2 (A^T psi^m + inj)),                           \
+ *   A^T psi = (L (vx2 psi_p + vn2 psi_q), D^T (vz2 (psi_p + psi_q))),                          \
+ * L symmetric on the zero exterior, (D^T y)_k = sum_m w^z[k+Rz-m][m] y_{k+Rz-m} (Eq. 5's rows   \
+ * transposed). Canonical order: s1 = fma(vx2, psi_p, vn2*psi_q); s2 = vz2*(psi_p + psi_q);      \
+ * L(s1) as in point_; DT = 0, then for m = 0..2Rz with k' = k+Rz-m inside the grid             \
+ * DT = fma(w^z[k'][m], s2(k'), DT); F_p = L (+ inj), F_q = DT (+ inj);                         \
+ * psi^{m-1} = g*fma(dt2, F, fma(-g, psi^{m+1}, 2*psi^m)). No Ricker term (adjoint sources come   \
+ * as injected traces, row = time index m - inj_t_first); receivers record psi^{m-1}.           \
+ * On entry p,q = psi^{m0}, pm,qm = psi^{m0+1}; on exit p,q = psi^{m0-nsteps}, pm,qm = the      \
+ * level after it. Injection points must be distinct.                                           \
+ */                                                                                            \
+int vto_adjoint_ex_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2,        \
+                         const T *vn2, const T *vz2, T *p, T *q, T *pm, T *qm, int64_t m0,     \
+                         int32_t nsteps, int32_t nthreads, int32_t n_inj,                      \
+                         const int32_t *inj_ijk, int32_t inj_mask, int32_t inj_nt,             \
+                         int64_t inj_t_first, const T *inj_tr, int32_t n_rec,                  \
+                         const int32_t *rec_ijk, int32_t rec_mask, T *rec_out)                 \
+{                                                                                              \
+    int rc = check_params(P);                                                                  \
+    if (rc) return rc;                                                                         \
+    if (n_inj < 0 || n_rec < 0 || (n_inj > 0 && (!inj_ijk || !inj_tr || inj_nt < 0 ||          \
+        inj_mask < 1 || inj_mask > 3)) || (n_rec > 0 && (!rec_ijk || !rec_out ||                \
+        rec_mask < 1 || rec_mask > 3))) return 1;                                              \
+    const int R = P->r_xy, Rz = P->r_z, nx = P->nx, ny = P->ny, nz = P->nz;                    \
+    if (R >= 64 || Rz >= 64) return 1;                                                         \
+    const int64_t N = (int64_t)nx * ny * nz;                                                   \
+    for (int r = 0; r < n_rec; ++r) {                                                          \
+        const int i = rec_ijk[3 * r], j = rec_ijk[3 * r + 1], k = rec_ijk[3 * r + 2];          \
+        if (i < 0 || i >= nx || j < 0 || j >= ny || k < 0 || k >= nz) return 2;                \
+    }                                                                                          \
+    int32_t *inj_at = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);                          \
+    T *s1 = (T *)calloc((size_t)N, sizeof(T)), *s2 = (T *)calloc((size_t)N, sizeof(T));         \
+    T *nxt_p = (T *)malloc(sizeof(T) * (size_t)N), *nxt_q = (T *)malloc(sizeof(T) * (size_t)N);  \
+    if (!inj_at || !s1 || !s2 || !nxt_p || !nxt_q) {                                           \
+        free(inj_at); free(s1); free(s2); free(nxt_p); free(nxt_q); return 3;                  \
+    }                                                                                          \
+    for (int64_t u = 0; u < N; ++u) inj_at[u] = -1;                                            \
+    for (int r = 0; r < n_inj; ++r) {                                                          \
+        const int i = inj_ijk[3 * r], j = inj_ijk[3 * r + 1], k = inj_ijk[3 * r + 2];          \
+        const int64_t u = ((int64_t)k * ny + j) * nx + i;                                      \
+        if (i < 0 || i >= nx || j < 0 || j >= ny || k < 0 || k >= nz || inj_at[u] >= 0) {      \
+            free(inj_at); free(s1); free(s2); free(nxt_p); free(nxt_q);                        \
+            return (i < 0 || i >= nx || j < 0 || j >= ny || k < 0 || k >= nz) ? 2 : 1;         \
+        }                                                                                      \
+        inj_at[u] = r;                                                                         \
+    }                                                                                          \
+    T cxy[64];                                                                                 \
+    for (int l = 0; l <= R; ++l) cxy[l] = (T)((double)wxy[l] / (P->h * P->h));                 \
+    const T dt2 = (T)(P->dt * P->dt);                                                          \
+    const int nt = nthreads > 0 ? nthreads : vto_max_threads();                                \
+    const int rec_nf = (rec_mask & 1) + ((rec_mask >> 1) & 1);                                 \
+    T *cp = p, *cq = q, *op = pm, *oq = qm;   /* psi^m and psi^{m+1} */                        \
+    for (int32_t step = 0; step < nsteps; ++step) {                                            \
+        const int64_t m = m0 - step;                                                           \
+        const T *inj_row = (n_inj > 0 && m >= inj_t_first && m < inj_t_first + inj_nt)         \
+                               ? inj_tr + (m - inj_t_first) * (int64_t)n_inj : NULL;           \
+        _Pragma("omp parallel for num_threads(nt)")                                            \
+        for (int64_t u = 0; u < N; ++u) {                                                      \
+            s1[u] = FMA(vx2[u], cp[u], vn2[u] * cq[u]);                                        \
+            s2[u] = vz2[u] * (cp[u] + cq[u]);                                                  \
+        }                                                                                      \
+        _Pragma("omp parallel for collapse(2) num_threads(nt)")                                \
+        for (int k = 0; k < nz; ++k)                                                           \
+            for (int j = 0; j < ny; ++j)                                                       \
+                for (int i = 0; i < nx; ++i) {                                                 \
+                    const int64_t u = ((int64_t)k * ny + j) * nx + i;                          \
+                    T L = cxy[0] * s1[u];                                                      \
+                    for (int l = 1; l <= R; ++l) {                                             \
+                        const T xp = i + l < nx ? s1[u + l] : (T)0;                            \
+                        const T xm = i - l >= 0 ? s1[u - l] : (T)0;                            \
+                        const T yp = j + l < ny ? s1[u + (int64_t)l * nx] : (T)0;              \
+                        const T ym = j - l >= 0 ? s1[u - (int64_t)l * nx] : (T)0;              \
+                        L = FMA(cxy[l], (xp + xm) + (yp + ym), L);                             \
+                    }                                                                          \
+                    T DT = (T)0;                                                               \
+                    for (int mm = 0; mm <= 2 * Rz; ++mm) {                                     \
+                        const int kk = k + Rz - mm;                                            \
+                        if (kk < 0 || kk >= nz) continue;                                      \
+                        DT = FMA(wz[(int64_t)kk * (2 * Rz + 1) + mm],                          \
+                                 s2[((int64_t)kk * ny + j) * nx + i], DT);                     \
+                    }                                                                          \
+                    T Fp = L, Fq = DT;                                                         \
+                    const int ir = inj_row ? inj_at[u] : -1;                                   \
+                    if (ir >= 0 && (inj_mask & 1)) Fp = Fp + inj_row[ir];                      \
+                    if (ir >= 0 && (inj_mask & 2)) Fq = Fq + inj_row[ir];                      \
+                    const T g = ((T)vto_damping(i, nx, P->damp_width, P->damp_alpha) *         \
+                                 (T)vto_damping(j, ny, P->damp_width, P->damp_alpha)) *        \
+                                (T)vto_damping(k, nz, P->damp_width, P->damp_alpha);           \
+                    nxt_p[u] = g * FMA(dt2, Fp, FMA(-g, op[u], (T)2 * cp[u]));                 \
+                    nxt_q[u] = g * FMA(dt2, Fq, FMA(-g, oq[u], (T)2 * cq[u]));                 \
+                }                                                                              \
+        memcpy(op, nxt_p, sizeof(T) * (size_t)N);   /* psi^{m-1} over psi^{m+1} */              \
+        memcpy(oq, nxt_q, sizeof(T) * (size_t)N);                                              \
+        T *t;                                                                                  \
+        t = cp; cp = op; op = t;                                                               \
+        t = cq; cq = oq; oq = t;                                                               \
+        for (int r = 0; r < n_rec; ++r) {                                                      \
+            const int64_t u = ((int64_t)rec_ijk[3 * r + 2] * ny + rec_ijk[3 * r + 1]) * nx +   \
+                              rec_ijk[3 * r];                                                  \
+            T *o = rec_out + ((int64_t)step * n_rec + r) * rec_nf;                             \
+            if (rec_mask & 1) *o++ = cp[u];                                                    \
+            if (rec_mask & 2) *o = cq[u];                                                      \
+        }                                                                                      \
+    }                                                                                          \
+    if (cp != p) {   /* results back in the caller's arrays: p,q current, pm,qm the other */   \
+        memcpy(nxt_p, p, sizeof(T) * (size_t)N); memcpy(p, cp, sizeof(T) * (size_t)N);        \
+        memcpy(pm, nxt_p, sizeof(T) * (size_t)N);                                              \
+        memcpy(nxt_q, q, sizeof(T) * (size_t)N); memcpy(q, cq, sizeof(T) * (size_t)N);        \
+        memcpy(qm, nxt_q, sizeof(T) * (size_t)N);                                              \
+    }                                                                                          \
+    free(inj_at); free(s1); free(s2); free(nxt_p); free(nxt_q);                                \
+    return 0;                                                                                  \
+}                                                                                              \
+                                                                                               \
 /* Forward run, Ricker source only (the path every pin in tests/test_oracle_pins.py drives). */ \
 int vto_run_##SFX(const vto_params *P, const T *wxy, const T *wz, const T *vx2,               \
                   const T *vn2, const T *vz2, T *p, T *q, T *pm, T *qm, int64_t n0,            \
