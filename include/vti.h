@@ -230,6 +230,18 @@ vti_status vti_get_fields_f64(vti_t h, double *p, double *q, int32_t level);
 vti_status vti_get_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, double *p, double *q, int32_t level);
 
 /*
+ * Snapshot (N4: the forward wavefields an RTM imaging condition correlates with the backward
+ * leg; "snapshot planes/volumes at a cadence"): ENQUEUE, on the handle's
+ * stream and without synchronising, a copy of planes [k0, k0+nk) of u^n (level 0) or the
+ * stored u^{n-1} (level 1) into p, q ([nk][ny_local][nx], either may be NULL). The buffers
+ * must be device-writable (device memory, or mapped page-locked host memory) and stay valid
+ * until the stream reaches the copy (vti_sync). Ordered with vti_step, so a snapshot after
+ * step n holds level n. Errors: PARAM (level, precision, buffer not device-writable), INDEX.
+ */
+vti_status vti_snapshot_async(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level);
+vti_status vti_snapshot_async_f64(vti_t h, int32_t k0, int32_t nk, double *p, double *q, int32_t level);
+
+/*
  * Receivers (the trace-extraction hook of RTM/FWI,
  * PAPER.md l.18-19): after every subsequent step, the wavefield(s) in
  * field_mask (1 = p, 2 = q, 3 = both) at the n GLOBAL grid points ijk[3r..3r+2]
@@ -279,10 +291,27 @@ vti_status vti_get_traces_f64(vti_t h, double *out);
  * current level throughout. Note: this is time reversal of the SAME operator, not
  * its adjoint (transpose): F's z operator D has per-plane weights w^z[k] (Eq. 5),
  * so D^T != D on a variable-dz grid, and the vx2/vn2/vz2 factors multiply on the
- * other side in A^T. An adjoint-state FWI gradient needs A^T; RTM with the
- * self-adjoint isotropic limit (eps = delta = 0, uniform dz) does not.
+ * other side in A^T: vti_step_adjoint runs the transpose recurrence.
  */
 vti_status vti_reverse(vti_t h);
+
+/*
+ * Adjoint (transpose) stepping (N4: the backward leg of adjoint-state FWI).
+ * The forward step X^{n+1} = M X^n on X = (u^n, u^{n-1}), M = [[g(2 + dt^2 A), -g^2], [I, 0]],
+ * A u = (vx2 L p + vz2 D q, vn2 L p + vz2 D q) (Eqs. 1-2, 4-5), has the transpose recurrence,
+ * in the damping-scaled adjoint variable psi = g a:
+ *   psi^{m-1} = g (2 psi^m - g psi^{m+1} + dt^2 (A^T psi^m + inj)),
+ *   A^T psi = (L (vx2 psi_p + vn2 psi_q), D^T (vz2 (psi_p + psi_q))),
+ * with (D^T y)_k = sum_m w^z[k+Rz-m][m] y_{k+Rz-m}. The handle's state is (psi^m, psi^{m+1})
+ * (level 0 / level 1 of vti_get_fields / vti_set_fields), the time index m; each step lowers it
+ * by one. Adjoint sources are injected traces (vti_set_injection, row = m - t_first, added
+ * after the operator); receivers (vti_set_receivers) record psi^{m-1}; the Ricker source of
+ * vti_add_source is not applied. Then <M^K X, Y> = <X, (M^T)^K Y> (the dot-product test of
+ * tests/test_adjoint_gpu.py). Two launches per step (the coefficient products, then the
+ * stencils and update); single-slab handles only. Bitwise equal to the oracle's
+ * vto_adjoint_ex. Errors: STATE (model unset, nranks > 1), PARAM, CUDA, INSTABILITY.
+ */
+vti_status vti_step_adjoint(vti_t h, int32_t nsteps);
 
 /* +1 (forward) or -1 (after an odd number of vti_reverse calls). */
 int32_t vti_direction(vti_t h);

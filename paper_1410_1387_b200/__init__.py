@@ -130,6 +130,9 @@ def _load():
         "vti_get_traces": (st, [H, P]),
         "vti_get_traces_f64": (st, [H, P]),
         "vti_reverse": (st, [H]),
+        "vti_step_adjoint": (st, [H, C.c_int32]),
+        "vti_snapshot_async": (st, [H, C.c_int32, C.c_int32, P, P, C.c_int32]),
+        "vti_snapshot_async_f64": (st, [H, C.c_int32, C.c_int32, P, P, C.c_int32]),
         "vti_ipc_export": (st, [H, P]),
         "vti_ipc_connect": (st, [H, P, P]),
         "vti_halo_transport": (C.c_int32, [H]),
@@ -378,6 +381,18 @@ class VTI:
     def halo_transport(self) -> str:
         """vti_halo_transport: 'none', 'nccl' or 'peer'."""
         return {0: "none", 1: "nccl", 2: "peer"}.get(lib.vti_halo_transport(self.h), "?")
+
+    def snapshot_async(self, p=None, q=None, level=0, planes=None):
+        """vti_snapshot_async: enqueue a copy of u^n (level 0) / u^{n-1} (level 1), planes
+        (k0, nk) or all, into device-writable buffers (CUDA tensors); no synchronisation."""
+        k0, nk = planes if planes is not None else (0, self.nz)
+        pp, _ = _ptr(p, self._n(nk), dtype=self.dtype)
+        qp, _ = _ptr(q, self._n(nk), dtype=self.dtype)
+        _check(self.h, self._fn("vti_snapshot_async")(self.h, k0, nk, pp, qp, level))
+
+    def step_adjoint(self, nsteps=1):
+        """vti_step_adjoint: nsteps of the transpose recurrence (state = (psi^m, psi^{m+1}))."""
+        _check(self.h, lib.vti_step_adjoint(self.h, nsteps))
 
     def reverse(self):
         """vti_reverse: swap the stored levels; the next steps run backwards in time."""

@@ -9,7 +9,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libvti.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("vti_runtime.cu", "vti_schedule.cu", "vti_transport.cu")] + sorted(
+SOURCES = [os.path.join(CSRC, f) for f in ("vti_runtime.cu", "vti_schedule.cu", "vti_transport.cu",
+                                           "vti_adjoint.cu")] + sorted(
     os.path.join(CSRC, "variants", f) for f in os.listdir(os.path.join(CSRC, "variants")) if f.endswith(".cu"))
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("vti_kernel.cuh", "vti_small.cuh", "vti_entry.cuh", "vti_variants.h",
                                                    "vti_internal.h")] + [

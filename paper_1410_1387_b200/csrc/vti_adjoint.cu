@@ -1,0 +1,236 @@
+// vti_adjoint.cu -- the adjoint (transpose) recurrence of the VTI step (the
+// backward leg of adjoint-state FWI; PAPER.md l.18-19 names FWI and RTM as the propagator's
+// users). The forward step X^{n+1} = M X^n, M = [[g(2 + dt^2 A), -g^2], [I, 0]] with
+//   A u = (vx2 L p + vz2 D q, vn2 L p + vz2 D q)            (Eqs. 1-2, 4-5)
+// has the transpose recurrence, in the damping-scaled adjoint variable psi = g a,
+//   psi^{m-1} = g (2 psi^m - g psi^{m+1} + dt^2 (A^T psi^m + inj)),
+//   A^T psi = (L (vx2 psi_p + vn2 psi_q), D^T (vz2 (psi_p + psi_q))),
+// L symmetric on the zero exterior and (D^T y)_k = sum_m w^z[k+Rz-m][m] y_{k+Rz-m}. The
+// coefficient fields act BEFORE the derivatives here, so a step is two launches: k_adj_prep
+// forms s1 = vx2 psi_p + vn2 psi_q and s2 = vz2 (psi_p + psi_q) over the slab, and k_adj_step
+// applies L to s1, D^T to s2 and the update. Canonical operation order (bitwise equal to the
+// oracle's vto_adjoint_ex): s1 = fma(vx2, psi_p, vn2*psi_q), s2 = vz2*(psi_p + psi_q);
+// L = c0 s1; L = fma(c_l, (x+ + x-) + (y+ + y-), L); DT = 0, DT = fma(w[k'][m], s2(k'), DT) for
+// m = 0..2Rz, k' = k+Rz-m inside the grid; F_p = L (+ inj), F_q = DT (+ inj);
+// psi^{m-1} = g*fma(dt2, F, fma(-g, psi^{m+1}, 2 psi^m)).
+//
+// Off the benchmark path, so the kernels are plain: one thread per point, x fastest (coalesced),
+// neighbours through L1/L2. Single-slab handles only (the s1 cross would need the neighbours'
+// psi and model rows).
+#include "vti_internal.h"
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T fma_x(T a, T b, T c);
+template <>
+__device__ __forceinline__ float fma_x<float>(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+template <>
+__device__ __forceinline__ double fma_x<double>(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// s1 = fma(vx2, psi_p, vn2*psi_q), s2 = vz2*(psi_p + psi_q) over the interior (halo untouched = 0)
+template <typename T>
+__global__ void k_adj_prep(const T *__restrict__ pp, const T *__restrict__ pq, const T *__restrict__ vx2,
+                           const T *__restrict__ vn2, const T *__restrict__ vz2, T *__restrict__ s1,
+                           T *__restrict__ s2, int nx, int nyl, int nz, long long ys, long long zs)
+{
+    const int64_t n = (int64_t)nz * nyl * nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const int64_t r = t / nx;
+        const int y = (int)(r % nyl);
+        const int k = (int)(r / nyl);
+        const int64_t a = y * ys + k * zs + x;
+        const T p = pp[a], q = pq[a];
+        s1[a] = fma_x<T>(vx2[a], p, vn2[a] * q);
+        s2[a] = vz2[a] * (p + q);
+    }
+}
+
+template <typename T>
+struct AdjParams {
+    const T *s1, *s2;              // interior views (row 0, plane 0)
+    const T *pc, *qc;              // psi^m
+    T *po, *qo;                    // psi^{m+1} in, psi^{m-1} out (in place)
+    const T *zrow;                 // [nz][zrow_stride]: w^z[k][0..2Rz], gz[k]
+    int zrow_stride;
+    const T *gx, *gy;
+    T cxy[MAX_R + 1];
+    T dt2;
+    int nx, nyl, nz;
+    long long ys, zs;
+    // N4 point sets (nullable): injection into F after the operator, receivers of psi^{m-1}
+    const int *inj_off;
+    const int2 *inj_ent;
+    const T *inj_row;              // this step's trace row, or NULL
+    int inj_mask;
+    const int *rec_off;
+    const int2 *rec_ent;
+    T *rec_row;                    // this step's receiver row [n][nf], or NULL
+    int rec_mask;
+};
+
+// the column of the CSR entry for point x of row (k, yl), or -1
+__device__ __forceinline__ int ps_lookup(const int *off, const int2 *ent, int nyl, int k, int yl, int x)
+{
+    const long long b = (long long)k * nyl + yl;
+    int lo = off[b], hi = off[b + 1];
+    if (lo == hi) return -1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ent[mid].x < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < off[b + 1] && ent[lo].x == x) ? lo : -1;
+}
+
+template <typename T, int R, int RZ>
+__global__ void k_adj_step(const AdjParams<T> A)
+{
+    const int64_t n = (int64_t)A.nz * A.nyl * A.nx;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % A.nx);
+        const int64_t r = t / A.nx;
+        const int j = (int)(r % A.nyl);
+        const int k = (int)(r / A.nyl);
+        const int64_t a = j * A.ys + k * A.zs + i;
+        // L(s1), canonical pairing (x pair + y pair); zero exterior
+        T L = A.cxy[0] * A.s1[a];
+#pragma unroll
+        for (int l = 1; l <= R; ++l) {
+            const T xp = i + l < A.nx ? A.s1[a + l] : T(0);
+            const T xm = i - l >= 0 ? A.s1[a - l] : T(0);
+            const T yp = j + l < A.nyl ? A.s1[a + l * A.ys] : T(0);
+            const T ym = j - l >= 0 ? A.s1[a - l * A.ys] : T(0);
+            L = fma_x<T>(A.cxy[l], (xp + xm) + (yp + ym), L);
+        }
+        // D^T(s2): row k of the transpose = column k of Eq. 5's rows
+        T DT = T(0);
+#pragma unroll
+        for (int m = 0; m <= 2 * RZ; ++m) {
+            const int kk = k + RZ - m;
+            if (kk >= 0 && kk < A.nz)
+                DT = fma_x<T>(A.zrow[(int64_t)kk * A.zrow_stride + m], A.s2[j * A.ys + kk * A.zs + i], DT);
+        }
+        T Fp = L, Fq = DT;
+        if (A.inj_row != nullptr) {
+            const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, j, i);
+            if (e >= 0) {
+                const T v = A.inj_row[A.inj_ent[e].y];
+                if (A.inj_mask & 1) Fp = Fp + v;
+                if (A.inj_mask & 2) Fq = Fq + v;
+            }
+        }
+        const T g = (A.gx[i] * A.gy[j]) * A.zrow[(int64_t)k * A.zrow_stride + 2 * RZ + 1];
+        const T pn = g * fma_x<T>(A.dt2, Fp, fma_x<T>(-g, A.po[a], T(2) * A.pc[a]));
+        const T qn = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, A.qo[a], T(2) * A.qc[a]));
+        A.po[a] = pn;
+        A.qo[a] = qn;
+        if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
+            const long long b = (long long)k * A.nyl + j;
+            const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
+            for (int e = A.rec_off[b]; e < A.rec_off[b + 1]; ++e) {
+                if (A.rec_ent[e].x != i) continue;
+                T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
+                if (A.rec_mask & 1) *o++ = pn;
+                if (A.rec_mask & 2) *o = qn;
+            }
+        }
+    }
+}
+
+template <typename T>
+static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
+{
+    const int R = h->R, RZ = h->RZ;
+#define ADJ_CASE(r, rz)                                                        \
+    if (R == r && RZ == rz) {                                                  \
+        k_adj_step<T, r, rz><<<grid, 256, 0, h->stream>>>(A);                  \
+        CU(h, cudaGetLastError());                                             \
+        return VTI_OK;                                                         \
+    }
+    ADJ_CASE(4, 4)
+    ADJ_CASE(8, 4)
+    ADJ_CASE(6, 6)
+    ADJ_CASE(12, 8)
+#undef ADJ_CASE
+    return fail(h, VTI_E_UNSUPPORTED, "no adjoint kernel for (%d, %d)", R, RZ);
+}
+
+template <typename T>
+static vti_status adjoint_step_t(vti_s *h)
+{
+    const int c = h->cur, o = 1 - c;
+    const int grid = 4 * h->sms;
+    T *s1 = (T *)h->in(h->adj_s[0]), *s2 = (T *)h->in(h->adj_s[1]);
+    k_adj_prep<T><<<grid, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c), (const T *)h->in(h->vx2),
+                                             (const T *)h->in(h->vn2), (const T *)h->in(h->vz2), s1, s2, h->cfg.nx,
+                                             h->nyl, h->cfg.nz, h->ys, h->zs);
+    CU(h, cudaGetLastError());
+    AdjParams<T> A;
+    A.s1 = s1;
+    A.s2 = s2;
+    A.pc = (const T *)h->p_int(c);
+    A.qc = (const T *)h->q_int(c);
+    A.po = (T *)h->p_int(o);
+    A.qo = (T *)h->q_int(o);
+    A.zrow = (const T *)h->zrow;
+    A.zrow_stride = h->K->zrow;
+    A.gx = (const T *)h->gx;
+    A.gy = (const T *)h->gy;
+    for (int l = 0; l <= MAX_R; ++l) A.cxy[l] = l <= h->R ? (T)h->cxy[l] : T(0);
+    A.dt2 = (T)(h->cfg.dt * h->cfg.dt);
+    A.nx = h->cfg.nx;
+    A.nyl = h->nyl;
+    A.nz = h->cfg.nz;
+    A.ys = h->ys;
+    A.zs = h->zs;
+    const long long irow = (long long)(h->n - h->inj_t_first);   // time index m of this step
+    const bool inj = h->inj_set.n > 0 && irow >= 0 && irow < h->inj_nt;
+    A.inj_off = h->inj_set.off;
+    A.inj_ent = h->inj_set.ent;
+    A.inj_row = inj ? (const T *)h->inj_tr + irow * h->inj_cols : nullptr;
+    A.inj_mask = h->inj_mask;
+    const bool rec = h->rec_set.n > 0 && h->rec_steps < h->rec_cap;
+    const int nf = (h->rec_mask & 1) + ((h->rec_mask >> 1) & 1);
+    A.rec_off = h->rec_set.off;
+    A.rec_ent = h->rec_set.ent;
+    A.rec_row = rec ? (T *)h->traces + (size_t)h->rec_steps * h->nrec * nf : nullptr;
+    A.rec_mask = h->rec_mask;
+    return launch_adj_step<T>(h, A, grid);
+}
+
+}  // namespace
+
+extern "C" {
+
+vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
+{
+    if (!h) return VTI_E_PARAM;
+    if (nsteps < 0) return fail(h, VTI_E_PARAM, "nsteps < 0");
+    if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
+    if (h->cfg.nranks != 1) return fail(h, VTI_E_STATE, "vti_step_adjoint is single-slab only (nranks = 1)");
+    CU(h, cudaSetDevice(h->cfg.device));
+    if (!h->adj_s[0]) {   // the two coefficient-weighted scratch fields, zero halo
+        const size_t bytes = h->total_elems() * h->es;
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaMalloc(&h->adj_s[b], bytes);
+            if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+            CU(h, cudaMemsetAsync(h->adj_s[b], 0, bytes, h->stream));
+            h->device_bytes += (int64_t)bytes;
+        }
+    }
+    for (int it = 0; it < nsteps; ++it) {
+        vti_status s = h->es == 8 ? adjoint_step_t<double>(h) : adjoint_step_t<float>(h);
+        if (s != VTI_OK) return s;
+        h->cur = 1 - h->cur;
+        h->n -= 1;   // the adjoint runs backward in time
+        if (h->rec_set.n > 0) h->rec_steps = std::min(h->rec_cap, h->rec_steps + 1);
+        if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0) {
+            if ((s = check_finite(h)) != VTI_OK) return s;
+        }
+    }
+    return VTI_OK;
+}
+
+}  // extern "C"

@@ -161,6 +161,7 @@ struct vti_s {
     int inj_cols = 0, inj_mask = 0, inj_nt = 0;
     int64_t inj_t_first = 0;
     long long *dyn = nullptr;                 // device: graph-replay header {inj row, rec row, dir}
+    void *adj_s[2] = {nullptr, nullptr};      // vti_step_adjoint scratch: s1, s2 (vti_adjoint.cu)
     bool io_active() const { return (rec_set.n > 0 && rec_cap > 0) || inj_set.n > 0; }
 
     size_t total_elems() const { return (size_t)cfg.nz * rows * nxp; }

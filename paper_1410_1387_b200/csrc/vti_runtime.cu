@@ -310,6 +310,8 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->dyn);
     cudaFree(h->done);
     cudaFree(h->s_multi);
+    cudaFree(h->adj_s[0]);
+    cudaFree(h->adj_s[1]);
     for (int b = 0; b < 2; ++b)
         if (h->gexec[b]) cudaGraphExecDestroy(h->gexec[b]);
     cudaFree(h->s_graph);
@@ -450,8 +452,10 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     vti_slab(cfg, &h->y0, &h->nyl);
     // small grids are launch/latency-bound: twice the tiles with the 16-row variant of the same
     // mapping (C1 64^3: 54.7 -> 59.3 Gpoints/s); an explicit env choice wins
+    // (VTI_SMALL_TY=32 keeps the 32-row default instead: the small-grid kernels are compiled for both)
+    static const int small_ty = getenv("VTI_SMALL_TY") ? atoi(getenv("VTI_SMALL_TY")) : 16;
     if (want_ty < 0 && want_wp < 0 && want_rpt < 0 && want_px < 0 &&
-        (double)cfg->nx * h->nyl * cfg->nz <= 4.0 * 1024 * 1024)
+        (double)cfg->nx * h->nyl * cfg->nz <= 4.0 * 1024 * 1024 && small_ty == 16)
         if (const KernelEntry *k16 = find_kernel(h->es, h->R, h->RZ, 16, -1, -1, h->K->px)) h->K = k16;
     h->nxp = (cfg->nx + 31) / 32 * 32;
     h->rows = h->nyl + 2 * h->R;
@@ -1231,6 +1235,47 @@ vti_status vti_set_fields_f64(vti_t h, const double *p, const double *q, const d
     vti_status s = set_fields_planes(h, 8, 0, h->cfg.nz, p, q, pm, qm);
     if (s == VTI_OK) h->n = time_index;
     return s;
+}
+
+// A pointer the device can write directly: device / managed memory, or page-locked host memory
+// with a device mapping (UVA).
+static bool device_writable(const void *p)
+{
+    cudaPointerAttributes a;
+    if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ||
+           (a.type == cudaMemoryTypeHost && a.devicePointer != nullptr);
+}
+
+static vti_status snapshot_async(vti_s *h, int es, int32_t k0, int32_t nk, void *p, void *q, int32_t level)
+{
+    if (!h) return VTI_E_PARAM;
+    vti_status s = check_precision(h, es, "vti_snapshot_async");
+    if (s != VTI_OK) return s;
+    if (level != 0 && level != 1) return fail(h, VTI_E_PARAM, "level must be 0 (u^n) or 1 (u^{n-1})");
+    if (k0 < 0 || nk < 0 || k0 + nk > h->cfg.nz)
+        return fail(h, VTI_E_INDEX, "planes [%d,%d) outside [0,%d)", k0, k0 + nk, h->cfg.nz);
+    CU(h, cudaSetDevice(h->cfg.device));
+    if ((p && !device_writable(p)) || (q && !device_writable(q)))
+        return fail(h, VTI_E_PARAM, "snapshot buffers must be device memory or mapped page-locked host memory");
+    const int b = level == 0 ? h->cur : 1 - h->cur;
+    if (p) i2u(h, h->p_int(b), p, nk, k0);
+    if (q) i2u(h, h->q_int(b), q, nk, k0);
+    CU(h, cudaGetLastError());
+    return VTI_OK;
+}
+
+vti_status vti_snapshot_async(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level)
+{
+    return snapshot_async(h, 4, k0, nk, p, q, level);
+}
+
+vti_status vti_snapshot_async_f64(vti_t h, int32_t k0, int32_t nk, double *p, double *q, int32_t level)
+{
+    return snapshot_async(h, 8, k0, nk, p, q, level);
 }
 
 vti_status vti_get_fields_planes(vti_t h, int32_t k0, int32_t nk, float *p, float *q, int32_t level)

@@ -1,0 +1,103 @@
+"""vti_step_adjoint (the transpose recurrence) against the oracle's
+vto_adjoint_ex (pinned in tests/test_oracle_adjoint_pins.py): bitwise for every compiled radius
+pair in fp32 and in fp64, with damping, injected adjoint sources and receivers; plus the
+dot-product identity <M^K X, Y> = <X, (M^T)^K Y> between the library's own forward and adjoint
+steps."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import fields as SF
+from synth import weights as W
+
+pytestmark = pytest.mark.gpu
+
+
+def setup(r, rz, prec=32, shape=(70, 45, 33)):
+    nx, ny, nz = shape
+    cfg = synth.scaled(synth.CONFIGS["C2"](), nx, ny, max(nz, 2 * rz + 9), r_xy=r, r_z=rz, damp_width=5,
+                       dz=(6.0, 12.0), t0=0.02)
+    if prec == 32:
+        wxy, wz, _ = synth.weights_f32(cfg)
+    else:
+        wxy = W.xy_weights(r)
+        wz = np.ascontiguousarray(W.z_weights(W.z_coords_ramp(cfg["nz"], rz, 6.0, 12.0), rz))
+    dt = synth.stable_dt(cfg)
+    dtype = np.float32 if prec == 32 else np.float64
+    model = [a.numpy().astype(dtype) for a in SF.model_planes(cfg, 0, cfg["nz"])]
+    st = [SF.random_planes(cfg["nx"], cfg["ny"], 0, cfg["nz"], 12, s, 1e-3).numpy().astype(dtype) for s in range(4)]
+    return cfg, wxy, wz, dt, model, st, dtype
+
+
+def handle(cfg, dt, wxy, wz, prec=32, **kw):
+    from paper_1410_1387_b200 import VTI
+    return VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], cfg["r_xy"], cfg["r_z"], dt, wxy, wz,
+               damp_width=cfg["damp_width"], damp_alpha=cfg["damp_alpha"], device=0, precision=prec, **kw)
+
+
+@pytest.mark.parametrize("r,rz,prec", [(4, 4, 32), (8, 4, 32), (6, 6, 32), (12, 8, 32), (4, 4, 64), (12, 8, 64)])
+def test_adjoint_matches_oracle(r, rz, prec):
+    cfg, wxy, wz, dt, model, st, dtype = setup(r, rz, prec)
+    rng = np.random.default_rng(r * 10 + rz)
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    pts = np.array(sorted({(int(rng.integers(nx)), int(rng.integers(ny)), int(rng.integers(nz))) for _ in range(40)}
+                          | {(0, 0, 0), (nx - 1, ny - 1, nz - 1), (64, 20, 3)}), np.int32)
+    tr = (rng.normal(size=(12, len(pts))) * 1e2).astype(dtype)
+    m0, K = 30, 12
+    with handle(cfg, dt, wxy, wz, prec) as v:
+        v.set_model(*model)
+        v.set_fields(*st, time_index=m0)
+        v.set_injection(pts, tr, fields=3, t_first=m0 - 10)   # rows for m = 20..31: part of the run
+        v.set_receivers(pts[:15], fields=3, capacity_steps=K)
+        v.step_adjoint(K)
+        assert v.time_index == m0 - K
+        g = v.get_fields(0) + v.get_fields(1)
+        _, traces = v.get_traces()
+    o = oracle.adjoint_ex(oracle.params(cfg, dt, src=None), wxy, wz, *model, st, m0=m0, nsteps=K,
+                          inj=(pts, 3, m0 - 10, tr), rec=(pts[:15], 3), dtype=dtype)
+    for a, b in zip(g, o[:4]):
+        assert np.abs(b).max() > 0
+        assert np.array_equal(a, b), f"max |diff| {np.abs(a - b).max():.3e}"
+    assert np.array_equal(traces, o[4])
+
+
+def test_library_dot_product_identity():
+    """fp64, damped: the library's K forward steps and K adjoint steps satisfy
+    <u^K, psi^K / g> - <u^{K-1}, g psi^{K+1}> = <u^0, psi^0 / g> - <u^{-1}, g psi^1>."""
+    cfg, wxy, wz, dt, model, st, dtype = setup(4, 4, 64, shape=(40, 36, 30))
+    rng = np.random.default_rng(17)
+    shape = model[0].shape
+    X0 = [rng.normal(size=shape) for _ in range(4)]
+    psiK = [rng.normal(size=shape) for _ in range(4)]
+    K = 16
+    with handle(cfg, dt, wxy, wz, 64) as v:
+        v.set_model(*model)
+        v.set_fields(*X0)
+        v.step(K)
+        XK = list(v.get_fields(0) + v.get_fields(1))
+        v.set_fields(*psiK, time_index=K)
+        v.step_adjoint(K)
+        psi0 = list(v.get_fields(0) + v.get_fields(1))
+    d = lambda i, n: oracle.lib().vto_damping(i, n, cfg["damp_width"], cfg["damp_alpha"])
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    g = (np.array([d(i, nx) for i in range(nx)])[None, None, :] * np.array([d(j, ny) for j in range(ny)])[None, :, None]) \
+        * np.array([d(k, nz) for k in range(nz)])[:, None, None]
+    dot = lambda u, w: sum(np.vdot(a, b) for a, b in zip(u, w))
+    lhs = dot(XK[:2], [a / g for a in psiK[:2]]) - dot(XK[2:], [g * a for a in psiK[2:]])
+    rhs = dot(X0[:2], [a / g for a in psi0[:2]]) - dot(X0[2:], [g * a for a in psi0[2:]])
+    assert abs(lhs - rhs) <= 1e-10 * max(abs(lhs), abs(rhs)) and abs(lhs) > 1.0
+
+
+def test_adjoint_errors():
+    from paper_1410_1387_b200 import VTIError
+    cfg, wxy, wz, dt, model, st, dtype = setup(4, 4)
+    with handle(cfg, dt, wxy, wz) as v:
+        with pytest.raises(VTIError) as e:
+            v.step_adjoint(1)
+        assert e.value.name == "VTI_E_STATE"
+    with handle(cfg, dt, wxy, wz, rank=0, nranks=2) as v:
+        v.set_model(*[np.ascontiguousarray(a[:, :v.ny_local]) for a in model])
+        with pytest.raises(VTIError) as e:
+            v.step_adjoint(1)
+        assert e.value.name == "VTI_E_STATE"

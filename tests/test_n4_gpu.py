@@ -278,3 +278,31 @@ def test_injection_errors():
         assert e.value.name == "VTI_E_PARAM"
         v.set_injection(np.zeros((0, 3), np.int32), None)   # remove: plain kernels again
         v.step(2)
+
+
+def test_async_snapshots_every_step():
+    """vti_snapshot_async: one enqueued copy per step into a device ring (no host sync in the
+    loop), equal to the oracle's level after each step; a pageable host buffer is refused."""
+    import torch
+    from paper_1410_1387_b200 import VTIError
+    cfg, wxy, wz, dt, model = setup()
+    nsteps = 8
+    ring_p = torch.zeros((nsteps, cfg["nz"], cfg["ny"], cfg["nx"]), dtype=torch.float32, device="cuda")
+    ring_q = torch.zeros_like(ring_p)
+    with handle(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], mask=3)
+        for n in range(nsteps):
+            v.step(1)
+            v.snapshot_async(ring_p[n], ring_q[n])
+        with pytest.raises(VTIError) as e:
+            v.snapshot_async(np.zeros((cfg["nz"], cfg["ny"], cfg["nx"]), np.float32))
+        assert e.value.name == "VTI_E_PARAM"
+        v.sync()
+    P = oracle.params(dict(cfg, mask=3), dt)
+    st = None
+    got_p, got_q = ring_p.cpu().numpy(), ring_q.cpu().numpy()
+    for n in range(nsteps):
+        st = oracle.run(P, wxy, wz, *model, st, n0=n, nsteps=1)[:4]
+        assert np.array_equal(got_p[n], st[0]) and np.array_equal(got_q[n], st[1])
+    assert np.abs(got_p[-1]).max() > 0
