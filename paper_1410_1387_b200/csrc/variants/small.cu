@@ -20,9 +20,8 @@ SmallTable vti_small_kernels()
     // fp32 only: an fp64 item (128 KB of shared memory, 1 CTA per SM) measured slower than the
     // persistent fp64 kernel on C1 (32.5 vs 39.4 Gpoints/s)
     static const SmallEntry t[] = {small_entry<float, 4, 4, 16>(), small_entry<float, 8, 4, 16>(),
-                                   small_entry<float, 6, 6, 16>(),
-                                   // 32-row tiles (VTI_SMALL_TY=32): half the items, one CTA per SM
-                                   small_entry<float, 4, 4, 32>(), small_entry<float, 8, 4, 32>(),
-                                   small_entry<float, 6, 6, 32>()};
+                                   small_entry<float, 6, 6, 16>()};
+    // 32-row small-grid tiles (128 items on C1, one CTA per SM) measured slower in round 2:
+    // one-step 74.5 vs 77.8-78.1 Gpoints/s, multi-step 47 vs 34 (both below the default)
     return SmallTable{t, (int)(sizeof t / sizeof t[0])};
 }

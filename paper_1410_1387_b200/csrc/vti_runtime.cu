@@ -452,10 +452,8 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
     vti_slab(cfg, &h->y0, &h->nyl);
     // small grids are launch/latency-bound: twice the tiles with the 16-row variant of the same
     // mapping (C1 64^3: 54.7 -> 59.3 Gpoints/s); an explicit env choice wins
-    // (VTI_SMALL_TY=32 keeps the 32-row default instead: the small-grid kernels are compiled for both)
-    static const int small_ty = getenv("VTI_SMALL_TY") ? atoi(getenv("VTI_SMALL_TY")) : 16;
     if (want_ty < 0 && want_wp < 0 && want_rpt < 0 && want_px < 0 &&
-        (double)cfg->nx * h->nyl * cfg->nz <= 4.0 * 1024 * 1024 && small_ty == 16)
+        (double)cfg->nx * h->nyl * cfg->nz <= 4.0 * 1024 * 1024)
         if (const KernelEntry *k16 = find_kernel(h->es, h->R, h->RZ, 16, -1, -1, h->K->px)) h->K = k16;
     h->nxp = (cfg->nx + 31) / 32 * 32;
     h->rows = h->nyl + 2 * h->R;
