@@ -105,7 +105,6 @@ struct vti_s {
     CUtensorMap tm_ph[2], tm_pi[2], tm_q[2], tm_vx, tm_vn, tm_vz;
     CUtensorMap tm_qcol[2];                   // q^n column views (box depth 2 R_z + 1) for the small-grid kernel
     const SmallEntry *small = nullptr;        // small-grid kernel in use (single slab, 1-plane items), or NULL
-    bool small_chain = false;                 // the launch being issued follows this handle's previous step kernel
     // multi-step small-grid kernel (vti_small_multi_kernel): one cooperative launch per vti_step
     // call (chunks of MULTI_MAX steps); done[] = per-item epoch counters, multi_epoch their value
     int multi_slots = 0;                      // co-resident multi-step CTAs on the device

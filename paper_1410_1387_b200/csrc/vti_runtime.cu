@@ -839,14 +839,6 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
         S.P.sync_ctr = nullptr;
         S.P.sync_base = 0;
         S.tm_qcol = h->tm_qcol[h->cur];
-        // VTI_SMALL_FLAGS: bit 0 early independent loads, bit 1 early dependent-launch trigger.
-        // Not both: an early trigger lets step n+1 start before step n has waited for step n-1,
-        // and u^n (step n+1's early u^{n-1} load) is step n-1's output.
-        // Early loads only when the previous launch on the stream is this handle's previous
-        // one-step kernel (h->small_chain), whose own wait ordered step n-1 before it.
-        static const int small_flags = getenv("VTI_SMALL_FLAGS") ? (atoi(getenv("VTI_SMALL_FLAGS")) & 3) : 0;
-        S.flags = small_flags == 3 ? 1 : small_flags;
-        if (!h->small_chain) S.flags &= ~1;
         cudaLaunchConfig_t sl = {};
         sl.gridDim = dim3(P.items);
         sl.blockDim = dim3(h->small->threads);
@@ -1333,10 +1325,8 @@ static vti_status build_graph(vti_s *h, int c)
     for (int i = 0; i < GRAPH_STEPS && s == VTI_OK; ++i) {
         h->cur = (c + i) & 1;
         h->capture_index = i;
-        h->small_chain = i > 0;   // node i follows node i - 1 (a memcpy precedes node 0)
         s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk, h->cap);
     }
-    h->small_chain = false;
     h->capturing = false;
     h->cur = keep_cur;
     cudaError_t e = cudaStreamEndCapture(h->stream, &g);
@@ -1503,15 +1493,11 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     // diagnostic: VTI_FORCE_SPLIT=1 runs a single slab with the multi-GPU two-launch schedule
     // (edge tile rows, then interior; no transport) to time what one rank's GPU does per step
     static const bool force_split = getenv("VTI_FORCE_SPLIT") && atoi(getenv("VTI_FORCE_SPLIT")) != 0;
-    const int it_direct0 = it;
     for (; it < nsteps; ++it) {
         if (!multi && force_split) {
             if ((s = launch_edge(h)) != VTI_OK || (s = launch_interior(h)) != VTI_OK) return s;
         } else if (!multi) {
-            h->small_chain = it > it_direct0;   // the previous launch was this loop's step kernel
-            s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk, h->cap);
-            h->small_chain = false;
-            if (s != VTI_OK) return s;
+            if ((s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk, h->cap)) != VTI_OK) return s;
         } else if (h->peer && h->fused()) {
             // one launch: edge items first (their PEER stores feed the neighbours' halos), the
             // last edge item raises the neighbours' flags from the device, the interior follows

@@ -21,9 +21,6 @@ template <typename T>
 struct SmallParams {
     StepParams<T> P;
     CUtensorMap tm_qcol;   // q^n interior view, box {TX, TY, 2 R_z + 1}
-    int flags;             // bit 0: issue the loads that do not depend on the previous step
-                           // before griddepcontrol.wait; bit 1: trigger the dependent launch early
-                           // (never both: see the runtime)
 };
 
 template <typename T, int R, int RZ, int TY>
@@ -149,27 +146,19 @@ __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (S.flags & 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        mbar_arrive_expect_tx(bar, SC::TX_BYTES);
-        // Loads that do not depend on the previous step (programmatic dependent launch): the
-        // model, the w^z row and u^{n-1} -- written two steps back, complete before the previous
-        // step's CTAs could exit and let this grid start; the previous step never writes it.
-        const bool early = S.flags & 1;
-        auto static_loads = [&] {
-            tma_load_3d(smem + SC::OFF_PM, &P.tm_pm, x0, y0, k, bar);
-            tma_load_3d(smem + SC::OFF_QM, &P.tm_qm, x0, y0, k, bar);
-            tma_load_3d(smem + SC::OFF_VX, &P.tm_vx, x0, y0, k, bar);
-            tma_load_3d(smem + SC::OFF_VN, &P.tm_vn, x0, y0, k, bar);
-            tma_load_3d(smem + SC::OFF_VZ, &P.tm_vz, x0, y0, k, bar);
-            bulk_load(smem + SC::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * C::ES, bar);
-        };
-        if (early) static_loads();
-        // the previous grid must complete before this item reads u^n / overwrites u^{n-1}
+        // programmatic dependent launch: everything above overlaps the previous step; the
+        // previous grid must complete before this item reads u^n / overwrites u^{n-1}
         // (no-op without the launch attribute). Every store below follows these loads.
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        mbar_arrive_expect_tx(bar, SC::TX_BYTES);
         tma_load_3d(smem + SC::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
         tma_load_3d(smem + SC::OFF_Q, &S.tm_qcol, x0, y0, k - RZ, bar);
-        if (!early) static_loads();
+        tma_load_3d(smem + SC::OFF_PM, &P.tm_pm, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_QM, &P.tm_qm, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_VX, &P.tm_vx, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_VN, &P.tm_vn, x0, y0, k, bar);
+        tma_load_3d(smem + SC::OFF_VZ, &P.tm_vz, x0, y0, k, bar);
+        bulk_load(smem + SC::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * C::ES, bar);
     }
     // independent of the loads: this thread's columns, damping and output pointers
     const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
