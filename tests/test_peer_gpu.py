@@ -314,3 +314,38 @@ def test_staged_transport_with_receivers_and_injection():
     for f in range(4):
         assert np.array_equal(got[f], o[f])
     assert np.array_equal(traces, o[4])
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_fused_step_with_point_sets(nranks, monkeypatch):
+    """The fused one-launch peer step (the multi-process default) with trace injection and
+    receivers: its PEER + IO instantiation, bitwise == oracle (vto_run_ex)."""
+    from paper_1410_1387_b200 import group_step
+    monkeypatch.setenv("VTI_FUSED_STEP", "1")
+    ny = nranks * 64
+    cfg = small_cfg(70, ny, 20, 4, 4, damp=5)
+    cfg["src"] = (30, ny // nranks, 10)
+    wxy, wz, dt, model, st = f32_inputs(cfg)
+    rng = np.random.default_rng(nranks)
+    pts = {(30, ny // nranks - 1, 10), (30, ny // nranks, 10), (0, 0, 0), (69, ny - 1, 19)}
+    while len(pts) < 40:
+        pts.add((int(rng.integers(70)), int(rng.integers(ny)), int(rng.integers(20))))
+    pts = np.array(sorted(pts), np.int32)
+    tr = rng.normal(size=(8, len(pts))).astype(np.float32)
+    hs = handles(cfg, dt, wxy, wz, nranks)
+    load(hs, model, st, 0, cfg)
+    for h in hs:
+        h.set_injection(pts, tr, fields=3)
+        h.set_receivers(pts, fields=3, capacity_steps=8)
+    group_step(hs, 8)
+    assert all(h.info()["launches_per_step"] == 1 for h in hs)
+    got = gather(hs)
+    traces = np.zeros((8, len(pts), 2), np.float32)
+    for h in hs:
+        ids, t = h.get_traces()
+        traces[:, ids] = t
+    close(hs)
+    o = oracle.run_ex(oracle.params(cfg, dt), wxy, wz, *model, st, nsteps=8, inj=(pts, 3, 0, tr), rec=(pts, 3))
+    for f in range(4):
+        assert np.array_equal(got[f], o[f]), f"field {f}"
+    assert np.array_equal(traces, o[4])
