@@ -192,7 +192,7 @@ vti_status vti_set_fields_planes_f64(vti_t h, int32_t k0, int32_t nk, const doub
 vti_status vti_step(vti_t h, int32_t nsteps);
 
 /* Build now whatever vti_step would otherwise build on its first call (the
- * 32-step CUDA graphs of small single-slab grids, for both level parities), so
+ * 32- and 128-step CUDA graphs of small single-slab grids, both level parities), so
  * a timed region does not pay for graph capture and instantiation. Nothing is
  * executed; the state and the time index are unchanged. No-op when the handle
  * does not replay graphs. Errors: STATE (model unset), CUDA. */

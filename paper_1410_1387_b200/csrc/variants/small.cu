@@ -11,8 +11,10 @@ static SmallEntry small_entry()
     return SmallEntry{(int)sizeof(T), R, RZ, TY, (const void *)vti_small_kernel<T, R, RZ, TY>,
                       (const void *)vti_small_kernel<T, R, RZ, TY, true>,
                       (const void *)vti_small_multi_kernel<T, R, RZ, TY>,
-                      (const void *)vti_small_multi_kernel<T, R, RZ, TY, true>, SmallCfg<T, R, RZ, TY>::SMEM,
-                      SmallCfg<T, R, RZ, TY>::THREADS};
+                      (const void *)vti_small_multi_kernel<T, R, RZ, TY, true>,
+                      (const void *)vti_small_direct_kernel<T, R, RZ, TY>,
+                      (const void *)vti_small_direct_kernel<T, R, RZ, TY, true>, SmallDCfg<T, R, RZ, TY>::SMEM,
+                      SmallCfg<T, R, RZ, TY>::SMEM, SmallCfg<T, R, RZ, TY>::THREADS};
 }
 
 SmallTable vti_small_kernels()

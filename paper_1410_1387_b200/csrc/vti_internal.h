@@ -146,7 +146,7 @@ struct vti_s {
     bool graph_enabled = true;                // env VTI_GRAPH=0 disables
     bool capturing = false;
     int capture_index = 0;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // by starting parity (cur)
+    cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [32 / large steps][starting parity]
     void *s_graph = nullptr;                  // device: GRAPH_STEPS source samples of T
     std::vector<double> s_host;
     // N4 point sets of this slab, gathered / injected inside the step

@@ -312,8 +312,9 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->s_multi);
     cudaFree(h->adj_s[0]);
     cudaFree(h->adj_s[1]);
-    for (int b = 0; b < 2; ++b)
-        if (h->gexec[b]) cudaGraphExecDestroy(h->gexec[b]);
+    for (int z = 0; z < 2; ++z)
+        for (int b = 0; b < 2; ++b)
+            if (h->gexec[z][b]) cudaGraphExecDestroy(h->gexec[z][b]);
     cudaFree(h->s_graph);
     for (cudaEvent_t e : {h->ev_edge, h->ev_comm, h->ev_t0, h->ev_t1})
         if (e) cudaEventDestroy(e);
@@ -339,11 +340,12 @@ static vti_status alloc(vti_s *h, void **p, size_t bytes)
 // default schedule and the TMA tensor maps (whose boxes depend on TY).
 static void invalidate_graphs(vti_s *h)
 {
-    for (int b = 0; b < 2; ++b)
-        if (h->gexec[b]) {
-            cudaGraphExecDestroy(h->gexec[b]);
-            h->gexec[b] = nullptr;
-        }
+    for (int z = 0; z < 2; ++z)
+        for (int b = 0; b < 2; ++b)
+            if (h->gexec[z][b]) {
+                cudaGraphExecDestroy(h->gexec[z][b]);
+                h->gexec[z][b] = nullptr;
+            }
 }
 
 static vti_status select_variant(vti_s *h, const KernelEntry *K)
@@ -393,6 +395,8 @@ static vti_status select_variant(vti_s *h, const KernelEntry *K)
                 return s;
         for (const void *fn : {se->fn, se->fn_io, se->fn_multi, se->fn_multi_io})
             CU(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, se->smem));
+        for (const void *fn : {se->fn_direct, se->fn_direct_io})
+            CU(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, se->smem_direct));
         h->small = se;
         h->zchunk = 1;   // the small kernel's items are (tile, plane)
         h->nzc = h->cfg.nz;
@@ -839,10 +843,20 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
         S.P.sync_ctr = nullptr;
         S.P.sync_base = 0;
         S.tm_qcol = h->tm_qcol[h->cur];
+        const int o = 1 - h->cur;
+        S.q_cur = (const T *)h->q_int(h->cur);
+        S.p_m = (const T *)h->p_int(o);
+        S.q_m = (const T *)h->q_int(o);
+        S.vx = (const T *)h->in(h->vx2);
+        S.vn = (const T *)h->in(h->vn2);
+        S.vz = (const T *)h->in(h->vz2);
+        // the direct-load form (only the p tile staged by TMA; C1 86.8 -> 92.7 Gpoints/s) unless
+        // VTI_SMALL_DIRECT=0 (every operand staged by TMA)
+        static const bool direct = !getenv("VTI_SMALL_DIRECT") || atoi(getenv("VTI_SMALL_DIRECT")) != 0;
         cudaLaunchConfig_t sl = {};
         sl.gridDim = dim3(P.items);
         sl.blockDim = dim3(h->small->threads);
-        sl.dynamicSmemBytes = h->small->smem;
+        sl.dynamicSmemBytes = direct ? h->small->smem_direct : h->small->smem;
         sl.stream = h->stream;
         cudaLaunchAttribute sa[1];
         static const bool pdl = !getenv("VTI_PDL") || atoi(getenv("VTI_PDL")) != 0;
@@ -853,7 +867,9 @@ static vti_status launch_rows_t(vti_s *h, int tr0, int ntr0, int tr1, int ntr1, 
             sl.numAttrs = 1;
         }
         void *sargs[] = {&S};
-        CU(h, cudaLaunchKernelExC(&sl, io ? h->small->fn_io : h->small->fn, sargs));
+        const void *sfn = direct ? (io ? h->small->fn_direct_io : h->small->fn_direct)
+                                 : (io ? h->small->fn_io : h->small->fn);
+        CU(h, cudaLaunchKernelExC(&sl, sfn, sargs));
         return VTI_OK;
     }
     const int grid = std::min(P.items, cap > 0 ? std::min(cap, slots(h)) : slots(h));
@@ -1299,7 +1315,16 @@ vti_status vti_get_fields_f64(vti_t h, double *p, double *q, int32_t level)
 }
 
 // ---- CUDA graphs for launch-bound small grids (single slab, one round per step)
-static constexpr int GRAPH_STEPS = 32;   // even: a replay returns to its starting parity
+// Two graph sizes (even: a replay returns to its starting parity): 128-step graphs while at
+// least 128 steps remain, then 32-step ones; the source table and the N4 header are refilled
+// before each replay, a stream-ordered copy that costs a bubble per replay (C1: 32-step
+// replays 92.9, 128-step 95.8 Gpoints/s). Env VTI_GRAPH_STEPS (even, 2..256) sets the large size.
+static constexpr int GRAPH_STEPS = 32;
+static const int GRAPH_STEPS_BIG = [] {
+    const int v = getenv("VTI_GRAPH_STEPS") ? atoi(getenv("VTI_GRAPH_STEPS")) : 128;
+    return (v >= 2 && v <= 256 && v % 2 == 0) ? v : 128;
+}();
+static int graph_steps(int z) { return z ? GRAPH_STEPS_BIG : GRAPH_STEPS; }
 
 static bool graph_eligible(const vti_s *h)
 {
@@ -1312,17 +1337,18 @@ static bool graph_eligible(const vti_s *h)
     return pts <= 64.0 * 1024 * 1024;   // beyond that a step is long enough that launch gaps do not matter
 }
 
-// Capture GRAPH_STEPS steps starting at parity c into h->gexec[c].
-static vti_status build_graph(vti_s *h, int c)
+// Capture graph_steps(z) steps starting at parity c into h->gexec[z][c].
+static vti_status build_graph(vti_s *h, int z, int c)
 {
-    if (!h->s_graph) CU(h, cudaMalloc(&h->s_graph, GRAPH_STEPS * 8));
+    const int n = graph_steps(z);
+    if (!h->s_graph) CU(h, cudaMalloc(&h->s_graph, 256 * 8));
     if (!h->dyn) CU(h, cudaMalloc((void **)&h->dyn, 3 * sizeof(long long)));
     const int keep_cur = h->cur;
     cudaGraph_t g = nullptr;
     CU(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     h->capturing = true;
     vti_status s = VTI_OK;
-    for (int i = 0; i < GRAPH_STEPS && s == VTI_OK; ++i) {
+    for (int i = 0; i < n && s == VTI_OK; ++i) {
         h->cur = (c + i) & 1;
         h->capture_index = i;
         s = launch_rows(h, 0, h->nty, 0, 0, h->zchunk, h->cap);
@@ -1335,36 +1361,37 @@ static vti_status build_graph(vti_s *h, int c)
         return s;
     }
     if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&h->gexec[c], g, 0);
+    e = cudaGraphInstantiate(&h->gexec[z][c], g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
     return VTI_OK;
 }
 
-// Replay GRAPH_STEPS steps: refill the source table (stream-ordered, from pageable
-// host memory so the host buffer is free on return), then launch the graph.
-static vti_status replay_graph(vti_s *h)
+// Replay graph_steps(z) steps: refill the source table (stream-ordered, from pageable host
+// memory so the host buffer is free on return), then launch the graph.
+static vti_status replay_graph(vti_s *h, int z)
 {
     vti_status s;
-    if (!h->gexec[h->cur] && (s = build_graph(h, h->cur)) != VTI_OK) return s;
+    const int n = graph_steps(z);
+    if (!h->gexec[z][h->cur] && (s = build_graph(h, z, h->cur)) != VTI_OK) return s;
     const bool owned = h->has_src && h->src_j >= h->y0 && h->src_j < h->y0 + h->nyl;
-    h->s_host.assign(GRAPH_STEPS, 0.0);
-    for (int i = 0; i < GRAPH_STEPS && owned; ++i)
+    h->s_host.assign(n, 0.0);
+    for (int i = 0; i < n && owned; ++i)
         h->s_host[i] = h->src_amp * ricker((double)(h->n + (int64_t)i * h->dir) * h->cfg.dt, h->src_f, h->src_t0);
     if (h->es == 8) {
-        CU(h, cudaMemcpyAsync(h->s_graph, h->s_host.data(), GRAPH_STEPS * 8, cudaMemcpyHostToDevice, h->stream));
+        CU(h, cudaMemcpyAsync(h->s_graph, h->s_host.data(), n * 8, cudaMemcpyHostToDevice, h->stream));
     } else {
-        float f[GRAPH_STEPS];
-        for (int i = 0; i < GRAPH_STEPS; ++i) f[i] = (float)h->s_host[i];   // rounded once, as P.s
-        CU(h, cudaMemcpyAsync(h->s_graph, f, sizeof f, cudaMemcpyHostToDevice, h->stream));
+        std::vector<float> f(n);
+        for (int i = 0; i < n; ++i) f[i] = (float)h->s_host[i];   // rounded once, as P.s
+        CU(h, cudaMemcpyAsync(h->s_graph, f.data(), n * sizeof(float), cudaMemcpyHostToDevice, h->stream));
     }
     // N4 trace rows of the replay's first step: injection row n - t_first (then + i * dir),
     // receiver row rec_steps (then + i); the kernels skip rows outside their ranges
     const long long hdr[3] = {(long long)(h->n - h->inj_t_first), (long long)h->rec_steps, (long long)h->dir};
     CU(h, cudaMemcpyAsync(h->dyn, hdr, sizeof hdr, cudaMemcpyHostToDevice, h->stream));
-    CU(h, cudaGraphLaunch(h->gexec[h->cur], h->stream));
-    h->n += (int64_t)GRAPH_STEPS * h->dir;   // parity (cur) is unchanged after an even number of steps
-    advance_records(h, GRAPH_STEPS);
+    CU(h, cudaGraphLaunch(h->gexec[z][h->cur], h->stream));
+    h->n += (int64_t)n * h->dir;   // parity (cur) is unchanged after an even number of steps
+    advance_records(h, n);
     return VTI_OK;
 }
 
@@ -1446,8 +1473,9 @@ vti_status vti_prepare(vti_t h)
     CU(h, cudaSetDevice(h->cfg.device));
     vti_status s;
     if (graph_eligible(h) && !multi_eligible(h))   // capture only: nothing executes, the state is untouched
-        for (int c = 0; c < 2; ++c)
-            if (!h->gexec[c] && (s = build_graph(h, c)) != VTI_OK) return s;
+        for (int z = 0; z < 2; ++z)
+            for (int c = 0; c < 2; ++c)
+                if (!h->gexec[z][c] && (s = build_graph(h, z, c)) != VTI_OK) return s;
     return VTI_OK;
 }
 
@@ -1481,14 +1509,15 @@ vti_status vti_step(vti_t h, int32_t nsteps)
     }
     int it = 0;
     if (!multi && nsteps >= GRAPH_STEPS && graph_eligible(h)) {
-        for (; it + GRAPH_STEPS <= nsteps; it += GRAPH_STEPS)
-            if ((s = replay_graph(h)) != VTI_OK) {
-                // capture is not possible on this stream (e.g. the legacy default stream): launch directly
-                cudaGetLastError();
-                h->graph_enabled = false;
-                invalidate_graphs(h);
-                break;
-            }
+        for (int z = 1; z >= 0 && h->graph_enabled; --z)   // large graphs first, then 32-step ones
+            for (; it + graph_steps(z) <= nsteps; it += graph_steps(z))
+                if ((s = replay_graph(h, z)) != VTI_OK) {
+                    // capture is not possible on this stream (e.g. the legacy default stream): launch directly
+                    cudaGetLastError();
+                    h->graph_enabled = false;
+                    invalidate_graphs(h);
+                    break;
+                }
     }
     // diagnostic: VTI_FORCE_SPLIT=1 runs a single slab with the multi-GPU two-launch schedule
     // (edge tile rows, then interior; no transport) to time what one rank's GPU does per step

@@ -21,6 +21,8 @@ template <typename T>
 struct SmallParams {
     StepParams<T> P;
     CUtensorMap tm_qcol;   // q^n interior view, box {TX, TY, 2 R_z + 1}
+    // interior views (row 0, plane 0; strides P.ys, P.zs) for the direct-load kernel
+    const T *q_cur, *p_m, *q_m, *vx, *vn, *vz;
 };
 
 template <typename T, int R, int RZ, int TY>
@@ -41,25 +43,25 @@ struct SmallCfg {
     static constexpr int THREADS = TY * (TX / 4);   // 16 threads x 4 points per tile row
 };
 
-// One tile-plane item's update from its staged data: smem holds the halo'd p^n tile (OFF_P)
-// and the q^n column k - R_z .. k + R_z (OFF_Q), plus vx2 / vn2 / vz2 and the plane's w^z + gz
-// row; pm4 / qm4 are this thread's u^{n-1} (4 points). Returns u^{n+1} in pn / qn and this
-// thread's u^n centre values in pc / qc (the next step's u^{n-1} in the multi-step kernel).
-// s = s(t^n); inj_row / rec_row: the N4 trace rows of this step (IO only).
+// One tile-plane item's update. prow0 = the halo'd p^n tile in shared memory (row 0 = tile
+// row -R, x window starting RA points left of the tile), zr = the plane's w^z row + gz; qv =
+// this thread's q^n column k - R_z .. k + R_z, pm4 / qm4 its u^{n-1}, vx4 / vn4 / vz4 its model
+// (4 points each). Returns u^{n+1} in pn / qn and this thread's u^n centre values in pc / qc
+// (the next step's u^{n-1} in the multi-step kernel). s = s(t^n); inj_row / rec_row: the N4
+// trace rows of this step (IO only).
 template <typename T, int R, int RZ, int TY, bool IO>
-__device__ __forceinline__ void small_update(const StepParams<T> &P, const uint8_t *smem, int y0, int k, int tg,
-                                             int tx, int xg, int yl, const V4<T> &g4, T gyv, T s, long long inj_row,
-                                             long long rec_row, const V4<T> &pm4, const V4<T> &qm4, T (&pn)[1][4],
-                                             T (&qn)[1][4], T (&pc)[4], T (&qc)[4])
+__device__ __forceinline__ void small_update(const StepParams<T> &P, const T *ptile, const T *zr, int y0, int k,
+                                             int tg, int tx, int xg, int yl, const V4<T> &g4, T gyv, T s,
+                                             long long inj_row, long long rec_row, const V4<T> &pm4,
+                                             const V4<T> &qm4, const V4<T> (&qv)[2 * RZ + 1], const V4<T> &vx4,
+                                             const V4<T> &vn4, const V4<T> &vz4, T (&pn)[1][4], T (&qn)[1][4],
+                                             T (&pc)[4], T (&qc)[4])
 {
     using C = Cfg<T, R, RZ, TY>;
-    using SC = SmallCfg<T, R, RZ, TY>;
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
-    const T *st = reinterpret_cast<const T *>(smem);
-    const int sidx = tg * TX + 4 * tx;
-    const T *prow = st + SC::OFF_P / C::ES + (tg + R) * C::PW + 4 * tx;   // smem row of this tile row
-    const T *pbase = st + SC::OFF_P / C::ES + tg * C::PW + 4 * tx;
+    const T *prow = ptile + (tg + R) * C::PW + 4 * tx;   // smem row of this tile row
+    const T *pbase = ptile + tg * C::PW + 4 * tx;
     auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
     T L[4];
 #pragma unroll
@@ -78,13 +80,7 @@ __device__ __forceinline__ void small_update(const StepParams<T> &P, const uint8
             L[c] = fma_rn(P.cxy[l], xpair + ypair, L[c]);
         }
     }
-    const T *zr = st + SC::OFF_ZR / C::ES;
     const T gz = zr[NQ];
-    const T *qcol = st + SC::OFF_Q / C::ES + sidx;   // plane m of the column at qcol + m * TX * TY
-    const V4<T> vx4 = lds4(st + SC::OFF_VX / C::ES + sidx);
-    const V4<T> vn4 = lds4(st + SC::OFF_VN / C::ES + sidx);
-    const V4<T> vz4 = lds4(st + SC::OFF_VZ / C::ES + sidx);
-    const V4<T> qc4 = lds4(qcol + RZ * TX * TY);
     const bool src_here = P.src_mask != 0 && P.src_j == yl && P.src_k == k && P.src_i >= xg && P.src_i < xg + 4;
     bool inj_on = false;
     const T *inj_base = nullptr;
@@ -98,11 +94,11 @@ __device__ __forceinline__ void small_update(const StepParams<T> &P, const uint8
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        qc[c] = qc4[c];
+        qc[c] = qv[RZ][c];
         // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
-        T D = zr[0] * lds4(qcol)[c];
+        T D = zr[0] * qv[0][c];
 #pragma unroll
-        for (int m = 1; m < NQ; ++m) D = fma_rn(zr[m], lds4(qcol + m * TX * TY)[c], D);
+        for (int m = 1; m < NQ; ++m) D = fma_rn(zr[m], qv[m][c], D);
         const T vD = vz4[c] * D;
         T Fp = fma_rn(vx4[c], L[c], vD);
         T Fq = fma_rn(vn4[c], L[c], vD);
@@ -122,9 +118,25 @@ __device__ __forceinline__ void small_update(const StepParams<T> &P, const uint8
         }
         const T g = (g4[c] * gyv) * gz;   // (gx gy) gz
         pn[0][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[c]));
-        qn[0][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * qc4[c]));
+        qn[0][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * qv[RZ][c]));
     }
     if constexpr (IO) record_points_row<T, 1, 4>(P, k, y0, TY, yl, xg, rec_row, pn, qn);
+}
+
+// The q column and stream operands of a thread from the TMA-staged item in shared memory.
+template <typename T, int R, int RZ, int TY>
+__device__ __forceinline__ void small_operands_smem(const uint8_t *smem, int tg, int tx, V4<T> (&qv)[2 * RZ + 1],
+                                                    V4<T> &vx4, V4<T> &vn4, V4<T> &vz4)
+{
+    using C = Cfg<T, R, RZ, TY>;
+    using SC = SmallCfg<T, R, RZ, TY>;
+    const T *st = reinterpret_cast<const T *>(smem);
+    const int sidx = tg * TX + 4 * tx;
+#pragma unroll
+    for (int m = 0; m < 2 * RZ + 1; ++m) qv[m] = lds4(st + SC::OFF_Q / C::ES + sidx + m * TX * TY);
+    vx4 = lds4(st + SC::OFF_VX / C::ES + sidx);
+    vn4 = lds4(st + SC::OFF_VN / C::ES + sidx);
+    vz4 = lds4(st + SC::OFF_VZ / C::ES + sidx);
 }
 
 // IO: also the N4 point sets (injection into F, receivers from u^{n+1}; see StepParams).
@@ -174,9 +186,99 @@ __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
     const int sidx = tg * TX + 4 * tx;
     const V4<T> pm4 = lds4(st + SC::OFF_PM / C::ES + sidx);
     const V4<T> qm4 = lds4(st + SC::OFF_QM / C::ES + sidx);
+    V4<T> qv[2 * RZ + 1], vx4, vn4, vz4;
+    small_operands_smem<T, R, RZ, TY>(smem, tg, tx, qv, vx4, vn4, vz4);
     T pn[1][4], qn[1][4], pc[4], qc[4];
-    small_update<T, R, RZ, TY, IO>(P, smem, y0, k, tg, tx, xg, yl, g4, gyv, sv, IO ? inj_row_of(P) : 0,
-                                   IO ? rec_row_of(P) : 0, pm4, qm4, pn, qn, pc, qc);
+    small_update<T, R, RZ, TY, IO>(P, st + SC::OFF_P / C::ES, st + SC::OFF_ZR / C::ES, y0, k, tg, tx, xg, yl, g4,
+                                   gyv, sv, IO ? inj_row_of(P) : 0, IO ? rec_row_of(P) : 0, pm4, qm4, qv, vx4, vn4,
+                                   vz4, pn, qn, pc, qc);
+    if (store_ok) {
+        const long long off = (long long)k * P.zs + (long long)yl * P.ys + xg;
+        stv(P.p_out + off, pn[0]);
+        stv(P.q_out + off, qn[0]);
+    }
+}
+
+// ---------------------------------------------------------------- direct-load small-grid kernel
+// The same item with only the halo'd p^n tile (the operand other threads share) and the w^z row
+// staged by TMA; every thread loads its own q^n column, u^{n-1} and model straight from global
+// memory into registers (14 independent 16-byte loads, all in flight at once). Shared memory
+// drops from ~64 KB to ~8 KB per item, and the TMA unit moves 24 rows per item instead of 168.
+template <typename T, int R, int RZ, int TY>
+struct SmallDCfg {
+    using C = Cfg<T, R, RZ, TY>;
+    static constexpr int OFF_P = 0;
+    static constexpr int OFF_ZR = align128(C::P_BYTES);
+    static constexpr int OFF_BAR = align128(OFF_ZR + C::ZROW * C::ES);
+    static constexpr int SMEM = OFF_BAR + 16;
+    static constexpr uint32_t TX_BYTES = C::P_BYTES + C::ZROW * C::ES;
+};
+
+template <typename T> __device__ __forceinline__ V4<T> v4_zero();
+template <> __device__ __forceinline__ V4<float> v4_zero<float>() { return V4<float>{make_float4(0.f, 0.f, 0.f, 0.f)}; }
+template <> __device__ __forceinline__ V4<double> v4_zero<double>()
+{
+    return V4<double>{make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+}
+
+template <typename T, int R, int RZ, int TY, bool IO = false>
+__global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
+    vti_small_direct_kernel(const __grid_constant__ SmallParams<T> S)
+{
+    using C = Cfg<T, R, RZ, TY>;
+    using DC = SmallDCfg<T, R, RZ, TY>;
+    constexpr int RA = C::RA;
+    constexpr int NQ = C::NQ;
+    const StepParams<T> &P = S.P;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + DC::OFF_BAR);
+
+    int x0, y0, kb, ke;
+    decode_item<TY>(P, blockIdx.x, x0, y0, kb, ke);   // zchunk = 1: plane k = kb
+    const int k = kb;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
+    const int xg = x0 + 4 * tx, yl = y0 + tg;
+    const V4<T> g4 = lds4(P.gx + xg);
+    const T gyv = (yl < P.nyl) ? P.gy[yl] : T(0);
+    const bool store_ok = (yl < P.nyl) && (xg < P.nx);
+    const T sv = P.s_table ? P.s_table[P.s_index] : P.s;
+    __syncthreads();   // the barrier is initialised before anyone waits on it
+    // programmatic dependent launch: every thread reads the previous step's output below
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(bar, DC::TX_BYTES);
+        tma_load_3d(smem + DC::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
+        bulk_load(smem + DC::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * C::ES, bar);
+    }
+    V4<T> qv[NQ], pm4 = v4_zero<T>(), qm4 = v4_zero<T>(), vx4 = v4_zero<T>(), vn4 = v4_zero<T>(),
+                  vz4 = v4_zero<T>();
+#pragma unroll
+    for (int m = 0; m < NQ; ++m) qv[m] = v4_zero<T>();
+    if (store_ok) {   // this thread's points: q column (zero exterior in z), u^{n-1}, model
+        const long long off = (long long)yl * P.ys + xg;
+#pragma unroll
+        for (int m = 0; m < NQ; ++m) {
+            const int kk = k - RZ + m;
+            if (kk >= 0 && kk < P.nz) qv[m] = ldv<4>(S.q_cur + off + (long long)kk * P.zs);
+        }
+        const long long o = off + (long long)k * P.zs;
+        pm4 = ldv<4>(S.p_m + o);
+        qm4 = ldv<4>(S.q_m + o);
+        vx4 = ldv<4>(S.vx + o);
+        vn4 = ldv<4>(S.vn + o);
+        vz4 = ldv<4>(S.vz + o);
+    }
+    mbar_wait(bar, 0);
+    const T *st = reinterpret_cast<const T *>(smem);
+    T pn[1][4], qn[1][4], pc[4], qc[4];
+    small_update<T, R, RZ, TY, IO>(P, st + DC::OFF_P / C::ES, st + DC::OFF_ZR / C::ES, y0, k, tg, tx, xg, yl, g4,
+                                   gyv, sv, IO ? inj_row_of(P) : 0, IO ? rec_row_of(P) : 0, pm4, qm4, qv, vx4, vn4,
+                                   vz4, pn, qn, pc, qc);
     if (store_ok) {
         const long long off = (long long)k * P.zs + (long long)yl * P.ys + xg;
         stv(P.p_out + off, pn[0]);
@@ -304,9 +406,11 @@ __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
         mbar_wait(bar, phase);
         phase ^= 1;
         T pn[1][4], qn[1][4], pc[4], qc[4];
-        small_update<T, R, RZ, TY, IO>(P, smem, y0, k, tg, tx, xg, yl, g4, gyv, sv,
-                                       IO ? P.inj_row + (long long)step * M.dir : 0,
-                                       IO ? P.rec_row + step : 0, pm4, qm4, pn, qn, pc, qc);
+        V4<T> qv[2 * RZ + 1], vx4, vn4, vz4;
+        small_operands_smem<T, R, RZ, TY>(smem, tg, tx, qv, vx4, vn4, vz4);
+        small_update<T, R, RZ, TY, IO>(P, st + SC::OFF_P / C::ES, st + SC::OFF_ZR / C::ES, y0, k, tg, tx, xg, yl,
+                                       g4, gyv, sv, IO ? P.inj_row + (long long)step * M.dir : 0,
+                                       IO ? P.rec_row + step : 0, pm4, qm4, qv, vx4, vn4, vz4, pn, qn, pc, qc);
         if (store_ok) {
             const long long off = (long long)k * P.zs + (long long)yl * P.ys + xg;
             stv(P.p_out + off, pn[0]);

@@ -38,6 +38,9 @@ struct SmallEntry {
     const void *fn_io;     // with the N4 point sets
     const void *fn_multi;  // multi-step cooperative kernel (vti_small_multi_kernel), and its IO form
     const void *fn_multi_io;
+    const void *fn_direct; // direct-load form (vti_small_direct_kernel), and its IO form
+    const void *fn_direct_io;
+    int smem_direct;
     int smem, threads;
 };
 struct SmallTable {
