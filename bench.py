@@ -83,12 +83,15 @@ def workload(args, world):
 
 
 def describe(cfg, world, scaling, bpp=BYTES_PER_POINT, transport="none"):
+    import synth
     npts = cfg["nx"] * cfg["ny"] * cfg["nz"]
     return {
         "workload": f"{cfg['name']}: {cfg['nx']}x{cfg['ny']}x{cfg['nz']} global, R_xy={cfg['r_xy']} R_z={cfg['r_z']}, "
                     f"{cfg['model']['kind']} VTI, W={cfg['damp_width']}, Ricker f={cfg['f']:g} Hz at the centre",
         "grid": [cfg["nx"], cfg["ny"], cfg["nz"]],
         "r_xy": cfg["r_xy"], "r_z": cfg["r_z"], "config_steps": cfg["steps"],
+        "dt": synth.stable_dt(cfg), "h": cfg["h"], "dz": list(cfg["dz"]), "src": list(cfg["src"]),
+        "damping": {"width": cfg["damp_width"], "alpha": cfg["damp_alpha"]},
         "decomposition": f"y-slabs x{world}" if world > 1 else "single GPU",
         "halo_transport": transport,
         "scaling": scaling,
