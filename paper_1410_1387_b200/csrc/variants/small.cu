@@ -21,6 +21,9 @@ SmallTable vti_small_kernels()
 {
     // fp32 only: an fp64 item (128 KB of shared memory, 1 CTA per SM) measured slower than the
     // persistent fp64 kernel on C1 (32.5 vs 39.4 Gpoints/s)
+    // fp32 only: fp64 items (the direct form at 184-246 registers, one CTA per SM) measured
+    // slower than the persistent fp64 kernel on C1 fp64 in round 2 too: 37.6 (direct) and 35.6
+    // (TMA-staged) vs 40.5 Gpoints/s
     static const SmallEntry t[] = {small_entry<float, 4, 4, 16>(), small_entry<float, 8, 4, 16>(),
                                    small_entry<float, 6, 6, 16>()};
     // 32-row small-grid tiles (128 items on C1, one CTA per SM) measured slower in round 2:
