@@ -14,9 +14,10 @@
 // m = 0..2Rz, k' = k+Rz-m inside the grid; F_p = L (+ inj), F_q = DT (+ inj);
 // psi^{m-1} = g*fma(dt2, F, fma(-g, psi^{m+1}, 2 psi^m)).
 //
-// Off the benchmark path, so the kernels are plain: one thread per point, x fastest (coalesced),
-// neighbours through L1/L2. Single-slab handles only (the s1 cross would need the neighbours'
-// psi and model rows).
+// k_adj_prep is elementwise; k_adj_step marches z per (tile, z-chunk) with the s1 tile staged in
+// shared memory and s2 in a register queue (the forward kernel's structure, plain loads instead
+// of its TMA ring). Single-slab handles only (the s1 cross would need the neighbours' psi and
+// model rows).
 #include "vti_internal.h"
 
 namespace {
@@ -84,56 +85,125 @@ __device__ __forceinline__ int ps_lookup(const int *off, const int2 *ent, int ny
     return (lo < off[b + 1] && ent[lo].x == x) ? lo : -1;
 }
 
+// The stencils and update, marching z: one CTA per (64 x 8 tile, z-chunk), 16 x 8 threads
+// of 4 x points each (the forward kernel's mapping). Per plane the s1 tile with its R_xy apron
+// is staged in shared memory (zero outside the slab), s2 marches in a (2R_z+1)-deep register
+// queue, and D^T takes the transposed weight diagonal w^z[k+Rz-m][m] from the plane table.
+constexpr int ADJ_TY = 8;
+constexpr int ADJ_ZCHUNK = 64;
+
 template <typename T, int R, int RZ>
-__global__ void k_adj_step(const AdjParams<T> A)
+__global__ void __launch_bounds__(16 * ADJ_TY) k_adj_step(const AdjParams<T> A, int ntx, int nty)
 {
-    const int64_t n = (int64_t)A.nz * A.nyl * A.nx;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int i = (int)(t % A.nx);
-        const int64_t r = t / A.nx;
-        const int j = (int)(r % A.nyl);
-        const int k = (int)(r / A.nyl);
-        const int64_t a = j * A.ys + k * A.zs + i;
-        // L(s1), canonical pairing (x pair + y pair); zero exterior
-        T L = A.cxy[0] * A.s1[a];
+    constexpr int NQ = 2 * RZ + 1;
+    constexpr int RA = (R + 3) / 4 * 4;   // apron rounded to whole 4-vectors
+    constexpr int PW = 64 + 2 * RA, PH = ADJ_TY + 2 * R;
+    __shared__ __align__(16) T tile[2][PH * PW];
+    const int b = blockIdx.x;
+    const int itx = b % ntx, ity = (b / ntx) % nty, izc = b / (ntx * nty);
+    const int x0 = itx * 64, y0 = ity * ADJ_TY;
+    const int kb = izc * ADJ_ZCHUNK, ke = min(A.nz, kb + ADJ_ZCHUNK);
+    const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
+    const int xg = x0 + 4 * tx, yl = y0 + tg;
+    const bool own = xg < A.nx && yl < A.nyl;
+    // s2 column queue: slot m holds plane k - RZ + m
+    T q[NQ][4];
+    auto load4 = [&](const T *base, int k, T (&v)[4]) {
 #pragma unroll
-        for (int l = 1; l <= R; ++l) {
-            const T xp = i + l < A.nx ? A.s1[a + l] : T(0);
-            const T xm = i - l >= 0 ? A.s1[a - l] : T(0);
-            const T yp = j + l < A.nyl ? A.s1[a + l * A.ys] : T(0);
-            const T ym = j - l >= 0 ? A.s1[a - l * A.ys] : T(0);
-            L = fma_x<T>(A.cxy[l], (xp + xm) + (yp + ym), L);
-        }
-        // D^T(s2): row k of the transpose = column k of Eq. 5's rows
-        T DT = T(0);
+        for (int c = 0; c < 4; ++c) v[c] = T(0);
+        if (!own || k < 0 || k >= A.nz) return;
+        const T *p = base + (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
 #pragma unroll
-        for (int m = 0; m <= 2 * RZ; ++m) {
-            const int kk = k + RZ - m;
-            if (kk >= 0 && kk < A.nz)
-                DT = fma_x<T>(A.zrow[(int64_t)kk * A.zrow_stride + m], A.s2[j * A.ys + kk * A.zs + i], DT);
+        for (int c = 0; c < 4; ++c) v[c] = (xg + c < A.nx) ? p[c] : T(0);
+    };
+#pragma unroll
+    for (int m = 0; m < NQ - 1; ++m) load4(A.s2, kb - RZ + m, q[m + 1]);
+    const T gy = own ? A.gy[yl] : T(0);
+    // s1 tile of plane k -> buffer (k & 1) with cp.async (out-of-slab elements zero-filled), so
+    // plane k+1 is in flight while plane k is computed
+    auto stage = [&](int k) {
+        T *dst = tile[k & 1];
+        for (int e = threadIdx.x; e < PH * PW; e += 16 * ADJ_TY) {
+            const int r = e / PW, c = e % PW;
+            const int yy = y0 - R + r, xx = x0 - RA + c;
+            const bool in = yy >= 0 && yy < A.nyl && xx >= 0 && xx < A.nx;
+            const T *src = in ? A.s1 + (int64_t)yy * A.ys + (int64_t)k * A.zs + xx : A.s1;
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + e);
+            if constexpr (sizeof(T) == 8)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(in ? 8 : 0) : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(in ? 4 : 0) : "memory");
         }
-        T Fp = L, Fq = DT;
-        if (A.inj_row != nullptr) {
-            const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, j, i);
-            if (e >= 0) {
-                const T v = A.inj_row[A.inj_ent[e].y];
-                if (A.inj_mask & 1) Fp = Fp + v;
-                if (A.inj_mask & 2) Fq = Fq + v;
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (kb < ke) stage(kb);
+    for (int k = kb; k < ke; ++k) {
+#pragma unroll
+        for (int m = 0; m < NQ - 1; ++m)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) q[m][c] = q[m + 1][c];
+        load4(A.s2, k + RZ, q[NQ - 1]);
+        __syncthreads();   // every thread is done with buffer (k+1) & 1 (plane k-1)
+        if (k + 1 < ke) {
+            stage(k + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");   // plane k landed
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();   // plane k visible to every thread
+        if (own) {
+            const T *row = tile[k & 1] + (tg + R) * PW + RA + 4 * tx;   // this thread's first point
+            T L[4], DT[4], Fp[4], Fq[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                // L(s1), canonical pairing (x pair + y pair); zero exterior in the staged tile
+                L[c] = A.cxy[0] * row[c];
+#pragma unroll
+                for (int l = 1; l <= R; ++l)
+                    L[c] = fma_x<T>(A.cxy[l], (row[c + l] + row[c - l]) + (row[c + l * PW] + row[c - l * PW]), L[c]);
+                // D^T(s2): ascending m over planes k' = k + RZ - m inside the grid
+                DT[c] = T(0);
             }
-        }
-        const T g = (A.gx[i] * A.gy[j]) * A.zrow[(int64_t)k * A.zrow_stride + 2 * RZ + 1];
-        const T pn = g * fma_x<T>(A.dt2, Fp, fma_x<T>(-g, A.po[a], T(2) * A.pc[a]));
-        const T qn = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, A.qo[a], T(2) * A.qc[a]));
-        A.po[a] = pn;
-        A.qo[a] = qn;
-        if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
-            const long long b = (long long)k * A.nyl + j;
-            const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
-            for (int e = A.rec_off[b]; e < A.rec_off[b + 1]; ++e) {
-                if (A.rec_ent[e].x != i) continue;
-                T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
-                if (A.rec_mask & 1) *o++ = pn;
-                if (A.rec_mask & 2) *o = qn;
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) {
+                const int kk = k + RZ - m;
+                if (kk < 0 || kk >= A.nz) continue;
+                const T w = A.zrow[(int64_t)kk * A.zrow_stride + m];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) DT[c] = fma_x<T>(w, q[NQ - 1 - m][c], DT[c]);
+            }
+            const T gz = A.zrow[(int64_t)k * A.zrow_stride + NQ];
+            const int64_t a0 = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (xg + c >= A.nx) continue;
+                const int64_t a = a0 + c;
+                const int i = xg + c;
+                Fp[c] = L[c];
+                Fq[c] = DT[c];
+                if (A.inj_row != nullptr) {
+                    const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, yl, i);
+                    if (e >= 0) {
+                        const T v = A.inj_row[A.inj_ent[e].y];
+                        if (A.inj_mask & 1) Fp[c] = Fp[c] + v;
+                        if (A.inj_mask & 2) Fq[c] = Fq[c] + v;
+                    }
+                }
+                const T g = (A.gx[i] * gy) * gz;
+                const T pn = g * fma_x<T>(A.dt2, Fp[c], fma_x<T>(-g, A.po[a], T(2) * A.pc[a]));
+                const T qn = g * fma_x<T>(A.dt2, Fq[c], fma_x<T>(-g, A.qo[a], T(2) * A.qc[a]));
+                A.po[a] = pn;
+                A.qo[a] = qn;
+                if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
+                    const long long rb = (long long)k * A.nyl + yl;
+                    const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
+                    for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
+                        if (A.rec_ent[e].x != i) continue;
+                        T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
+                        if (A.rec_mask & 1) *o++ = pn;
+                        if (A.rec_mask & 2) *o = qn;
+                    }
+                }
             }
         }
     }
@@ -143,11 +213,14 @@ template <typename T>
 static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
 {
     const int R = h->R, RZ = h->RZ;
-#define ADJ_CASE(r, rz)                                                        \
-    if (R == r && RZ == rz) {                                                  \
-        k_adj_step<T, r, rz><<<grid, 256, 0, h->stream>>>(A);                  \
-        CU(h, cudaGetLastError());                                             \
-        return VTI_OK;                                                         \
+    const int ntx = (h->cfg.nx + 63) / 64, nty = (h->nyl + ADJ_TY - 1) / ADJ_TY;
+    const int nzc = (h->cfg.nz + ADJ_ZCHUNK - 1) / ADJ_ZCHUNK;
+    (void)grid;
+#define ADJ_CASE(r, rz)                                                                          \
+    if (R == r && RZ == rz) {                                                                    \
+        k_adj_step<T, r, rz><<<ntx * nty * nzc, 16 * ADJ_TY, 0, h->stream>>>(A, ntx, nty);       \
+        CU(h, cudaGetLastError());                                                               \
+        return VTI_OK;                                                                           \
     }
     ADJ_CASE(4, 4)
     ADJ_CASE(8, 4)
