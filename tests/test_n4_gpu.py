@@ -306,3 +306,27 @@ def test_async_snapshots_every_step():
         st = oracle.run(P, wxy, wz, *model, st, n0=n, nsteps=1)[:4]
         assert np.array_equal(got_p[n], st[0]) and np.array_equal(got_q[n], st[1])
     assert np.abs(got_p[-1]).max() > 0
+
+
+@pytest.mark.parametrize("grid", [(60, 50, 40), (96, 96, 72)])
+def test_dense_surface_injection_and_receivers(grid):
+    """A whole plane of injection points and a whole plane of receivers (the RTM surface
+    acquisition): dense CSR rows on the small-grid and the persistent kernels, bitwise."""
+    cfg, wxy, wz, dt, model = setup(*grid, damp=6, src=(grid[0] // 2, grid[1] // 2, grid[2] // 2))
+    nx, ny, nz = grid
+    jj, ii = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    surface = lambda k: np.stack([ii.ravel(), jj.ravel(), np.full(ii.size, k)], 1).astype(np.int32)
+    inj, rec = surface(3), surface(nz - 9)
+    nsteps = 40
+    tr = (np.random.default_rng(8).normal(size=(nsteps, len(inj))) * 2.0).astype(np.float32)
+    with handle(cfg, dt, wxy, wz) as v:
+        v.set_model(*model)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        v.set_injection(inj, tr, fields=1)
+        v.set_receivers(rec, fields=3, capacity_steps=nsteps)
+        v.step(nsteps)
+        g = v.get_fields(0)
+        _, traces = v.get_traces()
+    o = oracle.run_ex(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=nsteps, inj=(inj, 1, 0, tr), rec=(rec, 3))
+    assert np.array_equal(g[0], o[0]) and np.array_equal(g[1], o[1])
+    assert np.array_equal(traces, o[4]) and np.abs(traces).max() > 0
