@@ -50,7 +50,8 @@ __global__ void k_adj_prep(const T *__restrict__ pp, const T *__restrict__ pq, c
 
 template <typename T>
 struct AdjParams {
-    const T *s1, *s2;              // interior views (row 0, plane 0)
+    const T *s1, *s2;              // interior views (row 0, plane 0) (two-pass form)
+    const T *vx, *vn, *vz;         // model interior views (one-pass form)
     const T *pc, *qc;              // psi^m
     T *po, *qo;                    // psi^{m+1} in, psi^{m-1} out (in place)
     const T *zrow;                 // [nz][zrow_stride]: w^z[k][0..2Rz], gz[k]
@@ -209,6 +210,170 @@ __global__ void __launch_bounds__(16 * ADJ_TY) k_adj_step(const AdjParams<T> A, 
     }
 }
 
+// One-pass form: the coefficient products are formed inside the stencil kernel, so a step
+// reads psi and the model once (36 B/pt like the forward step instead of 60 over two passes).
+// Per plane, cp.async stages psi_p, psi_q, vx2, vn2 tiles with the R_xy apron (double-buffered,
+// zero-filled outside the slab), the CTA forms the s1 tile in shared memory, and each thread
+// forms s2 = vz2 (psi_p + psi_q) of plane k + R_z for its register queue. Same arithmetic as
+// k_adj_prep + k_adj_step, so the same bits.
+template <typename T, int R, int RZ>
+struct AdjFusedCfg {
+    static constexpr int RA = (R + 3) / 4 * 4;
+    static constexpr int PW = 64 + 2 * RA, PH = ADJ_TY + 2 * R, TE = PH * PW;
+    static constexpr int VEC = 16 / (int)sizeof(T);   // elements per 16-byte cp.async
+    static constexpr int SMEM = 9 * TE * (int)sizeof(T);   // [2][4][TE] inputs + [TE] s1
+};
+
+template <typename T, int R, int RZ>
+__global__ void __launch_bounds__(16 * ADJ_TY) k_adj_fused(const AdjParams<T> A, int ntx, int nty)
+{
+    using F = AdjFusedCfg<T, R, RZ>;
+    constexpr int NQ = 2 * RZ + 1, RA = F::RA, PW = F::PW, PH = F::PH, TE = F::TE, VEC = F::VEC;
+    constexpr int NT = 16 * ADJ_TY;
+    extern __shared__ __align__(16) uint8_t adj_smem[];
+    T *inb = reinterpret_cast<T *>(adj_smem);   // [2][4][TE]: psi_p, psi_q, vx2, vn2
+    T *s1t = inb + 8 * TE;
+    const int b = blockIdx.x;
+    const int itx = b % ntx, ity = (b / ntx) % nty, izc = b / (ntx * nty);
+    const int x0 = itx * 64, y0 = ity * ADJ_TY;
+    const int kb = izc * ADJ_ZCHUNK, ke = min(A.nz, kb + ADJ_ZCHUNK);
+    const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
+    const int xg = x0 + 4 * tx, yl = y0 + tg;
+    const bool own = xg < A.nx && yl < A.nyl;
+    const T *src4[4] = {A.pc, A.qc, A.vx, A.vn};
+    auto stage = [&](int k) {
+        T *dst = inb + (k & 1) * 4 * TE;
+        for (int e = threadIdx.x; e < TE / VEC; e += NT) {
+            const int r = (e * VEC) / PW, c = (e * VEC) % PW;
+            const int yy = y0 - R + r, xx = x0 - RA + c;
+            const bool rowin = yy >= 0 && yy < A.nyl;
+            // valid bytes of this 16-byte chunk (zero fill beyond nx and outside the slab)
+            const int nvalid = (!rowin || xx >= A.nx || xx + VEC <= 0) ? 0 : min(VEC, A.nx - xx);
+            const bool whole_left = xx >= 0;   // chunks never straddle x = 0 (x0 - RA is a multiple of 4)
+            const int bytes = whole_left ? nvalid * (int)sizeof(T) : 0;
+            const int64_t off = rowin && whole_left ? (int64_t)yy * A.ys + (int64_t)k * A.zs + xx : 0;
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + f * TE + e * VEC);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src4[f] + off), "r"(bytes)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // s2 = vz2 (psi_p + psi_q) of plane k at this thread's 4 points (0 outside the grid)
+    auto s2_of = [&](int k, T (&v)[4]) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = T(0);
+        if (!own || k < 0 || k >= A.nz) return;
+        const int64_t a = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (xg + c < A.nx) v[c] = A.vz[a + c] * (A.pc[a + c] + A.qc[a + c]);
+    };
+    T q[NQ][4];
+#pragma unroll
+    for (int m = 0; m < NQ - 1; ++m) s2_of(kb - RZ + m, q[m + 1]);
+    const T gy = own ? A.gy[yl] : T(0);
+    if (kb < ke) stage(kb);
+    for (int k = kb; k < ke; ++k) {
+#pragma unroll
+        for (int m = 0; m < NQ - 1; ++m)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) q[m][c] = q[m + 1][c];
+        s2_of(k + RZ, q[NQ - 1]);
+        __syncthreads();   // every thread is done with s1t and with buffer (k+1) & 1 (plane k-1)
+        if (k + 1 < ke) {
+            stage(k + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");   // plane k landed
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();   // plane k inputs visible to every thread
+        const T *pin = inb + (k & 1) * 4 * TE;
+        for (int e = threadIdx.x; e < TE; e += NT)   // s1 = fma(vx2, psi_p, vn2 * psi_q) with the apron
+            s1t[e] = fma_x<T>(pin[2 * TE + e], pin[e], pin[3 * TE + e] * pin[TE + e]);
+        __syncthreads();
+        if (own) {
+            const int ctr = (tg + R) * PW + RA + 4 * tx;   // this thread's first point in the tile
+            const T *row = s1t + ctr;
+            T L[4], DT[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                L[c] = A.cxy[0] * row[c];
+#pragma unroll
+                for (int l = 1; l <= R; ++l)
+                    L[c] = fma_x<T>(A.cxy[l], (row[c + l] + row[c - l]) + (row[c + l * PW] + row[c - l * PW]), L[c]);
+                DT[c] = T(0);
+            }
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) {
+                const int kk = k + RZ - m;
+                if (kk < 0 || kk >= A.nz) continue;
+                const T w = A.zrow[(int64_t)kk * A.zrow_stride + m];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) DT[c] = fma_x<T>(w, q[NQ - 1 - m][c], DT[c]);
+            }
+            const T gz = A.zrow[(int64_t)k * A.zrow_stride + NQ];
+            const int64_t a0 = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (xg + c >= A.nx) continue;
+                const int64_t a = a0 + c;
+                const int i = xg + c;
+                T Fp = L[c], Fq = DT[c];
+                if (A.inj_row != nullptr) {
+                    const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, yl, i);
+                    if (e >= 0) {
+                        const T v = A.inj_row[A.inj_ent[e].y];
+                        if (A.inj_mask & 1) Fp = Fp + v;
+                        if (A.inj_mask & 2) Fq = Fq + v;
+                    }
+                }
+                const T g = (A.gx[i] * gy) * gz;
+                const T pn = g * fma_x<T>(A.dt2, Fp, fma_x<T>(-g, A.po[a], T(2) * pin[ctr + c]));
+                const T qn = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, A.qo[a], T(2) * pin[TE + ctr + c]));
+                A.po[a] = pn;
+                A.qo[a] = qn;
+                if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
+                    const long long rb = (long long)k * A.nyl + yl;
+                    const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
+                    for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
+                        if (A.rec_ent[e].x != i) continue;
+                        T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
+                        if (A.rec_mask & 1) *o++ = pn;
+                        if (A.rec_mask & 2) *o = qn;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+template <typename T>
+static vti_status launch_adj_fused(vti_s *h, const AdjParams<T> &A)
+{
+    const int ntx = (h->cfg.nx + 63) / 64, nty = (h->nyl + ADJ_TY - 1) / ADJ_TY;
+    const int nzc = (h->cfg.nz + ADJ_ZCHUNK - 1) / ADJ_ZCHUNK;
+    const int R = h->R, RZ = h->RZ;
+#define ADJF_CASE(r, rz)                                                                                   \
+    if (R == r && RZ == rz) {                                                                              \
+        const int smem = AdjFusedCfg<T, r, rz>::SMEM;                                                      \
+        CU(h, cudaFuncSetAttribute((const void *)k_adj_fused<T, r, rz>,                                    \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));                    \
+        k_adj_fused<T, r, rz><<<ntx * nty * nzc, 16 * ADJ_TY, smem, h->stream>>>(A, ntx, nty);            \
+        CU(h, cudaGetLastError());                                                                         \
+        return VTI_OK;                                                                                     \
+    }
+    ADJF_CASE(4, 4)
+    ADJF_CASE(8, 4)
+    ADJF_CASE(6, 6)
+    ADJF_CASE(12, 8)
+#undef ADJF_CASE
+    return fail(h, VTI_E_UNSUPPORTED, "no adjoint kernel for (%d, %d)", R, RZ);
+}
+
 template <typename T>
 static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
 {
@@ -230,19 +395,38 @@ static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
     return fail(h, VTI_E_UNSUPPORTED, "no adjoint kernel for (%d, %d)", R, RZ);
 }
 
+// Which form: measured on B200 (tools/adjoint_rate.py), the one-pass kernel wins at R_xy = 4
+// (C2 68.4 vs 59.3 Gpoints/s) and the two-pass one at larger radii, whose wider aprons make
+// the four staged input tiles costly (C3 53 vs 49, C5 49 vs 46, N1 36.6 vs 25.1).
+// Env VTI_ADJ_TWO_PASS=1/0 forces either.
+static bool adj_two_pass(const vti_s *h)
+{
+    static const int env = getenv("VTI_ADJ_TWO_PASS") ? atoi(getenv("VTI_ADJ_TWO_PASS")) : -1;
+    return env >= 0 ? env != 0 : h->R > 4;
+}
+
 template <typename T>
 static vti_status adjoint_step_t(vti_s *h)
 {
     const int c = h->cur, o = 1 - c;
     const int grid = 4 * h->sms;
-    T *s1 = (T *)h->in(h->adj_s[0]), *s2 = (T *)h->in(h->adj_s[1]);
-    k_adj_prep<T><<<grid, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c), (const T *)h->in(h->vx2),
-                                             (const T *)h->in(h->vn2), (const T *)h->in(h->vz2), s1, s2, h->cfg.nx,
-                                             h->nyl, h->cfg.nz, h->ys, h->zs);
-    CU(h, cudaGetLastError());
+    const bool two_pass = adj_two_pass(h);
+    T *s1 = nullptr, *s2 = nullptr;
+    if (two_pass) {
+        s1 = (T *)h->in(h->adj_s[0]);
+        s2 = (T *)h->in(h->adj_s[1]);
+        k_adj_prep<T><<<grid, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
+                                                 (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
+                                                 (const T *)h->in(h->vz2), s1, s2, h->cfg.nx, h->nyl, h->cfg.nz,
+                                                 h->ys, h->zs);
+        CU(h, cudaGetLastError());
+    }
     AdjParams<T> A;
     A.s1 = s1;
     A.s2 = s2;
+    A.vx = (const T *)h->in(h->vx2);
+    A.vn = (const T *)h->in(h->vn2);
+    A.vz = (const T *)h->in(h->vz2);
     A.pc = (const T *)h->p_int(c);
     A.qc = (const T *)h->q_int(c);
     A.po = (T *)h->p_int(o);
@@ -270,7 +454,7 @@ static vti_status adjoint_step_t(vti_s *h)
     A.rec_ent = h->rec_set.ent;
     A.rec_row = rec ? (T *)h->traces + (size_t)h->rec_steps * h->nrec * nf : nullptr;
     A.rec_mask = h->rec_mask;
-    return launch_adj_step<T>(h, A, grid);
+    return two_pass ? launch_adj_step<T>(h, A, grid) : launch_adj_fused<T>(h, A);
 }
 
 }  // namespace
@@ -284,7 +468,7 @@ vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
     if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
     if (h->cfg.nranks != 1) return fail(h, VTI_E_STATE, "vti_step_adjoint is single-slab only (nranks = 1)");
     CU(h, cudaSetDevice(h->cfg.device));
-    if (!h->adj_s[0]) {   // the two coefficient-weighted scratch fields, zero halo
+    if (adj_two_pass(h) && !h->adj_s[0]) {   // the two-pass form's coefficient-weighted scratch fields, zero halo
         const size_t bytes = h->total_elems() * h->es;
         for (int b = 0; b < 2; ++b) {
             cudaError_t e = cudaMalloc(&h->adj_s[b], bytes);
