@@ -307,9 +307,9 @@ vti_status vti_reverse(vti_t h);
  * by one. Adjoint sources are injected traces (vti_set_injection, row = m - t_first, added
  * after the operator); receivers (vti_set_receivers) record psi^{m-1}; the Ricker source of
  * vti_add_source is not applied. Then <M^K X, Y> = <X, (M^T)^K Y> (the dot-product test of
- * tests/test_adjoint_gpu.py). One launch per step at R_xy = 4 (the coefficient products formed
- * in the stencil kernel), two at larger radii (products, then stencils; env
- * VTI_ADJ_TWO_PASS forces either); single-slab handles only. Bitwise equal to the oracle's
+ * tests/test_adjoint_gpu.py). One launch per step (the coefficient products formed in the
+ * stencil kernel), or two at R_xy = 12 and for fp64 above R_xy = 4 (products, then stencils;
+ * env VTI_ADJ_TWO_PASS forces either); single-slab handles only. Bitwise equal to the oracle's
  * vto_adjoint_ex. Errors: STATE (model unset, nranks > 1), PARAM, CUDA, INSTABILITY.
  */
 vti_status vti_step_adjoint(vti_t h, int32_t nsteps);

@@ -216,26 +216,26 @@ __global__ void __launch_bounds__(16 * ADJ_TY) k_adj_step(const AdjParams<T> A, 
 // zero-filled outside the slab), the CTA forms the s1 tile in shared memory, and each thread
 // forms s2 = vz2 (psi_p + psi_q) of plane k + R_z for its register queue. Same arithmetic as
 // k_adj_prep + k_adj_step, so the same bits.
-template <typename T, int R, int RZ>
+template <typename T, int R, int RZ, int TY>
 struct AdjFusedCfg {
     static constexpr int RA = (R + 3) / 4 * 4;
-    static constexpr int PW = 64 + 2 * RA, PH = ADJ_TY + 2 * R, TE = PH * PW;
+    static constexpr int PW = 64 + 2 * RA, PH = TY + 2 * R, TE = PH * PW;
     static constexpr int VEC = 16 / (int)sizeof(T);   // elements per 16-byte cp.async
     static constexpr int SMEM = 9 * TE * (int)sizeof(T);   // [2][4][TE] inputs + [TE] s1
 };
 
-template <typename T, int R, int RZ>
-__global__ void __launch_bounds__(16 * ADJ_TY) k_adj_fused(const AdjParams<T> A, int ntx, int nty)
+template <typename T, int R, int RZ, int TY>
+__global__ void __launch_bounds__(16 * TY) k_adj_fused(const AdjParams<T> A, int ntx, int nty)
 {
-    using F = AdjFusedCfg<T, R, RZ>;
+    using F = AdjFusedCfg<T, R, RZ, TY>;
     constexpr int NQ = 2 * RZ + 1, RA = F::RA, PW = F::PW, PH = F::PH, TE = F::TE, VEC = F::VEC;
-    constexpr int NT = 16 * ADJ_TY;
+    constexpr int NT = 16 * TY;
     extern __shared__ __align__(16) uint8_t adj_smem[];
     T *inb = reinterpret_cast<T *>(adj_smem);   // [2][4][TE]: psi_p, psi_q, vx2, vn2
     T *s1t = inb + 8 * TE;
     const int b = blockIdx.x;
     const int itx = b % ntx, ity = (b / ntx) % nty, izc = b / (ntx * nty);
-    const int x0 = itx * 64, y0 = ity * ADJ_TY;
+    const int x0 = itx * 64, y0 = ity * TY;
     const int kb = izc * ADJ_ZCHUNK, ke = min(A.nz, kb + ADJ_ZCHUNK);
     const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
     const int xg = x0 + 4 * tx, yl = y0 + tg;
@@ -351,18 +351,18 @@ __global__ void __launch_bounds__(16 * ADJ_TY) k_adj_fused(const AdjParams<T> A,
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-template <typename T>
-static vti_status launch_adj_fused(vti_s *h, const AdjParams<T> &A)
+template <typename T, int TY>
+static vti_status launch_adj_fused_ty(vti_s *h, const AdjParams<T> &A)
 {
-    const int ntx = (h->cfg.nx + 63) / 64, nty = (h->nyl + ADJ_TY - 1) / ADJ_TY;
+    const int ntx = (h->cfg.nx + 63) / 64, nty = (h->nyl + TY - 1) / TY;
     const int nzc = (h->cfg.nz + ADJ_ZCHUNK - 1) / ADJ_ZCHUNK;
     const int R = h->R, RZ = h->RZ;
 #define ADJF_CASE(r, rz)                                                                                   \
     if (R == r && RZ == rz) {                                                                              \
-        const int smem = AdjFusedCfg<T, r, rz>::SMEM;                                                      \
-        CU(h, cudaFuncSetAttribute((const void *)k_adj_fused<T, r, rz>,                                    \
+        const int smem = AdjFusedCfg<T, r, rz, TY>::SMEM;                                                  \
+        CU(h, cudaFuncSetAttribute((const void *)k_adj_fused<T, r, rz, TY>,                                \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));                    \
-        k_adj_fused<T, r, rz><<<ntx * nty * nzc, 16 * ADJ_TY, smem, h->stream>>>(A, ntx, nty);            \
+        k_adj_fused<T, r, rz, TY><<<ntx * nty * nzc, 16 * TY, smem, h->stream>>>(A, ntx, nty);            \
         CU(h, cudaGetLastError());                                                                         \
         return VTI_OK;                                                                                     \
     }
@@ -372,6 +372,15 @@ static vti_status launch_adj_fused(vti_s *h, const AdjParams<T> &A)
     ADJF_CASE(12, 8)
 #undef ADJF_CASE
     return fail(h, VTI_E_UNSUPPORTED, "no adjoint kernel for (%d, %d)", R, RZ);
+}
+
+// fp32: 16-row tiles (env VTI_ADJ_TY=8 for 8); fp64: 8-row tiles (shared memory)
+template <typename T>
+static vti_status launch_adj_fused(vti_s *h, const AdjParams<T> &A)
+{
+    static const int ty = getenv("VTI_ADJ_TY") ? atoi(getenv("VTI_ADJ_TY")) : 16;
+    if (sizeof(T) == 4 && ty == 16) return launch_adj_fused_ty<T, 16>(h, A);
+    return launch_adj_fused_ty<T, 8>(h, A);
 }
 
 template <typename T>
@@ -395,14 +404,15 @@ static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
     return fail(h, VTI_E_UNSUPPORTED, "no adjoint kernel for (%d, %d)", R, RZ);
 }
 
-// Which form: measured on B200 (tools/adjoint_rate.py), the one-pass kernel wins at R_xy = 4
-// (C2 68.4 vs 59.3 Gpoints/s) and the two-pass one at larger radii, whose wider aprons make
-// the four staged input tiles costly (C3 53 vs 49, C5 49 vs 46, N1 36.6 vs 25.1).
-// Env VTI_ADJ_TWO_PASS=1/0 forces either.
+// Which form: measured on B200 (tools/adjoint_rate.py), fp32 one-pass with 16-row tiles vs
+// two-pass: C2 67.7 vs 59.2, C3 63.2 vs 53.1, C5 60.3 vs 49.6 Gpoints/s, but N1 (R_xy = 12,
+// whose 24-row apron makes the four staged inputs costly) 29.5 vs 36.6. fp64 runs 8-row tiles
+// (shared memory), measured at R_xy = 4 only with fp32's trend, so the one-pass form is kept to
+// R_xy <= 4 there. Env VTI_ADJ_TWO_PASS=1/0 forces either.
 static bool adj_two_pass(const vti_s *h)
 {
     static const int env = getenv("VTI_ADJ_TWO_PASS") ? atoi(getenv("VTI_ADJ_TWO_PASS")) : -1;
-    return env >= 0 ? env != 0 : h->R > 4;
+    return env >= 0 ? env != 0 : (h->es == 4 ? h->R > 8 : h->R > 4);
 }
 
 template <typename T>
