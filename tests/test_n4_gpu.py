@@ -1,4 +1,6 @@
 """SURVEY.md 8(f) N4 hooks: receiver traces and time reversal, against the oracle."""
+import os
+
 import numpy as np
 import pytest
 
@@ -171,7 +173,8 @@ def test_injection_and_receivers_match_oracle(grid, nsteps, small):
     tr = (rng.normal(size=(nt, len(pts))) * 5.0).astype(np.float32)
     rec = np.concatenate([pts[:40], REC[:3] % np.array(grid[::1], np.int32)])
     with handle(cfg, dt, wxy, wz) as v:
-        assert v.info()["small_kernel"] == int(small)
+        if os.environ.get("VTI_LAYOUT") != "yzx":   # the small-grid kernel is [z][y][x]-only
+            assert v.info()["small_kernel"] == int(small)
         v.set_model(*model)
         v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"], mask=1)
         v.set_injection(pts, tr, fields=3, t_first=t_first)
