@@ -49,39 +49,40 @@ struct SmallCfg {
 // (4 points each). Returns u^{n+1} in pn / qn and this thread's u^n centre values in pc / qc
 // (the next step's u^{n-1} in the multi-step kernel). s = s(t^n); inj_row / rec_row: the N4
 // trace rows of this step (IO only).
-template <typename T, int R, int RZ, int TY, bool IO>
+template <typename T, int R, int RZ, int TY, bool IO, int PX = 4>
 __device__ __forceinline__ void small_update(const StepParams<T> &P, const T *ptile, const T *zr, int y0, int k,
-                                             int tg, int tx, int xg, int yl, const V4<T> &g4, T gyv, T s,
-                                             long long inj_row, long long rec_row, const V4<T> &pm4,
-                                             const V4<T> &qm4, const V4<T> (&qv)[2 * RZ + 1], const V4<T> &vx4,
-                                             const V4<T> &vn4, const V4<T> &vz4, T (&pn)[1][4], T (&qn)[1][4],
-                                             T (&pc)[4], T (&qc)[4])
+                                             int tg, int tx, int xg, int yl, const Vec<T, PX> &g4, T gyv, T s,
+                                             long long inj_row, long long rec_row, const Vec<T, PX> &pm4,
+                                             const Vec<T, PX> &qm4, const Vec<T, PX> (&qv)[2 * RZ + 1],
+                                             const Vec<T, PX> &vx4, const Vec<T, PX> &vn4, const Vec<T, PX> &vz4,
+                                             T (&pn)[1][PX], T (&qn)[1][PX], T (&pc)[PX], T (&qc)[PX])
 {
     using C = Cfg<T, R, RZ, TY>;
     constexpr int NQ = C::NQ;
     constexpr int RA = C::RA;
-    const T *prow = ptile + (tg + R) * C::PW + 4 * tx;   // smem row of this tile row
-    const T *pbase = ptile + tg * C::PW + 4 * tx;
-    auto wx = [&](int i) { return lds4(prow + 4 * (i / 4))[i % 4]; };
-    T L[4];
+    static_assert(RA % PX == 0, "x apron must be whole vectors");
+    const T *prow = ptile + (tg + R) * C::PW + PX * tx;   // smem row of this tile row
+    const T *pbase = ptile + tg * C::PW + PX * tx;
+    auto wx = [&](int i) { return ldv<PX>(prow + PX * (i / PX))[i % PX]; };
+    T L[PX];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < PX; ++c) {
         pc[c] = wx(RA + c);
         L[c] = P.cxy[0] * pc[c];
     }
 #pragma unroll
     for (int l = 1; l <= R; ++l) {
-        const V4<T> yp = lds4(pbase + (R + l) * C::PW + RA);
-        const V4<T> ym = lds4(pbase + (R - l) * C::PW + RA);
+        const Vec<T, PX> yp = ldv<PX>(pbase + (R + l) * C::PW + RA);
+        const Vec<T, PX> ym = ldv<PX>(pbase + (R - l) * C::PW + RA);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < PX; ++c) {
             const T xpair = wx(RA + c + l) + wx(RA + c - l);
             const T ypair = yp[c] + ym[c];
             L[c] = fma_rn(P.cxy[l], xpair + ypair, L[c]);
         }
     }
     const T gz = zr[NQ];
-    const bool src_here = P.src_mask != 0 && P.src_j == yl && P.src_k == k && P.src_i >= xg && P.src_i < xg + 4;
+    const bool src_here = P.src_mask != 0 && P.src_j == yl && P.src_k == k && P.src_i >= xg && P.src_i < xg + PX;
     bool inj_on = false;
     const T *inj_base = nullptr;
     int inj_e = 0, inj_end = 0;
@@ -93,7 +94,7 @@ __device__ __forceinline__ void small_update(const StepParams<T> &P, const T *pt
         if (inj_on && yl < P.nyl) ps_row_range(P.inj_off, P.inj_ent, P.nyl, k, yl, xg, inj_e, inj_end);
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < PX; ++c) {
         qc[c] = qv[RZ][c];
         // Eq. 5: ascending m, D = w0 q_{k-Rz}; D = fma(w_m, q_{k-Rz+m}, D)
         T D = zr[0] * qv[0][c];
@@ -120,7 +121,7 @@ __device__ __forceinline__ void small_update(const StepParams<T> &P, const T *pt
         pn[0][c] = g * fma_rn(P.dt2, Fp, fma_rn(-g, pm4[c], T(2) * pc[c]));
         qn[0][c] = g * fma_rn(P.dt2, Fq, fma_rn(-g, qm4[c], T(2) * qv[RZ][c]));
     }
-    if constexpr (IO) record_points_row<T, 1, 4>(P, k, y0, TY, yl, xg, rec_row, pn, qn);
+    if constexpr (IO) record_points_row<T, 1, PX>(P, k, y0, TY, yl, xg, rec_row, pn, qn);
 }
 
 // The q column and stream operands of a thread from the TMA-staged item in shared memory.
@@ -214,6 +215,15 @@ struct SmallDCfg {
     static constexpr uint32_t TX_BYTES = C::P_BYTES + C::ZROW * C::ES;
 };
 
+template <typename T, int PX> __device__ __forceinline__ Vec<T, PX> vzero()
+{
+    Vec<T, PX> v;
+    if constexpr (std::is_same<T, float>::value && PX == 4) v.v = make_float4(0.f, 0.f, 0.f, 0.f);
+    else if constexpr (std::is_same<T, float>::value && PX == 2) v.v = make_float2(0.f, 0.f);
+    else if constexpr (PX == 4) v.a = v.b = make_double2(0.0, 0.0);
+    else v.a = make_double2(0.0, 0.0);
+    return v;
+}
 template <typename T> __device__ __forceinline__ V4<T> v4_zero();
 template <> __device__ __forceinline__ V4<float> v4_zero<float>() { return V4<float>{make_float4(0.f, 0.f, 0.f, 0.f)}; }
 template <> __device__ __forceinline__ V4<double> v4_zero<double>()
@@ -221,14 +231,18 @@ template <> __device__ __forceinline__ V4<double> v4_zero<double>()
     return V4<double>{make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
 }
 
-template <typename T, int R, int RZ, int TY, bool IO = false>
-__global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
+// PX consecutive x points per thread (TX / PX threads per tile row): fewer points per thread
+// shorten each thread's dependent instruction chain, the latency of a small-grid step.
+template <typename T, int R, int RZ, int TY, bool IO = false, int PX = 4>
+__global__ void __launch_bounds__(TY * (TX / PX))
     vti_small_direct_kernel(const __grid_constant__ SmallParams<T> S)
 {
     using C = Cfg<T, R, RZ, TY>;
     using DC = SmallDCfg<T, R, RZ, TY>;
+    using VP = Vec<T, PX>;
     constexpr int RA = C::RA;
     constexpr int NQ = C::NQ;
+    constexpr int TPR = TX / PX;
     const StepParams<T> &P = S.P;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + DC::OFF_BAR);
@@ -241,9 +255,9 @@ __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
-    const int xg = x0 + 4 * tx, yl = y0 + tg;
-    const V4<T> g4 = lds4(P.gx + xg);
+    const int tx = threadIdx.x % TPR, tg = threadIdx.x / TPR;
+    const int xg = x0 + PX * tx, yl = y0 + tg;
+    const VP g4 = ldv<PX>(P.gx + xg);
     const T gyv = (yl < P.nyl) ? P.gy[yl] : T(0);
     const bool store_ok = (yl < P.nyl) && (xg < P.nx);
     const T sv = P.s_table ? P.s_table[P.s_index] : P.s;
@@ -255,30 +269,30 @@ __global__ void __launch_bounds__(SmallCfg<T, R, RZ, TY>::THREADS)
         tma_load_3d(smem + DC::OFF_P, &P.tm_p, x0 - RA, y0, k, bar);
         bulk_load(smem + DC::OFF_ZR, P.zrow + (size_t)k * C::ZROW, C::ZROW * C::ES, bar);
     }
-    V4<T> qv[NQ], pm4 = v4_zero<T>(), qm4 = v4_zero<T>(), vx4 = v4_zero<T>(), vn4 = v4_zero<T>(),
-                  vz4 = v4_zero<T>();
+    VP qv[NQ], pm4 = vzero<T, PX>(), qm4 = vzero<T, PX>(), vx4 = vzero<T, PX>(), vn4 = vzero<T, PX>(),
+               vz4 = vzero<T, PX>();
 #pragma unroll
-    for (int m = 0; m < NQ; ++m) qv[m] = v4_zero<T>();
+    for (int m = 0; m < NQ; ++m) qv[m] = vzero<T, PX>();
     if (store_ok) {   // this thread's points: q column (zero exterior in z), u^{n-1}, model
         const long long off = (long long)yl * P.ys + xg;
 #pragma unroll
         for (int m = 0; m < NQ; ++m) {
             const int kk = k - RZ + m;
-            if (kk >= 0 && kk < P.nz) qv[m] = ldv<4>(S.q_cur + off + (long long)kk * P.zs);
+            if (kk >= 0 && kk < P.nz) qv[m] = ldv<PX>(S.q_cur + off + (long long)kk * P.zs);
         }
         const long long o = off + (long long)k * P.zs;
-        pm4 = ldv<4>(S.p_m + o);
-        qm4 = ldv<4>(S.q_m + o);
-        vx4 = ldv<4>(S.vx + o);
-        vn4 = ldv<4>(S.vn + o);
-        vz4 = ldv<4>(S.vz + o);
+        pm4 = ldv<PX>(S.p_m + o);
+        qm4 = ldv<PX>(S.q_m + o);
+        vx4 = ldv<PX>(S.vx + o);
+        vn4 = ldv<PX>(S.vn + o);
+        vz4 = ldv<PX>(S.vz + o);
     }
     mbar_wait(bar, 0);
     const T *st = reinterpret_cast<const T *>(smem);
-    T pn[1][4], qn[1][4], pc[4], qc[4];
-    small_update<T, R, RZ, TY, IO>(P, st + DC::OFF_P / C::ES, st + DC::OFF_ZR / C::ES, y0, k, tg, tx, xg, yl, g4,
-                                   gyv, sv, IO ? inj_row_of(P) : 0, IO ? rec_row_of(P) : 0, pm4, qm4, qv, vx4, vn4,
-                                   vz4, pn, qn, pc, qc);
+    T pn[1][PX], qn[1][PX], pc[PX], qc[PX];
+    small_update<T, R, RZ, TY, IO, PX>(P, st + DC::OFF_P / C::ES, st + DC::OFF_ZR / C::ES, y0, k, tg, tx, xg, yl,
+                                       g4, gyv, sv, IO ? inj_row_of(P) : 0, IO ? rec_row_of(P) : 0, pm4, qm4, qv,
+                                       vx4, vn4, vz4, pn, qn, pc, qc);
     if (store_ok) {
         const long long off = (long long)k * P.zs + (long long)yl * P.ys + xg;
         stv(P.p_out + off, pn[0]);
