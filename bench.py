@@ -557,7 +557,7 @@ def run_native(args):
         mc = mix_ceiling()
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": "Gpoints/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 5),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 7),
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": f"f{prec}",
             "data": "synthetic (seeded layered VTI model generated on device; zero initial state + Ricker source)",
             "config": describe(cfg, world, scaling, bpp, transport),

@@ -44,7 +44,7 @@ def test_native_arm_line():
     assert d["metric"] == json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 40 and d["warmup"] == 3
     assert d["dtype"] == "f32" and d["higher_is_better"] is True
-    assert abs(d["ms_per_step"] - 64 ** 3 / (d["value"] * 1e9) * 1e3) < 1e-3 * d["ms_per_step"] + 1e-6
+    assert abs(d["ms_per_step"] - 64 ** 3 / (d["value"] * 1e9) * 1e3) < 2e-3 * d["ms_per_step"] + 1e-7
     rf = d["roofline"]
     assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 0
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
