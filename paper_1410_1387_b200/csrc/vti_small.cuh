@@ -4,13 +4,18 @@
 // so a work item of one plane still walks 2 R_z priming loads and one full load
 // through its 3-stage ring, one round trip after another. That latency is most
 // of a step on grids like BASELINE C1 (64^3: 0.26 M points, ~4.6 us per step).
-// Here one CTA computes one (64 x TY tile, plane k) item, and a single elected
-// thread issues EVERY load of the item at once on one mbarrier: the halo'd p^n
-// plane tile, the whole q^n column k - R_z .. k + R_z as one 3-D TMA box
-// (planes outside 0..nz-1 are zero-filled, i.e. the paper's zero exterior in z),
-// p^{n-1}, q^{n-1}, vx2, vn2, vz2 and the plane's w^z + gz row. One round trip
-// per item. The arithmetic is the scalar canonical order of the main kernel
-// (reading c12), so results are bitwise identical.
+// Here one CTA computes one (64 x TY tile, plane k) item with one round trip of
+// loads, all in flight at once. Three forms, same arithmetic (the scalar
+// canonical order of the main kernel, reading c12, so results are
+// bitwise identical):
+//  * vti_small_direct_kernel (the default): TMA stages only what threads share,
+//    the halo'd p^n plane tile and the w^z + gz row; every thread loads its own
+//    q^n column k - R_z .. k + R_z (zero outside 0..nz-1: the zero exterior in
+//    z), p^{n-1}, q^{n-1} and model straight into registers;
+//  * vti_small_kernel (VTI_SMALL_DIRECT=0): one elected thread issues every
+//    load as TMA on one mbarrier, the q column as one 3-D box;
+//  * vti_small_multi_kernel (VTI_MULTI=1): a whole vti_step call in one
+//    cooperative launch, per-item epoch counters between steps (slower).
 #pragma once
 
 #include "vti_kernel.cuh"
