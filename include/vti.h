@@ -314,6 +314,12 @@ vti_status vti_reverse(vti_t h);
  */
 vti_status vti_step_adjoint(vti_t h, int32_t nsteps);
 
+/* The adjoint step for a local group of y-slab handles (created as for vti_group_step, any
+ * devices): per step every slab forms s1 / s2, copies its neighbours' R_xy boundary rows of s1
+ * into its halo, then runs the stencils; results are bitwise those of one slab. Errors: PARAM,
+ * STATE, CUDA. */
+vti_status vti_group_step_adjoint(vti_t *hs, int32_t n, int32_t nsteps);
+
 /* +1 (forward) or -1 (after an odd number of vti_reverse calls). */
 int32_t vti_direction(vti_t h);
 

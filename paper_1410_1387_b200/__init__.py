@@ -114,6 +114,7 @@ def _load():
         "vti_step_timed": (st, [H, C.c_int32, C.POINTER(C.c_float)]),
         "vti_group_step": (st, [C.POINTER(H), C.c_int32, C.c_int32]),
         "vti_group_step_staged": (st, [C.POINTER(H), C.c_int32, C.c_int32]),
+        "vti_group_step_adjoint": (st, [C.POINTER(H), C.c_int32, C.c_int32]),
         "vti_get_fields": (st, [H, P, P, C.c_int32]),
         "vti_get_fields_planes": (st, [H, C.c_int32, C.c_int32, P, P, C.c_int32]),
         "vti_sync": (st, [H]),
@@ -439,10 +440,12 @@ def group_step(handles, nsteps=1, transport="peer"):
 
     transport="peer": the fused peer-store halo transport (vti_group_step);
     "staged": the NCCL path's pack / exchange / unpack with device copies in place of
-    ncclSend/ncclRecv (vti_group_step_staged).
+    ncclSend/ncclRecv (vti_group_step_staged); "adjoint": nsteps of the adjoint
+    (transpose) recurrence over the slabs (vti_group_step_adjoint).
     """
     arr = (C.c_void_p * len(handles))(*[h.h for h in handles])
-    fn = {"peer": lib.vti_group_step, "staged": lib.vti_group_step_staged}[transport]
+    fn = {"peer": lib.vti_group_step, "staged": lib.vti_group_step_staged,
+          "adjoint": lib.vti_group_step_adjoint}[transport]
     st = fn(arr, len(handles), nsteps)
     if st != 0:
         for h in handles:

@@ -70,6 +70,8 @@ struct AdjParams {
     const int2 *rec_ent;
     T *rec_row;                    // this step's receiver row [n][nf], or NULL
     int rec_mask;
+    int y_lo, y_hi;                // rows of s1 the two-pass stencil may read: [y_lo, y_hi) (local rows;
+                                   // beyond [0, nyl) the neighbours' rows copied into the halo)
 };
 
 // the column of the CSR entry for point x of row (k, yl), or -1
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(16 * ADJ_TY) k_adj_step(const AdjParams<T> A, 
         for (int e = threadIdx.x; e < PH * PW; e += 16 * ADJ_TY) {
             const int r = e / PW, c = e % PW;
             const int yy = y0 - R + r, xx = x0 - RA + c;
-            const bool in = yy >= 0 && yy < A.nyl && xx >= 0 && xx < A.nx;
+            const bool in = yy >= A.y_lo && yy < A.y_hi && xx >= 0 && xx < A.nx;
             const T *src = in ? A.s1 + (int64_t)yy * A.ys + (int64_t)k * A.zs + xx : A.s1;
             const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + e);
             if constexpr (sizeof(T) == 8)
@@ -411,12 +413,28 @@ static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
 // R_xy <= 4 there. Env VTI_ADJ_TWO_PASS=1/0 forces either.
 static bool adj_two_pass(const vti_s *h)
 {
+    if (h->cfg.nranks > 1) return true;   // y-slabs: the s1 halo rows come from the neighbours
     static const int env = getenv("VTI_ADJ_TWO_PASS") ? atoi(getenv("VTI_ADJ_TWO_PASS")) : -1;
     return env >= 0 ? env != 0 : (h->es == 4 ? h->R > 8 : h->R > 4);
 }
 
+// Two-pass form, first launch: s1, s2 of the slab (phase 1 of a step).
 template <typename T>
-static vti_status adjoint_step_t(vti_s *h)
+static vti_status adjoint_prep_t(vti_s *h)
+{
+    const int c = h->cur;
+    k_adj_prep<T><<<4 * h->sms, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
+                                                   (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
+                                                   (const T *)h->in(h->vz2), (T *)h->in(h->adj_s[0]),
+                                                   (T *)h->in(h->adj_s[1]), h->cfg.nx, h->nyl, h->cfg.nz, h->ys,
+                                                   h->zs);
+    CU(h, cudaGetLastError());
+    return VTI_OK;
+}
+
+// The stencils and update (the whole step in the one-pass form; phase 2 of the two-pass one).
+template <typename T>
+static vti_status adjoint_step_t(vti_s *h, bool prep = true)
 {
     const int c = h->cur, o = 1 - c;
     const int grid = 4 * h->sms;
@@ -425,11 +443,10 @@ static vti_status adjoint_step_t(vti_s *h)
     if (two_pass) {
         s1 = (T *)h->in(h->adj_s[0]);
         s2 = (T *)h->in(h->adj_s[1]);
-        k_adj_prep<T><<<grid, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
-                                                 (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
-                                                 (const T *)h->in(h->vz2), s1, s2, h->cfg.nx, h->nyl, h->cfg.nz,
-                                                 h->ys, h->zs);
-        CU(h, cudaGetLastError());
+        if (prep) {
+            vti_status st = adjoint_prep_t<T>(h);
+            if (st != VTI_OK) return st;
+        }
     }
     AdjParams<T> A;
     A.s1 = s1;
@@ -464,29 +481,115 @@ static vti_status adjoint_step_t(vti_s *h)
     A.rec_ent = h->rec_set.ent;
     A.rec_row = rec ? (T *)h->traces + (size_t)h->rec_steps * h->nrec * nf : nullptr;
     A.rec_mask = h->rec_mask;
+    // a local group's slab reads its neighbours' s1 rows, copied into its halo (vti_group_step_adjoint)
+    A.y_lo = h->cfg.rank > 0 ? -h->R : 0;
+    A.y_hi = h->cfg.rank < h->cfg.nranks - 1 ? h->nyl + h->R : h->nyl;
     return two_pass ? launch_adj_step<T>(h, A, grid) : launch_adj_fused<T>(h, A);
 }
 
 }  // namespace
 
+static vti_status ensure_adj_scratch(vti_s *h)
+{
+    if (!adj_two_pass(h) || h->adj_s[0]) return VTI_OK;
+    // the two-pass form's coefficient-weighted fields s1, s2: the slab's geometry, zero halo
+    const size_t bytes = h->total_elems() * h->es;
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t e = cudaMalloc(&h->adj_s[b], bytes);
+        if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+        CU(h, cudaMemsetAsync(h->adj_s[b], 0, bytes, h->stream));
+        h->device_bytes += (int64_t)bytes;
+    }
+    return VTI_OK;
+}
+
+// s1's R boundary rows of the neighbour on `side` (0: rank-1, its last rows; 1: rank+1, its
+// first rows) into this slab's halo rows, on this handle's stream (the copy engine reads the
+// neighbour's memory directly, any device).
+static vti_status copy_s1_halo(vti_s *h, const vti_s *nb, int side)
+{
+    const char *src = nb->in(nb->adj_s[0]) + (size_t)(side == 0 ? nb->nyl - nb->R : 0) * nb->ys * nb->es;
+    char *dst = h->in(h->adj_s[0]) + (side == 0 ? -(long long)h->R : (long long)h->nyl) * h->ys * h->es;
+    // [z][y][x]: R rows are contiguous within each plane; [y][z][x]: one block
+    const size_t width = (size_t)h->R * h->ys * h->es;
+    const size_t height = h->layout_zyx ? (size_t)h->cfg.nz : 1;
+    const size_t spitch = h->layout_zyx ? (size_t)nb->zs * nb->es : width;
+    const size_t dpitch = h->layout_zyx ? (size_t)h->zs * h->es : width;
+    CU(h, cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, h->stream));
+    return VTI_OK;
+}
+
 extern "C" {
+
+vti_status vti_group_step_adjoint(vti_t *hs, int32_t n, int32_t nsteps)
+{
+    if (!hs || n < 1 || nsteps < 0) return VTI_E_PARAM;
+    if (n == 1) return vti_step_adjoint(hs[0], nsteps);
+    for (int i = 0; i < n; ++i) {
+        if (!hs[i]) return VTI_E_PARAM;
+        if (hs[i]->cfg.nranks != n || hs[i]->cfg.rank != i || !hs[i]->group_mode)
+            return fail(hs[i], VTI_E_STATE, "handle %d is not rank %d of a %d-handle local group", i, i, n);
+        if (!hs[i]->model_set) return fail(hs[i], VTI_E_STATE, "model not set");
+        if (hs[i]->n != hs[0]->n || hs[i]->cur != hs[0]->cur)
+            return fail(hs[i], VTI_E_STATE, "time indices or buffer parity differ inside the group");
+    }
+    vti_status s;
+    for (int i = 0; i < n; ++i) {
+        CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+        if ((s = ensure_adj_scratch(hs[i])) != VTI_OK) return s;
+    }
+    for (int it = 0; it < nsteps; ++it) {
+        // 1. s1, s2 of every slab; a slab's rows may be overwritten only once its neighbours
+        //    copied the previous step's (their ev_comm, recorded after those copies)
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            if (it > 0) {
+                if (i > 0) CU(h, cudaStreamWaitEvent(h->stream, hs[i - 1]->ev_comm, 0));
+                if (i < n - 1) CU(h, cudaStreamWaitEvent(h->stream, hs[i + 1]->ev_comm, 0));
+            }
+            s = h->es == 8 ? adjoint_prep_t<double>(h) : adjoint_prep_t<float>(h);
+            if (s != VTI_OK) return s;
+            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+        }
+        // 2. the neighbours' boundary rows of s1 into each halo
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            for (int side = 0; side < 2; ++side) {
+                const int j = side == 0 ? i - 1 : i + 1;
+                if (j < 0 || j >= n) continue;
+                CU(h, cudaStreamWaitEvent(h->stream, hs[j]->ev_edge, 0));
+                if ((s = copy_s1_halo(h, hs[j], side)) != VTI_OK) return s;
+            }
+            CU(h, cudaEventRecord(h->ev_comm, h->stream));
+        }
+        // 3. the stencils and update of every slab
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            s = h->es == 8 ? adjoint_step_t<double>(h, false) : adjoint_step_t<float>(h, false);
+            if (s != VTI_OK) return s;
+            h->cur = 1 - h->cur;
+            h->n -= 1;
+            if (h->rec_set.n > 0) h->rec_steps = std::min(h->rec_cap, h->rec_steps + 1);
+            if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0 && (s = check_finite(h)) != VTI_OK)
+                return s;
+        }
+    }
+    return VTI_OK;
+}
 
 vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
 {
     if (!h) return VTI_E_PARAM;
     if (nsteps < 0) return fail(h, VTI_E_PARAM, "nsteps < 0");
     if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
-    if (h->cfg.nranks != 1) return fail(h, VTI_E_STATE, "vti_step_adjoint is single-slab only (nranks = 1)");
+    if (h->cfg.nranks != 1)
+        return fail(h, VTI_E_STATE, "vti_step_adjoint is single-slab only; y-slabs: vti_group_step_adjoint");
     CU(h, cudaSetDevice(h->cfg.device));
-    if (adj_two_pass(h) && !h->adj_s[0]) {   // the two-pass form's coefficient-weighted scratch fields, zero halo
-        const size_t bytes = h->total_elems() * h->es;
-        for (int b = 0; b < 2; ++b) {
-            cudaError_t e = cudaMalloc(&h->adj_s[b], bytes);
-            if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
-            CU(h, cudaMemsetAsync(h->adj_s[b], 0, bytes, h->stream));
-            h->device_bytes += (int64_t)bytes;
-        }
-    }
+    vti_status s0 = ensure_adj_scratch(h);
+    if (s0 != VTI_OK) return s0;
     for (int it = 0; it < nsteps; ++it) {
         vti_status s = h->es == 8 ? adjoint_step_t<double>(h) : adjoint_step_t<float>(h);
         if (s != VTI_OK) return s;

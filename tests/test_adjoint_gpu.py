@@ -101,3 +101,39 @@ def test_adjoint_errors():
         with pytest.raises(VTIError) as e:
             v.step_adjoint(1)
         assert e.value.name == "VTI_E_STATE"
+
+
+@pytest.mark.parametrize("r,rz,prec,nranks", [(4, 4, 32, 2), (8, 4, 32, 3), (12, 8, 32, 2), (6, 6, 64, 3)])
+def test_group_adjoint_matches_single_slab_and_oracle(r, rz, prec, nranks):
+    """vti_group_step_adjoint over y-slabs (s1 halo rows copied from the neighbours): bitwise
+    equal to the oracle's adjoint, with injection (points on slab boundaries) and receivers."""
+    from paper_1410_1387_b200 import group_step
+    cfg, wxy, wz, dt, model, st, dtype = setup(r, rz, prec, shape=(70, 24 * nranks + 5, 2 * rz + 9))
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    from paper_1410_1387_b200 import slab
+    bounds = [slab(ny, q, nranks) for q in range(nranks)]
+    pts = [(5, 0, 0), (69, ny - 1, nz - 1), (30, ny // 2, nz // 2)]
+    for y0, nyl in bounds[1:]:
+        pts += [(31, y0 - 1, 3), (32, y0, 4), (33, y0 + 1, 5)]
+    pts = np.array(sorted(set(pts)), np.int32)
+    tr = np.random.default_rng(7).normal(size=(8, len(pts))).astype(dtype) * 10
+    m0, K = 20, 8
+    hs = [handle(cfg, dt, wxy, wz, prec, rank=q, nranks=nranks) for q in range(nranks)]
+    for h in hs:
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_model(*[np.ascontiguousarray(a[:, sl]) for a in model])
+        h.set_fields(*[np.ascontiguousarray(a[:, sl]) for a in st], time_index=m0)
+        h.set_injection(pts, tr, fields=3, t_first=m0 - 6)
+        h.set_receivers(pts, fields=1, capacity_steps=K)
+    group_step(hs, K, transport="adjoint")
+    got = [np.concatenate([h.get_fields(0)[f] for h in hs], axis=1) for f in range(2)]
+    traces = np.zeros((K, len(pts), 1), dtype)
+    for h in hs:
+        ids, t = h.get_traces()
+        traces[:, ids] = t
+        h.close()
+    o = oracle.adjoint_ex(oracle.params(cfg, dt, src=None), wxy, wz, *model, st, m0=m0, nsteps=K,
+                          inj=(pts, 3, m0 - 6, tr), rec=(pts, 1), dtype=dtype)
+    for f in range(2):
+        assert np.array_equal(got[f], o[f]), f"field {f}"
+    assert np.array_equal(traces, o[4])
