@@ -572,6 +572,7 @@ vti_status vti_group_step_adjoint(vti_t *hs, int32_t n, int32_t nsteps)
             if (s != VTI_OK) return s;
             h->cur = 1 - h->cur;
             h->n -= 1;
+            h->halo_dirty = true;   // p's halo rows are stale for a later forward step: re-publish then
             if (h->rec_set.n > 0) h->rec_steps = std::min(h->rec_cap, h->rec_steps + 1);
             if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0 && (s = check_finite(h)) != VTI_OK)
                 return s;
