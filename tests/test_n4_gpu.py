@@ -333,3 +333,46 @@ def test_dense_surface_injection_and_receivers(grid):
     o = oracle.run_ex(oracle.params(cfg, dt), wxy, wz, *model, None, nsteps=nsteps, inj=(inj, 1, 0, tr), rec=(rec, 3))
     assert np.array_equal(g[0], o[0]) and np.array_equal(g[1], o[1])
     assert np.array_equal(traces, o[4]) and np.abs(traces).max() > 0
+
+
+def test_async_snapshots_fp64_planes_and_slabs():
+    """Snapshots of a plane range in fp64, and per-slab snapshots of a local group (each slab
+    snapshots its own rows), equal to the oracle's level after each step."""
+    import torch
+    from synth import weights as W
+    from paper_1410_1387_b200 import group_step
+    cfg, _, _, dt, model = setup(60, 50, 40, damp=5)
+    wxy = W.xy_weights(cfg["r_xy"])
+    wz = np.ascontiguousarray(W.z_weights(W.z_coords_ramp(cfg["nz"], cfg["r_z"], 6.0, 12.0), cfg["r_z"]))
+    m64 = [a.astype(np.float64) for a in model]
+    k0, nk, nsteps = 11, 7, 5
+    ring = torch.zeros((nsteps, nk, cfg["ny"], cfg["nx"]), dtype=torch.float64, device="cuda")
+    with handle(cfg, dt, wxy, wz, precision=64) as v:
+        v.set_model(*m64)
+        v.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+        for n in range(nsteps):
+            v.step(1)
+            v.snapshot_async(ring[n], None, level=0, planes=(k0, nk))
+        v.sync()
+    P = oracle.params(cfg, dt)
+    st = None
+    for n in range(nsteps):
+        st = oracle.run(P, wxy, wz, *m64, st, n0=n, nsteps=1, dtype=np.float64)[:4]
+        assert np.array_equal(ring[n].cpu().numpy(), st[0][k0:k0 + nk])
+    # two slabs, fp32: each snapshots its own rows of u^n after the group's steps
+    wxy32, wz32 = wxy.astype(np.float32), wz.astype(np.float32)
+    hs = [handle(cfg, dt, wxy32, wz32, rank=r, nranks=2) for r in range(2)]
+    outs = []
+    for h in hs:
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_model(*[np.ascontiguousarray(a[:, sl]) for a in model])
+        h.add_source(*cfg["src"], f=cfg["f"], t0=cfg["t0"])
+    group_step(hs, 6)
+    for h in hs:
+        buf = torch.zeros((cfg["nz"], h.ny_local, cfg["nx"]), dtype=torch.float32, device="cuda")
+        h.snapshot_async(buf, None)
+        h.sync()
+        outs.append(buf.cpu().numpy())
+        h.close()
+    o = oracle.run(oracle.params(cfg, dt), wxy32, wz32, *model, None, nsteps=6)[0]
+    assert np.array_equal(np.concatenate(outs, axis=1), o)
