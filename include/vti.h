@@ -308,8 +308,8 @@ vti_status vti_reverse(vti_t h);
  * after the operator); receivers (vti_set_receivers) record psi^{m-1}; the Ricker source of
  * vti_add_source is not applied. Then <M^K X, Y> = <X, (M^T)^K Y> (the dot-product test of
  * tests/test_adjoint_gpu.py). One launch per step (the coefficient products formed in the
- * stencil kernel), or two at R_xy = 12 and for fp64 above R_xy = 4 (products, then stencils;
- * env VTI_ADJ_TWO_PASS forces either); single-slab handles only. Bitwise equal to the oracle's
+ * stencil kernel), or two for fp64 at R_xy >= 8 (products, then stencils; env
+ * VTI_ADJ_TWO_PASS forces either); single-slab handles (y-slabs: vti_group_step_adjoint). Bitwise equal to the oracle's
  * vto_adjoint_ex. Errors: STATE (model unset, nranks > 1), PARAM, CUDA, INSTABILITY.
  */
 vti_status vti_step_adjoint(vti_t h, int32_t nsteps);

@@ -111,13 +111,13 @@ __global__ void __launch_bounds__(16 * ADJ_TY) k_adj_step(const AdjParams<T> A, 
     const bool own = xg < A.nx && yl < A.nyl;
     // s2 column queue: slot m holds plane k - RZ + m
     T q[NQ][4];
-    auto load4 = [&](const T *base, int k, T (&v)[4]) {
+    auto load4 = [&](const T *base, int k, T (&v)[4]) {   // 16-byte loads (rows are padded to 32 points)
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[c] = T(0);
         if (!own || k < 0 || k >= A.nz) return;
-        const T *p = base + (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+        const V4<T> w = ldv<4>(base + (int64_t)yl * A.ys + (int64_t)k * A.zs + xg);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) v[c] = (xg + c < A.nx) ? p[c] : T(0);
+        for (int c = 0; c < 4; ++c) v[c] = (xg + c < A.nx) ? w[c] : T(0);
     };
 #pragma unroll
     for (int m = 0; m < NQ - 1; ++m) load4(A.s2, kb - RZ + m, q[m + 1]);
@@ -177,14 +177,15 @@ __global__ void __launch_bounds__(16 * ADJ_TY) k_adj_step(const AdjParams<T> A, 
             }
             const T gz = A.zrow[(int64_t)k * A.zrow_stride + NQ];
             const int64_t a0 = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+            const V4<T> po4 = ldv<4>(A.po + a0), qo4 = ldv<4>(A.qo + a0), gx4 = ldv<4>(A.gx + xg);
+            const V4<T> pc4 = ldv<4>(A.pc + a0), qc4 = ldv<4>(A.qc + a0);
+            T pn[4], qn[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                if (xg + c >= A.nx) continue;
-                const int64_t a = a0 + c;
                 const int i = xg + c;
                 Fp[c] = L[c];
                 Fq[c] = DT[c];
-                if (A.inj_row != nullptr) {
+                if (A.inj_row != nullptr && i < A.nx) {
                     const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, yl, i);
                     if (e >= 0) {
                         const T v = A.inj_row[A.inj_ent[e].y];
@@ -192,20 +193,37 @@ __global__ void __launch_bounds__(16 * ADJ_TY) k_adj_step(const AdjParams<T> A, 
                         if (A.inj_mask & 2) Fq[c] = Fq[c] + v;
                     }
                 }
-                const T g = (A.gx[i] * gy) * gz;
-                const T pn = g * fma_x<T>(A.dt2, Fp[c], fma_x<T>(-g, A.po[a], T(2) * A.pc[a]));
-                const T qn = g * fma_x<T>(A.dt2, Fq[c], fma_x<T>(-g, A.qo[a], T(2) * A.qc[a]));
-                A.po[a] = pn;
-                A.qo[a] = qn;
-                if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
-                    const long long rb = (long long)k * A.nyl + yl;
-                    const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
-                    for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
-                        if (A.rec_ent[e].x != i) continue;
-                        T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
-                        if (A.rec_mask & 1) *o++ = pn;
-                        if (A.rec_mask & 2) *o = qn;
+                const T g = (gx4[c] * gy) * gz;
+                pn[c] = g * fma_x<T>(A.dt2, Fp[c], fma_x<T>(-g, po4[c], T(2) * pc4[c]));
+                qn[c] = g * fma_x<T>(A.dt2, Fq[c], fma_x<T>(-g, qo4[c], T(2) * qc4[c]));
+            }
+            if (xg + 4 <= A.nx) {   // whole vector inside the row
+                stv(A.po + a0, pn);
+                stv(A.qo + a0, qn);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (xg + c < A.nx) {
+                        A.po[a0 + c] = pn[c];
+                        A.qo[a0 + c] = qn[c];
                     }
+            }
+            if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
+                const long long rb = (long long)k * A.nyl + yl;
+                const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
+                for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
+                    const int c = A.rec_ent[e].x - xg;
+                    if (c < 0 || c >= 4) continue;
+                    T vp = pn[0], vq = qn[0];
+#pragma unroll
+                    for (int cc = 1; cc < 4; ++cc)
+                        if (c == cc) {
+                            vp = pn[cc];
+                            vq = qn[cc];
+                        }
+                    T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
+                    if (A.rec_mask & 1) *o++ = vp;
+                    if (A.rec_mask & 2) *o = vq;
                 }
             }
         }
@@ -264,14 +282,15 @@ __global__ void __launch_bounds__(16 * TY) k_adj_fused(const AdjParams<T> A, int
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     // s2 = vz2 (psi_p + psi_q) of plane k at this thread's 4 points (0 outside the grid)
-    auto s2_of = [&](int k, T (&v)[4]) {
+    auto s2_of = [&](int k, T (&v)[4]) {   // 16-byte loads (rows are padded to 32 points)
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[c] = T(0);
         if (!own || k < 0 || k >= A.nz) return;
         const int64_t a = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+        const V4<T> vz = ldv<4>(A.vz + a), pp = ldv<4>(A.pc + a), qq = ldv<4>(A.qc + a);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-            if (xg + c < A.nx) v[c] = A.vz[a + c] * (A.pc[a + c] + A.qc[a + c]);
+            if (xg + c < A.nx) v[c] = vz[c] * (pp[c] + qq[c]);
     };
     T q[NQ][4];
 #pragma unroll
@@ -318,13 +337,14 @@ __global__ void __launch_bounds__(16 * TY) k_adj_fused(const AdjParams<T> A, int
             }
             const T gz = A.zrow[(int64_t)k * A.zrow_stride + NQ];
             const int64_t a0 = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+            const V4<T> po4 = ldv<4>(A.po + a0), qo4 = ldv<4>(A.qo + a0), gx4 = ldv<4>(A.gx + xg);
+            const V4<T> pc4 = ldv<4>(pin + ctr), qc4 = ldv<4>(pin + TE + ctr);
+            T pn[4], qn[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                if (xg + c >= A.nx) continue;
-                const int64_t a = a0 + c;
                 const int i = xg + c;
                 T Fp = L[c], Fq = DT[c];
-                if (A.inj_row != nullptr) {
+                if (A.inj_row != nullptr && i < A.nx) {
                     const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, yl, i);
                     if (e >= 0) {
                         const T v = A.inj_row[A.inj_ent[e].y];
@@ -332,20 +352,37 @@ __global__ void __launch_bounds__(16 * TY) k_adj_fused(const AdjParams<T> A, int
                         if (A.inj_mask & 2) Fq = Fq + v;
                     }
                 }
-                const T g = (A.gx[i] * gy) * gz;
-                const T pn = g * fma_x<T>(A.dt2, Fp, fma_x<T>(-g, A.po[a], T(2) * pin[ctr + c]));
-                const T qn = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, A.qo[a], T(2) * pin[TE + ctr + c]));
-                A.po[a] = pn;
-                A.qo[a] = qn;
-                if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
-                    const long long rb = (long long)k * A.nyl + yl;
-                    const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
-                    for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
-                        if (A.rec_ent[e].x != i) continue;
-                        T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
-                        if (A.rec_mask & 1) *o++ = pn;
-                        if (A.rec_mask & 2) *o = qn;
+                const T g = (gx4[c] * gy) * gz;
+                pn[c] = g * fma_x<T>(A.dt2, Fp, fma_x<T>(-g, po4[c], T(2) * pc4[c]));
+                qn[c] = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, qo4[c], T(2) * qc4[c]));
+            }
+            if (xg + 4 <= A.nx) {   // whole vector inside the row
+                stv(A.po + a0, pn);
+                stv(A.qo + a0, qn);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (xg + c < A.nx) {
+                        A.po[a0 + c] = pn[c];
+                        A.qo[a0 + c] = qn[c];
                     }
+            }
+            if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
+                const long long rb = (long long)k * A.nyl + yl;
+                const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
+                for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
+                    const int c = A.rec_ent[e].x - xg;
+                    if (c < 0 || c >= 4) continue;
+                    T vp = pn[0], vq = qn[0];
+#pragma unroll
+                    for (int cc = 1; cc < 4; ++cc)
+                        if (c == cc) {
+                            vp = pn[cc];
+                            vq = qn[cc];
+                        }
+                    T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
+                    if (A.rec_mask & 1) *o++ = vp;
+                    if (A.rec_mask & 2) *o = vq;
                 }
             }
         }
@@ -406,16 +443,17 @@ static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
     return fail(h, VTI_E_UNSUPPORTED, "no adjoint kernel for (%d, %d)", R, RZ);
 }
 
-// Which form: measured on B200 (tools/adjoint_rate.py), fp32 one-pass with 16-row tiles vs
-// two-pass: C2 67.7 vs 59.2, C3 63.2 vs 53.1, C5 60.3 vs 49.6 Gpoints/s, but N1 (R_xy = 12,
-// whose 24-row apron makes the four staged inputs costly) 29.5 vs 36.6. fp64 runs 8-row tiles
-// (shared memory), measured at R_xy = 4 only with fp32's trend, so the one-pass form is kept to
-// R_xy <= 4 there. Env VTI_ADJ_TWO_PASS=1/0 forces either.
+// Which form (single slab), measured on B200 with vectorised loads (tools/adjoint_rate.py,
+// profiles/r02/adjoint_rate_r02.txt): fp32 one-pass (16-row tiles) vs two-pass: C2 78.1 vs 56.2,
+// C3 81.4 vs 53.0, N1 38.7 vs 37.3 Gpoints/s; fp64 one-pass (8-row tiles, the shared-memory
+// limit) wins at R_xy = 4 and 6 (C2 36.9 vs 34.3, C5 34.1 vs 25.6) and loses at 8 and 12 (C3
+// 20.1 vs 31.2, N1 14.5 vs 19.3). Y-slab groups always run the two-pass form (the s1 halo rows
+// come from the neighbours). Env VTI_ADJ_TWO_PASS=1/0 forces either on a single slab.
 static bool adj_two_pass(const vti_s *h)
 {
-    if (h->cfg.nranks > 1) return true;   // y-slabs: the s1 halo rows come from the neighbours
+    if (h->cfg.nranks > 1) return true;
     static const int env = getenv("VTI_ADJ_TWO_PASS") ? atoi(getenv("VTI_ADJ_TWO_PASS")) : -1;
-    return env >= 0 ? env != 0 : (h->es == 4 ? h->R > 8 : h->R > 4);
+    return env >= 0 ? env != 0 : (h->es == 8 && h->R >= 8);
 }
 
 // Two-pass form, first launch: s1, s2 of the slab (phase 1 of a step).
@@ -432,7 +470,6 @@ static vti_status adjoint_prep_t(vti_s *h)
     return VTI_OK;
 }
 
-// The stencils and update (the whole step in the one-pass form; phase 2 of the two-pass one).
 template <typename T>
 static vti_status adjoint_step_t(vti_s *h, bool prep = true)
 {
