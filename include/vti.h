@@ -346,6 +346,13 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi);
 /* 0: none (single slab), 1: NCCL, 2: fused peer stores (local group or CUDA IPC). */
 int32_t vti_halo_transport(vti_t h);
 
+/* Diagnostics of the peer transport (tests): read (get4) and/or overwrite (set4) this handle's
+ * four flag words {DATA_LO, DATA_HI, ACK_LO, ACK_HI} -- the words its neighbours write --, and
+ * copy R_xy halo rows of p (side 0: the rows below the slab, side 1: above; level 0: u^n, 1:
+ * the stored level) to host memory [nz][R_xy][nx]. Both synchronise. Errors: PARAM, STATE, CUDA. */
+vti_status vti_debug_flags(vti_t h, uint32_t *get4, const uint32_t *set4);
+vti_status vti_debug_halo(vti_t h, int32_t level, int32_t side, void *out);
+
 /* Block until all work on the handle's stream(s) is done. */
 vti_status vti_sync(vti_t h);
 

@@ -137,6 +137,8 @@ def _load():
         "vti_ipc_export": (st, [H, P]),
         "vti_ipc_connect": (st, [H, P, P]),
         "vti_halo_transport": (C.c_int32, [H]),
+        "vti_debug_flags": (st, [H, P, P]),
+        "vti_debug_halo": (st, [H, C.c_int32, C.c_int32, P]),
         "vti_direction": (C.c_int32, [H]),
         "vti_autotune": (st, [H, C.c_int32, C.POINTER(TuneResult)]),
         "vti_last_error": (C.c_char_p, [H]),
@@ -394,6 +396,19 @@ class VTI:
     def step_adjoint(self, nsteps=1):
         """vti_step_adjoint: nsteps of the transpose recurrence (state = (psi^m, psi^{m+1}))."""
         _check(self.h, lib.vti_step_adjoint(self.h, nsteps))
+
+    def debug_flags(self, set4=None):
+        """vti_debug_flags: this handle's flag words (DATA_LO, DATA_HI, ACK_LO, ACK_HI); optionally set them."""
+        out = np.zeros(4, np.uint32)
+        src = None if set4 is None else np.ascontiguousarray(np.asarray(set4, np.uint32))
+        _check(self.h, lib.vti_debug_flags(self.h, out.ctypes.data, None if src is None else src.ctypes.data))
+        return out
+
+    def debug_halo(self, level=0, side=0):
+        """vti_debug_halo: p's R_xy halo rows below (side 0) / above (side 1) the slab, [nz][R][nx]."""
+        out = np.zeros((self.nz, self.cfg.r_xy, self.nx), dtype=self.dtype)
+        _check(self.h, lib.vti_debug_halo(self.h, level, side, out.ctypes.data))
+        return out
 
     def reverse(self):
         """vti_reverse: swap the stored levels; the next steps run backwards in time."""

@@ -426,6 +426,32 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
 
 int32_t vti_halo_transport(vti_t h) { return !h ? -1 : h->cfg.nranks < 2 ? 0 : h->peer ? 2 : h->comm_nccl ? 1 : 0; }
 
+vti_status vti_debug_flags(vti_t h, uint32_t *get4, const uint32_t *set4)
+{
+    if (!h) return VTI_E_PARAM;
+    if (!h->flags) return fail(h, VTI_E_STATE, "no flag words (nranks < 2)");
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    if (get4) CU(h, cudaMemcpy(get4, h->flags, 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    if (set4) CU(h, cudaMemcpy(h->flags, set4, 4 * sizeof(unsigned int), cudaMemcpyHostToDevice));
+    return VTI_OK;
+}
+
+vti_status vti_debug_halo(vti_t h, int32_t level, int32_t side, void *out)
+{
+    if (!h || !out || (level != 0 && level != 1) || (side != 0 && side != 1)) return VTI_E_PARAM;
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    const int b = level == 0 ? h->cur : 1 - h->cur;
+    // halo'd rows [0, R) (side 0) or [nyl + R, nyl + 2R) (side 1) of p buffer b -> out[nz][R][nx]
+    const char *src = (const char *)h->pbuf[b] + (size_t)(side == 0 ? 0 : h->nyl + h->R) * h->ys * h->es;
+    const size_t row = (size_t)h->cfg.nx * h->es;
+    for (int k = 0; k < h->cfg.nz; ++k)
+        CU(h, cudaMemcpy2D((char *)out + (size_t)k * h->R * row, row, src + (size_t)k * h->zs * h->es,
+                           (size_t)h->ys * h->es, row, h->R, cudaMemcpyDeviceToHost));
+    return VTI_OK;
+}
+
 // Local group: the fused peer-memory transport between handles of one process
 // (peer pointers are the neighbours' own device buffers), the same protocol as the
 // multi-process CUDA-IPC form.

@@ -90,3 +90,72 @@ def test_two_process_ipc_connect():
         assert got[r]["bench_transport"] == "peer" and got[r]["max"] == 1.25, got
     for p in procs:
         assert p.exitcode == 0
+
+
+def _one_sided_worker(rank, world, port, q):
+    """Rank 0 steps with its neighbour's flags pre-satisfied (no process waits on another's GPU
+    work); rank 1 stays idle and afterwards inspects what arrived in its memory over CUDA IPC."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import synth
+        from synth import fields as SF
+        from paper_1410_1387_b200 import VTI, multi
+        cfg = synth.scaled(synth.CONFIGS["C2"](), 70, 96, 20, damp_width=4, dz=(6.0, 12.0), t0=0.02)
+        wxy, wz, _ = synth.weights_f32(cfg)
+        dt = synth.stable_dt(cfg, wxy, wz)
+        h = VTI(cfg["nx"], cfg["ny"], cfg["nz"], cfg["h"], 4, 4, dt, wxy, wz, damp_width=4, device=0,
+                rank=rank, nranks=world)
+        assert multi.connect_peer(dist, h, rank, world)
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        h.set_model(*[np.ascontiguousarray(a.numpy()[:, sl]) for a in SF.model_planes(cfg, 0, cfg["nz"])])
+        res = {"launches": h.info()["launches_per_step"]}
+        K = 3
+        dist.barrier()
+        if rank == 0:
+            h.debug_flags(set4=[1 << 20] * 4)   # the neighbour's DATA / ACK: every wait passes
+            st = [SF.random_planes(cfg["nx"], cfg["ny"], 0, cfg["nz"], 5, s, 1e-3).numpy()[:, sl] for s in range(4)]
+            h.set_fields(*[np.ascontiguousarray(a) for a in st], time_index=0)
+            h.step(K)   # the fused one-launch peer step: PEER stores + device-side flag release over IPC
+            h.sync()
+            res["last_rows"] = h.get_fields(0)[0][:, -4:, :].copy()
+        dist.barrier()
+        if rank == 1:
+            # rank 0's output buffer of step K has index K % 2; this idle rank's cur is 0
+            res["halo"] = h.debug_halo(level=K % 2, side=0)
+            res["flags"] = h.debug_flags().tolist()
+        dist.barrier()
+        h.close()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_ipc_one_sided_step():
+    """The multi-process fused peer step across two processes on cuda:0 without mutual waiting:
+    rank 0's last R_xy rows of u^K land in rank 1's halo rows through CUDA-IPC peer stores, and
+    rank 0's last edge CTA raises rank 1's flag words (st.release.sys) to the publication count."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_one_sided_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        got = dict(q.get(timeout=300) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert got[0]["launches"] == 1 and got[1]["launches"] == 1
+    assert np.abs(got[0]["last_rows"]).max() > 0
+    assert np.array_equal(got[1]["halo"], got[0]["last_rows"])
+    # publications: the re-publication of the state set by the caller, then one per step
+    assert got[1]["flags"] == [4, 0, 3, 0], got[1]["flags"]
+    for p in procs:
+        assert p.exitcode == 0
