@@ -6,18 +6,22 @@
 //   psi^{m-1} = g (2 psi^m - g psi^{m+1} + dt^2 (A^T psi^m + inj)),
 //   A^T psi = (L (vx2 psi_p + vn2 psi_q), D^T (vz2 (psi_p + psi_q))),
 // L symmetric on the zero exterior and (D^T y)_k = sum_m w^z[k+Rz-m][m] y_{k+Rz-m}. The
-// coefficient fields act BEFORE the derivatives here, so a step is two launches: k_adj_prep
-// forms s1 = vx2 psi_p + vn2 psi_q and s2 = vz2 (psi_p + psi_q) over the slab, and k_adj_step
-// applies L to s1, D^T to s2 and the update. Canonical operation order (bitwise equal to the
-// oracle's vto_adjoint_ex): s1 = fma(vx2, psi_p, vn2*psi_q), s2 = vz2*(psi_p + psi_q);
+// coefficient fields act BEFORE the derivatives here: s1 = vx2 psi_p + vn2 psi_q is needed on the
+// R_xy apron of every tile, s2 = vz2 (psi_p + psi_q) along z. Canonical operation order (bitwise
+// equal to the oracle's vto_adjoint_ex): s1 = fma(vx2, psi_p, vn2*psi_q), s2 = vz2*(psi_p + psi_q);
 // L = c0 s1; L = fma(c_l, (x+ + x-) + (y+ + y-), L); DT = 0, DT = fma(w[k'][m], s2(k'), DT) for
 // m = 0..2Rz, k' = k+Rz-m inside the grid; F_p = L (+ inj), F_q = DT (+ inj);
 // psi^{m-1} = g*fma(dt2, F, fma(-g, psi^{m+1}, 2 psi^m)).
 //
-// k_adj_prep is elementwise; k_adj_step marches z per (tile, z-chunk) with the s1 tile staged in
-// shared memory and s2 in a register queue (the forward kernel's structure, plain loads instead
-// of its TMA ring). Single-slab handles only (the s1 cross would need the neighbours' psi and
-// model rows).
+// Forms (adj_form picks one; every form gives the same bits):
+//   * TMA one-pass (k_adj_tma): per plane, the halo'd psi_p, psi_q, vx2, vn2 boxes arrive by TMA
+//     and the CTA forms the s1 tile in shared memory; 36 B/pt in fp32 like the forward step.
+//   * TMA two-pass (k_adj_s1, then k_adj_tma2): s1 in HBM, read back as one halo'd box; chained
+//     across the steps of a call (each step also writes the next step's s1: 44 B/pt, one launch
+//     per step after the first). Y-slab groups run this form with the neighbours' s1 rows
+//     copied into each slab's halo between steps.
+//   * cp.async forms (k_adj_fused one-pass; k_adj_prep + k_adj_step two-pass): the round-2 first
+//     versions, for radii without a TMA entry and as A/B baselines (VTI_ADJ_TMA=0).
 #include "vti_internal.h"
 
 namespace {
@@ -54,6 +58,7 @@ struct AdjParams {
     const T *vx, *vn, *vz;         // model interior views (one-pass form)
     const T *pc, *qc;              // psi^m
     T *po, *qo;                    // psi^{m+1} in, psi^{m-1} out (in place)
+    T *s1o;                        // chained TMA two-pass form: s1 of psi^{m-1} out (interior view)
     const T *zrow;                 // [nz][zrow_stride]: w^z[k][0..2Rz], gz[k]
     int zrow_stride;
     const T *gx, *gy;
@@ -443,45 +448,778 @@ static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
     return fail(h, VTI_E_UNSUPPORTED, "no adjoint kernel for (%d, %d)", R, RZ);
 }
 
-// Which form (single slab), measured on B200 with vectorised loads (tools/adjoint_rate.py,
-// profiles/r02/adjoint_rate_r02.txt): fp32 one-pass (16-row tiles) vs two-pass: C2 78.1 vs 56.2,
-// C3 81.4 vs 53.0, N1 38.7 vs 37.3 Gpoints/s; fp64 one-pass (8-row tiles, the shared-memory
-// limit) wins at R_xy = 4 and 6 (C2 36.9 vs 34.3, C5 34.1 vs 25.6) and loses at 8 and 12 (C3
-// 20.1 vs 31.2, N1 14.5 vs 19.3). Y-slab groups always run the two-pass form (the s1 halo rows
-// come from the neighbours). Env VTI_ADJ_TWO_PASS=1/0 forces either on a single slab.
-static bool adj_two_pass(const vti_s *h)
+// ---------------------------------------------------------------- TMA form (single slab default)
+// The forward kernel's structure applied to the transpose. A persistent CTA walks (64 x TY tile,
+// z-chunk) items. A producer warp streams, per plane k, into an mbarrier ring
+// (cp.async.bulk.tensor, zero fill outside the grid):
+//   * the halo'd psi_p, psi_q, vx2, vn2 boxes of plane k (the s1 apron);
+//   * the interior psi_p, psi_q, vz2 boxes of plane k + Rz (the s2 queue front);
+//   * the interior psi^{m+1} boxes of plane k;
+//   * plane k's row of the transposed z weights wT[k][m] = w^z[k+Rz-m][m] (0 outside the grid).
+// Consumers form the s1 tile with its apron in shared memory (double-buffered: one named barrier
+// per plane), push s2(k + Rz) into a (2Rz+1)-deep register queue, take their own psi^m, psi^{m+1}
+// and D^T, release the stage, then apply L to s1 and update. DRAM: psi^m (2), model (3) and
+// psi^{m+1} (2) read once, psi^{m-1} (2) written = 36 B/pt in fp32 like the forward step; the
+// aprons and the Rz-ahead psi boxes come back from L2. Same canonical arithmetic as k_adj_prep +
+// k_adj_step (a skipped out-of-grid D^T term equals an fma with weight 0 and s2 = 0 bit for bit:
+// DT starts at +0 and +0 + (+-0) = +0), so the same bits as the oracle.
+template <typename T, int R, int RZ, int TY, int ST>
+struct AdjTmaCfg {
+    static constexpr int ES = (int)sizeof(T);
+    static constexpr int RA = (R + 3) / 4 * 4;
+    static constexpr int PW = TX + 2 * RA, PH = TY + 2 * R, TE = PW * PH;
+    static constexpr int NQ = 2 * RZ + 1;
+    static constexpr int ZROW = ((NQ + 1 + 3) / 4) * 4;   // = the forward table's row (Cfg::ZROW)
+    static constexpr int P_BYTES = align128(TE * ES);
+    static constexpr int S_BYTES = TX * TY * ES;
+    static constexpr int OFF_HP = 0, OFF_HQ = P_BYTES, OFF_HX = 2 * P_BYTES, OFF_HN = 3 * P_BYTES;
+    static constexpr int OFF_IP = 4 * P_BYTES, OFF_IQ = OFF_IP + S_BYTES, OFF_VZ = OFF_IQ + S_BYTES;
+    static constexpr int OFF_OP = OFF_VZ + S_BYTES, OFF_OQ = OFF_OP + S_BYTES, OFF_ZR = OFF_OQ + S_BYTES;
+    static constexpr int STAGE = align128(OFF_ZR + ZROW * ES);
+    static constexpr uint32_t FULL_TX = 4 * TE * ES + 5 * S_BYTES + ZROW * ES;
+    static constexpr uint32_t PRIME_TX = 3 * S_BYTES;
+    static constexpr int OFF_S1 = ST * STAGE;               // [2][P_BYTES]: s1 of planes k (even / odd)
+    static constexpr int OFF_BAR = OFF_S1 + 2 * P_BYTES;
+    static constexpr int SMEM = OFF_BAR + 2 * ST * 8;
+    static constexpr int NCONS = 16 * TY;                   // consumer threads, 4 x points each
+    static constexpr int NT = NCONS + 32;                   // + the producer warp
+    static_assert(PW % 4 == 0 && PW <= 256 && PH <= 256, "TMA box");
+};
+
+template <typename T>
+struct AdjTmaParams {
+    CUtensorMap tm[9];   // halo'd psi_p^m, psi_q^m, vx2, vn2; interior psi_p^m, psi_q^m, vz2, psi_p^{m+1}, psi_q^{m+1}
+    AdjParams<T> A;      // A.zrow: the transposed rows [nz][ZROW] (w^T[k][0..2Rz], gz[k])
+    int ntx, nty, zchunk, items;
+};
+
+template <int TY, typename T>
+__device__ __forceinline__ void adj_item(const AdjTmaParams<T> &P, int item, int &x0, int &y0, int &kb, int &ke)
 {
-    if (h->cfg.nranks > 1) return true;
-    static const int env = getenv("VTI_ADJ_TWO_PASS") ? atoi(getenv("VTI_ADJ_TWO_PASS")) : -1;
-    return env >= 0 ? env != 0 : (h->es == 8 && h->R >= 8);
+    const int tx = item % P.ntx, r = item / P.ntx;
+    x0 = tx * TX;
+    y0 = (r % P.nty) * TY;
+    kb = (r / P.nty) * P.zchunk;
+    ke = min(P.A.nz, kb + P.zchunk);
 }
 
-// Two-pass form, first launch: s1, s2 of the slab (phase 1 of a step).
+template <typename T, int R, int RZ, int TY, int ST, bool IO>
+__global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
+    k_adj_tma(const __grid_constant__ AdjTmaParams<T> P)
+{
+    using C = AdjTmaCfg<T, R, RZ, TY, ST>;
+    constexpr int NQ = C::NQ, RA = C::RA, PW = C::PW, ES = C::ES, NCONS = C::NCONS;
+    constexpr bool SHIFT = NQ > 9;   // i-cache: NQ unrolled copies of a deep body miss (ncu: no_instructions)
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
+    uint64_t *empty = full + ST;
+    const AdjParams<T> &A = P.A;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCONS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int i = 0; i < 9; ++i) prefetch_tmap(&P.tm[i]);
+    }
+    __syncthreads();
+    int stage = 0;
+    uint32_t phase = 0;
+    if (warp == NCONS / 32) {   // producer: one lane walks the load sequence of every item
+        if (lane != 0) return;
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            int x0, y0, kb, ke;
+            adj_item<TY>(P, item, x0, y0, kb, ke);
+            const int nload = (ke - kb) + 2 * RZ;
+            for (int t = 0; t < nload; ++t) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t *st = smem + stage * C::STAGE;
+                uint64_t *bar = &full[stage];
+                if (t < 2 * RZ) {   // priming: s2 inputs of planes kb - Rz .. kb + Rz - 1
+                    const int kk = kb - RZ + t;
+                    mbar_arrive_expect_tx(bar, C::PRIME_TX);
+                    tma_load_3d(st + C::OFF_IP, &P.tm[4], x0, y0, kk, bar);
+                    tma_load_3d(st + C::OFF_IQ, &P.tm[5], x0, y0, kk, bar);
+                    tma_load_3d(st + C::OFF_VZ, &P.tm[6], x0, y0, kk, bar);
+                } else {
+                    const int k = kb + t - 2 * RZ;
+                    mbar_arrive_expect_tx(bar, C::FULL_TX);
+                    // halo'd views: row y0 of the view is local row y0 - R
+                    tma_load_3d(st + C::OFF_HP, &P.tm[0], x0 - RA, y0, k, bar);
+                    tma_load_3d(st + C::OFF_HQ, &P.tm[1], x0 - RA, y0, k, bar);
+                    tma_load_3d(st + C::OFF_HX, &P.tm[2], x0 - RA, y0, k, bar);
+                    tma_load_3d(st + C::OFF_HN, &P.tm[3], x0 - RA, y0, k, bar);
+                    tma_load_3d(st + C::OFF_IP, &P.tm[4], x0, y0, k + RZ, bar);
+                    tma_load_3d(st + C::OFF_IQ, &P.tm[5], x0, y0, k + RZ, bar);
+                    tma_load_3d(st + C::OFF_VZ, &P.tm[6], x0, y0, k + RZ, bar);
+                    tma_load_3d(st + C::OFF_OP, &P.tm[7], x0, y0, k, bar);
+                    tma_load_3d(st + C::OFF_OQ, &P.tm[8], x0, y0, k, bar);
+                    bulk_load(st + C::OFF_ZR, A.zrow + (size_t)k * C::ZROW, C::ZROW * ES, bar);
+                }
+                if (++stage == ST) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    // consumers: 16 x TY threads, 4 consecutive x points each
+    const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
+    const int sidx = tg * TX + 4 * tx;   // this thread's first point in an interior box
+    T *s1buf = reinterpret_cast<T *>(smem + C::OFF_S1);
+    int par = 0;
+    for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+        int x0, y0, kb, ke;
+        adj_item<TY>(P, item, x0, y0, kb, ke);
+        const int xg = x0 + 4 * tx, yl = y0 + tg;
+        const bool own = xg < A.nx && yl < A.nyl;
+        const T gy = yl < A.nyl ? A.gy[yl] : T(0);
+        const V4<T> gx4 = ldv<4>(A.gx + xg);
+        T q[NQ][4];   // slot (u + j) % NQ holds s2 of plane k - Rz + j
+        auto push_s2 = [&](const T *st, T (&v)[4]) {
+            const V4<T> ip = ldv<4>(st + C::OFF_IP / ES + sidx), iq = ldv<4>(st + C::OFF_IQ / ES + sidx);
+            const V4<T> vz = ldv<4>(st + C::OFF_VZ / ES + sidx);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = vz[c] * (ip[c] + iq[c]);
+        };
+#pragma unroll
+        for (int t = 0; t < 2 * RZ; ++t) {
+            mbar_wait(&full[stage], phase);
+            push_s2(reinterpret_cast<const T *>(smem + stage * C::STAGE), q[SHIFT ? t + 1 : t]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == ST) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        // plane k; slot (u + j) % NQ of the queue holds s2 of plane k - Rz + j
+        auto plane = [&](const int k, const int u) {
+            mbar_wait(&full[stage], phase);
+            const T *st = reinterpret_cast<const T *>(smem + stage * C::STAGE);
+            // s1 = fma(vx2, psi_p, vn2 * psi_q) over the whole box (apron included)
+            T *s1 = s1buf + par * (C::P_BYTES / ES);
+            par ^= 1;
+            for (int e = threadIdx.x; e < C::TE / 4; e += NCONS) {
+                const V4<T> a = ldv<4>(st + C::OFF_HP / ES + 4 * e), b = ldv<4>(st + C::OFF_HQ / ES + 4 * e);
+                const V4<T> x = ldv<4>(st + C::OFF_HX / ES + 4 * e), n = ldv<4>(st + C::OFF_HN / ES + 4 * e);
+                T v[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[c] = fma_x<T>(x[c], a[c], n[c] * b[c]);
+                stv(s1 + 4 * e, v);
+            }
+            push_s2(st, q[(u + 2 * RZ) % NQ]);   // s2 of plane k + Rz
+            const int ctr = (tg + R) * PW + RA + 4 * tx;
+            const V4<T> pc4 = ldv<4>(st + C::OFF_HP / ES + ctr), qc4 = ldv<4>(st + C::OFF_HQ / ES + ctr);
+            const V4<T> po4 = ldv<4>(st + C::OFF_OP / ES + sidx), qo4 = ldv<4>(st + C::OFF_OQ / ES + sidx);
+            const T *zr = st + C::OFF_ZR / ES;
+            // D^T(s2): ascending m over planes k + Rz - m, weights w^T[k][m]
+            T DT[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) {
+                const T w = zr[m];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) DT[c] = fma_x<T>(w, q[(u + 2 * RZ - m) % NQ][c], DT[c]);
+            }
+            const T gz = zr[NQ];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == ST) {
+                stage = 0;
+                phase ^= 1;
+            }
+            named_bar_sync(1, NCONS);   // the s1 tile of plane k is complete
+            // L(s1), canonical pairing (x pair + y pair)
+            const T *base = s1 + tg * PW + 4 * tx;   // smem row tg = tile row tg - R
+            const T *prow = base + R * PW;
+            auto wx = [&](int i) { return ldv<4>(prow + 4 * (i / 4))[i % 4]; };
+            T L[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) L[c] = A.cxy[0] * wx(RA + c);
+#pragma unroll
+            for (int l = 1; l <= R; ++l) {
+                const V4<T> yp = ldv<4>(base + (R + l) * PW + RA), ym = ldv<4>(base + (R - l) * PW + RA);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    L[c] = fma_x<T>(A.cxy[l], (wx(RA + c + l) + wx(RA + c - l)) + (yp[c] + ym[c]), L[c]);
+            }
+            if (!own) return;
+            T pn[4], qn[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                T Fp = L[c], Fq = DT[c];
+                if constexpr (IO) {
+                    const int i = xg + c;
+                    if (A.inj_row != nullptr && i < A.nx) {
+                        const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, yl, i);
+                        if (e >= 0) {
+                            const T v = A.inj_row[A.inj_ent[e].y];
+                            if (A.inj_mask & 1) Fp = Fp + v;
+                            if (A.inj_mask & 2) Fq = Fq + v;
+                        }
+                    }
+                }
+                const T g = (gx4[c] * gy) * gz;
+                pn[c] = g * fma_x<T>(A.dt2, Fp, fma_x<T>(-g, po4[c], T(2) * pc4[c]));
+                qn[c] = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, qo4[c], T(2) * qc4[c]));
+            }
+            const int64_t a0 = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+            if (xg + 4 <= A.nx) {
+                stv(A.po + a0, pn);
+                stv(A.qo + a0, qn);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (xg + c < A.nx) {
+                        A.po[a0 + c] = pn[c];
+                        A.qo[a0 + c] = qn[c];
+                    }
+            }
+            if constexpr (IO) {
+                if (A.rec_row != nullptr) {   // receivers of psi^{m-1} (duplicates allowed: every entry)
+                    const long long rb = (long long)k * A.nyl + yl;
+                    const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
+                    for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
+                        const int c = A.rec_ent[e].x - xg;
+                        if (c < 0 || c >= 4) continue;
+                        T vp = pn[0], vq = qn[0];
+#pragma unroll
+                        for (int cc = 1; cc < 4; ++cc)
+                            if (c == cc) {
+                                vp = pn[cc];
+                                vq = qn[cc];
+                            }
+                        T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
+                        if (A.rec_mask & 1) *o++ = vp;
+                        if (A.rec_mask & 2) *o = vq;
+                    }
+                }
+            }
+        };
+        if constexpr (SHIFT) {   // deep queues: one loop body, the queue shifted by register moves
+            for (int k = kb; k < ke; ++k) {
+#pragma unroll
+                for (int m = 0; m < NQ - 1; ++m)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) q[m][c] = q[m + 1][c];
+                plane(k, 0);
+            }
+        } else {   // the queue index unrolled NQ times: no moves, NQ copies of the body
+            for (int kbase = kb; kbase < ke; kbase += NQ) {
+#pragma unroll
+                for (int u = 0; u < NQ; ++u) {
+                    if (kbase + u >= ke) break;
+                    plane(kbase + u, u);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- TMA two-pass form
+// Pass 1 (k_adj_s1): s1 = fma(vx2, psi_p, vn2 psi_q) over the slab, vectorised (20 B/pt fp32).
+// Pass 2 (k_adj_tma2): the forward kernel's shape with one halo'd box. Per plane k the producer
+// streams the halo'd s1 box, psi_p, psi_q, vz2 of plane k + Rz (the s2 queue front), psi^m and
+// psi^{m+1} of plane k and the transposed weight row; consumers (PX x points each) read
+// everything from the stage -- no shared-memory pass and no CTA barrier per plane. DRAM: s1,
+// psi^m (2), vz2, psi^{m+1} (2) read, psi^{m-1} (2) written = 32 B/pt fp32 (52 with pass 1).
+// y-slab groups take their neighbours' s1 rows in the halo rows (vti_group_step_adjoint).
 template <typename T>
-static vti_status adjoint_prep_t(vti_s *h)
+__global__ void k_adj_s1(const T *__restrict__ pp, const T *__restrict__ pq, const T *__restrict__ vx2,
+                         const T *__restrict__ vn2, T *__restrict__ s1, int nx4, int nyl, long long ys, long long zs)
+{
+    const int k = blockIdx.y, n = nyl * nx4;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int y = t / nx4, x = (t - y * nx4) * 4;
+        const int64_t a = (int64_t)y * ys + (int64_t)k * zs + x;
+        const V4<T> p = ldv<4>(pp + a), q = ldv<4>(pq + a), vx = ldv<4>(vx2 + a), vn = ldv<4>(vn2 + a);
+        T v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = fma_x<T>(vx[c], p[c], vn[c] * q[c]);
+        stv(s1 + a, v);
+    }
+}
+
+template <typename T, int R, int RZ, int TY, int ST, int PX, bool CH>
+struct AdjTma2Cfg {
+    static constexpr int ES = (int)sizeof(T);
+    static constexpr int RA = (R + 3) / 4 * 4;
+    static constexpr int PW = TX + 2 * RA, PH = TY + 2 * R, TE = PW * PH;
+    static constexpr int NQ = 2 * RZ + 1;
+    static constexpr int ZROW = ((NQ + 1 + 3) / 4) * 4;
+    static constexpr int P_BYTES = align128(TE * ES);
+    static constexpr int S_BYTES = TX * TY * ES;
+    static constexpr int OFF_S1 = 0, OFF_IP = P_BYTES, OFF_IQ = OFF_IP + S_BYTES, OFF_VZ = OFF_IQ + S_BYTES;
+    static constexpr int OFF_PC = OFF_VZ + S_BYTES, OFF_QC = OFF_PC + S_BYTES;
+    static constexpr int OFF_OP = OFF_QC + S_BYTES, OFF_OQ = OFF_OP + S_BYTES;
+    static constexpr int OFF_VX = OFF_OQ + S_BYTES, OFF_VN = OFF_VX + (CH ? S_BYTES : 0);   // CH only
+    static constexpr int OFF_ZR = OFF_VN + (CH ? S_BYTES : 0);
+    static constexpr int STAGE = align128(OFF_ZR + ZROW * ES);
+    static constexpr uint32_t FULL_TX = TE * ES + (CH ? 9 : 7) * S_BYTES + ZROW * ES;
+    static constexpr uint32_t PRIME_TX = 3 * S_BYTES;
+    static constexpr int OFF_BAR = ST * STAGE;
+    static constexpr int SMEM = OFF_BAR + 2 * ST * 8;
+    static constexpr int TPR = TX / PX;
+    static constexpr int NCONS = TY * TPR;
+    static constexpr int NT = NCONS + 32;
+    static_assert(PW % 4 == 0 && PW <= 256 && PH <= 256, "TMA box");
+    static_assert(NCONS % 32 == 0, "whole consumer warps");
+};
+
+template <typename T, int R, int RZ, int TY, int ST, int PX, bool IO, bool CH>
+__global__ void __launch_bounds__(AdjTma2Cfg<T, R, RZ, TY, ST, PX, CH>::NT, 1)
+    k_adj_tma2(const __grid_constant__ AdjTmaParams<T> P)
+{
+    using C = AdjTma2Cfg<T, R, RZ, TY, ST, PX, CH>;
+    using VP = Vec<T, PX>;
+    constexpr int NQ = C::NQ, RA = C::RA, PW = C::PW, ES = C::ES, NCONS = C::NCONS, TPR = C::TPR;
+    constexpr bool SHIFT = NQ > 9;   // i-cache: NQ unrolled copies of a deep body miss (ncu: no_instructions)
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
+    uint64_t *empty = full + ST;
+    const AdjParams<T> &A = P.A;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCONS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int i = 0; i < (CH ? 8 : 6); ++i) prefetch_tmap(&P.tm[i]);
+    }
+    __syncthreads();
+    int stage = 0;
+    uint32_t phase = 0;
+    if (warp == NCONS / 32) {   // producer
+        if (lane != 0) return;
+        for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+            int x0, y0, kb, ke;
+            adj_item<TY>(P, item, x0, y0, kb, ke);
+            const int nload = (ke - kb) + 2 * RZ;
+            for (int t = 0; t < nload; ++t) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t *st = smem + stage * C::STAGE;
+                uint64_t *bar = &full[stage];
+                if (t < 2 * RZ) {
+                    const int kk = kb - RZ + t;
+                    mbar_arrive_expect_tx(bar, C::PRIME_TX);
+                    tma_load_3d(st + C::OFF_IP, &P.tm[1], x0, y0, kk, bar);
+                    tma_load_3d(st + C::OFF_IQ, &P.tm[2], x0, y0, kk, bar);
+                    tma_load_3d(st + C::OFF_VZ, &P.tm[3], x0, y0, kk, bar);
+                } else {
+                    const int k = kb + t - 2 * RZ;
+                    mbar_arrive_expect_tx(bar, C::FULL_TX);
+                    tma_load_3d(st + C::OFF_S1, &P.tm[0], x0 - RA, y0, k, bar);   // halo'd: view row y0 = local y0 - R
+                    tma_load_3d(st + C::OFF_IP, &P.tm[1], x0, y0, k + RZ, bar);
+                    tma_load_3d(st + C::OFF_IQ, &P.tm[2], x0, y0, k + RZ, bar);
+                    tma_load_3d(st + C::OFF_VZ, &P.tm[3], x0, y0, k + RZ, bar);
+                    tma_load_3d(st + C::OFF_PC, &P.tm[1], x0, y0, k, bar);
+                    tma_load_3d(st + C::OFF_QC, &P.tm[2], x0, y0, k, bar);
+                    tma_load_3d(st + C::OFF_OP, &P.tm[4], x0, y0, k, bar);
+                    tma_load_3d(st + C::OFF_OQ, &P.tm[5], x0, y0, k, bar);
+                    if constexpr (CH) {
+                        tma_load_3d(st + C::OFF_VX, &P.tm[6], x0, y0, k, bar);
+                        tma_load_3d(st + C::OFF_VN, &P.tm[7], x0, y0, k, bar);
+                    }
+                    bulk_load(st + C::OFF_ZR, A.zrow + (size_t)k * C::ZROW, C::ZROW * ES, bar);
+                }
+                if (++stage == ST) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    const int tx = threadIdx.x % TPR, tg = threadIdx.x / TPR;
+    const int sidx = tg * TX + PX * tx;
+    for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+        int x0, y0, kb, ke;
+        adj_item<TY>(P, item, x0, y0, kb, ke);
+        const int xg = x0 + PX * tx, yl = y0 + tg;
+        const bool own = xg < A.nx && yl < A.nyl;
+        const T gy = yl < A.nyl ? A.gy[yl] : T(0);
+        const VP gxv = ldv<PX>(A.gx + xg);
+        T q[NQ][PX];
+        auto push_s2 = [&](const T *st, T (&v)[PX]) {
+            const VP ip = ldv<PX>(st + C::OFF_IP / ES + sidx), iq = ldv<PX>(st + C::OFF_IQ / ES + sidx);
+            const VP vz = ldv<PX>(st + C::OFF_VZ / ES + sidx);
+#pragma unroll
+            for (int c = 0; c < PX; ++c) v[c] = vz[c] * (ip[c] + iq[c]);
+        };
+#pragma unroll
+        for (int t = 0; t < 2 * RZ; ++t) {
+            mbar_wait(&full[stage], phase);
+            push_s2(reinterpret_cast<const T *>(smem + stage * C::STAGE), q[SHIFT ? t + 1 : t]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == ST) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        // plane k; slot (u + j) % NQ of the queue holds s2 of plane k - Rz + j
+        auto plane = [&](const int k, const int u) {
+            mbar_wait(&full[stage], phase);
+            const T *st = reinterpret_cast<const T *>(smem + stage * C::STAGE);
+            push_s2(st, q[(u + 2 * RZ) % NQ]);
+            const VP pcv = ldv<PX>(st + C::OFF_PC / ES + sidx), qcv = ldv<PX>(st + C::OFF_QC / ES + sidx);
+            const VP pov = ldv<PX>(st + C::OFF_OP / ES + sidx), qov = ldv<PX>(st + C::OFF_OQ / ES + sidx);
+            VP vxv, vnv;
+            if constexpr (CH) {
+                vxv = ldv<PX>(st + C::OFF_VX / ES + sidx);
+                vnv = ldv<PX>(st + C::OFF_VN / ES + sidx);
+            }
+            const T *zr = st + C::OFF_ZR / ES;
+            T DT[PX];
+#pragma unroll
+            for (int c = 0; c < PX; ++c) DT[c] = T(0);
+#pragma unroll
+            for (int m = 0; m < NQ; ++m) {
+                const T w = zr[m];
+#pragma unroll
+                for (int c = 0; c < PX; ++c) DT[c] = fma_x<T>(w, q[(u + 2 * RZ - m) % NQ][c], DT[c]);
+            }
+            const T gz = zr[NQ];
+            // L(s1) from the staged box, canonical pairing (x pair + y pair)
+            const T *base = st + C::OFF_S1 / ES + tg * PW + PX * tx;
+            const T *prow = base + R * PW;
+            auto wx = [&](int i) { return ldv<PX>(prow + PX * (i / PX))[i % PX]; };
+            T L[PX];
+#pragma unroll
+            for (int c = 0; c < PX; ++c) L[c] = A.cxy[0] * wx(RA + c);
+#pragma unroll
+            for (int l = 1; l <= R; ++l) {
+                const VP yp = ldv<PX>(base + (R + l) * PW + RA), ym = ldv<PX>(base + (R - l) * PW + RA);
+#pragma unroll
+                for (int c = 0; c < PX; ++c)
+                    L[c] = fma_x<T>(A.cxy[l], (wx(RA + c + l) + wx(RA + c - l)) + (yp[c] + ym[c]), L[c]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == ST) {
+                stage = 0;
+                phase ^= 1;
+            }
+            if (!own) return;
+            T pn[PX], qn[PX];
+#pragma unroll
+            for (int c = 0; c < PX; ++c) {
+                T Fp = L[c], Fq = DT[c];
+                if constexpr (IO) {
+                    const int i = xg + c;
+                    if (A.inj_row != nullptr && i < A.nx) {
+                        const int e = ps_lookup(A.inj_off, A.inj_ent, A.nyl, k, yl, i);
+                        if (e >= 0) {
+                            const T v = A.inj_row[A.inj_ent[e].y];
+                            if (A.inj_mask & 1) Fp = Fp + v;
+                            if (A.inj_mask & 2) Fq = Fq + v;
+                        }
+                    }
+                }
+                const T g = (gxv[c] * gy) * gz;
+                pn[c] = g * fma_x<T>(A.dt2, Fp, fma_x<T>(-g, pov[c], T(2) * pcv[c]));
+                qn[c] = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, qov[c], T(2) * qcv[c]));
+            }
+            const int64_t a0 = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
+            T s1n[PX];
+            if constexpr (CH) {   // the next step's s1 = fma(vx2, psi_p, vn2 * psi_q) of psi^{m-1}
+#pragma unroll
+                for (int c = 0; c < PX; ++c) s1n[c] = fma_x<T>(vxv[c], pn[c], vnv[c] * qn[c]);
+            }
+            if (xg + PX <= A.nx) {
+                stv(A.po + a0, pn);
+                stv(A.qo + a0, qn);
+                if constexpr (CH) stv(A.s1o + a0, s1n);
+            } else {
+#pragma unroll
+                for (int c = 0; c < PX; ++c)
+                    if (xg + c < A.nx) {
+                        A.po[a0 + c] = pn[c];
+                        A.qo[a0 + c] = qn[c];
+                        if constexpr (CH) A.s1o[a0 + c] = s1n[c];
+                    }
+            }
+            if constexpr (IO) {
+                if (A.rec_row != nullptr) {
+                    const long long rb = (long long)k * A.nyl + yl;
+                    const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
+                    for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
+                        const int c = A.rec_ent[e].x - xg;
+                        if (c < 0 || c >= PX) continue;
+                        T vp = pn[0], vq = qn[0];
+#pragma unroll
+                        for (int cc = 1; cc < PX; ++cc)
+                            if (c == cc) {
+                                vp = pn[cc];
+                                vq = qn[cc];
+                            }
+                        T *o = A.rec_row + (int64_t)A.rec_ent[e].y * nf;
+                        if (A.rec_mask & 1) *o++ = vp;
+                        if (A.rec_mask & 2) *o = vq;
+                    }
+                }
+            }
+        };
+        if constexpr (SHIFT) {   // deep queues: one loop body, the queue shifted by register moves
+            for (int k = kb; k < ke; ++k) {
+#pragma unroll
+                for (int m = 0; m < NQ - 1; ++m)
+#pragma unroll
+                    for (int c = 0; c < PX; ++c) q[m][c] = q[m + 1][c];
+                plane(k, 0);
+            }
+        } else {   // the queue index unrolled NQ times: no moves, NQ copies of the body
+            for (int kbase = kb; kbase < ke; kbase += NQ) {
+#pragma unroll
+                for (int u = 0; u < NQ; ++u) {
+                    if (kbase + u >= ke) break;
+                    plane(kbase + u, u);
+                }
+            }
+        }
+    }
+}
+
+// wT[k][m] = w^z[k+Rz-m][m] for planes inside the grid, else 0; wT[k][NQ] = gz[k]
+template <typename T>
+__global__ void k_adj_wt(const T *__restrict__ zrow, T *__restrict__ wt, int nz, int rz, int stride)
+{
+    const int NQ = 2 * rz + 1;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nz * stride; e += gridDim.x * blockDim.x) {
+        const int k = e / stride, m = e % stride;
+        T v = T(0);
+        if (m < NQ) {
+            const int kk = k + rz - m;
+            if (kk >= 0 && kk < nz) v = zrow[(size_t)kk * stride + m];
+        } else if (m == NQ) {
+            v = zrow[(size_t)k * stride + NQ];
+        }
+        wt[e] = v;
+    }
+}
+
+struct AdjTmaEntry {
+    int es, r, rz, form, ty, px, st;   // form 1: one-pass k_adj_tma; form 2: k_adj_s1 + k_adj_tma2; st: ring depth
+    const void *fn, *fn_io;        // form 2: the last step of a call (no s1 out)
+    int smem, threads, zrow;
+    const void *fn_ch, *fn_ch_io;  // form 2: chained steps (s1 of psi^{m-1} out)
+    int smem_ch;
+};
+
+template <typename T, int R, int RZ, int TY, int ST>
+constexpr AdjTmaEntry adj_tma1()
+{
+    using C = AdjTmaCfg<T, R, RZ, TY, ST>;
+    return {C::ES, R, RZ, 1, TY, 4, ST, (const void *)k_adj_tma<T, R, RZ, TY, ST, false>,
+            (const void *)k_adj_tma<T, R, RZ, TY, ST, true>, C::SMEM, C::NT, C::ZROW, nullptr, nullptr, 0};
+}
+
+template <typename T, int R, int RZ, int TY, int ST, int PX>
+constexpr AdjTmaEntry adj_tma2()
+{
+    using C = AdjTma2Cfg<T, R, RZ, TY, ST, PX, false>;
+    using CC = AdjTma2Cfg<T, R, RZ, TY, ST, PX, true>;
+    return {C::ES, R, RZ, 2, TY, PX, ST, (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, false>,
+            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, true, false>, C::SMEM, C::NT, C::ZROW,
+            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, true>,
+            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, true, true>, CC::SMEM};
+}
+
+// Per (precision, radii) the first eligible entry is the default. Env: VTI_ADJ_FORM=1|2 and
+// VTI_ADJ_TMA_TY / VTI_ADJ_TMA_PX restrict the choice; y-slab groups need form 2.
+static const AdjTmaEntry *find_adj_tma(int es, int r, int rz, bool group)
+{
+    static const AdjTmaEntry table[] = {
+        adj_tma1<float, 4, 4, 8, 3>(),        adj_tma1<float, 4, 4, 16, 2>(),    adj_tma2<float, 4, 4, 8, 4, 4>(),
+        adj_tma1<float, 8, 4, 16, 2>(),       adj_tma2<float, 8, 4, 8, 4, 4>(),
+        adj_tma1<float, 6, 6, 16, 2>(),       adj_tma2<float, 6, 6, 8, 4, 4>(),
+        adj_tma2<float, 12, 8, 8, 3, 4>(),    adj_tma2<float, 12, 8, 8, 4, 4>(),  adj_tma2<float, 12, 8, 8, 2, 4>(),
+        adj_tma1<float, 12, 8, 16, 2>(),
+        adj_tma2<double, 4, 4, 8, 2, 4>(),    adj_tma2<double, 4, 4, 8, 3, 4>(),  adj_tma1<double, 4, 4, 8, 2>(),
+        adj_tma2<double, 8, 4, 8, 2, 2>(),    adj_tma2<double, 6, 6, 8, 2, 2>(),
+        adj_tma2<double, 12, 8, 8, 2, 2>(),
+    };
+    static const int want_form = getenv("VTI_ADJ_FORM") ? atoi(getenv("VTI_ADJ_FORM")) : 0;
+    static const int want_ty = getenv("VTI_ADJ_TMA_TY") ? atoi(getenv("VTI_ADJ_TMA_TY")) : 0;
+    static const int want_px = getenv("VTI_ADJ_TMA_PX") ? atoi(getenv("VTI_ADJ_TMA_PX")) : 0;
+    static const int want_st = getenv("VTI_ADJ_TMA_ST") ? atoi(getenv("VTI_ADJ_TMA_ST")) : 0;
+    for (const AdjTmaEntry &e : table)
+        if (e.es == es && e.r == r && e.rz == rz && (!group || e.form == 2) && (!want_form || e.form == want_form) &&
+            (!want_ty || e.ty == want_ty) && (!want_px || e.px == want_px) && (!want_st || e.st == want_st))
+            return &e;
+    return nullptr;
+}
+
+static const AdjTmaEntry *adj_tma_of(const vti_s *h)
+{
+    static const bool on = !getenv("VTI_ADJ_TMA") || atoi(getenv("VTI_ADJ_TMA")) != 0;
+    if (!on) return nullptr;
+    return find_adj_tma(h->es, h->R, h->RZ, h->cfg.nranks > 1);
+}
+
+// builds the transposed weight rows (once) and the entry's tensor maps of both buffer parities
+static vti_status ensure_adj_tma(vti_s *h, const AdjTmaEntry *E, int &ctas)
+{
+    if (h->adj_tma < 0) return fail(h, VTI_E_CUDA, "adjoint TMA kernel setup failed earlier");
+    if (h->adj_tma == 0) {
+        h->adj_tma = -1;
+        if (E->zrow != h->K->zrow) return fail(h, VTI_E_CUDA, "adjoint z-row stride mismatch");
+        const size_t bytes = (size_t)h->cfg.nz * E->zrow * h->es;
+        cudaError_t e = cudaMalloc(&h->adj_wt, bytes);
+        if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+        h->device_bytes += (int64_t)bytes;
+        if (h->es == 8)
+            k_adj_wt<double><<<64, 256, 0, h->stream>>>((const double *)h->zrow, (double *)h->adj_wt, h->cfg.nz, h->RZ,
+                                                      E->zrow);
+        else
+            k_adj_wt<float><<<64, 256, 0, h->stream>>>((const float *)h->zrow, (float *)h->adj_wt, h->cfg.nz, h->RZ,
+                                                     E->zrow);
+        CU(h, cudaGetLastError());
+        const int RA = (h->R + 3) / 4 * 4, PW = TX + 2 * RA, PH = E->ty + 2 * h->R;
+        const CUtensorMapL2promotion hp = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        vti_status s;
+        for (int c = 0; c < 2; ++c) {
+            CUtensorMap *tm = h->adj_tm[c];
+            if (E->form == 1) {
+                void *halo[4] = {h->pbuf[c], h->qbuf[c], h->vx2, h->vn2};
+                for (int i = 0; i < 4; ++i)
+                    if ((s = encode(h, &tm[i], halo[i], h->rows, PW, PH, hp)) != VTI_OK) return s;
+                void *inter[5] = {h->p_int(c), h->q_int(c), h->in(h->vz2), h->p_int(1 - c), h->q_int(1 - c)};
+                for (int i = 0; i < 5; ++i)
+                    if ((s = encode(h, &tm[4 + i], inter[i], h->nyl, TX, E->ty)) != VTI_OK) return s;
+            } else {   // tm[0] (the s1 view) is taken from adj_tm_s1 at launch
+                void *inter[7] = {h->p_int(c),     h->q_int(c),   h->in(h->vz2), h->p_int(1 - c),
+                                  h->q_int(1 - c), h->in(h->vx2), h->in(h->vn2)};
+                for (int i = 0; i < 7; ++i)
+                    if ((s = encode(h, &tm[1 + i], inter[i], h->nyl, TX, E->ty)) != VTI_OK) return s;
+            }
+        }
+        if (E->form == 2)
+            for (int b = 0; b < 2; ++b)
+                if ((s = encode(h, &h->adj_tm_s1[b], h->adj_s[b], h->rows, PW, PH, hp)) != VTI_OK) return s;
+        int occ = 0;
+        for (const void *fn : {E->fn, E->fn_io})
+            CU(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, E->smem));
+        CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, E->fn, E->threads, E->smem));
+        if (occ < 1) return fail(h, VTI_E_CUDA, "adjoint TMA kernel cannot be resident (smem %d B)", E->smem);
+        h->adj_tma = occ * h->sms;   // the grid cap
+        if (E->fn_ch) {
+            for (const void *fn : {E->fn_ch, E->fn_ch_io})
+                CU(h, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, E->smem_ch));
+            CU(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, E->fn_ch, E->threads, E->smem_ch));
+            if (occ < 1) return fail(h, VTI_E_CUDA, "adjoint TMA kernel cannot be resident (smem %d B)", E->smem_ch);
+            h->adj_tma_ch = occ * h->sms;
+        }
+    }
+    ctas = h->adj_tma;
+    return VTI_OK;
+}
+
+// form 2: s1 of psi^m is in scratch buffer sb; chain: also write the next step's s1 into 1 - sb
+template <typename T>
+static vti_status launch_adj_tma(vti_s *h, const AdjTmaEntry *E, const AdjParams<T> &A, bool io, int sb, bool chain)
+{
+    int ctas = 0;
+    vti_status s = ensure_adj_tma(h, E, ctas);
+    if (s != VTI_OK) return s;
+    AdjTmaParams<T> P;
+    memcpy(P.tm, h->adj_tm[h->cur], sizeof(P.tm));
+    if (E->form == 2) P.tm[0] = h->adj_tm_s1[sb];
+    chain = chain && E->form == 2;
+    if (chain) ctas = h->adj_tma_ch;
+    P.A = A;
+    P.A.zrow = (const T *)h->adj_wt;
+    P.A.s1o = chain ? (T *)h->in(h->adj_s[1 - sb]) : nullptr;
+    P.ntx = (h->cfg.nx + TX - 1) / TX;
+    P.nty = (h->nyl + E->ty - 1) / E->ty;
+    const int tiles = P.ntx * P.nty;
+    static const int zenv = getenv("VTI_ADJ_ZCHUNK") ? atoi(getenv("VTI_ADJ_ZCHUNK")) : 0;
+    int nzc = std::max(1, std::min((h->cfg.nz + 31) / 32, (6 * ctas + tiles - 1) / tiles));
+    P.zchunk = zenv > 0 ? zenv : (h->cfg.nz + nzc - 1) / nzc;
+    nzc = (h->cfg.nz + P.zchunk - 1) / P.zchunk;
+    P.items = tiles * nzc;
+    const int grid = std::min(P.items, ctas);
+    void *args[] = {&P};
+    const void *fn = chain ? (io ? E->fn_ch_io : E->fn_ch) : (io ? E->fn_io : E->fn);
+    CU(h, cudaLaunchKernel(fn, dim3(grid), dim3(E->threads), args, chain ? E->smem_ch : E->smem, h->stream));
+    return VTI_OK;
+}
+
+// Which form. The TMA forms (above) when compiled for the handle's precision and radii; the
+// table's first entry per (precision, radii) is the measured best on one B200
+// (tools/adjoint_rate.py, profiles/r02/adjoint_tma_r02.txt, Gpoints/s):
+//   fp32: one-pass C2 (4,4) 172-174 (8-row tiles, 3 stages, 2 CTAs/SM), C3 (8,4) 139-141 and
+//         C5 (6,6) 135-136 (16-row tiles); chained two-pass N1 (12,8) 137 (one-pass: 29-54);
+//   fp64: chained two-pass C2 61, C3 60, C5 61, N1 56.
+// Before them, the cp.async forms: fp32 one-pass C2 78.1, C3 81.4, C5 82.2, N1 38.7; fp64
+// C2 36.9, C3 31.2, C5 34.1, N1 19.3 (two-pass at R_xy >= 8). With VTI_ADJ_TMA=0 those run:
+// y-slab groups the two-pass one, single slabs the one-pass one (VTI_ADJ_TWO_PASS=1/0 forces
+// either) except fp64 at R_xy >= 8.
+enum AdjForm { ADJ_FUSED = 0, ADJ_TWO_PASS = 1, ADJ_TMA1 = 2, ADJ_TMA2 = 3 };
+
+static AdjForm adj_form(const vti_s *h, const AdjTmaEntry **E = nullptr)
+{
+    const AdjTmaEntry *e = adj_tma_of(h);
+    if (E) *E = e;
+    if (e) return e->form == 1 ? ADJ_TMA1 : ADJ_TMA2;
+    if (h->cfg.nranks > 1) return ADJ_TWO_PASS;
+    static const int env = getenv("VTI_ADJ_TWO_PASS") ? atoi(getenv("VTI_ADJ_TWO_PASS")) : -1;
+    if (env >= 0) return env != 0 ? ADJ_TWO_PASS : ADJ_FUSED;
+    return h->es == 8 && h->R >= 8 ? ADJ_TWO_PASS : ADJ_FUSED;
+}
+
+// the scratch s1 (and, for the cp.async two-pass form, s2) is needed
+static bool adj_needs_s1(const vti_s *h)
+{
+    const AdjForm f = adj_form(h);
+    return f == ADJ_TWO_PASS || f == ADJ_TMA2;
+}
+
+// Two-pass forms, first launch (phase 1 of a step): s1 (k_adj_s1) or s1, s2 (k_adj_prep).
+template <typename T>
+static vti_status adjoint_prep_t(vti_s *h, int sb = 0)
 {
     const int c = h->cur;
-    k_adj_prep<T><<<4 * h->sms, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
-                                                   (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
-                                                   (const T *)h->in(h->vz2), (T *)h->in(h->adj_s[0]),
-                                                   (T *)h->in(h->adj_s[1]), h->cfg.nx, h->nyl, h->cfg.nz, h->ys,
-                                                   h->zs);
+    if (adj_form(h) == ADJ_TMA2) {
+        const int nx4 = (int)(h->nxp / 4), n = h->nyl * nx4;
+        const dim3 grid((unsigned)std::min((n + 255) / 256, 64), (unsigned)h->cfg.nz);
+        k_adj_s1<T><<<grid, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
+                                                (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
+                                                (T *)h->in(h->adj_s[sb]), nx4, h->nyl, h->ys, h->zs);
+    } else {
+        k_adj_prep<T><<<4 * h->sms, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
+                                                       (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
+                                                       (const T *)h->in(h->vz2), (T *)h->in(h->adj_s[0]),
+                                                       (T *)h->in(h->adj_s[1]), h->cfg.nx, h->nyl, h->cfg.nz,
+                                                       h->ys, h->zs);
+    }
     CU(h, cudaGetLastError());
     return VTI_OK;
 }
 
+// One adjoint step. Two-pass forms: prep = run the first pass (s1 of psi^m into scratch sb)
+// here; the chained TMA form (chain) also writes the next step's s1 into scratch 1 - sb.
 template <typename T>
-static vti_status adjoint_step_t(vti_s *h, bool prep = true)
+static vti_status adjoint_step_t(vti_s *h, bool prep = true, int sb = 0, bool chain = false)
 {
     const int c = h->cur, o = 1 - c;
     const int grid = 4 * h->sms;
-    const bool two_pass = adj_two_pass(h);
+    const AdjTmaEntry *E = nullptr;
+    const AdjForm form = adj_form(h, &E);
+    const bool two_pass = form == ADJ_TWO_PASS || form == ADJ_TMA2;
     T *s1 = nullptr, *s2 = nullptr;
     if (two_pass) {
-        s1 = (T *)h->in(h->adj_s[0]);
-        s2 = (T *)h->in(h->adj_s[1]);
+        s1 = (T *)h->in(h->adj_s[sb]);
+        if (form == ADJ_TWO_PASS) s2 = (T *)h->in(h->adj_s[1]);
         if (prep) {
-            vti_status st = adjoint_prep_t<T>(h);
+            vti_status st = adjoint_prep_t<T>(h, sb);
             if (st != VTI_OK) return st;
         }
     }
@@ -521,17 +1259,23 @@ static vti_status adjoint_step_t(vti_s *h, bool prep = true)
     // a local group's slab reads its neighbours' s1 rows, copied into its halo (vti_group_step_adjoint)
     A.y_lo = h->cfg.rank > 0 ? -h->R : 0;
     A.y_hi = h->cfg.rank < h->cfg.nranks - 1 ? h->nyl + h->R : h->nyl;
-    return two_pass ? launch_adj_step<T>(h, A, grid) : launch_adj_fused<T>(h, A);
+    const bool io = A.inj_row != nullptr || A.rec_row != nullptr;
+    switch (form) {
+    case ADJ_TMA1:
+    case ADJ_TMA2: return launch_adj_tma<T>(h, E, A, io, sb, chain);
+    case ADJ_TWO_PASS: return launch_adj_step<T>(h, A, grid);
+    default: return launch_adj_fused<T>(h, A);
+    }
 }
 
 }  // namespace
 
 static vti_status ensure_adj_scratch(vti_s *h)
 {
-    if (!adj_two_pass(h) || h->adj_s[0]) return VTI_OK;
-    // the two-pass form's coefficient-weighted fields s1, s2: the slab's geometry, zero halo
+    if (!adj_needs_s1(h) || h->adj_s[0]) return VTI_OK;
+    // the two-pass forms' coefficient-weighted fields s1 (and s2): the slab's geometry, zero halo
     const size_t bytes = h->total_elems() * h->es;
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 2; ++b) {   // s1, s2 (cp.async form) or two s1 buffers (chained TMA form)
         cudaError_t e = cudaMalloc(&h->adj_s[b], bytes);
         if (e != cudaSuccess) return fail(h, VTI_E_CUDA, "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
         CU(h, cudaMemsetAsync(h->adj_s[b], 0, bytes, h->stream));
@@ -543,16 +1287,27 @@ static vti_status ensure_adj_scratch(vti_s *h)
 // s1's R boundary rows of the neighbour on `side` (0: rank-1, its last rows; 1: rank+1, its
 // first rows) into this slab's halo rows, on this handle's stream (the copy engine reads the
 // neighbour's memory directly, any device).
-static vti_status copy_s1_halo(vti_s *h, const vti_s *nb, int side)
+static vti_status copy_s1_halo(vti_s *h, const vti_s *nb, int side, int sb = 0)
 {
-    const char *src = nb->in(nb->adj_s[0]) + (size_t)(side == 0 ? nb->nyl - nb->R : 0) * nb->ys * nb->es;
-    char *dst = h->in(h->adj_s[0]) + (side == 0 ? -(long long)h->R : (long long)h->nyl) * h->ys * h->es;
+    const char *src = nb->in(nb->adj_s[sb]) + (size_t)(side == 0 ? nb->nyl - nb->R : 0) * nb->ys * nb->es;
+    char *dst = h->in(h->adj_s[sb]) + (side == 0 ? -(long long)h->R : (long long)h->nyl) * h->ys * h->es;
     // [z][y][x]: R rows are contiguous within each plane; [y][z][x]: one block
     const size_t width = (size_t)h->R * h->ys * h->es;
     const size_t height = h->layout_zyx ? (size_t)h->cfg.nz : 1;
     const size_t spitch = h->layout_zyx ? (size_t)nb->zs * nb->es : width;
     const size_t dpitch = h->layout_zyx ? (size_t)h->zs * h->es : width;
     CU(h, cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, h->stream));
+    return VTI_OK;
+}
+
+// a group slab's bookkeeping after one adjoint step
+static vti_status adjoint_advance(vti_s *h)
+{
+    h->cur = 1 - h->cur;
+    h->n -= 1;
+    h->halo_dirty = true;   // p's halo rows are stale for a later forward step: re-publish then
+    if (h->rec_set.n > 0) h->rec_steps = std::min(h->rec_cap, h->rec_steps + 1);
+    if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0) return check_finite(h);
     return VTI_OK;
 }
 
@@ -574,6 +1329,46 @@ vti_status vti_group_step_adjoint(vti_t *hs, int32_t n, int32_t nsteps)
     for (int i = 0; i < n; ++i) {
         CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
         if ((s = ensure_adj_scratch(hs[i])) != VTI_OK) return s;
+    }
+    if (adj_form(hs[0]) == ADJ_TMA2) {
+        // chained TMA form: the first pass once, then per step (a) every slab's halo rows of the
+        // current s1 buffer from its neighbours (after their previous step wrote it: ev_edge),
+        // (b) the step, which also writes the next s1 into the other buffer -- only once the
+        // neighbours finished copying this slab's rows of that buffer a step earlier (ev_comm)
+        for (int i = 0; i < n; ++i) {
+            vti_s *h = hs[i];
+            CU(h, cudaSetDevice(h->cfg.device));
+            s = h->es == 8 ? adjoint_prep_t<double>(h, 0) : adjoint_prep_t<float>(h, 0);
+            if (s != VTI_OK) return s;
+            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+        }
+        int sb = 0;
+        for (int it = 0; it < nsteps; ++it) {
+            const bool chain = it + 1 < nsteps;
+            for (int i = 0; i < n; ++i) {
+                vti_s *h = hs[i];
+                CU(h, cudaSetDevice(h->cfg.device));
+                for (int side = 0; side < 2; ++side) {
+                    const int j = side == 0 ? i - 1 : i + 1;
+                    if (j < 0 || j >= n) continue;
+                    CU(h, cudaStreamWaitEvent(h->stream, hs[j]->ev_edge, 0));
+                    if ((s = copy_s1_halo(h, hs[j], side, sb)) != VTI_OK) return s;
+                }
+                CU(h, cudaEventRecord(h->ev_comm, h->stream));
+            }
+            for (int i = 0; i < n; ++i) {
+                vti_s *h = hs[i];
+                CU(h, cudaSetDevice(h->cfg.device));
+                if (i > 0) CU(h, cudaStreamWaitEvent(h->stream, hs[i - 1]->ev_comm, 0));
+                if (i < n - 1) CU(h, cudaStreamWaitEvent(h->stream, hs[i + 1]->ev_comm, 0));
+                s = h->es == 8 ? adjoint_step_t<double>(h, false, sb, chain) : adjoint_step_t<float>(h, false, sb, chain);
+                if (s != VTI_OK) return s;
+                CU(h, cudaEventRecord(h->ev_edge, h->stream));
+                if ((s = adjoint_advance(h)) != VTI_OK) return s;
+            }
+            sb ^= 1;
+        }
+        return VTI_OK;
     }
     for (int it = 0; it < nsteps; ++it) {
         // 1. s1, s2 of every slab; a slab's rows may be overwritten only once its neighbours
@@ -607,12 +1402,7 @@ vti_status vti_group_step_adjoint(vti_t *hs, int32_t n, int32_t nsteps)
             CU(h, cudaSetDevice(h->cfg.device));
             s = h->es == 8 ? adjoint_step_t<double>(h, false) : adjoint_step_t<float>(h, false);
             if (s != VTI_OK) return s;
-            h->cur = 1 - h->cur;
-            h->n -= 1;
-            h->halo_dirty = true;   // p's halo rows are stale for a later forward step: re-publish then
-            if (h->rec_set.n > 0) h->rec_steps = std::min(h->rec_cap, h->rec_steps + 1);
-            if (h->cfg.check_every > 0 && h->n % h->cfg.check_every == 0 && (s = check_finite(h)) != VTI_OK)
-                return s;
+            if ((s = adjoint_advance(h)) != VTI_OK) return s;
         }
     }
     return VTI_OK;
@@ -628,9 +1418,16 @@ vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
     CU(h, cudaSetDevice(h->cfg.device));
     vti_status s0 = ensure_adj_scratch(h);
     if (s0 != VTI_OK) return s0;
+    // the chained TMA two-pass form runs its first pass once per call: each step then writes the
+    // next step's s1 (scratch buffers alternate), the last one does not
+    static const bool chain_on = !getenv("VTI_ADJ_CHAIN") || atoi(getenv("VTI_ADJ_CHAIN")) != 0;
+    const bool chained = adj_form(h) == ADJ_TMA2 && chain_on;
+    int sb = 0;
     for (int it = 0; it < nsteps; ++it) {
-        vti_status s = h->es == 8 ? adjoint_step_t<double>(h) : adjoint_step_t<float>(h);
+        const bool prep = !chained || it == 0, chain = chained && it + 1 < nsteps;
+        vti_status s = h->es == 8 ? adjoint_step_t<double>(h, prep, sb, chain) : adjoint_step_t<float>(h, prep, sb, chain);
         if (s != VTI_OK) return s;
+        if (chain) sb ^= 1;
         h->cur = 1 - h->cur;
         h->n -= 1;   // the adjoint runs backward in time
         if (h->rec_set.n > 0) h->rec_steps = std::min(h->rec_cap, h->rec_steps + 1);

@@ -162,6 +162,13 @@ struct vti_s {
     int64_t inj_t_first = 0;
     long long *dyn = nullptr;                 // device: graph-replay header {inj row, rec row, dir}
     void *adj_s[2] = {nullptr, nullptr};      // vti_step_adjoint scratch: s1, s2 (vti_adjoint.cu)
+    // the TMA adjoint kernel (vti_adjoint.cu): transposed z-weight rows [nz][zrow] and, per buffer
+    // parity c of psi^m, its 9 tensor maps; adj_tma = 0 until built, -1 if setup failed, else the
+    // kernel's grid cap (resident CTAs)
+    void *adj_wt = nullptr;
+    CUtensorMap adj_tm[2][9];
+    CUtensorMap adj_tm_s1[2];                 // halo'd views of the two s1 scratch buffers (two-pass TMA form)
+    int adj_tma = 0, adj_tma_ch = 0;          // grid caps of the plain and the chained kernel
     bool io_active() const { return (rec_set.n > 0 && rec_cap > 0) || inj_set.n > 0; }
 
     size_t total_elems() const { return (size_t)cfg.nz * rows * nxp; }
@@ -194,7 +201,10 @@ void choose_schedule(vti_s *h);                 // z-chunks and CTA caps of the 
 // vti_runtime.cu
 vti_status launch_edge(vti_s *h);               // tile rows the neighbours receive (PEER kernel when connected)
 vti_status launch_interior(vti_s *h);
-void advance_records(vti_s *h, int steps);      // receiver rows written by `steps` steps (fused in the kernel)
+void advance_records(vti_s *h, int steps);
+// 3-D tensor map over (x, y, z) of an array with this handle's strides: rows of the view, box bx x by x bz
+vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx, int by,
+                  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B, int bz = 1);      // receiver rows written by `steps` steps (fused in the kernel)
 vti_status prepare_io(vti_s *h);                // an IO-capable step kernel while a point set is active
 vti_status check_finite(vti_s *h);              // check_every: INSTABILITY on a non-finite value
 

@@ -208,8 +208,8 @@ static bool is_device_ptr(const void *p)
 }
 
 // 3-D tensor map over (x, y, z) of an array with this handle's strides.
-static vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx, int by,
-                         CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B, int bz = 1)
+vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx, int by, CUtensorMapL2promotion promo,
+                  int bz)
 {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(h, VTI_E_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -312,6 +312,7 @@ vti_status vti_destroy(vti_t h)
     cudaFree(h->s_multi);
     cudaFree(h->adj_s[0]);
     cudaFree(h->adj_s[1]);
+    cudaFree(h->adj_wt);
     for (int z = 0; z < 2; ++z)
         for (int b = 0; b < 2; ++b)
             if (h->gexec[z][b]) cudaGraphExecDestroy(h->gexec[z][b]);

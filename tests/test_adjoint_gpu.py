@@ -62,6 +62,24 @@ def test_adjoint_matches_oracle(r, rz, prec):
     assert np.array_equal(traces, o[4])
 
 
+@pytest.mark.parametrize("r,rz,prec", [(4, 4, 32), (8, 4, 32), (6, 6, 32), (12, 8, 32),
+                                        (4, 4, 64), (8, 4, 64), (6, 6, 64), (12, 8, 64)])
+def test_adjoint_no_points_matches_oracle(r, rz, prec):
+    """The kernel without point sets, on a grid of 3 x tiles (ragged), ragged tile rows and
+    several z-chunks, from a damped random state: bitwise."""
+    cfg, wxy, wz, dt, model, st, dtype = setup(r, rz, prec, shape=(150, 37, 2 * rz + 60))
+    m0, K = 9, 5
+    with handle(cfg, dt, wxy, wz, prec) as v:
+        v.set_model(*model)
+        v.set_fields(*st, time_index=m0)
+        v.step_adjoint(K)
+        g = v.get_fields(0) + v.get_fields(1)
+    o = oracle.adjoint_ex(oracle.params(cfg, dt, src=None), wxy, wz, *model, st, m0=m0, nsteps=K, dtype=dtype)
+    for f, (a, b) in enumerate(zip(g, o[:4])):
+        assert np.abs(b).max() > 0
+        assert np.array_equal(a, b), f"field {f}: max |diff| {np.abs(a - b).max():.3e}"
+
+
 def test_library_dot_product_identity():
     """fp64, damped: the library's K forward steps and K adjoint steps satisfy
     <u^K, psi^K / g> - <u^{K-1}, g psi^{K+1}> = <u^0, psi^0 / g> - <u^{-1}, g psi^1>."""

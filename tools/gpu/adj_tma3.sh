@@ -1,0 +1,16 @@
+#!/bin/bash
+# Chained TMA two-pass adjoint: parity, then rates per config and form.
+mkdir -p gpurun_out
+O=gpurun_out/adj_tma3.log
+: > $O
+timeout 900 python -m pytest tests/test_adjoint_gpu.py -q -x >> $O 2>&1; echo "pytest rc=$?" >> $O
+r() { echo "[$*]" >> $O; env "$@" timeout 300 python tools/adjoint_rate.py $ARGS 2>&1 | grep -o '"adjoint_gpoints_s": [0-9.]*' >> $O; }
+ARGS="--config C2"; r X=C2 VTI_ADJ_FORM=2
+ARGS="--config C3"; r X=C3 VTI_ADJ_FORM=2; r X=C3
+ARGS="--config C5"; r X=C5 VTI_ADJ_FORM=2; r X=C5
+ARGS="--config N1"; r X=N1
+for c in C2 C3 C5 N1; do
+  ARGS="--config $c --precision 64"; r X=$c-f64
+done
+ARGS="--config C2 --precision 64"; r X=C2-f64 VTI_ADJ_FORM=2 VTI_ADJ_TMA_PX=2; r X=C2-f64-S3 VTI_ADJ_FORM=2 VTI_ADJ_TMA_PX=4 VTI_ADJ_STAGES=3
+echo done >> $O
