@@ -770,8 +770,8 @@ struct AdjTma2Cfg {
     static_assert(NCONS % 32 == 0, "whole consumer warps");
 };
 
-template <typename T, int R, int RZ, int TY, int ST, int PX, bool IO, bool CH>
-__global__ void __launch_bounds__(AdjTma2Cfg<T, R, RZ, TY, ST, PX, CH>::NT, 1)
+template <typename T, int R, int RZ, int TY, int ST, int PX, bool IO, bool CH, int MINB>
+__global__ void __launch_bounds__(AdjTma2Cfg<T, R, RZ, TY, ST, PX, CH>::NT, MINB)
     k_adj_tma2(const __grid_constant__ AdjTmaParams<T> P)
 {
     using C = AdjTma2Cfg<T, R, RZ, TY, ST, PX, CH>;
@@ -1006,7 +1006,8 @@ __global__ void k_adj_wt(const T *__restrict__ zrow, T *__restrict__ wt, int nz,
 }
 
 struct AdjTmaEntry {
-    int es, r, rz, form, ty, px, st;   // form 1: one-pass k_adj_tma; form 2: k_adj_s1 + k_adj_tma2; st: ring depth
+    int es, r, rz, form, ty, px, st, minb;   // form 1: one-pass k_adj_tma; form 2: k_adj_s1 + k_adj_tma2;
+                                             // st: ring depth; minb: __launch_bounds__ CTAs per SM
     const void *fn, *fn_io;        // form 2: the last step of a call (no s1 out)
     int smem, threads, zrow;
     const void *fn_ch, *fn_ch_io;  // form 2: chained steps (s1 of psi^{m-1} out)
@@ -1017,19 +1018,19 @@ template <typename T, int R, int RZ, int TY, int ST>
 constexpr AdjTmaEntry adj_tma1()
 {
     using C = AdjTmaCfg<T, R, RZ, TY, ST>;
-    return {C::ES, R, RZ, 1, TY, 4, ST, (const void *)k_adj_tma<T, R, RZ, TY, ST, false>,
+    return {C::ES, R, RZ, 1, TY, 4, ST, 1, (const void *)k_adj_tma<T, R, RZ, TY, ST, false>,
             (const void *)k_adj_tma<T, R, RZ, TY, ST, true>, C::SMEM, C::NT, C::ZROW, nullptr, nullptr, 0};
 }
 
-template <typename T, int R, int RZ, int TY, int ST, int PX>
+template <typename T, int R, int RZ, int TY, int ST, int PX, int MINB = 1>
 constexpr AdjTmaEntry adj_tma2()
 {
     using C = AdjTma2Cfg<T, R, RZ, TY, ST, PX, false>;
     using CC = AdjTma2Cfg<T, R, RZ, TY, ST, PX, true>;
-    return {C::ES, R, RZ, 2, TY, PX, ST, (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, false>,
-            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, true, false>, C::SMEM, C::NT, C::ZROW,
-            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, true>,
-            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, true, true>, CC::SMEM};
+    return {C::ES, R, RZ, 2, TY, PX, ST, MINB, (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, false, MINB>,
+            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, true, false, MINB>, C::SMEM, C::NT, C::ZROW,
+            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, true, MINB>,
+            (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, true, true, MINB>, CC::SMEM};
 }
 
 // Per (precision, radii) the first eligible entry is the default. Env: VTI_ADJ_FORM=1|2 and
@@ -1040,19 +1041,21 @@ static const AdjTmaEntry *find_adj_tma(int es, int r, int rz, bool group)
         adj_tma1<float, 4, 4, 8, 3>(),        adj_tma1<float, 4, 4, 16, 2>(),    adj_tma2<float, 4, 4, 8, 4, 4>(),
         adj_tma1<float, 8, 4, 16, 2>(),       adj_tma2<float, 8, 4, 8, 4, 4>(),
         adj_tma1<float, 6, 6, 16, 2>(),       adj_tma2<float, 6, 6, 8, 4, 4>(),
-        adj_tma2<float, 12, 8, 8, 3, 4>(),    adj_tma2<float, 12, 8, 8, 4, 4>(),  adj_tma2<float, 12, 8, 8, 2, 4>(),
-        adj_tma1<float, 12, 8, 16, 2>(),
-        adj_tma2<double, 4, 4, 8, 2, 4>(),    adj_tma2<double, 4, 4, 8, 3, 4>(),  adj_tma1<double, 4, 4, 8, 2>(),
-        adj_tma2<double, 8, 4, 8, 2, 2>(),    adj_tma2<double, 6, 6, 8, 2, 2>(),
+        adj_tma2<float, 12, 8, 8, 3, 4>(),    adj_tma2<float, 12, 8, 8, 4, 4>(), adj_tma1<float, 12, 8, 16, 2>(),
+        adj_tma2<double, 4, 4, 8, 3, 4>(),    adj_tma2<double, 4, 4, 8, 2, 4>(), adj_tma1<double, 4, 4, 8, 2>(),
+        adj_tma2<double, 8, 4, 8, 3, 4>(),    adj_tma2<double, 8, 4, 8, 2, 2>(),
+        adj_tma2<double, 6, 6, 8, 3, 4>(),    adj_tma2<double, 6, 6, 8, 2, 2>(),
         adj_tma2<double, 12, 8, 8, 2, 2>(),
     };
     static const int want_form = getenv("VTI_ADJ_FORM") ? atoi(getenv("VTI_ADJ_FORM")) : 0;
     static const int want_ty = getenv("VTI_ADJ_TMA_TY") ? atoi(getenv("VTI_ADJ_TMA_TY")) : 0;
     static const int want_px = getenv("VTI_ADJ_TMA_PX") ? atoi(getenv("VTI_ADJ_TMA_PX")) : 0;
     static const int want_st = getenv("VTI_ADJ_TMA_ST") ? atoi(getenv("VTI_ADJ_TMA_ST")) : 0;
+    static const int want_mb = getenv("VTI_ADJ_TMA_MINB") ? atoi(getenv("VTI_ADJ_TMA_MINB")) : 0;
     for (const AdjTmaEntry &e : table)
         if (e.es == es && e.r == r && e.rz == rz && (!group || e.form == 2) && (!want_form || e.form == want_form) &&
-            (!want_ty || e.ty == want_ty) && (!want_px || e.px == want_px) && (!want_st || e.st == want_st))
+            (!want_ty || e.ty == want_ty) && (!want_px || e.px == want_px) && (!want_st || e.st == want_st) &&
+            (!want_mb || e.minb == want_mb))
             return &e;
     return nullptr;
 }
@@ -1157,7 +1160,8 @@ static vti_status launch_adj_tma(vti_s *h, const AdjTmaEntry *E, const AdjParams
 // (tools/adjoint_rate.py, profiles/r02/adjoint_tma_r02.txt, Gpoints/s):
 //   fp32: one-pass C2 (4,4) 172-174 (8-row tiles, 3 stages, 2 CTAs/SM), C3 (8,4) 139-141 and
 //         C5 (6,6) 135-136 (16-row tiles); chained two-pass N1 (12,8) 137 (one-pass: 29-54);
-//   fp64: chained two-pass C2 61, C3 60, C5 61, N1 56.
+//   fp64: chained two-pass, 4 x points per thread and 3 stages: C2 72, C3 63, C5 66.5; 2 x points
+//         per thread (the (12,8) boxes need 2 stages to fit): N1 56.
 // Before them, the cp.async forms: fp32 one-pass C2 78.1, C3 81.4, C5 82.2, N1 38.7; fp64
 // C2 36.9, C3 31.2, C5 34.1, N1 19.3 (two-pass at R_xy >= 8). With VTI_ADJ_TMA=0 those run:
 // y-slab groups the two-pass one, single slabs the one-pass one (VTI_ADJ_TWO_PASS=1/0 forces
