@@ -307,17 +307,23 @@ vti_status vti_reverse(vti_t h);
  * by one. Adjoint sources are injected traces (vti_set_injection, row = m - t_first, added
  * after the operator); receivers (vti_set_receivers) record psi^{m-1}; the Ricker source of
  * vti_add_source is not applied. Then <M^K X, Y> = <X, (M^T)^K Y> (the dot-product test of
- * tests/test_adjoint_gpu.py). One launch per step (the coefficient products formed in the
- * stencil kernel), or two for fp64 at R_xy >= 8 (products, then stencils; env
- * VTI_ADJ_TWO_PASS forces either); single-slab handles (y-slabs: vti_group_step_adjoint). Bitwise equal to the oracle's
- * vto_adjoint_ex. Errors: STATE (model unset, nranks > 1), PARAM, CUDA, INSTABILITY.
+ * tests/test_adjoint_gpu.py). Kernels (csrc/vti_adjoint.cu): a TMA one-pass form (the coefficient
+ * products formed in the stencil kernel) or a chained two-pass form (s1 = vx2 psi_p + vn2 psi_q
+ * written once per call, then each step's kernel also writes the next step's s1), whichever
+ * measured faster for the precision and radii. nranks > 1, one process per slab: handles created
+ * with an NCCL id; the chained two-pass form with each step's s1 boundary rows exchanged over
+ * NCCL (pack, send/recv, unpack); every rank calls it with the same nsteps. Local groups:
+ * vti_group_step_adjoint. Bitwise equal to the oracle's vto_adjoint_ex. Errors: STATE (model
+ * unset; a local-group handle; nranks > 1 without the NCCL transport), UNSUPPORTED (nranks > 1
+ * and no two-pass kernel for the radii), PARAM, CUDA, COMM, INSTABILITY.
  */
 vti_status vti_step_adjoint(vti_t h, int32_t nsteps);
 
 /* The adjoint step for a local group of y-slab handles (created as for vti_group_step, any
- * devices): per step every slab forms s1 / s2, copies its neighbours' R_xy boundary rows of s1
- * into its halo, then runs the stencils; results are bitwise those of one slab. Errors: PARAM,
- * STATE, CUDA. */
+ * devices): the chained two-pass form, each slab's R_xy boundary rows of s1 exchanged between
+ * steps with the NCCL path's pack / copy / unpack sequence (copies between the slabs' send and
+ * receive buffers standing in for send/recv); results are bitwise those of one slab. Errors:
+ * PARAM, STATE, CUDA. */
 vti_status vti_group_step_adjoint(vti_t *hs, int32_t n, int32_t nsteps);
 
 /* +1 (forward) or -1 (after an odd number of vti_reverse calls). */

@@ -1335,41 +1335,31 @@ vti_status vti_group_step_adjoint(vti_t *hs, int32_t n, int32_t nsteps)
         if ((s = ensure_adj_scratch(hs[i])) != VTI_OK) return s;
     }
     if (adj_form(hs[0]) == ADJ_TMA2) {
-        // chained TMA form: the first pass once, then per step (a) every slab's halo rows of the
-        // current s1 buffer from its neighbours (after their previous step wrote it: ev_edge),
-        // (b) the step, which also writes the next s1 into the other buffer -- only once the
-        // neighbours finished copying this slab's rows of that buffer a step earlier (ev_comm)
+        // chained TMA form: the first pass once, its s1 halo rows exchanged (pack, copies between
+        // the slabs' send / recv buffers, unpack: the NCCL path's sequence, vti_transport.cu);
+        // then per step the kernel, which also writes the next s1 into the other buffer, and
+        // the exchange of that buffer's rows
+        std::vector<void *> bufs(n);
         for (int i = 0; i < n; ++i) {
             vti_s *h = hs[i];
             CU(h, cudaSetDevice(h->cfg.device));
             s = h->es == 8 ? adjoint_prep_t<double>(h, 0) : adjoint_prep_t<float>(h, 0);
             if (s != VTI_OK) return s;
-            CU(h, cudaEventRecord(h->ev_edge, h->stream));
+            bufs[i] = h->adj_s[0];
         }
+        if ((s = rows_exchange(hs, n, bufs.data(), false)) != VTI_OK) return s;
         int sb = 0;
         for (int it = 0; it < nsteps; ++it) {
             const bool chain = it + 1 < nsteps;
             for (int i = 0; i < n; ++i) {
                 vti_s *h = hs[i];
                 CU(h, cudaSetDevice(h->cfg.device));
-                for (int side = 0; side < 2; ++side) {
-                    const int j = side == 0 ? i - 1 : i + 1;
-                    if (j < 0 || j >= n) continue;
-                    CU(h, cudaStreamWaitEvent(h->stream, hs[j]->ev_edge, 0));
-                    if ((s = copy_s1_halo(h, hs[j], side, sb)) != VTI_OK) return s;
-                }
-                CU(h, cudaEventRecord(h->ev_comm, h->stream));
-            }
-            for (int i = 0; i < n; ++i) {
-                vti_s *h = hs[i];
-                CU(h, cudaSetDevice(h->cfg.device));
-                if (i > 0) CU(h, cudaStreamWaitEvent(h->stream, hs[i - 1]->ev_comm, 0));
-                if (i < n - 1) CU(h, cudaStreamWaitEvent(h->stream, hs[i + 1]->ev_comm, 0));
                 s = h->es == 8 ? adjoint_step_t<double>(h, false, sb, chain) : adjoint_step_t<float>(h, false, sb, chain);
                 if (s != VTI_OK) return s;
-                CU(h, cudaEventRecord(h->ev_edge, h->stream));
                 if ((s = adjoint_advance(h)) != VTI_OK) return s;
+                bufs[i] = h->adj_s[1 - sb];
             }
+            if (chain && (s = rows_exchange(hs, n, bufs.data(), false)) != VTI_OK) return s;
             sb ^= 1;
         }
         return VTI_OK;
@@ -1417,8 +1407,15 @@ vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
     if (!h) return VTI_E_PARAM;
     if (nsteps < 0) return fail(h, VTI_E_PARAM, "nsteps < 0");
     if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
-    if (h->cfg.nranks != 1)
-        return fail(h, VTI_E_STATE, "vti_step_adjoint is single-slab only; y-slabs: vti_group_step_adjoint");
+    // y-slabs, one process per slab: the chained TMA form with the s1 rows over NCCL
+    const bool mp = h->cfg.nranks > 1;
+    if (mp && h->group_mode)
+        return fail(h, VTI_E_STATE, "a local group's slabs step together: vti_group_step_adjoint");
+    if (mp && !h->comm_nccl)
+        return fail(h, VTI_E_STATE, "the multi-process adjoint exchanges s1 rows over NCCL: create the handles "
+                                    "with an NCCL id (the peer transport carries p only)");
+    if (mp && adj_form(h) != ADJ_TMA2)
+        return fail(h, VTI_E_UNSUPPORTED, "no two-pass TMA adjoint kernel for this precision and radius pair");
     CU(h, cudaSetDevice(h->cfg.device));
     vti_status s0 = ensure_adj_scratch(h);
     if (s0 != VTI_OK) return s0;
@@ -1427,10 +1424,22 @@ vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
     static const bool chain_on = !getenv("VTI_ADJ_CHAIN") || atoi(getenv("VTI_ADJ_CHAIN")) != 0;
     const bool chained = adj_form(h) == ADJ_TMA2 && chain_on;
     int sb = 0;
+    vti_s *const hv[1] = {h};
     for (int it = 0; it < nsteps; ++it) {
         const bool prep = !chained || it == 0, chain = chained && it + 1 < nsteps;
-        vti_status s = h->es == 8 ? adjoint_step_t<double>(h, prep, sb, chain) : adjoint_step_t<float>(h, prep, sb, chain);
+        vti_status s;
+        if (mp && prep) {   // s1 of the state the caller left, then its halo rows
+            if ((s = h->es == 8 ? adjoint_prep_t<double>(h, sb) : adjoint_prep_t<float>(h, sb)) != VTI_OK) return s;
+            void *b0 = h->adj_s[sb];
+            if ((s = rows_exchange(hv, 1, &b0, true)) != VTI_OK) return s;
+        }
+        s = h->es == 8 ? adjoint_step_t<double>(h, prep && !mp, sb, chain) : adjoint_step_t<float>(h, prep && !mp, sb, chain);
         if (s != VTI_OK) return s;
+        if (mp) h->halo_dirty = true;   // p's halo rows are stale for a later forward step
+        if (mp && chain) {
+            void *b1 = h->adj_s[1 - sb];
+            if ((s = rows_exchange(hv, 1, &b1, true)) != VTI_OK) return s;
+        }
         if (chain) sb ^= 1;
         h->cur = 1 - h->cur;
         h->n -= 1;   // the adjoint runs backward in time

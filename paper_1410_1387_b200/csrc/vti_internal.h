@@ -201,15 +201,18 @@ void choose_schedule(vti_s *h);                 // z-chunks and CTA caps of the 
 // vti_runtime.cu
 vti_status launch_edge(vti_s *h);               // tile rows the neighbours receive (PEER kernel when connected)
 vti_status launch_interior(vti_s *h);
-void advance_records(vti_s *h, int steps);
+void advance_records(vti_s *h, int steps);      // receiver rows written by `steps` steps (fused in the kernel)
 // 3-D tensor map over (x, y, z) of an array with this handle's strides: rows of the view, box bx x by x bz
 vti_status encode(vti_s *h, CUtensorMap *tm, void *base, int rows, int bx, int by,
-                  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B, int bz = 1);      // receiver rows written by `steps` steps (fused in the kernel)
+                  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B, int bz = 1);
 vti_status prepare_io(vti_s *h);                // an IO-capable step kernel while a point set is active
 vti_status check_finite(vti_s *h);              // check_every: INSTABILITY on a non-finite value
 
 // vti_transport.cu
 vti_status pack_send(vti_s *h, int b);          // NCCL: boundary rows of buffer b -> send buffers (main stream)
+// R boundary rows of halo'd slab arrays bufs[i] into the neighbours' halo rows: NCCL (one
+// handle of a multi-process job) or copies between a local group's send / recv buffers
+vti_status rows_exchange(vti_s *const *hs, int n, void *const *bufs, bool nccl_path);
 vti_status exchange_nccl(vti_s *h, int b);      // NCCL: send/recv + unpack on the comm stream, records ev_comm
 vti_status peer_pre_step(vti_s *h);             // peer: wait for the halo this step reads
 vti_status peer_post_edge(vti_s *h);            // peer: after the edge launch, ACK + DATA to the neighbours

@@ -132,21 +132,23 @@ vti_status pack_send(vti_s *h, int b)
     return VTI_OK;
 }
 
-// On the comm stream: unpack rbuf[0] (from rank-1) and rbuf[1] (from rank+1) into the halo rows of buffer b.
-static vti_status unpack_recv(vti_s *h, int b)
+// On the comm stream: unpack rbuf[0] (from rank-1) and rbuf[1] (from rank+1) into the halo rows
+// of the halo'd slab array buf (p: pbuf[b]; the adjoint's s1).
+static vti_status unpack_recv_buf(vti_s *h, void *buf)
 {
     const int r = h->cfg.rank, nr = h->cfg.nranks;
-    if (r > 0) unpack(h, h->rbuf[0], h->pbuf[b], 0, h->comm);
-    if (r < nr - 1) unpack(h, h->rbuf[1], h->pbuf[b], h->nyl + h->R, h->comm);
+    if (r > 0) unpack(h, h->rbuf[0], buf, 0, h->comm);
+    if (r < nr - 1) unpack(h, h->rbuf[1], buf, h->nyl + h->R, h->comm);
     CU(h, cudaGetLastError());
     return VTI_OK;
 }
+static vti_status unpack_recv(vti_s *h, int b) { return unpack_recv_buf(h, h->pbuf[b]); }
 
 // Staged local-group transport (vti_group_step_staged): the NCCL branch of vti_step for
 // handle i of a local group, with device copies from the neighbours' packed send buffers
 // standing in for ncclSend/ncclRecv. Comm stream: after this rank's and the neighbours'
 // ev_edge (their packs of buffer b), copy, unpack into the halo rows, record ev_comm.
-static vti_status exchange_staged(vti_s *const *hs, int n, int i, int b)
+static vti_status exchange_staged_buf(vti_s *const *hs, int n, int i, void *buf)
 {
     vti_s *h = hs[i];
     const size_t bytes = halo_elems(h) * h->es;
@@ -159,10 +161,15 @@ static vti_status exchange_staged(vti_s *const *hs, int n, int i, int b)
         CU(h, cudaStreamWaitEvent(h->comm, hs[i + 1]->ev_edge, 0));
         CU(h, cudaMemcpyAsync(h->rbuf[1], hs[i + 1]->sbuf[0], bytes, cudaMemcpyDefault, h->comm));
     }
-    vti_status s = unpack_recv(h, b);
+    vti_status s = unpack_recv_buf(h, buf);
     if (s != VTI_OK) return s;
     CU(h, cudaEventRecord(h->ev_comm, h->comm));
     return VTI_OK;
+}
+
+static vti_status exchange_staged(vti_s *const *hs, int n, int i, int b)
+{
+    return exchange_staged_buf(hs, n, i, hs[i]->pbuf[b]);
 }
 
 // The main stream of handle i waits for its own and its neighbours' exchanges: its halo rows
@@ -177,8 +184,8 @@ static vti_status wait_staged(vti_s *const *hs, int n, int i)
     return VTI_OK;
 }
 
-// NCCL transport on the comm stream after ev_edge, then unpack; records ev_comm.
-vti_status exchange_nccl(vti_s *h, int b)
+// NCCL transport on the comm stream after ev_edge, then unpack into buf; records ev_comm.
+static vti_status exchange_nccl_buf(vti_s *h, void *buf)
 {
     NcclApi &api = nccl();
     CU(h, cudaStreamWaitEvent(h->comm, h->ev_edge, 0));
@@ -197,9 +204,40 @@ vti_status exchange_nccl(vti_s *h, int b)
     ncclResult_t e2 = api.GroupEnd();
     if (e != ncclSuccess || e2 != ncclSuccess)
         return fail(h, VTI_E_COMM, "NCCL halo exchange: %s", api.GetErrorString(e != ncclSuccess ? e : e2));
-    vti_status s = unpack_recv(h, b);
+    vti_status s = unpack_recv_buf(h, buf);
     if (s != VTI_OK) return s;
     CU(h, cudaEventRecord(h->ev_comm, h->comm));
+    return VTI_OK;
+}
+vti_status exchange_nccl(vti_s *h, int b) { return exchange_nccl_buf(h, h->pbuf[b]); }
+
+// The R boundary rows of an arbitrary halo'd slab array (the adjoint's s1, vti_adjoint.cu) into
+// the neighbours' halo rows with the same pack / exchange / unpack as p's NCCL path: packs on each
+// main stream (ev_edge), then over NCCL (nccl: one handle of a multi-process job, n = 1) or, in a
+// local group, as copies from the neighbours' send buffers; every main stream then waits for the
+// exchanges that read its send buffers and fill its halo rows.
+vti_status rows_exchange(vti_s *const *hs, int n, void *const *bufs, bool nccl_path)
+{
+    vti_status s;
+    for (int i = 0; i < n; ++i) {
+        vti_s *h = hs[i];
+        CU(h, cudaSetDevice(h->cfg.device));
+        const int r = h->cfg.rank, nr = h->cfg.nranks;
+        if (r > 0) pack(h, bufs[i], h->sbuf[0], h->R, h->stream);
+        if (r < nr - 1) pack(h, bufs[i], h->sbuf[1], h->nyl, h->stream);
+        CU(h, cudaGetLastError());
+        CU(h, cudaEventRecord(h->ev_edge, h->stream));
+    }
+    for (int i = 0; i < n; ++i) {
+        CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+        if ((s = nccl_path ? exchange_nccl_buf(hs[i], bufs[i]) : exchange_staged_buf(hs, n, i, bufs[i])) != VTI_OK)
+            return s;
+    }
+    for (int i = 0; i < n; ++i) {
+        CU(hs[i], cudaSetDevice(hs[i]->cfg.device));
+        if (nccl_path) CU(hs[i], cudaStreamWaitEvent(hs[i]->stream, hs[i]->ev_comm, 0));
+        else if ((s = wait_staged(hs, n, i)) != VTI_OK) return s;
+    }
     return VTI_OK;
 }
 

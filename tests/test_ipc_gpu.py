@@ -1,14 +1,17 @@
-"""Multi-process bootstrap of the fused peer transport over CUDA IPC.
+"""Multi-process fused peer transport over CUDA IPC on one GPU.
 
-Two processes on cuda:0, each owning one y-slab handle (nranks = 2, nccl_id = NULL),
-run bench.py's own rank setup (bench.open_handle -> multi.connect_peer over a gloo
-group): export the IPC blobs, all-gather them, open the neighbour's buffers and flag
-words. The handles must then report the peer transport and the fused one-launch step,
-and bench.py's N > 1 guards run on them: multi.sync_or_die on the (idle) library stream
-and multi.max_over_ranks with a device tensor. Nothing is stepped: ranks that wait on one another must not share one GPU
-(B200_PROFILING.md), so the stepping protocol itself is covered by the local-group
-GPU tests (same kernels and flag sequence) and the CPU model check
-(tests/test_peer_protocol_cpu.py).
+Two processes on cuda:0, each owning one y-slab handle (nranks = 2, nccl_id = NULL).
+* Bootstrap: bench.py's own rank setup (bench.open_handle -> multi.connect_peer over a
+  gloo group) exports the IPC blobs, all-gathers them and opens the neighbour's buffers
+  and flag words; the handles report the peer transport and the fused one-launch step,
+  and bench.py's N > 1 guards run on them (multi.sync_or_die on the idle library stream,
+  multi.max_over_ranks with a device tensor).
+* One-sided stepping: ranks that wait on one another must not share one GPU
+  (B200_PROFILING.md), so rank 0 steps with its own flag words pre-set (test-only hook
+  vti_debug_flags) while rank 1 stays idle, then rank 1 checks what arrived in its memory.
+The two-sided protocol is covered by the local-group GPU tests (same kernels and flag
+sequence), the CPU model check (tests/test_peer_protocol_cpu.py) and, on >= 2 GPUs,
+tests/test_multigpu_gpu.py.
 """
 import os
 import socket
@@ -127,6 +130,12 @@ def _one_sided_worker(rank, world, port, q):
             # rank 0's output buffer of step K has index K % 2; this idle rank's cur is 0
             res["halo"] = h.debug_halo(level=K % 2, side=0)
             res["flags"] = h.debug_flags().tolist()
+            from paper_1410_1387_b200 import VTIError
+            try:   # the multi-process adjoint needs the NCCL transport (s1 rows)
+                h.step_adjoint(1)
+                res["adjoint"] = "ran"
+            except VTIError as e:
+                res["adjoint"] = e.name
         dist.barrier()
         h.close()
         q.put((rank, res))
@@ -157,5 +166,6 @@ def test_two_process_ipc_one_sided_step():
     assert np.array_equal(got[1]["halo"], got[0]["last_rows"])
     # publications: the re-publication of the state set by the caller, then one per step
     assert got[1]["flags"] == [4, 0, 3, 0], got[1]["flags"]
+    assert got[1]["adjoint"] == "VTI_E_STATE"
     for p in procs:
         assert p.exitcode == 0

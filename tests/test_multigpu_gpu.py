@@ -47,12 +47,17 @@ def _free_port():
     return p
 
 
-def _case(r, rz, ny):
+def _case(r, rz, ny, prec=32):
     cfg = synth.scaled(synth.CONFIGS["C2"](), 72, ny, 2 * rz + 12, r_xy=r, r_z=rz, damp_width=5,
                        dz=(6.0, 12.0), t0=0.02)
     cfg["src"] = (36, ny // 2, cfg["nz"] // 2)   # on or next to a slab boundary for even worlds
     wxy, wz, _ = synth.weights_f32(cfg)
-    return cfg, wxy, wz, synth.stable_dt(cfg, wxy, wz)
+    dt = synth.stable_dt(cfg, wxy, wz)
+    if prec == 64:
+        from synth import weights as W
+        wxy = W.xy_weights(r)
+        wz = np.ascontiguousarray(W.z_weights(W.z_coords_ramp(cfg["nz"], rz, 6.0, 12.0), rz))
+    return cfg, wxy, wz, dt
 
 
 def _worker(rank, world, port, q, halo, r, rz, ny, K):
@@ -132,6 +137,67 @@ def test_paper_radii_thin_slabs(halo):
     """(12,8) radii with slabs of 16 rows: every row of a slab is some neighbour's halo row."""
     _need(2)
     assert _run(2, halo, r=12, rz=8, ny=32, K=12) == [halo] * 2
+
+
+def _adj_worker(rank, world, port, q, r, rz, prec, ny, K):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(rank)
+        sys.path.insert(0, ROOT)
+        import bench
+        cfg, wxy, wz, dt = _case(r, rz, ny, prec)
+        h = bench.open_handle(cfg, dt, wxy, wz, rank, world, rank, prec, dist, "nccl")
+        sl = slice(h.y0, h.y0 + h.ny_local)
+        dtype = np.float32 if prec == 32 else np.float64
+        model = [np.ascontiguousarray(a.numpy()[:, sl].astype(dtype)) for a in SF.model_planes(cfg, 0, cfg["nz"])]
+        st = [np.ascontiguousarray(SF.random_planes(cfg["nx"], ny, 0, cfg["nz"], 7, s, 1e-3).numpy()[:, sl].astype(dtype))
+              for s in range(4)]
+        h.set_model(*model)
+        h.set_fields(*st, time_index=40)
+        h.step_adjoint(K)
+        h.sync()
+        res = {"transport": h.halo_transport, "y0": h.y0, "fields": h.get_fields(0) + h.get_fields(1)}
+        dist.barrier()
+        h.close()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("r,rz,prec", [(4, 4, 32), (12, 8, 32), (6, 6, 64)])
+def test_nccl_adjoint_slabs_equal_oracle(r, rz, prec):
+    """vti_step_adjoint over y-slabs, one process per GPU: the chained two-pass TMA form with the
+    s1 boundary rows exchanged over NCCL each step; bitwise equal to the oracle's adjoint."""
+    _need(2)
+    world, K = 2, 10
+    ny = 40 * world + 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_adj_worker, args=(rk, world, port, q, r, rz, prec, ny, K)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        got = dict(q.get(timeout=600) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.kill()
+    for p in procs:
+        assert p.exitcode == 0
+    cfg, wxy, wz, dt = _case(r, rz, ny, prec)
+    dtype = np.float32 if prec == 32 else np.float64
+    model = [a.numpy().astype(dtype) for a in SF.model_planes(cfg, 0, cfg["nz"])]
+    st = [SF.random_planes(cfg["nx"], ny, 0, cfg["nz"], 7, s, 1e-3).numpy().astype(dtype) for s in range(4)]
+    o = oracle.adjoint_ex(oracle.params(cfg, dt, src=None), wxy, wz, *model, st, m0=40, nsteps=K, dtype=dtype)
+    order = sorted(got, key=lambda k: got[k]["y0"])
+    assert [got[k]["transport"] for k in order] == ["nccl"] * world
+    for f in range(4):
+        g = np.concatenate([got[k]["fields"][f] for k in order], axis=1)
+        assert np.array_equal(g, o[f]), f"field {f}: max |diff| {np.abs(g - o[f]).max():.3e}"
 
 
 @pytest.mark.parametrize("halo", ["peer", "nccl"])
