@@ -80,6 +80,27 @@ def test_adjoint_no_points_matches_oracle(r, rz, prec):
         assert np.array_equal(a, b), f"field {f}: max |diff| {np.abs(a - b).max():.3e}"
 
 
+@pytest.mark.parametrize("r,rz,prec", [(4, 4, 32), (12, 8, 32), (4, 4, 64)])
+def test_adjoint_split_calls_equal_one_call(r, rz, prec):
+    """Calls of 1 + 3 + 4 adjoint steps equal one call of 8 (the chained form restarts its
+    first pass per call), with receivers spanning the calls and check_every on."""
+    cfg, wxy, wz, dt, model, st, dtype = setup(r, rz, prec, shape=(100, 40, 2 * rz + 30))
+    pts = np.array([(3, 4, 5), (50, 20, 10), (99, 39, 2 * rz + 29)], np.int32)
+    out = []
+    for split in ((8,), (1, 3, 4)):
+        with handle(cfg, dt, wxy, wz, prec, check_every=2) as v:
+            v.set_model(*model)
+            v.set_fields(*st, time_index=20)
+            v.set_receivers(pts, fields=3, capacity_steps=8)
+            for k in split:
+                v.step_adjoint(k)
+            out.append((v.get_fields(0) + v.get_fields(1), v.get_traces()[1], v.time_index))
+    assert out[0][2] == out[1][2] == 12
+    for a, b in zip(out[0][0], out[1][0]):
+        assert np.array_equal(a, b)
+    assert np.array_equal(out[0][1], out[1][1])
+
+
 def test_library_dot_product_identity():
     """fp64, damped: the library's K forward steps and K adjoint steps satisfy
     <u^K, psi^K / g> - <u^{K-1}, g psi^{K+1}> = <u^0, psi^0 / g> - <u^{-1}, g psi^1>."""
