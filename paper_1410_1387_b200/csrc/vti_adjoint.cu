@@ -463,7 +463,7 @@ static vti_status launch_adj_step(vti_s *h, const AdjParams<T> &A, int grid)
 // aprons and the Rz-ahead psi boxes come back from L2. Same canonical arithmetic as k_adj_prep +
 // k_adj_step (a skipped out-of-grid D^T term equals an fma with weight 0 and s2 = 0 bit for bit:
 // DT starts at +0 and +0 + (+-0) = +0), so the same bits as the oracle.
-template <typename T, int R, int RZ, int TY, int ST>
+template <typename T, int R, int RZ, int TY, int ST, int PX = 4>
 struct AdjTmaCfg {
     static constexpr int ES = (int)sizeof(T);
     static constexpr int RA = (R + 3) / 4 * 4;
@@ -481,7 +481,8 @@ struct AdjTmaCfg {
     static constexpr int OFF_S1 = ST * STAGE;               // [2][P_BYTES]: s1 of planes k (even / odd)
     static constexpr int OFF_BAR = OFF_S1 + 2 * P_BYTES;
     static constexpr int SMEM = OFF_BAR + 2 * ST * 8;
-    static constexpr int NCONS = 16 * TY;                   // consumer threads, 4 x points each
+    static constexpr int TPR = TX / PX;                     // consumer threads per tile row
+    static constexpr int NCONS = TPR * TY;                  // consumer threads, PX x points each
     static constexpr int NT = NCONS + 32;                   // + the producer warp
     static_assert(PW % 4 == 0 && PW <= 256 && PH <= 256, "TMA box");
 };
@@ -503,12 +504,13 @@ __device__ __forceinline__ void adj_item(const AdjTmaParams<T> &P, int item, int
     ke = min(P.A.nz, kb + P.zchunk);
 }
 
-template <typename T, int R, int RZ, int TY, int ST, bool IO>
-__global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
+template <typename T, int R, int RZ, int TY, int ST, int PX, bool IO>
+__global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST, PX>::NT, 1)
     k_adj_tma(const __grid_constant__ AdjTmaParams<T> P)
 {
-    using C = AdjTmaCfg<T, R, RZ, TY, ST>;
-    constexpr int NQ = C::NQ, RA = C::RA, PW = C::PW, ES = C::ES, NCONS = C::NCONS;
+    using C = AdjTmaCfg<T, R, RZ, TY, ST, PX>;
+    using VP = Vec<T, PX>;
+    constexpr int NQ = C::NQ, RA = C::RA, PW = C::PW, ES = C::ES, NCONS = C::NCONS, TPR = C::TPR;
     constexpr bool SHIFT = NQ > 9;   // i-cache: NQ unrolled copies of a deep body miss (ncu: no_instructions)
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
@@ -567,24 +569,24 @@ __global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
         return;
     }
 
-    // consumers: 16 x TY threads, 4 consecutive x points each
-    const int tx = threadIdx.x & 15, tg = threadIdx.x >> 4;
-    const int sidx = tg * TX + 4 * tx;   // this thread's first point in an interior box
+    // consumers: TPR x TY threads, PX consecutive x points each
+    const int tx = threadIdx.x % TPR, tg = threadIdx.x / TPR;
+    const int sidx = tg * TX + PX * tx;   // this thread's first point in an interior box
     T *s1buf = reinterpret_cast<T *>(smem + C::OFF_S1);
     int par = 0;
     for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
         int x0, y0, kb, ke;
         adj_item<TY>(P, item, x0, y0, kb, ke);
-        const int xg = x0 + 4 * tx, yl = y0 + tg;
+        const int xg = x0 + PX * tx, yl = y0 + tg;
         const bool own = xg < A.nx && yl < A.nyl;
         const T gy = yl < A.nyl ? A.gy[yl] : T(0);
-        const V4<T> gx4 = ldv<4>(A.gx + xg);
-        T q[NQ][4];   // slot (u + j) % NQ holds s2 of plane k - Rz + j
-        auto push_s2 = [&](const T *st, T (&v)[4]) {
-            const V4<T> ip = ldv<4>(st + C::OFF_IP / ES + sidx), iq = ldv<4>(st + C::OFF_IQ / ES + sidx);
-            const V4<T> vz = ldv<4>(st + C::OFF_VZ / ES + sidx);
+        const VP gx4 = ldv<PX>(A.gx + xg);
+        T q[NQ][PX];   // slot (u + j) % NQ holds s2 of plane k - Rz + j
+        auto push_s2 = [&](const T *st, T (&v)[PX]) {
+            const VP ip = ldv<PX>(st + C::OFF_IP / ES + sidx), iq = ldv<PX>(st + C::OFF_IQ / ES + sidx);
+            const VP vz = ldv<PX>(st + C::OFF_VZ / ES + sidx);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) v[c] = vz[c] * (ip[c] + iq[c]);
+            for (int c = 0; c < PX; ++c) v[c] = vz[c] * (ip[c] + iq[c]);
         };
 #pragma unroll
         for (int t = 0; t < 2 * RZ; ++t) {
@@ -613,17 +615,19 @@ __global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
                 stv(s1 + 4 * e, v);
             }
             push_s2(st, q[(u + 2 * RZ) % NQ]);   // s2 of plane k + Rz
-            const int ctr = (tg + R) * PW + RA + 4 * tx;
-            const V4<T> pc4 = ldv<4>(st + C::OFF_HP / ES + ctr), qc4 = ldv<4>(st + C::OFF_HQ / ES + ctr);
-            const V4<T> po4 = ldv<4>(st + C::OFF_OP / ES + sidx), qo4 = ldv<4>(st + C::OFF_OQ / ES + sidx);
+            const int ctr = (tg + R) * PW + RA + PX * tx;
+            const VP pc4 = ldv<PX>(st + C::OFF_HP / ES + ctr), qc4 = ldv<PX>(st + C::OFF_HQ / ES + ctr);
+            const VP po4 = ldv<PX>(st + C::OFF_OP / ES + sidx), qo4 = ldv<PX>(st + C::OFF_OQ / ES + sidx);
             const T *zr = st + C::OFF_ZR / ES;
             // D^T(s2): ascending m over planes k + Rz - m, weights w^T[k][m]
-            T DT[4] = {T(0), T(0), T(0), T(0)};
+            T DT[PX];
+#pragma unroll
+            for (int c = 0; c < PX; ++c) DT[c] = T(0);
 #pragma unroll
             for (int m = 0; m < NQ; ++m) {
                 const T w = zr[m];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) DT[c] = fma_x<T>(w, q[(u + 2 * RZ - m) % NQ][c], DT[c]);
+                for (int c = 0; c < PX; ++c) DT[c] = fma_x<T>(w, q[(u + 2 * RZ - m) % NQ][c], DT[c]);
             }
             const T gz = zr[NQ];
             __syncwarp();
@@ -634,23 +638,23 @@ __global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
             }
             named_bar_sync(1, NCONS);   // the s1 tile of plane k is complete
             // L(s1), canonical pairing (x pair + y pair)
-            const T *base = s1 + tg * PW + 4 * tx;   // smem row tg = tile row tg - R
+            const T *base = s1 + tg * PW + PX * tx;   // smem row tg = tile row tg - R
             const T *prow = base + R * PW;
-            auto wx = [&](int i) { return ldv<4>(prow + 4 * (i / 4))[i % 4]; };
-            T L[4];
+            auto wx = [&](int i) { return ldv<PX>(prow + PX * (i / PX))[i % PX]; };
+            T L[PX];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) L[c] = A.cxy[0] * wx(RA + c);
+            for (int c = 0; c < PX; ++c) L[c] = A.cxy[0] * wx(RA + c);
 #pragma unroll
             for (int l = 1; l <= R; ++l) {
-                const V4<T> yp = ldv<4>(base + (R + l) * PW + RA), ym = ldv<4>(base + (R - l) * PW + RA);
+                const VP yp = ldv<PX>(base + (R + l) * PW + RA), ym = ldv<PX>(base + (R - l) * PW + RA);
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < PX; ++c)
                     L[c] = fma_x<T>(A.cxy[l], (wx(RA + c + l) + wx(RA + c - l)) + (yp[c] + ym[c]), L[c]);
             }
             if (!own) return;
-            T pn[4], qn[4];
+            T pn[PX], qn[PX];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < PX; ++c) {
                 T Fp = L[c], Fq = DT[c];
                 if constexpr (IO) {
                     const int i = xg + c;
@@ -668,12 +672,12 @@ __global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
                 qn[c] = g * fma_x<T>(A.dt2, Fq, fma_x<T>(-g, qo4[c], T(2) * qc4[c]));
             }
             const int64_t a0 = (int64_t)yl * A.ys + (int64_t)k * A.zs + xg;
-            if (xg + 4 <= A.nx) {
+            if (xg + PX <= A.nx) {
                 stv(A.po + a0, pn);
                 stv(A.qo + a0, qn);
             } else {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < PX; ++c)
                     if (xg + c < A.nx) {
                         A.po[a0 + c] = pn[c];
                         A.qo[a0 + c] = qn[c];
@@ -685,10 +689,10 @@ __global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
                     const int nf = (A.rec_mask & 1) + ((A.rec_mask >> 1) & 1);
                     for (int e = A.rec_off[rb]; e < A.rec_off[rb + 1]; ++e) {
                         const int c = A.rec_ent[e].x - xg;
-                        if (c < 0 || c >= 4) continue;
+                        if (c < 0 || c >= PX) continue;
                         T vp = pn[0], vq = qn[0];
 #pragma unroll
-                        for (int cc = 1; cc < 4; ++cc)
+                        for (int cc = 1; cc < PX; ++cc)
                             if (c == cc) {
                                 vp = pn[cc];
                                 vq = qn[cc];
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST>::NT, 1)
 #pragma unroll
                 for (int m = 0; m < NQ - 1; ++m)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) q[m][c] = q[m + 1][c];
+                    for (int c = 0; c < PX; ++c) q[m][c] = q[m + 1][c];
                 plane(k, 0);
             }
         } else {   // the queue index unrolled NQ times: no moves, NQ copies of the body
@@ -1014,12 +1018,12 @@ struct AdjTmaEntry {
     int smem_ch;
 };
 
-template <typename T, int R, int RZ, int TY, int ST>
+template <typename T, int R, int RZ, int TY, int ST, int PX = 4>
 constexpr AdjTmaEntry adj_tma1()
 {
-    using C = AdjTmaCfg<T, R, RZ, TY, ST>;
-    return {C::ES, R, RZ, 1, TY, 4, ST, 1, (const void *)k_adj_tma<T, R, RZ, TY, ST, false>,
-            (const void *)k_adj_tma<T, R, RZ, TY, ST, true>, C::SMEM, C::NT, C::ZROW, nullptr, nullptr, 0};
+    using C = AdjTmaCfg<T, R, RZ, TY, ST, PX>;
+    return {C::ES, R, RZ, 1, TY, PX, ST, 1, (const void *)k_adj_tma<T, R, RZ, TY, ST, PX, false>,
+            (const void *)k_adj_tma<T, R, RZ, TY, ST, PX, true>, C::SMEM, C::NT, C::ZROW, nullptr, nullptr, 0};
 }
 
 template <typename T, int R, int RZ, int TY, int ST, int PX, int MINB = 1>
