@@ -1148,7 +1148,11 @@ static vti_status launch_adj_tma(vti_s *h, const AdjTmaEntry *E, const AdjParams
     P.nty = (h->nyl + E->ty - 1) / E->ty;
     const int tiles = P.ntx * P.nty;
     static const int zenv = getenv("VTI_ADJ_ZCHUNK") ? atoi(getenv("VTI_ADJ_ZCHUNK")) : 0;
-    int nzc = std::max(1, std::min((h->cfg.nz + 31) / 32, (6 * ctas + tiles - 1) / tiles));
+    // about 6 items per resident CTA, z-chunks of >= 32 planes (the 2R_z priming loads per item)
+    // unless that leaves CTAs idle (small grids: chunks down to 4 planes)
+    const int want = (6 * ctas + tiles - 1) / tiles;
+    int nzc = std::max(1, std::min((h->cfg.nz + 31) / 32, want));
+    if (tiles * nzc < ctas) nzc = std::max(1, std::min((h->cfg.nz + 3) / 4, want));
     P.zchunk = zenv > 0 ? zenv : (h->cfg.nz + nzc - 1) / nzc;
     nzc = (h->cfg.nz + P.zchunk - 1) / P.zchunk;
     P.items = tiles * nzc;
