@@ -310,12 +310,13 @@ vti_status vti_reverse(vti_t h);
  * tests/test_adjoint_gpu.py). Kernels (csrc/vti_adjoint.cu): a TMA one-pass form (the coefficient
  * products formed in the stencil kernel) or a chained two-pass form (s1 = vx2 psi_p + vn2 psi_q
  * written once per call, then each step's kernel also writes the next step's s1), whichever
- * measured faster for the precision and radii. nranks > 1, one process per slab: handles created
- * with an NCCL id; the chained two-pass form with each step's s1 boundary rows exchanged over
- * NCCL (pack, send/recv, unpack); every rank calls it with the same nsteps. Local groups:
- * vti_group_step_adjoint. Bitwise equal to the oracle's vto_adjoint_ex. Errors: STATE (model
- * unset; a local-group handle; nranks > 1 without the NCCL transport), UNSUPPORTED (nranks > 1
- * and no two-pass kernel for the radii), PARAM, CUDA, COMM, INSTABILITY.
+ * measured faster for the precision and radii. nranks > 1, one process per slab: the chained
+ * two-pass form with each step's s1 boundary rows exchanged over the handle's transport -- NCCL
+ * (pack, send/recv, unpack) or, after vti_ipc_connect, CUDA IPC (rows packed straight into the
+ * neighbours' receive buffers, ordered by flag words); every rank calls it with the same nsteps.
+ * Local groups: vti_group_step_adjoint. Bitwise equal to the oracle's vto_adjoint_ex. Errors:
+ * STATE (model unset; a local-group handle; nranks > 1 without a transport), UNSUPPORTED
+ * (nranks > 1 and no two-pass kernel for the radii), PARAM, CUDA, COMM, INSTABILITY.
  */
 vti_status vti_step_adjoint(vti_t h, int32_t nsteps);
 
@@ -352,12 +353,16 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi);
 /* 0: none (single slab), 1: NCCL, 2: fused peer stores (local group or CUDA IPC). */
 int32_t vti_halo_transport(vti_t h);
 
-/* Diagnostics of the peer transport (tests): read (get4) and/or overwrite (set4) this handle's
- * four flag words {DATA_LO, DATA_HI, ACK_LO, ACK_HI} -- the words its neighbours write --, and
- * copy R_xy halo rows of p (side 0: the rows below the slab, side 1: above; level 0: u^n, 1:
- * the stored level) to host memory [nz][R_xy][nx]. Both synchronise. Errors: PARAM, STATE, CUDA. */
-vti_status vti_debug_flags(vti_t h, uint32_t *get4, const uint32_t *set4);
+/* Diagnostics of the peer transport (tests): read (get8) and/or overwrite (set8) this handle's
+ * eight flag words {DATA_LO, DATA_HI, ACK_LO, ACK_HI} of p's halo and the same four of the
+ * adjoint's s1 rows -- the words its neighbours write --; copy R_xy halo rows of p (side 0: the
+ * rows below the slab, side 1: above; level 0: u^n, 1: the stored level) to host memory
+ * [nz][R_xy][nx]; vti_debug_rows copies R_xy rows of the adjoint's s1 scratch buffer what >> 1
+ * (what & 1 = 0: the slab's first rows, 1: its last rows) or, what = 4 / 5, the receive buffer
+ * filled by rank-1 / rank+1, to [nz][R_xy][nx]. All synchronise. Errors: PARAM, STATE, CUDA. */
+vti_status vti_debug_flags(vti_t h, uint32_t *get8, const uint32_t *set8);
 vti_status vti_debug_halo(vti_t h, int32_t level, int32_t side, void *out);
+vti_status vti_debug_rows(vti_t h, int32_t what, void *out);
 
 /* Block until all work on the handle's stream(s) is done. */
 vti_status vti_sync(vti_t h);

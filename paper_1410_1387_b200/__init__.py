@@ -139,6 +139,7 @@ def _load():
         "vti_halo_transport": (C.c_int32, [H]),
         "vti_debug_flags": (st, [H, P, P]),
         "vti_debug_halo": (st, [H, C.c_int32, C.c_int32, P]),
+        "vti_debug_rows": (st, [H, C.c_int32, P]),
         "vti_direction": (C.c_int32, [H]),
         "vti_autotune": (st, [H, C.c_int32, C.POINTER(TuneResult)]),
         "vti_last_error": (C.c_char_p, [H]),
@@ -397,10 +398,11 @@ class VTI:
         """vti_step_adjoint: nsteps of the transpose recurrence (state = (psi^m, psi^{m+1}))."""
         _check(self.h, lib.vti_step_adjoint(self.h, nsteps))
 
-    def debug_flags(self, set4=None):
-        """vti_debug_flags: this handle's flag words (DATA_LO, DATA_HI, ACK_LO, ACK_HI); optionally set them."""
-        out = np.zeros(4, np.uint32)
-        src = None if set4 is None else np.ascontiguousarray(np.asarray(set4, np.uint32))
+    def debug_flags(self, set8=None):
+        """vti_debug_flags: this handle's eight flag words (DATA_LO, DATA_HI, ACK_LO, ACK_HI of p's
+        halo, then of the adjoint's s1 rows); optionally set them."""
+        out = np.zeros(8, np.uint32)
+        src = None if set8 is None else np.ascontiguousarray(np.asarray(set8, np.uint32))
         _check(self.h, lib.vti_debug_flags(self.h, out.ctypes.data, None if src is None else src.ctypes.data))
         return out
 
@@ -408,6 +410,13 @@ class VTI:
         """vti_debug_halo: p's R_xy halo rows below (side 0) / above (side 1) the slab, [nz][R][nx]."""
         out = np.zeros((self.nz, self.cfg.r_xy, self.nx), dtype=self.dtype)
         _check(self.h, lib.vti_debug_halo(self.h, level, side, out.ctypes.data))
+        return out
+
+    def debug_rows(self, what):
+        """vti_debug_rows: R_xy rows of the adjoint's s1 scratch buffer what >> 1 (what & 1: the slab's
+        first / last rows) or, what = 4 / 5, the receive buffer filled by rank-1 / rank+1; [nz][R][nx]."""
+        out = np.zeros((self.nz, self.cfg.r_xy, self.nx), self.dtype)
+        _check(self.h, lib.vti_debug_rows(self.h, int(what), out.ctypes.data))
         return out
 
     def reverse(self):

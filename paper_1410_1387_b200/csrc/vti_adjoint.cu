@@ -1415,13 +1415,12 @@ vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
     if (!h) return VTI_E_PARAM;
     if (nsteps < 0) return fail(h, VTI_E_PARAM, "nsteps < 0");
     if (!h->model_set) return fail(h, VTI_E_STATE, "model not set (vti_set_model)");
-    // y-slabs, one process per slab: the chained TMA form with the s1 rows over NCCL
+    // y-slabs, one process per slab: the chained TMA form with the s1 rows over NCCL or CUDA IPC
     const bool mp = h->cfg.nranks > 1;
     if (mp && h->group_mode)
         return fail(h, VTI_E_STATE, "a local group's slabs step together: vti_group_step_adjoint");
-    if (mp && !h->comm_nccl)
-        return fail(h, VTI_E_STATE, "the multi-process adjoint exchanges s1 rows over NCCL: create the handles "
-                                    "with an NCCL id (the peer transport carries p only)");
+    if (mp && !h->comm_nccl && !h->peer)
+        return fail(h, VTI_E_STATE, "nranks > 1 needs an nccl_id at create time or vti_ipc_connect");
     if (mp && adj_form(h) != ADJ_TMA2)
         return fail(h, VTI_E_UNSUPPORTED, "no two-pass TMA adjoint kernel for this precision and radius pair");
     CU(h, cudaSetDevice(h->cfg.device));
@@ -1439,14 +1438,14 @@ vti_status vti_step_adjoint(vti_t h, int32_t nsteps)
         if (mp && prep) {   // s1 of the state the caller left, then its halo rows
             if ((s = h->es == 8 ? adjoint_prep_t<double>(h, sb) : adjoint_prep_t<float>(h, sb)) != VTI_OK) return s;
             void *b0 = h->adj_s[sb];
-            if ((s = rows_exchange(hv, 1, &b0, true)) != VTI_OK) return s;
+            if ((s = h->peer ? rows_exchange_peer(h, b0) : rows_exchange(hv, 1, &b0, true)) != VTI_OK) return s;
         }
         s = h->es == 8 ? adjoint_step_t<double>(h, prep && !mp, sb, chain) : adjoint_step_t<float>(h, prep && !mp, sb, chain);
         if (s != VTI_OK) return s;
         if (mp) h->halo_dirty = true;   // p's halo rows are stale for a later forward step
         if (mp && chain) {
             void *b1 = h->adj_s[1 - sb];
-            if ((s = rows_exchange(hv, 1, &b1, true)) != VTI_OK) return s;
+            if ((s = h->peer ? rows_exchange_peer(h, b1) : rows_exchange(hv, 1, &b1, true)) != VTI_OK) return s;
         }
         if (chain) sb ^= 1;
         h->cur = 1 - h->cur;

@@ -128,15 +128,18 @@ struct vti_s {
     bool group_mode = false;
     // fused peer-memory halo transport (local group, or multi-process after vti_ipc_connect):
     // the edge launch stores p^{n+1}'s boundary rows straight into the neighbours' halo rows;
-    // flags[] = {DATA_LO, DATA_HI, ACK_LO, ACK_HI}, written by the neighbours
+    // flags[] = {DATA_LO, DATA_HI, ACK_LO, ACK_HI} of p's halo, then the same four for the adjoint's
+    // s1 rows (multi-process peer ranks), written by the neighbours
     bool peer = false;
     unsigned int *flags = nullptr;
     void *peer_p[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side][b]: neighbour's pbuf[b] at the
                                                                       // first halo row this rank writes
     long long peer_zs[2] = {0, 0};                    // the neighbours' plane strides (elements)
     unsigned int *peer_flags[2] = {nullptr, nullptr}; // the neighbours' flags
-    void *ipc_opened[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // cudaIpcCloseMemHandle on destroy
+    void *ipc_opened[8] = {};                         // cudaIpcCloseMemHandle on destroy
     unsigned int xseq = 0;                            // halo publications so far (the flag values)
+    void *peer_rbuf[2] = {nullptr, nullptr};          // [side]: the neighbour's receive buffer for our rows
+    unsigned int adj_xseq = 0;                        // s1 row publications so far (peer adjoint)
     bool flush_remote = false;                        // CU_STREAM_WAIT_VALUE_FLUSH supported
     bool halo_dirty = false;
     bool suppress_src = false;                // autotune probes inject nothing
@@ -213,6 +216,9 @@ vti_status pack_send(vti_s *h, int b);          // NCCL: boundary rows of buffer
 // R boundary rows of halo'd slab arrays bufs[i] into the neighbours' halo rows: NCCL (one
 // handle of a multi-process job) or copies between a local group's send / recv buffers
 vti_status rows_exchange(vti_s *const *hs, int n, void *const *bufs, bool nccl_path);
+// the same over CUDA IPC for a multi-process peer rank: rows packed straight into the
+// neighbours' receive buffers, ordered by flag words 4..7
+vti_status rows_exchange_peer(vti_s *h, void *buf);
 vti_status exchange_nccl(vti_s *h, int b);      // NCCL: send/recv + unpack on the comm stream, records ev_comm
 vti_status peer_pre_step(vti_s *h);             // peer: wait for the halo this step reads
 vti_status peer_post_edge(vti_s *h);            // peer: after the edge launch, ACK + DATA to the neighbours

@@ -516,7 +516,7 @@ static vti_status create_impl(vti_s *h, const vti_config *cfg, const double *w_x
             if ((s = alloc(h, &h->sbuf[b], hb)) != VTI_OK) return s;
             if ((s = alloc(h, &h->rbuf[b], hb)) != VTI_OK) return s;
         }
-        if ((s = alloc(h, (void **)&h->flags, 4 * sizeof(unsigned int))) != VTI_OK) return s;
+        if ((s = alloc(h, (void **)&h->flags, 8 * sizeof(unsigned int))) != VTI_OK) return s;
         int flush = 0;
         if (cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, cfg->device) == cudaSuccess)
             h->flush_remote = flush != 0;

@@ -262,6 +262,8 @@ vti_status rows_exchange(vti_s *const *hs, int n, void *const *bufs, bool nccl_p
 // writes before any handle's step j+1 waits, and splits a re-publication into
 // a release half and a publish half.
 enum { F_DATA_LO = 0, F_DATA_HI = 1, F_ACK_LO = 2, F_ACK_HI = 3 };
+// the adjoint's s1 rows between multi-process peer ranks (rows_exchange_peer)
+enum { F_S1DATA_LO = 4, F_S1DATA_HI = 5, F_S1ACK_LO = 6, F_S1ACK_HI = 7 };
 
 static CUdeviceptr dev_ptr(const void *p) { return (CUdeviceptr)(uintptr_t)p; }
 static bool has_side(const vti_s *h, int side) { return side == 0 ? h->cfg.rank > 0 : h->cfg.rank < h->cfg.nranks - 1; }
@@ -285,6 +287,33 @@ static vti_status flag_write(vti_s *h, int side, int idx, unsigned int v)
     if (ops.write((CUstream)h->stream, dev_ptr(h->peer_flags[side] + idx), v, CU_STREAM_WRITE_VALUE_DEFAULT) !=
         CUDA_SUCCESS)
         return fail(h, VTI_E_COMM, "cuStreamWriteValue32 failed");
+    return VTI_OK;
+}
+
+// Multi-process peer ranks (CUDA IPC): publication j of buf's boundary rows, all on the main
+// stream. Per side: once the neighbour has unpacked publication j-1 (S1ACK >= j-1), pack our rows
+// straight into its receive buffer and raise its S1DATA to j; then, once its rows are in our
+// receive buffer (S1DATA >= j), unpack them into buf's halo rows and raise its S1ACK to j.
+// Every rank publishes in the same order, so the waits are always on writes the neighbour
+// makes before its own waits.
+vti_status rows_exchange_peer(vti_s *h, void *buf)
+{
+    const unsigned int j = ++h->adj_xseq;
+    vti_status s;
+    for (int side = 0; side < 2; ++side) {
+        if (!has_side(h, side)) continue;
+        if (j >= 2 && (s = flag_wait(h, side == 0 ? F_S1ACK_LO : F_S1ACK_HI, j - 1, false)) != VTI_OK) return s;
+        pack(h, buf, h->peer_rbuf[side], side == 0 ? h->R : h->nyl, h->stream);
+        CU(h, cudaGetLastError());
+        if ((s = flag_write(h, side, side == 0 ? F_S1DATA_HI : F_S1DATA_LO, j)) != VTI_OK) return s;
+    }
+    for (int side = 0; side < 2; ++side) {
+        if (!has_side(h, side)) continue;
+        if ((s = flag_wait(h, side == 0 ? F_S1DATA_LO : F_S1DATA_HI, j, true)) != VTI_OK) return s;
+        unpack(h, h->rbuf[side], buf, side == 0 ? 0 : h->nyl + h->R, h->stream);
+        CU(h, cudaGetLastError());
+        if ((s = flag_write(h, side, side == 0 ? F_S1ACK_HI : F_S1ACK_LO, j)) != VTI_OK) return s;
+    }
     return VTI_OK;
 }
 
@@ -393,7 +422,7 @@ vti_status vti_nccl_unique_id(void *out128)
 struct IpcBlob {
     uint32_t magic, version;
     int32_t rank, nranks, nyl, nxp, R, es, zyx;
-    cudaIpcMemHandle_t pbuf[2], flags;
+    cudaIpcMemHandle_t pbuf[2], flags, rbuf[2];
 };
 static_assert(sizeof(IpcBlob) <= VTI_IPC_BYTES, "IPC blob too large");
 static const uint32_t IPC_MAGIC = 0x56544932u;   // "VTI2"
@@ -417,6 +446,8 @@ vti_status vti_ipc_export(vti_t h, void *out)
     CU(h, cudaIpcGetMemHandle(&b.pbuf[0], h->pbuf[0]));
     CU(h, cudaIpcGetMemHandle(&b.pbuf[1], h->pbuf[1]));
     CU(h, cudaIpcGetMemHandle(&b.flags, h->flags));
+    CU(h, cudaIpcGetMemHandle(&b.rbuf[0], h->rbuf[0]));
+    CU(h, cudaIpcGetMemHandle(&b.rbuf[1], h->rbuf[1]));
     memset(out, 0, VTI_IPC_BYTES);
     memcpy(out, &b, sizeof b);
     return VTI_OK;
@@ -450,6 +481,12 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
         cudaError_t e = cudaIpcOpenMemHandle(&fl, b.flags, cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
         h->ipc_opened[3 * side + 2] = fl;
+        // the neighbour's receive buffer for our rows: rank-1's rbuf[1] (from its rank+1), rank+1's rbuf[0]
+        void *rb = nullptr;
+        e = cudaIpcOpenMemHandle(&rb, b.rbuf[side == 0 ? 1 : 0], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(h, VTI_E_COMM, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+        h->ipc_opened[6 + side] = rb;
+        h->peer_rbuf[side] = rb;
         // rank-1: our first rows go to its top halo (row R + nyl); rank+1: our last rows to its row 0.
         // Same layout on both sides, so the row stride is ours (h->ys); the plane stride is theirs.
         const size_t row0 = side == 0 ? (size_t)b.R + b.nyl : 0;
@@ -464,14 +501,34 @@ vti_status vti_ipc_connect(vti_t h, const void *lo, const void *hi)
 
 int32_t vti_halo_transport(vti_t h) { return !h ? -1 : h->cfg.nranks < 2 ? 0 : h->peer ? 2 : h->comm_nccl ? 1 : 0; }
 
-vti_status vti_debug_flags(vti_t h, uint32_t *get4, const uint32_t *set4)
+vti_status vti_debug_flags(vti_t h, uint32_t *get8, const uint32_t *set8)
 {
     if (!h) return VTI_E_PARAM;
     if (!h->flags) return fail(h, VTI_E_STATE, "no flag words (nranks < 2)");
     CU(h, cudaSetDevice(h->cfg.device));
     CU(h, cudaStreamSynchronize(h->stream));
-    if (get4) CU(h, cudaMemcpy(get4, h->flags, 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost));
-    if (set4) CU(h, cudaMemcpy(h->flags, set4, 4 * sizeof(unsigned int), cudaMemcpyHostToDevice));
+    if (get8) CU(h, cudaMemcpy(get8, h->flags, 8 * sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    if (set8) CU(h, cudaMemcpy(h->flags, set8, 8 * sizeof(unsigned int), cudaMemcpyHostToDevice));
+    return VTI_OK;
+}
+
+vti_status vti_debug_rows(vti_t h, int32_t what, void *out)
+{
+    if (!h || !out || what < 0 || what > 5) return VTI_E_PARAM;
+    CU(h, cudaSetDevice(h->cfg.device));
+    CU(h, cudaStreamSynchronize(h->stream));
+    const size_t row = (size_t)h->cfg.nx * h->es;
+    if (what >= 4) {   // receive buffer [nz][R][nx], packed
+        if (!h->rbuf[what - 4]) return fail(h, VTI_E_STATE, "no receive buffers (nranks < 2)");
+        CU(h, cudaMemcpy(out, h->rbuf[what - 4], (size_t)h->cfg.nz * h->R * row, cudaMemcpyDeviceToHost));
+        return VTI_OK;
+    }
+    if (!h->adj_s[what >> 1]) return fail(h, VTI_E_STATE, "no adjoint scratch buffers yet");
+    // own rows [0, R) (what & 1 == 0) or [nyl - R, nyl) of scratch buffer what >> 1 -> out[nz][R][nx]
+    const char *src = h->in(h->adj_s[what >> 1]) + (size_t)((what & 1) ? h->nyl - h->R : 0) * h->ys * h->es;
+    for (int k = 0; k < h->cfg.nz; ++k)
+        CU(h, cudaMemcpy2D((char *)out + (size_t)k * h->R * row, row, src + (size_t)k * h->zs * h->es,
+                           (size_t)h->ys * h->es, row, h->R, cudaMemcpyDeviceToHost));
     return VTI_OK;
 }
 

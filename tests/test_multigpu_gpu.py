@@ -139,7 +139,7 @@ def test_paper_radii_thin_slabs(halo):
     assert _run(2, halo, r=12, rz=8, ny=32, K=12) == [halo] * 2
 
 
-def _adj_worker(rank, world, port, q, r, rz, prec, ny, K):
+def _adj_worker(rank, world, port, q, r, rz, prec, ny, K, halo):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -148,7 +148,7 @@ def _adj_worker(rank, world, port, q, r, rz, prec, ny, K):
         sys.path.insert(0, ROOT)
         import bench
         cfg, wxy, wz, dt = _case(r, rz, ny, prec)
-        h = bench.open_handle(cfg, dt, wxy, wz, rank, world, rank, prec, dist, "nccl")
+        h = bench.open_handle(cfg, dt, wxy, wz, rank, world, rank, prec, dist, halo)
         sl = slice(h.y0, h.y0 + h.ny_local)
         dtype = np.float32 if prec == 32 else np.float64
         model = [np.ascontiguousarray(a.numpy()[:, sl].astype(dtype)) for a in SF.model_planes(cfg, 0, cfg["nz"])]
@@ -166,17 +166,19 @@ def _adj_worker(rank, world, port, q, r, rz, prec, ny, K):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("halo", ["nccl", "peer"])
 @pytest.mark.parametrize("r,rz,prec", [(4, 4, 32), (12, 8, 32), (6, 6, 64)])
-def test_nccl_adjoint_slabs_equal_oracle(r, rz, prec):
+def test_adjoint_slabs_equal_oracle(r, rz, prec, halo):
     """vti_step_adjoint over y-slabs, one process per GPU: the chained two-pass TMA form with the
-    s1 boundary rows exchanged over NCCL each step; bitwise equal to the oracle's adjoint."""
+    s1 boundary rows exchanged each step over NCCL or CUDA IPC; bitwise equal to the oracle."""
     _need(2)
     world, K = 2, 10
     ny = 40 * world + 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_adj_worker, args=(rk, world, port, q, r, rz, prec, ny, K)) for rk in range(world)]
+    procs = [ctx.Process(target=_adj_worker, args=(rk, world, port, q, r, rz, prec, ny, K, halo))
+             for rk in range(world)]
     for p in procs:
         p.start()
     try:
@@ -194,7 +196,7 @@ def test_nccl_adjoint_slabs_equal_oracle(r, rz, prec):
     st = [SF.random_planes(cfg["nx"], ny, 0, cfg["nz"], 7, s, 1e-3).numpy().astype(dtype) for s in range(4)]
     o = oracle.adjoint_ex(oracle.params(cfg, dt, src=None), wxy, wz, *model, st, m0=40, nsteps=K, dtype=dtype)
     order = sorted(got, key=lambda k: got[k]["y0"])
-    assert [got[k]["transport"] for k in order] == ["nccl"] * world
+    assert [got[k]["transport"] for k in order] == [halo] * world
     for f in range(4):
         g = np.concatenate([got[k]["fields"][f] for k in order], axis=1)
         assert np.array_equal(g, o[f]), f"field {f}: max |diff| {np.abs(g - o[f]).max():.3e}"
