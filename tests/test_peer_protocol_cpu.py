@@ -20,6 +20,8 @@ and checks, for random interleavings of the ranks' streams:
 and, for the local group, that the host enqueue order is deadlock-free even if
 every stream of every handle shares ONE in-order hardware channel (the
 enqueue-order rule: a value-wait may only wait on an earlier-enqueued write).
+The adjoint's s1 row exchange between peer ranks (rows_exchange_peer) is checked
+the same way at the end of the file.
 """
 import random
 
@@ -257,3 +259,89 @@ def test_model_catches_a_wait_before_the_write_in_one_channel():
             break
         execute(ranks, ranks[r], ranks[r].ops[i], [])
     assert blocked == (0, 1)
+
+
+# ---- the adjoint's s1 rows between multi-process peer ranks (rows_exchange_peer, vti_transport.cu):
+# one receive buffer per side; publication j of a rank, enqueued on its stream:
+#   per side: wait S1ACK >= j-1; PACK into the neighbour's receive buffer; write nb.S1DATA = j
+#   per side: wait S1DATA >= j; UNPACK own receive buffer (must hold exactly j); write nb.S1ACK = j
+S1DATA, S1ACK = 2, 3
+
+
+class S1Rank(Rank):
+    def __init__(self, r, n):
+        super().__init__(r, n)
+        self.flags.update({(S1DATA, LO): 0, (S1DATA, HI): 0, (S1ACK, LO): 0, (S1ACK, HI): 0})
+        self.rbuf = [0, 0]       # publication in the receive buffer of each side
+        self.consumed = [0, 0]   # last publication unpacked from each side
+        self.adj_xseq = 0
+
+
+def enqueue_s1(R, ack_wait=True):
+    R.adj_xseq += 1
+    j = R.adj_xseq
+    for s in R.sides():
+        if ack_wait and j >= 2:
+            R.ops.append(("wait", (S1ACK, s), j - 1))
+        R.ops.append(("s1pack", s, j))
+        R.ops.append(("write", s, (S1DATA, other(s)), j))
+    for s in R.sides():
+        R.ops.append(("wait", (S1DATA, s), j))
+        R.ops.append(("s1unpack", s, j))
+        R.ops.append(("write", s, (S1ACK, other(s)), j))
+
+
+def execute_s1(ranks, R, op, errors):
+    if op[0] == "s1pack":
+        _, s, j = op
+        N = nb(ranks, R.r, s)
+        if N.rbuf[other(s)] != N.consumed[other(s)]:
+            errors.append(f"rank {R.r} overwrote publication {N.rbuf[other(s)]} in rank {N.r}'s buffer unread")
+        N.rbuf[other(s)] = j
+    elif op[0] == "s1unpack":
+        _, s, j = op
+        if R.rbuf[s] != j:
+            errors.append(f"rank {R.r} unpacking publication {j} from side {s} found {R.rbuf[s]}")
+        R.consumed[s] = j
+    else:
+        execute(ranks, R, op, errors)
+
+
+def run_s1(ranks, rng):
+    pcs = [0] * len(ranks)
+    errors = []
+    while True:
+        live = [i for i, R in enumerate(ranks) if pcs[i] < len(R.ops)]
+        if not live:
+            return errors
+        runnable = [i for i in live if ready(ranks, ranks[i], ranks[i].ops[pcs[i]])]
+        if not runnable:
+            return errors + [f"deadlock at {[(i, ranks[i].ops[pcs[i]]) for i in live]}"]
+        i = rng.choice(runnable)
+        execute_s1(ranks, ranks[i], ranks[i].ops[pcs[i]], errors)
+        pcs[i] += 1
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_s1_exchange_delivers_every_publication(n):
+    """vti_step_adjoint on peer ranks publishes once per call plus once per chained step; every
+    interleaving of the ranks' streams is deadlock-free and unpacks exactly the publication it
+    expects, with no receive buffer overwritten before it was unpacked."""
+    for seed in range(300):
+        ranks = [S1Rank(r, n) for r in range(n)]
+        for _ in range(9):
+            for R in ranks:
+                enqueue_s1(R)
+        errs = run_s1(ranks, random.Random(seed))
+        assert not errs, (seed, errs[:3])
+
+
+def test_s1_model_catches_a_missing_ack_wait():
+    bad = 0
+    for seed in range(300):
+        ranks = [S1Rank(r, 3) for r in range(3)]
+        for _ in range(6):
+            for R in ranks:
+                enqueue_s1(R, ack_wait=False)
+        bad += bool(run_s1(ranks, random.Random(seed)))
+    assert bad > 0
