@@ -527,6 +527,9 @@ __global__ void __launch_bounds__(AdjTmaCfg<T, R, RZ, TY, ST, PX>::NT, 1)
         for (int i = 0; i < 9; ++i) prefetch_tmap(&P.tm[i]);
     }
     __syncthreads();
+    // programmatic dependent launch: the prologue above overlaps the previous kernel's tail; every
+    // global access below waits for its completion (a no-op without the launch attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     int stage = 0;
     uint32_t phase = 0;
     if (warp == NCONS / 32) {   // producer: one lane walks the load sequence of every item
@@ -736,6 +739,7 @@ template <typename T>
 __global__ void k_adj_s1(const T *__restrict__ pp, const T *__restrict__ pq, const T *__restrict__ vx2,
                          const T *__restrict__ vn2, T *__restrict__ s1, int nx4, int nyl, long long ys, long long zs)
 {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // programmatic dependent launch (see k_adj_tma)
     const int k = blockIdx.y, n = nyl * nx4;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const int y = t / nx4, x = (t - y * nx4) * 4;
@@ -797,6 +801,7 @@ __global__ void __launch_bounds__(AdjTma2Cfg<T, R, RZ, TY, ST, PX, CH>::NT, MINB
         for (int i = 0; i < (CH ? 8 : 6); ++i) prefetch_tmap(&P.tm[i]);
     }
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // programmatic dependent launch (see k_adj_tma)
     int stage = 0;
     uint32_t phase = 0;
     if (warp == NCONS / 32) {   // producer
@@ -1009,6 +1014,23 @@ __global__ void k_adj_wt(const T *__restrict__ zrow, T *__restrict__ wt, int nz,
     }
 }
 
+// launches of the TMA adjoint forms: programmatic dependent launch (env VTI_PDL=0: plain)
+static cudaError_t adj_launch(vti_s *h, const void *fn, dim3 grid, dim3 block, void **args, size_t smem)
+{
+    static const bool pdl = !getenv("VTI_PDL") || atoi(getenv("VTI_PDL")) != 0;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelExC(&lc, fn, args);
+}
+
 struct AdjTmaEntry {
     int es, r, rz, form, ty, px, st, minb;   // form 1: one-pass k_adj_tma; form 2: k_adj_s1 + k_adj_tma2;
                                              // st: ring depth; minb: __launch_bounds__ CTAs per SM
@@ -1159,7 +1181,7 @@ static vti_status launch_adj_tma(vti_s *h, const AdjTmaEntry *E, const AdjParams
     const int grid = std::min(P.items, ctas);
     void *args[] = {&P};
     const void *fn = chain ? (io ? E->fn_ch_io : E->fn_ch) : (io ? E->fn_io : E->fn);
-    CU(h, cudaLaunchKernel(fn, dim3(grid), dim3(E->threads), args, chain ? E->smem_ch : E->smem, h->stream));
+    CU(h, adj_launch(h, fn, dim3(grid), dim3(E->threads), args, chain ? E->smem_ch : E->smem));
     return VTI_OK;
 }
 
@@ -1202,9 +1224,13 @@ static vti_status adjoint_prep_t(vti_s *h, int sb = 0)
     if (adj_form(h) == ADJ_TMA2) {
         const int nx4 = (int)(h->nxp / 4), n = h->nyl * nx4;
         const dim3 grid((unsigned)std::min((n + 255) / 256, 64), (unsigned)h->cfg.nz);
-        k_adj_s1<T><<<grid, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
-                                                (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
-                                                (T *)h->in(h->adj_s[sb]), nx4, h->nyl, h->ys, h->zs);
+        const T *pp = (const T *)h->p_int(c), *pq = (const T *)h->q_int(c);
+        const T *vx = (const T *)h->in(h->vx2), *vn = (const T *)h->in(h->vn2);
+        T *s1 = (T *)h->in(h->adj_s[sb]);
+        long long ys = h->ys, zs = h->zs;
+        int nyl = h->nyl, nx4v = nx4;
+        void *args[] = {&pp, &pq, &vx, &vn, &s1, &nx4v, &nyl, &ys, &zs};
+        CU(h, adj_launch(h, (const void *)k_adj_s1<T>, grid, dim3(256), args, 0));
     } else {
         k_adj_prep<T><<<4 * h->sms, 256, 0, h->stream>>>((const T *)h->p_int(c), (const T *)h->q_int(c),
                                                        (const T *)h->in(h->vx2), (const T *)h->in(h->vn2),
