@@ -101,6 +101,24 @@ def test_adjoint_split_calls_equal_one_call(r, rz, prec):
     assert np.array_equal(out[0][1], out[1][1])
 
 
+@pytest.mark.parametrize("r,rz,prec", [(4, 4, 32), (12, 8, 32), (4, 4, 64)])
+def test_adjoint_long_calls_match_oracle(r, rz, prec):
+    """Long calls (37 then 20 steps: programmatic dependent launches back to back, the chained
+    s1 buffers alternating from both buffer parities), bitwise against the oracle."""
+    cfg, wxy, wz, dt, model, st, dtype = setup(r, rz, prec, shape=(70, 40, 2 * rz + 20))
+    with handle(cfg, dt, wxy, wz, prec) as v:
+        v.set_model(*model)
+        v.set_fields(*st, time_index=80)
+        v.step_adjoint(37)
+        v.step_adjoint(20)
+        assert v.time_index == 23
+        g = v.get_fields(0) + v.get_fields(1)
+    o = oracle.adjoint_ex(oracle.params(cfg, dt, src=None), wxy, wz, *model, st, m0=80, nsteps=57, dtype=dtype)
+    for f, (a, b) in enumerate(zip(g, o[:4])):
+        assert np.abs(b).max() > 0
+        assert np.array_equal(a, b), f"field {f}: max |diff| {np.abs(a - b).max():.3e}"
+
+
 def test_library_dot_product_identity():
     """fp64, damped: the library's K forward steps and K adjoint steps satisfy
     <u^K, psi^K / g> - <u^{K-1}, g psi^{K+1}> = <u^0, psi^0 / g> - <u^{-1}, g psi^1>."""
