@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define VTI_ABI_VERSION 4
+#define VTI_ABI_VERSION 5
 #define VTI_IPC_BYTES 512   /* size of a vti_ipc_export blob */
 
 typedef struct vti_s *vti_t;
