@@ -1044,6 +1044,7 @@ template <typename T, int R, int RZ, int TY, int ST, int PX = 4>
 constexpr AdjTmaEntry adj_tma1()
 {
     using C = AdjTmaCfg<T, R, RZ, TY, ST, PX>;
+    static_assert(C::SMEM <= 227 * 1024, "one-pass adjoint stage ring exceeds the per-CTA shared memory");
     return {C::ES, R, RZ, 1, TY, PX, ST, 1, (const void *)k_adj_tma<T, R, RZ, TY, ST, PX, false>,
             (const void *)k_adj_tma<T, R, RZ, TY, ST, PX, true>, C::SMEM, C::NT, C::ZROW, nullptr, nullptr, 0};
 }
@@ -1053,6 +1054,7 @@ constexpr AdjTmaEntry adj_tma2()
 {
     using C = AdjTma2Cfg<T, R, RZ, TY, ST, PX, false>;
     using CC = AdjTma2Cfg<T, R, RZ, TY, ST, PX, true>;
+    static_assert(CC::SMEM <= 227 * 1024, "chained adjoint stage ring exceeds the per-CTA shared memory");
     return {C::ES, R, RZ, 2, TY, PX, ST, MINB, (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, false, MINB>,
             (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, true, false, MINB>, C::SMEM, C::NT, C::ZROW,
             (const void *)k_adj_tma2<T, R, RZ, TY, ST, PX, false, true, MINB>,
