@@ -1073,7 +1073,7 @@ static const AdjTmaEntry *find_adj_tma(int es, int r, int rz, bool group)
         adj_tma2<double, 4, 4, 8, 3, 4>(),    adj_tma2<double, 4, 4, 8, 2, 4>(), adj_tma1<double, 4, 4, 8, 2>(),
         adj_tma2<double, 8, 4, 8, 3, 4>(),    adj_tma2<double, 8, 4, 8, 2, 2>(),
         adj_tma2<double, 6, 6, 8, 3, 4>(),    adj_tma2<double, 6, 6, 8, 2, 2>(),
-        adj_tma2<double, 12, 8, 8, 2, 2>(),
+        adj_tma2<double, 12, 8, 4, 3, 2>(),   adj_tma2<double, 12, 8, 8, 2, 2>(),
     };
     static const int want_form = getenv("VTI_ADJ_FORM") ? atoi(getenv("VTI_ADJ_FORM")) : 0;
     static const int want_ty = getenv("VTI_ADJ_TMA_TY") ? atoi(getenv("VTI_ADJ_TMA_TY")) : 0;
@@ -1192,8 +1192,8 @@ static vti_status launch_adj_tma(vti_s *h, const AdjTmaEntry *E, const AdjParams
 // (tools/adjoint_rate.py, profiles/r02/adjoint_tma_r02.txt, Gpoints/s):
 //   fp32: one-pass C2 (4,4) 172-174 (8-row tiles, 3 stages, 2 CTAs/SM), C3 (8,4) 139-141 and
 //         C5 (6,6) 135-136 (16-row tiles); chained two-pass N1 (12,8) 137 (one-pass: 29-54);
-//   fp64: chained two-pass, 4 x points per thread and 3 stages: C2 72, C3 63, C5 66.5; 2 x points
-//         per thread (the (12,8) boxes need 2 stages to fit): N1 56.
+//   fp64: chained two-pass, 4 x points per thread and 3 stages: C2 72, C3 63, C5 66.5; for
+//         (12,8) 2 x points per thread on 4-row tiles, 3 stages: N1 64 (8-row tiles: 56).
 // Before them, the cp.async forms: fp32 one-pass C2 78.1, C3 81.4, C5 82.2, N1 38.7; fp64
 // C2 36.9, C3 31.2, C5 34.1, N1 19.3 (two-pass at R_xy >= 8). With VTI_ADJ_TMA=0 those run:
 // y-slab groups the two-pass one, single slabs the one-pass one (VTI_ADJ_TWO_PASS=1/0 forces
